@@ -1,0 +1,346 @@
+"""Pins for the CPU oracle (oracle/hsf_oracle.py) against what the paper and the
+mathematics fix: paper worked examples, closed forms, brute force, invariants.
+None of these compare the oracle with itself."""
+import math
+import os
+
+import numpy as np
+import pytest
+
+from hsf_inputs import make_config, random_small_circuit
+from hsf_inputs.circuits import make_sbm_qaoa
+from oracle import hsf_oracle as O
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _circ(text):
+    return O.parse_circuit(text)
+
+
+# ------------------------------------------------------------------ gates
+@pytest.mark.parametrize("name,params,k", [("h", (), 1), ("x", (), 1), ("z", (), 1), ("rx", (0.3,), 1),
+                                           ("rz", (1.1,), 1), ("cz", (), 2), ("cx", (), 2), ("swap", (), 2),
+                                           ("cp", (0.7,), 2), ("rzz", (2.2,), 2)])
+def test_library_gates_unitary(name, params, k):
+    U = O.gate_matrix(name, params, k)
+    assert np.allclose(U.conj().T @ U, np.eye(1 << k), atol=1e-12)
+
+
+def test_cnot_is_paper_bipartite_form():
+    # PAPER.md Example 2: CNOT = P0 (x) I + P1 (x) X, written out by hand
+    expect = np.array([[1, 0, 0, 0], [0, 1, 0, 0], [0, 0, 0, 1], [0, 0, 1, 0]], dtype=complex)
+    assert np.array_equal(O.gate_matrix("cx", (), 2), expect)
+
+
+def test_rzz_is_exponential_of_zz():
+    # RZZ(t) = exp(-i t/2 Z(x)Z): compare with a Taylor series of the 4x4 generator
+    t = 0.913
+    Z = np.diag([1, -1]).astype(complex)
+    G = -0.5j * t * np.kron(Z, Z)
+    E, term = np.eye(4, dtype=complex), np.eye(4, dtype=complex)
+    for j in range(1, 40):
+        term = term @ G / j
+        E = E + term
+    assert np.allclose(O.gate_matrix("rzz", (t,), 2), E, atol=1e-14)
+
+
+def test_rx_is_exponential_of_x():
+    t = 1.37
+    X = np.array([[0, 1], [1, 0]], dtype=complex)
+    G = -0.5j * t * X
+    E, term = np.eye(2, dtype=complex), np.eye(2, dtype=complex)
+    for j in range(1, 40):
+        term = term @ G / j
+        E = E + term
+    assert np.allclose(O.gate_matrix("rx", (t,), 1), E, atol=1e-14)
+
+
+# ------------------------------------------------------------ Schroedinger
+def test_bell_state_paper_example1():
+    text = open(os.path.join(GOLD, "bell.txt")).read()
+    circ = "\n".join(l for l in text.splitlines() if not l.startswith("#"))
+    n, g = _circ(circ)
+    psi = O.schrodinger(n, g)
+    expect = np.array([1, 0, 0, 1]) / math.sqrt(2)
+    assert np.allclose(psi, expect, atol=1e-15)
+
+
+@pytest.mark.parametrize("n,n_low", [(4, 2), (7, 3), (10, 5)])
+def test_ghz_across_cut(n, n_low):
+    text = f"qubits {n}\nh 0\n" + "".join(f"cx {q} {q + 1}\n" for q in range(n - 1))
+    n, g = _circ(text)
+    expect = np.zeros(1 << n, dtype=complex)
+    expect[0] = expect[-1] = 1 / math.sqrt(2)
+    assert np.allclose(O.schrodinger(n, g), expect, atol=1e-14)
+    assert np.allclose(O.hsf(n, g, n_low), expect, atol=1e-14)
+    # individual cut: a single crossing CNOT, rank 2
+    P = O.plan(n, g, n_low, None, "individual")
+    assert P.radices == [2]
+
+
+def _rev(i, n):
+    return int(format(i, "0%db" % n)[::-1], 2)
+
+
+@pytest.mark.parametrize("n", [6, 8, 12])
+def test_qft_closed_form(n):
+    # QFT without final swaps of |x>: psi[i] = 2^{-n/2} exp(2 pi i x rev_n(i) / 2^n)
+    inst = make_config("c2", twin=True, n=n, n_low=n // 2, seed=11 + n)
+    nn, g = _circ(inst.text)
+    x = inst.meta["x"]
+    cf = np.array([np.exp(2j * np.pi * x * _rev(i, n) / 2 ** n) for i in range(1 << n)]) / 2 ** (n / 2)
+    assert np.abs(O.schrodinger(nn, g) - cf).max() < 1e-13
+    assert np.abs(O.hsf(nn, g, inst.n_low, inst.blocks) - cf).max() < 1e-13
+    P = O.plan(nn, g, inst.n_low, inst.blocks)
+    assert P.radices == [2] * (n - n // 2)  # each ladder tail is one rank-2 block
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_schrodinger_vs_bruteforce_unitary(seed):
+    inst = random_small_circuit(seed, n=int(3 + seed % 4), n_gates=14)
+    n, g = _circ(inst.text)
+    U = O.unitary_bruteforce(n, g)
+    assert np.allclose(U.conj().T @ U, np.eye(1 << n), atol=1e-12)
+    for init in (0, (1 << n) - 1, 5 % (1 << n)):
+        assert np.allclose(O.schrodinger(n, g, init), U[:, init], atol=1e-12)
+
+
+# ---------------------------------------------------------- Schmidt step
+def _single_unit(text, n_low):
+    n, g = _circ(text)
+    P = O.plan(n, g, n_low, [list(range(len(g)))])
+    assert len(P.units) == 1
+    return P.units[0], g
+
+
+def test_schmidt_ranks_individual_gates():
+    assert _single_unit("qubits 2\ncx 1 0\n", 1)[0].rank == 2
+    assert _single_unit("qubits 2\ncz 1 0\n", 1)[0].rank == 2
+    assert _single_unit("qubits 2\nswap 1 0\n", 1)[0].rank == 4  # P:131 (SWAP r = 4)
+    assert _single_unit(f"qubits 2\nrzz {0.0.hex()} 1 0\n", 1)[0].rank == 1
+    assert _single_unit(f"qubits 2\nrzz {0.7.hex()} 1 0\n", 1)[0].rank == 2
+
+
+def test_rzz_singular_values_closed_form():
+    # RZZ(t) = cos(t/2) I(x)I - i sin(t/2) Z(x)Z; unit-Frobenius factors give
+    # sigma = (2|cos t/2|, 2|sin t/2|); unitary-scale coefficients = (|cos|, |sin|)
+    t = 0.7
+    u, _ = _single_unit(f"qubits 2\nrzz {t.hex()} 1 0\n", 1)
+    assert np.allclose(sorted(u.sigmas), sorted([2 * abs(math.cos(t / 2)), 2 * abs(math.sin(t / 2))]), atol=1e-14)
+    assert np.allclose(sorted(np.abs(u.c)), sorted([abs(math.cos(t / 2)), abs(math.sin(t / 2))]), atol=1e-14)
+
+
+def test_product_operator_rank_one():
+    txt = "qubits 2\nh 1\nrx %s 0\n" % (0.4).hex()
+    n, g = _circ(txt)
+    P = O.plan(n, g, 1, [[0, 1]])
+    assert P.units[0].rank == 1
+
+
+def test_cnot_cascade_eq11():
+    # Example 4 / Eq. 11: 3-CNOT cascade from control q3 (side a)
+    # onto q2,q1,q0 (side b): C = P0(x)I(x)I(x)I + P1(x)X(x)X(x)X, rank 2 (vs 2^3).
+    u, g = _single_unit("qubits 4\ncx 3 2\ncx 3 1\ncx 3 0\n", 3)
+    assert u.rank == 2
+    # the X factors span {P0, P1}; the Y factors span {I, XXX}
+    P0 = np.diag([1, 0]).astype(complex)
+    P1 = np.diag([0, 1]).astype(complex)
+    X1 = np.array([[0, 1], [1, 0]], dtype=complex)
+    XXX = np.kron(np.kron(X1, X1), X1)
+    basis_a = np.stack([P0.ravel(), P1.ravel()], 1)
+    basis_b = np.stack([np.eye(8).ravel(), XXX.ravel()], 1)
+    for Xm in u.X:
+        coef, *_ = np.linalg.lstsq(basis_a, Xm.ravel(), rcond=None)
+        assert np.allclose(basis_a @ coef, Xm.ravel(), atol=1e-12)
+    for Ym in u.Y:
+        coef, *_ = np.linalg.lstsq(basis_b, Ym.ravel(), rcond=None)
+        assert np.allclose(basis_b @ coef, Ym.ravel(), atol=1e-12)
+    expect = np.kron(P0, np.eye(8)) + np.kron(P1, XXX)
+    assert np.allclose(O.unit_reconstruction(u), expect, atol=1e-12)
+    # individually cut: 2^3 paths
+    n, gg = _circ("qubits 4\ncx 3 2\ncx 3 1\ncx 3 0\n")
+    assert O.plan(n, gg, 3, None, "individual").n_paths == 8
+
+
+@pytest.mark.parametrize("depth", [1, 2, 4, 8])
+def test_joint_rank_saturates_at_16(depth):
+    # Example 3 / Eq. 10: a 2+2 block has rank <= 2^(2*2)
+    rng = np.random.default_rng(depth)
+    lines = ["qubits 4"]
+    for _ in range(depth):
+        for q in range(4):
+            v = rng.standard_normal(4)
+            a, b, c, d = v / np.linalg.norm(v)
+            lines.append("u 1 %d %s" % (q, " ".join(x.hex() for x in [a, b, c, d, -c, d, a, -b])))
+        lines.append("cx 1 2")
+        lines.append("cz 0 3")
+        lines.append("swap 1 3")
+    n, g = _circ("\n".join(lines) + "\n")
+    P = O.plan(n, g, 2, [list(range(len(g)))])
+    Pi = O.plan(n, g, 2, None, "individual")
+    assert P.units[0].rank <= 16
+    assert Pi.n_paths == (2 * 2 * 4) ** depth
+    if depth >= 2:
+        assert P.n_paths < Pi.n_paths
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_reconstruction_random_blocks(seed):
+    inst = random_small_circuit(seed, max_block_qubits=6)
+    n, g = _circ(inst.text)
+    P = O.plan(n, g, inst.n_low, inst.blocks)
+    for u in P.units:
+        ref = O.unit_matrix(g, u)
+        assert np.linalg.norm(O.unit_reconstruction(u) - ref) <= 1e-12 * np.linalg.norm(ref)
+        # Eq. 10 rank bound
+        assert u.rank <= min(4 ** len(u.Sa), 4 ** len(u.Sb))
+        # unitary block -> sum |c_m|^2 = 1 with unitary-scale factors
+        assert abs(np.sum(np.abs(u.c) ** 2) - 1) < 1e-12
+
+
+def test_nonconvex_block_rejected():
+    n, g = _circ("qubits 3\ncx 2 0\nh 0\ncx 2 1\ncx 0 1\n")
+    # {g0, g3} with g1 (h 0) between them on qubit 0 and g3 after g1: cycle
+    with pytest.raises(O.NonConvexBlock):
+        O.plan(n, g, 1, [[0, 3]])
+
+
+# ------------------------------------------------------------- path sums
+@pytest.mark.parametrize("seed", range(30))
+def test_joint_equals_individual_equals_schrodinger_random(seed):
+    inst = random_small_circuit(seed, n_gates=8 + seed % 17)
+    n, g = _circ(inst.text)
+    ref = O.schrodinger(n, g)
+    P = O.plan(n, g, inst.n_low, inst.blocks)
+    if P.n_paths > 1024:
+        inst = random_small_circuit(seed, n_gates=8)
+        n, g = _circ(inst.text)
+        ref = O.schrodinger(n, g)
+    joint = O.hsf(n, g, inst.n_low, inst.blocks)
+    assert np.abs(joint - ref).max() < 1e-12
+    Pi = O.plan(n, g, inst.n_low, None, "individual")
+    if Pi.n_paths <= 512:
+        ind = O.hsf(n, g, inst.n_low, None, "individual")
+        assert np.abs(ind - ref).max() < 1e-12
+
+
+@pytest.mark.parametrize("name", ["c1", "c3", "c4", "c5"])
+def test_configs_twins_match_schrodinger(name):
+    inst = make_config(name, twin=True)
+    n, g = _circ(inst.text)
+    ref = O.schrodinger(n, g)
+    P = O.plan(n, g, inst.n_low, inst.blocks)
+    A, B, c = O.half_states(P)
+    full = O.recombine_full(A, B, c)
+    assert np.abs(full - ref).max() < 1e-13
+    assert abs(O.gram_norm2(A, B, c) - 1) < 1e-12
+    if inst.bitstrings is not None:
+        amps = O.recombine_bits(A, B, c, inst.bitstrings, inst.n_low)
+        assert np.abs(amps - ref[inst.bitstrings.astype(np.int64)]).max() < 1e-13
+
+
+def test_c1_full_size_paths():
+    inst = make_config("c1")
+    n, g = _circ(inst.text)
+    P = O.plan(n, g, inst.n_low, inst.blocks)
+    Pi = O.plan(n, g, inst.n_low, None, "individual")
+    assert (P.n_paths, Pi.n_paths) == (16, 4096)  # BJ configs[0]: <=16 vs 2^12
+    ref = O.schrodinger(n, g)
+    assert np.abs(O.hsf(n, g, inst.n_low, inst.blocks) - ref).max() < 1e-13
+
+
+def test_path_counts_full_configs():
+    # BJ: c2 2^12 joint; c3 4^4; c4 4^3; c5 2^8 joint vs 2^48 individual
+    expect = {"c2": (4096, None), "c3": (256, 256), "c4": (64, 64), "c5": (256, 2 ** 48)}
+    for name, (pj, pt) in expect.items():
+        inst = make_config(name, n_bits=0) if name in ("c3", "c5") else make_config(name)
+        n, g = _circ(inst.text)
+        P = O.plan(n, g, inst.n_low, inst.blocks)
+        assert P.n_paths == pj, name
+        if pt is not None:
+            # individual ranks: every crossing gate here has rank 2
+            ncross = sum(1 for x in g if O.classify(x.qubits, inst.n_low) == "cross")
+            assert 2 ** ncross == pt, name
+
+
+def test_no_crossing_gates_is_kron():
+    rng = np.random.default_rng(3)
+    lines = ["qubits 6"]
+    for q in range(6):
+        v = rng.standard_normal(4)
+        a, b, c, d = v / np.linalg.norm(v)
+        lines.append("u 1 %d %s" % (q, " ".join(x.hex() for x in [a, b, c, d, -c, d, a, -b])))
+    lines += ["cx 0 1", "cz 4 5", "cx 3 4"]
+    n, g = _circ("\n".join(lines) + "\n")
+    P = O.plan(n, g, 3)
+    assert P.n_paths == 1
+    A, B, c = O.half_states(P)
+    assert np.allclose(O.recombine_full(A, B, c), np.kron(A[:, 0], B[:, 0]), atol=1e-15)
+    assert np.abs(O.recombine_full(A, B, c) - O.schrodinger(n, g)).max() < 1e-14
+
+
+def test_path_ranges_sum_to_whole():
+    # partition of the path index (per-GPU ranges) sums to the 1-way result
+    inst = make_config("c5", twin=True)
+    n, g = _circ(inst.text)
+    P = O.plan(n, g, inst.n_low, inst.blocks)
+    ref = O.recombine_full(*O.half_states(P))
+    for G in (2, 4, 8):
+        tot = 0
+        for r in range(G):
+            p0, p1 = r * P.n_paths // G, (r + 1) * P.n_paths // G
+            tot = tot + O.recombine_full(*O.half_states(P, p0, p1))
+        assert np.abs(tot - ref).max() < 1e-14
+
+
+# ------------------------------------------------- paper tables (path counts)
+def _table2():
+    rows = []
+    for line in open(os.path.join(GOLD, "table2_paths.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        name, lt, lj, blocks, sep, sepc = line.split()
+        rows.append((name, int(lt), int(lj), int(blocks), int(sep), int(sepc)))
+    return rows
+
+
+@pytest.mark.parametrize("row", _table2(), ids=lambda r: r[0])
+def test_table2_path_counts(row):
+    # Build crossing structure with the paper's counts: `blocks` RZZ cascades
+    # holding (sep_cuts - sep) crossing gates plus `sep` separate crossing RZZs.
+    # The oracle must reproduce Table I's path counts n_p^j and n_p^t.
+    name, lt, lj, blocks, sep, sepc = row
+    assert lt == sepc
+    in_blocks = sepc - sep
+    sizes = [in_blocks // blocks + (1 if i < in_blocks % blocks else 0) for i in range(blocks)]
+    nb = 16
+    lines, blk = [f"qubits {nb + blocks + sep}"], []
+    gi, t = 0, 0
+    for i, s in enumerate(sizes):
+        ids = []
+        for _ in range(s):
+            lines.append(f"rzz {0.37.hex()} {t % nb} {nb + i}")
+            ids.append(gi)
+            gi += 1
+            t += 1
+        blk.append(ids)
+    for j in range(sep):
+        lines.append(f"rzz {0.61.hex()} {t % nb} {nb + blocks + j}")
+        gi += 1
+        t += 1
+    n, g = _circ("\n".join(lines) + "\n")
+    P = O.plan(n, g, nb, blk)
+    Pi = O.plan(n, g, nb, None, "individual")
+    assert P.n_paths == 2 ** lj
+    assert Pi.n_paths == 2 ** lt
+
+
+def test_sbm_qaoa_blocks_are_rank2_cascades():
+    inst = make_sbm_qaoa(seed=31, sizes=(6, 6), p_inter=0.3)
+    n, g = _circ(inst.text)
+    P = O.plan(n, g, inst.n_low, inst.blocks)
+    for u in P.units:
+        assert u.rank == 2
+    assert abs(np.linalg.norm(O.hsf(n, g, inst.n_low, inst.blocks)) - 1) < 1e-12
+    assert np.abs(O.hsf(n, g, inst.n_low, inst.blocks) - O.schrodinger(n, g)).max() < 1e-13
