@@ -1,0 +1,177 @@
+/*
+ * hsf.h — C ABI of libhsf.so: joint-cut Hybrid Schroedinger-Feynman (HSF)
+ * path evaluation on NVIDIA B200 (sm_100a).
+ *
+ * Method: arXiv 2502.06959 (PAPER.md, cited as P:<line>).
+ *   - HSF partitions the qubits into halves a (high) and b (low); every gate
+ *     crossing the cut is replaced by a bipartite (Schmidt) representation
+ *     A = sum_m sigma_m X_m (x) Y_m  (Eq. 4).  Each choice of one
+ *     term per cut unit is a "path"; n_p = prod_i r_i.  The result is
+ *     the sum over paths of c_p psi_A^p (x) psi_B^p.
+ *   - Joint cutting groups gates into blocks, multiplies them and
+ *     Schmidt-decomposes the block unitary via reshape (Eq. 5-6,
+ *     P:163-172), SVD (Eq. 7) and absorption of U, V* into the factors
+ *     (Eq. 8-9).
+ *
+ * Conventions:
+ *   - qubit 0 is the least-significant bit of a basis index;
+ *   - n_low = number of qubits in half B = qubits [0, n_low); half A = the
+ *     paper's partition a = qubits [n_low, n); the paper's cut position
+ *     l = n_low - 1;
+ *   - full output index i = i_A * 2^n_low + i_B, row-major [2^nA][2^nB];
+ *   - complex numbers are interleaved (re, im), complex64 = 2 x float32,
+ *     complex128 = 2 x float64;
+ *   - bitstring bit q = qubit q (uint64, so n <= 63 for bitstring runs);
+ *   - paths are numbered mixed-radix over the cut units in schedule order,
+ *     last unit fastest.
+ *
+ * Errors: every call returns hsf_status; HSF_OK == 0.  No C++ exception or
+ * abort crosses the ABI.  A thread-local message describing the last error is
+ * available through hsf_last_error().  On error the output buffer contents are
+ * undefined; the plan stays valid unless the status is HSF_ERR_CUDA.
+ *
+ * Threading: a plan is immutable after hsf_plan() except for its device
+ * workspace; hsf_run() calls on one plan must be serialised by the caller.
+ */
+#ifndef HSF_H_
+#define HSF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HSF_OK = 0,
+  HSF_ERR_INVALID_ARG = 1,       /* null pointer, bad size, bad cut, bad range */
+  HSF_ERR_PARSE = 2,             /* malformed circuit text (message has the line) */
+  HSF_ERR_UNSUPPORTED_GATE = 3,  /* unknown gate name or arity */
+  HSF_ERR_DUPLICATE_QUBIT = 4,   /* a gate lists a qubit twice / qubit out of range */
+  HSF_ERR_NONCONVEX_BLOCK = 5,   /* a block is not convex in the wire DAG */
+  HSF_ERR_BLOCK_TOO_LARGE = 6,   /* dense block > max_dense_block_qubits, or a
+                                    dense factor on > 5 qubits of one half */
+  HSF_ERR_SVD_NO_CONVERGENCE = 7,
+  HSF_ERR_PATH_BUDGET = 8,       /* n_p exceeds 2^log2_path_budget */
+  HSF_ERR_OUT_OF_MEMORY = 9,     /* host or device allocation failed */
+  HSF_ERR_CUDA = 10,             /* CUDA runtime error (sticky for the plan) */
+  HSF_ERR_UNSUPPORTED = 11       /* valid request this build does not handle */
+} hsf_status;
+
+typedef enum { HSF_C64 = 0, HSF_C128 = 1 } hsf_dtype;
+
+/* Arithmetic of the full-output path-sum Psi = (Psi_A diag(c)) Psi_B^T
+ * (P:109).  Half-state simulation always runs in the plan dtype. */
+typedef enum {
+  HSF_PREC_AUTO = 0,    /* c64: BF16X3 ; c128: FP64 SIMT */
+  HSF_PREC_SIMT = 1,    /* CUDA-core FMA in the plan dtype (fp32 / fp64) */
+  HSF_PREC_BF16X3 = 2,  /* tcgen05 bf16 MMA, fp32 accumulate in TMEM, operands
+                           split hi+lo, 3 products (hi*hi + hi*lo + lo*hi) */
+  HSF_PREC_BF16X1 = 3   /* tcgen05 bf16 MMA, single product (error study only) */
+} hsf_precision;
+
+typedef struct {
+  hsf_dtype dtype;               /* default HSF_C64 */
+  double svd_rel_tol;            /* drop sigma_m <= tol * sigma_0; default 1e-12 */
+  int32_t max_dense_block_qubits;/* default 10 (dense block assembly O(D^3)) */
+  double log2_path_budget;       /* default 26 */
+  int32_t individual;            /* 1 => ignore blocks, cut every crossing gate alone */
+  int32_t tile_qubits;           /* amplitudes per SMEM tile = 2^tile_qubits for
+                                    halves larger than the SMEM-resident limit;
+                                    0 => default (12) */
+  int32_t fuse_gates;            /* 1 (default) => host gate fusion */
+} hsf_plan_opts;
+
+typedef struct hsf_plan_s hsf_plan_t; /* opaque */
+
+/* Fill *opts with the defaults listed above. */
+hsf_status hsf_plan_opts_default(hsf_plan_opts* opts);
+
+/*
+ * hsf_plan — parse the circuit, classify gates, contract and schedule the
+ * joint-cut blocks, Schmidt-decompose every cut unit (host fp64: assembly or
+ * diagonal route, reshape Eq. 6, one-sided Jacobi SVD Eq. 7, truncation and
+ * normalisation Eq. 8-9), count paths and build the per-half device
+ * programs.  Host only: touches no GPU.
+ *
+ *   circuit_text, text_len : circuit file contents (format in DESIGN.md)
+ *   n_low                  : qubits in half B; 1 <= n_low < n
+ *   n_blocks               : number of joint blocks (0 => every crossing gate
+ *                            is its own unit)
+ *   block_offsets          : CSR offsets, length n_blocks+1 (may be NULL iff
+ *                            n_blocks == 0)
+ *   block_gate_ids         : gate indices (0-based, file order) of each block
+ *   opts                   : NULL => defaults
+ *   out                    : receives a new plan; free with hsf_plan_free
+ * Inputs are copied; the caller keeps ownership.
+ */
+hsf_status hsf_plan(const char* circuit_text, size_t text_len, int32_t n_low, int64_t n_blocks,
+                    const int64_t* block_offsets, const int64_t* block_gate_ids,
+                    const hsf_plan_opts* opts, hsf_plan_t** out);
+
+typedef struct {
+  int32_t n_qubits, n_a, n_b;
+  int32_t n_units;
+  uint64_t n_paths;             /* joint-cut paths n_p^j (exact, <= budget) */
+  double log2_n_paths_individual; /* log2 of n_p^t = prod of individual ranks */
+  const int32_t* ranks;         /* [n_units] Schmidt ranks r_u (plan-owned) */
+  const int32_t* support_a;     /* [n_units] |S_a| */
+  const int32_t* support_b;     /* [n_units] |S_b| */
+  const int64_t* sigma_offsets; /* [n_units+1] into sigmas */
+  const double* sigmas;         /* kept singular values, descending per unit */
+  int32_t levels_a, levels_b;   /* materialised path-tree levels per half */
+  int32_t passes_a, passes_b;   /* device passes over all levels per half */
+  int32_t ops_a, ops_b;         /* device ops after fusion */
+  uint64_t plan_hash;           /* FNV-1a of the device program + tables */
+} hsf_plan_info;
+
+/* Pointers in *info stay valid until hsf_plan_free. */
+hsf_status hsf_plan_info_get(const hsf_plan_t* plan, hsf_plan_info* info);
+
+typedef struct {
+  /* Bitstring mode: n_bitstrings > 0.  out receives n_bitstrings complex
+   * amplitudes in input order (duplicates allowed).  Full mode: bitstrings ==
+   * NULL and n_bitstrings == 0; out receives rows [row_begin,row_end) of the
+   * [2^nA][2^nB] output, i.e. (row_end-row_begin) * 2^nB complex values. */
+  const uint64_t* bitstrings;
+  uint64_t n_bitstrings;
+  int32_t bits_on_device;       /* 1 => device pointer, 0 => host pointer */
+  void* out;                    /* caller-owned, plan dtype */
+  int32_t out_on_device;        /* 1 => device pointer, 0 => host (copied back) */
+  uint64_t path_begin, path_end;/* paths evaluated [begin,end); 0,0 => all.  The
+                                   result is the partial sum over this range. */
+  uint64_t row_begin, row_end;  /* full mode only; 0,0 => all 2^nA rows */
+  void* cuda_stream;            /* cudaStream_t; NULL => legacy default stream */
+  hsf_precision precision;
+  int32_t device;               /* CUDA device ordinal; -1 => current */
+  double* phase_ms;             /* optional [4]: sim A, sim B, path-sum, total
+                                   (CUDA events; synchronises when non-NULL) */
+} hsf_run_args;
+
+/* hsf_run — evaluate the paths [path_begin, path_end) on the GPU: path-tree
+ * half-state simulation of both halves, coefficient fold
+ * c_p = prod_u c_{u,d_u}, then the Kronecker path-sum
+ * into `out`.  Enqueued on cuda_stream; returns after the stream work has
+ * been enqueued if out_on_device, after completion otherwise.  The plan owns
+ * its device tables and workspace (grown on demand, freed by hsf_plan_free). */
+hsf_status hsf_run(hsf_plan_t* plan, const hsf_run_args* args);
+
+/* Bytes of device workspace hsf_run would need for these args (0 on error). */
+size_t hsf_workspace_bytes(const hsf_plan_t* plan, const hsf_run_args* args);
+
+void hsf_plan_free(hsf_plan_t* plan);
+
+const char* hsf_status_str(hsf_status s);
+
+/* Copy the calling thread's last error message into buf (NUL-terminated,
+ * truncated to len); returns the full message length. */
+size_t hsf_last_error(char* buf, size_t len);
+
+/* Library build identification string (compile flags, arch). */
+const char* hsf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HSF_H_ */

@@ -1,0 +1,130 @@
+// hsf_internal.h — host-side plan structures shared by plan.cpp and run.cu.
+// Not part of the ABI (include/hsf.h is).
+#pragma once
+
+#include <complex>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/hsf.h"
+
+namespace hsf {
+
+using cd = std::complex<double>;
+
+struct Error {
+  hsf_status st;
+  std::string msg;
+};
+[[noreturn]] void fail(hsf_status st, const std::string& msg);
+void set_last_error(const std::string& msg);
+
+// ---------------------------------------------------------------- circuit
+struct Gate {
+  std::string name;
+  int k = 0;
+  std::vector<int> q;   // as listed in the file: q[0] = MSB of the local index
+  std::vector<cd> U;    // 2^k x 2^k row-major
+  bool diag = false;    // every off-diagonal entry exactly zero
+};
+
+// ------------------------------------------------------------ cut units
+struct Unit {
+  std::vector<int> gids;           // member gates (file order)
+  std::vector<int> support, Sa, Sb;// ascending global qubit ids
+  bool diag_route = false;         // all members diagonal => diagonal factors
+  int rank = 0;
+  std::vector<double> sigma;       // kept singular values (descending)
+  std::vector<cd> c;               // sigma_m / sqrt(2^|S|)
+  // per term: dense (2^k x 2^k row-major) or diagonal (2^k) matrices with
+  // local index LSB = smallest support qubit of that side
+  std::vector<std::vector<cd>> X, Y;
+  double log2_individual = 0;      // only for reporting
+};
+
+// ------------------------------------------------------------ device ops
+enum OpKind : int32_t { OP_DENSE = 0, OP_DIAG = 1 };
+constexpr int kMaxOpQ = 13;      // widest diagonal op (2^13 entries)
+constexpr int kMaxDenseQ = 5;    // widest dense op in the SMEM kernels
+
+// One operation of a half-circuit program (half-local qubits, LSB-first:
+// q[j] is bit j of the op's local index).
+struct HostOp {
+  int kind = OP_DENSE;
+  int k = 0;
+  int q[kMaxOpQ] = {0};
+  int unit = -1;        // >= 0: Schmidt factor of this unit, matrix selected by digit
+  int64_t table = 0;    // complex offset of the digit-0 matrix in the coef table
+  int64_t stride = 0;   // complex elements between digit matrices
+};
+
+// POD mirrored byte-for-byte on the device (see sim_kernels.cuh).
+struct DevOp {
+  int32_t kind, k;
+  int32_t q[kMaxOpQ];   // dense: tile positions; diag: half-local qubit ids
+  int32_t radix;        // 1 for fixed ops
+  int32_t contiguous;   // diag: q[j] == q[0] + j  => index = (g >> q0) & mask
+  int32_t pad;
+  int64_t div;          // factor digit = (node_global / div) % radix
+  int64_t table, stride;
+};
+static_assert(sizeof(DevOp) == 96, "DevOp layout");
+
+struct Pass {
+  int t = 0;                 // tile qubits (t == m => whole state in SMEM)
+  std::vector<int> T;        // T[i] = half qubit of tile position i
+  int64_t op_begin = 0, op_end = 0;  // into Half::dev_ops
+};
+
+struct Transition {
+  int level_in = -1;         // -1 => start from |0...0>
+  int level_out = 0;
+  std::vector<Pass> passes;
+};
+
+struct Half {
+  int m = 0;                 // qubits in this half
+  int first_qubit = 0;       // global id of half-local qubit 0
+  std::vector<HostOp> ops;   // after fusion
+  std::vector<int64_t> seg_end;      // seg_end[l] = ops index after seg_l, l = 0..U
+  std::vector<int> materialized;     // ascending levels; always contains U
+  std::vector<Transition> trans;
+  std::vector<DevOp> dev_ops;
+  int n_passes = 0;
+};
+
+struct Plan {
+  int n = 0, n_low = 0;
+  hsf_plan_opts opts{};
+  std::vector<Gate> gates;
+  std::vector<Unit> units;          // schedule order
+  std::vector<int32_t> ranks, sa, sb;
+  std::vector<int64_t> sigma_off;
+  std::vector<double> sigmas;
+  uint64_t n_paths = 1;
+  double log2_individual = 0;
+  std::vector<cd> coef;             // all device matrices (fp64 master copy)
+  Half half[2];                     // 0 = A (high), 1 = B (low)
+  uint64_t hash = 0;
+  void* dev = nullptr;              // device state (run.cu)
+};
+
+Plan* build_plan(const char* text, size_t len, int n_low, int64_t n_blocks, const int64_t* off,
+                 const int64_t* ids, const hsf_plan_opts& opts);
+
+// node-count helpers (levels 0..U; level l = after the first l units)
+inline uint64_t suffix_prod(const std::vector<int32_t>& r, int from) {
+  uint64_t s = 1;
+  for (size_t v = from; v < r.size(); ++v) s *= (uint64_t)r[v];
+  return s;
+}
+inline uint64_t range_prod(const std::vector<int32_t>& r, int from, int to) {  // [from, to)
+  uint64_t s = 1;
+  for (int v = from; v < to; ++v) s *= (uint64_t)r[v];
+  return s;
+}
+
+void destroy_device(Plan* p);
+
+}  // namespace hsf

@@ -1,0 +1,757 @@
+// plan.cpp — host planner for joint-cut HSF (arXiv 2502.06959).
+//
+// Steps (all fp64, host, once per plan — off the timed path):
+//   H1 parse + validate the circuit file                     (DESIGN.md format)
+//   H2 classify, contract blocks in the wire DAG, Kahn schedule;
+//      non-convex block => HSF_ERR_NONCONVEX_BLOCK
+//   H3 block assembly: dense product of embedded members, or the diagonal
+//      route when every member is diagonal
+//   H4 reshape / matricise  A~[(i^b,j^b),(i^a,j^a)]         (Eq. 5-6)
+//   H5 one-sided complex Jacobi SVD                          (Eq. 7)
+//   H6 truncate sigma_m <= tol*sigma_0; absorb U, V* into Y_m, X_m (Eq. 8-9,
+//      P:177-181); rescale to unitary-scale factors
+//   H7 radices, n_p = prod r_u, path budget
+//   H8 per-half programs: fixed local gates + factor slots, gate fusion
+//      (P:282), path-tree levels, SMEM tile passes
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <queue>
+#include <set>
+#include <sstream>
+
+#include "hsf_internal.h"
+
+namespace hsf {
+
+[[noreturn]] void fail(hsf_status st, const std::string& msg) { throw Error{st, msg}; }
+
+// ------------------------------------------------------------- gate library
+static std::vector<cd> diag_mat(std::initializer_list<cd> d) {
+  int n = (int)d.size();
+  std::vector<cd> U(n * n, 0.0);
+  int i = 0;
+  for (cd v : d) { U[i * n + i] = v; ++i; }
+  return U;
+}
+
+static Gate make_named(const std::string& name, const std::vector<double>& prm, const std::vector<int>& q) {
+  Gate g;
+  g.name = name;
+  g.q = q;
+  g.k = (int)q.size();
+  const double s2 = 1.0 / std::sqrt(2.0);
+  const cd I(0, 1);
+  if (name == "h") g.U = {s2, s2, s2, -s2};
+  else if (name == "x") g.U = {0.0, 1.0, 1.0, 0.0};
+  else if (name == "z") g.U = diag_mat({1.0, -1.0});
+  else if (name == "rx") {
+    double c = std::cos(prm[0] / 2), s = std::sin(prm[0] / 2);
+    g.U = {c, -I * s, -I * s, c};
+  } else if (name == "rz") g.U = diag_mat({std::exp(-I * (prm[0] / 2)), std::exp(I * (prm[0] / 2))});
+  else if (name == "cz") g.U = diag_mat({1.0, 1.0, 1.0, -1.0});
+  else if (name == "cx") {  // control = first listed (MSB): P0 (x) I + P1 (x) X
+    g.U.assign(16, 0.0);
+    g.U[0 * 4 + 0] = 1; g.U[1 * 4 + 1] = 1; g.U[2 * 4 + 3] = 1; g.U[3 * 4 + 2] = 1;
+  } else if (name == "swap") {
+    g.U.assign(16, 0.0);
+    g.U[0] = 1; g.U[1 * 4 + 2] = 1; g.U[2 * 4 + 1] = 1; g.U[15] = 1;
+  } else if (name == "cp") g.U = diag_mat({1.0, 1.0, 1.0, std::exp(I * prm[0])});
+  else if (name == "rzz") {
+    cd a = std::exp(-I * (prm[0] / 2)), b = std::exp(I * (prm[0] / 2));
+    g.U = diag_mat({a, b, b, a});
+  } else fail(HSF_ERR_UNSUPPORTED_GATE, "unsupported gate '" + name + "'");
+  return g;
+}
+
+static bool is_diag(const Gate& g) {
+  int d = 1 << g.k;
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < d; ++j)
+      if (i != j && g.U[i * d + j] != cd(0.0)) return false;
+  return true;
+}
+
+// --------------------------------------------------------------- H1 parser
+static std::vector<Gate> parse(const char* text, size_t len, int* n_out) {
+  std::string s(text, len);
+  std::istringstream in(s);
+  std::string line;
+  int n = -1, lineno = 0;
+  std::vector<Gate> gates;
+  static const std::map<std::string, std::pair<int, int>> arity = {
+      {"h", {0, 1}}, {"x", {0, 1}}, {"z", {0, 1}}, {"rx", {1, 1}}, {"rz", {1, 1}},
+      {"cz", {0, 2}}, {"cx", {0, 2}}, {"swap", {0, 2}}, {"cp", {1, 2}}, {"rzz", {1, 2}}};
+  auto num = [&](const std::string& t) {
+    char* e = nullptr;
+    double v = std::strtod(t.c_str(), &e);
+    if (e == t.c_str() || *e) fail(HSF_ERR_PARSE, "line " + std::to_string(lineno) + ": bad number '" + t + "'");
+    return v;
+  };
+  auto integer = [&](const std::string& t) {
+    char* e = nullptr;
+    long v = std::strtol(t.c_str(), &e, 10);
+    if (e == t.c_str() || *e) fail(HSF_ERR_PARSE, "line " + std::to_string(lineno) + ": bad integer '" + t + "'");
+    return (int)v;
+  };
+  while (std::getline(in, line)) {
+    ++lineno;
+    auto h = line.find('#');
+    if (h != std::string::npos) line = line.substr(0, h);
+    std::istringstream ls(line);
+    std::vector<std::string> tok;
+    std::string t;
+    while (ls >> t) tok.push_back(t);
+    if (tok.empty()) continue;
+    if (tok[0] == "qubits") {
+      if (tok.size() != 2) fail(HSF_ERR_PARSE, "line " + std::to_string(lineno) + ": 'qubits <n>'");
+      n = integer(tok[1]);
+      if (n < 2 || n > 64) fail(HSF_ERR_INVALID_ARG, "qubits must be in [2,64]");
+      continue;
+    }
+    if (n < 0) fail(HSF_ERR_PARSE, "line " + std::to_string(lineno) + ": gate before 'qubits'");
+    Gate g;
+    if (tok[0] == "u") {
+      if (tok.size() < 2) fail(HSF_ERR_PARSE, "line " + std::to_string(lineno) + ": 'u k q.. reals'");
+      int k = integer(tok[1]);
+      if (k < 1 || k > 12) fail(HSF_ERR_UNSUPPORTED_GATE, "u gate arity must be 1..12");
+      size_t need = 2 + (size_t)k + 2 * ((size_t)1 << (2 * k));
+      if (tok.size() != need) fail(HSF_ERR_PARSE, "line " + std::to_string(lineno) + ": bad u payload length");
+      g.name = "u";
+      g.k = k;
+      for (int j = 0; j < k; ++j) g.q.push_back(integer(tok[2 + j]));
+      size_t d2 = (size_t)1 << (2 * k);
+      g.U.resize(d2);
+      for (size_t e = 0; e < d2; ++e) g.U[e] = cd(num(tok[2 + k + 2 * e]), num(tok[3 + k + 2 * e]));
+    } else {
+      auto it = arity.find(tok[0]);
+      if (it == arity.end()) fail(HSF_ERR_UNSUPPORTED_GATE, "line " + std::to_string(lineno) + ": unknown gate '" + tok[0] + "'");
+      int np = it->second.first, nq = it->second.second;
+      if ((int)tok.size() != 1 + np + nq) fail(HSF_ERR_UNSUPPORTED_GATE, "line " + std::to_string(lineno) + ": wrong arity");
+      std::vector<double> prm;
+      std::vector<int> q;
+      for (int j = 0; j < np; ++j) prm.push_back(num(tok[1 + j]));
+      for (int j = 0; j < nq; ++j) q.push_back(integer(tok[1 + np + j]));
+      g = make_named(tok[0], prm, q);
+    }
+    std::set<int> seen;
+    for (int q : g.q) {
+      if (q < 0 || q >= n) fail(HSF_ERR_DUPLICATE_QUBIT, "line " + std::to_string(lineno) + ": qubit out of range");
+      if (!seen.insert(q).second) fail(HSF_ERR_DUPLICATE_QUBIT, "line " + std::to_string(lineno) + ": duplicate qubit");
+    }
+    g.diag = is_diag(g);
+    gates.push_back(std::move(g));
+  }
+  if (n < 0) fail(HSF_ERR_PARSE, "missing 'qubits' line");
+  *n_out = n;
+  return gates;
+}
+
+// ------------------------------------------------------------- linear algebra
+// Embed gate g into a block-local space whose bit t is support[t].
+static std::vector<cd> embed(const Gate& g, const std::vector<int>& support) {
+  const int ks = (int)support.size();
+  const size_t N = (size_t)1 << ks;
+  std::vector<int> pos(g.k);
+  for (int j = 0; j < g.k; ++j)
+    pos[j] = (int)(std::find(support.begin(), support.end(), g.q[j]) - support.begin());
+  std::vector<cd> E(N * N, 0.0);
+  const int dg = 1 << g.k;
+  for (size_t col = 0; col < N; ++col) {
+    int jl = 0;
+    for (int j = 0; j < g.k; ++j) jl = (jl << 1) | (int)((col >> pos[j]) & 1);
+    size_t clear = col;
+    for (int j = 0; j < g.k; ++j) clear &= ~((size_t)1 << pos[j]);
+    for (int il = 0; il < dg; ++il) {
+      size_t row = clear;
+      for (int j = 0; j < g.k; ++j) row |= (size_t)((il >> (g.k - 1 - j)) & 1) << pos[j];
+      E[row * N + col] += g.U[(size_t)il * dg + jl];
+    }
+  }
+  return E;
+}
+
+static std::vector<cd> matmul(const std::vector<cd>& A, const std::vector<cd>& B, size_t N) {
+  std::vector<cd> C(N * N, 0.0);
+  for (size_t i = 0; i < N; ++i)
+    for (size_t k = 0; k < N; ++k) {
+      cd a = A[i * N + k];
+      if (a == cd(0.0)) continue;
+      for (size_t j = 0; j < N; ++j) C[i * N + j] += a * B[k * N + j];
+    }
+  return C;
+}
+
+// One-sided (Hestenes) complex Jacobi SVD of an R x C matrix (row-major).
+// Returns sigma (descending), U (R x r, column m = left vector), V (C x r).
+struct Svd {
+  std::vector<double> s;
+  std::vector<std::vector<cd>> u, v;  // per singular triple
+};
+
+static Svd jacobi_svd_tall(const std::vector<cd>& M, int R, int C) {
+  // columns of A (R x C) as separate vectors
+  std::vector<std::vector<cd>> a(C, std::vector<cd>(R)), v(C, std::vector<cd>(C, 0.0));
+  for (int j = 0; j < C; ++j) {
+    for (int i = 0; i < R; ++i) a[j][i] = M[(size_t)i * C + j];
+    v[j][j] = 1.0;
+  }
+  // convergence: |a_i^H a_j| <= tol * |a_i||a_j|, plus an absolute floor so
+  // pairs of round-off-level columns (zero singular values) do not rotate forever
+  const double tol = 1e-15 * std::max(1.0, std::sqrt((double)R));
+  double frob2 = 0;
+  for (const cd& x : M) frob2 += std::norm(x);
+  const double floor_abs = 1e-32 * frob2;
+  bool converged = false;
+  for (int sweep = 0; sweep < 80 && !converged; ++sweep) {
+    converged = true;
+    for (int i = 0; i < C - 1; ++i)
+      for (int j = i + 1; j < C; ++j) {
+        double al = 0, be = 0;
+        cd ga = 0;
+        for (int r = 0; r < R; ++r) {
+          al += std::norm(a[i][r]);
+          be += std::norm(a[j][r]);
+          ga += std::conj(a[i][r]) * a[j][r];
+        }
+        double g = std::abs(ga);
+        if (g <= floor_abs || g <= tol * std::sqrt(al * be)) continue;
+        converged = false;
+        cd ph = ga / g;  // e^{i phi}
+        double zeta = (be - al) / (2.0 * g);
+        double t = (zeta >= 0 ? 1.0 : -1.0) / (std::fabs(zeta) + std::sqrt(1.0 + zeta * zeta));
+        double c = 1.0 / std::sqrt(1.0 + t * t), s = c * t;
+        cd sph = s * std::conj(ph), cph = c * std::conj(ph);
+        for (int r = 0; r < R; ++r) {
+          cd x = a[i][r], y = a[j][r];
+          a[i][r] = c * x - sph * y;
+          a[j][r] = s * x + cph * y;
+        }
+        for (int r = 0; r < C; ++r) {
+          cd x = v[i][r], y = v[j][r];
+          v[i][r] = c * x - sph * y;
+          v[j][r] = s * x + cph * y;
+        }
+      }
+  }
+  if (!converged) fail(HSF_ERR_SVD_NO_CONVERGENCE, "Jacobi SVD did not converge in 80 sweeps");
+  std::vector<int> idx(C);
+  std::vector<double> nrm(C);
+  for (int j = 0; j < C; ++j) {
+    double s = 0;
+    for (int r = 0; r < R; ++r) s += std::norm(a[j][r]);
+    nrm[j] = std::sqrt(s);
+    idx[j] = j;
+  }
+  std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) { return nrm[x] > nrm[y]; });
+  Svd out;
+  for (int j : idx) {
+    out.s.push_back(nrm[j]);
+    std::vector<cd> u(R);
+    for (int r = 0; r < R; ++r) u[r] = nrm[j] > 0 ? a[j][r] / nrm[j] : cd(0.0);
+    out.u.push_back(std::move(u));
+    out.v.push_back(v[j]);
+  }
+  return out;
+}
+
+static Svd jacobi_svd(const std::vector<cd>& M, int R, int C) {
+  if (C <= R) return jacobi_svd_tall(M, R, C);
+  // M^H = U' S V'^H  =>  M = V' S U'^H
+  std::vector<cd> MH((size_t)C * R);
+  for (int i = 0; i < R; ++i)
+    for (int j = 0; j < C; ++j) MH[(size_t)j * R + i] = std::conj(M[(size_t)i * C + j]);
+  Svd t = jacobi_svd_tall(MH, C, R);
+  std::swap(t.u, t.v);
+  return t;
+}
+
+// ----------------------------------------------------- H3-H6 one cut unit
+static void decompose_unit(const std::vector<Gate>& gates, Unit& u, int n_low, const hsf_plan_opts& o) {
+  std::set<int> sup;
+  for (int gi : u.gids)
+    for (int q : gates[gi].q) sup.insert(q);
+  u.support.assign(sup.begin(), sup.end());
+  for (int q : u.support) (q < n_low ? u.Sb : u.Sa).push_back(q);
+  const int nb = (int)u.Sb.size(), na = (int)u.Sa.size(), ks = nb + na;
+  u.diag_route = true;
+  for (int gi : u.gids) u.diag_route = u.diag_route && gates[gi].diag;
+  Svd sv;
+  if (u.diag_route) {
+    if (ks > 24) fail(HSF_ERR_BLOCK_TOO_LARGE, "diagonal block on more than 24 qubits");
+    const size_t N = (size_t)1 << ks;
+    std::vector<cd> d(N, 1.0);
+    for (int gi : u.gids) {
+      const Gate& g = gates[gi];
+      std::vector<int> pos(g.k);
+      for (int j = 0; j < g.k; ++j)
+        pos[j] = (int)(std::find(u.support.begin(), u.support.end(), g.q[j]) - u.support.begin());
+      const int dg = 1 << g.k;
+      for (size_t i = 0; i < N; ++i) {
+        int il = 0;
+        for (int j = 0; j < g.k; ++j) il = (il << 1) | (int)((i >> pos[j]) & 1);
+        d[i] *= g.U[(size_t)il * dg + il];
+      }
+    }
+    // M[i^b, i^a] = u(i^a, i^b): the diagonal operator's operator-Schmidt matrix
+    const int R = 1 << nb, C = 1 << na;
+    std::vector<cd> M((size_t)R * C);
+    for (size_t i = 0; i < N; ++i) M[(i & (R - 1)) * C + (i >> nb)] = d[i];
+    sv = jacobi_svd(M, R, C);
+  } else {
+    if (ks > o.max_dense_block_qubits)
+      fail(HSF_ERR_BLOCK_TOO_LARGE, "dense block on " + std::to_string(ks) + " qubits exceeds max_dense_block_qubits");
+    const size_t N = (size_t)1 << ks;
+    std::vector<cd> US(N * N, 0.0);
+    for (size_t i = 0; i < N; ++i) US[i * N + i] = 1.0;
+    for (int gi : u.gids) US = matmul(embed(gates[gi], u.support), US, N);  // later gates on the left
+    // Eq. 6: A~[(i^b,j^b),(i^a,j^a)] = U_S[(i^a,i^b),(j^a,j^b)]
+    const int R = 1 << (2 * nb), C = 1 << (2 * na);
+    const size_t db = (size_t)1 << nb, da = (size_t)1 << na;
+    std::vector<cd> At((size_t)R * C);
+    for (size_t ia = 0; ia < da; ++ia)
+      for (size_t ib = 0; ib < db; ++ib)
+        for (size_t ja = 0; ja < da; ++ja)
+          for (size_t jb = 0; jb < db; ++jb) {
+            size_t row = ((ia << nb) | ib), col = ((ja << nb) | jb);
+            At[(ib * db + jb) * C + (ia * da + ja)] = US[row * N + col];
+          }
+    sv = jacobi_svd(At, R, C);
+  }
+  // H6: truncation + unitary-scale normalisation
+  const double s0 = sv.s.empty() ? 0.0 : sv.s[0];
+  if (!(s0 > 0)) fail(HSF_ERR_INVALID_ARG, "block operator is zero");
+  const double sa = std::sqrt((double)(1 << na)), sb = std::sqrt((double)(1 << nb));
+  for (size_t m = 0; m < sv.s.size(); ++m) {
+    if (!(sv.s[m] > o.svd_rel_tol * s0)) break;
+    u.sigma.push_back(sv.s[m]);
+    u.c.push_back(cd(sv.s[m] / (sa * sb), 0.0));
+    // Eq. 8: X_m = sum V*_{m,(i^a,j^a)} |i^a><j^a| ; V*_{m,.} = conj(v_m)
+    std::vector<cd> X(sv.v[m].size()), Y(sv.u[m].size());
+    for (size_t e = 0; e < X.size(); ++e) X[e] = std::conj(sv.v[m][e]) * sa;
+    // Eq. 9: Y_m = sum U_{(i^b,j^b),m} |i^b><j^b|
+    for (size_t e = 0; e < Y.size(); ++e) Y[e] = sv.u[m][e] * sb;
+    u.X.push_back(std::move(X));
+    u.Y.push_back(std::move(Y));
+  }
+  u.rank = (int)u.sigma.size();
+}
+
+// -------------------------------------------------------------- H2 schedule
+struct SchedItem {
+  bool unit;
+  int id;  // gate id or unit id
+};
+
+static std::vector<SchedItem> schedule(const std::vector<Gate>& gates, const std::vector<std::vector<int>>& units) {
+  const int G = (int)gates.size();
+  std::vector<int> owner(G, -1);
+  for (size_t u = 0; u < units.size(); ++u)
+    for (int gi : units[u]) owner[gi] = (int)u;
+  // node ids: units first (0..U-1), then free gates (U + gi)
+  const int U = (int)units.size();
+  auto node_of = [&](int gi) { return owner[gi] >= 0 ? owner[gi] : U + gi; };
+  const int NN = U + G;
+  std::vector<std::set<int>> succ(NN);
+  std::vector<int> indeg(NN, 0), minid(NN, 1 << 30);
+  std::vector<char> exists(NN, 0);
+  std::map<int, int> last;
+  for (int gi = 0; gi < G; ++gi) {
+    int nd = node_of(gi);
+    exists[nd] = 1;
+    minid[nd] = std::min(minid[nd], gi);
+    for (int q : gates[gi].q) {
+      auto it = last.find(q);
+      if (it != last.end() && it->second != nd && succ[it->second].insert(nd).second) indeg[nd]++;
+      last[q] = nd;
+    }
+  }
+  using P = std::pair<int, int>;
+  std::priority_queue<P, std::vector<P>, std::greater<P>> pq;
+  int total = 0;
+  for (int v = 0; v < NN; ++v)
+    if (exists[v]) {
+      ++total;
+      if (indeg[v] == 0) pq.push({minid[v], v});
+    }
+  std::vector<SchedItem> order;
+  while (!pq.empty()) {
+    int v = pq.top().second;
+    pq.pop();
+    order.push_back(v < U ? SchedItem{true, v} : SchedItem{false, v - U});
+    for (int s : succ[v])
+      if (--indeg[s] == 0) pq.push({minid[s], s});
+  }
+  if ((int)order.size() != total) fail(HSF_ERR_NONCONVEX_BLOCK, "a block is not convex in the wire DAG");
+  return order;
+}
+
+// ----------------------------------------------------- H8 half programs
+static int64_t push_coef(Plan& P, const std::vector<cd>& v) {
+  int64_t off = (int64_t)P.coef.size();
+  P.coef.insert(P.coef.end(), v.begin(), v.end());
+  return off;
+}
+
+// Convert a gate (file order, first-listed = MSB) to an LSB-first op on a half.
+static HostOp gate_op(Plan& P, const Gate& g, int first_qubit) {
+  HostOp op;
+  op.k = g.k;
+  op.kind = g.diag ? OP_DIAG : OP_DENSE;
+  for (int j = 0; j < g.k; ++j) op.q[j] = g.q[g.k - 1 - j] - first_qubit;  // bit j <- last-listed first
+  const int d = 1 << g.k;
+  if (g.diag) {
+    std::vector<cd> dd(d);
+    for (int i = 0; i < d; ++i) dd[i] = g.U[(size_t)i * d + i];
+    op.table = push_coef(P, dd);
+  } else {
+    op.table = push_coef(P, g.U);  // MSB-first local index == LSB-first with reversed q list
+  }
+  op.stride = 0;
+  return op;
+}
+
+static std::vector<cd> op_matrix(const Plan& P, const HostOp& op) {
+  const size_t d = (size_t)1 << op.k;
+  if (op.kind == OP_DIAG) return std::vector<cd>(P.coef.begin() + op.table, P.coef.begin() + op.table + d);
+  return std::vector<cd>(P.coef.begin() + op.table, P.coef.begin() + op.table + d * d);
+}
+
+// Fusion inside one segment ("gate fusion"): (1) a 1-qubit dense op
+// merges into the previous op if that op is a fixed 1-qubit dense op on the
+// same qubit and nothing in between touched the qubit; (2) adjacent fixed
+// diagonal ops merge while their union has <= 12 qubits.
+static void fuse_segment(Plan& P, std::vector<HostOp>& seg) {
+  // (1)
+  std::vector<HostOp> out;
+  std::map<int, int> last;  // qubit -> index in out of last op touching it
+  for (const HostOp& op : seg) {
+    if (op.unit < 0 && op.kind == OP_DENSE && op.k == 1) {
+      auto it = last.find(op.q[0]);
+      if (it != last.end()) {
+        HostOp& prev = out[it->second];
+        if (prev.unit < 0 && prev.kind == OP_DENSE && prev.k == 1) {
+          auto A = op_matrix(P, op), B = op_matrix(P, prev);
+          std::vector<cd> C(4);
+          for (int i = 0; i < 2; ++i)
+            for (int j = 0; j < 2; ++j) C[i * 2 + j] = A[i * 2 + 0] * B[0 * 2 + j] + A[i * 2 + 1] * B[1 * 2 + j];
+          prev.table = push_coef(P, C);
+          continue;
+        }
+      }
+    }
+    out.push_back(op);
+    for (int j = 0; j < op.k; ++j) last[op.q[j]] = (int)out.size() - 1;
+  }
+  // (2)
+  std::vector<HostOp> out2;
+  for (const HostOp& op : out) {
+    if (!out2.empty() && op.unit < 0 && op.kind == OP_DIAG && out2.back().unit < 0 && out2.back().kind == OP_DIAG) {
+      HostOp& prev = out2.back();
+      std::set<int> uni(prev.q, prev.q + prev.k);
+      uni.insert(op.q, op.q + op.k);
+      if ((int)uni.size() <= 12) {
+        std::vector<int> qs(uni.begin(), uni.end());  // ascending
+        const int k = (int)qs.size();
+        auto Da = op_matrix(P, prev), Db = op_matrix(P, op);
+        std::vector<cd> D((size_t)1 << k);
+        for (size_t i = 0; i < D.size(); ++i) {
+          int ia = 0, ib = 0;
+          for (int j = 0; j < prev.k; ++j) {
+            int pos = (int)(std::find(qs.begin(), qs.end(), prev.q[j]) - qs.begin());
+            ia |= (int)((i >> pos) & 1) << j;
+          }
+          for (int j = 0; j < op.k; ++j) {
+            int pos = (int)(std::find(qs.begin(), qs.end(), op.q[j]) - qs.begin());
+            ib |= (int)((i >> pos) & 1) << j;
+          }
+          D[i] = Da[ia] * Db[ib];
+        }
+        HostOp f;
+        f.kind = OP_DIAG;
+        f.k = k;
+        for (int j = 0; j < k; ++j) f.q[j] = qs[j];
+        f.table = push_coef(P, D);
+        prev = f;
+        continue;
+      }
+    }
+    out2.push_back(op);
+  }
+  seg.swap(out2);
+}
+
+// Greedy tile-pass planner for halves larger than the SMEM-resident limit.
+// Tile = 2^t amplitudes with tile qubits T (always 0..4 for 256 B coalesced
+// rows).  A dense op joins the pass if its qubits fit in T (|T| <= t); a
+// diagonal op joins regardless of T (its non-tile bits are fixed per tile);
+// an op touching a qubit already deferred is deferred (order is preserved).
+static DevOp to_dev(const HostOp& op, const std::vector<int>* T) {
+  DevOp d{};
+  d.kind = op.kind;
+  d.k = op.k;
+  for (int j = 0; j < op.k; ++j)
+    d.q[j] = (T && op.kind == OP_DENSE) ? (int)(std::find(T->begin(), T->end(), op.q[j]) - T->begin()) : op.q[j];
+  d.radix = 1;
+  d.table = op.table;
+  d.stride = op.stride;
+  d.div = op.unit;  // unit id until resolved per transition
+  return d;
+}
+
+static void plan_passes(Half& H, Transition& tr, int64_t ob, int64_t oe, int t) {
+  const int low = 5;
+  std::vector<int64_t> pending;
+  for (int64_t i = ob; i < oe; ++i) pending.push_back(i);
+  do {
+    std::set<int> T;
+    for (int i = 0; i < low; ++i) T.insert(i);
+    std::set<int> blocked;
+    std::vector<int64_t> take, rest;
+    for (int64_t oi : pending) {
+      const HostOp& op = H.ops[oi];
+      bool blk = false;
+      for (int j = 0; j < op.k; ++j) blk = blk || blocked.count(op.q[j]);
+      if (blk) {
+        for (int j = 0; j < op.k; ++j) blocked.insert(op.q[j]);
+        rest.push_back(oi);
+        continue;
+      }
+      if (op.kind == OP_DIAG) {
+        take.push_back(oi);
+        continue;
+      }
+      std::set<int> need = T;
+      for (int j = 0; j < op.k; ++j) need.insert(op.q[j]);
+      if ((int)need.size() <= t) {
+        T = need;
+        take.push_back(oi);
+      } else {
+        for (int j = 0; j < op.k; ++j) blocked.insert(op.q[j]);
+        rest.push_back(oi);
+      }
+    }
+    if (take.empty() && !pending.empty()) fail(HSF_ERR_UNSUPPORTED, "pass planner made no progress");
+    for (int q = 0; q < H.m && (int)T.size() < t; ++q) T.insert(q);
+    Pass p;
+    p.t = t;
+    p.T.assign(T.begin(), T.end());  // ascending: tile positions 0..4 are qubits 0..4
+    p.op_begin = (int64_t)H.dev_ops.size();
+    for (int64_t oi : take) H.dev_ops.push_back(to_dev(H.ops[oi], &p.T));
+    p.op_end = (int64_t)H.dev_ops.size();
+    tr.passes.push_back(std::move(p));
+    pending.swap(rest);
+  } while (!pending.empty());
+}
+
+static void build_half(Plan& P, int h, const std::vector<SchedItem>& order) {
+  Half& H = P.half[h];
+  const int n_low = P.n_low;
+  H.first_qubit = (h == 0) ? n_low : 0;
+  H.m = (h == 0) ? P.n - n_low : n_low;
+  const int U = (int)P.units.size();
+  // segments
+  std::vector<std::vector<HostOp>> segs(U + 1);
+  std::vector<HostOp> factors(U);
+  int level = 0;
+  for (const SchedItem& it : order) {
+    if (it.unit) {
+      const Unit& u = P.units[it.id];
+      const std::vector<int>& S = (h == 0) ? u.Sa : u.Sb;
+      const auto& F = (h == 0) ? u.X : u.Y;
+      HostOp op;
+      op.k = (int)S.size();
+      op.kind = u.diag_route ? OP_DIAG : OP_DENSE;
+      if (op.kind == OP_DENSE && op.k > kMaxDenseQ)
+        fail(HSF_ERR_BLOCK_TOO_LARGE, "dense Schmidt factor on more than 5 qubits of one half");
+      if (op.kind == OP_DIAG && op.k > kMaxOpQ) fail(HSF_ERR_BLOCK_TOO_LARGE, "diagonal factor on more than 13 qubits");
+      for (int j = 0; j < op.k; ++j) op.q[j] = S[j] - H.first_qubit;  // ascending = LSB-first
+      op.unit = it.id;
+      op.table = (int64_t)P.coef.size();
+      for (const auto& f : F) P.coef.insert(P.coef.end(), f.begin(), f.end());
+      op.stride = (int64_t)F[0].size();
+      factors[it.id] = op;
+      level = it.id + 1;
+    } else {
+      const Gate& g = P.gates[it.id];
+      bool low = true, high = true;
+      for (int q : g.q) {
+        low = low && q < n_low;
+        high = high && q >= n_low;
+      }
+      if ((h == 0 && high) || (h == 1 && low)) {
+        HostOp op = gate_op(P, g, H.first_qubit);
+        if (op.kind == OP_DENSE && op.k > kMaxDenseQ) fail(HSF_ERR_UNSUPPORTED, "dense local gate on more than 5 qubits");
+        if (op.kind == OP_DIAG && op.k > kMaxOpQ) fail(HSF_ERR_UNSUPPORTED, "diagonal local gate on more than 13 qubits");
+        segs[level].push_back(op);
+      }
+    }
+  }
+  if (P.opts.fuse_gates)
+    for (auto& s : segs) fuse_segment(P, s);
+  // flatten: seg_0, F_0, seg_1, ..., F_{U-1}, seg_U
+  H.ops.clear();
+  H.seg_end.assign(U + 1, 0);
+  for (int l = 0; l <= U; ++l) {
+    if (l > 0) H.ops.push_back(factors[l - 1]);
+    for (auto& op : segs[l]) H.ops.push_back(op);
+    H.seg_end[l] = (int64_t)H.ops.size();
+  }
+  // materialised levels: those followed by a dense op in their segment, plus the leaves
+  H.materialized.clear();
+  for (int l = 0; l < U; ++l) {
+    bool dense = false;
+    for (auto& op : segs[l]) dense = dense || op.kind == OP_DENSE;
+    if (dense) H.materialized.push_back(l);
+  }
+  H.materialized.push_back(U);
+  // transitions + passes
+  const int smem_limit = (P.opts.dtype == HSF_C64) ? 13 : 12;
+  const int t = std::min(H.m, P.opts.tile_qubits);
+  H.trans.clear();
+  H.dev_ops.clear();
+  H.n_passes = 0;
+  int prev = -1;
+  for (int L : H.materialized) {
+    Transition tr;
+    tr.level_in = prev;
+    tr.level_out = L;
+    int64_t ob = (prev < 0) ? 0 : H.seg_end[prev];
+    int64_t oe = H.seg_end[L];
+    if (H.m <= smem_limit) {
+      Pass p;
+      p.t = H.m;
+      for (int i = 0; i < H.m; ++i) p.T.push_back(i);
+      p.op_begin = (int64_t)H.dev_ops.size();
+      for (int64_t oi = ob; oi < oe; ++oi) H.dev_ops.push_back(to_dev(H.ops[oi], nullptr));
+      p.op_end = (int64_t)H.dev_ops.size();
+      tr.passes.push_back(p);
+    } else {
+      plan_passes(H, tr, ob, oe, t);
+    }
+    // resolve factor digits for this transition's output level
+    for (auto& p : tr.passes)
+      for (int64_t i = p.op_begin; i < p.op_end; ++i) {
+        DevOp& d = H.dev_ops[i];
+        int unit = (int)d.div;
+        if (unit >= 0) {
+          d.radix = P.ranks[unit];
+          d.div = (int64_t)range_prod(P.ranks, unit + 1, L);
+        } else {
+          d.radix = 1;
+          d.div = 1;
+        }
+        d.contiguous = 1;
+        for (int j = 1; j < d.k; ++j) d.contiguous = d.contiguous && (d.q[j] == d.q[0] + j);
+      }
+    H.n_passes += (int)tr.passes.size();
+    H.trans.push_back(std::move(tr));
+    prev = L;
+  }
+}
+
+static uint64_t fnv(uint64_t h, const void* p, size_t n) {
+  const unsigned char* b = (const unsigned char*)p;
+  for (size_t i = 0; i < n; ++i) {
+    h ^= b[i];
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+// ----------------------------------------------------------------- driver
+Plan* build_plan(const char* text, size_t len, int n_low, int64_t n_blocks, const int64_t* off, const int64_t* ids,
+                 const hsf_plan_opts& opts) {
+  auto P = std::make_unique<Plan>();
+  P->opts = opts;
+  P->gates = parse(text, len, &P->n);
+  P->n_low = n_low;
+  if (n_low < 1 || n_low >= P->n) fail(HSF_ERR_INVALID_ARG, "n_low must satisfy 1 <= n_low < n");
+  const int G = (int)P->gates.size();
+  auto crossing = [&](int gi) {
+    bool lo = false, hi = false;
+    for (int q : P->gates[gi].q) (q < n_low ? lo : hi) = true;
+    return lo && hi;
+  };
+  // units: user blocks (joint mode) + singleton crossing gates
+  std::vector<std::vector<int>> units;
+  std::vector<char> in_block(G, 0);
+  if (!opts.individual && n_blocks > 0) {
+    if (!off || !ids) fail(HSF_ERR_INVALID_ARG, "block CSR arrays are NULL");
+    for (int64_t b = 0; b < n_blocks; ++b) {
+      if (off[b + 1] < off[b]) fail(HSF_ERR_INVALID_ARG, "block offsets not monotone");
+      std::vector<int> blk;
+      for (int64_t e = off[b]; e < off[b + 1]; ++e) {
+        int64_t gi = ids[e];
+        if (gi < 0 || gi >= G) fail(HSF_ERR_INVALID_ARG, "block gate id out of range");
+        if (in_block[gi]) fail(HSF_ERR_INVALID_ARG, "gate in two blocks");
+        in_block[gi] = 1;
+        blk.push_back((int)gi);
+      }
+      if (blk.empty()) continue;
+      std::sort(blk.begin(), blk.end());
+      units.push_back(blk);
+    }
+  }
+  for (int gi = 0; gi < G; ++gi)
+    if (!in_block[gi] && crossing(gi)) units.push_back({gi});
+  auto order = schedule(P->gates, units);
+  // renumber units in schedule order
+  std::vector<int> remap(units.size(), -1);
+  int nu = 0;
+  for (auto& it : order)
+    if (it.unit) {
+      remap[it.id] = nu;
+      P->units.emplace_back();
+      P->units.back().gids = units[it.id];
+      it.id = nu++;
+    }
+  // H3-H6
+  double log2_np = 0;
+  for (auto& u : P->units) {
+    decompose_unit(P->gates, u, n_low, opts);
+    log2_np += std::log2((double)u.rank);
+  }
+  // individual-cut count n_p^t: product of the individual crossing-gate ranks
+  P->log2_individual = 0;
+  {
+    hsf_plan_opts o2 = opts;
+    for (int gi = 0; gi < G; ++gi)
+      if (crossing(gi)) {
+        Unit tmp;
+        tmp.gids = {gi};
+        decompose_unit(P->gates, tmp, n_low, o2);
+        P->log2_individual += std::log2((double)tmp.rank);
+      }
+  }
+  // H7
+  if (log2_np > opts.log2_path_budget + 1e-9)
+    fail(HSF_ERR_PATH_BUDGET, "n_p = 2^" + std::to_string(log2_np) + " exceeds the path budget");
+  P->n_paths = 1;
+  P->sigma_off.push_back(0);
+  for (auto& u : P->units) {
+    P->n_paths *= (uint64_t)u.rank;
+    P->ranks.push_back(u.rank);
+    P->sa.push_back((int32_t)u.Sa.size());
+    P->sb.push_back((int32_t)u.Sb.size());
+    P->sigmas.insert(P->sigmas.end(), u.sigma.begin(), u.sigma.end());
+    P->sigma_off.push_back((int64_t)P->sigmas.size());
+  }
+  // H8
+  build_half(*P, 0, order);
+  build_half(*P, 1, order);
+  // hash
+  uint64_t h = 1469598103934665603ull;
+  h = fnv(h, &P->n, sizeof(int));
+  h = fnv(h, &P->n_low, sizeof(int));
+  for (int s = 0; s < 2; ++s)
+    h = fnv(h, P->half[s].dev_ops.data(), P->half[s].dev_ops.size() * sizeof(DevOp));
+  h = fnv(h, P->coef.data(), P->coef.size() * sizeof(cd));
+  h = fnv(h, P->ranks.data(), P->ranks.size() * sizeof(int32_t));
+  P->hash = h;
+  return P.release();
+}
+
+}  // namespace hsf

@@ -1,0 +1,521 @@
+// run.cu — C ABI of libhsf.so (include/hsf.h): plan lifetime, device tables,
+// workspace, and hsf_run's launch sequence
+//   half A tree -> half B tree -> coefficient fold -> path-sum.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "hsf_internal.h"
+#include "sim_kernels.cuh"
+#include "sum_kernels.cuh"
+#include "gemm_tc.cuh"
+
+namespace hsf {
+
+static thread_local std::string g_last_error;
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+#define CK(x)                                                                                          \
+  do {                                                                                                 \
+    cudaError_t e_ = (x);                                                                              \
+    if (e_ != cudaSuccess)                                                                             \
+      fail(HSF_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_) + " @" + std::to_string(__LINE__)); \
+  } while (0)
+
+struct DeviceState {
+  int device = -1;
+  size_t elem = 8;          // bytes per complex
+  void* coef = nullptr;     // complex table (run dtype)
+  DevOp* ops[2] = {nullptr, nullptr};
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  // cached per-range path coefficients
+  void* cp = nullptr;
+  size_t cp_cap = 0;
+  uint64_t cp_p0 = ~0ull, cp_p1 = ~0ull;
+  cudaEvent_t ev[5] = {};
+  bool sticky = false;
+};
+
+void destroy_device(Plan* p) {
+  auto* d = (DeviceState*)p->dev;
+  if (!d) return;
+  int cur = -1;
+  cudaGetDevice(&cur);
+  if (d->device >= 0) cudaSetDevice(d->device);
+  cudaFree(d->coef);
+  cudaFree(d->ops[0]);
+  cudaFree(d->ops[1]);
+  cudaFree(d->ws);
+  cudaFree(d->cp);
+  for (auto& e : d->ev)
+    if (e) cudaEventDestroy(e);
+  if (cur >= 0) cudaSetDevice(cur);
+  delete d;
+  p->dev = nullptr;
+}
+
+static DeviceState* ensure_device(Plan* P, int device) {
+  auto* d = (DeviceState*)P->dev;
+  if (d && d->sticky) fail(HSF_ERR_CUDA, "plan is unusable after an earlier CUDA error");
+  if (device < 0) CK(cudaGetDevice(&device));
+  if (d && d->device != device) fail(HSF_ERR_INVALID_ARG, "plan already bound to another device");
+  CK(cudaSetDevice(device));
+  if (d) return d;
+  d = new DeviceState();
+  P->dev = d;
+  d->device = device;
+  const bool c64 = P->opts.dtype == HSF_C64;
+  d->elem = c64 ? 8 : 16;
+  // coefficient table in the run dtype (fp64 master -> fp32 by RNE)
+  size_t n = std::max<size_t>(P->coef.size(), 1);
+  CK(cudaMalloc(&d->coef, n * d->elem));
+  if (c64) {
+    std::vector<float2> h(n);
+    for (size_t i = 0; i < P->coef.size(); ++i) h[i] = make_float2((float)P->coef[i].real(), (float)P->coef[i].imag());
+    CK(cudaMemcpy(d->coef, h.data(), n * 8, cudaMemcpyHostToDevice));
+  } else {
+    CK(cudaMemcpy(d->coef, P->coef.data(), P->coef.size() * 16, cudaMemcpyHostToDevice));
+  }
+  for (int h = 0; h < 2; ++h) {
+    size_t no = std::max<size_t>(P->half[h].dev_ops.size(), 1);
+    CK(cudaMalloc(&d->ops[h], no * sizeof(DevOp)));
+    if (!P->half[h].dev_ops.empty())
+      CK(cudaMemcpy(d->ops[h], P->half[h].dev_ops.data(), P->half[h].dev_ops.size() * sizeof(DevOp),
+                    cudaMemcpyHostToDevice));
+  }
+  for (auto& e : d->ev) CK(cudaEventCreate(&e));
+  return d;
+}
+
+// ----------------------------------------------------------- workspace
+struct Layout {
+  uint64_t p0, p1, K;
+  bool bits_mode;
+  uint64_t r0, r1;
+  hsf_precision prec;
+  size_t scratch_elems = 0;    // per ping-pong buffer
+  size_t off_scratch[2] = {0, 0};
+  size_t off_leaves[2] = {0, 0};
+  size_t off_T[2] = {0, 0};    // transposed operands (bitstring mode)
+  size_t off_bits = 0, off_out = 0, off_tc = 0;
+  size_t tc_bytes = 0;
+  size_t total = 0;
+};
+
+static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static uint64_t nodes_at(const Plan& P, int L, uint64_t p0, uint64_t p1) {
+  uint64_t S = suffix_prod(P.ranks, L);
+  return (p1 - 1) / S - p0 / S + 1;
+}
+
+static Layout make_layout(const Plan& P, const hsf_run_args& a, size_t elem) {
+  Layout L{};
+  L.p0 = a.path_begin;
+  L.p1 = a.path_end;
+  if (L.p0 == 0 && L.p1 == 0) L.p1 = P.n_paths;
+  if (L.p0 >= L.p1 || L.p1 > P.n_paths) fail(HSF_ERR_INVALID_ARG, "bad path range");
+  L.K = L.p1 - L.p0;
+  L.bits_mode = a.n_bitstrings > 0;
+  if (!L.bits_mode && a.bitstrings) fail(HSF_ERR_INVALID_ARG, "bitstrings given with n_bitstrings == 0");
+  if (L.bits_mode && !a.bitstrings) fail(HSF_ERR_INVALID_ARG, "n_bitstrings > 0 but bitstrings is NULL");
+  if (L.bits_mode && P.n > 63) fail(HSF_ERR_INVALID_ARG, "bitstring runs need n <= 63");
+  const int nA = P.n - P.n_low, nB = P.n_low;
+  L.r0 = a.row_begin;
+  L.r1 = a.row_end;
+  if (L.r0 == 0 && L.r1 == 0) L.r1 = 1ull << nA;
+  if (!L.bits_mode && (L.r0 >= L.r1 || L.r1 > (1ull << nA))) fail(HSF_ERR_INVALID_ARG, "bad row range");
+  L.prec = a.precision;
+  if (L.prec == HSF_PREC_AUTO) L.prec = HSF_PREC_SIMT;
+  if (P.opts.dtype == HSF_C128 && L.prec != HSF_PREC_SIMT) fail(HSF_ERR_UNSUPPORTED, "complex128 path-sum is SIMT fp64 only");
+  size_t off = 0;
+  for (int h = 0; h < 2; ++h) {
+    const Half& H = P.half[h];
+    const size_t st = (size_t)1 << H.m;
+    for (size_t i = 0; i + 1 < H.trans.size(); ++i)
+      L.scratch_elems = std::max(L.scratch_elems, (size_t)nodes_at(P, H.trans[i].level_out, L.p0, L.p1) * st);
+  }
+  for (int b = 0; b < 2; ++b) {
+    L.off_scratch[b] = off;
+    off = align_up(off + L.scratch_elems * elem);
+  }
+  for (int h = 0; h < 2; ++h) {
+    L.off_leaves[h] = off;
+    off = align_up(off + ((size_t)L.K << P.half[h].m) * elem);
+  }
+  if (L.bits_mode) {
+    for (int h = 0; h < 2; ++h) {
+      L.off_T[h] = off;
+      off = align_up(off + ((size_t)L.K << P.half[h].m) * elem);
+    }
+    if (!a.bits_on_device) {
+      L.off_bits = off;
+      off = align_up(off + a.n_bitstrings * 8);
+    }
+    if (!a.out_on_device) {
+      L.off_out = off;
+      off = align_up(off + a.n_bitstrings * elem);
+    }
+  } else {
+    if (L.prec == HSF_PREC_BF16X3 || L.prec == HSF_PREC_BF16X1) {
+      L.tc_bytes = tc_workspace_bytes((long long)L.K, (long long)(L.r1 - L.r0), 1ll << nB, L.prec == HSF_PREC_BF16X3);
+      L.off_tc = off;
+      off = align_up(off + L.tc_bytes);
+    }
+    if (!a.out_on_device) {
+      L.off_out = off;
+      off = align_up(off + ((size_t)(L.r1 - L.r0) << nB) * elem);
+    }
+  }
+  L.total = off;
+  return L;
+}
+
+static void ensure_ws(DeviceState* d, size_t bytes) {
+  if (d->ws_bytes >= bytes) return;
+  if (d->ws) CK(cudaFree(d->ws));
+  d->ws = nullptr;
+  d->ws_bytes = 0;
+  cudaError_t e = cudaMalloc(&d->ws, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    fail(HSF_ERR_OUT_OF_MEMORY, "device workspace of " + std::to_string(bytes) + " bytes");
+  }
+  d->ws_bytes = bytes;
+}
+
+// c_p = prod_u c_{u, d_u} for p in [p0, p1), fp64 on the host -> run dtype
+static void ensure_cp(Plan* P, DeviceState* d, uint64_t p0, uint64_t p1, cudaStream_t st) {
+  if (d->cp_p0 == p0 && d->cp_p1 == p1) return;
+  const uint64_t K = p1 - p0;
+  if (d->cp_cap < K) {
+    if (d->cp) CK(cudaFree(d->cp));
+    CK(cudaMalloc(&d->cp, K * d->elem));
+    d->cp_cap = K;
+  }
+  const int U = (int)P->units.size();
+  std::vector<cd> c(K);
+  for (uint64_t p = p0; p < p1; ++p) {
+    uint64_t x = p;
+    cd v = 1.0;
+    for (int u = U - 1; u >= 0; --u) {
+      v *= P->units[u].c[x % P->ranks[u]];
+      x /= P->ranks[u];
+    }
+    c[p - p0] = v;
+  }
+  if (P->opts.dtype == HSF_C64) {
+    std::vector<float2> h(K);
+    for (uint64_t i = 0; i < K; ++i) h[i] = make_float2((float)c[i].real(), (float)c[i].imag());
+    CK(cudaMemcpyAsync(d->cp, h.data(), K * 8, cudaMemcpyHostToDevice, st));
+  } else {
+    CK(cudaMemcpyAsync(d->cp, c.data(), K * 16, cudaMemcpyHostToDevice, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  d->cp_p0 = p0;
+  d->cp_p1 = p1;
+}
+
+template <typename R>
+static void run_half(const Plan& P, DeviceState* d, int h, const Layout& L, cudaStream_t st) {
+  using C = typename cplx<R>::T;
+  const Half& H = P.half[h];
+  char* ws = (char*)d->ws;
+  const size_t st_elems = (size_t)1 << H.m;
+  const void* prev_buf = nullptr;
+  int prev_level = -1;
+  for (size_t ti = 0; ti < H.trans.size(); ++ti) {
+    const Transition& tr = H.trans[ti];
+    const bool last = (ti + 1 == H.trans.size());
+    void* out = ws + (last ? L.off_leaves[h] : L.off_scratch[ti & 1]);
+    const uint64_t S_out = suffix_prod(P.ranks, tr.level_out);
+    const uint64_t first_out = L.p0 / S_out;
+    const uint64_t n_out = (L.p1 - 1) / S_out - first_out + 1;
+    for (size_t pi = 0; pi < tr.passes.size(); ++pi) {
+      const Pass& ps = tr.passes[pi];
+      PassParams pp{};
+      pp.dst = out;
+      pp.ops = d->ops[h] + ps.op_begin;
+      pp.n_ops = (int)(ps.op_end - ps.op_begin);
+      pp.coef = d->coef;
+      pp.m = H.m;
+      pp.t = ps.t;
+      pp.state_elems = (long long)st_elems;
+      if (ps.t < H.m) {
+        pp.n_hi = ps.t - 5;
+        for (int j = 5; j < ps.t; ++j) pp.T_hi[j - 5] = ps.T[j];
+        pp.n_nt = 0;
+        for (int q = 0; q < H.m; ++q)
+          if (std::find(ps.T.begin(), ps.T.end(), q) == ps.T.end()) pp.nonT[pp.n_nt++] = q;
+        if (pp.n_nt > kMaxNonTile) fail(HSF_ERR_UNSUPPORTED, "half too large for the tile kernel");
+      }
+      const size_t smem = (sizeof(C) << ps.t) + (ps.t < H.m ? (sizeof(long long) << (ps.t - 5)) : 0);
+      CK(cudaFuncSetAttribute(hsf_pass_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      const uint64_t tiles = 1ull << (H.m - ps.t);
+      for (uint64_t y0 = 0; y0 < n_out; y0 += 65535) {
+        const uint64_t ny = std::min<uint64_t>(65535, n_out - y0);
+        pp.node_first = (long long)(first_out + y0);
+        pp.node_local0 = (long long)y0;
+        if (pi == 0) {
+          if (prev_level < 0) {
+            pp.src = nullptr;
+          } else {
+            pp.src = prev_buf;
+            const uint64_t S_in = suffix_prod(P.ranks, prev_level);
+            pp.src_first = (long long)(L.p0 / S_in);
+            pp.src_div = (long long)range_prod(P.ranks, prev_level, tr.level_out);
+          }
+        } else {  // in place on this level's buffer
+          pp.src = out;
+          pp.src_first = (long long)first_out;
+          pp.src_div = 1;
+        }
+        dim3 grid((unsigned)tiles, (unsigned)ny);
+        hsf_pass_kernel<R><<<grid, kSimThreads, smem, st>>>(pp);
+        CK(cudaGetLastError());
+      }
+    }
+    prev_buf = out;
+    prev_level = tr.level_out;
+  }
+}
+
+template <typename R>
+static void run_sum(Plan* P, DeviceState* d, const Layout& L, const hsf_run_args& a, cudaStream_t st) {
+  using C = typename cplx<R>::T;
+  char* ws = (char*)d->ws;
+  const int nA = P->n - P->n_low, nB = P->n_low;
+  const long long K = (long long)L.K;
+  const C* cp = (const C*)d->cp;
+  const C* leavesA = (const C*)(ws + L.off_leaves[0]);
+  const C* leavesB = (const C*)(ws + L.off_leaves[1]);
+  if (L.bits_mode) {
+    C* AT = (C*)(ws + L.off_T[0]);
+    C* BT = (C*)(ws + L.off_T[1]);
+    dim3 blk(32, 8);
+    dim3 gA((unsigned)(((1ll << nA) + 31) / 32), (unsigned)((K + 31) / 32));
+    transpose_fold_kernel<C><<<gA, blk, 0, st>>>(leavesA, AT, cp, K, 1ll << nA);
+    CK(cudaGetLastError());
+    dim3 gB((unsigned)(((1ll << nB) + 31) / 32), (unsigned)((K + 31) / 32));
+    transpose_fold_kernel<C><<<gB, blk, 0, st>>>(leavesB, BT, nullptr, K, 1ll << nB);
+    CK(cudaGetLastError());
+    const unsigned long long* bits = (const unsigned long long*)a.bitstrings;
+    if (!a.bits_on_device) {
+      bits = (const unsigned long long*)(ws + L.off_bits);
+      CK(cudaMemcpyAsync((void*)bits, a.bitstrings, a.n_bitstrings * 8, cudaMemcpyHostToDevice, st));
+    }
+    C* out = a.out_on_device ? (C*)a.out : (C*)(ws + L.off_out);
+    const long long ns = (long long)a.n_bitstrings;
+    long long blocks = std::min<long long>((ns + 7) / 8, 148ll * 64);
+    if (sizeof(R) == 4 && K % 64 == 0) {
+      gather_dot_c64_vec_kernel<<<(unsigned)blocks, 256, 0, st>>>((const float4*)AT, (const float4*)BT, bits,
+                                                                  (float2*)out, ns, K, nB);
+    } else {
+      gather_dot_kernel<C><<<(unsigned)blocks, 256, 0, st>>>(AT, BT, bits, out, ns, K, nB);
+    }
+    CK(cudaGetLastError());
+    if (!a.out_on_device) CK(cudaMemcpyAsync(a.out, out, a.n_bitstrings * sizeof(C), cudaMemcpyDeviceToHost, st));
+  } else {
+    const long long rows = (long long)(L.r1 - L.r0);
+    C* out = a.out_on_device ? (C*)a.out : (C*)(ws + L.off_out);
+    if (L.prec == HSF_PREC_SIMT) {
+      dim3 grid((unsigned)(((1ll << nB) + 63) / 64), (unsigned)((rows + 63) / 64));
+      simt_gemm_kernel<C, R><<<grid, 256, 0, st>>>(leavesA, leavesB, cp, out, K, 1ll << nA, 1ll << nB,
+                                                   (long long)L.r0, rows);
+      CK(cudaGetLastError());
+    } else {
+      if (sizeof(R) != 4) fail(HSF_ERR_UNSUPPORTED, "tensor-core path-sum needs complex64");
+      tc_path_sum((const float2*)leavesA, (const float2*)leavesB, (const float2*)cp, (float2*)out, K, 1ll << nA,
+                  1ll << nB, (long long)L.r0, rows, L.prec == HSF_PREC_BF16X3, ws + L.off_tc, L.tc_bytes, st);
+    }
+    if (!a.out_on_device)
+      CK(cudaMemcpyAsync(a.out, out, ((size_t)rows << nB) * sizeof(C), cudaMemcpyDeviceToHost, st));
+  }
+}
+
+static void run(Plan* P, const hsf_run_args& a) {
+  DeviceState* d = ensure_device(P, a.device);
+  Layout L = make_layout(*P, a, d->elem);
+  if (!a.out) fail(HSF_ERR_INVALID_ARG, "out is NULL");
+  ensure_ws(d, L.total);
+  cudaStream_t st = (cudaStream_t)a.cuda_stream;
+  ensure_cp(P, d, L.p0, L.p1, st);
+  const bool timed = a.phase_ms != nullptr;
+  try {
+    if (timed) CK(cudaEventRecord(d->ev[0], st));
+    if (P->opts.dtype == HSF_C64) {
+      run_half<float>(*P, d, 0, L, st);
+      if (timed) CK(cudaEventRecord(d->ev[1], st));
+      run_half<float>(*P, d, 1, L, st);
+      if (timed) CK(cudaEventRecord(d->ev[2], st));
+      run_sum<float>(P, d, L, a, st);
+    } else {
+      run_half<double>(*P, d, 0, L, st);
+      if (timed) CK(cudaEventRecord(d->ev[1], st));
+      run_half<double>(*P, d, 1, L, st);
+      if (timed) CK(cudaEventRecord(d->ev[2], st));
+      run_sum<double>(P, d, L, a, st);
+    }
+    if (timed) CK(cudaEventRecord(d->ev[3], st));
+    if (timed || !a.out_on_device) CK(cudaStreamSynchronize(st));
+    if (timed) {
+      float t0, t1, t2, t3;
+      CK(cudaEventElapsedTime(&t0, d->ev[0], d->ev[1]));
+      CK(cudaEventElapsedTime(&t1, d->ev[1], d->ev[2]));
+      CK(cudaEventElapsedTime(&t2, d->ev[2], d->ev[3]));
+      CK(cudaEventElapsedTime(&t3, d->ev[0], d->ev[3]));
+      a.phase_ms[0] = t0;
+      a.phase_ms[1] = t1;
+      a.phase_ms[2] = t2;
+      a.phase_ms[3] = t3;
+    }
+  } catch (Error& e) {
+    if (e.st == HSF_ERR_CUDA) d->sticky = true;
+    throw;
+  }
+}
+
+}  // namespace hsf
+
+using namespace hsf;
+
+#define ABI_GUARD(body)                        \
+  try {                                        \
+    body;                                      \
+    return HSF_OK;                             \
+  } catch (const Error& e) {                   \
+    set_last_error(e.msg);                     \
+    return e.st;                               \
+  } catch (const std::bad_alloc&) {            \
+    set_last_error("host allocation failed");  \
+    return HSF_ERR_OUT_OF_MEMORY;              \
+  } catch (const std::exception& e) {          \
+    set_last_error(e.what());                  \
+    return HSF_ERR_INVALID_ARG;                \
+  } catch (...) {                              \
+    set_last_error("unknown C++ exception");   \
+    return HSF_ERR_INVALID_ARG;                \
+  }
+
+extern "C" {
+
+hsf_status hsf_plan_opts_default(hsf_plan_opts* o) {
+  if (!o) return HSF_ERR_INVALID_ARG;
+  o->dtype = HSF_C64;
+  o->svd_rel_tol = 1e-12;
+  o->max_dense_block_qubits = 10;
+  o->log2_path_budget = 26;
+  o->individual = 0;
+  o->tile_qubits = 12;
+  o->fuse_gates = 1;
+  return HSF_OK;
+}
+
+hsf_status hsf_plan(const char* text, size_t len, int32_t n_low, int64_t n_blocks, const int64_t* off,
+                    const int64_t* ids, const hsf_plan_opts* opts, hsf_plan_t** out) {
+  ABI_GUARD({
+    if (!text || !out) fail(HSF_ERR_INVALID_ARG, "NULL argument");
+    if (n_blocks < 0) fail(HSF_ERR_INVALID_ARG, "n_blocks < 0");
+    *out = nullptr;
+    hsf_plan_opts o;
+    hsf_plan_opts_default(&o);
+    if (opts) o = *opts;
+    if (o.tile_qubits == 0) o.tile_qubits = 12;
+    if (o.tile_qubits < 6 || o.tile_qubits > 13) fail(HSF_ERR_INVALID_ARG, "tile_qubits must be in [6,13]");
+    if (o.dtype != HSF_C64 && o.dtype != HSF_C128) fail(HSF_ERR_INVALID_ARG, "bad dtype");
+    if (!(o.svd_rel_tol >= 0 && o.svd_rel_tol < 1)) fail(HSF_ERR_INVALID_ARG, "bad svd_rel_tol");
+    if (o.max_dense_block_qubits < 1 || o.max_dense_block_qubits > 12) fail(HSF_ERR_INVALID_ARG, "bad max_dense_block_qubits");
+    *out = reinterpret_cast<hsf_plan_t*>(build_plan(text, len, n_low, n_blocks, off, ids, o));
+  })
+}
+
+hsf_status hsf_plan_info_get(const hsf_plan_t* plan, hsf_plan_info* info) {
+  ABI_GUARD({
+    if (!plan || !info) fail(HSF_ERR_INVALID_ARG, "NULL argument");
+    const Plan* P = reinterpret_cast<const Plan*>(plan);
+    info->n_qubits = P->n;
+    info->n_a = P->n - P->n_low;
+    info->n_b = P->n_low;
+    info->n_units = (int32_t)P->units.size();
+    info->n_paths = P->n_paths;
+    info->log2_n_paths_individual = P->log2_individual;
+    info->ranks = P->ranks.data();
+    info->support_a = P->sa.data();
+    info->support_b = P->sb.data();
+    info->sigma_offsets = P->sigma_off.data();
+    info->sigmas = P->sigmas.data();
+    info->levels_a = (int32_t)P->half[0].materialized.size();
+    info->levels_b = (int32_t)P->half[1].materialized.size();
+    info->passes_a = P->half[0].n_passes;
+    info->passes_b = P->half[1].n_passes;
+    info->ops_a = (int32_t)P->half[0].ops.size();
+    info->ops_b = (int32_t)P->half[1].ops.size();
+    info->plan_hash = P->hash;
+  })
+}
+
+hsf_status hsf_run(hsf_plan_t* plan, const hsf_run_args* args) {
+  ABI_GUARD({
+    if (!plan || !args) fail(HSF_ERR_INVALID_ARG, "NULL argument");
+    run(reinterpret_cast<Plan*>(plan), *args);
+  })
+}
+
+size_t hsf_workspace_bytes(const hsf_plan_t* plan, const hsf_run_args* args) {
+  try {
+    if (!plan || !args) return 0;
+    const Plan* P = reinterpret_cast<const Plan*>(plan);
+    return make_layout(*P, *args, P->opts.dtype == HSF_C64 ? 8 : 16).total;
+  } catch (const Error& e) {
+    set_last_error(e.msg);
+    return 0;
+  }
+}
+
+void hsf_plan_free(hsf_plan_t* plan) {
+  if (!plan) return;
+  Plan* P = reinterpret_cast<Plan*>(plan);
+  try {
+    destroy_device(P);
+  } catch (...) {
+  }
+  delete P;
+}
+
+const char* hsf_status_str(hsf_status s) {
+  switch (s) {
+    case HSF_OK: return "HSF_OK";
+    case HSF_ERR_INVALID_ARG: return "HSF_ERR_INVALID_ARG";
+    case HSF_ERR_PARSE: return "HSF_ERR_PARSE";
+    case HSF_ERR_UNSUPPORTED_GATE: return "HSF_ERR_UNSUPPORTED_GATE";
+    case HSF_ERR_DUPLICATE_QUBIT: return "HSF_ERR_DUPLICATE_QUBIT";
+    case HSF_ERR_NONCONVEX_BLOCK: return "HSF_ERR_NONCONVEX_BLOCK";
+    case HSF_ERR_BLOCK_TOO_LARGE: return "HSF_ERR_BLOCK_TOO_LARGE";
+    case HSF_ERR_SVD_NO_CONVERGENCE: return "HSF_ERR_SVD_NO_CONVERGENCE";
+    case HSF_ERR_PATH_BUDGET: return "HSF_ERR_PATH_BUDGET";
+    case HSF_ERR_OUT_OF_MEMORY: return "HSF_ERR_OUT_OF_MEMORY";
+    case HSF_ERR_CUDA: return "HSF_ERR_CUDA";
+    case HSF_ERR_UNSUPPORTED: return "HSF_ERR_UNSUPPORTED";
+  }
+  return "HSF_ERR_UNKNOWN";
+}
+
+size_t hsf_last_error(char* buf, size_t len) {
+  const std::string& m = g_last_error;
+  if (buf && len) {
+    size_t n = std::min(len - 1, m.size());
+    std::memcpy(buf, m.data(), n);
+    buf[n] = 0;
+  }
+  return m.size();
+}
+
+const char* hsf_version(void) { return "libhsf 0.1 sm_100a (tcgen05 bf16x3 path-sum, SMEM/tile-pass simulator)"; }
+
+}  // extern "C"

@@ -1,0 +1,245 @@
+// sim_kernels.cuh — batched half-state simulator (K1 SMEM-resident tier and
+// K2 HBM/L2-streamed tile-pass tier in one kernel).
+//
+// One CTA owns one (path-tree node, tile) pair: it loads 2^t amplitudes of
+// that node's half-state into shared memory, applies every op of the pass
+// (fixed local gates and the node's Schmidt factors X_{u,d}/Y_{u,d})
+// and writes the tile back.  t == m is the SMEM-resident tier (whole half-state
+// on chip, one pass per tree level).  t < m is the streamed tier: tile qubits T
+// always include qubits 0..4 so every global access is a 256 B (c64) row;
+// diagonal ops are applied to any qubit (their non-tile bits are fixed per
+// tile); dense ops only touch tile qubits (the host pass planner guarantees it).
+//
+// Thread mapping: element e of the tile is owned by thread e % blockDim for
+// load, diagonal sweeps and store, so only dense ops need __syncthreads().
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "hsf_internal.h"
+
+namespace hsf {
+
+template <typename R>
+struct cplx;
+template <>
+struct cplx<float> {
+  using T = float2;
+};
+template <>
+struct cplx<double> {
+  using T = double2;
+};
+
+template <typename C>
+__device__ __forceinline__ C cmul(C a, C b) {
+  C r;
+  r.x = a.x * b.x - a.y * b.y;
+  r.y = a.x * b.y + a.y * b.x;
+  return r;
+}
+template <typename C>
+__device__ __forceinline__ C cfma(C a, C b, C acc) {  // acc + a*b
+  acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
+  acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
+  return acc;
+}
+
+constexpr int kSimThreads = 256;
+constexpr int kMaxNonTile = 56;
+
+struct PassParams {
+  const void* src;         // parent level buffer, nullptr => |0...0>
+  void* dst;               // output level buffer (node-major [nodes][2^m])
+  const DevOp* ops;
+  const void* coef;        // complex table in the run dtype
+  int n_ops;
+  int m, t;
+  int n_hi;                // t - 5 when t < m
+  int T_hi[8];             // half qubits at tile positions 5..t-1
+  int n_nt;                // m - t
+  int nonT[kMaxNonTile];   // half qubits outside the tile, ascending
+  long long state_elems;   // 2^m
+  long long node_first;    // global index (at the output level) of blockIdx.y == 0
+  long long node_local0;   // local output-node index of blockIdx.y == 0
+  long long src_first;     // global index of the first node of the input level
+  long long src_div;       // parent = node_global / src_div
+};
+
+template <int K, typename C>
+__device__ __forceinline__ void apply_dense_k(C* s, int t, const DevOp& op, const C* __restrict__ M) {
+  constexpr int D = 1 << K;
+  int ps[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) ps[j] = op.q[j];
+  // sort positions ascending for zero-bit insertion
+#pragma unroll
+  for (int a = 0; a < K; ++a)
+#pragma unroll
+    for (int b = a + 1; b < K; ++b)
+      if (ps[b] < ps[a]) {
+        int tmp = ps[a];
+        ps[a] = ps[b];
+        ps[b] = tmp;
+      }
+  int off[D];
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    int o = 0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) o |= ((i >> j) & 1) << op.q[j];
+    off[i] = o;
+  }
+  const int ngroups = 1 << (t - K);
+  if (K <= 2) {
+    C mat[D * D];
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) mat[i] = M[i];
+    for (int g = threadIdx.x; g < ngroups; g += blockDim.x) {
+      int b = g;
+#pragma unroll
+      for (int j = 0; j < K; ++j) b = ((b >> ps[j]) << (ps[j] + 1)) | (b & ((1 << ps[j]) - 1));
+      C v[D];
+#pragma unroll
+      for (int i = 0; i < D; ++i) v[i] = s[b + off[i]];
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        C acc;
+        acc.x = 0;
+        acc.y = 0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) acc = cfma(mat[i * D + j], v[j], acc);
+        s[b + off[i]] = acc;
+      }
+    }
+  } else {
+    for (int g = threadIdx.x; g < ngroups; g += blockDim.x) {
+      int b = g;
+#pragma unroll
+      for (int j = 0; j < K; ++j) b = ((b >> ps[j]) << (ps[j] + 1)) | (b & ((1 << ps[j]) - 1));
+      C v[D];
+#pragma unroll
+      for (int i = 0; i < D; ++i) v[i] = s[b + off[i]];
+#pragma unroll 1
+      for (int i = 0; i < D; ++i) {
+        C acc;
+        acc.x = 0;
+        acc.y = 0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) acc = cfma(__ldg(&M[i * D + j]), v[j], acc);
+        int o = 0;
+        for (int j = 0; j < K; ++j) o |= ((i >> j) & 1) << op.q[j];
+        s[b + o] = acc;
+      }
+    }
+  }
+}
+
+template <typename C>
+__device__ __forceinline__ void apply_dense(C* s, int t, const DevOp& op, const C* M) {
+  switch (op.k) {
+    case 1: apply_dense_k<1>(s, t, op, M); break;
+    case 2: apply_dense_k<2>(s, t, op, M); break;
+    case 3: apply_dense_k<3>(s, t, op, M); break;
+    case 4: apply_dense_k<4>(s, t, op, M); break;
+    case 5: apply_dense_k<5>(s, t, op, M); break;
+    default: break;
+  }
+}
+
+__device__ __forceinline__ long long diag_index(const DevOp& op, long long g) {
+  if (op.contiguous) return (g >> op.q[0]) & ((1ll << op.k) - 1);
+  long long idx = 0;
+  for (int j = 0; j < op.k; ++j) idx |= ((g >> op.q[j]) & 1ll) << j;
+  return idx;
+}
+
+template <typename R>
+__global__ void __launch_bounds__(kSimThreads, 2) hsf_pass_kernel(const PassParams p) {
+  using C = typename cplx<R>::T;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* s = reinterpret_cast<C*>(smem_raw);
+  long long* hi_off = reinterpret_cast<long long*>(smem_raw + (sizeof(C) << p.t));
+  __shared__ DevOp sops[32];
+
+  const long long tile = blockIdx.x;
+  const long long node_local = p.node_local0 + blockIdx.y;
+  const long long node_g = p.node_first + blockIdx.y;
+  const int nel = 1 << p.t;
+  const bool whole = (p.t == p.m);
+
+  long long base = 0;
+  if (!whole) {
+    for (int j = 0; j < p.n_nt; ++j) base |= ((tile >> j) & 1ll) << p.nonT[j];
+    const int nh = 1 << p.n_hi;
+    for (int j = threadIdx.x; j < nh; j += blockDim.x) {
+      long long o = 0;
+      for (int b = 0; b < p.n_hi; ++b) o |= (long long)((j >> b) & 1) << p.T_hi[b];
+      hi_off[j] = o;
+    }
+    __syncthreads();
+  }
+  auto gidx_of = [&](int e) -> long long { return whole ? (long long)e : (base | (e & 31) | hi_off[e >> 5]); };
+
+  const C* src = nullptr;
+  if (p.src) {
+    long long parent = node_g / p.src_div - p.src_first;
+    src = reinterpret_cast<const C*>(p.src) + parent * p.state_elems;
+  }
+  C* dst = reinterpret_cast<C*>(p.dst) + node_local * p.state_elems;
+  const C* coef = reinterpret_cast<const C*>(p.coef);
+
+  // load (the first output pass reads the parent; later passes are in place)
+  for (int e = threadIdx.x; e < nel; e += blockDim.x) {
+    long long g = gidx_of(e);
+    C v;
+    if (src) {
+      v = src[g];
+    } else {
+      v.x = (g == 0) ? R(1) : R(0);
+      v.y = R(0);
+    }
+    s[e] = v;
+  }
+
+  bool need_sync = true;  // dense ops use a different thread mapping than loads
+  for (int ob = 0; ob < p.n_ops; ob += 32) {
+    const int cnt = min(32, p.n_ops - ob);
+    __syncthreads();  // previous chunk done with sops
+    if (threadIdx.x < cnt) sops[threadIdx.x] = p.ops[ob + threadIdx.x];
+    __syncthreads();
+    need_sync = false;
+    int i = 0;
+    while (i < cnt) {
+      const DevOp& op = sops[i];
+      if (op.kind == OP_DENSE) {
+        if (need_sync) __syncthreads();
+        long long digit = (op.radix > 1) ? (node_g / op.div) % op.radix : 0;
+        apply_dense<C>(s, p.t, op, coef + op.table + digit * op.stride);
+        __syncthreads();
+        need_sync = false;
+        ++i;
+      } else {
+        // a run of diagonal ops in one sweep (element-owner mapping)
+        int j = i;
+        while (j < cnt && sops[j].kind == OP_DIAG) ++j;
+        for (int e = threadIdx.x; e < nel; e += blockDim.x) {
+          long long g = gidx_of(e);
+          C v = s[e];
+          for (int r = i; r < j; ++r) {
+            const DevOp& d = sops[r];
+            long long digit = (d.radix > 1) ? (node_g / d.div) % d.radix : 0;
+            v = cmul(v, coef[d.table + digit * d.stride + diag_index(d, g)]);
+          }
+          s[e] = v;
+        }
+        need_sync = true;
+        i = j;
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nel; e += blockDim.x) dst[gidx_of(e)] = s[e];
+}
+
+}  // namespace hsf

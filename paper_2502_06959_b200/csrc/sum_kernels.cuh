@@ -1,0 +1,172 @@
+// sum_kernels.cuh — Kronecker path-sum kernels:
+//   psi[i_A * 2^nB + i_B] = sum_p c_p Psi_A[i_A, p] Psi_B[i_B, p]
+//
+//   K4t  transpose_fold : node-major leaves [K][2^m] -> row-major [2^m][K],
+//                         optionally folding c_p (a3)
+//   K6   gather_dot     : bitstring amplitudes (one warp per sample, two
+//                         contiguous K-rows, warp-shuffle reduction)
+//   K5s  simt_gemm      : full output on CUDA cores (fp32 / fp64 FMA),
+//                         reading the node-major leaves directly
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sim_kernels.cuh"
+
+namespace hsf {
+
+// ------------------------------------------------------------------ K4t
+template <typename C>
+__global__ void transpose_fold_kernel(const C* __restrict__ in, C* __restrict__ out, const C* __restrict__ cp,
+                                      long long K, long long M) {
+  __shared__ C tile[32][33];
+  const long long m0 = (long long)blockIdx.x * 32, k0 = (long long)blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int r = ty; r < 32; r += 8) {
+    long long k = k0 + r, m = m0 + tx;
+    C v;
+    v.x = 0;
+    v.y = 0;
+    if (k < K && m < M) {
+      v = in[k * M + m];
+      if (cp) v = cmul(v, cp[k]);
+    }
+    tile[r][tx] = v;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    long long m = m0 + r, k = k0 + tx;
+    if (k < K && m < M) out[m * K + k] = tile[tx][r];
+  }
+}
+
+// ------------------------------------------------------------------- K6
+// amp[s] = sum_p AT[s >> nB][p] * BT[s & maskB][p]   (AT already holds c_p)
+template <typename C>
+__global__ void gather_dot_kernel(const C* __restrict__ AT, const C* __restrict__ BT,
+                                  const unsigned long long* __restrict__ bits, C* __restrict__ out,
+                                  long long n_samples, long long K, int n_low) {
+  const int lane = threadIdx.x & 31;
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const unsigned long long maskB = (1ull << n_low) - 1ull;
+  for (long long s = warp; s < n_samples; s += nwarps) {
+    unsigned long long b = bits[s];
+    const C* a = AT + (long long)(b >> n_low) * K;
+    const C* bb = BT + (long long)(b & maskB) * K;
+    C acc;
+    acc.x = 0;
+    acc.y = 0;
+    for (long long p = lane; p < K; p += 32) acc = cfma(__ldg(&a[p]), __ldg(&bb[p]), acc);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    }
+    if (lane == 0) out[s] = acc;
+  }
+}
+
+// Specialisation for K % 64 == 0 with complex64: 16 B loads, 2 complex per lane
+// per step, 4 steps in flight.
+__global__ void gather_dot_c64_vec_kernel(const float4* __restrict__ AT, const float4* __restrict__ BT,
+                                          const unsigned long long* __restrict__ bits, float2* __restrict__ out,
+                                          long long n_samples, long long K, int n_low) {
+  const int lane = threadIdx.x & 31;
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const unsigned long long maskB = (1ull << n_low) - 1ull;
+  const long long K2 = K >> 1;  // float4 per row
+  for (long long s = warp; s < n_samples; s += nwarps) {
+    unsigned long long b = bits[s];
+    const float4* a = AT + (long long)(b >> n_low) * K2;
+    const float4* bb = BT + (long long)(b & maskB) * K2;
+    float re = 0.f, im = 0.f;
+    for (long long p = lane; p < K2; p += 32) {
+      float4 x = __ldg(&a[p]);
+      float4 y = __ldg(&bb[p]);
+      re = fmaf(x.x, y.x, fmaf(-x.y, y.y, re));
+      im = fmaf(x.x, y.y, fmaf(x.y, y.x, im));
+      re = fmaf(x.z, y.z, fmaf(-x.w, y.w, re));
+      im = fmaf(x.z, y.w, fmaf(x.w, y.z, im));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      re += __shfl_xor_sync(0xffffffffu, re, o);
+      im += __shfl_xor_sync(0xffffffffu, im, o);
+    }
+    if (lane == 0) out[s] = make_float2(re, im);
+  }
+}
+
+// ------------------------------------------------------------------ K5s
+// out[(i - row0) * MB + j] = sum_p c_p A[p][i] B[p][j]  for i in [row0, row0+rows)
+// A: [K][MA] node-major leaves, B: [K][MB].  64x64 output tile per CTA,
+// 256 threads x (4x4) outputs, K staged in chunks of 16 through SMEM.
+template <typename C, typename R>
+__global__ void __launch_bounds__(256) simt_gemm_kernel(const C* __restrict__ A, const C* __restrict__ B,
+                                                        const C* __restrict__ cp, C* __restrict__ out,
+                                                        long long K, long long MA, long long MB, long long row0,
+                                                        long long rows) {
+  constexpr int BM = 64, BN = 64, BK = 16;
+  __shared__ C As[BK][BM];
+  __shared__ C Bs[BK][BN];
+  const int tid = threadIdx.x;
+  const int tr = tid / 16, tc = tid % 16;  // 16 x 16 threads, each 4 x 4
+  const long long i0 = row0 + (long long)blockIdx.y * BM;
+  const long long j0 = (long long)blockIdx.x * BN;
+  C acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      acc[a][b].x = 0;
+      acc[a][b].y = 0;
+    }
+  for (long long k0 = 0; k0 < K; k0 += BK) {
+    for (int e = tid; e < BK * BM; e += 256) {
+      int kk = e / BM, ii = e % BM;
+      long long k = k0 + kk, i = i0 + ii;
+      C v;
+      v.x = 0;
+      v.y = 0;
+      if (k < K && i < row0 + rows && i < MA) v = cmul(A[k * MA + i], cp[k]);
+      As[kk][ii] = v;
+    }
+    for (int e = tid; e < BK * BN; e += 256) {
+      int kk = e / BN, jj = e % BN;
+      long long k = k0 + kk, j = j0 + jj;
+      C v;
+      v.x = 0;
+      v.y = 0;
+      if (k < K && j < MB) v = B[k * MB + j];
+      Bs[kk][jj] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      C a[4], b[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) a[x] = As[kk][tr + 16 * x];
+#pragma unroll
+      for (int y = 0; y < 4; ++y) b[y] = Bs[kk][tc + 16 * y];
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[x][y] = cfma(a[x], b[y], acc[x][y]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    long long i = i0 + tr + 16 * x;
+    if (i >= row0 + rows || i >= MA) continue;
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      long long j = j0 + tc + 16 * y;
+      if (j < MB) out[(i - row0) * MB + j] = acc[x][y];
+    }
+  }
+}
+
+}  // namespace hsf

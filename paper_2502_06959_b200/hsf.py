@@ -1,0 +1,206 @@
+"""Thin ctypes binding of libhsf.so (include/hsf.h).  Argument marshalling only:
+every step of the HSF path runs in the library's CUDA kernels.  There is no
+CPU fallback: if the library or a GPU is missing, calls raise.
+
+PyTorch is used only for device memory and streams (``torch.Tensor`` data
+pointers, ``torch.cuda.current_stream()``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libhsf.so")
+
+HSF_C64, HSF_C128 = 0, 1
+PREC = {"auto": 0, "simt": 1, "bf16x3": 2, "bf16x1": 3}
+STATUS = {}
+
+
+class HsfError(RuntimeError):
+    def __init__(self, status: int, name: str, msg: str):
+        super().__init__(f"{name}: {msg}")
+        self.status = status
+        self.name = name
+
+
+class _Opts(C.Structure):
+    _fields_ = [("dtype", C.c_int), ("svd_rel_tol", C.c_double), ("max_dense_block_qubits", C.c_int32),
+                ("log2_path_budget", C.c_double), ("individual", C.c_int32), ("tile_qubits", C.c_int32),
+                ("fuse_gates", C.c_int32)]
+
+
+class _Info(C.Structure):
+    _fields_ = [("n_qubits", C.c_int32), ("n_a", C.c_int32), ("n_b", C.c_int32), ("n_units", C.c_int32),
+                ("n_paths", C.c_uint64), ("log2_n_paths_individual", C.c_double),
+                ("ranks", C.POINTER(C.c_int32)), ("support_a", C.POINTER(C.c_int32)),
+                ("support_b", C.POINTER(C.c_int32)), ("sigma_offsets", C.POINTER(C.c_int64)),
+                ("sigmas", C.POINTER(C.c_double)), ("levels_a", C.c_int32), ("levels_b", C.c_int32),
+                ("passes_a", C.c_int32), ("passes_b", C.c_int32), ("ops_a", C.c_int32), ("ops_b", C.c_int32),
+                ("plan_hash", C.c_uint64)]
+
+
+class _RunArgs(C.Structure):
+    _fields_ = [("bitstrings", C.c_void_p), ("n_bitstrings", C.c_uint64), ("bits_on_device", C.c_int32),
+                ("out", C.c_void_p), ("out_on_device", C.c_int32), ("path_begin", C.c_uint64),
+                ("path_end", C.c_uint64), ("row_begin", C.c_uint64), ("row_end", C.c_uint64),
+                ("cuda_stream", C.c_void_p), ("precision", C.c_int), ("device", C.c_int32),
+                ("phase_ms", C.POINTER(C.c_double))]
+
+
+_lib = None
+
+EXPORTS = ["hsf_plan_opts_default", "hsf_plan", "hsf_plan_info_get", "hsf_run", "hsf_workspace_bytes",
+           "hsf_plan_free", "hsf_status_str", "hsf_last_error", "hsf_version"]
+
+
+def lib():
+    """Load libhsf.so (built in-tree by paper_2502_06959_b200/build.py)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"libhsf.so not built ({LIB_PATH}); run `python -m paper_2502_06959_b200.build`")
+    L = C.CDLL(LIB_PATH)
+    L.hsf_plan_opts_default.argtypes = [C.POINTER(_Opts)]
+    L.hsf_plan.argtypes = [C.c_char_p, C.c_size_t, C.c_int32, C.c_int64, C.POINTER(C.c_int64),
+                           C.POINTER(C.c_int64), C.POINTER(_Opts), C.POINTER(C.c_void_p)]
+    L.hsf_plan_info_get.argtypes = [C.c_void_p, C.POINTER(_Info)]
+    L.hsf_run.argtypes = [C.c_void_p, C.POINTER(_RunArgs)]
+    L.hsf_workspace_bytes.argtypes = [C.c_void_p, C.POINTER(_RunArgs)]
+    L.hsf_workspace_bytes.restype = C.c_size_t
+    L.hsf_plan_free.argtypes = [C.c_void_p]
+    L.hsf_plan_free.restype = None
+    L.hsf_status_str.argtypes = [C.c_int]
+    L.hsf_status_str.restype = C.c_char_p
+    L.hsf_last_error.argtypes = [C.c_char_p, C.c_size_t]
+    L.hsf_last_error.restype = C.c_size_t
+    L.hsf_version.restype = C.c_char_p
+    for f in ("hsf_plan_opts_default", "hsf_plan", "hsf_plan_info_get", "hsf_run"):
+        getattr(L, f).restype = C.c_int
+    _lib = L
+    return L
+
+
+def _check(st: int):
+    if st != 0:
+        L = lib()
+        buf = C.create_string_buffer(4096)
+        L.hsf_last_error(buf, 4096)
+        raise HsfError(st, L.hsf_status_str(st).decode(), buf.value.decode(errors="replace"))
+
+
+def version() -> str:
+    return lib().hsf_version().decode()
+
+
+class Plan:
+    """hsf_plan(): host-side joint-cut plan.  `blocks` is a list of
+    gate-index lists; `individual=True` cuts every crossing gate alone."""
+
+    def __init__(self, circuit_text: str, n_low: int, blocks=None, dtype: str = "c64", individual: bool = False,
+                 svd_rel_tol: float = 1e-12, tile_qubits: int = 12, fuse_gates: bool = True,
+                 log2_path_budget: float = 26.0, max_dense_block_qubits: int = 10):
+        L = lib()
+        o = _Opts()
+        _check(L.hsf_plan_opts_default(C.byref(o)))
+        o.dtype = HSF_C64 if dtype == "c64" else HSF_C128
+        o.svd_rel_tol = svd_rel_tol
+        o.individual = int(individual)
+        o.tile_qubits = tile_qubits
+        o.fuse_gates = int(fuse_gates)
+        o.log2_path_budget = log2_path_budget
+        o.max_dense_block_qubits = max_dense_block_qubits
+        blocks = blocks or []
+        offs = np.zeros(len(blocks) + 1, dtype=np.int64)
+        for i, b in enumerate(blocks):
+            offs[i + 1] = offs[i] + len(b)
+        ids = np.array([g for b in blocks for g in b] or [0], dtype=np.int64)
+        txt = circuit_text.encode()
+        h = C.c_void_p()
+        _check(L.hsf_plan(txt, len(txt), n_low, len(blocks), offs.ctypes.data_as(C.POINTER(C.c_int64)),
+                          ids.ctypes.data_as(C.POINTER(C.c_int64)), C.byref(o), C.byref(h)))
+        self._h = h
+        self.dtype = dtype
+        self._info = _Info()
+        _check(L.hsf_plan_info_get(self._h, C.byref(self._info)))
+        i = self._info
+        self.n, self.n_a, self.n_b = i.n_qubits, i.n_a, i.n_b
+        self.n_paths = int(i.n_paths)
+        self.ranks = [i.ranks[u] for u in range(i.n_units)]
+        self.log2_n_paths_individual = i.log2_n_paths_individual
+        self.sigmas = [[i.sigmas[j] for j in range(i.sigma_offsets[u], i.sigma_offsets[u + 1])]
+                       for u in range(i.n_units)]
+        self.support = [(i.support_a[u], i.support_b[u]) for u in range(i.n_units)]
+        self.levels = (i.levels_a, i.levels_b)
+        self.passes = (i.passes_a, i.passes_b)
+        self.ops = (i.ops_a, i.ops_b)
+        self.plan_hash = int(i.plan_hash)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.hsf_plan_free(h)
+            self._h = None
+
+    # -------------------------------------------------------------- run
+    def _args(self, out_ptr, out_dev, bits_ptr, n_bits, bits_dev, path_range, row_range, precision, stream, device,
+              phase):
+        a = _RunArgs()
+        a.bitstrings = bits_ptr
+        a.n_bitstrings = n_bits
+        a.bits_on_device = int(bits_dev)
+        a.out = out_ptr
+        a.out_on_device = int(out_dev)
+        a.path_begin, a.path_end = path_range if path_range else (0, 0)
+        a.row_begin, a.row_end = row_range if row_range else (0, 0)
+        a.cuda_stream = stream
+        a.precision = PREC[precision]
+        a.device = device
+        a.phase_ms = phase
+        return a
+
+    def run(self, out, bitstrings=None, path_range=None, row_range=None, precision: str = "auto", stream=None,
+            timings: bool = False):
+        """hsf_run(): evaluate paths [path_range) into `out`.
+
+        `out` / `bitstrings` are torch tensors (device or host) or numpy arrays
+        (host).  Returns per-phase ms [simA, simB, sum, total] if `timings`."""
+        import torch
+
+        def ptr(x):
+            if isinstance(x, torch.Tensor):
+                if not x.is_contiguous():
+                    raise ValueError("tensor must be contiguous")
+                return x.data_ptr(), x.is_cuda, x.numel()
+            x = np.ascontiguousarray(x)
+            return x.ctypes.data, False, x.size
+
+        op, odev, _ = ptr(out)
+        bp, bdev, nb = (None, False, 0) if bitstrings is None else ptr(bitstrings)
+        dev = torch.cuda.current_device() if torch.cuda.is_available() else -1
+        st = stream if stream is not None else (torch.cuda.current_stream().cuda_stream if torch.cuda.is_available() else None)
+        phase = (C.c_double * 4)() if timings else None
+        a = self._args(op, odev, bp, nb, bdev, path_range, row_range, precision, st, dev,
+                       C.cast(phase, C.POINTER(C.c_double)) if timings else None)
+        _check(lib().hsf_run(self._h, C.byref(a)))
+        return list(phase) if timings else None
+
+    def workspace_bytes(self, bitstrings_count: int = 0, path_range=None, row_range=None, precision="auto") -> int:
+        a = self._args(1, True, 1 if bitstrings_count else None, bitstrings_count, True, path_range, row_range,
+                       precision, None, -1, None)
+        return int(lib().hsf_workspace_bytes(self._h, C.byref(a)))
+
+
+def path_range_for_rank(n_paths: int, rank: int, world: int):
+    """Contiguous path range of one rank (whole subtrees when world divides the
+    leading radices)."""
+    return (n_paths * rank // world, n_paths * (rank + 1) // world)
+
+
+def row_range_for_rank(n_a: int, rank: int, world: int):
+    rows = 1 << n_a
+    return (rows * rank // world, rows * (rank + 1) // world)

@@ -1,0 +1,149 @@
+"""CPU tests of libhsf.so: the library loads and exports every symbol of
+include/hsf.h, and the host planner (hsf_plan: C++ parser, convex schedule,
+block assembly, Jacobi SVD, path counts) agrees with what the paper and the
+oracle fix.  No GPU compute is called here."""
+import ctypes
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+from hsf_inputs import make_config, random_small_circuit
+from hsf_inputs.circuits import make_sbm_qaoa
+from oracle import hsf_oracle as O
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def hsf():
+    from paper_2502_06959_b200 import build, hsf as H
+    build.build()
+    return H
+
+
+def test_header_symbols_exported(hsf):
+    hdr = open(os.path.join(ROOT, "include", "hsf.h")).read()
+    names = set(re.findall(r"^\w[\w\s\*]*?\b(hsf_\w+)\s*\(", hdr, re.M))
+    assert {"hsf_plan", "hsf_run", "hsf_plan_free", "hsf_plan_info_get"} <= names
+    lib = ctypes.CDLL(hsf.LIB_PATH)
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(hsf.EXPORTS) == names
+
+
+def test_version_and_status_strings(hsf):
+    assert "sm_100a" in hsf.version()
+    L = hsf.lib()
+    assert L.hsf_status_str(0) == b"HSF_OK"
+    assert L.hsf_status_str(5) == b"HSF_ERR_NONCONVEX_BLOCK"
+
+
+def _sig(inst, **kw):
+    from paper_2502_06959_b200 import Plan
+    return Plan(inst.text, inst.n_low, inst.blocks, dtype=inst.dtype, **kw)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_path_counts_and_sigmas_full_configs(hsf, name):
+    inst = make_config(name, n_bits=0) if name in ("c3", "c5") else make_config(name)
+    P = _sig(inst)
+    n, g = O.parse_circuit(inst.text)
+    Po = O.plan(n, g, inst.n_low, inst.blocks)
+    expect = {"c1": 16, "c2": 4096, "c3": 256, "c4": 64, "c5": 256}[name]
+    assert P.n_paths == Po.n_paths == expect
+    assert P.ranks == Po.radices
+    for s_cpp, u in zip(P.sigmas, Po.units):
+        assert np.allclose(s_cpp, u.sigmas, rtol=1e-12, atol=1e-12 * u.sigmas[0])
+    expect_t = {"c1": 12, "c2": 144, "c3": 8, "c4": 6, "c5": 48}[name]
+    assert abs(P.log2_n_paths_individual - expect_t) < 1e-9
+
+
+@pytest.mark.parametrize("seed", range(25))
+def test_sigmas_random_blocks_match_lapack(hsf, seed):
+    inst = random_small_circuit(seed, max_block_qubits=6)
+    n, g = O.parse_circuit(inst.text)
+    Po = O.plan(n, g, inst.n_low, inst.blocks)
+    P = _sig(inst)
+    assert P.ranks == Po.radices
+    for s_cpp, u in zip(P.sigmas, Po.units):
+        assert np.allclose(s_cpp, u.sigmas, rtol=1e-11, atol=1e-12 * u.sigmas[0])
+    Pi = _sig(inst, individual=True)
+    Poi = O.plan(n, g, inst.n_low, None, "individual")
+    assert Pi.ranks == Poi.radices
+
+
+def test_paper_examples_ranks(hsf):
+    from paper_2502_06959_b200 import Plan
+    # Example 2: CNOT rank 2; SWAP rank 4; Eq. 11 cascade rank 2
+    assert Plan("qubits 2\ncx 1 0\n", 1, [[0]]).ranks == [2]
+    assert Plan("qubits 2\nswap 1 0\n", 1, [[0]]).ranks == [4]
+    P = Plan("qubits 4\ncx 3 2\ncx 3 1\ncx 3 0\n", 3, [[0, 1, 2]])
+    assert P.ranks == [2]
+    assert abs(P.log2_n_paths_individual - 3) < 1e-12
+    # RZZ(t): sigma = (2|cos t/2|, 2|sin t/2|)
+    t = 0.7
+    P = Plan(f"qubits 2\nrzz {t.hex()} 1 0\n", 1, [[0]])
+    assert np.allclose(P.sigmas[0], [2 * math.cos(t / 2), 2 * math.sin(t / 2)], atol=1e-14)
+
+
+def test_table2_like_counts(hsf):
+    from paper_2502_06959_b200 import Plan
+    inst = make_sbm_qaoa(seed=30, sizes=(15, 15), p_inter=0.1)
+    P = Plan(inst.text, inst.n_low, inst.blocks)
+    n, g = O.parse_circuit(inst.text)
+    Po = O.plan(n, g, inst.n_low, inst.blocks)
+    assert P.n_paths == Po.n_paths
+    assert all(r == 2 for r in P.ranks)
+
+
+@pytest.mark.parametrize("text,n_low,blocks,status", [
+    ("qubits 3\ncx 2 0\nh 0\ncx 2 1\ncx 0 1\n", 1, [[0, 3]], "HSF_ERR_NONCONVEX_BLOCK"),
+    ("qubits 2\nfoo 0\n", 1, None, "HSF_ERR_UNSUPPORTED_GATE"),
+    ("qubits 2\ncx 0 0\n", 1, None, "HSF_ERR_DUPLICATE_QUBIT"),
+    ("qubits 2\ncx 0 2\n", 1, None, "HSF_ERR_DUPLICATE_QUBIT"),
+    ("h 0\n", 1, None, "HSF_ERR_PARSE"),
+    ("qubits 2\nrx zz 0\n", 1, None, "HSF_ERR_PARSE"),
+    ("qubits 2\nh 0\n", 0, None, "HSF_ERR_INVALID_ARG"),
+    ("qubits 2\nh 0\n", 2, None, "HSF_ERR_INVALID_ARG"),
+])
+def test_errors(hsf, text, n_low, blocks, status):
+    from paper_2502_06959_b200 import Plan, HsfError
+    with pytest.raises(HsfError) as ei:
+        Plan(text, n_low, blocks)
+    assert ei.value.name == status
+
+
+def test_path_budget(hsf):
+    from paper_2502_06959_b200 import HsfError, Plan
+    inst = make_config("c5", n_bits=0)
+    with pytest.raises(HsfError) as ei:
+        Plan(inst.text, inst.n_low, None, individual=True)  # 2^48 > 2^26
+    assert ei.value.name == "HSF_ERR_PATH_BUDGET"
+
+
+def test_dense_block_too_large(hsf):
+    from paper_2502_06959_b200 import HsfError, Plan
+    inst = make_config("c3", n_bits=0)
+    with pytest.raises(HsfError) as ei:
+        Plan(inst.text, inst.n_low, [list(range(0, 200))], max_dense_block_qubits=6)
+    assert ei.value.name in ("HSF_ERR_BLOCK_TOO_LARGE", "HSF_ERR_NONCONVEX_BLOCK")
+
+
+def test_plan_hash_deterministic(hsf):
+    from paper_2502_06959_b200 import Plan
+    inst = make_config("c4")
+    assert Plan(inst.text, inst.n_low, inst.blocks).plan_hash == Plan(inst.text, inst.n_low, inst.blocks).plan_hash
+    inst2 = make_config("c4", seed=99)
+    assert Plan(inst.text, inst.n_low, inst.blocks).plan_hash != Plan(inst2.text, inst2.n_low, inst2.blocks).plan_hash
+
+
+def test_workspace_bytes_no_gpu(hsf):
+    from paper_2502_06959_b200 import Plan
+    inst = make_config("c5", n_bits=0)
+    P = Plan(inst.text, inst.n_low, inst.blocks)
+    b = P.workspace_bytes(bitstrings_count=1 << 22)
+    # leaves + transposed copies of both halves (256 x 2^20 complex64 each) dominate
+    assert b >= 4 * 256 * (1 << 20) * 8

@@ -1,0 +1,219 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.  Tolerances (BASELINE.json north_star): max|d amp| <= 1e-5
+for complex64, <= 1e-11 for complex128; relative L2 is reported and bounded
+too."""
+import math
+
+import numpy as np
+import pytest
+
+from hsf_inputs import make_config, random_small_circuit
+from oracle import hsf_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"c64": 1e-5, "c128": 1e-11}
+REL = {"c64": 2e-5, "c128": 1e-12}
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as T
+    from paper_2502_06959_b200 import build
+    build.build()
+    assert T.cuda.is_available()
+    return T
+
+
+def _cdt(torch, dtype):
+    return torch.complex64 if dtype == "c64" else torch.complex128
+
+
+def gpu_full(torch, inst, dtype=None, precision="auto", path_range=None, row_range=None, **kw):
+    from paper_2502_06959_b200 import Plan
+    dtype = dtype or inst.dtype
+    P = Plan(inst.text, inst.n_low, inst.blocks, dtype=dtype, **kw)
+    r0, r1 = row_range or (0, 1 << P.n_a)
+    out = torch.empty((r1 - r0) << P.n_b, dtype=_cdt(torch, dtype), device="cuda")
+    P.run(out, path_range=path_range, row_range=row_range, precision=precision)
+    torch.cuda.synchronize()
+    return out.cpu().numpy(), P
+
+
+def gpu_bits(torch, inst, bits, dtype=None, path_range=None, **kw):
+    from paper_2502_06959_b200 import Plan
+    dtype = dtype or inst.dtype
+    P = Plan(inst.text, inst.n_low, inst.blocks, dtype=dtype, **kw)
+    b = torch.from_numpy(np.asarray(bits, dtype=np.uint64).view(np.int64)).cuda()
+    out = torch.empty(len(bits), dtype=_cdt(torch, dtype), device="cuda")
+    P.run(out, bitstrings=b, path_range=path_range)
+    torch.cuda.synchronize()
+    return out.cpu().numpy(), P
+
+
+def check(got, ref, dtype):
+    d = np.abs(got - ref)
+    rel = np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-300)
+    assert d.max() <= TOL[dtype], (d.max(), rel)
+    assert rel <= REL[dtype], (d.max(), rel)
+    return d.max(), rel
+
+
+# ---------------------------------------------------------------- small
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_twins_full_output(torch, name, dtype):
+    inst = make_config(name, twin=True)
+    n, g = O.parse_circuit(inst.text)
+    ref = O.schrodinger(n, g)
+    got, _ = gpu_full(torch, inst, dtype=dtype, precision="simt")
+    check(got, ref, dtype)
+
+
+@pytest.mark.parametrize("name", ["c3", "c5"])
+def test_twins_bitstrings(torch, name):
+    inst = make_config(name, twin=True)
+    n, g = O.parse_circuit(inst.text)
+    ref = O.schrodinger(n, g)[inst.bitstrings.astype(np.int64)]
+    got, _ = gpu_bits(torch, inst, inst.bitstrings)
+    check(got, ref, "c64")
+
+
+def test_c1_full_size_complex128(torch):
+    inst = make_config("c1")
+    n, g = O.parse_circuit(inst.text)
+    ref = O.schrodinger(n, g)
+    got, P = gpu_full(torch, inst, dtype="c128", precision="simt")
+    assert P.n_paths == 16
+    assert np.abs(got - ref).max() <= 1e-11
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_small_circuits(torch, seed):
+    inst = random_small_circuit(seed, n_gates=8 + seed % 17)
+    n, g = O.parse_circuit(inst.text)
+    if O.plan(n, g, inst.n_low, inst.blocks).n_paths > 4096:
+        inst = random_small_circuit(seed, n_gates=8)
+        n, g = O.parse_circuit(inst.text)
+    ref = O.schrodinger(n, g)
+    for dtype in ("c64", "c128"):
+        got, _ = gpu_full(torch, inst, dtype=dtype, precision="simt")
+        check(got, ref, dtype)
+    got, _ = gpu_full(torch, inst, dtype="c128", precision="simt", individual=True) \
+        if O.plan(n, g, inst.n_low, None, "individual").n_paths <= 4096 else (ref, None)
+    check(got, ref, "c128")
+
+
+@pytest.mark.parametrize("tile", [6, 8, 10])
+def test_tile_passes_forced(torch, tile):
+    # halves above the SMEM-resident limit stream through 2^tile tiles; force
+    # the tiled tier on small halves by lowering tile_qubits below m
+    inst = make_config("c3", twin=True, n=28, n_low=14, depth=8, n_bits=2048)
+    n, g = O.parse_circuit(inst.text)
+    P = O.plan(n, g, inst.n_low, inst.blocks)
+    A, B, c = O.half_states(P, 0, 16)
+    ref = O.recombine_bits(A, B, c, inst.bitstrings, inst.n_low)
+    got, Pg = gpu_bits(torch, inst, inst.bitstrings, path_range=(0, 16), tile_qubits=tile)
+    assert Pg.passes[0] > Pg.levels[0]
+    check(got, ref, "c64")
+
+
+def test_no_crossing_gates(torch):
+    inst = random_small_circuit(3, n=8, n_gates=20)
+    # keep only local gates
+    gates = [x for x in inst.gates if all(q < inst.n_low for q in x[2]) or all(q >= inst.n_low for q in x[2])]
+    from hsf_inputs.circuits import Instance
+    inst2 = Instance("local", inst.n, inst.n_low, gates, [], None, "c128")
+    n, g = O.parse_circuit(inst2.text)
+    got, P = gpu_full(torch, inst2, dtype="c128", precision="simt")
+    assert P.n_paths == 1
+    check(got, O.schrodinger(n, g), "c128")
+
+
+def test_path_range_partition_sums(torch):
+    inst = make_config("c5", twin=True)
+    full, P = gpu_full(torch, inst, precision="simt")
+    tot = 0
+    for r in range(4):
+        p0, p1 = P.n_paths * r // 4, P.n_paths * (r + 1) // 4
+        part, _ = gpu_full(torch, inst, precision="simt", path_range=(p0, p1))
+        tot = tot + part
+    assert np.abs(tot - full).max() < 1e-6
+
+
+def test_row_range(torch):
+    inst = make_config("c4", twin=True)
+    full, P = gpu_full(torch, inst, precision="simt")
+    rows = 1 << P.n_a
+    part, _ = gpu_full(torch, inst, precision="simt", row_range=(rows // 4, rows // 2))
+    assert np.array_equal(part, full[(rows // 4) << P.n_b:(rows // 2) << P.n_b])
+
+
+def test_host_buffers(torch):
+    from paper_2502_06959_b200 import Plan
+    inst = make_config("c5", twin=True)
+    n, g = O.parse_circuit(inst.text)
+    ref = O.schrodinger(n, g)[inst.bitstrings.astype(np.int64)]
+    P = Plan(inst.text, inst.n_low, inst.blocks)
+    out = np.zeros(len(inst.bitstrings), dtype=np.complex64)
+    P.run(out, bitstrings=inst.bitstrings)
+    check(out, ref, "c64")
+
+
+def test_bad_range_errors(torch):
+    from paper_2502_06959_b200 import HsfError, Plan
+    inst = make_config("c1")
+    P = Plan(inst.text, inst.n_low, inst.blocks)
+    out = torch.empty(1 << 12, dtype=torch.complex64, device="cuda")
+    with pytest.raises(HsfError):
+        P.run(out, path_range=(5, 5 + 100))
+    with pytest.raises(HsfError):
+        P.run(out, row_range=(10, 5))
+
+
+# ---------------------------------------------------------- full sizes
+def test_c2_full_size_qft_closed_form(torch):
+    inst = make_config("c2")
+    got, P = gpu_full(torch, inst, precision="simt")
+    n, x = inst.n, inst.meta["x"]
+    i = np.arange(1 << n, dtype=np.int64)
+    rev = np.zeros_like(i)
+    for b in range(n):
+        rev |= ((i >> b) & 1) << (n - 1 - b)
+    ph = (x * rev) % (1 << n)
+    ref = np.exp(2j * np.pi * ph / (1 << n)) / 2 ** (n / 2)
+    check(got, ref, "c64")
+    assert P.n_paths == 4096
+
+
+def test_c3_full_size_partial_paths(torch):
+    # singular values of the c3 blocks are non-degenerate, so every Schmidt term
+    # (hence a partial path sum) is unique up to round-off: compare ranges
+    inst = make_config("c3")
+    n, g = O.parse_circuit(inst.text)
+    P = O.plan(n, g, inst.n_low, inst.blocks)
+    bits = inst.bitstrings[:8192]
+    A, B, c = O.half_states(P, 0, 16)
+    ref = O.recombine_bits(A, B, c, bits, inst.n_low)
+    got, _ = gpu_bits(torch, inst, bits, path_range=(0, 16))
+    check(got, ref, "c64")
+
+
+def test_c5_full_size_partial_paths(torch):
+    inst = make_config("c5")
+    n, g = O.parse_circuit(inst.text)
+    P = O.plan(n, g, inst.n_low, inst.blocks)
+    bits = inst.bitstrings[:8192]
+    A, B, c = O.half_states(P, 100, 104)
+    ref = O.recombine_bits(A, B, c, bits, inst.n_low)
+    got, _ = gpu_bits(torch, inst, bits, path_range=(100, 104))
+    check(got, ref, "c64")
+
+
+def test_c5_full_run_norm_sampled(torch):
+    # all 256 paths, all 2^22 bitstrings: |amp|^2 averages to 2^-40 per sample
+    inst = make_config("c5")
+    got, P = gpu_bits(torch, inst, inst.bitstrings)
+    assert np.isfinite(got).all()
+    m = np.mean(np.abs(got) ** 2) * 2.0 ** 40
+    assert 0.8 < m < 1.2
