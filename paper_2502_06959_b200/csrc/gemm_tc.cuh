@@ -1,20 +1,443 @@
-// gemm_tc.cuh — tensor-core (tcgen05) split-bf16 complex path-sum (K4 + K5).
-// Placeholder until the tcgen05 kernel lands: reports HSF_ERR_UNSUPPORTED.
+// gemm_tc.cuh — full-output Kronecker path-sum on the 5th-generation tensor
+// cores (tcgen05 + TMEM + TMA), split-bf16 emulation of the complex64 product
+//
+//   psi[i][j] = sum_p (c_p A[p][i]) B[p][j]          (a3 folded in)
+//
+// as ONE real GEMM  D[i][2j+c] = sum_kk A''[i][kk] B''[2j+c][kk]  whose fp32
+// row-major output IS the interleaved complex64 result:
+//   A'' row i       = (re, im) of c_p A[p][i]          for p = 0..K-1
+//   B'' row 2j      = (re, -im) of B[p][j]
+//   B'' row 2j+1    = (im,  re) of B[p][j]
+// Each operand x is split x = hi + lo with hi = bf16_rn(x), lo = bf16_rn(x-hi);
+// per k-block the kernel loads A_hi, A_lo, B_hi, B_lo once and issues three
+// MMAs into the same TMEM accumulator: A_hi*B_hi + A_hi*B_lo + A_lo*B_hi
+// (HSF_PREC_BF16X3; BF16X1 issues only the first).
+//
+// K4 (split_a/split_b): node-major leaves -> K-major bf16 hi/lo operands.
+// K5 (tc_gemm_kernel): persistent, warp-specialised, one CTA per SM:
+//   warp 0  TMA producer (cp.async.bulk.tensor, SWIZZLE_128B, mbarrier tx)
+//   warp 1  TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=256,
+//           K=16 per instruction), tcgen05.commit -> smem/TMEM barriers
+//   warps 2-5 epilogue: tcgen05.ld 32x32b -> registers -> global fp32
+//   2 SMEM stages x (16+16+32+32) KB, 2 TMEM accumulators x 256 columns.
 #pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <stdint.h>
 
 #include "hsf_internal.h"
 
 namespace hsf {
+namespace tc {
 
-inline size_t tc_workspace_bytes(long long K, long long rows, long long MB, bool x3) {
-  (void)K; (void)rows; (void)MB; (void)x3;
-  return 0;
+constexpr int BM = 128, BN = 256, BK = 64;  // BK in bf16 elements = 128 B rows
+constexpr int STAGES = 2;
+constexpr int A_TILE = BM * BK * 2;  // 16 KB
+constexpr int B_TILE = BN * BK * 2;  // 32 KB
+constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024;  // + alignment slack
+constexpr int THREADS = 192;
+constexpr int TMEM_COLS = 512;  // 2 accumulators x 256 fp32 columns
+
+struct Params {
+  int num_m, num_n, num_k;  // blocks
+  int x3;
+  float* out;               // D, row-major, ld = ldo floats
+  long long ldo;
+  long long rows, cols;     // valid D extent (rows of this call, 2*MB)
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  // UMMA shared-memory descriptor, K-major, SWIZZLE_128B: start>>4, LBO=1 (unused),
+  // SBO=1024 B between 8-row swizzle atoms, version 1 (sm_100), layout type 2.
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// kind::f16 instruction descriptor: D=F32, A=B=BF16, K-major both, N=BN, M=BM
+constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                           ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accum));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
 }
 
-inline void tc_path_sum(const float2*, const float2*, const float2*, float2*, long long, long long, long long,
-                        long long, long long, bool, void*, size_t, cudaStream_t) {
-  fail(HSF_ERR_UNSUPPORTED, "tcgen05 path-sum not built yet");
+__global__ void __launch_bounds__(THREADS, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUtensorMap mA_lo,
+                   const __grid_constant__ CUtensorMap mB_hi, const __grid_constant__ CUtensorMap mB_lo,
+                   const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES], tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_base_sh;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int num_tiles = p.num_m * p.num_n;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mA_hi) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mB_hi) : "memory");
+    if (p.x3) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&mA_lo) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&mB_lo) : "memory");
+    }
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem_base = tmem_base_sh;
+
+  const uint32_t stage_bytes = p.x3 ? (uint32_t)STAGE_BYTES : (uint32_t)(A_TILE + B_TILE);
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int mb = tile % p.num_m, nb = tile / p.num_m;
+        for (int kb = 0; kb < p.num_k; ++kb) {
+          mbar_wait(&empty_bar[s], ph ^ 1);
+          uint8_t* st = smem + s * STAGE_BYTES;
+          mbar_expect_tx(&full_bar[s], stage_bytes);
+          tma_load_2d(st, &mA_hi, &full_bar[s], kb * BK, mb * BM);
+          tma_load_2d(st + 2 * A_TILE, &mB_hi, &full_bar[s], kb * BK, nb * BN);
+          if (p.x3) {
+            tma_load_2d(st + A_TILE, &mA_lo, &full_bar[s], kb * BK, mb * BM);
+            tma_load_2d(st + 2 * A_TILE + B_TILE, &mB_lo, &full_bar[s], kb * BK, nb * BN);
+          }
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t aph = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        mbar_wait(&tempty_bar[acc], aph ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t d = tmem_base + (uint32_t)(acc * BN);
+        for (int kb = 0; kb < p.num_k; ++kb) {
+          mbar_wait(&full_bar[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
+          const uint32_t a_hi = st, a_lo = st + A_TILE, b_hi = st + 2 * A_TILE, b_lo = st + 2 * A_TILE + B_TILE;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint32_t ko = k * 32;  // 16 bf16 = 32 B inside the 128 B swizzle row
+            mma_bf16(d, sw128_desc(a_hi + ko), sw128_desc(b_hi + ko), (kb | k) ? 1u : 0u);
+            if (p.x3) {
+              mma_bf16(d, sw128_desc(a_hi + ko), sw128_desc(b_lo + ko), 1u);
+              mma_bf16(d, sw128_desc(a_lo + ko), sw128_desc(b_hi + ko), 1u);
+            }
+          }
+          mma_commit(&empty_bar[s]);  // frees the smem stage when these MMAs retire
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        mma_commit(&tfull_bar[acc]);  // accumulator ready for the epilogue
+        if (++acc == 2) {
+          acc = 0;
+          aph ^= 1;
+        }
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- epilogue
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = q * 32 + lane;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int mb = tile % p.num_m, nb = tile / p.num_m;
+      mbar_wait(&tfull_bar[acc], aph);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const long long gi = (long long)mb * BM + row;
+      const long long gc0 = (long long)nb * BN;
+      float* orow = p.out + gi * p.ldo;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        const uint32_t taddr = tmem_base + (uint32_t)(acc * BN + c * 32) + ((uint32_t)(q * 32) << 16);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
+              "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+              "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        const long long gc = gc0 + c * 32;
+        if (gi < p.rows) {
+          if (gc + 32 <= p.cols) {
+            float4* o4 = reinterpret_cast<float4*>(orow + gc);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              o4[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                  __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (gc + j < p.cols) orow[gc + j] = __uint_as_float(v[j]);
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        aph ^= 1;
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+}
+
+// ----------------------------------------------------------------------- K4
+__device__ __forceinline__ void split_bf16(float x, __nv_bfloat16& hi, __nv_bfloat16& lo) {
+  hi = __float2bfloat16_rn(x);
+  lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+}
+
+// A'' rows [0, rows_pad): row i <- (re, im) of c_p * A[p][r0 + i]; zero padding
+__global__ void split_a_kernel(const float2* __restrict__ leaves, const float2* __restrict__ cp,
+                               __nv_bfloat162* __restrict__ hi, __nv_bfloat162* __restrict__ lo, long long K,
+                               long long Kpad, long long MA, long long r0, long long rows) {
+  __shared__ float2 t[32][33];
+  const long long i0 = (long long)blockIdx.x * 32, p0 = (long long)blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int r = ty; r < 32; r += 8) {
+    long long p = p0 + r, i = i0 + tx;
+    float2 v = make_float2(0.f, 0.f);
+    if (p < K && i < rows) {
+      float2 a = leaves[p * MA + r0 + i], c = cp[p];
+      v = make_float2(a.x * c.x - a.y * c.y, a.x * c.y + a.y * c.x);
+    }
+    t[r][tx] = v;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    long long i = i0 + r, p = p0 + tx;
+    float2 v = t[tx][r];
+    __nv_bfloat162 h, l;
+    split_bf16(v.x, h.x, l.x);
+    split_bf16(v.y, h.y, l.y);
+    hi[i * Kpad + p] = h;
+    if (lo) lo[i * Kpad + p] = l;
+  }
+}
+
+// B'' rows [0, 2*MB_pad): row 2j <- (re, -im), row 2j+1 <- (im, re) of B[p][j]
+__global__ void split_b_kernel(const float2* __restrict__ leaves, __nv_bfloat162* __restrict__ hi,
+                               __nv_bfloat162* __restrict__ lo, long long K, long long Kpad, long long MB) {
+  __shared__ float2 t[32][33];
+  const long long j0 = (long long)blockIdx.x * 32, p0 = (long long)blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int r = ty; r < 32; r += 8) {
+    long long p = p0 + r, j = j0 + tx;
+    float2 v = make_float2(0.f, 0.f);
+    if (p < K && j < MB) v = leaves[p * MB + j];
+    t[r][tx] = v;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    long long j = j0 + r, p = p0 + tx;
+    float2 v = t[tx][r];
+    __nv_bfloat162 h0, l0, h1, l1;
+    split_bf16(v.x, h0.x, l0.x);
+    split_bf16(-v.y, h0.y, l0.y);
+    split_bf16(v.y, h1.x, l1.x);
+    split_bf16(v.x, h1.y, l1.y);
+    hi[(2 * j) * Kpad + p] = h0;
+    hi[(2 * j + 1) * Kpad + p] = h1;
+    if (lo) {
+      lo[(2 * j) * Kpad + p] = l0;
+      lo[(2 * j + 1) * Kpad + p] = l1;
+    }
+  }
+}
+
+}  // namespace tc
+
+// ------------------------------------------------------------------ host side
+struct TcDims {
+  long long Kpad, rows_pad, nrows_b_pad;  // Kpad in complex; operand rows
+  size_t a_bytes, b_bytes;
+};
+
+inline TcDims tc_dims(long long K, long long rows, long long MB) {
+  TcDims d;
+  d.Kpad = (K + 31) / 32 * 32;  // 32 complex = 64 bf16 = one BK block
+  d.rows_pad = (rows + tc::BM - 1) / tc::BM * tc::BM;
+  d.nrows_b_pad = (2 * MB + tc::BN - 1) / tc::BN * tc::BN;
+  d.a_bytes = (size_t)d.rows_pad * d.Kpad * 4;  // Kpad complex = 2*Kpad bf16
+  d.b_bytes = (size_t)d.nrows_b_pad * d.Kpad * 4;
+  return d;
+}
+
+inline size_t tc_workspace_bytes(long long K, long long rows, long long MB, bool x3) {
+  TcDims d = tc_dims(K, rows, MB);
+  return (x3 ? 2 : 1) * (((d.a_bytes + 1023) & ~(size_t)1023) + ((d.b_bytes + 1023) & ~(size_t)1023));
+}
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+inline PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !p)
+      fail(HSF_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+    fn = (PFN_encodeTiled)p;
+  }
+  return fn;
+}
+
+inline CUtensorMap make_map(void* base, long long rows, long long cols_bf16, int box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)cols_bf16, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols_bf16 * 2};
+  cuuint32_t box[2] = {(cuuint32_t)tc::BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(HSF_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
+inline int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+inline void tc_path_sum(const float2* leavesA, const float2* leavesB, const float2* cp, float2* out, long long K,
+                        long long MA, long long MB, long long r0, long long rows, bool x3, void* ws, size_t ws_bytes,
+                        cudaStream_t st) {
+  TcDims d = tc_dims(K, rows, MB);
+  if (tc_workspace_bytes(K, rows, MB, x3) > ws_bytes) fail(HSF_ERR_INVALID_ARG, "tc workspace too small");
+  char* w = (char*)ws;
+  auto take = [&](size_t b) {
+    char* r = w;
+    w += (b + 1023) & ~(size_t)1023;
+    return r;
+  };
+  __nv_bfloat162* a_hi = (__nv_bfloat162*)take(d.a_bytes);
+  __nv_bfloat162* b_hi = (__nv_bfloat162*)take(d.b_bytes);
+  __nv_bfloat162* a_lo = x3 ? (__nv_bfloat162*)take(d.a_bytes) : nullptr;
+  __nv_bfloat162* b_lo = x3 ? (__nv_bfloat162*)take(d.b_bytes) : nullptr;
+  dim3 blk(32, 8);
+  tc::split_a_kernel<<<dim3((unsigned)(d.rows_pad / 32), (unsigned)(d.Kpad / 32)), blk, 0, st>>>(
+      leavesA, cp, a_hi, a_lo, K, d.Kpad, MA, r0, rows);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("split_a: ") + cudaGetErrorString(e));
+  tc::split_b_kernel<<<dim3((unsigned)(d.nrows_b_pad / 64), (unsigned)(d.Kpad / 32)), blk, 0, st>>>(
+      leavesB, b_hi, b_lo, K, d.Kpad, MB);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("split_b: ") + cudaGetErrorString(e));
+  const long long kcols = 2 * d.Kpad;  // bf16 per operand row
+  CUtensorMap mAh = make_map(a_hi, d.rows_pad, kcols, tc::BM);
+  CUtensorMap mBh = make_map(b_hi, d.nrows_b_pad, kcols, tc::BN);
+  CUtensorMap mAl = x3 ? make_map(a_lo, d.rows_pad, kcols, tc::BM) : mAh;
+  CUtensorMap mBl = x3 ? make_map(b_lo, d.nrows_b_pad, kcols, tc::BN) : mBh;
+  tc::Params p;
+  p.num_m = (int)(d.rows_pad / tc::BM);
+  p.num_n = (int)(d.nrows_b_pad / tc::BN);
+  p.num_k = (int)(kcols / tc::BK);
+  p.x3 = x3 ? 1 : 0;
+  p.out = (float*)out;
+  p.ldo = 2 * MB;
+  p.rows = rows;
+  p.cols = 2 * MB;
+  static bool attr = false;
+  if (!attr) {
+    e = cudaFuncSetAttribute(tc::tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
+    if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("tc smem attr: ") + cudaGetErrorString(e));
+    attr = true;
+  }
+  const long long tiles = (long long)p.num_m * p.num_n;
+  const int grid = (int)std::min<long long>(tiles, num_sms());
+  tc::tc_gemm_kernel<<<grid, tc::THREADS, tc::SMEM_BYTES, st>>>(mAh, mAl, mBh, mBl, p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("tc_gemm: ") + cudaGetErrorString(e));
 }
 
 }  // namespace hsf
