@@ -77,7 +77,7 @@ typedef struct {
   int32_t max_dense_block_qubits;/* default 10 (dense block assembly O(D^3)) */
   double log2_path_budget;       /* default 26 */
   int32_t individual;            /* 1 => ignore blocks, cut every crossing gate alone */
-  int32_t tile_qubits;           /* amplitudes per SMEM tile = 2^tile_qubits for
+  int32_t tile_qubits;           /* in [10,13]: amplitudes per SMEM tile = 2^tile_qubits for
                                     halves larger than the SMEM-resident limit;
                                     0 => default (12) */
   int32_t fuse_gates;            /* 1 (default) => host gate fusion */

@@ -422,7 +422,10 @@ static std::vector<cd> op_matrix(const Plan& P, const HostOp& op) {
 // Fusion inside one segment ("gate fusion"): (1) a 1-qubit dense op
 // merges into the previous op if that op is a fixed 1-qubit dense op on the
 // same qubit and nothing in between touched the qubit; (2) adjacent fixed
-// diagonal ops merge while their union has <= 12 qubits.
+// diagonal ops merge while their union has <= kFuseDiagQ qubits (tables of
+// <= 256 entries stay L1-resident in the simulator kernels).
+constexpr int kFuseDiagQ = 8;
+
 static void fuse_segment(Plan& P, std::vector<HostOp>& seg) {
   // (1)
   std::vector<HostOp> out;
@@ -452,7 +455,7 @@ static void fuse_segment(Plan& P, std::vector<HostOp>& seg) {
       HostOp& prev = out2.back();
       std::set<int> uni(prev.q, prev.q + prev.k);
       uni.insert(op.q, op.q + op.k);
-      if ((int)uni.size() <= 12) {
+      if ((int)uni.size() <= kFuseDiagQ) {
         std::vector<int> qs(uni.begin(), uni.end());  // ascending
         const int k = (int)qs.size();
         auto Da = op_matrix(P, prev), Db = op_matrix(P, op);
@@ -600,11 +603,16 @@ static void build_half(Plan& P, int h, const std::vector<SchedItem>& order) {
     H.seg_end[l] = (int64_t)H.ops.size();
   }
   // materialised levels: those followed by a dense op in their segment, plus the leaves
+  // A level is materialised (its node states written to HBM/L2) when the work
+  // a child would otherwise redo is heavy: a dense op in its segment, or a
+  // wide diagonal (> 2^8-entry table, not L1-resident) in the factor that
+  // leads to it or in its segment.  Otherwise children recompute it on chip.
   H.materialized.clear();
   for (int l = 0; l < U; ++l) {
-    bool dense = false;
-    for (auto& op : segs[l]) dense = dense || op.kind == OP_DENSE;
-    if (dense) H.materialized.push_back(l);
+    bool heavy = false;
+    for (auto& op : segs[l]) heavy = heavy || op.kind == OP_DENSE || (op.kind == OP_DIAG && op.k > kFuseDiagQ);
+    if (l > 0) heavy = heavy || factors[l - 1].kind == OP_DENSE || factors[l - 1].k > kFuseDiagQ;
+    if (heavy) H.materialized.push_back(l);
   }
   H.materialized.push_back(U);
   // transitions + passes

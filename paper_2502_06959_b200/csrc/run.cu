@@ -132,7 +132,7 @@ static Layout make_layout(const Plan& P, const hsf_run_args& a, size_t elem) {
   if (L.r0 == 0 && L.r1 == 0) L.r1 = 1ull << nA;
   if (!L.bits_mode && (L.r0 >= L.r1 || L.r1 > (1ull << nA))) fail(HSF_ERR_INVALID_ARG, "bad row range");
   L.prec = a.precision;
-  if (L.prec == HSF_PREC_AUTO) L.prec = HSF_PREC_SIMT;
+  if (L.prec == HSF_PREC_AUTO) L.prec = (P.opts.dtype == HSF_C64) ? HSF_PREC_BF16X3 : HSF_PREC_SIMT;
   if (P.opts.dtype == HSF_C128 && L.prec != HSF_PREC_SIMT) fail(HSF_ERR_UNSUPPORTED, "complex128 path-sum is SIMT fp64 only");
   size_t off = 0;
   for (int h = 0; h < 2; ++h) {
@@ -427,7 +427,7 @@ hsf_status hsf_plan(const char* text, size_t len, int32_t n_low, int64_t n_block
     hsf_plan_opts_default(&o);
     if (opts) o = *opts;
     if (o.tile_qubits == 0) o.tile_qubits = 12;
-    if (o.tile_qubits < 6 || o.tile_qubits > 13) fail(HSF_ERR_INVALID_ARG, "tile_qubits must be in [6,13]");
+    if (o.tile_qubits < 10 || o.tile_qubits > 13) fail(HSF_ERR_INVALID_ARG, "tile_qubits must be in [10,13]");
     if (o.dtype != HSF_C64 && o.dtype != HSF_C128) fail(HSF_ERR_INVALID_ARG, "bad dtype");
     if (!(o.svd_rel_tol >= 0 && o.svd_rel_tol < 1)) fail(HSF_ERR_INVALID_ARG, "bad svd_rel_tol");
     if (o.max_dense_block_qubits < 1 || o.max_dense_block_qubits > 12) fail(HSF_ERR_INVALID_ARG, "bad max_dense_block_qubits");

@@ -220,18 +220,43 @@ __global__ void __launch_bounds__(kSimThreads, 2) hsf_pass_kernel(const PassPara
         need_sync = false;
         ++i;
       } else {
-        // a run of diagonal ops in one sweep (element-owner mapping)
+        // a run of diagonal ops in one sweep (element-owner mapping); each
+        // thread keeps 8 elements in registers so the table loads of one op
+        // are 8 independent requests in flight
         int j = i;
         while (j < cnt && sops[j].kind == OP_DIAG) ++j;
-        for (int e = threadIdx.x; e < nel; e += blockDim.x) {
-          long long g = gidx_of(e);
-          C v = s[e];
+        for (int e0 = threadIdx.x; e0 < nel; e0 += 8 * blockDim.x) {
+          C v[8];
+          long long g[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * blockDim.x;
+            if (e < nel) {
+              v[u] = s[e];
+              g[u] = gidx_of(e);
+            }
+          }
           for (int r = i; r < j; ++r) {
             const DevOp& d = sops[r];
-            long long digit = (d.radix > 1) ? (node_g / d.div) % d.radix : 0;
-            v = cmul(v, coef[d.table + digit * d.stride + diag_index(d, g)]);
+            const long long digit = (d.radix > 1) ? (node_g / d.div) % d.radix : 0;
+            const C* tab = coef + d.table + digit * d.stride;
+            if (d.contiguous) {
+              const int q0 = d.q[0];
+              const long long mask = (1ll << d.k) - 1;
+#pragma unroll
+              for (int u = 0; u < 8; ++u)
+                if (e0 + u * (int)blockDim.x < nel) v[u] = cmul(v[u], __ldg(&tab[(g[u] >> q0) & mask]));
+            } else {
+#pragma unroll
+              for (int u = 0; u < 8; ++u)
+                if (e0 + u * (int)blockDim.x < nel) v[u] = cmul(v[u], __ldg(&tab[diag_index(d, g[u])]));
+            }
           }
-          s[e] = v;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * blockDim.x;
+            if (e < nel) s[e] = v[u];
+          }
         }
         need_sync = true;
         i = j;

@@ -104,7 +104,7 @@ def test_random_small_circuits(torch, seed):
     check(got, ref, "c128")
 
 
-@pytest.mark.parametrize("tile", [6, 8, 10])
+@pytest.mark.parametrize("tile", [10, 11, 12])
 def test_tile_passes_forced(torch, tile):
     # halves above the SMEM-resident limit stream through 2^tile tiles; force
     # the tiled tier on small halves by lowering tile_qubits below m
@@ -217,3 +217,48 @@ def test_c5_full_run_norm_sampled(torch):
     assert np.isfinite(got).all()
     m = np.mean(np.abs(got) ** 2) * 2.0 ** 40
     assert 0.8 < m < 1.2
+
+
+# --------------------------------------------------- tensor-core path-sum
+@pytest.mark.parametrize("name", ["c1", "c2", "c4", "c5"])
+def test_twins_full_output_bf16x3(torch, name):
+    inst = make_config(name, twin=True)
+    n, g = O.parse_circuit(inst.text)
+    ref = O.schrodinger(n, g)
+    got, _ = gpu_full(torch, inst, dtype="c64", precision="bf16x3")
+    check(got, ref, "c64")
+
+
+def test_bf16x1_is_lower_precision(torch):
+    inst = make_config("c2", twin=True)
+    n, g = O.parse_circuit(inst.text)
+    ref = O.schrodinger(n, g)
+    x1, _ = gpu_full(torch, inst, dtype="c64", precision="bf16x1")
+    x3, _ = gpu_full(torch, inst, dtype="c64", precision="bf16x3")
+    e1 = np.linalg.norm(x1 - ref) / np.linalg.norm(ref)
+    e3 = np.linalg.norm(x3 - ref) / np.linalg.norm(ref)
+    assert e1 < 2e-2 and e3 < 2e-5 and e3 < e1 / 20, (e1, e3)
+
+
+def test_bf16x3_ragged_rows_and_paths(torch):
+    # K not a multiple of 32, row range not a multiple of 128, 2*MB < 256
+    inst = make_config("c5", twin=True)
+    full, P = gpu_full(torch, inst, precision="simt")
+    rows = 1 << P.n_a
+    for pr, rr in [((3, 200), (5, 37)), ((0, 256), (0, rows)), ((17, 18), (1, 2))]:
+        ref, _ = gpu_full(torch, inst, precision="simt", path_range=pr, row_range=rr)
+        got, _ = gpu_full(torch, inst, precision="bf16x3", path_range=pr, row_range=rr)
+        assert np.abs(got - ref).max() <= 1e-5 * max(1.0, np.abs(ref).max() * 100)
+
+
+def test_c2_full_size_bf16x3(torch):
+    inst = make_config("c2")
+    got, P = gpu_full(torch, inst, precision="bf16x3")
+    n, x = inst.n, inst.meta["x"]
+    i = np.arange(1 << n, dtype=np.int64)
+    rev = np.zeros_like(i)
+    for b in range(n):
+        rev |= ((i >> b) & 1) << (n - 1 - b)
+    ref = np.exp(2j * np.pi * ((x * rev) % (1 << n)) / (1 << n)) / 2 ** (n / 2)
+    md, rel = check(got, ref, "c64")
+    print(f"c2 bf16x3 max|d|={md:.3e} relL2={rel:.3e}")
