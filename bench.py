@@ -162,8 +162,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != a.gpus:
-        world = a.gpus if world == 1 else world
+    if world != a.gpus and rank == 0:
+        print(f"note: --gpus {a.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -210,14 +210,8 @@ def main():
     for _ in range(max(3, a.warmup)):
         step()
     torch.cuda.synchronize()
-    # per-phase device times (separate pass: timings=True synchronises)
-    phases = []
-    for _ in range(3):
-        flush.fill_(1)
-        phases.append(P.run(out, bitstrings=bits_d, path_range=pr, precision=a.precision, timings=True))
-    phase = [statistics.median(p[i] for p in phases) for i in range(4)]
-
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    phases = []
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -225,12 +219,20 @@ def main():
         for i in range(a.steps):
             flush.fill_(i & 0xFF)
             evs[i][0].record(stream)
-            step()
+            # timings=True: the library brackets each phase with CUDA events on
+            # the stream it launches on (and synchronises at the end of the run)
+            phases.append(P.run(out, bitstrings=bits_d, path_range=pr, precision=a.precision, timings=True))
+            if world > 1:
+                if full:
+                    dist.reduce_scatter_tensor(shard, out)
+                else:
+                    dist.all_reduce(out)
             evs[i][1].record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    ms = [s.elapsed_time(e) for s, e in evs]
+    ms = [s_.elapsed_time(e_) for s_, e_ in evs]
+    phase = [statistics.mean(p_[i] for p_ in phases) for i in range(5)]
     t_step = statistics.mean(ms)
     if world > 1:
         t = torch.tensor([t_step], dtype=torch.float64, device="cuda")
@@ -268,38 +270,43 @@ def main():
     hbm = peaks.get("hbm_gbs", 6650.0)
     bf16 = peaks.get("bf16_tflops", 1590.0)
     K = pr[1] - pr[0]
-    roof = None
-    sim_ms = phase[0] + phase[1]
-    sum_ms = phase[2]
+    core_ms = phase[3]
     prec = a.precision
-    if full:
-        MA, MB = 1 << (inst.n - inst.n_low), 1 << inst.n_low
-        useful = 8.0 * MA * MB * K
-        if prec in ("auto", "bf16x3", "bf16x1") and inst.dtype == "c64" and H.PREC.get(prec, 0) != 1 and \
-                getattr(P, "_tc_ok", True) and False:
-            pass
-        # SIMT path today: FP32 FMA-pipe bound, report against the guide's unit
-        # counts: 148 SMs x 128 FP32 lanes x 2 flop x measured SM clock
-        clk_mhz = peaks.get("clocks_under_load", {}).get("sm_mhz_median", 1305.0)
+    eff_prec = ("bf16x3" if inst.dtype == "c64" else "simt") if prec == "auto" else prec
+    MA, MB = 1 << (inst.n - inst.n_low), 1 << inst.n_low
+    clk_mhz = peaks.get("clocks_under_load", {}).get("sm_mhz_median", 1305.0)
+    if full and eff_prec in ("bf16x3", "bf16x1"):
+        # executed tensor-core flops: (3 | 1) real GEMMs of rows x 2MB x 2K
+        nprod = 3 if eff_prec == "bf16x3" else 1
+        tflop = nprod * 2.0 * MA * (2 * MB) * (2 * K)
+        ach = tflop / (core_ms * 1e-3) / 1e12
+        roof = {"bound": "tensor", "kernel": "tc_gemm_kernel (tcgen05 bf16, split x%d)" % nprod,
+                "achieved": ach, "peak": bf16, "unit": "TFLOP/s", "frac": ach / bf16, "traffic": None,
+                "flops_per_launch": tflop, "useful_complex_flops": 8.0 * MA * MB * K,
+                "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst); sustained %.1f" %
+                               peaks.get("bf16_tflops_sustained", 0.0),
+                "kernel_ms": core_ms}
+    elif full:
         alu_peak = 148 * 128 * 2 * clk_mhz * 1e6 / 1e12
-        ach = useful / (sum_ms * 1e-3) / 1e12
-        roof = {"bound": "alu", "kernel": "simt_gemm_kernel (complex fp32 path-sum)", "achieved": ach,
-                "peak": alu_peak, "unit": "TFLOP/s", "frac": ach / alu_peak, "traffic": None,
+        useful = 8.0 * MA * MB * K
+        ach = useful / (core_ms * 1e-3) / 1e12
+        roof = {"bound": "alu", "kernel": "simt_gemm_kernel (complex FMA path-sum)", "achieved": ach,
+                "peak": alu_peak, "unit": "TFLOP/s", "frac": ach / alu_peak, "traffic": None, "kernel_ms": core_ms,
                 "peak_source": "148 SM x 128 FP32 lanes x 2 x median SM clock under load (MEASURED_PEAKS.json)"}
     else:
-        MA, MB = 1 << (inst.n - inst.n_low), 1 << inst.n_low
         nb = len(inst.bitstrings)
         byts = nb * 2 * K * esz
-        ach = byts / (sum_ms * 1e-3) / 1e9
-        roof = {"bound": "hbm", "kernel": "path-sum (transpose + gather)", "achieved": ach, "peak": hbm,
-                "unit": "GB/s", "frac": ach / hbm, "traffic": None}
+        ach = byts / (core_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": "gather_dot (bitstring path-sum)", "achieved": ach, "peak": hbm,
+                "unit": "GB/s", "frac": ach / hbm, "traffic": None, "kernel_ms": core_ms,
+                "note": "algorithmic bytes = 2 K-rows per sample (upper bound; repeated rows hit L2)"}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         r, sample, thr, _ = cpu_oracle_rate(inst, budget_s=15.0)
         cpu = {"value": r, "unit": "paths/s", "cores": thr, "kind": "oracle", "sample": sample}
 
-    n_launch = P.passes[0] + P.passes[1] + (1 if full else 3)
+    n_launch = P.passes[0] + P.passes[1] + (1 if (full and eff_prec == "simt") else 3)
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "paths/s", "n_gpus": world, "steps": a.steps,
                 "warmup": max(3, a.warmup), "ms_per_step": t_step, "higher_is_better": True, "scaling": "strong",
@@ -309,7 +316,8 @@ def main():
                            "outputs": N_out, "precision": prec, "parallelism": f"paths{world}",
                            "l2": "flushed (256 MiB write) between timed steps"},
                 "amplitudes_per_s": amps, "terms_per_s": amps * P.n_paths,
-                "phase_ms": {"sim_A": phase[0], "sim_B": phase[1], "path_sum": phase[2], "run_total": phase[3]},
+                "phase_ms": {"sim_A": phase[0], "sim_B": phase[1], "prep": phase[2], "core": phase[3],
+                             "run_total": phase[4]},
                 "plan_s": t_plan, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": n_launch, "clocks": clk.summary()}
         print(json.dumps(line), flush=True)

@@ -145,8 +145,14 @@ typedef struct {
   void* cuda_stream;            /* cudaStream_t; NULL => legacy default stream */
   hsf_precision precision;
   int32_t device;               /* CUDA device ordinal; -1 => current */
-  double* phase_ms;             /* optional [4]: sim A, sim B, path-sum, total
-                                   (CUDA events; synchronises when non-NULL) */
+  double* phase_ms;             /* optional [5], ms from CUDA events (synchronises):
+                                   [0] start -> half-A leaves done (caller stream)
+                                   [1] start -> half-B leaves done (side stream;
+                                       the two path trees run concurrently)
+                                   [2] operand prep after the later tree (K4)
+                                   [3] core path-sum kernel (tcgen05 GEMM /
+                                       SIMT GEMM / gather)
+                                   [4] total */
 } hsf_run_args;
 
 /* hsf_run — evaluate the paths [path_begin, path_end) on the GPU: path-tree

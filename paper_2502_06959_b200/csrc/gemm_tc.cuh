@@ -389,10 +389,14 @@ inline int num_sms() {
   return n;
 }
 
-inline void tc_path_sum(const float2* leavesA, const float2* leavesB, const float2* cp, float2* out, long long K,
-                        long long MA, long long MB, long long r0, long long rows, bool x3, void* ws, size_t ws_bytes,
-                        cudaStream_t st) {
-  TcDims d = tc_dims(K, rows, MB);
+struct TcBuffers {
+  TcDims d;
+  __nv_bfloat162 *a_hi, *a_lo, *b_hi, *b_lo;
+};
+
+inline TcBuffers tc_buffers(long long K, long long rows, long long MB, bool x3, void* ws, size_t ws_bytes) {
+  TcBuffers t;
+  t.d = tc_dims(K, rows, MB);
   if (tc_workspace_bytes(K, rows, MB, x3) > ws_bytes) fail(HSF_ERR_INVALID_ARG, "tc workspace too small");
   char* w = (char*)ws;
   auto take = [&](size_t b) {
@@ -400,27 +404,40 @@ inline void tc_path_sum(const float2* leavesA, const float2* leavesB, const floa
     w += (b + 1023) & ~(size_t)1023;
     return r;
   };
-  __nv_bfloat162* a_hi = (__nv_bfloat162*)take(d.a_bytes);
-  __nv_bfloat162* b_hi = (__nv_bfloat162*)take(d.b_bytes);
-  __nv_bfloat162* a_lo = x3 ? (__nv_bfloat162*)take(d.a_bytes) : nullptr;
-  __nv_bfloat162* b_lo = x3 ? (__nv_bfloat162*)take(d.b_bytes) : nullptr;
-  dim3 blk(32, 8);
-  tc::split_a_kernel<<<dim3((unsigned)(d.rows_pad / 32), (unsigned)(d.Kpad / 32)), blk, 0, st>>>(
-      leavesA, cp, a_hi, a_lo, K, d.Kpad, MA, r0, rows);
+  t.a_hi = (__nv_bfloat162*)take(t.d.a_bytes);
+  t.b_hi = (__nv_bfloat162*)take(t.d.b_bytes);
+  t.a_lo = x3 ? (__nv_bfloat162*)take(t.d.a_bytes) : nullptr;
+  t.b_lo = x3 ? (__nv_bfloat162*)take(t.d.b_bytes) : nullptr;
+  return t;
+}
+
+// K4 for half A (c_p folded) — may run on its own stream
+inline void tc_prep_a(const TcBuffers& t, const float2* leavesA, const float2* cp, long long K, long long MA,
+                      long long r0, long long rows, cudaStream_t st) {
+  tc::split_a_kernel<<<dim3((unsigned)(t.d.rows_pad / 32), (unsigned)(t.d.Kpad / 32)), dim3(32, 8), 0, st>>>(
+      leavesA, cp, t.a_hi, t.a_lo, K, t.d.Kpad, MA, r0, rows);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("split_a: ") + cudaGetErrorString(e));
-  tc::split_b_kernel<<<dim3((unsigned)(d.nrows_b_pad / 64), (unsigned)(d.Kpad / 32)), blk, 0, st>>>(
-      leavesB, b_hi, b_lo, K, d.Kpad, MB);
-  e = cudaGetLastError();
+}
+
+// K4 for half B — may run on its own stream
+inline void tc_prep_b(const TcBuffers& t, const float2* leavesB, long long K, long long MB, cudaStream_t st) {
+  tc::split_b_kernel<<<dim3((unsigned)(t.d.nrows_b_pad / 64), (unsigned)(t.d.Kpad / 32)), dim3(32, 8), 0, st>>>(
+      leavesB, t.b_hi, t.b_lo, K, t.d.Kpad, MB);
+  cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("split_b: ") + cudaGetErrorString(e));
-  const long long kcols = 2 * d.Kpad;  // bf16 per operand row
-  CUtensorMap mAh = make_map(a_hi, d.rows_pad, kcols, tc::BM);
-  CUtensorMap mBh = make_map(b_hi, d.nrows_b_pad, kcols, tc::BN);
-  CUtensorMap mAl = x3 ? make_map(a_lo, d.rows_pad, kcols, tc::BM) : mAh;
-  CUtensorMap mBl = x3 ? make_map(b_lo, d.nrows_b_pad, kcols, tc::BN) : mBh;
+}
+
+// K5: the persistent tcgen05 GEMM
+inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long rows, bool x3, cudaStream_t st) {
+  const long long kcols = 2 * t.d.Kpad;  // bf16 per operand row
+  CUtensorMap mAh = make_map(t.a_hi, t.d.rows_pad, kcols, tc::BM);
+  CUtensorMap mBh = make_map(t.b_hi, t.d.nrows_b_pad, kcols, tc::BN);
+  CUtensorMap mAl = x3 ? make_map(t.a_lo, t.d.rows_pad, kcols, tc::BM) : mAh;
+  CUtensorMap mBl = x3 ? make_map(t.b_lo, t.d.nrows_b_pad, kcols, tc::BN) : mBh;
   tc::Params p;
-  p.num_m = (int)(d.rows_pad / tc::BM);
-  p.num_n = (int)(d.nrows_b_pad / tc::BN);
+  p.num_m = (int)(t.d.rows_pad / tc::BM);
+  p.num_n = (int)(t.d.nrows_b_pad / tc::BN);
   p.num_k = (int)(kcols / tc::BK);
   p.x3 = x3 ? 1 : 0;
   p.out = (float*)out;
@@ -428,6 +445,7 @@ inline void tc_path_sum(const float2* leavesA, const float2* leavesB, const floa
   p.rows = rows;
   p.cols = 2 * MB;
   static bool attr = false;
+  cudaError_t e;
   if (!attr) {
     e = cudaFuncSetAttribute(tc::tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
     if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("tc smem attr: ") + cudaGetErrorString(e));

@@ -38,7 +38,8 @@ struct DeviceState {
   void* cp = nullptr;
   size_t cp_cap = 0;
   uint64_t cp_p0 = ~0ull, cp_p1 = ~0ull;
-  cudaEvent_t ev[5] = {};
+  cudaEvent_t ev[6] = {};
+  cudaStream_t side = nullptr;  // half-B stream
   bool sticky = false;
 };
 
@@ -55,6 +56,7 @@ void destroy_device(Plan* p) {
   cudaFree(d->cp);
   for (auto& e : d->ev)
     if (e) cudaEventDestroy(e);
+  if (d->side) cudaStreamDestroy(d->side);
   if (cur >= 0) cudaSetDevice(cur);
   delete d;
   p->dev = nullptr;
@@ -89,7 +91,8 @@ static DeviceState* ensure_device(Plan* P, int device) {
       CK(cudaMemcpy(d->ops[h], P->half[h].dev_ops.data(), P->half[h].dev_ops.size() * sizeof(DevOp),
                     cudaMemcpyHostToDevice));
   }
-  for (auto& e : d->ev) CK(cudaEventCreate(&e));
+  for (auto& e : d->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDefault));
+  CK(cudaStreamCreateWithFlags(&d->side, cudaStreamNonBlocking));
   return d;
 }
 
@@ -286,25 +289,41 @@ static void run_half(const Plan& P, DeviceState* d, int h, const Layout& L, cuda
   }
 }
 
+// Path-sum operand preparation for one half (runs on that half's stream):
+// bitstring mode -> transpose (+ c_p fold for A) to [2^m][K]; full mode on the
+// tensor cores -> split-bf16 K-major operands; SIMT full mode reads the
+// node-major leaves directly (nothing to prepare).
 template <typename R>
-static void run_sum(Plan* P, DeviceState* d, const Layout& L, const hsf_run_args& a, cudaStream_t st) {
+static void prep_half(Plan* P, DeviceState* d, const Layout& L, int h, cudaStream_t st) {
+  using C = typename cplx<R>::T;
+  char* ws = (char*)d->ws;
+  const int m = P->half[h].m;
+  const long long K = (long long)L.K;
+  const C* leaves = (const C*)(ws + L.off_leaves[h]);
+  if (L.bits_mode) {
+    C* T = (C*)(ws + L.off_T[h]);
+    dim3 g((unsigned)(((1ll << m) + 31) / 32), (unsigned)((K + 31) / 32));
+    transpose_fold_kernel<C><<<g, dim3(32, 8), 0, st>>>(leaves, T, h == 0 ? (const C*)d->cp : nullptr, K, 1ll << m);
+    CK(cudaGetLastError());
+  } else if (L.prec != HSF_PREC_SIMT) {
+    const int nB = P->n_low;
+    TcBuffers t = tc_buffers(K, (long long)(L.r1 - L.r0), 1ll << nB, L.prec == HSF_PREC_BF16X3, ws + L.off_tc, L.tc_bytes);
+    if (h == 0)
+      tc_prep_a(t, (const float2*)leaves, (const float2*)d->cp, K, 1ll << m, (long long)L.r0, (long long)(L.r1 - L.r0), st);
+    else
+      tc_prep_b(t, (const float2*)leaves, K, 1ll << m, st);
+  }
+}
+
+template <typename R>
+static void run_core(Plan* P, DeviceState* d, const Layout& L, const hsf_run_args& a, cudaStream_t st) {
   using C = typename cplx<R>::T;
   char* ws = (char*)d->ws;
   const int nA = P->n - P->n_low, nB = P->n_low;
   const long long K = (long long)L.K;
-  const C* cp = (const C*)d->cp;
-  const C* leavesA = (const C*)(ws + L.off_leaves[0]);
-  const C* leavesB = (const C*)(ws + L.off_leaves[1]);
   if (L.bits_mode) {
-    C* AT = (C*)(ws + L.off_T[0]);
-    C* BT = (C*)(ws + L.off_T[1]);
-    dim3 blk(32, 8);
-    dim3 gA((unsigned)(((1ll << nA) + 31) / 32), (unsigned)((K + 31) / 32));
-    transpose_fold_kernel<C><<<gA, blk, 0, st>>>(leavesA, AT, cp, K, 1ll << nA);
-    CK(cudaGetLastError());
-    dim3 gB((unsigned)(((1ll << nB) + 31) / 32), (unsigned)((K + 31) / 32));
-    transpose_fold_kernel<C><<<gB, blk, 0, st>>>(leavesB, BT, nullptr, K, 1ll << nB);
-    CK(cudaGetLastError());
+    const C* AT = (const C*)(ws + L.off_T[0]);
+    const C* BT = (const C*)(ws + L.off_T[1]);
     const unsigned long long* bits = (const unsigned long long*)a.bitstrings;
     if (!a.bits_on_device) {
       bits = (const unsigned long long*)(ws + L.off_bits);
@@ -320,22 +339,45 @@ static void run_sum(Plan* P, DeviceState* d, const Layout& L, const hsf_run_args
       gather_dot_kernel<C><<<(unsigned)blocks, 256, 0, st>>>(AT, BT, bits, out, ns, K, nB);
     }
     CK(cudaGetLastError());
-    if (!a.out_on_device) CK(cudaMemcpyAsync(a.out, out, a.n_bitstrings * sizeof(C), cudaMemcpyDeviceToHost, st));
   } else {
     const long long rows = (long long)(L.r1 - L.r0);
     C* out = a.out_on_device ? (C*)a.out : (C*)(ws + L.off_out);
     if (L.prec == HSF_PREC_SIMT) {
+      const C* leavesA = (const C*)(ws + L.off_leaves[0]);
+      const C* leavesB = (const C*)(ws + L.off_leaves[1]);
       dim3 grid((unsigned)(((1ll << nB) + 63) / 64), (unsigned)((rows + 63) / 64));
-      simt_gemm_kernel<C, R><<<grid, 256, 0, st>>>(leavesA, leavesB, cp, out, K, 1ll << nA, 1ll << nB,
+      simt_gemm_kernel<C, R><<<grid, 256, 0, st>>>(leavesA, leavesB, (const C*)d->cp, out, K, 1ll << nA, 1ll << nB,
                                                    (long long)L.r0, rows);
       CK(cudaGetLastError());
     } else {
       if (sizeof(R) != 4) fail(HSF_ERR_UNSUPPORTED, "tensor-core path-sum needs complex64");
-      tc_path_sum((const float2*)leavesA, (const float2*)leavesB, (const float2*)cp, (float2*)out, K, 1ll << nA,
-                  1ll << nB, (long long)L.r0, rows, L.prec == HSF_PREC_BF16X3, ws + L.off_tc, L.tc_bytes, st);
+      TcBuffers t = tc_buffers(K, rows, 1ll << nB, L.prec == HSF_PREC_BF16X3, ws + L.off_tc, L.tc_bytes);
+      tc_gemm(t, (float2*)out, 1ll << nB, rows, L.prec == HSF_PREC_BF16X3, st);
     }
-    if (!a.out_on_device)
-      CK(cudaMemcpyAsync(a.out, out, ((size_t)rows << nB) * sizeof(C), cudaMemcpyDeviceToHost, st));
+  }
+}
+
+template <typename R>
+static void run_all(Plan* P, DeviceState* d, const Layout& L, const hsf_run_args& a, cudaStream_t st, bool timed) {
+  using C = typename cplx<R>::T;
+  // half B (and its operand prep) on the side stream, half A on the caller's
+  // stream; the two path trees are independent until the path-sum
+  CK(cudaEventRecord(d->ev[0], st));
+  CK(cudaStreamWaitEvent(d->side, d->ev[0], 0));
+  run_half<R>(*P, d, 1, L, d->side);
+  if (timed) CK(cudaEventRecord(d->ev[2], d->side));
+  prep_half<R>(P, d, L, 1, d->side);
+  CK(cudaEventRecord(d->ev[5], d->side));
+  run_half<R>(*P, d, 0, L, st);
+  if (timed) CK(cudaEventRecord(d->ev[1], st));
+  prep_half<R>(P, d, L, 0, st);
+  CK(cudaStreamWaitEvent(st, d->ev[5], 0));
+  if (timed) CK(cudaEventRecord(d->ev[3], st));
+  run_core<R>(P, d, L, a, st);
+  if (timed) CK(cudaEventRecord(d->ev[4], st));
+  if (!a.out_on_device) {
+    const size_t n = L.bits_mode ? (size_t)a.n_bitstrings : ((size_t)(L.r1 - L.r0) << P->n_low);
+    CK(cudaMemcpyAsync(a.out, (char*)d->ws + L.off_out, n * sizeof(C), cudaMemcpyDeviceToHost, st));
   }
 }
 
@@ -348,32 +390,23 @@ static void run(Plan* P, const hsf_run_args& a) {
   ensure_cp(P, d, L.p0, L.p1, st);
   const bool timed = a.phase_ms != nullptr;
   try {
-    if (timed) CK(cudaEventRecord(d->ev[0], st));
-    if (P->opts.dtype == HSF_C64) {
-      run_half<float>(*P, d, 0, L, st);
-      if (timed) CK(cudaEventRecord(d->ev[1], st));
-      run_half<float>(*P, d, 1, L, st);
-      if (timed) CK(cudaEventRecord(d->ev[2], st));
-      run_sum<float>(P, d, L, a, st);
-    } else {
-      run_half<double>(*P, d, 0, L, st);
-      if (timed) CK(cudaEventRecord(d->ev[1], st));
-      run_half<double>(*P, d, 1, L, st);
-      if (timed) CK(cudaEventRecord(d->ev[2], st));
-      run_sum<double>(P, d, L, a, st);
-    }
-    if (timed) CK(cudaEventRecord(d->ev[3], st));
+    if (P->opts.dtype == HSF_C64)
+      run_all<float>(P, d, L, a, st, timed);
+    else
+      run_all<double>(P, d, L, a, st, timed);
     if (timed || !a.out_on_device) CK(cudaStreamSynchronize(st));
     if (timed) {
-      float t0, t1, t2, t3;
-      CK(cudaEventElapsedTime(&t0, d->ev[0], d->ev[1]));
-      CK(cudaEventElapsedTime(&t1, d->ev[1], d->ev[2]));
-      CK(cudaEventElapsedTime(&t2, d->ev[2], d->ev[3]));
-      CK(cudaEventElapsedTime(&t3, d->ev[0], d->ev[3]));
-      a.phase_ms[0] = t0;
-      a.phase_ms[1] = t1;
-      a.phase_ms[2] = t2;
-      a.phase_ms[3] = t3;
+      float tA, tB, tprep, tcore, ttot;
+      CK(cudaEventElapsedTime(&tA, d->ev[0], d->ev[1]));
+      CK(cudaEventElapsedTime(&tB, d->ev[0], d->ev[2]));
+      CK(cudaEventElapsedTime(&tprep, d->ev[0], d->ev[3]));
+      CK(cudaEventElapsedTime(&tcore, d->ev[3], d->ev[4]));
+      CK(cudaEventElapsedTime(&ttot, d->ev[0], d->ev[4]));
+      a.phase_ms[0] = tA;
+      a.phase_ms[1] = tB;
+      a.phase_ms[2] = tprep - std::max(tA, tB);
+      a.phase_ms[3] = tcore;
+      a.phase_ms[4] = ttot;
     }
   } catch (Error& e) {
     if (e.st == HSF_ERR_CUDA) d->sticky = true;

@@ -168,7 +168,7 @@ class Plan:
         """hsf_run(): evaluate paths [path_range) into `out`.
 
         `out` / `bitstrings` are torch tensors (device or host) or numpy arrays
-        (host).  Returns per-phase ms [simA, simB, sum, total] if `timings`."""
+        (host).  Returns per-phase ms [simA, simB, prep, core, total] if `timings`."""
         import torch
 
         def ptr(x):
@@ -183,7 +183,7 @@ class Plan:
         bp, bdev, nb = (None, False, 0) if bitstrings is None else ptr(bitstrings)
         dev = torch.cuda.current_device() if torch.cuda.is_available() else -1
         st = stream if stream is not None else (torch.cuda.current_stream().cuda_stream if torch.cuda.is_available() else None)
-        phase = (C.c_double * 4)() if timings else None
+        phase = (C.c_double * 5)() if timings else None
         a = self._args(op, odev, bp, nb, bdev, path_range, row_range, precision, st, dev,
                        C.cast(phase, C.POINTER(C.c_double)) if timings else None)
         _check(lib().hsf_run(self._h, C.byref(a)))
