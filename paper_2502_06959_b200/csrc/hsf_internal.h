@@ -64,12 +64,15 @@ struct DevOp {
   int32_t kind, k;
   int32_t q[kMaxOpQ];   // dense: tile positions; diag: half-local qubit ids
   int32_t radix;        // 1 for fixed ops
-  int32_t contiguous;   // diag: q[j] == q[0] + j  => index = (g >> q0) & mask
+  int32_t nruns;        // diag: contiguous qubit runs (1..3 => fast index), 0 => generic
+  uint8_t rshift[4];    // run r covers index bits [roff[r], roff[r]+rlen[r]) taken
+  uint8_t rlen[4];      //   from state bits [rshift[r], rshift[r]+rlen[r])
+  uint8_t roff[4];
   int32_t pad;
   int64_t div;          // factor digit = (node_global / div) % radix
   int64_t table, stride;
 };
-static_assert(sizeof(DevOp) == 96, "DevOp layout");
+static_assert(sizeof(DevOp) == 112, "DevOp layout");
 
 struct Pass {
   int t = 0;                 // tile qubits (t == m => whole state in SMEM)

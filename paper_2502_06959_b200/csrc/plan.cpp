@@ -455,7 +455,15 @@ static void fuse_segment(Plan& P, std::vector<HostOp>& seg) {
       HostOp& prev = out2.back();
       std::set<int> uni(prev.q, prev.q + prev.k);
       uni.insert(op.q, op.q + op.k);
-      if ((int)uni.size() <= kFuseDiagQ) {
+      int runs = 0;
+      {
+        int prevq = -2;
+        for (int q : uni) {
+          if (q != prevq + 1) ++runs;
+          prevq = q;
+        }
+      }
+      if ((int)uni.size() <= kFuseDiagQ && runs <= 2) {
         std::vector<int> qs(uni.begin(), uni.end());  // ascending
         const int k = (int)qs.size();
         auto Da = op_matrix(P, prev), Db = op_matrix(P, op);
@@ -554,6 +562,7 @@ static void build_half(Plan& P, int h, const std::vector<SchedItem>& order) {
   const int n_low = P.n_low;
   H.first_qubit = (h == 0) ? n_low : 0;
   H.m = (h == 0) ? P.n - n_low : n_low;
+  if (H.m > 30) fail(HSF_ERR_UNSUPPORTED, "half-states above 30 qubits are not supported (32-bit device indexing)");
   const int U = (int)P.units.size();
   // segments
   std::vector<std::vector<HostOp>> segs(U + 1);
@@ -651,8 +660,23 @@ static void build_half(Plan& P, int h, const std::vector<SchedItem>& order) {
           d.radix = 1;
           d.div = 1;
         }
-        d.contiguous = 1;
-        for (int j = 1; j < d.k; ++j) d.contiguous = d.contiguous && (d.q[j] == d.q[0] + j);
+        // contiguous runs of the diagonal's qubit list (index bit j <- q[j])
+        d.nruns = 0;
+        if (d.kind == OP_DIAG) {
+          int r = 0;
+          for (int j = 0; j < d.k;) {
+            int e = j + 1;
+            while (e < d.k && d.q[e] == d.q[e - 1] + 1) ++e;
+            if (r < 3) {
+              d.rshift[r] = (uint8_t)d.q[j];
+              d.rlen[r] = (uint8_t)(e - j);
+              d.roff[r] = (uint8_t)j;
+            }
+            ++r;
+            j = e;
+          }
+          d.nruns = (r <= 3) ? r : 0;
+        }
       }
     H.n_passes += (int)tr.passes.size();
     H.trans.push_back(std::move(tr));

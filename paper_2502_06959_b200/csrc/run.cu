@@ -102,8 +102,8 @@ struct Layout {
   bool bits_mode;
   uint64_t r0, r1;
   hsf_precision prec;
-  size_t scratch_elems = 0;    // per ping-pong buffer
-  size_t off_scratch[2] = {0, 0};
+  size_t scratch_elems[2] = {0, 0};  // per ping-pong buffer, per half
+  size_t off_scratch[2][2] = {{0, 0}, {0, 0}};  // [half][ping/pong]: the halves run concurrently
   size_t off_leaves[2] = {0, 0};
   size_t off_T[2] = {0, 0};    // transposed operands (bitstring mode)
   size_t off_bits = 0, off_out = 0, off_tc = 0;
@@ -142,11 +142,11 @@ static Layout make_layout(const Plan& P, const hsf_run_args& a, size_t elem) {
     const Half& H = P.half[h];
     const size_t st = (size_t)1 << H.m;
     for (size_t i = 0; i + 1 < H.trans.size(); ++i)
-      L.scratch_elems = std::max(L.scratch_elems, (size_t)nodes_at(P, H.trans[i].level_out, L.p0, L.p1) * st);
-  }
-  for (int b = 0; b < 2; ++b) {
-    L.off_scratch[b] = off;
-    off = align_up(off + L.scratch_elems * elem);
+      L.scratch_elems[h] = std::max(L.scratch_elems[h], (size_t)nodes_at(P, H.trans[i].level_out, L.p0, L.p1) * st);
+    for (int b = 0; b < 2; ++b) {
+      L.off_scratch[h][b] = off;
+      off = align_up(off + L.scratch_elems[h] * elem);
+    }
   }
   for (int h = 0; h < 2; ++h) {
     L.off_leaves[h] = off;
@@ -236,7 +236,7 @@ static void run_half(const Plan& P, DeviceState* d, int h, const Layout& L, cuda
   for (size_t ti = 0; ti < H.trans.size(); ++ti) {
     const Transition& tr = H.trans[ti];
     const bool last = (ti + 1 == H.trans.size());
-    void* out = ws + (last ? L.off_leaves[h] : L.off_scratch[ti & 1]);
+    void* out = ws + (last ? L.off_leaves[h] : L.off_scratch[h][ti & 1]);
     const uint64_t S_out = suffix_prod(P.ranks, tr.level_out);
     const uint64_t first_out = L.p0 / S_out;
     const uint64_t n_out = (L.p1 - 1) / S_out - first_out + 1;
@@ -258,9 +258,15 @@ static void run_half(const Plan& P, DeviceState* d, int h, const Layout& L, cuda
           if (std::find(ps.T.begin(), ps.T.end(), q) == ps.T.end()) pp.nonT[pp.n_nt++] = q;
         if (pp.n_nt > kMaxNonTile) fail(HSF_ERR_UNSUPPORTED, "half too large for the tile kernel");
       }
-      const size_t smem = (sizeof(C) << ps.t) + (ps.t < H.m ? (sizeof(long long) << (ps.t - 5)) : 0);
-      CK(cudaFuncSetAttribute(hsf_pass_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      const size_t smem = (sizeof(C) << ps.t) + (ps.t < H.m ? (sizeof(uint32_t) << (ps.t - 5)) : 0);
       const uint64_t tiles = 1ull << (H.m - ps.t);
+      // narrow levels (few CTAs) use one 1024-thread CTA per (node, tile) to
+      // shorten the dependent chain of small launches at the top of the tree
+      const bool wide = tiles * n_out < 2ull * (uint64_t)num_sms() && ps.t >= 11;
+      if (wide)
+        CK(cudaFuncSetAttribute(hsf_pass_kernel<R, kSimThreadsWide>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      else
+        CK(cudaFuncSetAttribute(hsf_pass_kernel<R, kSimThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       for (uint64_t y0 = 0; y0 < n_out; y0 += 65535) {
         const uint64_t ny = std::min<uint64_t>(65535, n_out - y0);
         pp.node_first = (long long)(first_out + y0);
@@ -280,7 +286,10 @@ static void run_half(const Plan& P, DeviceState* d, int h, const Layout& L, cuda
           pp.src_div = 1;
         }
         dim3 grid((unsigned)tiles, (unsigned)ny);
-        hsf_pass_kernel<R><<<grid, kSimThreads, smem, st>>>(pp);
+        if (wide)
+          hsf_pass_kernel<R, kSimThreadsWide><<<grid, kSimThreadsWide, smem, st>>>(pp);
+        else
+          hsf_pass_kernel<R, kSimThreads><<<grid, kSimThreads, smem, st>>>(pp);
         CK(cudaGetLastError());
       }
     }

@@ -45,8 +45,9 @@ __device__ __forceinline__ C cfma(C a, C b, C acc) {  // acc + a*b
   return acc;
 }
 
-constexpr int kSimThreads = 256;
-constexpr int kMaxNonTile = 56;
+constexpr int kSimThreads = 256;      // default CTA (3 CTAs/SM at <= 85 regs)
+constexpr int kSimThreadsWide = 1024; // narrow tree levels: one wide CTA per node
+constexpr int kMaxNonTile = 32;
 
 struct PassParams {
   const void* src;         // parent level buffer, nullptr => |0...0>
@@ -72,7 +73,6 @@ __device__ __forceinline__ void apply_dense_k(C* s, int t, const DevOp& op, cons
   int ps[K];
 #pragma unroll
   for (int j = 0; j < K; ++j) ps[j] = op.q[j];
-  // sort positions ascending for zero-bit insertion
 #pragma unroll
   for (int a = 0; a < K; ++a)
 #pragma unroll
@@ -82,16 +82,16 @@ __device__ __forceinline__ void apply_dense_k(C* s, int t, const DevOp& op, cons
         ps[a] = ps[b];
         ps[b] = tmp;
       }
-  int off[D];
-#pragma unroll
-  for (int i = 0; i < D; ++i) {
-    int o = 0;
-#pragma unroll
-    for (int j = 0; j < K; ++j) o |= ((i >> j) & 1) << op.q[j];
-    off[i] = o;
-  }
   const int ngroups = 1 << (t - K);
   if (K <= 2) {
+    int off[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      int o = 0;
+#pragma unroll
+      for (int j = 0; j < K; ++j) o |= ((i >> j) & 1) << op.q[j];
+      off[i] = o;
+    }
     C mat[D * D];
 #pragma unroll
     for (int i = 0; i < D * D; ++i) mat[i] = M[i];
@@ -119,7 +119,12 @@ __device__ __forceinline__ void apply_dense_k(C* s, int t, const DevOp& op, cons
       for (int j = 0; j < K; ++j) b = ((b >> ps[j]) << (ps[j] + 1)) | (b & ((1 << ps[j]) - 1));
       C v[D];
 #pragma unroll
-      for (int i = 0; i < D; ++i) v[i] = s[b + off[i]];
+      for (int i = 0; i < D; ++i) {
+        int o = 0;
+#pragma unroll
+        for (int j = 0; j < K; ++j) o |= ((i >> j) & 1) << op.q[j];
+        v[i] = s[b + o];
+      }
 #pragma unroll 1
       for (int i = 0; i < D; ++i) {
         C acc;
@@ -135,63 +140,116 @@ __device__ __forceinline__ void apply_dense_k(C* s, int t, const DevOp& op, cons
   }
 }
 
+// Wide dense ops (4, 5 qubits): one group of 2^K amplitudes per 2^K lanes;
+// each lane holds one input amplitude and computes one output row, the
+// other inputs arrive by warp shuffles (all reads precede the write).
+template <int K, typename C>
+__device__ __forceinline__ void apply_dense_shfl(C* s, int t, const DevOp& op, const C* __restrict__ M) {
+  constexpr int GS = 1 << K, GPW = 32 / GS;
+  int ps[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) ps[j] = op.q[j];
+#pragma unroll
+  for (int a = 0; a < K; ++a)
+#pragma unroll
+    for (int b = a + 1; b < K; ++b)
+      if (ps[b] < ps[a]) {
+        int tmp = ps[a];
+        ps[a] = ps[b];
+        ps[b] = tmp;
+      }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int sub = lane / GS, r = lane % GS;
+  int off = 0;
+#pragma unroll
+  for (int j = 0; j < K; ++j) off |= ((r >> j) & 1) << op.q[j];
+  const int ngroups = 1 << (t - K);
+  for (int g0 = wid * GPW; g0 < ngroups; g0 += nw * GPW) {
+    const int g = g0 + sub;
+    const bool ok = g < ngroups;
+    int b = ok ? g : 0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) b = ((b >> ps[j]) << (ps[j] + 1)) | (b & ((1 << ps[j]) - 1));
+    C v = s[b + off];
+    C acc;
+    acc.x = 0;
+    acc.y = 0;
+#pragma unroll 4
+    for (int j = 0; j < GS; ++j) {
+      C vj;
+      vj.x = __shfl_sync(0xffffffffu, v.x, sub * GS + j);
+      vj.y = __shfl_sync(0xffffffffu, v.y, sub * GS + j);
+      acc = cfma(__ldg(&M[r * GS + j]), vj, acc);
+    }
+    if (ok) s[b + off] = acc;
+  }
+}
+
 template <typename C>
 __device__ __forceinline__ void apply_dense(C* s, int t, const DevOp& op, const C* M) {
   switch (op.k) {
     case 1: apply_dense_k<1>(s, t, op, M); break;
     case 2: apply_dense_k<2>(s, t, op, M); break;
     case 3: apply_dense_k<3>(s, t, op, M); break;
-    case 4: apply_dense_k<4>(s, t, op, M); break;
-    case 5: apply_dense_k<5>(s, t, op, M); break;
+    case 4: apply_dense_shfl<4>(s, t, op, M); break;
+    case 5: apply_dense_shfl<5>(s, t, op, M); break;
     default: break;
   }
 }
 
-__device__ __forceinline__ long long diag_index(const DevOp& op, long long g) {
-  if (op.contiguous) return (g >> op.q[0]) & ((1ll << op.k) - 1);
-  long long idx = 0;
-  for (int j = 0; j < op.k; ++j) idx |= ((g >> op.q[j]) & 1ll) << j;
+// table index of a diagonal op: bit j <- state bit q[j]; fast path for up to
+// three contiguous runs of qubits
+__device__ __forceinline__ uint32_t diag_idx(const DevOp& d, uint32_t g) {
+  if (d.nruns == 0) {
+    uint32_t idx = 0;
+    for (int j = 0; j < d.k; ++j) idx |= ((g >> d.q[j]) & 1u) << j;
+    return idx;
+  }
+  uint32_t idx = (g >> d.rshift[0]) & ((1u << d.rlen[0]) - 1u);
+  if (d.nruns > 1) idx |= ((g >> d.rshift[1]) & ((1u << d.rlen[1]) - 1u)) << d.roff[1];
+  if (d.nruns > 2) idx |= ((g >> d.rshift[2]) & ((1u << d.rlen[2]) - 1u)) << d.roff[2];
   return idx;
 }
 
-template <typename R>
-__global__ void __launch_bounds__(kSimThreads, 2) hsf_pass_kernel(const PassParams p) {
+template <typename R, int NT>
+__global__ void __launch_bounds__(NT, (NT == 256 ? 3 : 1)) hsf_pass_kernel(const PassParams p) {
   using C = typename cplx<R>::T;
+  constexpr int CH = (NT == 256) ? 8 : 4;  // elements per thread kept in registers by diagonal sweeps
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* s = reinterpret_cast<C*>(smem_raw);
-  long long* hi_off = reinterpret_cast<long long*>(smem_raw + (sizeof(C) << p.t));
+  uint32_t* hi_off = reinterpret_cast<uint32_t*>(smem_raw + (sizeof(C) << p.t));
   __shared__ DevOp sops[32];
+  __shared__ const C* sM[32];  // per-op matrix/table pointer for this node's digit
 
-  const long long tile = blockIdx.x;
+  const uint32_t tile = blockIdx.x;
   const long long node_local = p.node_local0 + blockIdx.y;
   const long long node_g = p.node_first + blockIdx.y;
   const int nel = 1 << p.t;
   const bool whole = (p.t == p.m);
 
-  long long base = 0;
+  uint32_t base = 0;
   if (!whole) {
-    for (int j = 0; j < p.n_nt; ++j) base |= ((tile >> j) & 1ll) << p.nonT[j];
+    for (int j = 0; j < p.n_nt; ++j) base |= ((tile >> j) & 1u) << p.nonT[j];
     const int nh = 1 << p.n_hi;
-    for (int j = threadIdx.x; j < nh; j += blockDim.x) {
-      long long o = 0;
-      for (int b = 0; b < p.n_hi; ++b) o |= (long long)((j >> b) & 1) << p.T_hi[b];
+    for (int j = threadIdx.x; j < nh; j += NT) {
+      uint32_t o = 0;
+      for (int b = 0; b < p.n_hi; ++b) o |= (uint32_t)((j >> b) & 1) << p.T_hi[b];
       hi_off[j] = o;
     }
     __syncthreads();
   }
-  auto gidx_of = [&](int e) -> long long { return whole ? (long long)e : (base | (e & 31) | hi_off[e >> 5]); };
+  auto gidx_of = [&](int e) -> uint32_t { return whole ? (uint32_t)e : (base | (e & 31) | hi_off[e >> 5]); };
 
   const C* src = nullptr;
   if (p.src) {
-    long long parent = node_g / p.src_div - p.src_first;
+    const long long parent = node_g / p.src_div - p.src_first;
     src = reinterpret_cast<const C*>(p.src) + parent * p.state_elems;
   }
   C* dst = reinterpret_cast<C*>(p.dst) + node_local * p.state_elems;
   const C* coef = reinterpret_cast<const C*>(p.coef);
 
-  // load (the first output pass reads the parent; later passes are in place)
-  for (int e = threadIdx.x; e < nel; e += blockDim.x) {
-    long long g = gidx_of(e);
+  for (int e = threadIdx.x; e < nel; e += NT) {
+    const uint32_t g = gidx_of(e);
     C v;
     if (src) {
       v = src[g];
@@ -202,35 +260,36 @@ __global__ void __launch_bounds__(kSimThreads, 2) hsf_pass_kernel(const PassPara
     s[e] = v;
   }
 
-  bool need_sync = true;  // dense ops use a different thread mapping than loads
   for (int ob = 0; ob < p.n_ops; ob += 32) {
     const int cnt = min(32, p.n_ops - ob);
-    __syncthreads();  // previous chunk done with sops
-    if (threadIdx.x < cnt) sops[threadIdx.x] = p.ops[ob + threadIdx.x];
+    __syncthreads();  // previous chunk done with sops; loads/diag sweeps done
+    if (threadIdx.x < cnt) {
+      const DevOp d = p.ops[ob + threadIdx.x];
+      sops[threadIdx.x] = d;
+      const long long digit = (d.radix > 1) ? (node_g / d.div) % d.radix : 0;
+      sM[threadIdx.x] = coef + d.table + digit * d.stride;
+    }
     __syncthreads();
-    need_sync = false;
+    bool need_sync = false;
     int i = 0;
     while (i < cnt) {
-      const DevOp& op = sops[i];
-      if (op.kind == OP_DENSE) {
+      if (sops[i].kind == OP_DENSE) {
         if (need_sync) __syncthreads();
-        long long digit = (op.radix > 1) ? (node_g / op.div) % op.radix : 0;
-        apply_dense<C>(s, p.t, op, coef + op.table + digit * op.stride);
+        apply_dense<C>(s, p.t, sops[i], sM[i]);
         __syncthreads();
         need_sync = false;
         ++i;
       } else {
-        // a run of diagonal ops in one sweep (element-owner mapping); each
-        // thread keeps 8 elements in registers so the table loads of one op
-        // are 8 independent requests in flight
+        // a run of diagonal ops in one sweep; CH elements per thread stay in
+        // registers so each op's table loads are CH independent requests
         int j = i;
         while (j < cnt && sops[j].kind == OP_DIAG) ++j;
-        for (int e0 = threadIdx.x; e0 < nel; e0 += 8 * blockDim.x) {
-          C v[8];
-          long long g[8];
+        for (int e0 = threadIdx.x; e0 < nel; e0 += CH * NT) {
+          C v[CH];
+          uint32_t g[CH];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int e = e0 + u * blockDim.x;
+          for (int u = 0; u < CH; ++u) {
+            const int e = e0 + u * NT;
             if (e < nel) {
               v[u] = s[e];
               g[u] = gidx_of(e);
@@ -238,23 +297,14 @@ __global__ void __launch_bounds__(kSimThreads, 2) hsf_pass_kernel(const PassPara
           }
           for (int r = i; r < j; ++r) {
             const DevOp& d = sops[r];
-            const long long digit = (d.radix > 1) ? (node_g / d.div) % d.radix : 0;
-            const C* tab = coef + d.table + digit * d.stride;
-            if (d.contiguous) {
-              const int q0 = d.q[0];
-              const long long mask = (1ll << d.k) - 1;
+            const C* tab = sM[r];
 #pragma unroll
-              for (int u = 0; u < 8; ++u)
-                if (e0 + u * (int)blockDim.x < nel) v[u] = cmul(v[u], __ldg(&tab[(g[u] >> q0) & mask]));
-            } else {
-#pragma unroll
-              for (int u = 0; u < 8; ++u)
-                if (e0 + u * (int)blockDim.x < nel) v[u] = cmul(v[u], __ldg(&tab[diag_index(d, g[u])]));
-            }
+            for (int u = 0; u < CH; ++u)
+              if (e0 + u * NT < nel) v[u] = cmul(v[u], __ldg(&tab[diag_idx(d, g[u])]));
           }
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int e = e0 + u * blockDim.x;
+          for (int u = 0; u < CH; ++u) {
+            const int e = e0 + u * NT;
             if (e < nel) s[e] = v[u];
           }
         }
@@ -264,7 +314,7 @@ __global__ void __launch_bounds__(kSimThreads, 2) hsf_pass_kernel(const PassPara
     }
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < nel; e += blockDim.x) dst[gidx_of(e)] = s[e];
+  for (int e = threadIdx.x; e < nel; e += NT) dst[gidx_of(e)] = s[e];
 }
 
 }  // namespace hsf
