@@ -44,7 +44,15 @@ struct Unit {
 };
 
 // ------------------------------------------------------------ device ops
-enum OpKind : int32_t { OP_DENSE = 0, OP_DIAG = 1 };
+// OP_DENSE : SMEM sweep of a dense k-qubit op (q = tile positions)
+// OP_DIAG  : diagonal op, elementwise (q = half-local qubits, any position)
+// OP_RPASS : register pass header: q[0..3] = tile positions of the 4 register
+//            qubits, k = number of following OP_R1 / OP_DIAG ops applied to
+//            2^4 amplitudes held in registers per thread
+// OP_R1    : 1-qubit dense op inside a register pass, q[0] = register slot
+enum OpKind : int32_t { OP_DENSE = 0, OP_DIAG = 1, OP_RPASS = 2, OP_R1 = 3 };
+constexpr int kRegQ = 4;          // register qubits per pass (16 amplitudes/thread)
+constexpr int kMaxPassOps = 128;  // ops per kernel pass (all staged in SMEM)
 constexpr int kMaxOpQ = 13;      // widest diagonal op (2^13 entries)
 constexpr int kMaxDenseQ = 5;    // widest dense op in the SMEM kernels
 

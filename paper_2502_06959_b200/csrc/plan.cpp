@@ -557,6 +557,88 @@ static void plan_passes(Half& H, Transition& tr, int64_t ob, int64_t oe, int t) 
   } while (!pending.empty());
 }
 
+// Register passes: maximal runs of 1-qubit dense ops on at most kRegQ distinct
+// tile qubits, interleaved with diagonal ops, become one OP_RPASS whose ops the
+// kernel applies to 2^kRegQ amplitudes kept in registers per thread (one SMEM
+// round trip for the whole run instead of one sweep + barrier per gate).
+static std::vector<DevOp> regpass_rewrite(const std::vector<DevOp>& ops, int t) {
+  if (t < kRegQ) return ops;
+  std::vector<DevOp> out;
+  int hdr = -1;
+  std::vector<int> RS;
+  auto close = [&]() {
+    if (hdr < 0) return;
+    DevOp& h = out[hdr];
+    for (int q = 0; q < t && (int)RS.size() < kRegQ; ++q)
+      if (std::find(RS.begin(), RS.end(), q) == RS.end()) RS.push_back(q);
+    h = DevOp{};
+    h.kind = OP_RPASS;
+    h.k = (int)out.size() - hdr - 1;
+    for (int j = 0; j < kRegQ; ++j) h.q[j] = RS[j];
+    h.radix = 1;
+    h.div = 1;
+    hdr = -1;
+    RS.clear();
+  };
+  for (const DevOp& d : ops) {
+    if (hdr >= 0 && (int)out.size() - hdr >= kMaxPassOps / 2) close();
+    if (d.kind == OP_DENSE && d.k == 1) {
+      const int pos = d.q[0];
+      auto it = std::find(RS.begin(), RS.end(), pos);
+      if (hdr >= 0 && it == RS.end() && (int)RS.size() == kRegQ) close();
+      if (hdr < 0) {
+        hdr = (int)out.size();
+        out.push_back(DevOp{});
+      }
+      it = std::find(RS.begin(), RS.end(), pos);
+      int slot = (int)(it - RS.begin());
+      if (it == RS.end()) RS.push_back(pos);
+      DevOp r = d;
+      r.kind = OP_R1;
+      r.q[0] = slot;
+      out.push_back(r);
+    } else if (d.kind == OP_DIAG) {
+      out.push_back(d);
+    } else {
+      close();
+      out.push_back(d);
+    }
+  }
+  close();
+  return out;
+}
+
+static void finalize_half(Half& H) {
+  std::vector<DevOp> out;
+  H.n_passes = 0;
+  for (auto& tr : H.trans) {
+    std::vector<Pass> np;
+    for (const Pass& p : tr.passes) {
+      std::vector<DevOp> ops(H.dev_ops.begin() + p.op_begin, H.dev_ops.begin() + p.op_end);
+      std::vector<DevOp> rw = regpass_rewrite(ops, p.t);
+      // split into kernel passes of <= kMaxPassOps ops without cutting a register pass
+      size_t i = 0;
+      do {
+        Pass q = p;
+        q.op_begin = (int64_t)out.size();
+        size_t n = 0;
+        while (i < rw.size()) {
+          size_t w = (rw[i].kind == OP_RPASS) ? (size_t)rw[i].k + 1 : 1;
+          if (n + w > (size_t)kMaxPassOps && n > 0) break;
+          for (size_t j = 0; j < w; ++j) out.push_back(rw[i + j]);
+          n += w;
+          i += w;
+        }
+        q.op_end = (int64_t)out.size();
+        np.push_back(q);
+      } while (i < rw.size());
+    }
+    tr.passes.swap(np);
+    H.n_passes += (int)tr.passes.size();
+  }
+  H.dev_ops.swap(out);
+}
+
 static void build_half(Plan& P, int h, const std::vector<SchedItem>& order) {
   Half& H = P.half[h];
   const int n_low = P.n_low;
@@ -678,10 +760,10 @@ static void build_half(Plan& P, int h, const std::vector<SchedItem>& order) {
           d.nruns = (r <= 3) ? r : 0;
         }
       }
-    H.n_passes += (int)tr.passes.size();
     H.trans.push_back(std::move(tr));
     prev = L;
   }
+  finalize_half(H);
 }
 
 static uint64_t fnv(uint64_t h, const void* p, size_t n) {

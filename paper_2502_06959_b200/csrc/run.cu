@@ -258,7 +258,9 @@ static void run_half(const Plan& P, DeviceState* d, int h, const Layout& L, cuda
           if (std::find(ps.T.begin(), ps.T.end(), q) == ps.T.end()) pp.nonT[pp.n_nt++] = q;
         if (pp.n_nt > kMaxNonTile) fail(HSF_ERR_UNSUPPORTED, "half too large for the tile kernel");
       }
-      const size_t smem = (sizeof(C) << ps.t) + (ps.t < H.m ? (sizeof(uint32_t) << (ps.t - 5)) : 0);
+      const int n_ops = (int)(ps.op_end - ps.op_begin);
+      size_t smem = (sizeof(C) << ps.t) + (ps.t < H.m ? (sizeof(uint32_t) << (ps.t - 5)) : 0);
+      smem = ((smem + 15) & ~(size_t)15) + (size_t)n_ops * (sizeof(DevOp) + sizeof(void*));
       const uint64_t tiles = 1ull << (H.m - ps.t);
       // narrow levels (few CTAs) use one 1024-thread CTA per (node, tile) to
       // shorten the dependent chain of small launches at the top of the tree

@@ -46,7 +46,7 @@ __device__ __forceinline__ C cfma(C a, C b, C acc) {  // acc + a*b
 }
 
 constexpr int kSimThreads = 256;      // default CTA (3 CTAs/SM at <= 85 regs)
-constexpr int kSimThreadsWide = 1024; // narrow tree levels: one wide CTA per node
+constexpr int kSimThreadsWide = 512;  // narrow tree levels: one wide CTA per node
 constexpr int kMaxNonTile = 32;
 
 struct PassParams {
@@ -211,21 +211,64 @@ __device__ __forceinline__ uint32_t diag_idx(const DevOp& d, uint32_t g) {
   return idx;
 }
 
+// Branch-free two-run index in registers (runs beyond the second use the
+// generic path).
+struct DiagIdx {
+  uint32_t s0, m0, s1, m1, o1;
+  bool slow;
+  __device__ __forceinline__ void load(const DevOp& d) {
+    slow = d.nruns == 0 || d.nruns > 2;
+    s0 = d.rshift[0];
+    m0 = (1u << d.rlen[0]) - 1u;
+    s1 = d.nruns > 1 ? d.rshift[1] : 0u;
+    m1 = d.nruns > 1 ? (1u << d.rlen[1]) - 1u : 0u;
+    o1 = d.nruns > 1 ? d.roff[1] : 0u;
+  }
+  __device__ __forceinline__ uint32_t operator()(const DevOp& d, uint32_t g) const {
+    if (slow) return diag_idx(d, g);
+    return ((g >> s0) & m0) | (((g >> s1) & m1) << o1);
+  }
+};
+
+template <int J, typename C>
+__device__ __forceinline__ void reg_apply1(C (&v)[16], const C m00, const C m01, const C m10, const C m11) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    if (i & (1 << J)) continue;
+    const C a = v[i], b = v[i | (1 << J)];
+    C x, y;
+    x.x = 0;
+    x.y = 0;
+    y = x;
+    x = cfma(m00, a, x);
+    x = cfma(m01, b, x);
+    y = cfma(m10, a, y);
+    y = cfma(m11, b, y);
+    v[i] = x;
+    v[i | (1 << J)] = y;
+  }
+}
+
 template <typename R, int NT>
-__global__ void __launch_bounds__(NT, (NT == 256 ? 3 : 1)) hsf_pass_kernel(const PassParams p) {
+__global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) hsf_pass_kernel(const PassParams p) {
   using C = typename cplx<R>::T;
-  constexpr int CH = (NT == 256) ? 8 : 4;  // elements per thread kept in registers by diagonal sweeps
+  constexpr int CH = (NT == 256) ? 8 : 4;  // elements per thread in registers for diagonal sweeps
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* s = reinterpret_cast<C*>(smem_raw);
-  uint32_t* hi_off = reinterpret_cast<uint32_t*>(smem_raw + (sizeof(C) << p.t));
-  __shared__ DevOp sops[32];
-  __shared__ const C* sM[32];  // per-op matrix/table pointer for this node's digit
+  size_t off = sizeof(C) << p.t;
+  uint32_t* hi_off = reinterpret_cast<uint32_t*>(smem_raw + off);
+  off += (p.t < p.m) ? (sizeof(uint32_t) << (p.t - 5)) : 0;
+  off = (off + 15) & ~(size_t)15;
+  DevOp* sops = reinterpret_cast<DevOp*>(smem_raw + off);
+  off += sizeof(DevOp) * p.n_ops;
+  const C** sM = reinterpret_cast<const C**>(smem_raw + off);  // per-op matrix for this node's digit
 
   const uint32_t tile = blockIdx.x;
   const long long node_local = p.node_local0 + blockIdx.y;
   const long long node_g = p.node_first + blockIdx.y;
   const int nel = 1 << p.t;
   const bool whole = (p.t == p.m);
+  const C* coef = reinterpret_cast<const C*>(p.coef);
 
   uint32_t base = 0;
   if (!whole) {
@@ -236,8 +279,14 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 3 : 1)) hsf_pass_kernel(const
       for (int b = 0; b < p.n_hi; ++b) o |= (uint32_t)((j >> b) & 1) << p.T_hi[b];
       hi_off[j] = o;
     }
-    __syncthreads();
   }
+  for (int i = threadIdx.x; i < p.n_ops; i += NT) {
+    const DevOp d = p.ops[i];
+    sops[i] = d;
+    const long long digit = (d.radix > 1) ? (node_g / d.div) % d.radix : 0;
+    sM[i] = coef + d.table + digit * d.stride;
+  }
+  __syncthreads();
   auto gidx_of = [&](int e) -> uint32_t { return whole ? (uint32_t)e : (base | (e & 31) | hi_off[e >> 5]); };
 
   const C* src = nullptr;
@@ -246,7 +295,6 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 3 : 1)) hsf_pass_kernel(const
     src = reinterpret_cast<const C*>(p.src) + parent * p.state_elems;
   }
   C* dst = reinterpret_cast<C*>(p.dst) + node_local * p.state_elems;
-  const C* coef = reinterpret_cast<const C*>(p.coef);
 
   for (int e = threadIdx.x; e < nel; e += NT) {
     const uint32_t g = gidx_of(e);
@@ -260,57 +308,121 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 3 : 1)) hsf_pass_kernel(const
     s[e] = v;
   }
 
-  for (int ob = 0; ob < p.n_ops; ob += 32) {
-    const int cnt = min(32, p.n_ops - ob);
-    __syncthreads();  // previous chunk done with sops; loads/diag sweeps done
-    if (threadIdx.x < cnt) {
-      const DevOp d = p.ops[ob + threadIdx.x];
-      sops[threadIdx.x] = d;
-      const long long digit = (d.radix > 1) ? (node_g / d.div) % d.radix : 0;
-      sM[threadIdx.x] = coef + d.table + digit * d.stride;
-    }
-    __syncthreads();
-    bool need_sync = false;
-    int i = 0;
-    while (i < cnt) {
-      if (sops[i].kind == OP_DENSE) {
-        if (need_sync) __syncthreads();
-        apply_dense<C>(s, p.t, sops[i], sM[i]);
-        __syncthreads();
-        need_sync = false;
-        ++i;
-      } else {
-        // a run of diagonal ops in one sweep; CH elements per thread stay in
-        // registers so each op's table loads are CH independent requests
-        int j = i;
-        while (j < cnt && sops[j].kind == OP_DIAG) ++j;
-        for (int e0 = threadIdx.x; e0 < nel; e0 += CH * NT) {
-          C v[CH];
-          uint32_t g[CH];
+  // mapping discipline: loads, stores and standalone diagonal sweeps use the
+  // element-owner mapping (e % NT); dense sweeps and register passes use group
+  // mappings and are bracketed by barriers
+  int i = 0;
+  while (i < p.n_ops) {
+    const int kind = sops[i].kind;
+    if (kind == OP_DENSE) {
+      __syncthreads();
+      apply_dense<C>(s, p.t, sops[i], sM[i]);
+      __syncthreads();
+      ++i;
+    } else if (kind == OP_RPASS) {
+      const DevOp& h = sops[i];
+      const int n = h.k;
+      int ps[kRegQ];
+      uint32_t ebit[kRegQ], gbit[kRegQ];  // tile-index and state-index bit of each register qubit
 #pragma unroll
-          for (int u = 0; u < CH; ++u) {
-            const int e = e0 + u * NT;
-            if (e < nel) {
-              v[u] = s[e];
-              g[u] = gidx_of(e);
+      for (int j = 0; j < kRegQ; ++j) {
+        const int pos = h.q[j];
+        ps[j] = pos;
+        ebit[j] = 1u << pos;
+        gbit[j] = 1u << (whole || pos < 5 ? pos : p.T_hi[pos - 5]);
+      }
+#pragma unroll
+      for (int a = 0; a < kRegQ; ++a)
+#pragma unroll
+        for (int b = a + 1; b < kRegQ; ++b)
+          if (ps[b] < ps[a]) {
+            int tmp = ps[a];
+            ps[a] = ps[b];
+            ps[b] = tmp;
+          }
+      __syncthreads();
+      const int ngr = 1 << (p.t - kRegQ);
+      for (int gi = threadIdx.x; gi < ngr; gi += NT) {
+        int b = gi;
+#pragma unroll
+        for (int j = 0; j < kRegQ; ++j) b = ((b >> ps[j]) << (ps[j] + 1)) | (b & ((1 << ps[j]) - 1));
+        const uint32_t gb = gidx_of(b);
+        C v[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          uint32_t e = (uint32_t)b;
+#pragma unroll
+          for (int j = 0; j < kRegQ; ++j)
+            if ((k >> j) & 1) e |= ebit[j];
+          v[k] = s[e];
+        }
+        for (int r = i + 1; r <= i + n; ++r) {
+          const DevOp& d = sops[r];
+          const C* M = sM[r];
+          if (d.kind == OP_R1) {
+            const C m00 = M[0], m01 = M[1], m10 = M[2], m11 = M[3];
+            switch (d.q[0]) {
+              case 0: reg_apply1<0>(v, m00, m01, m10, m11); break;
+              case 1: reg_apply1<1>(v, m00, m01, m10, m11); break;
+              case 2: reg_apply1<2>(v, m00, m01, m10, m11); break;
+              default: reg_apply1<3>(v, m00, m01, m10, m11); break;
+            }
+          } else {
+            DiagIdx di;
+            di.load(d);
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              uint32_t g = gb;
+#pragma unroll
+              for (int j = 0; j < kRegQ; ++j)
+                if ((k >> j) & 1) g |= gbit[j];
+              v[k] = cmul(v[k], __ldg(&M[di(d, g)]));
             }
           }
-          for (int r = i; r < j; ++r) {
-            const DevOp& d = sops[r];
-            const C* tab = sM[r];
+        }
 #pragma unroll
-            for (int u = 0; u < CH; ++u)
-              if (e0 + u * NT < nel) v[u] = cmul(v[u], __ldg(&tab[diag_idx(d, g[u])]));
-          }
+        for (int k = 0; k < 16; ++k) {
+          uint32_t e = (uint32_t)b;
 #pragma unroll
-          for (int u = 0; u < CH; ++u) {
-            const int e = e0 + u * NT;
-            if (e < nel) s[e] = v[u];
+          for (int j = 0; j < kRegQ; ++j)
+            if ((k >> j) & 1) e |= ebit[j];
+          s[e] = v[k];
+        }
+      }
+      __syncthreads();
+      i += n + 1;
+    } else {
+      // standalone run of diagonal ops, element-owner mapping, CH elements
+      // per thread in registers (CH independent table loads per op)
+      int j = i;
+      while (j < p.n_ops && sops[j].kind == OP_DIAG) ++j;
+      for (int e0 = threadIdx.x; e0 < nel; e0 += CH * NT) {
+        C v[CH];
+        uint32_t g[CH];
+#pragma unroll
+        for (int u = 0; u < CH; ++u) {
+          const int e = e0 + u * NT;
+          if (e < nel) {
+            v[u] = s[e];
+            g[u] = gidx_of(e);
           }
         }
-        need_sync = true;
-        i = j;
+        for (int r = i; r < j; ++r) {
+          const DevOp& d = sops[r];
+          const C* tab = sM[r];
+          DiagIdx di;
+          di.load(d);
+#pragma unroll
+          for (int u = 0; u < CH; ++u)
+            if (e0 + u * NT < nel) v[u] = cmul(v[u], __ldg(&tab[di(d, g[u])]));
+        }
+#pragma unroll
+        for (int u = 0; u < CH; ++u) {
+          const int e = e0 + u * NT;
+          if (e < nel) s[e] = v[u];
+        }
       }
+      i = j;
     }
   }
   __syncthreads();
