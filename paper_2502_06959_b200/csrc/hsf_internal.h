@@ -53,6 +53,8 @@ struct Unit {
 enum OpKind : int32_t { OP_DENSE = 0, OP_DIAG = 1, OP_RPASS = 2, OP_R1 = 3 };
 constexpr int kRegQ = 4;          // register qubits per pass (16 amplitudes/thread)
 constexpr int kMaxPassOps = 128;  // ops per kernel pass (all staged in SMEM)
+constexpr int kSmemTableQ = 8;     // diag tables with <= 2^8 entries are staged in SMEM
+constexpr int kSmemTableBytes = 48 * 1024;  // per-pass cap on staged tables
 constexpr int kMaxOpQ = 13;      // widest diagonal op (2^13 entries)
 constexpr int kMaxDenseQ = 5;    // widest dense op in the SMEM kernels
 
@@ -76,7 +78,8 @@ struct DevOp {
   uint8_t rshift[4];    // run r covers index bits [roff[r], roff[r]+rlen[r]) taken
   uint8_t rlen[4];      //   from state bits [rshift[r], rshift[r]+rlen[r])
   uint8_t roff[4];
-  int32_t pad;
+  int32_t soff;         // diag: element offset of this op's table in the pass's SMEM
+                        // table area, -1 => read from global (L2)
   int64_t div;          // factor digit = (node_global / div) % radix
   int64_t table, stride;
 };
@@ -86,6 +89,7 @@ struct Pass {
   int t = 0;                 // tile qubits (t == m => whole state in SMEM)
   std::vector<int> T;        // T[i] = half qubit of tile position i
   int64_t op_begin = 0, op_end = 0;  // into Half::dev_ops
+  int64_t tbl_elems = 0;             // SMEM table area (complex elements)
 };
 
 struct Transition {

@@ -608,7 +608,7 @@ static std::vector<DevOp> regpass_rewrite(const std::vector<DevOp>& ops, int t) 
   return out;
 }
 
-static void finalize_half(Half& H) {
+static void finalize_half(Half& H, size_t elem_bytes) {
   std::vector<DevOp> out;
   H.n_passes = 0;
   for (auto& tr : H.trans) {
@@ -630,6 +630,18 @@ static void finalize_half(Half& H) {
           i += w;
         }
         q.op_end = (int64_t)out.size();
+        // stage small diagonal tables of this pass in SMEM (bank-spread LDS
+        // gathers instead of scattered L1 wavefronts)
+        q.tbl_elems = 0;
+        for (int64_t oi = q.op_begin; oi < q.op_end; ++oi) {
+          DevOp& d = out[oi];
+          d.soff = -1;
+          if (d.kind == OP_DIAG && d.k <= kSmemTableQ &&
+              (size_t)(q.tbl_elems + (1 << d.k)) * elem_bytes <= (size_t)kSmemTableBytes) {
+            d.soff = (int32_t)q.tbl_elems;
+            q.tbl_elems += 1 << d.k;
+          }
+        }
         np.push_back(q);
       } while (i < rw.size());
     }
@@ -763,7 +775,7 @@ static void build_half(Plan& P, int h, const std::vector<SchedItem>& order) {
     H.trans.push_back(std::move(tr));
     prev = L;
   }
-  finalize_half(H);
+  finalize_half(H, P.opts.dtype == HSF_C64 ? 8 : 16);
 }
 
 static uint64_t fnv(uint64_t h, const void* p, size_t n) {

@@ -261,6 +261,8 @@ static void run_half(const Plan& P, DeviceState* d, int h, const Layout& L, cuda
       const int n_ops = (int)(ps.op_end - ps.op_begin);
       size_t smem = (sizeof(C) << ps.t) + (ps.t < H.m ? (sizeof(uint32_t) << (ps.t - 5)) : 0);
       smem = ((smem + 15) & ~(size_t)15) + (size_t)n_ops * (sizeof(DevOp) + sizeof(void*));
+      smem = ((smem + 15) & ~(size_t)15) + (size_t)ps.tbl_elems * sizeof(C);
+      pp.tbl_elems = (int)ps.tbl_elems;
       const uint64_t tiles = 1ull << (H.m - ps.t);
       // narrow levels (few CTAs) use one 1024-thread CTA per (node, tile) to
       // shorten the dependent chain of small launches at the top of the tree

@@ -65,6 +65,7 @@ struct PassParams {
   long long node_local0;   // local output-node index of blockIdx.y == 0
   long long src_first;     // global index of the first node of the input level
   long long src_div;       // parent = node_global / src_div
+  int tbl_elems;           // SMEM diagonal-table area (complex elements)
 };
 
 template <int K, typename C>
@@ -262,6 +263,9 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) hsf_pass_kernel(const
   DevOp* sops = reinterpret_cast<DevOp*>(smem_raw + off);
   off += sizeof(DevOp) * p.n_ops;
   const C** sM = reinterpret_cast<const C**>(smem_raw + off);  // per-op matrix for this node's digit
+  off += sizeof(void*) * p.n_ops;
+  off = (off + 15) & ~(size_t)15;
+  C* stab = reinterpret_cast<C*>(smem_raw + off);  // staged diagonal tables
 
   const uint32_t tile = blockIdx.x;
   const long long node_local = p.node_local0 + blockIdx.y;
@@ -284,9 +288,21 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) hsf_pass_kernel(const
     const DevOp d = p.ops[i];
     sops[i] = d;
     const long long digit = (d.radix > 1) ? (node_g / d.div) % d.radix : 0;
-    sM[i] = coef + d.table + digit * d.stride;
+    sM[i] = (d.kind == OP_DIAG && d.soff >= 0) ? stab + d.soff : coef + d.table + digit * d.stride;
   }
   __syncthreads();
+  if (p.tbl_elems > 0) {
+    // stage this node's digit-resolved small diagonal tables (one warp per op)
+    const int lane = threadIdx.x & 31;
+    for (int i = threadIdx.x >> 5; i < p.n_ops; i += NT / 32) {
+      const DevOp& d = sops[i];
+      if (d.kind != OP_DIAG || d.soff < 0) continue;
+      const long long digit = (d.radix > 1) ? (node_g / d.div) % d.radix : 0;
+      const C* g = coef + d.table + digit * d.stride;
+      for (int e = lane; e < (1 << d.k); e += 32) stab[d.soff + e] = __ldg(&g[e]);
+    }
+    __syncthreads();
+  }
   auto gidx_of = [&](int e) -> uint32_t { return whole ? (uint32_t)e : (base | (e & 31) | hi_off[e >> 5]); };
 
   const C* src = nullptr;
@@ -376,7 +392,7 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) hsf_pass_kernel(const
 #pragma unroll
               for (int j = 0; j < kRegQ; ++j)
                 if ((k >> j) & 1) g |= gbit[j];
-              v[k] = cmul(v[k], __ldg(&M[di(d, g)]));
+              v[k] = cmul(v[k], M[di(d, g)]);
             }
           }
         }
@@ -414,7 +430,7 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) hsf_pass_kernel(const
           di.load(d);
 #pragma unroll
           for (int u = 0; u < CH; ++u)
-            if (e0 + u * NT < nel) v[u] = cmul(v[u], __ldg(&tab[di(d, g[u])]));
+            if (e0 + u * NT < nel) v[u] = cmul(v[u], tab[di(d, g[u])]);
         }
 #pragma unroll
         for (int u = 0; u < CH; ++u) {
