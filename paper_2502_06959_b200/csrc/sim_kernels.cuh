@@ -45,6 +45,24 @@ __device__ __forceinline__ C cfma(C a, C b, C acc) {  // acc + a*b
   return acc;
 }
 
+// two consecutive amplitudes (16 B for complex64: one LDG.128 / STG.128)
+__device__ __forceinline__ void ld2(const float2* p, float2& a, float2& b) {
+  const float4 x = *reinterpret_cast<const float4*>(p);
+  a = make_float2(x.x, x.y);
+  b = make_float2(x.z, x.w);
+}
+__device__ __forceinline__ void ld2(const double2* p, double2& a, double2& b) {
+  a = p[0];
+  b = p[1];
+}
+__device__ __forceinline__ void st2(float2* p, float2 a, float2 b) {
+  *reinterpret_cast<float4*>(p) = make_float4(a.x, a.y, b.x, b.y);
+}
+__device__ __forceinline__ void st2(double2* p, double2 a, double2 b) {
+  p[0] = a;
+  p[1] = b;
+}
+
 constexpr int kSimThreads = 256;      // default CTA (3 CTAs/SM at <= 85 regs)
 constexpr int kSimThreadsWide = 512;  // narrow tree levels: one wide CTA per node
 constexpr int kMaxNonTile = 32;
@@ -312,16 +330,36 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) hsf_pass_kernel(const
   }
   C* dst = reinterpret_cast<C*>(p.dst) + node_local * p.state_elems;
 
-  for (int e = threadIdx.x; e < nel; e += NT) {
-    const uint32_t g = gidx_of(e);
-    C v;
-    if (src) {
-      v = src[g];
-    } else {
-      v.x = (g == 0) ? R(1) : R(0);
-      v.y = R(0);
+  // load: pairs (e, e+1) are contiguous in global memory (tile position 0 is
+  // qubit 0), so each thread moves 2 amplitudes per request and keeps LB
+  // requests in flight
+  if (src) {
+    constexpr int LB = 4;
+    for (int e0 = 2 * threadIdx.x; e0 < nel; e0 += 2 * NT * LB) {
+      C a[LB], b[LB];
+#pragma unroll
+      for (int u = 0; u < LB; ++u) {
+        const int e = e0 + 2 * NT * u;
+        if (e < nel) {
+          ld2(src + gidx_of(e), a[u], b[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < LB; ++u) {
+        const int e = e0 + 2 * NT * u;
+        if (e < nel) {
+          s[e] = a[u];
+          s[e + 1] = b[u];
+        }
+      }
     }
-    s[e] = v;
+  } else {
+    for (int e = threadIdx.x; e < nel; e += NT) {
+      C v;
+      v.x = (gidx_of(e) == 0) ? R(1) : R(0);
+      v.y = R(0);
+      s[e] = v;
+    }
   }
 
   // mapping discipline: loads, stores and standalone diagonal sweeps use the
@@ -442,7 +480,9 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) hsf_pass_kernel(const
     }
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < nel; e += NT) dst[gidx_of(e)] = s[e];
+  for (int e = 2 * threadIdx.x; e < nel; e += 2 * NT) {
+    st2(dst + gidx_of(e), s[e], s[e + 1]);
+  }
 }
 
 }  // namespace hsf

@@ -1,7 +1,7 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests/test_gpu_parity.py -q --timeout 300 -rf > gpurun_out/gpu_tests.log 2>&1
-timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench.log 2>&1
-timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/plain.log 2>&1 && \
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches.csv \
-  python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
-tail -3 gpurun_out/gpu_tests.log; tail -c 1200 gpurun_out/bench.log
+timeout 300 python scripts/prof_once.py c2 > gpurun_out/prof_plain.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"hsf_pass" --launch-skip 11 --launch-count 2 \
+  -o gpurun_out/prof_qft2 python scripts/prof_once.py c2 > gpurun_out/ncu_full.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"hsf_pass" --launch-skip 23 --launch-count 1 \
+  -o gpurun_out/prof_alev python scripts/prof_once.py c2 > gpurun_out/ncu_full2.log 2>&1
+tail -2 gpurun_out/ncu_full.log
