@@ -362,9 +362,11 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) hsf_pass_kernel(const
     }
   }
 
-  // mapping discipline: loads, stores and standalone diagonal sweeps use the
-  // element-owner mapping (e % NT); dense sweeps and register passes use group
-  // mappings and are bracketed by barriers
+  __syncthreads();  // the pair-mapped load differs from every op mapping below
+
+  // mapping discipline: standalone diagonal sweeps use the element-owner
+  // mapping (e % NT); dense sweeps and register passes use group mappings and
+  // are bracketed by barriers; the final store is pair-mapped after a barrier
   int i = 0;
   while (i < p.n_ops) {
     const int kind = sops[i].kind;
