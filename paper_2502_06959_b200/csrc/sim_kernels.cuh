@@ -424,16 +424,32 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) hsf_pass_kernel(const
               default: reg_apply1<3>(v, m00, m01, m10, m11); break;
             }
           } else {
+            // 16 independent table reads issued back to back, then applied
             DiagIdx di;
             di.load(d);
+            C tv[16];
+            if (d.soff >= 0) {
+              const C* T = stab + d.soff;  // shared-memory table (LDS)
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
-              uint32_t g = gb;
+              for (int k = 0; k < 16; ++k) {
+                uint32_t g = gb;
 #pragma unroll
-              for (int j = 0; j < kRegQ; ++j)
-                if ((k >> j) & 1) g |= gbit[j];
-              v[k] = cmul(v[k], M[di(d, g)]);
+                for (int j = 0; j < kRegQ; ++j)
+                  if ((k >> j) & 1) g |= gbit[j];
+                tv[k] = T[di(d, g)];
+              }
+            } else {
+#pragma unroll
+              for (int k = 0; k < 16; ++k) {
+                uint32_t g = gb;
+#pragma unroll
+                for (int j = 0; j < kRegQ; ++j)
+                  if ((k >> j) & 1) g |= gbit[j];
+                tv[k] = __ldg(&M[di(d, g)]);
+              }
             }
+#pragma unroll
+            for (int k = 0; k < 16; ++k) v[k] = cmul(v[k], tv[k]);
           }
         }
 #pragma unroll
@@ -465,12 +481,20 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) hsf_pass_kernel(const
         }
         for (int r = i; r < j; ++r) {
           const DevOp& d = sops[r];
-          const C* tab = sM[r];
           DiagIdx di;
           di.load(d);
+          C tv[CH];
+          if (d.soff >= 0) {
+            const C* T = stab + d.soff;
 #pragma unroll
-          for (int u = 0; u < CH; ++u)
-            if (e0 + u * NT < nel) v[u] = cmul(v[u], tab[di(d, g[u])]);
+            for (int u = 0; u < CH; ++u) tv[u] = T[(e0 + u * NT < nel) ? di(d, g[u]) : 0];
+          } else {
+            const C* T = sM[r];
+#pragma unroll
+            for (int u = 0; u < CH; ++u) tv[u] = __ldg(&T[(e0 + u * NT < nel) ? di(d, g[u]) : 0]);
+          }
+#pragma unroll
+          for (int u = 0; u < CH; ++u) v[u] = cmul(v[u], tv[u]);
         }
 #pragma unroll
         for (int u = 0; u < CH; ++u) {
