@@ -102,7 +102,7 @@ __device__ __forceinline__ void apply_dense_k(C* s, int t, const DevOp& op, cons
         ps[b] = tmp;
       }
   const int ngroups = 1 << (t - K);
-  if (K <= 2) {
+  if (K == 1) {
     int off[D];
 #pragma unroll
     for (int i = 0; i < D; ++i) {
@@ -269,7 +269,7 @@ __device__ __forceinline__ void reg_apply1(C (&v)[16], const C m00, const C m01,
 }
 
 template <typename R, int NT>
-__global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) hsf_pass_kernel(const PassParams p) {
+__global__ void __launch_bounds__(NT, (NT == 256 ? 3 : 1)) hsf_pass_kernel(const PassParams p) {
   using C = typename cplx<R>::T;
   constexpr int CH = (NT == 256) ? 8 : 4;  // elements per thread in registers for diagonal sweeps
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -427,29 +427,23 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 2 : 1)) hsf_pass_kernel(const
             // 16 independent table reads issued back to back, then applied
             DiagIdx di;
             di.load(d);
-            C tv[16];
-            if (d.soff >= 0) {
-              const C* T = stab + d.soff;  // shared-memory table (LDS)
+            const C* T = (d.soff >= 0) ? stab + d.soff : M;
+            const bool sh = d.soff >= 0;
 #pragma unroll
-              for (int k = 0; k < 16; ++k) {
+            for (int hk = 0; hk < 16; hk += 8) {
+              C tv[8];
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
                 uint32_t g = gb;
 #pragma unroll
                 for (int j = 0; j < kRegQ; ++j)
-                  if ((k >> j) & 1) g |= gbit[j];
-                tv[k] = T[di(d, g)];
+                  if (((hk + k) >> j) & 1) g |= gbit[j];
+                const uint32_t x = di(d, g);
+                tv[k] = sh ? T[x] : __ldg(&T[x]);
               }
-            } else {
 #pragma unroll
-              for (int k = 0; k < 16; ++k) {
-                uint32_t g = gb;
-#pragma unroll
-                for (int j = 0; j < kRegQ; ++j)
-                  if ((k >> j) & 1) g |= gbit[j];
-                tv[k] = __ldg(&M[di(d, g)]);
-              }
+              for (int k = 0; k < 8; ++k) v[hk + k] = cmul(v[hk + k], tv[k]);
             }
-#pragma unroll
-            for (int k = 0; k < 16; ++k) v[k] = cmul(v[k], tv[k]);
           }
         }
 #pragma unroll
