@@ -90,6 +90,7 @@ struct Pass {
   std::vector<int> T;        // T[i] = half qubit of tile position i
   int64_t op_begin = 0, op_end = 0;  // into Half::dev_ops
   int64_t tbl_elems = 0;             // SMEM table area (complex elements)
+  bool heavy = false;                // needs register passes / 3..5-qubit dense ops
 };
 
 struct Transition {

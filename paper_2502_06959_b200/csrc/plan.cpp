@@ -15,6 +15,8 @@
 //      (P:282), path-tree levels, SMEM tile passes
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -568,6 +570,21 @@ static std::vector<DevOp> regpass_rewrite(const std::vector<DevOp>& ops, int t) 
   std::vector<int> RS;
   auto close = [&]() {
     if (hdr < 0) return;
+    int n_r1 = 0;
+    for (size_t j = hdr + 1; j < out.size(); ++j) n_r1 += out[j].kind == OP_R1;
+    if (n_r1 < 2) {
+      // a single 1-qubit gate: a plain SMEM sweep is cheaper than a register
+      // pass and keeps the pass on the light kernel variant
+      for (size_t j = hdr + 1; j < out.size(); ++j)
+        if (out[j].kind == OP_R1) {
+          out[j].kind = OP_DENSE;
+          out[j].q[0] = RS[out[j].q[0]];
+        }
+      out.erase(out.begin() + hdr);
+      hdr = -1;
+      RS.clear();
+      return;
+    }
     DevOp& h = out[hdr];
     for (int q = 0; q < t && (int)RS.size() < kRegQ; ++q)
       if (std::find(RS.begin(), RS.end(), q) == RS.end()) RS.push_back(q);
@@ -630,6 +647,9 @@ static void finalize_half(Half& H, size_t elem_bytes) {
           i += w;
         }
         q.op_end = (int64_t)out.size();
+        q.heavy = false;
+        for (int64_t oi = q.op_begin; oi < q.op_end; ++oi)
+          q.heavy = q.heavy || out[oi].kind == OP_RPASS || (out[oi].kind == OP_DENSE && out[oi].k > 2);
         // stage small diagonal tables of this pass in SMEM (bank-spread LDS
         // gathers instead of scattered L1 wavefronts)
         q.tbl_elems = 0;
@@ -776,6 +796,23 @@ static void build_half(Plan& P, int h, const std::vector<SchedItem>& order) {
     prev = L;
   }
   finalize_half(H, P.opts.dtype == HSF_C64 ? 8 : 16);
+  if (std::getenv("HSF_DEBUG_PLAN")) {
+    static const char* kn[] = {"DENSE", "DIAG", "RPASS", "R1"};
+    std::fprintf(stderr, "half %c: m=%d levels=%zu\n", h == 0 ? 'A' : 'B', H.m, H.materialized.size());
+    for (auto& tr : H.trans) {
+      std::fprintf(stderr, " trans %d->%d passes=%zu\n", tr.level_in, tr.level_out, tr.passes.size());
+      for (auto& p : tr.passes) {
+        std::fprintf(stderr, "  pass t=%d tbl=%lld:", p.t, (long long)p.tbl_elems);
+        for (int64_t i = p.op_begin; i < p.op_end; ++i) {
+          const DevOp& d = H.dev_ops[i];
+          std::fprintf(stderr, " %s%s(k%d q", kn[d.kind], d.radix > 1 ? "*" : "", d.k);
+          for (int j = 0; j < std::min(d.k, 4); ++j) std::fprintf(stderr, "%s%d", j ? "," : "", d.q[j]);
+          std::fprintf(stderr, ")");
+        }
+        std::fprintf(stderr, "\n");
+      }
+    }
+  }
 }
 
 static uint64_t fnv(uint64_t h, const void* p, size_t n) {

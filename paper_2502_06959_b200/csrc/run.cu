@@ -267,10 +267,10 @@ static void run_half(const Plan& P, DeviceState* d, int h, const Layout& L, cuda
       // narrow levels (few CTAs) use one 1024-thread CTA per (node, tile) to
       // shorten the dependent chain of small launches at the top of the tree
       const bool wide = tiles * n_out < 2ull * (uint64_t)num_sms() && ps.t >= 11;
-      if (wide)
-        CK(cudaFuncSetAttribute(hsf_pass_kernel<R, kSimThreadsWide>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      else
-        CK(cudaFuncSetAttribute(hsf_pass_kernel<R, kSimThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      auto kern = wide ? (ps.heavy ? hsf_pass_kernel<R, kSimThreadsWide, true> : hsf_pass_kernel<R, kSimThreadsWide, false>)
+                       : (ps.heavy ? hsf_pass_kernel<R, kSimThreads, true> : hsf_pass_kernel<R, kSimThreads, false>);
+      const int nthr = wide ? kSimThreadsWide : kSimThreads;
+      CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       for (uint64_t y0 = 0; y0 < n_out; y0 += 65535) {
         const uint64_t ny = std::min<uint64_t>(65535, n_out - y0);
         pp.node_first = (long long)(first_out + y0);
@@ -290,10 +290,7 @@ static void run_half(const Plan& P, DeviceState* d, int h, const Layout& L, cuda
           pp.src_div = 1;
         }
         dim3 grid((unsigned)tiles, (unsigned)ny);
-        if (wide)
-          hsf_pass_kernel<R, kSimThreadsWide><<<grid, kSimThreadsWide, smem, st>>>(pp);
-        else
-          hsf_pass_kernel<R, kSimThreads><<<grid, kSimThreads, smem, st>>>(pp);
+        kern<<<grid, nthr, smem, st>>>(pp);
         CK(cudaGetLastError());
       }
     }

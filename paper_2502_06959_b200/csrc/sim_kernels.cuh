@@ -268,11 +268,52 @@ __device__ __forceinline__ void reg_apply1(C (&v)[16], const C m00, const C m01,
   }
 }
 
-template <typename R, int NT>
-__global__ void __launch_bounds__(NT, (NT == 256 ? 3 : 1)) hsf_pass_kernel(const PassParams p) {
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// Whole-state tier: the node state is one contiguous block, moved by the TMA
+// bulk-copy engine (cp.async.bulk) with an mbarrier transaction count.
+__device__ __forceinline__ void bulk_load(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  const uint32_t b = smem_addr(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+  for (uint32_t off = 0; off < bytes; off += 65536u) {
+    const uint32_t n = min(65536u, bytes - off);
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr((const char*)sdst + off)),
+                 "l"((const char*)gsrc + off), "r"(n), "r"(b)
+                 : "memory");
+  }
+}
+__device__ __forceinline__ void mbar_wait0(uint64_t* bar) {
+  const uint32_t b = smem_addr(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "W_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
+      "@!P1 bra W_%=;\n"
+      "}\n" ::"r"(b)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
+  for (uint32_t off = 0; off < bytes; off += 65536u) {
+    const uint32_t n = min(65536u, bytes - off);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"((char*)gdst + off),
+                 "r"(smem_addr((const char*)ssrc + off)), "r"(n)
+                 : "memory");
+  }
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem may be released
+}
+
+// HEAVY = register passes and 3..5-qubit dense ops compiled in (128 regs,
+// 2 CTAs/SM); light passes (diagonals + 1/2-qubit SMEM sweeps) run a lean
+// variant at 4 CTAs/SM.  The host picks the variant per pass.
+template <typename R, int NT, bool HEAVY>
+__global__ void __launch_bounds__(NT, (NT == 256 ? (HEAVY ? 2 : 4) : 1)) hsf_pass_kernel(const PassParams p) {
   using C = typename cplx<R>::T;
-  constexpr int CH = (NT == 256) ? 8 : 4;  // elements per thread in registers for diagonal sweeps
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int CH = (NT == 256 && HEAVY) ? 8 : 4;  // elements per thread in registers for diagonal sweeps
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t load_bar;
   C* s = reinterpret_cast<C*>(smem_raw);
   size_t off = sizeof(C) << p.t;
   uint32_t* hi_off = reinterpret_cast<uint32_t*>(smem_raw + off);
@@ -291,6 +332,20 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 3 : 1)) hsf_pass_kernel(const
   const int nel = 1 << p.t;
   const bool whole = (p.t == p.m);
   const C* coef = reinterpret_cast<const C*>(p.coef);
+
+  const C* src = nullptr;
+  if (p.src) {
+    const long long parent = node_g / p.src_div - p.src_first;
+    src = reinterpret_cast<const C*>(p.src) + parent * p.state_elems;
+  }
+  C* dst = reinterpret_cast<C*>(p.dst) + node_local * p.state_elems;
+  const bool bulk = whole && src != nullptr;
+  // kick off the state load first so it overlaps the op staging below
+  if (bulk && threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&load_bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    bulk_load(s, src, (uint32_t)(sizeof(C) << p.t), &load_bar);
+  }
 
   uint32_t base = 0;
   if (!whole) {
@@ -319,30 +374,21 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 3 : 1)) hsf_pass_kernel(const
       const C* g = coef + d.table + digit * d.stride;
       for (int e = lane; e < (1 << d.k); e += 32) stab[d.soff + e] = __ldg(&g[e]);
     }
-    __syncthreads();
   }
   auto gidx_of = [&](int e) -> uint32_t { return whole ? (uint32_t)e : (base | (e & 31) | hi_off[e >> 5]); };
 
-  const C* src = nullptr;
-  if (p.src) {
-    const long long parent = node_g / p.src_div - p.src_first;
-    src = reinterpret_cast<const C*>(p.src) + parent * p.state_elems;
-  }
-  C* dst = reinterpret_cast<C*>(p.dst) + node_local * p.state_elems;
-
-  // load: pairs (e, e+1) are contiguous in global memory (tile position 0 is
-  // qubit 0), so each thread moves 2 amplitudes per request and keeps LB
-  // requests in flight
-  if (src) {
+  if (bulk) {
+    mbar_wait0(&load_bar);
+  } else if (src) {
+    // tiled tier: pairs (e, e+1) are contiguous in global memory (tile
+    // position 0 is qubit 0); LB 16-byte requests in flight per thread
     constexpr int LB = 4;
     for (int e0 = 2 * threadIdx.x; e0 < nel; e0 += 2 * NT * LB) {
       C a[LB], b[LB];
 #pragma unroll
       for (int u = 0; u < LB; ++u) {
         const int e = e0 + 2 * NT * u;
-        if (e < nel) {
-          ld2(src + gidx_of(e), a[u], b[u]);
-        }
+        if (e < nel) ld2(src + gidx_of(e), a[u], b[u]);
       }
 #pragma unroll
       for (int u = 0; u < LB; ++u) {
@@ -361,21 +407,27 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 3 : 1)) hsf_pass_kernel(const
       s[e] = v;
     }
   }
-
-  __syncthreads();  // the pair-mapped load differs from every op mapping below
+  __syncthreads();  // state and staged tables visible to every mapping below
 
   // mapping discipline: standalone diagonal sweeps use the element-owner
   // mapping (e % NT); dense sweeps and register passes use group mappings and
-  // are bracketed by barriers; the final store is pair-mapped after a barrier
+  // are bracketed by barriers
   int i = 0;
   while (i < p.n_ops) {
     const int kind = sops[i].kind;
     if (kind == OP_DENSE) {
       __syncthreads();
-      apply_dense<C>(s, p.t, sops[i], sM[i]);
+      if (HEAVY) {
+        apply_dense<C>(s, p.t, sops[i], sM[i]);
+      } else {
+        if (sops[i].k == 1)
+          apply_dense_k<1>(s, p.t, sops[i], sM[i]);
+        else
+          apply_dense_k<2>(s, p.t, sops[i], sM[i]);
+      }
       __syncthreads();
       ++i;
-    } else if (kind == OP_RPASS) {
+    } else if (HEAVY && kind == OP_RPASS) {
       const DevOp& h = sops[i];
       const int n = h.k;
       int ps[kRegQ];
@@ -424,9 +476,14 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 3 : 1)) hsf_pass_kernel(const
               default: reg_apply1<3>(v, m00, m01, m10, m11); break;
             }
           } else {
-            // 16 independent table reads issued back to back, then applied
+            // the table index is a bitwise gather, so
+            // idx(gb | gbit[j] | ...) = idx(gb) | ibit[j] | ...
             DiagIdx di;
             di.load(d);
+            const uint32_t i0 = di(d, gb);
+            uint32_t ib[kRegQ];
+#pragma unroll
+            for (int j = 0; j < kRegQ; ++j) ib[j] = di(d, gbit[j]);
             const C* T = (d.soff >= 0) ? stab + d.soff : M;
             const bool sh = d.soff >= 0;
 #pragma unroll
@@ -434,11 +491,10 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 3 : 1)) hsf_pass_kernel(const
               C tv[8];
 #pragma unroll
               for (int k = 0; k < 8; ++k) {
-                uint32_t g = gb;
+                uint32_t x = i0;
 #pragma unroll
                 for (int j = 0; j < kRegQ; ++j)
-                  if (((hk + k) >> j) & 1) g |= gbit[j];
-                const uint32_t x = di(d, g);
+                  if (((hk + k) >> j) & 1) x |= ib[j];
                 tv[k] = sh ? T[x] : __ldg(&T[x]);
               }
 #pragma unroll
@@ -500,8 +556,13 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? 3 : 1)) hsf_pass_kernel(const
     }
   }
   __syncthreads();
-  for (int e = 2 * threadIdx.x; e < nel; e += 2 * NT) {
-    st2(dst + gidx_of(e), s[e], s[e + 1]);
+  if (whole) {
+    if (threadIdx.x == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> async proxy
+      bulk_store(dst, s, (uint32_t)(sizeof(C) << p.t));
+    }
+  } else {
+    for (int e = 2 * threadIdx.x; e < nel; e += 2 * NT) st2(dst + gidx_of(e), s[e], s[e + 1]);
   }
 }
 
