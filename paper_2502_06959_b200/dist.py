@@ -1,0 +1,110 @@
+"""Multi-GPU partition of the HSF path evaluation (DESIGN.md
+"Multi-GPU").  One process per GPU; torch.distributed (NCCL on the box, gloo
+in the CPU tests) is plumbing only: it carries the single exchange step the
+method has -- the sum over paths of the partial amplitude vectors (P:109,
+"adding up all contributions") -- or nothing at all when the output is
+row-sharded.
+
+Modes (`mode`):
+  "allreduce"       paths split in contiguous ranges (whole subtrees); every
+                    rank evaluates its range into a full-size partial output,
+                    then one all-reduce(sum).  Bitstring runs (c3, c5), tiny
+                    full runs (c1).
+  "reduce_scatter"  paths split; full-size partial output; one
+                    reduce-scatter(sum): rank r keeps rows
+                    [r*2^nA/G, (r+1)*2^nA/G) of the [2^nA][2^nB] output.  The
+                    literal BASELINE.json c4 reading; K-split c2.
+  "rows"            every rank evaluates ALL paths but writes only its row
+                    shard (rows as above) -- no collective on the data path.
+                    The recommended c4 mode.
+
+The per-rank evaluation is a callable `partial(path_range, row_range, out)`
+so the partition and collective logic can be exercised on CPU with gloo
+(tests/test_dist_gloo.py); on the GPU it is `Plan.run` (see `run_sharded`).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+MODES = ("allreduce", "reduce_scatter", "rows")
+
+
+@dataclass(frozen=True)
+class Shard:
+    mode: str
+    path_range: tuple      # paths this rank evaluates [p0, p1)
+    row_range: tuple | None  # rows this rank's kernel writes (None => all rows / bitstrings)
+    out_rows: tuple | None   # rows this rank holds after the collective (None => everything)
+
+
+def path_range_for_rank(n_paths: int, rank: int, world: int):
+    """Contiguous range of the linear (mixed-radix, last unit fastest) path
+    index: whole subtrees of the path tree when `world` divides the leading
+    radices (true for c1..c5 at 1/2/4/8)."""
+    return (n_paths * rank // world, n_paths * (rank + 1) // world)
+
+
+def row_range_for_rank(n_a: int, rank: int, world: int):
+    rows = 1 << n_a
+    return (rows * rank // world, rows * (rank + 1) // world)
+
+
+def default_mode(full_output: bool, n_paths: int, n_a: int, n_b: int, world: int) -> str:
+    """Cheapest exchange for the run: bitstrings and
+    small outputs all-reduce; a full output whose partial vectors are large
+    relative to the leaves (K small) is row-sharded; otherwise reduce-scatter."""
+    if not full_output:
+        return "allreduce"
+    if world == 1:
+        return "rows"
+    out_bytes = 8 << (n_a + n_b)
+    leaf_bytes = 8 * n_paths * ((1 << n_a) + (1 << n_b))
+    if out_bytes > 64 * leaf_bytes or (1 << n_a) < world:
+        return "rows" if (1 << n_a) >= world else "allreduce"
+    return "reduce_scatter"
+
+
+def make_shard(mode: str, n_paths: int, n_a: int, rank: int, world: int, full_output: bool) -> Shard:
+    if mode not in MODES:
+        raise ValueError(f"unknown mode {mode!r}")
+    if not full_output and mode != "allreduce":
+        raise ValueError("bitstring runs use mode='allreduce'")
+    if mode in ("reduce_scatter", "rows") and (1 << n_a) % world:
+        raise ValueError("row sharding needs world to divide 2^n_A")
+    pr = path_range_for_rank(n_paths, rank, world)
+    if mode == "allreduce":
+        return Shard(mode, pr, None, None)
+    rr = row_range_for_rank(n_a, rank, world)
+    if mode == "reduce_scatter":
+        return Shard(mode, pr, None, rr)
+    return Shard(mode, (0, n_paths), rr, rr)
+
+
+def sharded_step(shard: Shard, partial, out, shard_out=None, group=None):
+    """One rank's step: evaluate, then the mode's collective.
+
+    out       : full-size output buffer (allreduce / reduce_scatter), or the
+                row shard itself (rows mode)
+    shard_out : reduce_scatter destination (rows shard)
+    Returns the tensor holding this rank's result."""
+    import torch
+    import torch.distributed as dist
+
+    partial(shard.path_range, shard.row_range, out)
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world == 1 or shard.mode == "rows":
+        return out
+    if shard.mode == "allreduce":
+        dist.all_reduce(torch.view_as_real(out), op=dist.ReduceOp.SUM, group=group)
+        return out
+    dist.reduce_scatter_tensor(torch.view_as_real(shard_out), torch.view_as_real(out),
+                               op=dist.ReduceOp.SUM, group=group)
+    return shard_out
+
+
+def run_sharded(plan, out, shard: Shard, shard_out=None, bitstrings=None, precision="auto", group=None):
+    """GPU entry: `plan.run` (libhsf.so, C ABI) on this rank's range, then the
+    collective over NCCL."""
+    def partial(path_range, row_range, o):
+        plan.run(o, bitstrings=bitstrings, path_range=path_range, row_range=row_range, precision=precision)
+    return sharded_step(shard, partial, out, shard_out, group)

@@ -193,14 +193,3 @@ class Plan:
         a = self._args(1, True, 1 if bitstrings_count else None, bitstrings_count, True, path_range, row_range,
                        precision, None, -1, None)
         return int(lib().hsf_workspace_bytes(self._h, C.byref(a)))
-
-
-def path_range_for_rank(n_paths: int, rank: int, world: int):
-    """Contiguous path range of one rank (whole subtrees when world divides the
-    leading radices)."""
-    return (n_paths * rank // world, n_paths * (rank + 1) // world)
-
-
-def row_range_for_rank(n_a: int, rank: int, world: int):
-    rows = 1 << n_a
-    return (rows * rank // world, rows * (rank + 1) // world)

@@ -1,0 +1,128 @@
+"""Multi-process (world_size 2, gloo, CPU) coverage of the N>1 path partition
+and its single exchange step (paper_2502_06959_b200/dist.py).
+
+Each rank evaluates its shard with the CPU oracle standing in for `Plan.run`
+(the GPU kernels are covered by tests/test_gpu_parity.py, including the
+path-range and row-range arguments these shards feed them); the collective
+must reassemble exactly the single-process oracle result."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from hsf_inputs import make_config
+from oracle import hsf_oracle as O
+from paper_2502_06959_b200 import dist as D
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _oracle_partial(inst, P, bits):
+    import torch
+
+    def partial(path_range, row_range, out):
+        A, B, c = O.half_states(P, *path_range)
+        if bits is not None:
+            v = O.recombine_bits(A, B, c, bits, inst.n_low)
+        else:
+            v = O.recombine_full(A, B, c)
+            if row_range is not None:
+                v = v[row_range[0] << inst.n_low:row_range[1] << inst.n_low]
+        out.copy_(torch.from_numpy(np.ascontiguousarray(v)))
+    return partial
+
+
+def _worker(rank, world, port, name, mode, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        inst = make_config(name, twin=True)
+        n, g = O.parse_circuit(inst.text)
+        P = O.plan(n, g, inst.n_low, inst.blocks)
+        full = inst.bitstrings is None
+        n_a = n - inst.n_low
+        sh = D.make_shard(mode, P.n_paths, n_a, rank, world, full)
+        if full:
+            rows = (sh.row_range[1] - sh.row_range[0]) if sh.row_range else (1 << n_a)
+            out = torch.zeros(rows << inst.n_low, dtype=torch.complex128)
+            shard_out = torch.zeros((1 << n) // world, dtype=torch.complex128) if mode == "reduce_scatter" else None
+        else:
+            out = torch.zeros(len(inst.bitstrings), dtype=torch.complex128)
+            shard_out = None
+        res = D.sharded_step(sh, _oracle_partial(inst, P, inst.bitstrings), out, shard_out)
+        # gather every rank's piece on rank 0 in rank order
+        pieces = [None] * world
+        dist.all_gather_object(pieces, (sh.out_rows, res.numpy()))
+        if rank == 0:
+            q.put(pieces)
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(name, mode, world=2):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, name, mode, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = q.get()  # read before join: a large pickled result blocks the pipe
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    return res
+
+
+def _reference(name):
+    inst = make_config(name, twin=True)
+    n, g = O.parse_circuit(inst.text)
+    psi = O.schrodinger(n, g)
+    return inst, psi if inst.bitstrings is None else psi[inst.bitstrings.astype(np.int64)]
+
+
+@pytest.mark.parametrize("name,mode", [("c4", "reduce_scatter"), ("c4", "rows"), ("c4", "allreduce"),
+                                       ("c1", "allreduce"), ("c5", "allreduce"), ("c3", "allreduce")])
+def test_two_rank_shards_reassemble(name, mode):
+    inst, ref = _reference(name)
+    pieces = _run(name, mode)
+    if mode == "allreduce":
+        for _, v in pieces:  # every rank holds the whole reduced result
+            assert np.abs(v - ref).max() <= 1e-12
+    else:
+        got = np.concatenate([v for _, v in sorted(pieces, key=lambda x: x[0][0])])
+        assert [r for r, _ in pieces] == [D.row_range_for_rank(inst.n - inst.n_low, r, 2) for r in range(2)]
+        assert np.abs(got - ref).max() <= 1e-12
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_path_ranges_cover_and_are_subtrees(world):
+    # c1..c5 radices: the ranges tile [0, n_p) and start on subtree boundaries
+    # (world divides the product of the leading radices)
+    for name, radices in [("c1", [2] * 4), ("c2", [2] * 12), ("c3", [4] * 4), ("c4", [4] * 3), ("c5", [2] * 8)]:
+        n_p = int(np.prod(radices))
+        rs = [D.path_range_for_rank(n_p, r, world) for r in range(world)]
+        assert rs[0][0] == 0 and rs[-1][1] == n_p
+        assert all(rs[i][1] == rs[i + 1][0] for i in range(world - 1))
+        sub = n_p // world
+        assert all((p1 - p0) == sub and p0 % sub == 0 for p0, p1 in rs)
+
+
+def test_default_modes():
+    # c4 (K = 64, 2^34 outputs): rows; c2 (K = 4096): reduce-scatter; bitstrings: all-reduce
+    assert D.default_mode(True, 64, 17, 17, 8) == "rows"
+    assert D.default_mode(True, 4096, 12, 12, 8) == "reduce_scatter"
+    assert D.default_mode(False, 256, 20, 20, 8) == "allreduce"
+    with pytest.raises(ValueError):
+        D.make_shard("rows", 16, 6, 0, 2, full_output=False)
+    with pytest.raises(ValueError):
+        D.make_shard("rows", 16, 1, 0, 4, full_output=True)
