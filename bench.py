@@ -37,7 +37,8 @@ def _args():
     ap.add_argument("--precision", default="auto")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--collective", default="auto", choices=["auto", "reduce_scatter", "allreduce", "rows"])
+    ap.add_argument("--collective", default="auto", choices=["auto", "reduce_scatter", "allreduce", "rows"],
+                    help="N>1 exchange (paper_2502_06959_b200/dist.py); auto = cheapest for the output mode")
     return ap.parse_args()
 
 
@@ -105,11 +106,15 @@ def cpu_oracle_rate(inst, budget_s: float = 15.0):
     k = 1
     done = 0
     t_sim = 0.0
+    # full outputs beyond 2^24 amplitudes: the Kronecker sum over a row subset,
+    # the rate scaled by the fraction of rows (c4: 2^34 outputs)
+    rows_all = 1 << (n - inst.n_low)
+    rows = rows_all if inst.bitstrings is not None else max(1, min(rows_all, (1 << 24) >> inst.n_low))
     while True:
         t1 = time.perf_counter()
         A, B, c = O.half_states(P, done, min(P.n_paths, done + k))
         if inst.bitstrings is None:
-            O.recombine_full(A, B, c)
+            O.recombine_full(A[:rows], B, c)
         else:
             O.recombine_bits(A, B, c, inst.bitstrings, inst.n_low)
         t_sim += time.perf_counter() - t1
@@ -118,8 +123,15 @@ def cpu_oracle_rate(inst, budget_s: float = 15.0):
             break
         k = max(1, min(P.n_paths - done, int(k * 2)))
     threads = int(os.environ.get("OMP_NUM_THREADS", "0")) or len(os.sched_getaffinity(0))
-    out = "full 2^%d output" % n if inst.bitstrings is None else "%d bitstrings" % len(inst.bitstrings)
-    return done / t_sim, f"{done} of {P.n_paths} paths ({out}); plan {t_plan:.3f}s excluded", threads, t_sim / done
+    if inst.bitstrings is None:
+        out = "full 2^%d output" % n if rows == rows_all else \
+            "%d of %d output rows (rate scaled by the row fraction)" % (rows, rows_all)
+    else:
+        out = "%d bitstrings" % len(inst.bitstrings)
+    # simulation of the half-states is per path and not scaled; the row
+    # fraction only scales the recombination, so this rate is an upper bound
+    rate = done / t_sim * (rows / rows_all)
+    return rate, f"{done} of {P.n_paths} paths ({out}); plan {t_plan:.3f}s excluded", threads, t_sim / done
 
 
 def reference_arm(a):
@@ -156,8 +168,8 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2502_06959_b200 import Plan, build, path_range_for_rank
-    from paper_2502_06959_b200 import hsf as H
+    from paper_2502_06959_b200 import Plan, build
+    from paper_2502_06959_b200 import dist as D
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -181,29 +193,34 @@ def main():
         dist.all_gather(hs, h)
         if any(int(x.item()) != int(h.item()) for x in hs):
             raise RuntimeError("plan hash mismatch across ranks")
-    pr = path_range_for_rank(P.n_paths, rank, world)
+    full = inst.bitstrings is None
+    mode = a.collective if a.collective != "auto" else D.default_mode(full, P.n_paths, P.n_a, P.n_b, world)
+    sh = D.make_shard(mode, P.n_paths, P.n_a, rank, world, full)
+    pr = sh.path_range
     cdt = torch.complex64 if inst.dtype == "c64" else torch.complex128
     esz = 8 if inst.dtype == "c64" else 16
     stream = torch.cuda.current_stream()
-    full = inst.bitstrings is None
     if full:
         N_out = 1 << inst.n
-        out = torch.empty(N_out, dtype=cdt, device="cuda")
-        shard = torch.empty(N_out // world, dtype=cdt, device="cuda") if world > 1 else None
+        rows = (sh.row_range[1] - sh.row_range[0]) if sh.row_range else (1 << P.n_a)
+        out = torch.empty(rows << P.n_b, dtype=cdt, device="cuda")
+        shard = torch.empty(N_out // world, dtype=cdt, device="cuda") if mode == "reduce_scatter" and world > 1 \
+            else None
         bits_d = None
     else:
         N_out = len(inst.bitstrings)
         out = torch.empty(N_out, dtype=cdt, device="cuda")
         bits_d = torch.from_numpy(inst.bitstrings.view(np.int64)).cuda()
         shard = None
+    phases = []
 
-    def step():
-        P.run(out, bitstrings=bits_d, path_range=pr, precision=a.precision)
-        if world > 1:
-            if full:
-                dist.reduce_scatter_tensor(shard, out)
-            else:
-                dist.all_reduce(out)
+    def step(timed=False):
+        def partial(path_range, row_range, o):
+            ph = P.run(o, bitstrings=bits_d, path_range=path_range, row_range=row_range, precision=a.precision,
+                       timings=timed)
+            if timed:
+                phases.append(ph)
+        D.sharded_step(sh, partial, out, shard)
 
     # L2 flush buffer (> 126 MB L2) written between timed steps, outside the events
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -211,7 +228,6 @@ def main():
         step()
     torch.cuda.synchronize()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
-    phases = []
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -221,12 +237,7 @@ def main():
             evs[i][0].record(stream)
             # timings=True: the library brackets each phase with CUDA events on
             # the stream it launches on (and synchronises at the end of the run)
-            phases.append(P.run(out, bitstrings=bits_d, path_range=pr, precision=a.precision, timings=True))
-            if world > 1:
-                if full:
-                    dist.reduce_scatter_tensor(shard, out)
-                else:
-                    dist.all_reduce(out)
+            step(timed=True)
             evs[i][1].record(stream)
         torch.cuda.synchronize()
     if world > 1:
@@ -244,7 +255,15 @@ def main():
     # end-to-end through the public API with host buffers: plan (host SVD etc.)
     # + table upload + run + copy of the result to pinned host memory
     e2e = None
-    if rank == 0:
+    try:
+        import psutil
+        host_avail = psutil.virtual_memory().available
+    except Exception:
+        host_avail = 0
+    if rank == 0 and N_out * esz > host_avail // 4:
+        e2e = {"value": None, "unit": "paths/s", "skipped": "output of %d bytes exceeds a quarter of the host's "
+               "available memory (%d bytes) for a pinned host buffer" % (N_out * esz, host_avail)}
+    elif rank == 0:
         host_out = torch.empty(N_out, dtype=cdt, pin_memory=True)
         host_bits = None if full else torch.from_numpy(inst.bitstrings.view(np.int64)).pin_memory()
         tt = []
@@ -273,19 +292,27 @@ def main():
     core_ms = phase[3]
     prec = a.precision
     eff_prec = ("bf16x3" if inst.dtype == "c64" else "simt") if prec == "auto" else prec
-    MA, MB = 1 << (inst.n - inst.n_low), 1 << inst.n_low
+    MA, MB = (rows if full else 1 << (inst.n - inst.n_low)), 1 << inst.n_low
     clk_mhz = peaks.get("clocks_under_load", {}).get("sm_mhz_median", 1305.0)
     if full and eff_prec in ("bf16x3", "bf16x1"):
-        # executed tensor-core flops: (3 | 1) real GEMMs of rows x 2MB x 2K
+        # executed tensor-core flops: (3 | 1) real GEMMs of rows x 2MB x 2K;
+        # algorithmic bytes: the fp32 output written once (+ bf16 operands)
         nprod = 3 if eff_prec == "bf16x3" else 1
         tflop = nprod * 2.0 * MA * (2 * MB) * (2 * K)
-        ach = tflop / (core_ms * 1e-3) / 1e12
-        roof = {"bound": "tensor", "kernel": "tc_gemm_kernel (tcgen05 bf16, split x%d)" % nprod,
-                "achieved": ach, "peak": bf16, "unit": "TFLOP/s", "frac": ach / bf16, "traffic": None,
-                "flops_per_launch": tflop, "useful_complex_flops": 8.0 * MA * MB * K,
-                "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst); sustained %.1f" %
-                               peaks.get("bf16_tflops_sustained", 0.0),
-                "kernel_ms": core_ms}
+        obytes = MA * MB * esz + (2 if nprod == 3 else 1) * 4.0 * K * (MA + 2 * MB)
+        t_tensor, t_hbm = tflop / (bf16 * 1e12), obytes / (hbm * 1e9)
+        if t_tensor >= t_hbm:
+            ach = tflop / (core_ms * 1e-3) / 1e12
+            roof = {"bound": "tensor", "achieved": ach, "peak": bf16, "unit": "TFLOP/s", "frac": ach / bf16,
+                    "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst); sustained %.1f" %
+                                   peaks.get("bf16_tflops_sustained", 0.0)}
+        else:
+            ach = obytes / (core_ms * 1e-3) / 1e9
+            roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+        roof.update({"kernel": "tc_gemm_kernel (tcgen05 bf16, split x%d)" % nprod, "traffic": None,
+                     "flops_per_launch": tflop, "bytes_per_launch": obytes,
+                     "useful_complex_flops": 8.0 * MA * MB * K, "kernel_ms": core_ms})
     elif full:
         alu_peak = 148 * 128 * 2 * clk_mhz * 1e6 / 1e12
         useful = 8.0 * MA * MB * K
@@ -313,7 +340,7 @@ def main():
                 "vs_baseline": None, "dtype": inst.dtype, "data": "synthetic",
                 "config": {"workload": a.config, "n_qubits": inst.n, "n_low": inst.n_low,
                            "n_paths_joint": P.n_paths, "log2_n_paths_individual": P.log2_n_paths_individual,
-                           "outputs": N_out, "precision": prec, "parallelism": f"paths{world}",
+                           "outputs": N_out, "precision": prec, "parallelism": f"{mode}{world}",
                            "l2": "flushed (256 MiB write) between timed steps"},
                 "amplitudes_per_s": amps, "terms_per_s": amps * P.n_paths,
                 "phase_ms": {"sim_A": phase[0], "sim_B": phase[1], "prep": phase[2], "core": phase[3],

@@ -79,7 +79,8 @@ typedef struct {
   int32_t individual;            /* 1 => ignore blocks, cut every crossing gate alone */
   int32_t tile_qubits;           /* in [10,13]: amplitudes per SMEM tile = 2^tile_qubits for
                                     halves larger than the SMEM-resident limit;
-                                    0 => default (12) */
+                                    0 => auto (default): 12, widened to 13 for
+                                    complex64 where that saves an HBM pass */
   int32_t fuse_gates;            /* 1 (default) => host gate fusion */
 } hsf_plan_opts;
 
@@ -138,7 +139,11 @@ typedef struct {
   uint64_t n_bitstrings;
   int32_t bits_on_device;       /* 1 => device pointer, 0 => host pointer */
   void* out;                    /* caller-owned, plan dtype */
-  int32_t out_on_device;        /* 1 => device pointer, 0 => host (copied back) */
+  int32_t out_on_device;        /* 1 => device pointer, 0 => host pointer: full-mode
+                                   rows are computed in chunks of <= 256 MiB into two
+                                   device staging buffers and copied back while the
+                                   next chunk is computed (bounded device memory);
+                                   pinned host memory gives overlapped copies */
   uint64_t path_begin, path_end;/* paths evaluated [begin,end); 0,0 => all.  The
                                    result is the partial sum over this range. */
   uint64_t row_begin, row_end;  /* full mode only; 0,0 => all 2^nA rows */

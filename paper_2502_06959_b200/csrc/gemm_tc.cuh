@@ -428,15 +428,20 @@ inline void tc_prep_b(const TcBuffers& t, const float2* leavesB, long long K, lo
   if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("split_b: ") + cudaGetErrorString(e));
 }
 
-// K5: the persistent tcgen05 GEMM
-inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long rows, bool x3, cudaStream_t st) {
+// K5: the persistent tcgen05 GEMM over operand rows [row0, row0 + rows)
+// (row0 a multiple of BM) into out[rows][2*MB] fp32
+inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row0, long long rows, bool x3,
+                    cudaStream_t st) {
   const long long kcols = 2 * t.d.Kpad;  // bf16 per operand row
-  CUtensorMap mAh = make_map(t.a_hi, t.d.rows_pad, kcols, tc::BM);
+  if (row0 % tc::BM) fail(HSF_ERR_INVALID_ARG, "tc_gemm row offset not tile aligned");
+  const long long rpad = (rows + tc::BM - 1) / tc::BM * tc::BM;
+  if (row0 + rpad > t.d.rows_pad) fail(HSF_ERR_INVALID_ARG, "tc_gemm rows out of range");
+  CUtensorMap mAh = make_map(t.a_hi + row0 * t.d.Kpad, rpad, kcols, tc::BM);
   CUtensorMap mBh = make_map(t.b_hi, t.d.nrows_b_pad, kcols, tc::BN);
-  CUtensorMap mAl = x3 ? make_map(t.a_lo, t.d.rows_pad, kcols, tc::BM) : mAh;
+  CUtensorMap mAl = x3 ? make_map(t.a_lo + row0 * t.d.Kpad, rpad, kcols, tc::BM) : mAh;
   CUtensorMap mBl = x3 ? make_map(t.b_lo, t.d.nrows_b_pad, kcols, tc::BN) : mBh;
   tc::Params p;
-  p.num_m = (int)(t.d.rows_pad / tc::BM);
+  p.num_m = (int)(rpad / tc::BM);
   p.num_n = (int)(t.d.nrows_b_pad / tc::BN);
   p.num_k = (int)(kcols / tc::BK);
   p.x3 = x3 ? 1 : 0;

@@ -514,8 +514,14 @@ static DevOp to_dev(const HostOp& op, const std::vector<int>* T) {
   return d;
 }
 
-static void plan_passes(Half& H, Transition& tr, int64_t ob, int64_t oe, int t) {
+struct PassChoice {
+  std::vector<int> T;          // ascending tile qubits
+  std::vector<int64_t> take;   // op indices (into H.ops) applied in this pass
+};
+
+static std::vector<PassChoice> greedy_passes(const Half& H, int64_t ob, int64_t oe, int t) {
   const int low = 5;
+  std::vector<PassChoice> out;
   std::vector<int64_t> pending;
   for (int64_t i = ob; i < oe; ++i) pending.push_back(i);
   do {
@@ -548,15 +554,34 @@ static void plan_passes(Half& H, Transition& tr, int64_t ob, int64_t oe, int t) 
     }
     if (take.empty() && !pending.empty()) fail(HSF_ERR_UNSUPPORTED, "pass planner made no progress");
     for (int q = 0; q < H.m && (int)T.size() < t; ++q) T.insert(q);
-    Pass p;
-    p.t = t;
-    p.T.assign(T.begin(), T.end());  // ascending: tile positions 0..4 are qubits 0..4
-    p.op_begin = (int64_t)H.dev_ops.size();
-    for (int64_t oi : take) H.dev_ops.push_back(to_dev(H.ops[oi], &p.T));
-    p.op_end = (int64_t)H.dev_ops.size();
-    tr.passes.push_back(std::move(p));
+    out.push_back({std::vector<int>(T.begin(), T.end()), take});
     pending.swap(rest);
   } while (!pending.empty());
+  return out;
+}
+
+// Tile size per transition: t, or up to t_max (tile_qubits == 0 => auto: 12,
+// or 13 for complex64 = 64 KiB tiles) when a wider tile needs fewer HBM passes
+// over the level.
+static void plan_passes(Half& H, Transition& tr, int64_t ob, int64_t oe, int t, int t_max) {
+  std::vector<PassChoice> best = greedy_passes(H, ob, oe, t);
+  int bt = t;
+  for (int t2 = t + 1; t2 <= t_max && t2 <= H.m; ++t2) {
+    std::vector<PassChoice> c = greedy_passes(H, ob, oe, t2);
+    if (c.size() < best.size()) {
+      best.swap(c);
+      bt = t2;
+    }
+  }
+  for (auto& pc : best) {
+    Pass p;
+    p.t = bt;
+    p.T = pc.T;  // ascending: tile positions 0..4 are qubits 0..4
+    p.op_begin = (int64_t)H.dev_ops.size();
+    for (int64_t oi : pc.take) H.dev_ops.push_back(to_dev(H.ops[oi], &p.T));
+    p.op_end = (int64_t)H.dev_ops.size();
+    tr.passes.push_back(std::move(p));
+  }
 }
 
 // Register passes: maximal runs of 1-qubit dense ops on at most kRegQ distinct
@@ -740,7 +765,8 @@ static void build_half(Plan& P, int h, const std::vector<SchedItem>& order) {
   H.materialized.push_back(U);
   // transitions + passes
   const int smem_limit = (P.opts.dtype == HSF_C64) ? 13 : 12;
-  const int t = std::min(H.m, P.opts.tile_qubits);
+  const int t = std::min(H.m, P.opts.tile_qubits > 0 ? P.opts.tile_qubits : 12);
+  const int t_max = (P.opts.tile_qubits == 0 && P.opts.dtype == HSF_C64) ? 13 : t;
   H.trans.clear();
   H.dev_ops.clear();
   H.n_passes = 0;
@@ -760,7 +786,7 @@ static void build_half(Plan& P, int h, const std::vector<SchedItem>& order) {
       p.op_end = (int64_t)H.dev_ops.size();
       tr.passes.push_back(p);
     } else {
-      plan_passes(H, tr, ob, oe, t);
+      plan_passes(H, tr, ob, oe, t, t_max);
     }
     // resolve factor digits for this transition's output level
     for (auto& p : tr.passes)

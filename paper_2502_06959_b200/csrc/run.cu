@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -39,7 +40,8 @@ struct DeviceState {
   size_t cp_cap = 0;
   uint64_t cp_p0 = ~0ull, cp_p1 = ~0ull;
   cudaEvent_t ev[6] = {};
-  cudaStream_t side = nullptr;  // half-B stream
+  cudaEvent_t evg[2] = {}, evc[2] = {};  // host-output chunks: GEMM done / D2H done
+  cudaStream_t side = nullptr;  // half-B stream; D2H stream of host-output chunks
   bool sticky = false;
 };
 
@@ -56,6 +58,10 @@ void destroy_device(Plan* p) {
   cudaFree(d->cp);
   for (auto& e : d->ev)
     if (e) cudaEventDestroy(e);
+  for (int i = 0; i < 2; ++i) {
+    if (d->evg[i]) cudaEventDestroy(d->evg[i]);
+    if (d->evc[i]) cudaEventDestroy(d->evc[i]);
+  }
   if (d->side) cudaStreamDestroy(d->side);
   if (cur >= 0) cudaSetDevice(cur);
   delete d;
@@ -92,6 +98,10 @@ static DeviceState* ensure_device(Plan* P, int device) {
                     cudaMemcpyHostToDevice));
   }
   for (auto& e : d->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDefault));
+  for (int i = 0; i < 2; ++i) {
+    CK(cudaEventCreateWithFlags(&d->evg[i], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&d->evc[i], cudaEventDisableTiming));
+  }
   CK(cudaStreamCreateWithFlags(&d->side, cudaStreamNonBlocking));
   return d;
 }
@@ -108,10 +118,13 @@ struct Layout {
   size_t off_T[2] = {0, 0};    // transposed operands (bitstring mode)
   size_t off_bits = 0, off_out = 0, off_tc = 0;
   size_t tc_bytes = 0;
+  uint64_t chunk_rows = 0;     // full mode, host output: rows per staged D2H chunk
+  size_t chunk_bytes = 0;
   size_t total = 0;
 };
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+constexpr size_t kHostChunkBytes = (size_t)256 << 20;
 
 static uint64_t nodes_at(const Plan& P, int L, uint64_t p0, uint64_t p1) {
   uint64_t S = suffix_prod(P.ranks, L);
@@ -172,8 +185,18 @@ static Layout make_layout(const Plan& P, const hsf_run_args& a, size_t elem) {
       off = align_up(off + L.tc_bytes);
     }
     if (!a.out_on_device) {
+      // host output: rows are produced in chunks of <= kHostChunkBytes into two
+      // device staging buffers; the D2H copy of one chunk overlaps the
+      // path-sum of the next (bounded device memory for any output size)
+      const size_t row_bytes = ((size_t)1 << nB) * elem;
+      size_t chunk = kHostChunkBytes;
+      if (const char* e = std::getenv("HSF_HOST_CHUNK_BYTES")) chunk = std::max<size_t>(1, std::strtoull(e, nullptr, 10));
+      uint64_t cr = std::max<uint64_t>(1, chunk / row_bytes);
+      if (L.prec != HSF_PREC_SIMT) cr = std::max<uint64_t>(128, cr / 128 * 128);  // whole tensor-core M tiles
+      L.chunk_rows = std::min<uint64_t>(cr, L.r1 - L.r0);
+      L.chunk_bytes = align_up(L.chunk_rows * row_bytes);
       L.off_out = off;
-      off = align_up(off + ((size_t)(L.r1 - L.r0) << nB) * elem);
+      off = align_up(off + 2 * L.chunk_bytes);
     }
   }
   L.total = off;
@@ -325,45 +348,53 @@ static void prep_half(Plan* P, DeviceState* d, const Layout& L, int h, cudaStrea
   }
 }
 
+// bitstring path-sum (K6) into `out` (device)
 template <typename R>
-static void run_core(Plan* P, DeviceState* d, const Layout& L, const hsf_run_args& a, cudaStream_t st) {
+static void run_core_bits(Plan* P, DeviceState* d, const Layout& L, const hsf_run_args& a, cudaStream_t st,
+                          typename cplx<R>::T* out) {
+  using C = typename cplx<R>::T;
+  char* ws = (char*)d->ws;
+  const int nB = P->n_low;
+  const long long K = (long long)L.K;
+  const C* AT = (const C*)(ws + L.off_T[0]);
+  const C* BT = (const C*)(ws + L.off_T[1]);
+  const unsigned long long* bits = (const unsigned long long*)a.bitstrings;
+  if (!a.bits_on_device) {
+    bits = (const unsigned long long*)(ws + L.off_bits);
+    CK(cudaMemcpyAsync((void*)bits, a.bitstrings, a.n_bitstrings * 8, cudaMemcpyHostToDevice, st));
+  }
+  const long long ns = (long long)a.n_bitstrings;
+  long long blocks = std::min<long long>((ns + 7) / 8, 148ll * 64);
+  if (sizeof(R) == 4 && K % 64 == 0) {
+    gather_dot_c64_vec_kernel<<<(unsigned)blocks, 256, 0, st>>>((const float4*)AT, (const float4*)BT, bits,
+                                                                (float2*)out, ns, K, nB);
+  } else {
+    gather_dot_kernel<C><<<(unsigned)blocks, 256, 0, st>>>(AT, BT, bits, out, ns, K, nB);
+  }
+  CK(cudaGetLastError());
+}
+
+// full-output path-sum (K5 / K5s) of rows [L.r0 + lo, L.r0 + lo + nrows) into `out`
+// (device, row-major [nrows][2^nB]); lo is a multiple of the tensor-core M tile
+template <typename R>
+static void run_core_full(Plan* P, DeviceState* d, const Layout& L, cudaStream_t st, uint64_t lo, uint64_t nrows,
+                          typename cplx<R>::T* out) {
   using C = typename cplx<R>::T;
   char* ws = (char*)d->ws;
   const int nA = P->n - P->n_low, nB = P->n_low;
   const long long K = (long long)L.K;
-  if (L.bits_mode) {
-    const C* AT = (const C*)(ws + L.off_T[0]);
-    const C* BT = (const C*)(ws + L.off_T[1]);
-    const unsigned long long* bits = (const unsigned long long*)a.bitstrings;
-    if (!a.bits_on_device) {
-      bits = (const unsigned long long*)(ws + L.off_bits);
-      CK(cudaMemcpyAsync((void*)bits, a.bitstrings, a.n_bitstrings * 8, cudaMemcpyHostToDevice, st));
-    }
-    C* out = a.out_on_device ? (C*)a.out : (C*)(ws + L.off_out);
-    const long long ns = (long long)a.n_bitstrings;
-    long long blocks = std::min<long long>((ns + 7) / 8, 148ll * 64);
-    if (sizeof(R) == 4 && K % 64 == 0) {
-      gather_dot_c64_vec_kernel<<<(unsigned)blocks, 256, 0, st>>>((const float4*)AT, (const float4*)BT, bits,
-                                                                  (float2*)out, ns, K, nB);
-    } else {
-      gather_dot_kernel<C><<<(unsigned)blocks, 256, 0, st>>>(AT, BT, bits, out, ns, K, nB);
-    }
+  if (L.prec == HSF_PREC_SIMT) {
+    const C* leavesA = (const C*)(ws + L.off_leaves[0]);
+    const C* leavesB = (const C*)(ws + L.off_leaves[1]);
+    dim3 grid((unsigned)(((1ll << nB) + 63) / 64), (unsigned)((nrows + 63) / 64));
+    simt_gemm_kernel<C, R><<<grid, 256, 0, st>>>(leavesA, leavesB, (const C*)d->cp, out, K, 1ll << nA, 1ll << nB,
+                                                 (long long)(L.r0 + lo), (long long)nrows);
     CK(cudaGetLastError());
   } else {
-    const long long rows = (long long)(L.r1 - L.r0);
-    C* out = a.out_on_device ? (C*)a.out : (C*)(ws + L.off_out);
-    if (L.prec == HSF_PREC_SIMT) {
-      const C* leavesA = (const C*)(ws + L.off_leaves[0]);
-      const C* leavesB = (const C*)(ws + L.off_leaves[1]);
-      dim3 grid((unsigned)(((1ll << nB) + 63) / 64), (unsigned)((rows + 63) / 64));
-      simt_gemm_kernel<C, R><<<grid, 256, 0, st>>>(leavesA, leavesB, (const C*)d->cp, out, K, 1ll << nA, 1ll << nB,
-                                                   (long long)L.r0, rows);
-      CK(cudaGetLastError());
-    } else {
-      if (sizeof(R) != 4) fail(HSF_ERR_UNSUPPORTED, "tensor-core path-sum needs complex64");
-      TcBuffers t = tc_buffers(K, rows, 1ll << nB, L.prec == HSF_PREC_BF16X3, ws + L.off_tc, L.tc_bytes);
-      tc_gemm(t, (float2*)out, 1ll << nB, rows, L.prec == HSF_PREC_BF16X3, st);
-    }
+    if (sizeof(R) != 4) fail(HSF_ERR_UNSUPPORTED, "tensor-core path-sum needs complex64");
+    TcBuffers t = tc_buffers(K, (long long)(L.r1 - L.r0), 1ll << nB, L.prec == HSF_PREC_BF16X3, ws + L.off_tc,
+                             L.tc_bytes);
+    tc_gemm(t, (float2*)out, 1ll << nB, (long long)lo, (long long)nrows, L.prec == HSF_PREC_BF16X3, st);
   }
 }
 
@@ -383,12 +414,32 @@ static void run_all(Plan* P, DeviceState* d, const Layout& L, const hsf_run_args
   prep_half<R>(P, d, L, 0, st);
   CK(cudaStreamWaitEvent(st, d->ev[5], 0));
   if (timed) CK(cudaEventRecord(d->ev[3], st));
-  run_core<R>(P, d, L, a, st);
-  if (timed) CK(cudaEventRecord(d->ev[4], st));
-  if (!a.out_on_device) {
-    const size_t n = L.bits_mode ? (size_t)a.n_bitstrings : ((size_t)(L.r1 - L.r0) << P->n_low);
-    CK(cudaMemcpyAsync(a.out, (char*)d->ws + L.off_out, n * sizeof(C), cudaMemcpyDeviceToHost, st));
+  char* ws = (char*)d->ws;
+  if (L.bits_mode) {
+    C* out = a.out_on_device ? (C*)a.out : (C*)(ws + L.off_out);
+    run_core_bits<R>(P, d, L, a, st, out);
+    if (!a.out_on_device)
+      CK(cudaMemcpyAsync(a.out, out, (size_t)a.n_bitstrings * sizeof(C), cudaMemcpyDeviceToHost, st));
+  } else if (a.out_on_device) {
+    run_core_full<R>(P, d, L, st, 0, L.r1 - L.r0, (C*)a.out);
+  } else {
+    // host output: double-buffered chunks, path-sum on `st`, D2H on `side`
+    const uint64_t rows = L.r1 - L.r0;
+    const size_t row_bytes = sizeof(C) << P->n_low;
+    int c = 0;
+    for (uint64_t lo = 0; lo < rows; lo += L.chunk_rows, ++c) {
+      const uint64_t nr = std::min<uint64_t>(L.chunk_rows, rows - lo);
+      C* buf = (C*)(ws + L.off_out + (size_t)(c & 1) * L.chunk_bytes);
+      if (c >= 2) CK(cudaStreamWaitEvent(st, d->evc[c & 1], 0));
+      run_core_full<R>(P, d, L, st, lo, nr, buf);
+      CK(cudaEventRecord(d->evg[c & 1], st));
+      CK(cudaStreamWaitEvent(d->side, d->evg[c & 1], 0));
+      CK(cudaMemcpyAsync((char*)a.out + lo * row_bytes, buf, nr * row_bytes, cudaMemcpyDeviceToHost, d->side));
+      CK(cudaEventRecord(d->evc[c & 1], d->side));
+    }
+    for (int i = 0; i < std::min(c, 2); ++i) CK(cudaStreamWaitEvent(st, d->evc[i], 0));
   }
+  if (timed) CK(cudaEventRecord(d->ev[4], st));
 }
 
 static void run(Plan* P, const hsf_run_args& a) {
@@ -455,7 +506,7 @@ hsf_status hsf_plan_opts_default(hsf_plan_opts* o) {
   o->max_dense_block_qubits = 10;
   o->log2_path_budget = 26;
   o->individual = 0;
-  o->tile_qubits = 12;
+  o->tile_qubits = 0;
   o->fuse_gates = 1;
   return HSF_OK;
 }
@@ -469,8 +520,8 @@ hsf_status hsf_plan(const char* text, size_t len, int32_t n_low, int64_t n_block
     hsf_plan_opts o;
     hsf_plan_opts_default(&o);
     if (opts) o = *opts;
-    if (o.tile_qubits == 0) o.tile_qubits = 12;
-    if (o.tile_qubits < 10 || o.tile_qubits > 13) fail(HSF_ERR_INVALID_ARG, "tile_qubits must be in [10,13]");
+    if (o.tile_qubits != 0 && (o.tile_qubits < 10 || o.tile_qubits > 13))
+      fail(HSF_ERR_INVALID_ARG, "tile_qubits must be 0 (auto) or in [10,13]");
     if (o.dtype != HSF_C64 && o.dtype != HSF_C128) fail(HSF_ERR_INVALID_ARG, "bad dtype");
     if (!(o.svd_rel_tol >= 0 && o.svd_rel_tol < 1)) fail(HSF_ERR_INVALID_ARG, "bad svd_rel_tol");
     if (o.max_dense_block_qubits < 1 || o.max_dense_block_qubits > 12) fail(HSF_ERR_INVALID_ARG, "bad max_dense_block_qubits");

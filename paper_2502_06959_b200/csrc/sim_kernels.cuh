@@ -63,6 +63,26 @@ __device__ __forceinline__ void st2(double2* p, double2 a, double2 b) {
   p[1] = b;
 }
 
+// SMEM layout of a tile: element e lives at sw(e) = e ^ ((e >> 4) & 15).  The
+// XOR folds index bits 4..7 into the bank bits 0..3, so the register passes
+// (a thread owns the 16 amplitudes spanned by 4 tile qubits, often qubits
+// 0..3) and the 1/2-qubit sweeps hit 16 distinct 8-byte bank slots per
+// half-warp instead of one.  sw is an involution (bits 4..7 are unchanged).
+__device__ __forceinline__ int sw(int e) { return e ^ ((e >> 4) & 15); }
+
+// in-place layout conversion linear <-> swizzled (bulk-copied whole states)
+template <typename C, int NT>
+__device__ __forceinline__ void swizzle_inplace(C* s, int nel) {
+  for (int e = threadIdx.x; e < nel; e += NT) {
+    const int f = sw(e);
+    if (f > e) {
+      const C a = s[e], b = s[f];
+      s[e] = b;
+      s[f] = a;
+    }
+  }
+}
+
 constexpr int kSimThreads = 256;      // default CTA (3 CTAs/SM at <= 85 regs)
 constexpr int kSimThreadsWide = 512;  // narrow tree levels: one wide CTA per node
 constexpr int kMaxNonTile = 32;
@@ -120,7 +140,7 @@ __device__ __forceinline__ void apply_dense_k(C* s, int t, const DevOp& op, cons
       for (int j = 0; j < K; ++j) b = ((b >> ps[j]) << (ps[j] + 1)) | (b & ((1 << ps[j]) - 1));
       C v[D];
 #pragma unroll
-      for (int i = 0; i < D; ++i) v[i] = s[b + off[i]];
+      for (int i = 0; i < D; ++i) v[i] = s[sw(b + off[i])];
 #pragma unroll
       for (int i = 0; i < D; ++i) {
         C acc;
@@ -128,7 +148,7 @@ __device__ __forceinline__ void apply_dense_k(C* s, int t, const DevOp& op, cons
         acc.y = 0;
 #pragma unroll
         for (int j = 0; j < D; ++j) acc = cfma(mat[i * D + j], v[j], acc);
-        s[b + off[i]] = acc;
+        s[sw(b + off[i])] = acc;
       }
     }
   } else {
@@ -142,7 +162,7 @@ __device__ __forceinline__ void apply_dense_k(C* s, int t, const DevOp& op, cons
         int o = 0;
 #pragma unroll
         for (int j = 0; j < K; ++j) o |= ((i >> j) & 1) << op.q[j];
-        v[i] = s[b + o];
+        v[i] = s[sw(b + o)];
       }
 #pragma unroll 1
       for (int i = 0; i < D; ++i) {
@@ -153,7 +173,7 @@ __device__ __forceinline__ void apply_dense_k(C* s, int t, const DevOp& op, cons
         for (int j = 0; j < D; ++j) acc = cfma(__ldg(&M[i * D + j]), v[j], acc);
         int o = 0;
         for (int j = 0; j < K; ++j) o |= ((i >> j) & 1) << op.q[j];
-        s[b + o] = acc;
+        s[sw(b + o)] = acc;
       }
     }
   }
@@ -189,7 +209,7 @@ __device__ __forceinline__ void apply_dense_shfl(C* s, int t, const DevOp& op, c
     int b = ok ? g : 0;
 #pragma unroll
     for (int j = 0; j < K; ++j) b = ((b >> ps[j]) << (ps[j] + 1)) | (b & ((1 << ps[j]) - 1));
-    C v = s[b + off];
+    C v = s[sw(b + off)];
     C acc;
     acc.x = 0;
     acc.y = 0;
@@ -200,7 +220,7 @@ __device__ __forceinline__ void apply_dense_shfl(C* s, int t, const DevOp& op, c
       vj.y = __shfl_sync(0xffffffffu, v.y, sub * GS + j);
       acc = cfma(__ldg(&M[r * GS + j]), vj, acc);
     }
-    if (ok) s[b + off] = acc;
+    if (ok) s[sw(b + off)] = acc;
   }
 }
 
@@ -379,6 +399,8 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? (HEAVY ? 2 : 4) : 1)) hsf_pas
 
   if (bulk) {
     mbar_wait0(&load_bar);
+    __syncthreads();
+    swizzle_inplace<C, NT>(s, nel);
   } else if (src) {
     // tiled tier: pairs (e, e+1) are contiguous in global memory (tile
     // position 0 is qubit 0); LB 16-byte requests in flight per thread
@@ -394,8 +416,8 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? (HEAVY ? 2 : 4) : 1)) hsf_pas
       for (int u = 0; u < LB; ++u) {
         const int e = e0 + 2 * NT * u;
         if (e < nel) {
-          s[e] = a[u];
-          s[e + 1] = b[u];
+          s[sw(e)] = a[u];
+          s[sw(e + 1)] = b[u];
         }
       }
     }
@@ -404,7 +426,7 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? (HEAVY ? 2 : 4) : 1)) hsf_pas
       C v;
       v.x = (gidx_of(e) == 0) ? R(1) : R(0);
       v.y = R(0);
-      s[e] = v;
+      s[sw(e)] = v;
     }
   }
   __syncthreads();  // state and staged tables visible to every mapping below
@@ -462,7 +484,7 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? (HEAVY ? 2 : 4) : 1)) hsf_pas
 #pragma unroll
           for (int j = 0; j < kRegQ; ++j)
             if ((k >> j) & 1) e |= ebit[j];
-          v[k] = s[e];
+          v[k] = s[sw(e)];
         }
         for (int r = i + 1; r <= i + n; ++r) {
           const DevOp& d = sops[r];
@@ -508,7 +530,7 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? (HEAVY ? 2 : 4) : 1)) hsf_pas
 #pragma unroll
           for (int j = 0; j < kRegQ; ++j)
             if ((k >> j) & 1) e |= ebit[j];
-          s[e] = v[k];
+          s[sw(e)] = v[k];
         }
       }
       __syncthreads();
@@ -525,7 +547,7 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? (HEAVY ? 2 : 4) : 1)) hsf_pas
         for (int u = 0; u < CH; ++u) {
           const int e = e0 + u * NT;
           if (e < nel) {
-            v[u] = s[e];
+            v[u] = s[sw(e)];
             g[u] = gidx_of(e);
           }
         }
@@ -549,7 +571,7 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? (HEAVY ? 2 : 4) : 1)) hsf_pas
 #pragma unroll
         for (int u = 0; u < CH; ++u) {
           const int e = e0 + u * NT;
-          if (e < nel) s[e] = v[u];
+          if (e < nel) s[sw(e)] = v[u];
         }
       }
       i = j;
@@ -557,12 +579,14 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? (HEAVY ? 2 : 4) : 1)) hsf_pas
   }
   __syncthreads();
   if (whole) {
+    swizzle_inplace<C, NT>(s, nel);
+    __syncthreads();
     if (threadIdx.x == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> async proxy
       bulk_store(dst, s, (uint32_t)(sizeof(C) << p.t));
     }
   } else {
-    for (int e = 2 * threadIdx.x; e < nel; e += 2 * NT) st2(dst + gidx_of(e), s[e], s[e + 1]);
+    for (int e = 2 * threadIdx.x; e < nel; e += 2 * NT) st2(dst + gidx_of(e), s[sw(e)], s[sw(e + 1)]);
   }
 }
 

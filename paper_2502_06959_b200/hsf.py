@@ -102,7 +102,7 @@ class Plan:
     gate-index lists; `individual=True` cuts every crossing gate alone."""
 
     def __init__(self, circuit_text: str, n_low: int, blocks=None, dtype: str = "c64", individual: bool = False,
-                 svd_rel_tol: float = 1e-12, tile_qubits: int = 12, fuse_gates: bool = True,
+                 svd_rel_tol: float = 1e-12, tile_qubits: int = 0, fuse_gates: bool = True,
                  log2_path_budget: float = 26.0, max_dense_block_qubits: int = 10):
         L = lib()
         o = _Opts()

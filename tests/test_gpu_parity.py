@@ -262,3 +262,52 @@ def test_c2_full_size_bf16x3(torch):
     ref = np.exp(2j * np.pi * ((x * rev) % (1 << n)) / (1 << n)) / 2 ** (n / 2)
     md, rel = check(got, ref, "c64")
     print(f"c2 bf16x3 max|d|={md:.3e} relL2={rel:.3e}")
+
+
+@pytest.mark.parametrize("precision", ["simt", "bf16x3"])
+def test_host_output_chunked(torch, precision, monkeypatch):
+    # full output into a host buffer, staged through 2 device chunks of
+    # 128 rows: 8 chunks, copies overlapped with the next chunk's path-sum
+    from paper_2502_06959_b200 import Plan
+    inst = make_config("c4", twin=True, n=20, n_low=10)
+    dev, P = gpu_full(torch, inst, precision=precision)
+    monkeypatch.setenv("HSF_HOST_CHUNK_BYTES", str(128 << 10 << 3))
+    host = torch.empty(1 << inst.n, dtype=torch.complex64).pin_memory()
+    P2 = Plan(inst.text, inst.n_low, inst.blocks)
+    P2.run(host, precision=precision)
+    assert np.array_equal(host.numpy(), dev)
+    n, g = O.parse_circuit(inst.text)
+    check(dev, O.schrodinger(n, g), "c64")
+
+
+def test_c4_full_size_sampled(torch):
+    # BASELINE.json c4 at full size on one GPU: all 2^34 amplitudes (128 GiB
+    # complex64) from the tcgen05 path-sum.  The oracle evaluates the 64 paths'
+    # half-states and recombines 2^16 sampled output indices one by one; the
+    # whole output must carry unit norm (sum over every amplitude).
+    inst = make_config("c4")
+    free, _ = torch.cuda.mem_get_info()
+    if free < (140 << 30):
+        pytest.skip("needs ~140 GB of free device memory")
+    from paper_2502_06959_b200 import Plan
+    P = Plan(inst.text, inst.n_low, inst.blocks)
+    assert P.n_paths == 64
+    out = torch.empty(1 << inst.n, dtype=torch.complex64, device="cuda")
+    P.run(out)
+    torch.cuda.synchronize()
+    norm2 = 0.0
+    flat = torch.view_as_real(out).view(-1)
+    for c0 in range(0, flat.numel(), 1 << 28):  # fp64 sum of |psi|^2 in 1 GiB chunks
+        norm2 += float(torch.sum(flat[c0:c0 + (1 << 28)].double() ** 2))
+    norm = norm2 ** 0.5
+    n, g = O.parse_circuit(inst.text)
+    OP = O.plan(n, g, inst.n_low, inst.blocks)
+    A, B, c = O.half_states(OP)
+    rng = np.random.default_rng(404)
+    idx = rng.integers(0, 1 << n, size=1 << 16, dtype=np.int64)
+    idx[:4] = [0, (1 << n) - 1, (1 << inst.n_low) - 1, 1 << inst.n_low]
+    ref = O.recombine_bits(A, B, c, idx.astype(np.uint64), inst.n_low)
+    got = out[torch.from_numpy(idx).cuda()].cpu().numpy()
+    del out
+    check(got, ref, "c64")
+    assert abs(norm - 1.0) < 1e-4, norm
