@@ -82,6 +82,10 @@ typedef struct {
                                     0 => auto (default): 12, widened to 13 for
                                     complex64 where that saves an HBM pass */
   int32_t fuse_gates;            /* 1 (default) => host gate fusion */
+  int32_t hoist_gates;           /* 1 (default) => commutation-aware path tree: a local gate
+                                    is hoisted above every cut unit whose factors it commutes
+                                    with (disjoint support, or both diagonal), so it runs once
+                                    per shared prefix node; 0 => schedule order */
 } hsf_plan_opts;
 
 typedef struct hsf_plan_s hsf_plan_t; /* opaque */

@@ -18,7 +18,10 @@
 //   warp 0  TMA producer (cp.async.bulk.tensor, SWIZZLE_128B, mbarrier tx)
 //   warp 1  TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=256,
 //           K=16 per instruction), tcgen05.commit -> smem/TMEM barriers
-//   warps 2-5 epilogue: tcgen05.ld 32x32b -> registers -> global fp32
+//   warps 2-5 epilogue: tcgen05.ld 32x32b -> registers -> st.shared into a
+//           128B-swizzled 32x32 fp32 box -> TMA store (cp.async.bulk.tensor,
+//           bulk_group, double-buffered per warp), so the output is written
+//           as full 128 B row segments by the TMA engine
 //   2 SMEM stages x (16+16+32+32) KB, 2 TMEM accumulators x 256 columns.
 #pragma once
 #include <cuda.h>
@@ -36,12 +39,15 @@ constexpr int STAGES = 2;
 constexpr int A_TILE = BM * BK * 2;  // 16 KB
 constexpr int B_TILE = BN * BK * 2;  // 32 KB
 constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024;  // + alignment slack
+constexpr int EPI_BYTES = 4 * 2 * 4096;  // per epilogue warp: 2 staging boxes of 32 rows x 128 B
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024;  // + alignment slack
 constexpr int THREADS = 192;
 constexpr int TMEM_COLS = 512;  // 2 accumulators x 256 fp32 columns
 
 struct Params {
   int num_m, num_n, num_k;  // blocks
+  int n_fastest;            // tile raster: 1 => consecutive tiles walk N (output-write-bound
+                            // shapes: neighbouring CTAs write adjacent row segments)
   int x3;
   float* out;               // D, row-major, ld = ldo floats
   long long ldo;
@@ -79,6 +85,11 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   // UMMA shared-memory descriptor, K-major, SWIZZLE_128B: start>>4, LBO=1 (unused),
   // SBO=1024 B between 8-row swizzle atoms, version 1 (sm_100), layout type 2.
@@ -103,10 +114,20 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
+__device__ __forceinline__ void tile_coords(const Params& p, int tile, int& mb, int& nb) {
+  if (p.n_fastest) {
+    mb = tile / p.num_n;
+    nb = tile % p.num_n;
+  } else {
+    mb = tile % p.num_m;
+    nb = tile / p.num_m;
+  }
+}
+
 __global__ void __launch_bounds__(THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUtensorMap mA_lo,
                    const __grid_constant__ CUtensorMap mB_hi, const __grid_constant__ CUtensorMap mB_lo,
-                   const Params p) {
+                   const __grid_constant__ CUtensorMap mOut, const Params p) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES], tfull_bar[2], tempty_bar[2];
   __shared__ uint32_t tmem_base_sh;
@@ -150,7 +171,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       int s = 0;
       uint32_t ph = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int mb = tile % p.num_m, nb = tile / p.num_m;
+        int mb, nb;
+        tile_coords(p, tile, mb, nb);
         for (int kb = 0; kb < p.num_k; ++kb) {
           mbar_wait(&empty_bar[s], ph ^ 1);
           uint8_t* st = smem + s * STAGE_BYTES;
@@ -208,17 +230,15 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else {
     // ---------------------------------------------------------------- epilogue
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
-    const int row = q * 32 + lane;
-    int acc = 0;
+    const int q = warp & 3;  // TMEM lane quarter this warp may access (rows 32q..32q+31)
+    uint8_t* stg = smem + STAGES * STAGE_BYTES + q * 8192;  // 1024-aligned, 2 x 4 KB
+    int acc = 0, buf = 0;
     uint32_t aph = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      const int mb = tile % p.num_m, nb = tile / p.num_m;
+      int mb, nb;
+      tile_coords(p, tile, mb, nb);
       mbar_wait(&tfull_bar[acc], aph);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      const long long gi = (long long)mb * BM + row;
-      const long long gc0 = (long long)nb * BN;
-      float* orow = p.out + gi * p.ldo;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t v[32];
@@ -233,28 +253,33 @@ __global__ void __launch_bounds__(THREADS, 1)
               "=r"(v[30]), "=r"(v[31])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        const long long gc = gc0 + c * 32;
-        if (gi < p.rows) {
-          if (gc + 32 <= p.cols) {
-            float4* o4 = reinterpret_cast<float4*>(orow + gc);
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              o4[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
-                                  __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (gc + j < p.cols) orow[gc + j] = __uint_as_float(v[j]);
-          }
+        if (c == BN / 32 - 1) {  // accumulator fully read: release it to the MMA warp
+          asm volatile("tcgen05.fence::before_thread_sync;");
+          mbar_arrive(&tempty_bar[acc]);
         }
+        // the TMA store issued from this buffer two chunks ago must have read it
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncwarp();
+        // row `lane` of the 32x32 box, 128B swizzle: 16 B chunk j at j ^ (row & 7)
+        float4* dst = reinterpret_cast<float4*>(stg + buf * 4096 + lane * 128);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          dst[j ^ (lane & 7)] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                            __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async proxy
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&mOut, stg + buf * 4096, nb * BN + c * 32, mb * BM + q * 32);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        buf ^= 1;
       }
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      mbar_arrive(&tempty_bar[acc]);
       if (++acc == 2) {
         acc = 0;
         aph ^= 1;
       }
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -379,6 +404,20 @@ inline CUtensorMap make_map(void* base, long long rows, long long cols_bf16, int
   return m;
 }
 
+// fp32 output [rows][cols] (row-major, cols = 2*MB), 32x32 boxes, 128B swizzle
+inline CUtensorMap make_out_map(float* base, long long rows, long long cols) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(HSF_ERR_CUDA, "cuTensorMapEncodeTiled (output) failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
 inline int num_sms() {
   static int n = 0;
   if (!n) {
@@ -445,6 +484,10 @@ inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row
   p.num_n = (int)(t.d.nrows_b_pad / tc::BN);
   p.num_k = (int)(kcols / tc::BK);
   p.x3 = x3 ? 1 : 0;
+  // short K (c4: K'' = 128): the kernel is output-write-bound and its operands
+  // are L2-resident, so walk N for DRAM locality of the stores; long K (c2):
+  // walk M so concurrent tiles share B tiles in L2
+  p.n_fastest = (p.num_k <= 4) ? 1 : 0;
   p.out = (float*)out;
   p.ldo = 2 * MB;
   p.rows = rows;
@@ -458,7 +501,8 @@ inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row
   }
   const long long tiles = (long long)p.num_m * p.num_n;
   const int grid = (int)std::min<long long>(tiles, num_sms());
-  tc::tc_gemm_kernel<<<grid, tc::THREADS, tc::SMEM_BYTES, st>>>(mAh, mAl, mBh, mBl, p);
+  CUtensorMap mO = make_out_map((float*)out, rows, 2 * MB);
+  tc::tc_gemm_kernel<<<grid, tc::THREADS, tc::SMEM_BYTES, st>>>(mAh, mAl, mBh, mBl, mO, p);
   e = cudaGetLastError();
   if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("tc_gemm: ") + cudaGetErrorString(e));
 }

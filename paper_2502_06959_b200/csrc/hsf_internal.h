@@ -108,6 +108,7 @@ struct Half {
   std::vector<Transition> trans;
   std::vector<DevOp> dev_ops;
   int n_passes = 0;
+  double est_ms = 0;                 // planner's cost-model estimate of the tree (all paths)
 };
 
 struct Plan {

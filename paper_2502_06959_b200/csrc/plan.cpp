@@ -703,10 +703,37 @@ static void build_half(Plan& P, int h, const std::vector<SchedItem>& order) {
   H.m = (h == 0) ? P.n - n_low : n_low;
   if (H.m > 30) fail(HSF_ERR_UNSUPPORTED, "half-states above 30 qubits are not supported (32-bit device indexing)");
   const int U = (int)P.units.size();
-  // segments
+  // segments.  Factor of unit u opens segment u+1.  With hoisting (default),
+  // each local gate goes to the EARLIEST level its dependencies allow: it
+  // must follow every earlier op on a shared qubit that it does not commute
+  // with (commuting = both diagonal); a factor pins level u+1.  A gate that
+  // commutes with a unit's factors (disjoint support, or both diagonal) thus
+  // runs once per prefix node above that unit instead of once per child --
+  // the same circuit (every reordering swaps commuting operators only),
+  // evaluated on fewer path-tree nodes.
   std::vector<std::vector<HostOp>> segs(U + 1);
   std::vector<HostOp> factors(U);
   int level = 0;
+  const bool hoist = P.opts.hoist_gates != 0;
+  std::vector<int> last_nd(H.m, 0), diag_max(H.m, 0);  // per half-local qubit
+  auto dep_level = [&](const HostOp& op) {
+    int l = 0;
+    for (int j = 0; j < op.k; ++j) {
+      l = std::max(l, last_nd[op.q[j]]);
+      if (op.kind != OP_DIAG) l = std::max(l, diag_max[op.q[j]]);
+    }
+    return l;
+  };
+  auto record = [&](const HostOp& op, int l) {
+    for (int j = 0; j < op.k; ++j) {
+      if (op.kind == OP_DIAG) {
+        diag_max[op.q[j]] = std::max(diag_max[op.q[j]], l);
+      } else {
+        last_nd[op.q[j]] = l;
+        diag_max[op.q[j]] = l;
+      }
+    }
+  };
   for (const SchedItem& it : order) {
     if (it.unit) {
       const Unit& u = P.units[it.id];
@@ -725,6 +752,8 @@ static void build_half(Plan& P, int h, const std::vector<SchedItem>& order) {
       op.stride = (int64_t)F[0].size();
       factors[it.id] = op;
       level = it.id + 1;
+      if (dep_level(op) > level) fail(HSF_ERR_INVALID_ARG, "internal: factor below its dependencies");
+      record(op, level);
     } else {
       const Gate& g = P.gates[it.id];
       bool low = true, high = true;
@@ -736,7 +765,9 @@ static void build_half(Plan& P, int h, const std::vector<SchedItem>& order) {
         HostOp op = gate_op(P, g, H.first_qubit);
         if (op.kind == OP_DENSE && op.k > kMaxDenseQ) fail(HSF_ERR_UNSUPPORTED, "dense local gate on more than 5 qubits");
         if (op.kind == OP_DIAG && op.k > kMaxOpQ) fail(HSF_ERR_UNSUPPORTED, "diagonal local gate on more than 13 qubits");
-        segs[level].push_back(op);
+        const int l = hoist ? dep_level(op) : level;
+        record(op, l);
+        segs[l].push_back(op);
       }
     }
   }
@@ -750,23 +781,75 @@ static void build_half(Plan& P, int h, const std::vector<SchedItem>& order) {
     for (auto& op : segs[l]) H.ops.push_back(op);
     H.seg_end[l] = (int64_t)H.ops.size();
   }
-  // materialised levels: those followed by a dense op in their segment, plus the leaves
-  // A level is materialised (its node states written to HBM/L2) when the work
-  // a child would otherwise redo is heavy: a dense op in its segment, or a
-  // wide diagonal (> 2^8-entry table, not L1-resident) in the factor that
-  // leads to it or in its segment.  Otherwise children recompute it on chip.
-  H.materialized.clear();
-  for (int l = 0; l < U; ++l) {
-    bool heavy = false;
-    for (auto& op : segs[l]) heavy = heavy || op.kind == OP_DENSE || (op.kind == OP_DIAG && op.k > kFuseDiagQ);
-    if (l > 0) heavy = heavy || factors[l - 1].kind == OP_DENSE || factors[l - 1].k > kFuseDiagQ;
-    if (heavy) H.materialized.push_back(l);
-  }
-  H.materialized.push_back(U);
-  // transitions + passes
+  // Materialised levels (node states written to HBM/L2; the others are
+  // recomputed on chip by their children): chosen by dynamic programming over
+  // the levels with a per-transition cost model --
+  //   launches x 3 us + state bytes / 5 TB/s + wide diagonal table bytes /
+  //   15 TB/s (L2) + amplitude-ops / 2.5e13 FMA/s,
+  // where a transition a -> b writes every level-b node once per pass, reads
+  // its level-a parent (siblings mostly hit L2) and re-applies all ops of the
+  // skipped levels per child.  The leaves (level U) are always materialised.
   const int smem_limit = (P.opts.dtype == HSF_C64) ? 13 : 12;
   const int t = std::min(H.m, P.opts.tile_qubits > 0 ? P.opts.tile_qubits : 12);
   const int t_max = (P.opts.tile_qubits == 0 && P.opts.dtype == HSF_C64) ? 13 : t;
+  const bool whole = H.m <= smem_limit;
+  {
+    const double elem = (P.opts.dtype == HSF_C64) ? 8.0 : 16.0;
+    const double amps = std::ldexp(1.0, H.m), S = amps * elem;
+    auto nodes = [&](int l) { return (double)range_prod(P.ranks, 0, l); };
+    auto cost = [&](int a, int b) {
+      const int64_t ob = (a < 0) ? 0 : H.seg_end[a], oe = H.seg_end[b];
+      size_t np = 1;
+      int tt = H.m;
+      if (!whole) {
+        np = greedy_passes(H, ob, oe, t).size();
+        tt = t;
+        for (int t2 = t + 1; t2 <= t_max && t2 <= H.m; ++t2) {
+          size_t n2 = greedy_passes(H, ob, oe, t2).size();
+          if (n2 < np) {
+            np = n2;
+            tt = t2;
+          }
+        }
+      }
+      const double Nb = nodes(b), Na = (a < 0) ? 0.0 : nodes(a);
+      double bytes = 0;
+      for (size_t i = 0; i < np; ++i) {
+        const double rd = (i == 0) ? ((a < 0) ? 0.0 : S * (Na + 0.3 * (Nb - Na))) : S * Nb;
+        bytes += rd + S * Nb;
+      }
+      double fma = 0, table = 0;
+      const double tiles = std::ldexp(1.0, H.m - tt);
+      for (int64_t i = ob; i < oe; ++i) {
+        const HostOp& op = H.ops[i];
+        if (op.kind == OP_DIAG) {
+          fma += 6;
+          if (op.k > kSmemTableQ) table += Nb * tiles * std::ldexp(1.0, std::min(op.k, tt)) * elem;
+        } else {
+          fma += 4.0 * std::ldexp(1.0, op.k);
+        }
+      }
+      return 3e-6 * (double)np + bytes / 5e12 + table / 15e12 + fma * amps * Nb / 2.5e13;
+    };
+    std::vector<double> best(U + 1, 1e300);
+    std::vector<int> from(U + 1, -1);
+    for (int b2 = 0; b2 <= U; ++b2) {
+      best[b2] = cost(-1, b2);
+      from[b2] = -1;
+      for (int a2 = 0; a2 < b2; ++a2) {
+        const double c = best[a2] + cost(a2, b2);
+        if (c < best[b2]) {
+          best[b2] = c;
+          from[b2] = a2;
+        }
+      }
+    }
+    H.materialized.clear();
+    for (int l = U; l >= 0; l = from[l]) H.materialized.push_back(l);
+    std::reverse(H.materialized.begin(), H.materialized.end());
+    H.est_ms = best[U] * 1e3;
+  }
+  // transitions + passes
   H.trans.clear();
   H.dev_ops.clear();
   H.n_passes = 0;
@@ -777,7 +860,7 @@ static void build_half(Plan& P, int h, const std::vector<SchedItem>& order) {
     tr.level_out = L;
     int64_t ob = (prev < 0) ? 0 : H.seg_end[prev];
     int64_t oe = H.seg_end[L];
-    if (H.m <= smem_limit) {
+    if (whole) {
       Pass p;
       p.t = H.m;
       for (int i = 0; i < H.m; ++i) p.T.push_back(i);
@@ -824,7 +907,7 @@ static void build_half(Plan& P, int h, const std::vector<SchedItem>& order) {
   finalize_half(H, P.opts.dtype == HSF_C64 ? 8 : 16);
   if (std::getenv("HSF_DEBUG_PLAN")) {
     static const char* kn[] = {"DENSE", "DIAG", "RPASS", "R1"};
-    std::fprintf(stderr, "half %c: m=%d levels=%zu\n", h == 0 ? 'A' : 'B', H.m, H.materialized.size());
+    std::fprintf(stderr, "half %c: m=%d levels=%zu est=%.3f ms\n", h == 0 ? 'A' : 'B', H.m, H.materialized.size(), H.est_ms);
     for (auto& tr : H.trans) {
       std::fprintf(stderr, " trans %d->%d passes=%zu\n", tr.level_in, tr.level_out, tr.passes.size());
       for (auto& p : tr.passes) {

@@ -508,6 +508,7 @@ hsf_status hsf_plan_opts_default(hsf_plan_opts* o) {
   o->individual = 0;
   o->tile_qubits = 0;
   o->fuse_gates = 1;
+  o->hoist_gates = 1;
   return HSF_OK;
 }
 

@@ -311,3 +311,33 @@ def test_c4_full_size_sampled(torch):
     del out
     check(got, ref, "c64")
     assert abs(norm - 1.0) < 1e-4, norm
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_hoisting_and_tree_shape_invariant(torch, seed):
+    # the commutation-aware path tree (hoist_gates=True, default) and the plain
+    # schedule-order tree evaluate the same circuit: both match the oracle
+    inst = random_small_circuit(100 + seed, n=10 + seed % 4, n_gates=40 + 5 * seed)
+    n, g = O.parse_circuit(inst.text)
+    if O.plan(n, g, inst.n_low, inst.blocks).n_paths > 4096:
+        inst = random_small_circuit(100 + seed, n=10, n_gates=20)
+        n, g = O.parse_circuit(inst.text)
+    ref = O.schrodinger(n, g)
+    for hoist in (True, False):
+        got, _ = gpu_full(torch, inst, dtype="c128", precision="simt", hoist_gates=hoist)
+        check(got, ref, "c128")
+        got, _ = gpu_full(torch, inst, dtype="c64", precision="simt", hoist_gates=hoist, tile_qubits=10)
+        check(got, ref, "c64")
+
+
+@pytest.mark.parametrize("name", ["c3", "c5"])
+def test_hoisting_tiled_twins(torch, name):
+    # 2^14-amplitude halves through the tiled (K2) tier with and without hoisting
+    inst = make_config(name, twin=True, n=28, n_low=14, n_bits=4096)
+    n, g = O.parse_circuit(inst.text)
+    P = O.plan(n, g, inst.n_low, inst.blocks)
+    A, B, c = O.half_states(P, 0, 8)
+    ref = O.recombine_bits(A, B, c, inst.bitstrings, inst.n_low)
+    for hoist in (True, False):
+        got, _ = gpu_bits(torch, inst, inst.bitstrings, path_range=(0, 8), hoist_gates=hoist)
+        check(got, ref, "c64")
