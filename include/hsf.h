@@ -86,6 +86,10 @@ typedef struct {
                                     is hoisted above every cut unit whose factors it commutes
                                     with (disjoint support, or both diagonal), so it runs once
                                     per shared prefix node; 0 => schedule order */
+  int32_t fold_trailing_diag;    /* 1 (default) => bitstring runs fold trailing all-diagonal
+                                    units with no gate after them into a per-sample weight
+                                    (the block's diagonal at the sample's bits) instead of
+                                    extending the path tree; results are identical */
 } hsf_plan_opts;
 
 typedef struct hsf_plan_s hsf_plan_t; /* opaque */
@@ -129,6 +133,7 @@ typedef struct {
   int32_t passes_a, passes_b;   /* device passes over all levels per half */
   int32_t ops_a, ops_b;         /* device ops after fusion */
   uint64_t plan_hash;           /* FNV-1a of the device program + tables */
+  int32_t fold_units;           /* trailing diagonal units folded in bitstring runs (0 = none) */
 } hsf_plan_info;
 
 /* Pointers in *info stay valid until hsf_plan_free. */

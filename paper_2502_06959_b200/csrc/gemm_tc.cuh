@@ -18,10 +18,11 @@
 //   warp 0  TMA producer (cp.async.bulk.tensor, SWIZZLE_128B, mbarrier tx)
 //   warp 1  TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=256,
 //           K=16 per instruction), tcgen05.commit -> smem/TMEM barriers
-//   warps 2-5 epilogue: tcgen05.ld 32x32b -> registers -> st.shared into a
+//   warps 2-9 epilogue (2 per TMEM lane quarter, alternating 32-column
+//           chunks): tcgen05.ld 32x32b -> registers -> st.shared into a
 //           128B-swizzled 32x32 fp32 box -> TMA store (cp.async.bulk.tensor,
-//           bulk_group, double-buffered per warp), so the output is written
-//           as full 128 B row segments by the TMA engine
+//           bulk_group, L2 evict-first), so the output is written as full
+//           128 B row segments by the TMA engine
 //   2 SMEM stages x (16+16+32+32) KB, 2 TMEM accumulators x 256 columns.
 #pragma once
 #include <cuda.h>
@@ -39,15 +40,16 @@ constexpr int STAGES = 2;
 constexpr int A_TILE = BM * BK * 2;  // 16 KB
 constexpr int B_TILE = BN * BK * 2;  // 32 KB
 constexpr int STAGE_BYTES = 2 * A_TILE + 2 * B_TILE;
-constexpr int EPI_BYTES = 4 * 2 * 4096;  // per epilogue warp: 2 staging boxes of 32 rows x 128 B
+constexpr int EPI_WARPS = 8;             // 2 per TMEM lane quarter, alternating 32-column chunks
+constexpr int EPI_BYTES = EPI_WARPS * 4096;  // per epilogue warp: one 32 x 128 B staging box
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024;  // + alignment slack
-constexpr int THREADS = 192;
+constexpr int THREADS = 64 + 32 * EPI_WARPS;
 constexpr int TMEM_COLS = 512;  // 2 accumulators x 256 fp32 columns
 
 struct Params {
   int num_m, num_n, num_k;  // blocks
-  int n_fastest;            // tile raster: 1 => consecutive tiles walk N (output-write-bound
-                            // shapes: neighbouring CTAs write adjacent row segments)
+  int n_fastest;            // tile raster: 1 => consecutive tiles walk N
+  int a_evict_last;         // 1 => A operand loads carry an L2 evict-last hint
   int x3;
   float* out;               // D, row-major, ld = ldo floats
   long long ldo;
@@ -85,10 +87,36 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
-__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
-  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
-               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                                 uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, "
+      "%4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+// output tiles are written once and never re-read by this kernel: evict-first
+// so the streaming stores do not push the re-used operand tiles out of L2
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1, uint64_t policy) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;" ::"l"(
+                   map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "l"(policy)
                : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   // UMMA shared-memory descriptor, K-major, SWIZZLE_128B: start>>4, LBO=1 (unused),
@@ -143,7 +171,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 128);
+      mbar_init(&tempty_bar[a], 32 * EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mA_hi) : "memory");
@@ -168,6 +196,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA producer
     if (lane == 0) {
+      // A row-block tiles are re-read once per N tile: keep them in L2 when the
+      // whole A operand fits comfortably (c4); otherwise normal priority
+      const uint64_t a_pol = p.a_evict_last ? policy_evict_last() : policy_evict_normal();
       int s = 0;
       uint32_t ph = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -177,10 +208,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           mbar_wait(&empty_bar[s], ph ^ 1);
           uint8_t* st = smem + s * STAGE_BYTES;
           mbar_expect_tx(&full_bar[s], stage_bytes);
-          tma_load_2d(st, &mA_hi, &full_bar[s], kb * BK, mb * BM);
+          tma_load_2d_hint(st, &mA_hi, &full_bar[s], kb * BK, mb * BM, a_pol);
           tma_load_2d(st + 2 * A_TILE, &mB_hi, &full_bar[s], kb * BK, nb * BN);
           if (p.x3) {
-            tma_load_2d(st + A_TILE, &mA_lo, &full_bar[s], kb * BK, mb * BM);
+            tma_load_2d_hint(st + A_TILE, &mA_lo, &full_bar[s], kb * BK, mb * BM, a_pol);
             tma_load_2d(st + 2 * A_TILE + B_TILE, &mB_lo, &full_bar[s], kb * BK, nb * BN);
           }
           if (++s == STAGES) {
@@ -230,9 +261,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else {
     // ---------------------------------------------------------------- epilogue
+    const uint64_t st_pol = policy_evict_first();
     const int q = warp & 3;  // TMEM lane quarter this warp may access (rows 32q..32q+31)
-    uint8_t* stg = smem + STAGES * STAGE_BYTES + q * 8192;  // 1024-aligned, 2 x 4 KB
-    int acc = 0, buf = 0;
+    const int half = (warp - 2) / 4;  // which alternate chunks this warp drains
+    uint8_t* stg = smem + STAGES * STAGE_BYTES + (warp - 2) * 4096;  // 1024-aligned 4 KB box
+    int acc = 0;
     uint32_t aph = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       int mb, nb;
@@ -240,7 +273,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_wait(&tfull_bar[acc], aph);
       asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = half; c < BN / 32; c += 2) {
         uint32_t v[32];
         const uint32_t taddr = tmem_base + (uint32_t)(acc * BN + c * 32) + ((uint32_t)(q * 32) << 16);
         asm volatile(
@@ -253,15 +286,16 @@ __global__ void __launch_bounds__(THREADS, 1)
               "=r"(v[30]), "=r"(v[31])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (c == BN / 32 - 1) {  // accumulator fully read: release it to the MMA warp
+        if (c >= BN / 32 - 2) {  // this warp's last chunk read: release its share of the accumulator
           asm volatile("tcgen05.fence::before_thread_sync;");
           mbar_arrive(&tempty_bar[acc]);
         }
-        // the TMA store issued from this buffer two chunks ago must have read it
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        // the previous TMA store from this box must have finished reading it
+        // (overlapped with the tcgen05.ld above)
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncwarp();
         // row `lane` of the 32x32 box, 128B swizzle: 16 B chunk j at j ^ (row & 7)
-        float4* dst = reinterpret_cast<float4*>(stg + buf * 4096 + lane * 128);
+        float4* dst = reinterpret_cast<float4*>(stg + lane * 128);
 #pragma unroll
         for (int j = 0; j < 8; ++j)
           dst[j ^ (lane & 7)] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
@@ -269,10 +303,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async proxy
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d(&mOut, stg + buf * 4096, nb * BN + c * 32, mb * BM + q * 32);
+          tma_store_2d(&mOut, stg, nb * BN + c * 32, mb * BM + q * 32, st_pol);
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
-        buf ^= 1;
       }
       if (++acc == 2) {
         acc = 0;
@@ -484,10 +517,13 @@ inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row
   p.num_n = (int)(t.d.nrows_b_pad / tc::BN);
   p.num_k = (int)(kcols / tc::BK);
   p.x3 = x3 ? 1 : 0;
-  // short K (c4: K'' = 128): the kernel is output-write-bound and its operands
-  // are L2-resident, so walk N for DRAM locality of the stores; long K (c2):
-  // walk M so concurrent tiles share B tiles in L2
-  p.n_fastest = (p.num_k <= 4) ? 1 : 0;
+  // M-fastest raster: the ~148 concurrent tiles share one B tile (read once
+  // from DRAM) and sweep A; A stays L2-resident (evict-last) when it is small
+  // (c4: 64 MiB for hi+lo), while the streaming output stores are evict-first.
+  // (N-fastest re-reads all of B per row block: 7 GB of DRAM reads per 1/16
+  // of c4, ncu profiles/r01.)
+  p.n_fastest = 0;
+  p.a_evict_last = ((x3 ? 2 : 1) * rpad * kcols * 2 <= (64ll << 20)) ? 1 : 0;
   p.out = (float*)out;
   p.ldo = 2 * MB;
   p.rows = rows;

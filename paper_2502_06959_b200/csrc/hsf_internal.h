@@ -57,6 +57,7 @@ constexpr int kSmemTableQ = 8;     // diag tables with <= 2^8 entries are staged
 constexpr int kSmemTableBytes = 48 * 1024;  // per-pass cap on staged tables
 constexpr int kMaxOpQ = 13;      // widest diagonal op (2^13 entries)
 constexpr int kMaxDenseQ = 5;    // widest dense op in the SMEM kernels
+constexpr int kMaxTrail = 8;     // folded trailing diagonal units (bitstring runs)
 
 // One operation of a half-circuit program (half-local qubits, LSB-first:
 // q[j] is bit j of the op's local index).
@@ -109,6 +110,7 @@ struct Half {
   std::vector<DevOp> dev_ops;
   int n_passes = 0;
   double est_ms = 0;                 // planner's cost-model estimate of the tree (all paths)
+  int last_gate_level = 0;           // deepest level holding a local gate
 };
 
 struct Plan {
@@ -123,6 +125,13 @@ struct Plan {
   double log2_individual = 0;
   std::vector<cd> coef;             // all device matrices (fp64 master copy)
   Half half[2];                     // 0 = A (high), 1 = B (low)
+  // trailing-diagonal fold (bitstring runs; see build_plan)
+  int fold_u0 = -1;                 // tree depth of the folded variant, -1 => none
+  uint64_t fold_T = 1;              // product of the folded units' ranks
+  Half half_fold[2];
+  std::vector<uint64_t> trail_mask; // per folded unit: global support bits
+  std::vector<int64_t> trail_off;   // per folded unit: offset into trail_tab
+  std::vector<cd> trail_tab;        // per folded unit: block diagonal D_u over its support
   uint64_t hash = 0;
   void* dev = nullptr;              // device state (run.cu)
 };

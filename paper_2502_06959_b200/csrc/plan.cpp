@@ -696,13 +696,16 @@ static void finalize_half(Half& H, size_t elem_bytes) {
   H.dev_ops.swap(out);
 }
 
-static void build_half(Plan& P, int h, const std::vector<SchedItem>& order) {
-  Half& H = P.half[h];
+// Builds half h's path-tree program over the first U_tree units (U_tree <
+// n_units only for the trailing-diagonal fold, whose dropped units carry no
+// gate after them).
+static void build_half(Plan& P, int h, const std::vector<SchedItem>& order, int U_tree, Half& H) {
   const int n_low = P.n_low;
   H.first_qubit = (h == 0) ? n_low : 0;
   H.m = (h == 0) ? P.n - n_low : n_low;
   if (H.m > 30) fail(HSF_ERR_UNSUPPORTED, "half-states above 30 qubits are not supported (32-bit device indexing)");
-  const int U = (int)P.units.size();
+  const int U = U_tree;
+  H.last_gate_level = 0;
   // segments.  Factor of unit u opens segment u+1.  With hoisting (default),
   // each local gate goes to the EARLIEST level its dependencies allow: it
   // must follow every earlier op on a shared qubit that it does not commute
@@ -735,6 +738,7 @@ static void build_half(Plan& P, int h, const std::vector<SchedItem>& order) {
     }
   };
   for (const SchedItem& it : order) {
+    if (it.unit && it.id >= U_tree) continue;  // folded trailing unit (diagonal, nothing after it)
     if (it.unit) {
       const Unit& u = P.units[it.id];
       const std::vector<int>& S = (h == 0) ? u.Sa : u.Sb;
@@ -766,8 +770,10 @@ static void build_half(Plan& P, int h, const std::vector<SchedItem>& order) {
         if (op.kind == OP_DENSE && op.k > kMaxDenseQ) fail(HSF_ERR_UNSUPPORTED, "dense local gate on more than 5 qubits");
         if (op.kind == OP_DIAG && op.k > kMaxOpQ) fail(HSF_ERR_UNSUPPORTED, "diagonal local gate on more than 13 qubits");
         const int l = hoist ? dep_level(op) : level;
+        if (l > U) fail(HSF_ERR_INVALID_ARG, "internal: gate below a folded unit");
         record(op, l);
         segs[l].push_back(op);
+        H.last_gate_level = std::max(H.last_gate_level, l);
       }
     }
   }
@@ -1012,14 +1018,54 @@ Plan* build_plan(const char* text, size_t len, int n_low, int64_t n_blocks, cons
     P->sigma_off.push_back((int64_t)P->sigmas.size());
   }
   // H8
-  build_half(*P, 0, order);
-  build_half(*P, 1, order);
+  const int U = (int)P->units.size();
+  build_half(*P, 0, order, U, P->half[0]);
+  build_half(*P, 1, order, U, P->half[1]);
+  // Trailing-diagonal fold (bitstring runs): when the last units are all
+  // diagonal and no gate follows them in either half (after hoisting), their
+  // factors commute to the end of both half-circuits, so for an output sample
+  // s = (i_A, i_B) the sum over their Schmidt terms collapses to a scalar:
+  //   amp(s) = [prod_u sum_d c_{u,d} X_{u,d}(i_A) Y_{u,d}(i_B)] * sum_{p'} c_p' A_p'(i_A) B_p'(i_B)
+  // and the bracket is the block's diagonal D_u evaluated at s's support bits
+  // (P:104-109 regrouped).  The path tree then stops at level u0.
+  P->fold_u0 = -1;
+  if (opts.fold_trailing_diag && U > 0 && P->n <= 63) {
+    int u0 = std::max({P->half[0].last_gate_level, P->half[1].last_gate_level, U - kMaxTrail});
+    for (int u = U - 1; u >= u0; --u)
+      if (!P->units[u].diag_route || P->units[u].support.size() > 16) {
+        u0 = u + 1;
+        break;
+      }
+    if (u0 < U) {
+      P->fold_u0 = u0;
+      P->fold_T = range_prod(P->ranks, u0, U);
+      build_half(*P, 0, order, u0, P->half_fold[0]);
+      build_half(*P, 1, order, u0, P->half_fold[1]);
+      for (int u = u0; u < U; ++u) {
+        const Unit& un = P->units[u];
+        const int ka = (int)un.Sa.size(), kb = (int)un.Sb.size();
+        uint64_t mask = 0;
+        for (int q : un.support) mask |= 1ull << q;
+        P->trail_mask.push_back(mask);
+        P->trail_off.push_back((int64_t)P->trail_tab.size());
+        for (size_t x = 0; x < ((size_t)1 << (ka + kb)); ++x) {
+          const size_t xb = x & (((size_t)1 << kb) - 1), xa = x >> kb;
+          cd v = 0;
+          for (int d = 0; d < un.rank; ++d) v += un.c[d] * un.X[d][xa] * un.Y[d][xb];
+          P->trail_tab.push_back(v);
+        }
+      }
+    }
+  }
   // hash
   uint64_t h = 1469598103934665603ull;
   h = fnv(h, &P->n, sizeof(int));
   h = fnv(h, &P->n_low, sizeof(int));
-  for (int s = 0; s < 2; ++s)
+  for (int s = 0; s < 2; ++s) {
     h = fnv(h, P->half[s].dev_ops.data(), P->half[s].dev_ops.size() * sizeof(DevOp));
+    h = fnv(h, P->half_fold[s].dev_ops.data(), P->half_fold[s].dev_ops.size() * sizeof(DevOp));
+  }
+  h = fnv(h, P->trail_tab.data(), P->trail_tab.size() * sizeof(cd));
   h = fnv(h, P->coef.data(), P->coef.size() * sizeof(cd));
   h = fnv(h, P->ranks.data(), P->ranks.size() * sizeof(int32_t));
   P->hash = h;

@@ -33,12 +33,15 @@ struct DeviceState {
   size_t elem = 8;          // bytes per complex
   void* coef = nullptr;     // complex table (run dtype)
   DevOp* ops[2] = {nullptr, nullptr};
+  DevOp* ops_fold[2] = {nullptr, nullptr};  // trailing-diagonal fold variant
+  void* trail = nullptr;                    // folded units' block diagonals (run dtype)
   void* ws = nullptr;
   size_t ws_bytes = 0;
   // cached per-range path coefficients
   void* cp = nullptr;
   size_t cp_cap = 0;
   uint64_t cp_p0 = ~0ull, cp_p1 = ~0ull;
+  int cp_units = -1;
   cudaEvent_t ev[6] = {};
   cudaEvent_t evg[2] = {}, evc[2] = {};  // host-output chunks: GEMM done / D2H done
   cudaStream_t side = nullptr;  // half-B stream; D2H stream of host-output chunks
@@ -54,6 +57,9 @@ void destroy_device(Plan* p) {
   cudaFree(d->coef);
   cudaFree(d->ops[0]);
   cudaFree(d->ops[1]);
+  cudaFree(d->ops_fold[0]);
+  cudaFree(d->ops_fold[1]);
+  cudaFree(d->trail);
   cudaFree(d->ws);
   cudaFree(d->cp);
   for (auto& e : d->ev)
@@ -90,12 +96,26 @@ static DeviceState* ensure_device(Plan* P, int device) {
   } else {
     CK(cudaMemcpy(d->coef, P->coef.data(), P->coef.size() * 16, cudaMemcpyHostToDevice));
   }
+  auto upload_ops = [&](const Half& H, DevOp** dst) {
+    size_t no = std::max<size_t>(H.dev_ops.size(), 1);
+    CK(cudaMalloc(dst, no * sizeof(DevOp)));
+    if (!H.dev_ops.empty())
+      CK(cudaMemcpy(*dst, H.dev_ops.data(), H.dev_ops.size() * sizeof(DevOp), cudaMemcpyHostToDevice));
+  };
   for (int h = 0; h < 2; ++h) {
-    size_t no = std::max<size_t>(P->half[h].dev_ops.size(), 1);
-    CK(cudaMalloc(&d->ops[h], no * sizeof(DevOp)));
-    if (!P->half[h].dev_ops.empty())
-      CK(cudaMemcpy(d->ops[h], P->half[h].dev_ops.data(), P->half[h].dev_ops.size() * sizeof(DevOp),
-                    cudaMemcpyHostToDevice));
+    upload_ops(P->half[h], &d->ops[h]);
+    if (P->fold_u0 >= 0) upload_ops(P->half_fold[h], &d->ops_fold[h]);
+  }
+  if (P->fold_u0 >= 0) {
+    const size_t nt = P->trail_tab.size();
+    CK(cudaMalloc(&d->trail, nt * d->elem));
+    if (c64) {
+      std::vector<float2> h(nt);
+      for (size_t i = 0; i < nt; ++i) h[i] = make_float2((float)P->trail_tab[i].real(), (float)P->trail_tab[i].imag());
+      CK(cudaMemcpy(d->trail, h.data(), nt * 8, cudaMemcpyHostToDevice));
+    } else {
+      CK(cudaMemcpy(d->trail, P->trail_tab.data(), nt * 16, cudaMemcpyHostToDevice));
+    }
   }
   for (auto& e : d->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDefault));
   for (int i = 0; i < 2; ++i) {
@@ -108,7 +128,11 @@ static DeviceState* ensure_device(Plan* P, int device) {
 
 // ----------------------------------------------------------- workspace
 struct Layout {
-  uint64_t p0, p1, K;
+  uint64_t p0, p1, K;          // TREE path range (folded runs: full range / fold_T)
+  bool fold = false;           // trailing-diagonal fold active (bitstring runs)
+  int U_tree = 0;              // units in the evaluated tree
+  std::vector<int32_t> ranks;  // their radices
+  const Half* half[2] = {nullptr, nullptr};
   bool bits_mode;
   uint64_t r0, r1;
   hsf_precision prec;
@@ -126,8 +150,8 @@ struct Layout {
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 constexpr size_t kHostChunkBytes = (size_t)256 << 20;
 
-static uint64_t nodes_at(const Plan& P, int L, uint64_t p0, uint64_t p1) {
-  uint64_t S = suffix_prod(P.ranks, L);
+static uint64_t nodes_at(const Layout& Y, int L, uint64_t p0, uint64_t p1) {
+  uint64_t S = suffix_prod(Y.ranks, L);
   return (p1 - 1) / S - p0 / S + 1;
 }
 
@@ -137,8 +161,18 @@ static Layout make_layout(const Plan& P, const hsf_run_args& a, size_t elem) {
   L.p1 = a.path_end;
   if (L.p0 == 0 && L.p1 == 0) L.p1 = P.n_paths;
   if (L.p0 >= L.p1 || L.p1 > P.n_paths) fail(HSF_ERR_INVALID_ARG, "bad path range");
-  L.K = L.p1 - L.p0;
   L.bits_mode = a.n_bitstrings > 0;
+  // the folded tree evaluates path groups of fold_T consecutive paths (the
+  // folded units are the fastest digits), so the range must be aligned
+  L.fold = L.bits_mode && P.fold_u0 >= 0 && L.p0 % P.fold_T == 0 && L.p1 % P.fold_T == 0;
+  L.U_tree = L.fold ? P.fold_u0 : (int)P.units.size();
+  L.ranks.assign(P.ranks.begin(), P.ranks.begin() + L.U_tree);
+  for (int h = 0; h < 2; ++h) L.half[h] = L.fold ? &P.half_fold[h] : &P.half[h];
+  if (L.fold) {
+    L.p0 /= P.fold_T;
+    L.p1 /= P.fold_T;
+  }
+  L.K = L.p1 - L.p0;
   if (!L.bits_mode && a.bitstrings) fail(HSF_ERR_INVALID_ARG, "bitstrings given with n_bitstrings == 0");
   if (L.bits_mode && !a.bitstrings) fail(HSF_ERR_INVALID_ARG, "n_bitstrings > 0 but bitstrings is NULL");
   if (L.bits_mode && P.n > 63) fail(HSF_ERR_INVALID_ARG, "bitstring runs need n <= 63");
@@ -152,10 +186,10 @@ static Layout make_layout(const Plan& P, const hsf_run_args& a, size_t elem) {
   if (P.opts.dtype == HSF_C128 && L.prec != HSF_PREC_SIMT) fail(HSF_ERR_UNSUPPORTED, "complex128 path-sum is SIMT fp64 only");
   size_t off = 0;
   for (int h = 0; h < 2; ++h) {
-    const Half& H = P.half[h];
+    const Half& H = *L.half[h];
     const size_t st = (size_t)1 << H.m;
     for (size_t i = 0; i + 1 < H.trans.size(); ++i)
-      L.scratch_elems[h] = std::max(L.scratch_elems[h], (size_t)nodes_at(P, H.trans[i].level_out, L.p0, L.p1) * st);
+      L.scratch_elems[h] = std::max(L.scratch_elems[h], (size_t)nodes_at(L, H.trans[i].level_out, L.p0, L.p1) * st);
     for (int b = 0; b < 2; ++b) {
       L.off_scratch[h][b] = off;
       off = align_up(off + L.scratch_elems[h] * elem);
@@ -163,12 +197,12 @@ static Layout make_layout(const Plan& P, const hsf_run_args& a, size_t elem) {
   }
   for (int h = 0; h < 2; ++h) {
     L.off_leaves[h] = off;
-    off = align_up(off + ((size_t)L.K << P.half[h].m) * elem);
+    off = align_up(off + ((size_t)L.K << L.half[h]->m) * elem);
   }
   if (L.bits_mode) {
     for (int h = 0; h < 2; ++h) {
       L.off_T[h] = off;
-      off = align_up(off + ((size_t)L.K << P.half[h].m) * elem);
+      off = align_up(off + ((size_t)L.K << L.half[h]->m) * elem);
     }
     if (!a.bits_on_device) {
       L.off_bits = off;
@@ -216,16 +250,17 @@ static void ensure_ws(DeviceState* d, size_t bytes) {
   d->ws_bytes = bytes;
 }
 
-// c_p = prod_u c_{u, d_u} for p in [p0, p1), fp64 on the host -> run dtype
-static void ensure_cp(Plan* P, DeviceState* d, uint64_t p0, uint64_t p1, cudaStream_t st) {
-  if (d->cp_p0 == p0 && d->cp_p1 == p1) return;
+// c_p = prod_u c_{u,d_u} over the tree's units for tree paths p in [p0, p1),
+// fp64 on the host -> run dtype
+static void ensure_cp(Plan* P, DeviceState* d, uint64_t p0, uint64_t p1, int U_tree, cudaStream_t st) {
+  if (d->cp_p0 == p0 && d->cp_p1 == p1 && d->cp_units == U_tree) return;
   const uint64_t K = p1 - p0;
   if (d->cp_cap < K) {
     if (d->cp) CK(cudaFree(d->cp));
     CK(cudaMalloc(&d->cp, K * d->elem));
     d->cp_cap = K;
   }
-  const int U = (int)P->units.size();
+  const int U = U_tree;
   std::vector<cd> c(K);
   for (uint64_t p = p0; p < p1; ++p) {
     uint64_t x = p;
@@ -246,12 +281,14 @@ static void ensure_cp(Plan* P, DeviceState* d, uint64_t p0, uint64_t p1, cudaStr
   CK(cudaStreamSynchronize(st));
   d->cp_p0 = p0;
   d->cp_p1 = p1;
+  d->cp_units = U_tree;
 }
 
 template <typename R>
 static void run_half(const Plan& P, DeviceState* d, int h, const Layout& L, cudaStream_t st) {
   using C = typename cplx<R>::T;
-  const Half& H = P.half[h];
+  const Half& H = *L.half[h];
+  DevOp* dops = L.fold ? d->ops_fold[h] : d->ops[h];
   char* ws = (char*)d->ws;
   const size_t st_elems = (size_t)1 << H.m;
   const void* prev_buf = nullptr;
@@ -260,14 +297,14 @@ static void run_half(const Plan& P, DeviceState* d, int h, const Layout& L, cuda
     const Transition& tr = H.trans[ti];
     const bool last = (ti + 1 == H.trans.size());
     void* out = ws + (last ? L.off_leaves[h] : L.off_scratch[h][ti & 1]);
-    const uint64_t S_out = suffix_prod(P.ranks, tr.level_out);
+    const uint64_t S_out = suffix_prod(L.ranks, tr.level_out);
     const uint64_t first_out = L.p0 / S_out;
     const uint64_t n_out = (L.p1 - 1) / S_out - first_out + 1;
     for (size_t pi = 0; pi < tr.passes.size(); ++pi) {
       const Pass& ps = tr.passes[pi];
       PassParams pp{};
       pp.dst = out;
-      pp.ops = d->ops[h] + ps.op_begin;
+      pp.ops = dops + ps.op_begin;
       pp.n_ops = (int)(ps.op_end - ps.op_begin);
       pp.coef = d->coef;
       pp.m = H.m;
@@ -303,9 +340,9 @@ static void run_half(const Plan& P, DeviceState* d, int h, const Layout& L, cuda
             pp.src = nullptr;
           } else {
             pp.src = prev_buf;
-            const uint64_t S_in = suffix_prod(P.ranks, prev_level);
+            const uint64_t S_in = suffix_prod(L.ranks, prev_level);
             pp.src_first = (long long)(L.p0 / S_in);
-            pp.src_div = (long long)range_prod(P.ranks, prev_level, tr.level_out);
+            pp.src_div = (long long)range_prod(L.ranks, prev_level, tr.level_out);
           }
         } else {  // in place on this level's buffer
           pp.src = out;
@@ -365,11 +402,19 @@ static void run_core_bits(Plan* P, DeviceState* d, const Layout& L, const hsf_ru
   }
   const long long ns = (long long)a.n_bitstrings;
   long long blocks = std::min<long long>((ns + 7) / 8, 148ll * 64);
+  TrailParams tw{};
+  if (L.fold) {
+    tw.n = (int)P->trail_mask.size();
+    for (int u = 0; u < tw.n; ++u) {
+      tw.mask[u] = P->trail_mask[u];
+      tw.off[u] = P->trail_off[u];
+    }
+  }
   if (sizeof(R) == 4 && K % 64 == 0) {
     gather_dot_c64_vec_kernel<<<(unsigned)blocks, 256, 0, st>>>((const float4*)AT, (const float4*)BT, bits,
-                                                                (float2*)out, ns, K, nB);
+                                                                (float2*)out, ns, K, nB, tw, (const float2*)d->trail);
   } else {
-    gather_dot_kernel<C><<<(unsigned)blocks, 256, 0, st>>>(AT, BT, bits, out, ns, K, nB);
+    gather_dot_kernel<C><<<(unsigned)blocks, 256, 0, st>>>(AT, BT, bits, out, ns, K, nB, tw, (const C*)d->trail);
   }
   CK(cudaGetLastError());
 }
@@ -448,7 +493,7 @@ static void run(Plan* P, const hsf_run_args& a) {
   if (!a.out) fail(HSF_ERR_INVALID_ARG, "out is NULL");
   ensure_ws(d, L.total);
   cudaStream_t st = (cudaStream_t)a.cuda_stream;
-  ensure_cp(P, d, L.p0, L.p1, st);
+  ensure_cp(P, d, L.p0, L.p1, L.U_tree, st);
   const bool timed = a.phase_ms != nullptr;
   try {
     if (P->opts.dtype == HSF_C64)
@@ -509,6 +554,7 @@ hsf_status hsf_plan_opts_default(hsf_plan_opts* o) {
   o->tile_qubits = 0;
   o->fuse_gates = 1;
   o->hoist_gates = 1;
+  o->fold_trailing_diag = 1;
   return HSF_OK;
 }
 
@@ -552,6 +598,7 @@ hsf_status hsf_plan_info_get(const hsf_plan_t* plan, hsf_plan_info* info) {
     info->ops_a = (int32_t)P->half[0].ops.size();
     info->ops_b = (int32_t)P->half[1].ops.size();
     info->plan_hash = P->hash;
+    info->fold_units = P->fold_u0 >= 0 ? (int32_t)P->units.size() - P->fold_u0 : 0;
   })
 }
 

@@ -41,11 +41,34 @@ __global__ void transpose_fold_kernel(const C* __restrict__ in, C* __restrict__ 
 }
 
 // ------------------------------------------------------------------- K6
+// Folded trailing diagonal units: amp(s) *= prod_u D_u[s's bits on supp(u)]
+// (block-local index, LSB = smallest support qubit; see plan.cpp).
+struct TrailParams {
+  int n;                               // folded units (0 => weight 1)
+  unsigned long long mask[kMaxTrail];  // global support bits of unit u
+  long long off[kMaxTrail];            // offset of D_u in the table
+};
+
+template <typename C>
+__device__ __forceinline__ C trail_weight(const TrailParams& tw, const C* __restrict__ tab, unsigned long long s) {
+  C w;
+  w.x = 1;
+  w.y = 0;
+  for (int u = 0; u < tw.n; ++u) {
+    unsigned long long m = tw.mask[u];
+    uint32_t idx = 0;
+    for (int j = 0; m; ++j, m &= m - 1) idx |= (uint32_t)((s >> (__ffsll((long long)m) - 1)) & 1ull) << j;
+    w = cmul(w, __ldg(&tab[tw.off[u] + idx]));
+  }
+  return w;
+}
+
 // amp[s] = sum_p AT[s >> nB][p] * BT[s & maskB][p]   (AT already holds c_p)
 template <typename C>
 __global__ void gather_dot_kernel(const C* __restrict__ AT, const C* __restrict__ BT,
                                   const unsigned long long* __restrict__ bits, C* __restrict__ out,
-                                  long long n_samples, long long K, int n_low) {
+                                  long long n_samples, long long K, int n_low, const TrailParams tw,
+                                  const C* __restrict__ trail) {
   const int lane = threadIdx.x & 31;
   const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -63,7 +86,7 @@ __global__ void gather_dot_kernel(const C* __restrict__ AT, const C* __restrict_
       acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
       acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
     }
-    if (lane == 0) out[s] = acc;
+    if (lane == 0) out[s] = tw.n ? cmul(acc, trail_weight(tw, trail, b)) : acc;
   }
 }
 
@@ -71,7 +94,8 @@ __global__ void gather_dot_kernel(const C* __restrict__ AT, const C* __restrict_
 // per step, 4 steps in flight.
 __global__ void gather_dot_c64_vec_kernel(const float4* __restrict__ AT, const float4* __restrict__ BT,
                                           const unsigned long long* __restrict__ bits, float2* __restrict__ out,
-                                          long long n_samples, long long K, int n_low) {
+                                          long long n_samples, long long K, int n_low, const TrailParams tw,
+                                          const float2* __restrict__ trail) {
   const int lane = threadIdx.x & 31;
   const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -95,7 +119,10 @@ __global__ void gather_dot_c64_vec_kernel(const float4* __restrict__ AT, const f
       re += __shfl_xor_sync(0xffffffffu, re, o);
       im += __shfl_xor_sync(0xffffffffu, im, o);
     }
-    if (lane == 0) out[s] = make_float2(re, im);
+    if (lane == 0) {
+      const float2 a = make_float2(re, im);
+      out[s] = tw.n ? cmul(a, trail_weight(tw, trail, b)) : a;
+    }
   }
 }
 

@@ -30,7 +30,7 @@ class HsfError(RuntimeError):
 class _Opts(C.Structure):
     _fields_ = [("dtype", C.c_int), ("svd_rel_tol", C.c_double), ("max_dense_block_qubits", C.c_int32),
                 ("log2_path_budget", C.c_double), ("individual", C.c_int32), ("tile_qubits", C.c_int32),
-                ("fuse_gates", C.c_int32), ("hoist_gates", C.c_int32)]
+                ("fuse_gates", C.c_int32), ("hoist_gates", C.c_int32), ("fold_trailing_diag", C.c_int32)]
 
 
 class _Info(C.Structure):
@@ -40,7 +40,7 @@ class _Info(C.Structure):
                 ("support_b", C.POINTER(C.c_int32)), ("sigma_offsets", C.POINTER(C.c_int64)),
                 ("sigmas", C.POINTER(C.c_double)), ("levels_a", C.c_int32), ("levels_b", C.c_int32),
                 ("passes_a", C.c_int32), ("passes_b", C.c_int32), ("ops_a", C.c_int32), ("ops_b", C.c_int32),
-                ("plan_hash", C.c_uint64)]
+                ("plan_hash", C.c_uint64), ("fold_units", C.c_int32)]
 
 
 class _RunArgs(C.Structure):
@@ -103,7 +103,8 @@ class Plan:
 
     def __init__(self, circuit_text: str, n_low: int, blocks=None, dtype: str = "c64", individual: bool = False,
                  svd_rel_tol: float = 1e-12, tile_qubits: int = 0, fuse_gates: bool = True,
-                 log2_path_budget: float = 26.0, max_dense_block_qubits: int = 10, hoist_gates: bool = True):
+                 log2_path_budget: float = 26.0, max_dense_block_qubits: int = 10, hoist_gates: bool = True,
+                 fold_trailing_diag: bool = True):
         L = lib()
         o = _Opts()
         _check(L.hsf_plan_opts_default(C.byref(o)))
@@ -113,6 +114,7 @@ class Plan:
         o.tile_qubits = tile_qubits
         o.fuse_gates = int(fuse_gates)
         o.hoist_gates = int(hoist_gates)
+        o.fold_trailing_diag = int(fold_trailing_diag)
         o.log2_path_budget = log2_path_budget
         o.max_dense_block_qubits = max_dense_block_qubits
         blocks = blocks or []
@@ -140,6 +142,7 @@ class Plan:
         self.passes = (i.passes_a, i.passes_b)
         self.ops = (i.ops_a, i.ops_b)
         self.plan_hash = int(i.plan_hash)
+        self.fold_units = int(i.fold_units)
 
     def __del__(self):
         h = getattr(self, "_h", None)

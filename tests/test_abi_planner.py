@@ -145,5 +145,26 @@ def test_workspace_bytes_no_gpu(hsf):
     inst = make_config("c5", n_bits=0)
     P = Plan(inst.text, inst.n_low, inst.blocks)
     b = P.workspace_bytes(bitstrings_count=1 << 22)
-    # leaves + transposed copies of both halves (256 x 2^20 complex64 each) dominate
-    assert b >= 4 * 256 * (1 << 20) * 8
+    # leaves + transposed copies of both halves dominate: 128 x 2^20 complex64
+    # each with the last (diagonal) unit folded, 256 x 2^20 without
+    assert 4 * 128 * (1 << 20) * 8 <= b < 4 * 256 * (1 << 20) * 8
+    P2 = Plan(inst.text, inst.n_low, inst.blocks, fold_trailing_diag=False)
+    assert P2.workspace_bytes(bitstrings_count=1 << 22) >= 4 * 256 * (1 << 20) * 8
+
+
+def test_trailing_fold_detection(hsf):
+    # fold needs: last units all-diagonal and no local gate after them
+    from paper_2502_06959_b200 import Plan
+    for name, units in [("c1", 1), ("c2", 0), ("c3", 0), ("c4", 0), ("c5", 1)]:
+        inst = make_config(name, twin=True)
+        P = Plan(inst.text, inst.n_low, inst.blocks)
+        assert P.fold_units == units, name
+        assert Plan(inst.text, inst.n_low, inst.blocks, fold_trailing_diag=False).fold_units == 0
+    # three trailing CZ across the cut, nothing after: all three fold
+    txt = "qubits 4\nh 0\nh 1\nh 2\nh 3\ncz 1 2\ncz 0 3\ncz 1 3\n"
+    P = Plan(txt, 2, [])
+    assert P.fold_units == 3 and P.n_paths == 8
+    # an H on qubit 2 after cz(1,2) pins the tree to level 1: the two later
+    # units still fold; an H on qubit 3 (after every unit) blocks all folding
+    assert Plan(txt + "h 2\n", 2, []).fold_units == 2
+    assert Plan(txt + "h 3\n", 2, []).fold_units == 0

@@ -341,3 +341,23 @@ def test_hoisting_tiled_twins(torch, name):
     for hoist in (True, False):
         got, _ = gpu_bits(torch, inst, inst.bitstrings, path_range=(0, 8), hoist_gates=hoist)
         check(got, ref, "c64")
+
+
+@pytest.mark.parametrize("path_range", [None, (4, 12), (3, 9)])
+def test_trailing_diagonal_fold(torch, path_range):
+    # c5's last CP fan-out block is diagonal with no gate after it: bitstring
+    # runs fold its two Schmidt terms into a per-sample weight.  Folded,
+    # unfolded, and an unaligned range (falls back to the full tree) all match
+    # the oracle's partial sums.
+    inst = make_config("c5", twin=True)
+    n, g = O.parse_circuit(inst.text)
+    P = O.plan(n, g, inst.n_low, inst.blocks)
+    p0, p1 = path_range or (0, P.n_paths)
+    A, B, c = O.half_states(P, p0, p1)
+    ref = O.recombine_bits(A, B, c, inst.bitstrings, inst.n_low)
+    for fold in (True, False):
+        got, Pg = gpu_bits(torch, inst, inst.bitstrings, path_range=path_range, fold_trailing_diag=fold)
+        assert Pg.fold_units == (1 if fold else 0)
+        check(got, ref, "c64")
+    got, _ = gpu_bits(torch, inst, inst.bitstrings, dtype="c128", path_range=path_range)
+    check(got, ref, "c128")
