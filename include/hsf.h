@@ -90,6 +90,10 @@ typedef struct {
                                     units with no gate after them into a per-sample weight
                                     (the block's diagonal at the sample's bits) instead of
                                     extending the path tree; results are identical */
+  int32_t jit;                   /* 1 (default) => every simulator tile pass runs as a kernel
+                                    specialised to its op list (generated CUDA, NVRTC for
+                                    sm_100a, compiled at the first hsf_run on a device and
+                                    cached per process); 0 => generic interpreter kernel */
 } hsf_plan_opts;
 
 typedef struct hsf_plan_s hsf_plan_t; /* opaque */
@@ -187,6 +191,14 @@ const char* hsf_status_str(hsf_status s);
 /* Copy the calling thread's last error message into buf (NUL-terminated,
  * truncated to len); returns the full message length. */
 size_t hsf_last_error(char* buf, size_t len);
+
+/* Debug/inspection: CUDA source of the specialised kernel of tile pass `pass`
+ * (flattened over transitions) of half `half` (0 = A, 1 = B) of tree variant
+ * `variant` (0 = full tree, 1 = trailing-diagonal fold).  Copies at most
+ * len-1 bytes + NUL into buf (may be NULL) and returns the full length; 0 if
+ * the pass does not exist.  Host only. */
+size_t hsf_debug_pass_source(const hsf_plan_t* plan, int32_t variant, int32_t half, int32_t pass, char* buf,
+                             size_t len);
 
 /* Library build identification string (compile flags, arch). */
 const char* hsf_version(void);

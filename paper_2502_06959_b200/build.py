@@ -9,7 +9,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libhsf.so")
-NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+NVCC = os.environ.get("NVCC", os.path.join(CUDA, "bin", "nvcc"))
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CXXFLAGS = ["-O3", "-std=c++17", "-fPIC", "-Wall", "-Wno-unused-function"]
 
@@ -32,13 +33,19 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(LIBDIR, exist_ok=True)
     obj_dir = os.path.join(LIBDIR, "obj")
     os.makedirs(obj_dir, exist_ok=True)
+    # the NVRTC prelude is embedded in the library as a raw string literal
+    with open(os.path.join(CSRC, "jit_prelude.cuh")) as fh:
+        prelude = fh.read()
+    with open(os.path.join(obj_dir, "jit_prelude.inc"), "w") as fh:
+        fh.write('R"HSFJITPRELUDE(' + prelude + ')HSFJITPRELUDE"\n')
     objs = []
     cmds = []
     for f in sorted(os.listdir(CSRC)):
         src = os.path.join(CSRC, f)
         if f.endswith(".cpp"):
             o = os.path.join(obj_dir, f + ".o")
-            cmds.append(["g++", *CXXFLAGS, "-I", os.path.join(HERE, "..", "include"), "-c", src, "-o", o])
+            cmds.append(["g++", *CXXFLAGS, "-I", os.path.join(HERE, "..", "include"), "-I", obj_dir,
+                         "-I", os.path.join(CUDA, "include"), "-c", src, "-o", o])
             objs.append(o)
         elif f.endswith(".cu"):
             o = os.path.join(obj_dir, f + ".o")
@@ -56,7 +63,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
             with open(c[-1] + ".ptxas.txt", "w") as fh:
                 fh.write(r.stderr)
     tmp = LIB + ".tmp"
-    link = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"]
+    link = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-L", os.path.join(CUDA, "lib64"), "-lnvrtc",
+            "-Xlinker", "-rpath=" + os.path.join(CUDA, "lib64")]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode:
         sys.stderr.write(r.stdout + r.stderr)

@@ -1,0 +1,405 @@
+// jit.cpp — run-time specialisation of the simulator tile passes.
+//
+// For every tile pass of a plan (both halves, both tree variants) the host
+// generates one CUDA kernel in which every qubit position, tile map, table
+// offset, digit divisor and loop bound of the pass's op list is a
+// compile-time constant, compiles it with NVRTC for sm_100a (once per
+// distinct source per process and device, in parallel host threads) and
+// launches it through the driver API.  The generated kernels compute exactly
+// what the generic interpreter kernel hsf_pass_kernel (sim_kernels.cuh)
+// computes for the same pass -- same CTA/tile/node mapping, same swizzled
+// shared-memory layout, same op order -- without its per-op dispatch and
+// variable-shift index arithmetic (ncu on the interpreter: FFMA was 20 % of
+// the issued instructions, profiles/r01).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nvrtc.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "hsf_internal.h"
+#include "jit.h"
+
+namespace hsf {
+
+static const char* kPrelude =
+#include "jit_prelude.inc"
+    ;
+
+// ------------------------------------------------------------ code generation
+namespace {
+
+std::string u(uint64_t v) {
+  char b[32];
+  std::snprintf(b, sizeof b, "%lluu", (unsigned long long)v);
+  return b;
+}
+
+// expression gathering bits: sum_j ((x >> from[j]) & 1) << to[j], merged into runs
+std::string gather_expr(const std::string& x, const std::vector<int>& from, const std::vector<int>& to) {
+  std::vector<std::string> terms;
+  size_t j = 0;
+  while (j < from.size()) {
+    size_t e = j + 1;
+    while (e < from.size() && from[e] == from[e - 1] + 1 && to[e] == to[e - 1] + 1) ++e;
+    const int len = (int)(e - j);
+    const uint64_t mask = (len >= 32) ? 0xffffffffull : ((1ull << len) - 1);
+    std::string t = "((" + x + " >> " + std::to_string(from[j]) + ") & " + u(mask) + ")";
+    if (to[j]) t = "(" + t + " << " + std::to_string(to[j]) + ")";
+    terms.push_back(t);
+    j = e;
+  }
+  if (terms.empty()) return "0u";
+  std::string s = terms[0];
+  for (size_t i = 1; i < terms.size(); ++i) s += " | " + terms[i];
+  return "(" + s + ")";
+}
+
+struct Gen {
+  std::ostringstream o;
+  const Half& H;
+  const Pass& ps;
+  bool c64;
+  int t, m;
+  bool whole;
+  std::vector<DevOp> ops;
+  std::vector<int> pos2q;  // tile position -> half qubit
+
+  Gen(const Half& h, const Pass& p, bool c) : H(h), ps(p), c64(c) {
+    t = p.t;
+    m = h.m;
+    whole = (t == m);
+    ops.assign(h.dev_ops.begin() + p.op_begin, h.dev_ops.begin() + p.op_end);
+    pos2q.resize(t);
+    for (int i = 0; i < t; ++i) pos2q[i] = whole ? i : p.T[i];
+  }
+
+  std::string table(int i) const { return "M" + std::to_string(i); }
+  std::string didx(const DevOp& d, const std::string& g) const {
+    std::vector<int> from(d.q, d.q + d.k), to(d.k);
+    for (int j = 0; j < d.k; ++j) to[j] = j;
+    // order by destination bit j (already), merge runs where both advance by 1
+    return gather_expr(g, from, to);
+  }
+  bool staged(const DevOp& d) const { return d.kind == OP_DIAG && d.soff >= 0; }
+  std::string tload(const DevOp& d, int i, const std::string& idx) const {
+    return staged(d) ? table(i) + "[" + idx + "]" : "__ldg(&" + table(i) + "[" + idx + "])";
+  }
+
+  void header(const std::string& name, int minb) {
+    o << "extern \"C\" __global__ void __launch_bounds__(256, " << minb << ") " << name << "(const JitArgs a) {\n";
+    o << "  typedef " << (c64 ? "float2" : "double2") << " C;\n";
+    o << "  constexpr u32 NT = 256u, NEL = 1u << " << t << ";\n";
+    o << "  extern __shared__ __align__(128) unsigned char smem_raw[];\n";
+    o << "  C* s = reinterpret_cast<C*>(smem_raw);\n";
+    o << "  C* stab = reinterpret_cast<C*>(smem_raw + (sizeof(C) << " << t << "));\n";
+    o << "  (void)stab;\n";
+    o << "  const long long node_g = a.node_first + blockIdx.y;\n";
+    o << "  const C* coef = reinterpret_cast<const C*>(a.coef);\n";
+    o << "  C* dst = reinterpret_cast<C*>(a.dst) + (a.node_local0 + blockIdx.y) * " << (1ll << m) << "ll;\n";
+    o << "  const C* src = a.src ? reinterpret_cast<const C*>(a.src) + (node_g / a.src_div - a.src_first) * "
+      << (1ll << m) << "ll : nullptr;\n";
+    // tile -> state index map
+    if (whole) {
+      o << "  auto G = [&](u32 e) -> u32 { return e; };\n";
+    } else {
+      std::vector<int> nonT;
+      for (int q = 0; q < m; ++q)
+        if (std::find(ps.T.begin(), ps.T.end(), q) == ps.T.end()) nonT.push_back(q);
+      std::vector<int> from(nonT.size()), to = nonT;
+      for (size_t j = 0; j < nonT.size(); ++j) from[j] = (int)j;
+      o << "  const u32 tile = blockIdx.x;\n";
+      o << "  const u32 base = " << gather_expr("tile", from, to) << ";\n";
+      std::vector<int> pf, pt;
+      for (int i = 0; i < t; ++i) {
+        pf.push_back(i);
+        pt.push_back(pos2q[i]);
+      }
+      o << "  auto G = [&](u32 e) -> u32 { return base | " << gather_expr("e", pf, pt) << "; };\n";
+    }
+    // per-op table pointers (digit-resolved for Schmidt factors)
+    for (size_t i = 0; i < ops.size(); ++i) {
+      const DevOp& d = ops[i];
+      if (d.kind == OP_RPASS) continue;
+      std::string ptr = "coef + " + std::to_string(d.table) + "ll";
+      if (d.radix > 1)
+        ptr += " + ((node_g / " + std::to_string(d.div) + "ll) % " + std::to_string(d.radix) + "ll) * " +
+               std::to_string(d.stride) + "ll";
+      if (staged(d)) {
+        o << "  C* " << table(i) << " = stab + " << d.soff << ";\n";
+        o << "  { const C* g_ = " << ptr << "; for (u32 e = threadIdx.x; e < " << (1u << d.k)
+          << "u; e += NT) " << table(i) << "[e] = __ldg(&g_[e]); }\n";
+      } else {
+        o << "  const C* __restrict__ " << table(i) << " = " << ptr << ";\n";
+      }
+    }
+    // load (or |0...0>)
+    o << "  if (src) {\n";
+    o << "#pragma unroll 4\n";
+    o << "    for (u32 e = 2u * threadIdx.x; e < NEL; e += 2u * NT) { C x_, y_; ld2(src + G(e), x_, y_); "
+         "s[sw(e)] = x_; s[sw(e + 1)] = y_; }\n";
+    o << "  } else {\n";
+    o << "    for (u32 e = threadIdx.x; e < NEL; e += NT) { C v_ = czero<C>(); if (G(e) == 0u) v_.x = 1; s[sw(e)] = v_; }\n";
+    o << "  }\n  __syncthreads();\n";
+  }
+
+  void dense(const DevOp& d, int i) {
+    const int K = d.k, D = 1 << K;
+    std::vector<int> sorted(d.q, d.q + K);
+    std::sort(sorted.begin(), sorted.end());
+    o << "  __syncthreads();\n";
+    o << "  for (u32 g = threadIdx.x; g < (NEL >> " << K << "); g += NT) {\n";
+    o << "    u32 b = g;";
+    for (int p : sorted) o << " b = ins0<" << p << ">(b);";
+    o << "\n    C v[" << D << "];\n";
+    std::vector<uint32_t> off(D);
+    for (int r = 0; r < D; ++r) {
+      uint32_t x = 0;
+      for (int j = 0; j < K; ++j)
+        if ((r >> j) & 1) x |= 1u << d.q[j];
+      off[r] = x;
+      o << "    v[" << r << "] = s[sw(b + " << x << "u)];\n";
+    }
+    if (K <= 3) {
+      for (int r = 0; r < D; ++r) {
+        o << "    { C acc = czero<C>();";
+        for (int c = 0; c < D; ++c) o << " acc = cfma(__ldg(&" << table(i) << "[" << r * D + c << "]), v[" << c << "], acc);";
+        o << " s[sw(b + " << off[r] << "u)] = acc; }\n";
+      }
+    } else {
+      o << "    const u32 offs[" << D << "] = {";
+      for (int r = 0; r < D; ++r) o << (r ? ", " : "") << off[r] << "u";
+      o << "};\n";
+      o << "#pragma unroll 1\n    for (int r = 0; r < " << D << "; ++r) { C acc = czero<C>();\n";
+      o << "#pragma unroll\n      for (int c = 0; c < " << D << "; ++c) acc = cfma(__ldg(&" << table(i) << "[r * " << D
+        << " + c]), v[c], acc);\n";
+      o << "      s[sw(b + offs[r])] = acc; }\n";
+    }
+    o << "  }\n  __syncthreads();\n";
+  }
+
+  // register pass: header at ops[i], then ops[i+1 .. i+n]
+  void rpass(size_t i) {
+    const DevOp& h = ops[i];
+    const int n = h.k;
+    int pos[4], qreg[4];
+    for (int j = 0; j < 4; ++j) {
+      pos[j] = h.q[j];
+      qreg[j] = pos2q[pos[j]];
+    }
+    std::vector<int> sorted(pos, pos + 4);
+    std::sort(sorted.begin(), sorted.end());
+    o << "  __syncthreads();\n";
+    o << "  for (u32 gi = threadIdx.x; gi < (NEL >> 4); gi += NT) {\n";
+    o << "    u32 b = gi;";
+    for (int p : sorted) o << " b = ins0<" << p << ">(b);";
+    o << "\n    const u32 gb = G(b); (void)gb;\n    C v[16];\n";
+    uint32_t ek[16];
+    for (int k = 0; k < 16; ++k) {
+      uint32_t e = 0;
+      for (int j = 0; j < 4; ++j)
+        if ((k >> j) & 1) e |= 1u << pos[j];
+      ek[k] = e;
+      o << "    v[" << k << "] = s[sw(b | " << e << "u)];\n";
+    }
+    for (size_t r = i + 1; r <= i + (size_t)n; ++r) {
+      const DevOp& d = ops[r];
+      if (d.kind == OP_R1) {
+        o << "    r1<" << d.q[0] << ">(v, " << table((int)r) << ");\n";
+      } else {  // diagonal: index of element k = i0 | IK[k]
+        o << "    { const u32 i0 = " << didx(d, "gb") << ";\n";
+        for (int k = 0; k < 16; ++k) {
+          uint32_t ik = 0;
+          for (int j = 0; j < 4; ++j)
+            if ((k >> j) & 1)
+              for (int jj = 0; jj < d.k; ++jj)
+                if (d.q[jj] == qreg[j]) ik |= 1u << jj;
+          o << "      v[" << k << "] = cmul(v[" << k << "], " << tload(d, (int)r, "i0 | " + std::to_string(ik) + "u")
+            << ");\n";
+        }
+        o << "    }\n";
+      }
+    }
+    for (int k = 0; k < 16; ++k) o << "    s[sw(b | " << ek[k] << "u)] = v[" << k << "];\n";
+    o << "  }\n  __syncthreads();\n";
+  }
+
+  // run of standalone diagonal ops [i, j): element-owner mapping, 4 per thread
+  void diag_run(size_t i, size_t j) {
+    o << "  for (u32 e0 = threadIdx.x; e0 < NEL; e0 += 4u * NT) {\n";
+    o << "#pragma unroll\n    for (u32 w = 0; w < 4u; ++w) { const u32 e = e0 + w * NT;";
+    o << " if (e < NEL) { const u32 g = G(e); C v = s[sw(e)];\n";
+    for (size_t r = i; r < j; ++r)
+      o << "      v = cmul(v, " << tload(ops[r], (int)r, didx(ops[r], "g")) << ");\n";
+    o << "      s[sw(e)] = v; } }\n  }\n";
+  }
+
+  std::string build(const std::string& name) {
+    bool heavy = false;
+    for (auto& d : ops) heavy = heavy || d.kind == OP_RPASS || (d.kind == OP_DENSE && d.k > 2);
+    header(name, heavy ? 2 : 3);
+    size_t i = 0;
+    while (i < ops.size()) {
+      const DevOp& d = ops[i];
+      if (d.kind == OP_DENSE) {
+        dense(d, (int)i);
+        ++i;
+      } else if (d.kind == OP_RPASS) {
+        rpass(i);
+        i += (size_t)d.k + 1;
+      } else {
+        size_t j = i;
+        while (j < ops.size() && ops[j].kind == OP_DIAG) ++j;
+        diag_run(i, j);
+        o << "  __syncthreads();\n";  // element-owner mapping differs from the store mapping
+        i = j;
+      }
+    }
+    o << "  __syncthreads();\n";
+    o << "#pragma unroll 4\n";
+    o << "  for (u32 e = 2u * threadIdx.x; e < NEL; e += 2u * NT) st2(dst + G(e), s[sw(e)], s[sw(e + 1)]);\n";
+    o << "}\n";
+    return o.str();
+  }
+};
+
+// ------------------------------------------------------------ driver API
+struct Drv {
+  CUresult (*moduleLoadData)(CUmodule*, const void*) = nullptr;
+  CUresult (*moduleGetFunction)(CUfunction*, CUmodule, const char*) = nullptr;
+  CUresult (*funcSetAttribute)(CUfunction, CUfunction_attribute, int) = nullptr;
+  CUresult (*launchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                           CUstream, void**, void**) = nullptr;
+};
+
+template <typename F>
+void load_sym(F& f, const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess || !p)
+    fail(HSF_ERR_CUDA, std::string("driver entry point ") + name + " unavailable");
+  f = reinterpret_cast<F>(p);
+}
+
+Drv& drv() {
+  static Drv d;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    load_sym(d.moduleLoadData, "cuModuleLoadData");
+    load_sym(d.moduleGetFunction, "cuModuleGetFunction");
+    load_sym(d.funcSetAttribute, "cuFuncSetAttribute");
+    load_sym(d.launchKernel, "cuLaunchKernel");
+  });
+  return d;
+}
+
+uint64_t fnv64(const std::string& s) {
+  uint64_t h = 1469598103934665603ull;
+  for (unsigned char c : s) {
+    h ^= c;
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+std::mutex g_mu;
+std::map<std::pair<int, std::string>, void*> g_cache;  // (device, source) -> CUfunction
+
+std::vector<char> nvrtc_compile(const std::string& src, std::string& log) {
+  nvrtcProgram prog;
+  if (nvrtcCreateProgram(&prog, src.c_str(), "hsf_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+    log = "nvrtcCreateProgram failed";
+    return {};
+  }
+  const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo", "--fmad=true"};
+  nvrtcResult r = nvrtcCompileProgram(prog, 4, opts);
+  size_t n = 0;
+  nvrtcGetProgramLogSize(prog, &n);
+  log.assign(n, '\0');
+  if (n) nvrtcGetProgramLog(prog, &log[0]);
+  std::vector<char> cubin;
+  if (r == NVRTC_SUCCESS) {
+    size_t cb = 0;
+    nvrtcGetCUBINSize(prog, &cb);
+    cubin.resize(cb);
+    nvrtcGetCUBIN(prog, cubin.data());
+  }
+  nvrtcDestroyProgram(&prog);
+  return cubin;
+}
+
+}  // namespace
+
+std::string jit_pass_source(const Half& H, const Pass& ps, bool c64) {
+  Gen g(H, ps, c64);
+  return std::string(kPrelude) + "\n" + g.build("hsf_jit_pass");
+}
+
+size_t jit_smem_bytes(const Pass& ps, bool c64) {
+  const size_t elem = c64 ? 8 : 16;
+  return (elem << ps.t) + (size_t)ps.tbl_elems * elem;
+}
+
+std::vector<void*> jit_compile_all(int device, const std::vector<std::string>& sources) {
+  std::vector<void*> fns(sources.size(), nullptr);
+  std::vector<size_t> todo;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (size_t i = 0; i < sources.size(); ++i) {
+      auto it = g_cache.find({device, sources[i]});
+      if (it != g_cache.end())
+        fns[i] = it->second;
+      else if (std::find_if(todo.begin(), todo.end(), [&](size_t j) { return sources[j] == sources[i]; }) == todo.end())
+        todo.push_back(i);
+    }
+  }
+  if (!todo.empty()) {
+    std::vector<std::vector<char>> bins(todo.size());
+    std::vector<std::string> logs(todo.size());
+    std::atomic<size_t> next{0};
+    const unsigned nth = std::max(1u, std::min<unsigned>((unsigned)todo.size(), std::thread::hardware_concurrency()));
+    std::vector<std::thread> th;
+    for (unsigned w = 0; w < nth; ++w)
+      th.emplace_back([&] {
+        for (size_t k; (k = next++) < todo.size();) bins[k] = nvrtc_compile(sources[todo[k]], logs[k]);
+      });
+    for (auto& x : th) x.join();
+    Drv& D = drv();
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (size_t k = 0; k < todo.size(); ++k) {
+      if (bins[k].empty())
+        fail(HSF_ERR_UNSUPPORTED, "NVRTC compile of a specialised pass failed: " + logs[k].substr(0, 2000));
+      CUmodule mod;
+      CUfunction f;
+      if (D.moduleLoadData(&mod, bins[k].data()) != CUDA_SUCCESS) fail(HSF_ERR_CUDA, "cuModuleLoadData failed");
+      if (D.moduleGetFunction(&f, mod, "hsf_jit_pass") != CUDA_SUCCESS) fail(HSF_ERR_CUDA, "cuModuleGetFunction failed");
+      if (D.funcSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, 227 * 1024) != CUDA_SUCCESS)
+        fail(HSF_ERR_CUDA, "cuFuncSetAttribute failed");
+      g_cache[{device, sources[todo[k]]}] = (void*)f;  // modules live for the process
+    }
+    for (size_t i = 0; i < sources.size(); ++i)
+      if (!fns[i]) fns[i] = g_cache[{device, sources[i]}];
+  }
+  return fns;
+}
+
+void jit_launch(void* fn, unsigned gx, unsigned gy, size_t smem, void* stream, const JitLaunchArgs& a) {
+  JitLaunchArgs args = a;
+  void* params[] = {&args};
+  if (drv().launchKernel((CUfunction)fn, gx, gy, 1, 256, 1, 1, (unsigned)smem, (CUstream)stream, params, nullptr) !=
+      CUDA_SUCCESS)
+    fail(HSF_ERR_CUDA, "cuLaunchKernel (specialised pass) failed");
+}
+
+uint64_t jit_source_hash(const std::string& s) { return fnv64(s); }
+
+}  // namespace hsf

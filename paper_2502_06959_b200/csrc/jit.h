@@ -1,0 +1,29 @@
+// jit.h — run-time specialised simulator passes (jit.cpp).  Not ABI.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "hsf_internal.h"
+
+namespace hsf {
+
+// Mirrors JitArgs in jit_prelude.cuh (passed by value to the kernel).
+struct JitLaunchArgs {
+  const void* src;
+  void* dst;
+  const void* coef;
+  long long node_first, node_local0, src_first, src_div;
+};
+
+// CUDA source of the kernel "hsf_jit_pass" specialised to one tile pass.
+std::string jit_pass_source(const Half& H, const Pass& ps, bool c64);
+// dynamic shared memory of that kernel (tile + staged diagonal tables)
+size_t jit_smem_bytes(const Pass& ps, bool c64);
+// NVRTC-compile (cached per device and source, parallel) and load; returns CUfunctions
+std::vector<void*> jit_compile_all(int device, const std::vector<std::string>& sources);
+void jit_launch(void* fn, unsigned gx, unsigned gy, size_t smem, void* stream, const JitLaunchArgs& a);
+uint64_t jit_source_hash(const std::string& s);
+
+}  // namespace hsf

@@ -1,0 +1,84 @@
+// jit_prelude.cuh — device helpers shared by every run-time specialised
+// simulator pass (jit.cpp generates one kernel per tile pass and compiles it
+// with NVRTC for sm_100a).  Self-contained: NVRTC sees only this text plus
+// the generated kernel, no system headers.
+//
+// Semantics are those of hsf_pass_kernel (sim_kernels.cuh): one CTA owns one
+// (path-tree node, tile) pair, the tile lives in shared memory with the
+// XOR-swizzled layout sw(e) = e ^ ((e >> 4) & 15), and the pass's ops are
+// applied in order.  In the generated kernels every qubit position, table
+// offset, digit divisor and loop bound is a compile-time constant.
+typedef unsigned int u32;
+typedef unsigned long long u64;
+
+struct JitArgs {
+  const void* src;       // parent level buffer, nullptr => |0...0>
+  void* dst;             // output level buffer (node-major)
+  const void* coef;      // complex table in the run dtype
+  long long node_first;  // global index (output level) of blockIdx.y == 0
+  long long node_local0; // local output-node index of blockIdx.y == 0
+  long long src_first;   // global index of the first node of the input level
+  long long src_div;     // parent = node_global / src_div
+};
+
+__device__ __forceinline__ int sw(int e) { return e ^ ((e >> 4) & 15); }
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 cfma(float2 a, float2 b, float2 acc) {
+  acc.x = fmaf(a.x, b.x, fmaf(-a.y, b.y, acc.x));
+  acc.y = fmaf(a.x, b.y, fmaf(a.y, b.x, acc.y));
+  return acc;
+}
+__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 acc) {
+  acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
+  acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
+  return acc;
+}
+template <typename C>
+__device__ __forceinline__ C czero();
+template <>
+__device__ __forceinline__ float2 czero<float2>() { return make_float2(0.f, 0.f); }
+template <>
+__device__ __forceinline__ double2 czero<double2>() { return make_double2(0.0, 0.0); }
+
+// two consecutive amplitudes from / to global memory (16 B for complex64)
+__device__ __forceinline__ void ld2(const float2* p, float2& a, float2& b) {
+  const float4 x = *reinterpret_cast<const float4*>(p);
+  a = make_float2(x.x, x.y);
+  b = make_float2(x.z, x.w);
+}
+__device__ __forceinline__ void ld2(const double2* p, double2& a, double2& b) {
+  a = p[0];
+  b = p[1];
+}
+__device__ __forceinline__ void st2(float2* p, float2 a, float2 b) {
+  *reinterpret_cast<float4*>(p) = make_float4(a.x, a.y, b.x, b.y);
+}
+__device__ __forceinline__ void st2(double2* p, double2 a, double2 b) {
+  p[0] = a;
+  p[1] = b;
+}
+
+// 1-qubit gate on register slot J of 16 amplitudes held by one thread
+template <int J, typename C>
+__device__ __forceinline__ void r1(C (&v)[16], const C* __restrict__ M) {
+  const C m00 = __ldg(&M[0]), m01 = __ldg(&M[1]), m10 = __ldg(&M[2]), m11 = __ldg(&M[3]);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    if (i & (1 << J)) continue;
+    const C a = v[i], b = v[i | (1 << J)];
+    v[i] = cfma(m01, b, cmul(m00, a));
+    v[i | (1 << J)] = cfma(m11, b, cmul(m10, a));
+  }
+}
+
+// insert a zero bit at position P (ascending use: smallest position first)
+template <int P>
+__device__ __forceinline__ u32 ins0(u32 b) {
+  return ((b >> P) << (P + 1)) | (b & ((1u << P) - 1u));
+}

@@ -15,6 +15,7 @@
 #include "sim_kernels.cuh"
 #include "sum_kernels.cuh"
 #include "gemm_tc.cuh"
+#include "jit.h"
 
 namespace hsf {
 
@@ -35,6 +36,8 @@ struct DeviceState {
   DevOp* ops[2] = {nullptr, nullptr};
   DevOp* ops_fold[2] = {nullptr, nullptr};  // trailing-diagonal fold variant
   void* trail = nullptr;                    // folded units' block diagonals (run dtype)
+  bool jit = false;                         // specialised pass kernels loaded
+  std::vector<void*> jit_fn[2][2];          // [variant][half] per flattened pass
   void* ws = nullptr;
   size_t ws_bytes = 0;
   // cached per-range path coefficients
@@ -116,6 +119,25 @@ static DeviceState* ensure_device(Plan* P, int device) {
     } else {
       CK(cudaMemcpy(d->trail, P->trail_tab.data(), nt * 16, cudaMemcpyHostToDevice));
     }
+  }
+  if (P->opts.jit) {
+    // one specialised kernel per tile pass (jit.cpp), compiled once per process
+    std::vector<std::string> src;
+    std::vector<std::pair<int, int>> owner;
+    for (int v = 0; v < 2; ++v) {
+      if (v == 1 && P->fold_u0 < 0) continue;
+      for (int h = 0; h < 2; ++h) {
+        const Half& H = v ? P->half_fold[h] : P->half[h];
+        for (const auto& tr : H.trans)
+          for (const auto& ps : tr.passes) {
+            src.push_back(jit_pass_source(H, ps, c64));
+            owner.push_back({v, h});
+          }
+      }
+    }
+    std::vector<void*> fns = jit_compile_all(device, src);
+    for (size_t i = 0; i < fns.size(); ++i) d->jit_fn[owner[i].first][owner[i].second].push_back(fns[i]);
+    d->jit = true;
   }
   for (auto& e : d->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDefault));
   for (int i = 0; i < 2; ++i) {
@@ -293,6 +315,8 @@ static void run_half(const Plan& P, DeviceState* d, int h, const Layout& L, cuda
   const size_t st_elems = (size_t)1 << H.m;
   const void* prev_buf = nullptr;
   int prev_level = -1;
+  size_t pass_ord = 0;
+  const std::vector<void*>* jf = d->jit ? &d->jit_fn[L.fold ? 1 : 0][h] : nullptr;
   for (size_t ti = 0; ti < H.trans.size(); ++ti) {
     const Transition& tr = H.trans[ti];
     const bool last = (ti + 1 == H.trans.size());
@@ -300,7 +324,7 @@ static void run_half(const Plan& P, DeviceState* d, int h, const Layout& L, cuda
     const uint64_t S_out = suffix_prod(L.ranks, tr.level_out);
     const uint64_t first_out = L.p0 / S_out;
     const uint64_t n_out = (L.p1 - 1) / S_out - first_out + 1;
-    for (size_t pi = 0; pi < tr.passes.size(); ++pi) {
+    for (size_t pi = 0; pi < tr.passes.size(); ++pi, ++pass_ord) {
       const Pass& ps = tr.passes[pi];
       PassParams pp{};
       pp.dst = out;
@@ -349,9 +373,14 @@ static void run_half(const Plan& P, DeviceState* d, int h, const Layout& L, cuda
           pp.src_first = (long long)first_out;
           pp.src_div = 1;
         }
-        dim3 grid((unsigned)tiles, (unsigned)ny);
-        kern<<<grid, nthr, smem, st>>>(pp);
-        CK(cudaGetLastError());
+        if (jf) {
+          JitLaunchArgs ja{pp.src, pp.dst, pp.coef, pp.node_first, pp.node_local0, pp.src_first, pp.src_div};
+          jit_launch((*jf)[pass_ord], (unsigned)tiles, (unsigned)ny, jit_smem_bytes(ps, sizeof(R) == 4), st, ja);
+        } else {
+          dim3 grid((unsigned)tiles, (unsigned)ny);
+          kern<<<grid, nthr, smem, st>>>(pp);
+          CK(cudaGetLastError());
+        }
       }
     }
     prev_buf = out;
@@ -555,6 +584,7 @@ hsf_status hsf_plan_opts_default(hsf_plan_opts* o) {
   o->fuse_gates = 1;
   o->hoist_gates = 1;
   o->fold_trailing_diag = 1;
+  o->jit = 1;
   return HSF_OK;
 }
 
@@ -656,6 +686,30 @@ size_t hsf_last_error(char* buf, size_t len) {
     buf[n] = 0;
   }
   return m.size();
+}
+
+size_t hsf_debug_pass_source(const hsf_plan_t* plan, int32_t variant, int32_t half, int32_t pass, char* buf,
+                             size_t len) {
+  try {
+    const Plan* P = reinterpret_cast<const Plan*>(plan);
+    if (!P || half < 0 || half > 1 || variant < 0 || variant > 1 || (variant == 1 && P->fold_u0 < 0)) return 0;
+    const Half& H = variant ? P->half_fold[half] : P->half[half];
+    int k = 0;
+    for (const auto& tr : H.trans)
+      for (const auto& ps : tr.passes)
+        if (k++ == pass) {
+          const std::string s = jit_pass_source(H, ps, P->opts.dtype == HSF_C64);
+          if (buf && len) {
+            const size_t n = std::min(len - 1, s.size());
+            std::memcpy(buf, s.data(), n);
+            buf[n] = 0;
+          }
+          return s.size();
+        }
+    return 0;
+  } catch (...) {
+    return 0;
+  }
 }
 
 const char* hsf_version(void) { return "libhsf 0.1 sm_100a (tcgen05 bf16x3 path-sum, SMEM/tile-pass simulator)"; }

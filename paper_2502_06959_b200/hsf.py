@@ -30,7 +30,8 @@ class HsfError(RuntimeError):
 class _Opts(C.Structure):
     _fields_ = [("dtype", C.c_int), ("svd_rel_tol", C.c_double), ("max_dense_block_qubits", C.c_int32),
                 ("log2_path_budget", C.c_double), ("individual", C.c_int32), ("tile_qubits", C.c_int32),
-                ("fuse_gates", C.c_int32), ("hoist_gates", C.c_int32), ("fold_trailing_diag", C.c_int32)]
+                ("fuse_gates", C.c_int32), ("hoist_gates", C.c_int32), ("fold_trailing_diag", C.c_int32),
+                ("jit", C.c_int32)]
 
 
 class _Info(C.Structure):
@@ -54,7 +55,7 @@ class _RunArgs(C.Structure):
 _lib = None
 
 EXPORTS = ["hsf_plan_opts_default", "hsf_plan", "hsf_plan_info_get", "hsf_run", "hsf_workspace_bytes",
-           "hsf_plan_free", "hsf_status_str", "hsf_last_error", "hsf_version"]
+           "hsf_plan_free", "hsf_status_str", "hsf_last_error", "hsf_version", "hsf_debug_pass_source"]
 
 
 def lib():
@@ -79,6 +80,8 @@ def lib():
     L.hsf_last_error.argtypes = [C.c_char_p, C.c_size_t]
     L.hsf_last_error.restype = C.c_size_t
     L.hsf_version.restype = C.c_char_p
+    L.hsf_debug_pass_source.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_char_p, C.c_size_t]
+    L.hsf_debug_pass_source.restype = C.c_size_t
     for f in ("hsf_plan_opts_default", "hsf_plan", "hsf_plan_info_get", "hsf_run"):
         getattr(L, f).restype = C.c_int
     _lib = L
@@ -104,7 +107,7 @@ class Plan:
     def __init__(self, circuit_text: str, n_low: int, blocks=None, dtype: str = "c64", individual: bool = False,
                  svd_rel_tol: float = 1e-12, tile_qubits: int = 0, fuse_gates: bool = True,
                  log2_path_budget: float = 26.0, max_dense_block_qubits: int = 10, hoist_gates: bool = True,
-                 fold_trailing_diag: bool = True):
+                 fold_trailing_diag: bool = True, jit: bool = True):
         L = lib()
         o = _Opts()
         _check(L.hsf_plan_opts_default(C.byref(o)))
@@ -115,6 +118,7 @@ class Plan:
         o.fuse_gates = int(fuse_gates)
         o.hoist_gates = int(hoist_gates)
         o.fold_trailing_diag = int(fold_trailing_diag)
+        o.jit = int(jit)
         o.log2_path_budget = log2_path_budget
         o.max_dense_block_qubits = max_dense_block_qubits
         blocks = blocks or []
@@ -192,6 +196,16 @@ class Plan:
                        C.cast(phase, C.POINTER(C.c_double)) if timings else None)
         _check(lib().hsf_run(self._h, C.byref(a)))
         return list(phase) if timings else None
+
+    def pass_source(self, half: int, pass_index: int, variant: int = 0) -> str | None:
+        """CUDA source of one specialised simulator pass kernel (inspection)."""
+        L = lib()
+        n = L.hsf_debug_pass_source(self._h, variant, half, pass_index, None, 0)
+        if not n:
+            return None
+        buf = C.create_string_buffer(n + 1)
+        L.hsf_debug_pass_source(self._h, variant, half, pass_index, buf, n + 1)
+        return buf.value.decode()
 
     def workspace_bytes(self, bitstrings_count: int = 0, path_range=None, row_range=None, precision="auto") -> int:
         a = self._args(1, True, 1 if bitstrings_count else None, bitstrings_count, True, path_range, row_range,

@@ -361,3 +361,25 @@ def test_trailing_diagonal_fold(torch, path_range):
         check(got, ref, "c64")
     got, _ = gpu_bits(torch, inst, inst.bitstrings, dtype="c128", path_range=path_range)
     check(got, ref, "c128")
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_interpreter_kernel_twins(torch, name):
+    # jit=False: the generic interpreter pass kernel (hsf_pass_kernel) instead
+    # of the run-time specialised kernels; both must match the oracle
+    inst = make_config(name, twin=True)
+    n, g = O.parse_circuit(inst.text)
+    ref = O.schrodinger(n, g)
+    for dtype in ("c64", "c128"):
+        got, _ = gpu_full(torch, inst, dtype=dtype, precision="simt", jit=False)
+        check(got, ref, dtype)
+    inst = make_config(name, twin=True, n=26, n_low=13) if name in ("c3", "c5") else None
+    if inst is not None:
+        n, g = O.parse_circuit(inst.text)
+        P = O.plan(n, g, inst.n_low, inst.blocks)
+        A, B, c = O.half_states(P, 0, 8)
+        bits = inst.bitstrings[:2048]
+        ref = O.recombine_bits(A, B, c, bits, inst.n_low)
+        for jit in (False, True):
+            got, _ = gpu_bits(torch, inst, bits, path_range=(0, 8), jit=jit, tile_qubits=11)
+            check(got, ref, "c64")
