@@ -322,11 +322,14 @@ def main():
                 "peak_source": "148 SM x 128 FP32 lanes x 2 x median SM clock under load (MEASURED_PEAKS.json)"}
     else:
         nb = len(inst.bitstrings)
-        byts = nb * 2 * K * esz
+        # folded trailing diagonal units shrink the operand rows (tree paths)
+        Kt = K // (int(np.prod(P.ranks[len(P.ranks) - P.fold_units:])) if P.fold_units else 1)
+        byts = nb * 2 * Kt * esz
         ach = byts / (core_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "kernel": "gather_dot (bitstring path-sum)", "achieved": ach, "peak": hbm,
                 "unit": "GB/s", "frac": ach / hbm, "traffic": None, "kernel_ms": core_ms,
-                "note": "algorithmic bytes = 2 K-rows per sample (upper bound; repeated rows hit L2)"}
+                "note": "algorithmic bytes = 2 operand rows of %d tree paths per sample (upper bound; rows "
+                        "shared by samples hit L2, so frac > 1 means L2-resident operands)" % Kt}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
