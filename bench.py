@@ -37,6 +37,8 @@ def _args():
     ap.add_argument("--precision", default="auto")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--standard", action="store_true",
+                    help="also time standard HSF (every crossing gate cut alone) on the same output: T/J")
     ap.add_argument("--collective", default="auto", choices=["auto", "reduce_scatter", "allreduce", "rows"],
                     help="N>1 exchange (paper_2502_06959_b200/dist.py); auto = cheapest for the output mode")
     return ap.parse_args()
@@ -101,7 +103,8 @@ def cpu_oracle_rate(inst, budget_s: float = 15.0):
     from oracle import hsf_oracle as O
     n, g = O.parse_circuit(inst.text)
     t0 = time.perf_counter()
-    P = O.plan(n, g, inst.n_low, inst.blocks)
+    blocks = O.find_cascades(g, inst.n_low)[0] if inst.blocks == "auto" else inst.blocks
+    P = O.plan(n, g, inst.n_low, blocks)
     t_plan = time.perf_counter() - t0
     k = 1
     done = 0
@@ -109,6 +112,8 @@ def cpu_oracle_rate(inst, budget_s: float = 15.0):
     # full outputs beyond 2^24 amplitudes: the Kronecker sum over a row subset,
     # the rate scaled by the fraction of rows (c4: 2^34 outputs)
     rows_all = 1 << (n - inst.n_low)
+    if inst.meta.get("prefix"):  # the workload itself is a row prefix (first 10^6 amplitudes)
+        rows_all = -(-inst.meta["prefix"] // (1 << inst.n_low))
     rows = rows_all if inst.bitstrings is not None else max(1, min(rows_all, (1 << 24) >> inst.n_low))
     while True:
         t1 = time.perf_counter()
@@ -149,7 +154,8 @@ def reference_arm(a):
     v = statistics.median(vals)
     from oracle import hsf_oracle as O
     n, g = O.parse_circuit(inst.text)
-    npaths = O.plan(n, g, inst.n_low, inst.blocks).n_paths
+    blocks = O.find_cascades(g, inst.n_low)[0] if inst.blocks == "auto" else inst.blocks
+    npaths = O.plan(n, g, inst.n_low, blocks).n_paths
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "paths/s", "n_gpus": a.gpus,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * npaths / v, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
@@ -158,6 +164,41 @@ def reference_arm(a):
             "e2e": {"value": v, "unit": "paths/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+# ------------------------------------------------------- standard HSF (T/J)
+def standard_hsf(inst, precision, t_joint_ms, prefix_rows, out, bits_d, budget_s=20.0):
+    """Standard HSF (every crossing gate cut alone) on the same output,
+    run through the same library in path chunks accumulated in place
+    (hsf_run accumulate=1).  Timed with CUDA events once after a warm-up
+    chunk; beyond `budget_s` the remaining chunks are extrapolated and the
+    time reported as a lower bound (the paper reports a timeout bound)."""
+    import torch
+    from paper_2502_06959_b200 import Plan
+    Pi = Plan(inst.text, inst.n_low, None, dtype=inst.dtype, individual=True, log2_path_budget=62)
+    m = max(Pi.n_a, Pi.n_b)
+    chunk = max(1, min(Pi.n_paths, (1 << 33) >> (m + 3)))  # <= 8 GiB of leaves per half per chunk
+    rr = (0, prefix_rows) if prefix_rows else None
+    n_chunks = -(-Pi.n_paths // chunk)
+    Pi.run(out, bitstrings=bits_d, path_range=(0, min(chunk, Pi.n_paths)), row_range=rr, precision=precision)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    done, t0 = 0, time.perf_counter()
+    e0.record()
+    for c in range(n_chunks):
+        p0, p1 = c * chunk, min(Pi.n_paths, (c + 1) * chunk)
+        Pi.run(out, bitstrings=bits_d, path_range=(p0, p1), row_range=rr, precision=precision, accumulate=c > 0)
+        done = p1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    full_ms = ms * Pi.n_paths / done
+    return {"n_paths_individual": Pi.n_paths, "ms": full_ms, "measured_paths": done,
+            "lower_bound": done < Pi.n_paths, "T_over_J": full_ms / t_joint_ms,
+            "note": "same library, every crossing gate its own cut unit; chunks of %d paths accumulated on "
+                    "the device" % chunk}
 
 
 # ----------------------------------------------------------------- our arm
@@ -194,15 +235,20 @@ def main():
         if any(int(x.item()) != int(h.item()) for x in hs):
             raise RuntimeError("plan hash mismatch across ranks")
     full = inst.bitstrings is None
-    mode = a.collective if a.collective != "auto" else D.default_mode(full, P.n_paths, P.n_a, P.n_b, world)
+    prefix = inst.meta.get("prefix")
+    prefix_rows = -(-prefix // (1 << P.n_b)) if prefix else None
+    if prefix:  # small output (first `prefix` amplitudes): split paths, all-reduce
+        mode = "allreduce"
+    else:
+        mode = a.collective if a.collective != "auto" else D.default_mode(full, P.n_paths, P.n_a, P.n_b, world)
     sh = D.make_shard(mode, P.n_paths, P.n_a, rank, world, full)
     pr = sh.path_range
     cdt = torch.complex64 if inst.dtype == "c64" else torch.complex128
     esz = 8 if inst.dtype == "c64" else 16
     stream = torch.cuda.current_stream()
     if full:
-        N_out = 1 << inst.n
-        rows = (sh.row_range[1] - sh.row_range[0]) if sh.row_range else (1 << P.n_a)
+        N_out = prefix if prefix else 1 << inst.n
+        rows = (sh.row_range[1] - sh.row_range[0]) if sh.row_range else (prefix_rows or (1 << P.n_a))
         out = torch.empty(rows << P.n_b, dtype=cdt, device="cuda")
         shard = torch.empty(N_out // world, dtype=cdt, device="cuda") if mode == "reduce_scatter" and world > 1 \
             else None
@@ -216,6 +262,8 @@ def main():
 
     def step(timed=False):
         def partial(path_range, row_range, o):
+            if prefix:
+                row_range = (0, prefix_rows)
             ph = P.run(o, bitstrings=bits_d, path_range=path_range, row_range=row_range, precision=a.precision,
                        timings=timed)
             if timed:
@@ -264,14 +312,15 @@ def main():
         e2e = {"value": None, "unit": "paths/s", "skipped": "output of %d bytes exceeds a quarter of the host's "
                "available memory (%d bytes) for a pinned host buffer" % (N_out * esz, host_avail)}
     elif rank == 0:
-        host_out = torch.empty(N_out, dtype=cdt, pin_memory=True)
+        host_out = torch.empty(max(N_out, (rows << P.n_b) if full else 0), dtype=cdt, pin_memory=True)
         host_bits = None if full else torch.from_numpy(inst.bitstrings.view(np.int64)).pin_memory()
         tt = []
         for i in range(max(2, min(a.steps, 5))):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             P2 = Plan(inst.text, inst.n_low, inst.blocks, dtype=inst.dtype)
-            P2.run(host_out, bitstrings=host_bits, precision=a.precision)
+            P2.run(host_out[:rows << P.n_b] if full else host_out, bitstrings=host_bits, precision=a.precision,
+                   row_range=(0, prefix_rows) if prefix else None)
             tt.append(time.perf_counter() - t0)
             del P2
         te = statistics.median(tt[1:]) if len(tt) > 1 else tt[0]
@@ -331,6 +380,27 @@ def main():
                 "note": "algorithmic bytes = 2 operand rows of %d tree paths per sample (upper bound; rows "
                         "shared by samples hit L2, so frac > 1 means L2-resident operands)" % Kt}
 
+    # the simulator tree (both halves concurrently): algorithmic bytes of its
+    # tile passes over this rank's share of the paths / the sim phase
+    used_fold = (not full) and P.fold_units > 0
+    tb = P.fold_tree_bytes if used_fold else P.tree_bytes
+    sim_ms = max(phase[0], phase[1])
+    sim_bytes = (tb[0] + tb[1]) * (K / P.n_paths)
+    sim_ach = sim_bytes / (sim_ms * 1e-3) / 1e9
+    roof_sim = {"bound": "hbm", "kernel": "simulator tile passes (hsf_jit_pass, both halves)", "achieved": sim_ach,
+                "peak": hbm, "unit": "GB/s", "frac": sim_ach / hbm, "traffic": None, "kernel_ms": sim_ms,
+                "bytes": sim_bytes,
+                "note": "algorithmic bytes = every pass reads + writes each output node state once; small "
+                        "states stay L2/SMEM-resident, so frac can exceed 1"}
+    if sim_ms > core_ms:
+        roof, roof_other = roof_sim, roof
+    else:
+        roof_other = roof_sim
+
+    std = None
+    if a.standard and rank == 0 and world == 1:
+        std = standard_hsf(inst, a.precision, t_step, prefix_rows, out, bits_d)
+
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         r, sample, thr, _ = cpu_oracle_rate(inst, budget_s=15.0)
@@ -348,7 +418,9 @@ def main():
                 "amplitudes_per_s": amps, "terms_per_s": amps * P.n_paths,
                 "phase_ms": {"sim_A": phase[0], "sim_B": phase[1], "prep": phase[2], "core": phase[3],
                              "run_total": phase[4]},
-                "plan_s": t_plan, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "plan_s": t_plan, "roofline": roof, "roofline_other": roof_other, "cpu_baseline": cpu,
+                "e2e": e2e, "joint_blocks": P.n_joint_blocks, "separate_cuts": P.n_units - P.n_joint_blocks,
+                "folded_units": P.fold_units if not full else 0, "standard_hsf": std,
                 "gpu_launches": n_launch, "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -15,6 +15,8 @@ from .circuits import (  # noqa: F401
     make_c4,
     make_c5,
     make_sbm_qaoa,
+    make_table2,
+    TABLE2,
     random_small_circuit,
     serialize,
 )

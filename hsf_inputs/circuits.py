@@ -280,6 +280,30 @@ def make_sbm_qaoa(seed: int = 30, sizes=(15, 15), p_intra: float = 0.8, p_inter:
     return Instance(f"sbm{n}", n, nb, g, blocks, bits, "c64", {"seed": seed})
 
 
+# ------------------------------------------- Table II-shaped QAOA (NEXT row 1)
+# PAPER.md Table II: single-layer QAOA MaxCut on two-community
+# stochastic-block-model graphs, p_intra 0.8, cut after the first partition,
+# output = the first 10^6 amplitudes.  Synthetic stand-ins:
+# same shapes, our seeds (the paper's graphs are unpublished).  Blocks are
+# found by the planner ("auto").
+TABLE2 = {
+    "q30-1": ((15, 15), 0.10), "q30-2": ((15, 15), 0.15), "q30-3": ((15, 15), 0.17),
+    "q31-1": ((15, 16), 0.10), "q31-2": ((15, 16), 0.15), "q31-3": ((15, 16), 0.17),
+    "q32-1": ((16, 16), 0.10), "q32-2": ((16, 16), 0.11), "q32-3": ((16, 16), 0.12),
+    "q33-1": ((16, 17), 0.10), "q33-2": ((16, 17), 0.11), "q33-3": ((16, 17), 0.12),
+}
+
+
+def make_table2(name: str, seed: int | None = None, prefix: int = 10 ** 6) -> Instance:
+    sizes, p_inter = TABLE2[name]
+    idx = sorted(TABLE2).index(name)
+    inst = make_sbm_qaoa(seed=3000 + idx if seed is None else seed, sizes=sizes, p_intra=0.8, p_inter=p_inter)
+    inst.name = name
+    inst.blocks = "auto"
+    inst.meta.update({"prefix": prefix, "sizes": sizes, "p_inter": p_inter, "p_intra": 0.8})
+    return inst
+
+
 # ---------------------------------------------------------- random small sweeps
 _NAMED_1Q = ("h", "x", "z", "rx", "rz")
 _NAMED_2Q = ("cz", "cx", "swap", "cp", "rzz")
@@ -365,6 +389,14 @@ TWINS = {
 
 
 def make_config(name: str, seed: int | None = None, twin: bool = False, **kw) -> Instance:
+    if name in TABLE2:
+        if twin:  # oracle-sized stand-in of the same family
+            inst = make_sbm_qaoa(seed=3100 + sorted(TABLE2).index(name) if seed is None else seed, sizes=(6, 6),
+                                 p_intra=0.8, p_inter=0.3)
+            inst.name, inst.blocks = name + "t", "auto"
+            inst.meta["prefix"] = 1000
+            return inst
+        return make_table2(name, seed, **kw)
     fn = CONFIGS[name]
     args = dict(TWINS[name]) if twin else {}
     args.update(kw)

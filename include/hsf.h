@@ -111,7 +111,10 @@ hsf_status hsf_plan_opts_default(hsf_plan_opts* opts);
  *   circuit_text, text_len : circuit file contents (format in DESIGN.md)
  *   n_low                  : qubits in half B; 1 <= n_low < n
  *   n_blocks               : number of joint blocks (0 => every crossing gate
- *                            is its own unit)
+ *                            is its own unit; -1 => automatic cascades: the
+ *                            fewest groups of commuting diagonal two-qubit
+ *                            crossing gates sharing one qubit (minimum vertex
+ *                            cover), other crossing gates alone)
  *   block_offsets          : CSR offsets, length n_blocks+1 (may be NULL iff
  *                            n_blocks == 0)
  *   block_gate_ids         : gate indices (0-based, file order) of each block
@@ -138,6 +141,11 @@ typedef struct {
   int32_t ops_a, ops_b;         /* device ops after fusion */
   uint64_t plan_hash;           /* FNV-1a of the device program + tables */
   int32_t fold_units;           /* trailing diagonal units folded in bitstring runs (0 = none) */
+  int32_t n_joint_blocks;       /* units holding more than one gate (the paper's "blocks";
+                                   n_units - n_joint_blocks = its "separate cuts") */
+  double tree_bytes_a, tree_bytes_b; /* state bytes the simulator tile passes read + write
+                                   for all paths (full tree; roofline numerator) */
+  double fold_tree_bytes_a, fold_tree_bytes_b; /* same for the folded tree (0 if none) */
 } hsf_plan_info;
 
 /* Pointers in *info stay valid until hsf_plan_free. */
@@ -171,6 +179,9 @@ typedef struct {
                                    [3] core path-sum kernel (tcgen05 GEMM /
                                        SIMT GEMM / gather)
                                    [4] total */
+  int32_t accumulate;           /* 1 => out += this run's result (device output only;
+                                   e.g. path ranges run in chunks, or partial sums
+                                   combined on one GPU); 0 => out is overwritten */
 } hsf_run_args;
 
 /* hsf_run — evaluate the paths [path_begin, path_end) on the GPU: path-tree

@@ -210,9 +210,21 @@ class NonConvexBlock(ValueError):
     pass
 
 
+def _is_diagonal(U) -> bool:
+    return bool(np.count_nonzero(U - np.diag(np.diag(U))) == 0)
+
+
 def _schedule(gates, n_low, units_gate_ids):
-    """Contract each unit in the wire DAG and Kahn-sort (ties: smallest gate id).
-    Returns [("gate", gid) | ("unit", uid)]; raises NonConvexBlock on a cycle."""
+    """Contract each unit in the gate-dependency DAG and Kahn-sort (ties:
+    smallest gate id).  Returns [("gate", gid) | ("unit", uid)]; raises
+    NonConvexBlock on a cycle.
+
+    Dependencies follow commutation: an op depends on every earlier op on a
+    shared qubit unless both are diagonal (diagonal operators commute), so a
+    block of mutually commuting diagonal gates (the paper's RZZ cascades, which
+    "mutually commute, which gives a lot of freedom to reorder the gates such
+    that grouping ... can be performed") is convex however the
+    commuting gates are interleaved in the file."""
     owner = {}
     for u, ids in enumerate(units_gate_ids):
         for gi in ids:
@@ -223,14 +235,27 @@ def _schedule(gates, n_low, units_gate_ids):
         nodes.setdefault(key, []).append(gi)
     succ = {k: set() for k in nodes}
     indeg = {k: 0 for k in nodes}
-    last = {}
+    last_nd = {}   # qubit -> node of the last non-diagonal gate
+    diags = {}     # qubit -> nodes of diagonal gates since then
     for gi, g in enumerate(gates):
         key = owner.get(gi, ("gate", gi))
+        diag = _is_diagonal(g.U)
+        deps = set()
         for q in g.qubits:
-            if q in last and last[q] != key and key not in succ[last[q]]:
-                succ[last[q]].add(key)
+            if q in last_nd:
+                deps.add(last_nd[q])
+            if not diag:
+                deps.update(diags.get(q, ()))
+        for d in deps:
+            if d != key and key not in succ[d]:
+                succ[d].add(key)
                 indeg[key] += 1
-            last[q] = key
+        for q in g.qubits:
+            if diag:
+                diags.setdefault(q, set()).add(key)
+            else:
+                last_nd[q] = key
+                diags[q] = set()
     import heapq
     heap = [(min(nodes[k]), k) for k in nodes if indeg[k] == 0]
     heapq.heapify(heap)
@@ -360,6 +385,45 @@ def plan(n, gates, n_low, blocks=None, mode="joint") -> Plan:
     remap = {u: i for i, u in enumerate(sched_units)}
     order = [("unit", remap[k[1]]) if k[0] == "unit" else k for k in order]
     return Plan(n, n_low, gates, units, order)
+
+
+def find_cascades(gates, n_low):
+    """Automatic joint blocks: cascades of commuting diagonal
+    two-qubit crossing gates sharing one qubit, as few as possible.
+
+    Each such gate is an edge between its low and high qubit, each tagged with
+    its epoch (count of earlier non-diagonal gates on that qubit); a minimum
+    vertex cover of this bipartite multigraph (networkx Hopcroft-Karp matching
+    + Koenig's theorem, a library primitive) is a smallest set of cascade
+    centres.  Returns (blocks with >= 2 gates, number of cascades)."""
+    import networkx as nx
+    from networkx.algorithms import bipartite
+    epoch = {}
+    G = nx.Graph()
+    edges = []
+    for gi, g in enumerate(gates):
+        if len(g.qubits) == 2 and _is_diagonal(g.U):
+            b, a = sorted(g.qubits)
+            if b < n_low <= a:
+                lb, ra = ("L", b, epoch.get(b, 0)), ("R", a, epoch.get(a, 0))
+                G.add_node(lb, bipartite=0)
+                G.add_node(ra, bipartite=1)
+                G.add_edge(lb, ra)
+                edges.append((gi, lb, ra))
+        if not _is_diagonal(g.U):
+            for q in g.qubits:
+                epoch[q] = epoch.get(q, 0) + 1
+    if not edges:
+        return [], 0
+    left = {v for v in G if v[0] == "L"}
+    matching = bipartite.hopcroft_karp_matching(G, top_nodes=left)
+    cover = bipartite.to_vertex_cover(G, matching, top_nodes=left)
+    groups = {}
+    for gi, lb, ra in edges:
+        key = lb if lb in cover else ra
+        groups.setdefault(key, []).append(gi)
+    blocks = sorted(sorted(v) for v in groups.values() if len(v) >= 2)
+    return blocks, len(cover)
 
 
 # ----------------------------------------------------------------- path engine

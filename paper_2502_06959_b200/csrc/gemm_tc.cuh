@@ -50,6 +50,7 @@ struct Params {
   int num_m, num_n, num_k;  // blocks
   int n_fastest;            // tile raster: 1 => consecutive tiles walk N
   int a_evict_last;         // 1 => A operand loads carry an L2 evict-last hint
+  int accumulate;           // 1 => out += D (TMA reduce-add) instead of out = D
   int x3;
   float* out;               // D, row-major, ld = ldo floats
   long long ldo;
@@ -102,6 +103,15 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
                    map),
                "r"(smem_u32(src)), "r"(c0), "r"(c1), "l"(policy)
                : "memory");
+}
+// accumulate mode: the TMA engine adds the box into global memory (fp32 add)
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const void* src, int c0, int c1,
+                                                  uint64_t policy) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;" ::"l"(
+          map),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
 }
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
@@ -303,7 +313,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async proxy
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d(&mOut, stg, nb * BN + c * 32, mb * BM + q * 32, st_pol);
+          if (p.accumulate)
+            tma_reduce_add_2d(&mOut, stg, nb * BN + c * 32, mb * BM + q * 32, st_pol);
+          else
+            tma_store_2d(&mOut, stg, nb * BN + c * 32, mb * BM + q * 32, st_pol);
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
       }
@@ -503,7 +516,7 @@ inline void tc_prep_b(const TcBuffers& t, const float2* leavesB, long long K, lo
 // K5: the persistent tcgen05 GEMM over operand rows [row0, row0 + rows)
 // (row0 a multiple of BM) into out[rows][2*MB] fp32
 inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row0, long long rows, bool x3,
-                    cudaStream_t st) {
+                    cudaStream_t st, bool accumulate = false) {
   const long long kcols = 2 * t.d.Kpad;  // bf16 per operand row
   if (row0 % tc::BM) fail(HSF_ERR_INVALID_ARG, "tc_gemm row offset not tile aligned");
   const long long rpad = (rows + tc::BM - 1) / tc::BM * tc::BM;
@@ -517,6 +530,7 @@ inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row
   p.num_n = (int)(t.d.nrows_b_pad / tc::BN);
   p.num_k = (int)(kcols / tc::BK);
   p.x3 = x3 ? 1 : 0;
+  p.accumulate = accumulate ? 1 : 0;
   // M-fastest raster: the ~148 concurrent tiles share one B tile (read once
   // from DRAM) and sweep A; A stays L2-resident (evict-last) when it is small
   // (c4: 64 MiB for hi+lo), while the streaming output stores are evict-first.

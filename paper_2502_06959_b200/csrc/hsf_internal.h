@@ -111,6 +111,7 @@ struct Half {
   int n_passes = 0;
   double est_ms = 0;                 // planner's cost-model estimate of the tree (all paths)
   int last_gate_level = 0;           // deepest level holding a local gate
+  double tree_bytes = 0;             // state bytes the tile passes read + write (all paths)
 };
 
 struct Plan {

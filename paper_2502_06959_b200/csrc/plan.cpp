@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <queue>
@@ -359,15 +360,35 @@ static std::vector<SchedItem> schedule(const std::vector<Gate>& gates, const std
   std::vector<std::set<int>> succ(NN);
   std::vector<int> indeg(NN, 0), minid(NN, 1 << 30);
   std::vector<char> exists(NN, 0);
-  std::map<int, int> last;
+  // dependencies follow commutation: an op depends on every earlier op on a
+  // shared qubit unless both are diagonal (diagonal operators commute), so a
+  // block of commuting diagonal gates is convex however they are interleaved
+  // (the paper reorders commuting RZZ gates to form cascades)
+  std::map<int, int> last_nd;             // qubit -> node of the last non-diagonal gate
+  std::map<int, std::set<int>> diags;     // qubit -> diagonal nodes since then
   for (int gi = 0; gi < G; ++gi) {
     int nd = node_of(gi);
     exists[nd] = 1;
     minid[nd] = std::min(minid[nd], gi);
+    const bool dg = gates[gi].diag;
+    std::set<int> deps;
     for (int q : gates[gi].q) {
-      auto it = last.find(q);
-      if (it != last.end() && it->second != nd && succ[it->second].insert(nd).second) indeg[nd]++;
-      last[q] = nd;
+      auto it = last_nd.find(q);
+      if (it != last_nd.end()) deps.insert(it->second);
+      if (!dg) {
+        auto jt = diags.find(q);
+        if (jt != diags.end()) deps.insert(jt->second.begin(), jt->second.end());
+      }
+    }
+    for (int d : deps)
+      if (d != nd && succ[d].insert(nd).second) indeg[nd]++;
+    for (int q : gates[gi].q) {
+      if (dg) {
+        diags[q].insert(nd);
+      } else {
+        last_nd[q] = nd;
+        diags[q].clear();
+      }
     }
   }
   using P = std::pair<int, int>;
@@ -386,7 +407,8 @@ static std::vector<SchedItem> schedule(const std::vector<Gate>& gates, const std
     for (int s : succ[v])
       if (--indeg[s] == 0) pq.push({minid[s], s});
   }
-  if ((int)order.size() != total) fail(HSF_ERR_NONCONVEX_BLOCK, "a block is not convex in the wire DAG");
+  if ((int)order.size() != total)
+    fail(HSF_ERR_NONCONVEX_BLOCK, "a block is not convex in the gate-dependency DAG (non-commuting gate inside)");
   return order;
 }
 
@@ -911,6 +933,16 @@ static void build_half(Plan& P, int h, const std::vector<SchedItem>& order, int 
     prev = L;
   }
   finalize_half(H, P.opts.dtype == HSF_C64 ? 8 : 16);
+  // algorithmic traffic of the tree: every pass reads and writes each output
+  // node's state once (the first pass from |0...0> reads nothing)
+  H.tree_bytes = 0;
+  {
+    const double S = std::ldexp(1.0, H.m) * (P.opts.dtype == HSF_C64 ? 8.0 : 16.0);
+    for (const auto& tr : H.trans) {
+      const double N = (double)range_prod(P.ranks, 0, tr.level_out);
+      H.tree_bytes += N * S * (2.0 * (double)tr.passes.size() - (tr.level_in < 0 ? 1.0 : 0.0));
+    }
+  }
   if (std::getenv("HSF_DEBUG_PLAN")) {
     static const char* kn[] = {"DENSE", "DIAG", "RPASS", "R1"};
     std::fprintf(stderr, "half %c: m=%d levels=%zu est=%.3f ms\n", h == 0 ? 'A' : 'B', H.m, H.materialized.size(), H.est_ms);
@@ -939,6 +971,100 @@ static uint64_t fnv(uint64_t h, const void* p, size_t n) {
   return h;
 }
 
+// ------------------------------------------------------ automatic joint blocks
+// The paper groups commuting RZZ gates into cascades sharing one qubit and
+// cuts each cascade jointly ("we use a brute force algorithm to reassemble
+// cascades of RZZ gates which can be cut jointly"; a cascade of
+// diagonal two-qubit gates with a common qubit has Schmidt rank <= 2, Eq. 11,
+// P:197-207).  Here: every diagonal two-qubit gate crossing the cut is an
+// edge between its low-side and high-side qubit, each endpoint tagged with
+// its "epoch" (number of non-diagonal gates on that qubit before the gate,
+// so a cascade never spans a non-commuting gate on its shared qubit).  A
+// minimum vertex cover of this bipartite multigraph (Koenig: from a maximum
+// matching) gives the fewest cascades covering every such gate; each gate
+// joins the cascade of a covering endpoint.  Cascades of one gate stay
+// separate cuts; other crossing gates are cut individually.
+static std::vector<std::vector<int>> auto_blocks(const std::vector<Gate>& gates, int n_low) {
+  std::map<std::pair<int, int>, int> lid, rid;  // (qubit, epoch) -> vertex id
+  std::vector<std::pair<int, int>> edges;       // (left vertex, right vertex) per candidate gate
+  std::vector<int> egate;
+  std::map<int, int> epoch;
+  for (int gi = 0; gi < (int)gates.size(); ++gi) {
+    const Gate& g = gates[gi];
+    if (g.k == 2 && g.diag && ((g.q[0] < n_low) != (g.q[1] < n_low))) {
+      const int b = std::min(g.q[0], g.q[1]), a = std::max(g.q[0], g.q[1]);
+      auto kb = std::make_pair(b, epoch[b]), ka = std::make_pair(a, epoch[a]);
+      if (!lid.count(kb)) lid[kb] = (int)lid.size();
+      if (!rid.count(ka)) rid[ka] = (int)rid.size();
+      edges.push_back({lid[kb], rid[ka]});
+      egate.push_back(gi);
+    }
+    if (!g.diag)
+      for (int q : g.q) epoch[q]++;
+  }
+  const int NL = (int)lid.size(), NR = (int)rid.size();
+  std::vector<std::vector<int>> adj(NL);
+  for (auto& e : edges) adj[e.first].push_back(e.second);
+  for (auto& v : adj) {
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+  }
+  // maximum matching (Kuhn's augmenting paths; graphs here have <= ~100 vertices)
+  std::vector<int> matchR(NR, -1), matchL(NL, -1);
+  std::vector<char> seen;
+  std::function<bool(int)> augment = [&](int l) -> bool {
+    for (int r : adj[l]) {
+      if (seen[r]) continue;
+      seen[r] = 1;
+      if (matchR[r] < 0 || augment(matchR[r])) {
+        matchR[r] = l;
+        matchL[l] = r;
+        return true;
+      }
+    }
+    return false;
+  };
+  for (int l = 0; l < NL; ++l) {
+    seen.assign(NR, 0);
+    augment(l);
+  }
+  // Koenig: Z = vertices reachable from unmatched left vertices by alternating paths
+  std::vector<char> zl(NL, 0), zr(NR, 0);
+  std::vector<int> stack;
+  for (int l = 0; l < NL; ++l)
+    if (matchL[l] < 0) {
+      zl[l] = 1;
+      stack.push_back(l);
+    }
+  while (!stack.empty()) {
+    int l = stack.back();
+    stack.pop_back();
+    for (int r : adj[l])
+      if (!zr[r] && matchL[l] != r) {
+        zr[r] = 1;
+        int l2 = matchR[r];
+        if (l2 >= 0 && !zl[l2]) {
+          zl[l2] = 1;
+          stack.push_back(l2);
+        }
+      }
+  }
+  // cover = (L \ Z) u (R n Z); each gate joins a covering endpoint (left first)
+  std::map<std::pair<int, int>, std::vector<int>> groups;  // (side, vertex) -> gates
+  for (size_t i = 0; i < edges.size(); ++i) {
+    const int l = edges[i].first, r = edges[i].second;
+    if (!zl[l])
+      groups[{0, l}].push_back(egate[i]);
+    else
+      groups[{1, r}].push_back(egate[i]);
+  }
+  std::vector<std::vector<int>> blocks;
+  for (auto& kv : groups)
+    if (kv.second.size() >= 2) blocks.push_back(kv.second);
+  std::sort(blocks.begin(), blocks.end());
+  return blocks;
+}
+
 // ----------------------------------------------------------------- driver
 Plan* build_plan(const char* text, size_t len, int n_low, int64_t n_blocks, const int64_t* off, const int64_t* ids,
                  const hsf_plan_opts& opts) {
@@ -956,6 +1082,17 @@ Plan* build_plan(const char* text, size_t len, int n_low, int64_t n_blocks, cons
   // units: user blocks (joint mode) + singleton crossing gates
   std::vector<std::vector<int>> units;
   std::vector<char> in_block(G, 0);
+  std::vector<std::vector<int>> found;
+  if (!opts.individual && n_blocks < 0) {
+    found = auto_blocks(P->gates, n_low);
+    n_blocks = 0;
+  }
+  if (!opts.individual && !found.empty()) {
+    for (auto& blk : found) {
+      for (int gi : blk) in_block[gi] = 1;
+      units.push_back(blk);
+    }
+  }
   if (!opts.individual && n_blocks > 0) {
     if (!off || !ids) fail(HSF_ERR_INVALID_ARG, "block CSR arrays are NULL");
     for (int64_t b = 0; b < n_blocks; ++b) {

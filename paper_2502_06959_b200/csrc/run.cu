@@ -441,9 +441,11 @@ static void run_core_bits(Plan* P, DeviceState* d, const Layout& L, const hsf_ru
   }
   if (sizeof(R) == 4 && K % 64 == 0) {
     gather_dot_c64_vec_kernel<<<(unsigned)blocks, 256, 0, st>>>((const float4*)AT, (const float4*)BT, bits,
-                                                                (float2*)out, ns, K, nB, tw, (const float2*)d->trail);
+                                                                (float2*)out, ns, K, nB, tw, (const float2*)d->trail,
+                                                                a.accumulate);
   } else {
-    gather_dot_kernel<C><<<(unsigned)blocks, 256, 0, st>>>(AT, BT, bits, out, ns, K, nB, tw, (const C*)d->trail);
+    gather_dot_kernel<C><<<(unsigned)blocks, 256, 0, st>>>(AT, BT, bits, out, ns, K, nB, tw, (const C*)d->trail,
+                                                           a.accumulate);
   }
   CK(cudaGetLastError());
 }
@@ -452,7 +454,7 @@ static void run_core_bits(Plan* P, DeviceState* d, const Layout& L, const hsf_ru
 // (device, row-major [nrows][2^nB]); lo is a multiple of the tensor-core M tile
 template <typename R>
 static void run_core_full(Plan* P, DeviceState* d, const Layout& L, cudaStream_t st, uint64_t lo, uint64_t nrows,
-                          typename cplx<R>::T* out) {
+                          typename cplx<R>::T* out, bool accumulate) {
   using C = typename cplx<R>::T;
   char* ws = (char*)d->ws;
   const int nA = P->n - P->n_low, nB = P->n_low;
@@ -462,13 +464,13 @@ static void run_core_full(Plan* P, DeviceState* d, const Layout& L, cudaStream_t
     const C* leavesB = (const C*)(ws + L.off_leaves[1]);
     dim3 grid((unsigned)(((1ll << nB) + 63) / 64), (unsigned)((nrows + 63) / 64));
     simt_gemm_kernel<C, R><<<grid, 256, 0, st>>>(leavesA, leavesB, (const C*)d->cp, out, K, 1ll << nA, 1ll << nB,
-                                                 (long long)(L.r0 + lo), (long long)nrows);
+                                                 (long long)(L.r0 + lo), (long long)nrows, accumulate ? 1 : 0);
     CK(cudaGetLastError());
   } else {
     if (sizeof(R) != 4) fail(HSF_ERR_UNSUPPORTED, "tensor-core path-sum needs complex64");
     TcBuffers t = tc_buffers(K, (long long)(L.r1 - L.r0), 1ll << nB, L.prec == HSF_PREC_BF16X3, ws + L.off_tc,
                              L.tc_bytes);
-    tc_gemm(t, (float2*)out, 1ll << nB, (long long)lo, (long long)nrows, L.prec == HSF_PREC_BF16X3, st);
+    tc_gemm(t, (float2*)out, 1ll << nB, (long long)lo, (long long)nrows, L.prec == HSF_PREC_BF16X3, st, accumulate);
   }
 }
 
@@ -495,7 +497,7 @@ static void run_all(Plan* P, DeviceState* d, const Layout& L, const hsf_run_args
     if (!a.out_on_device)
       CK(cudaMemcpyAsync(a.out, out, (size_t)a.n_bitstrings * sizeof(C), cudaMemcpyDeviceToHost, st));
   } else if (a.out_on_device) {
-    run_core_full<R>(P, d, L, st, 0, L.r1 - L.r0, (C*)a.out);
+    run_core_full<R>(P, d, L, st, 0, L.r1 - L.r0, (C*)a.out, a.accumulate != 0);
   } else {
     // host output: double-buffered chunks, path-sum on `st`, D2H on `side`
     const uint64_t rows = L.r1 - L.r0;
@@ -505,7 +507,7 @@ static void run_all(Plan* P, DeviceState* d, const Layout& L, const hsf_run_args
       const uint64_t nr = std::min<uint64_t>(L.chunk_rows, rows - lo);
       C* buf = (C*)(ws + L.off_out + (size_t)(c & 1) * L.chunk_bytes);
       if (c >= 2) CK(cudaStreamWaitEvent(st, d->evc[c & 1], 0));
-      run_core_full<R>(P, d, L, st, lo, nr, buf);
+      run_core_full<R>(P, d, L, st, lo, nr, buf, false);
       CK(cudaEventRecord(d->evg[c & 1], st));
       CK(cudaStreamWaitEvent(d->side, d->evg[c & 1], 0));
       CK(cudaMemcpyAsync((char*)a.out + lo * row_bytes, buf, nr * row_bytes, cudaMemcpyDeviceToHost, d->side));
@@ -520,6 +522,7 @@ static void run(Plan* P, const hsf_run_args& a) {
   DeviceState* d = ensure_device(P, a.device);
   Layout L = make_layout(*P, a, d->elem);
   if (!a.out) fail(HSF_ERR_INVALID_ARG, "out is NULL");
+  if (a.accumulate && !a.out_on_device) fail(HSF_ERR_INVALID_ARG, "accumulate needs a device output buffer");
   ensure_ws(d, L.total);
   cudaStream_t st = (cudaStream_t)a.cuda_stream;
   ensure_cp(P, d, L.p0, L.p1, L.U_tree, st);
@@ -592,7 +595,7 @@ hsf_status hsf_plan(const char* text, size_t len, int32_t n_low, int64_t n_block
                     const int64_t* ids, const hsf_plan_opts* opts, hsf_plan_t** out) {
   ABI_GUARD({
     if (!text || !out) fail(HSF_ERR_INVALID_ARG, "NULL argument");
-    if (n_blocks < 0) fail(HSF_ERR_INVALID_ARG, "n_blocks < 0");
+    if (n_blocks < -1) fail(HSF_ERR_INVALID_ARG, "n_blocks < -1");
     *out = nullptr;
     hsf_plan_opts o;
     hsf_plan_opts_default(&o);
@@ -629,6 +632,12 @@ hsf_status hsf_plan_info_get(const hsf_plan_t* plan, hsf_plan_info* info) {
     info->ops_b = (int32_t)P->half[1].ops.size();
     info->plan_hash = P->hash;
     info->fold_units = P->fold_u0 >= 0 ? (int32_t)P->units.size() - P->fold_u0 : 0;
+    info->tree_bytes_a = P->half[0].tree_bytes;
+    info->tree_bytes_b = P->half[1].tree_bytes;
+    info->fold_tree_bytes_a = P->fold_u0 >= 0 ? P->half_fold[0].tree_bytes : 0.0;
+    info->fold_tree_bytes_b = P->fold_u0 >= 0 ? P->half_fold[1].tree_bytes : 0.0;
+    info->n_joint_blocks = 0;
+    for (const auto& un : P->units) info->n_joint_blocks += un.gids.size() > 1 ? 1 : 0;
   })
 }
 

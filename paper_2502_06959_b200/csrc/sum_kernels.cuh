@@ -68,7 +68,7 @@ template <typename C>
 __global__ void gather_dot_kernel(const C* __restrict__ AT, const C* __restrict__ BT,
                                   const unsigned long long* __restrict__ bits, C* __restrict__ out,
                                   long long n_samples, long long K, int n_low, const TrailParams tw,
-                                  const C* __restrict__ trail) {
+                                  const C* __restrict__ trail, int accumulate) {
   const int lane = threadIdx.x & 31;
   const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -86,7 +86,14 @@ __global__ void gather_dot_kernel(const C* __restrict__ AT, const C* __restrict_
       acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
       acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
     }
-    if (lane == 0) out[s] = tw.n ? cmul(acc, trail_weight(tw, trail, b)) : acc;
+    if (lane == 0) {
+      C r = tw.n ? cmul(acc, trail_weight(tw, trail, b)) : acc;
+      if (accumulate) {
+        r.x += out[s].x;
+        r.y += out[s].y;
+      }
+      out[s] = r;
+    }
   }
 }
 
@@ -95,7 +102,7 @@ __global__ void gather_dot_kernel(const C* __restrict__ AT, const C* __restrict_
 __global__ void gather_dot_c64_vec_kernel(const float4* __restrict__ AT, const float4* __restrict__ BT,
                                           const unsigned long long* __restrict__ bits, float2* __restrict__ out,
                                           long long n_samples, long long K, int n_low, const TrailParams tw,
-                                          const float2* __restrict__ trail) {
+                                          const float2* __restrict__ trail, int accumulate) {
   const int lane = threadIdx.x & 31;
   const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -121,7 +128,12 @@ __global__ void gather_dot_c64_vec_kernel(const float4* __restrict__ AT, const f
     }
     if (lane == 0) {
       const float2 a = make_float2(re, im);
-      out[s] = tw.n ? cmul(a, trail_weight(tw, trail, b)) : a;
+      float2 r = tw.n ? cmul(a, trail_weight(tw, trail, b)) : a;
+      if (accumulate) {
+        r.x += out[s].x;
+        r.y += out[s].y;
+      }
+      out[s] = r;
     }
   }
 }
@@ -134,7 +146,7 @@ template <typename C, typename R>
 __global__ void __launch_bounds__(256) simt_gemm_kernel(const C* __restrict__ A, const C* __restrict__ B,
                                                         const C* __restrict__ cp, C* __restrict__ out,
                                                         long long K, long long MA, long long MB, long long row0,
-                                                        long long rows) {
+                                                        long long rows, int accumulate) {
   constexpr int BM = 64, BN = 64, BK = 16;
   __shared__ C As[BK][BM];
   __shared__ C Bs[BK][BN];
@@ -191,7 +203,14 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(const C* __restrict__ A,
 #pragma unroll
     for (int y = 0; y < 4; ++y) {
       long long j = j0 + tc + 16 * y;
-      if (j < MB) out[(i - row0) * MB + j] = acc[x][y];
+      if (j < MB) {
+        C r = acc[x][y];
+        if (accumulate) {
+          r.x += out[(i - row0) * MB + j].x;
+          r.y += out[(i - row0) * MB + j].y;
+        }
+        out[(i - row0) * MB + j] = r;
+      }
     }
   }
 }

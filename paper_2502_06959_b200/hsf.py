@@ -41,7 +41,9 @@ class _Info(C.Structure):
                 ("support_b", C.POINTER(C.c_int32)), ("sigma_offsets", C.POINTER(C.c_int64)),
                 ("sigmas", C.POINTER(C.c_double)), ("levels_a", C.c_int32), ("levels_b", C.c_int32),
                 ("passes_a", C.c_int32), ("passes_b", C.c_int32), ("ops_a", C.c_int32), ("ops_b", C.c_int32),
-                ("plan_hash", C.c_uint64), ("fold_units", C.c_int32)]
+                ("plan_hash", C.c_uint64), ("fold_units", C.c_int32),
+                ("n_joint_blocks", C.c_int32), ("tree_bytes_a", C.c_double), ("tree_bytes_b", C.c_double),
+                ("fold_tree_bytes_a", C.c_double), ("fold_tree_bytes_b", C.c_double)]
 
 
 class _RunArgs(C.Structure):
@@ -49,7 +51,7 @@ class _RunArgs(C.Structure):
                 ("out", C.c_void_p), ("out_on_device", C.c_int32), ("path_begin", C.c_uint64),
                 ("path_end", C.c_uint64), ("row_begin", C.c_uint64), ("row_end", C.c_uint64),
                 ("cuda_stream", C.c_void_p), ("precision", C.c_int), ("device", C.c_int32),
-                ("phase_ms", C.POINTER(C.c_double))]
+                ("phase_ms", C.POINTER(C.c_double)), ("accumulate", C.c_int32)]
 
 
 _lib = None
@@ -102,7 +104,8 @@ def version() -> str:
 
 class Plan:
     """hsf_plan(): host-side joint-cut plan.  `blocks` is a list of
-    gate-index lists; `individual=True` cuts every crossing gate alone."""
+    gate-index lists, or "auto" (automatic cascades of commuting diagonal
+    crossing gates); `individual=True` cuts every crossing gate alone."""
 
     def __init__(self, circuit_text: str, n_low: int, blocks=None, dtype: str = "c64", individual: bool = False,
                  svd_rel_tol: float = 1e-12, tile_qubits: int = 0, fuse_gates: bool = True,
@@ -121,14 +124,17 @@ class Plan:
         o.jit = int(jit)
         o.log2_path_budget = log2_path_budget
         o.max_dense_block_qubits = max_dense_block_qubits
-        blocks = blocks or []
+        auto = isinstance(blocks, str)
+        if auto and blocks != "auto":
+            raise ValueError("blocks must be a list of gate-index lists or 'auto'")
+        blocks = [] if auto else (blocks or [])
         offs = np.zeros(len(blocks) + 1, dtype=np.int64)
         for i, b in enumerate(blocks):
             offs[i + 1] = offs[i] + len(b)
         ids = np.array([g for b in blocks for g in b] or [0], dtype=np.int64)
         txt = circuit_text.encode()
         h = C.c_void_p()
-        _check(L.hsf_plan(txt, len(txt), n_low, len(blocks), offs.ctypes.data_as(C.POINTER(C.c_int64)),
+        _check(L.hsf_plan(txt, len(txt), n_low, -1 if auto else len(blocks), offs.ctypes.data_as(C.POINTER(C.c_int64)),
                           ids.ctypes.data_as(C.POINTER(C.c_int64)), C.byref(o), C.byref(h)))
         self._h = h
         self.dtype = dtype
@@ -147,6 +153,10 @@ class Plan:
         self.ops = (i.ops_a, i.ops_b)
         self.plan_hash = int(i.plan_hash)
         self.fold_units = int(i.fold_units)
+        self.n_joint_blocks = int(i.n_joint_blocks)
+        self.n_units = int(i.n_units)
+        self.tree_bytes = (float(i.tree_bytes_a), float(i.tree_bytes_b))
+        self.fold_tree_bytes = (float(i.fold_tree_bytes_a), float(i.fold_tree_bytes_b))
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -156,7 +166,7 @@ class Plan:
 
     # -------------------------------------------------------------- run
     def _args(self, out_ptr, out_dev, bits_ptr, n_bits, bits_dev, path_range, row_range, precision, stream, device,
-              phase):
+              phase, accumulate=False):
         a = _RunArgs()
         a.bitstrings = bits_ptr
         a.n_bitstrings = n_bits
@@ -169,10 +179,11 @@ class Plan:
         a.precision = PREC[precision]
         a.device = device
         a.phase_ms = phase
+        a.accumulate = int(accumulate)
         return a
 
     def run(self, out, bitstrings=None, path_range=None, row_range=None, precision: str = "auto", stream=None,
-            timings: bool = False):
+            timings: bool = False, accumulate: bool = False):
         """hsf_run(): evaluate paths [path_range) into `out`.
 
         `out` / `bitstrings` are torch tensors (device or host) or numpy arrays
@@ -193,7 +204,7 @@ class Plan:
         st = stream if stream is not None else (torch.cuda.current_stream().cuda_stream if torch.cuda.is_available() else None)
         phase = (C.c_double * 5)() if timings else None
         a = self._args(op, odev, bp, nb, bdev, path_range, row_range, precision, st, dev,
-                       C.cast(phase, C.POINTER(C.c_double)) if timings else None)
+                       C.cast(phase, C.POINTER(C.c_double)) if timings else None, accumulate)
         _check(lib().hsf_run(self._h, C.byref(a)))
         return list(phase) if timings else None
 

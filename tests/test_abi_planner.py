@@ -168,3 +168,21 @@ def test_trailing_fold_detection(hsf):
     # units still fold; an H on qubit 3 (after every unit) blocks all folding
     assert Plan(txt + "h 2\n", 2, []).fold_units == 2
     assert Plan(txt + "h 3\n", 2, []).fold_units == 0
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_auto_blocks_match_oracle_finder(hsf, seed):
+    # the C++ cascade finder (hsf_plan n_blocks = -1) and the oracle's
+    # networkx-based finder agree on the number of units and paths
+    from hsf_inputs.circuits import make_sbm_qaoa
+    from oracle import hsf_oracle as O
+    from paper_2502_06959_b200 import Plan
+    sizes = [(6, 6), (7, 8), (15, 15), (16, 17)][seed % 4]
+    inst = make_sbm_qaoa(seed=200 + seed, sizes=sizes, p_inter=0.1 + 0.02 * (seed % 4))
+    n, g = O.parse_circuit(inst.text)
+    blocks, ncasc = O.find_cascades(g, inst.n_low)
+    Po = O.plan(n, g, inst.n_low, blocks)
+    P = Plan(inst.text, inst.n_low, "auto", log2_path_budget=40)
+    assert P.n_units == len(Po.units) == ncasc
+    assert P.n_paths == Po.n_paths
+    assert P.n_joint_blocks == len(blocks)

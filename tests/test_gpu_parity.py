@@ -383,3 +383,73 @@ def test_interpreter_kernel_twins(torch, name):
         for jit in (False, True):
             got, _ = gpu_bits(torch, inst, bits, path_range=(0, 8), jit=jit, tile_qubits=11)
             check(got, ref, "c64")
+
+
+@pytest.mark.parametrize("mode", ["bits", "simt", "bf16x3"])
+def test_accumulate_path_chunks(torch, mode):
+    # hsf_run(accumulate=1) adds into out: four path-range chunks accumulated
+    # in place equal the single run (the TMA reduce-add epilogue for bf16x3)
+    from paper_2502_06959_b200 import Plan
+    inst = make_config("c5", twin=True)
+    P = Plan(inst.text, inst.n_low, inst.blocks)
+    n, g = O.parse_circuit(inst.text)
+    psi = O.schrodinger(n, g)
+    if mode == "bits":
+        bits = torch.from_numpy(inst.bitstrings.view(np.int64)).cuda()
+        ref = psi[inst.bitstrings.astype(np.int64)]
+        out = torch.zeros(len(inst.bitstrings), dtype=torch.complex64, device="cuda")
+        kw = dict(bitstrings=bits)
+    else:
+        ref = psi
+        out = torch.zeros(1 << n, dtype=torch.complex64, device="cuda")
+        kw = dict(precision=mode)
+    for r in range(4):
+        P.run(out, path_range=(P.n_paths * r // 4, P.n_paths * (r + 1) // 4), accumulate=True, **kw)
+    torch.cuda.synchronize()
+    check(out.cpu().numpy(), ref, "c64")
+    # accumulate again: exactly twice the result
+    for r in range(4):
+        P.run(out, path_range=(P.n_paths * r // 4, P.n_paths * (r + 1) // 4), accumulate=True, **kw)
+    torch.cuda.synchronize()
+    check(out.cpu().numpy() / 2, ref, "c64")
+
+
+# ------------------------------------------ Table II-shaped QAOA (NEXT row 1)
+def _oracle_blocks(inst, g):
+    return O.find_cascades(g, inst.n_low)[0] if inst.blocks == "auto" else inst.blocks
+
+
+@pytest.mark.parametrize("name", ["q30-1", "q31-2", "q33-3"])
+def test_table2_twins_auto_blocks(torch, name):
+    # automatic cascades (C++ finder) on oracle-sized members of the family
+    inst = make_config(name, twin=True)
+    n, g = O.parse_circuit(inst.text)
+    ref = O.schrodinger(n, g)
+    got, P = gpu_full(torch, inst)
+    assert P.n_joint_blocks >= 1
+    check(got, ref, "c64")
+    assert P.n_paths == O.plan(n, g, inst.n_low, _oracle_blocks(inst, g)).n_paths
+
+
+def test_table2_q30_prefix_full_paths(torch):
+    # q30-1 at full size (15|15, 2^15 halves), the paper's output: the first
+    # 10^6 amplitudes, all joint-cut paths; the oracle sums the same paths
+    # with its own cascade grouping (amplitudes are unique)
+    inst = make_config("q30-1")
+    n, g = O.parse_circuit(inst.text)
+    OP = O.plan(n, g, inst.n_low, _oracle_blocks(inst, g))
+    rows = -(-inst.meta["prefix"] // (1 << inst.n_low))
+    A, B, c = O.half_states(OP)
+    ref = O.recombine_full(A[:rows], B, c)
+    got, P = gpu_full(torch, inst, row_range=(0, rows))
+    assert P.n_paths == OP.n_paths
+    check(got, ref, "c64")
+    # standard HSF (individual cuts) on the GPU gives the same prefix
+    from paper_2502_06959_b200 import Plan
+    Pi = Plan(inst.text, inst.n_low, None, individual=True, log2_path_budget=40)
+    out = torch.zeros(rows << inst.n_low, dtype=torch.complex64, device="cuda")
+    ch = 1 << 14
+    for p0 in range(0, Pi.n_paths, ch):
+        Pi.run(out, path_range=(p0, min(Pi.n_paths, p0 + ch)), row_range=(0, rows), accumulate=True)
+    torch.cuda.synchronize()
+    check(out.cpu().numpy(), ref, "c64")

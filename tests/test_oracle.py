@@ -344,3 +344,79 @@ def test_sbm_qaoa_blocks_are_rank2_cascades():
         assert u.rank == 2
     assert abs(np.linalg.norm(O.hsf(n, g, inst.n_low, inst.blocks)) - 1) < 1e-12
     assert np.abs(O.hsf(n, g, inst.n_low, inst.blocks) - O.schrodinger(n, g)).max() < 1e-13
+
+
+# ------------------------------------------------- commutation + block finder
+def test_interleaved_commuting_block_is_convex():
+    # RZZ(1,2) and RZZ(1,3) share qubit 1 with RZZ(0,1) between them: all are
+    # diagonal, so the block {g0, g2} is convex after commuting
+    txt = ("qubits 4\nh 0\nh 1\nh 2\nh 3\n" + f"rzz {0.3.hex()} 1 2\nrzz {0.5.hex()} 0 1\nrzz {0.7.hex()} 1 3\n"
+           + "rx 0.4 0\nrx 0.4 1\nrx 0.4 2\nrx 0.4 3\n").replace("rx 0.4", "rx " + 0.4.hex())
+    n, g = _circ(txt)
+    P = O.plan(n, g, 2, [[4, 6]])
+    assert [u.rank for u in P.units] == [2]  # the cascade centred on qubit 1
+    assert np.abs(O.hsf(n, g, 2, [[4, 6]]) - O.schrodinger(n, g)).max() < 1e-14
+    # a non-diagonal gate on the shared qubit between them breaks convexity
+    n2, g2 = _circ(txt.replace(f"rzz {0.5.hex()} 0 1", "h 1"))
+    with pytest.raises(O.NonConvexBlock):
+        O.plan(n2, g2, 2, [[4, 6]])
+
+
+def _brute_min_cover(edge_list):
+    verts = sorted({v for e in edge_list for v in e})
+    for k in range(len(verts) + 1):
+        import itertools
+        for cov in itertools.combinations(verts, k):
+            c = set(cov)
+            if all(a in c or b in c for a, b in edge_list):
+                return k
+    return len(verts)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_find_cascades_minimum_cover_bruteforce(seed):
+    # the finder's cascade count is a minimum vertex cover (Koenig), checked
+    # by exhaustive search on small random crossing graphs; the planned joint
+    # HSF with its blocks reproduces the Schroedinger state
+    rng = np.random.default_rng([seed, 11])
+    nb, na = 4, 4
+    lines = [f"qubits {nb + na}"] + [f"h {q}" for q in range(nb + na)]
+    edges = set()
+    for _ in range(int(rng.integers(3, 10))):
+        b, a = int(rng.integers(nb)), int(nb + rng.integers(na))
+        edges.add((b, a))
+        lines.append(f"rzz {float(rng.uniform(0, 3)).hex()} {b} {a}")
+    lines += [f"rx {0.3.hex()} {q}" for q in range(nb + na)]
+    n, g = _circ("\n".join(lines) + "\n")
+    blocks, ncasc = O.find_cascades(g, nb)
+    assert ncasc == _brute_min_cover(sorted(edges))
+    P = O.plan(n, g, nb, blocks)
+    assert all(u.rank <= 2 for u in P.units)
+    assert P.n_paths == 2 ** ncasc
+    assert np.abs(O.hsf(n, g, nb, blocks) - O.schrodinger(n, g)).max() < 1e-13
+
+
+@pytest.mark.parametrize("row", _table2(), ids=lambda r: r[0])
+def test_table2_counts_from_block_finder(row):
+    # Table I/II structure (blocks + separate RZZ cuts) rebuilt as a circuit
+    # with the gates in file order scattered: the automatic finder recovers
+    # n_p^j = 2^(blocks + sep)
+    name, lt, lj, blocks, sep, sepc = row
+    in_blocks = sepc - sep
+    sizes = [in_blocks // blocks + (1 if i < in_blocks % blocks else 0) for i in range(blocks)]
+    nb = 40
+    gl, t = [], 0
+    for i, sz in enumerate(sizes):
+        for _ in range(sz):
+            gl.append((t, nb + i))
+            t += 1
+    for j in range(sep):
+        gl.append((t, nb + blocks + j))
+        t += 1
+    rng = np.random.default_rng(len(gl))
+    rng.shuffle(gl)
+    lines = [f"qubits {nb + blocks + sep}"] + [f"rzz {0.37.hex()} {b} {a}" for b, a in gl]
+    n, g = _circ("\n".join(lines) + "\n")
+    found, ncasc = O.find_cascades(g, nb)
+    assert ncasc == lj
+    assert len(found) == blocks
