@@ -30,6 +30,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+
 #include "hsf_internal.h"
 
 namespace hsf {
@@ -333,6 +335,236 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
 }
 
+// ------------------------------------------------- K5, CTA-pair (cta_group::2)
+// Two CTAs of a cluster (one TPC) cooperate on a 256 x 256 output tile: each
+// holds its own 128 A rows and HALF of the tile's B rows (128 of 256) in
+// shared memory; the leader CTA (rank 0) issues tcgen05.mma.cta_group::2
+// with M = 256, N = 256, which reads A from each CTA's SMEM and the B halves
+// from both, and accumulates each CTA's 128 rows x 256 columns into that
+// CTA's TMEM.  Per SM this halves the B operand traffic (TMA into SMEM and
+// MMA reads out of it): single-CTA x3 needs ~160 B/clk of SMEM bandwidth per
+// SM at full tensor rate (ncu: tensor pipe 77 % active), the pair ~104 B/clk.
+// Protocol (CUTLASS sm100 2SM conventions): every CTA's TMA loads signal the
+// LEADER's full barrier (shared::cluster address with the peer bit cleared,
+// .cta_group::2); only the leader arms it with both CTAs' bytes; MMA commits
+// multicast to both CTAs' empty / accumulator-full barriers; every epilogue
+// thread of both CTAs arrives on the leader's accumulator-empty barrier.
+constexpr int B2_TILE = (BN / 2) * BK * 2;               // 16 KB: this CTA's half of B
+constexpr int STAGE2_BYTES = 2 * A_TILE + 2 * B2_TILE;   // 64 KB
+constexpr int STAGES2 = 3;
+constexpr int SMEM2_BYTES = STAGES2 * STAGE2_BYTES + EPI_BYTES + 1024;
+constexpr uint32_t IDESC2 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                            ((uint32_t)((2 * BM) >> 4) << 24);
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // shared::cluster address -> the pair's rank-0 CTA
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2sm(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                             uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar) & kPeerMask), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void mma2_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(IDESC2), "r"(accum));
+}
+__device__ __forceinline__ void mma2_commit_both(uint64_t* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .b16 m;\n"
+      "mov.b16 m, 3;\n"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n"
+      "}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & kPeerMask)
+               : "memory");
+}
+
+// p.num_m counts 256-row PAIR tiles here
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    tc_gemm2_kernel(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUtensorMap mA_lo,
+                    const __grid_constant__ CUtensorMap mB_hi, const __grid_constant__ CUtensorMap mB_lo,
+                    const __grid_constant__ CUtensorMap mOut, const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[STAGES2], empty_bar[STAGES2], tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_base_sh;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int num_tiles = p.num_m * p.num_n;
+  const uint32_t rank = cluster_rank();
+  const int pair = blockIdx.x >> 1, num_pairs = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES2; ++s) {
+      mbar_init(&full_bar[s], 1);   // the leader's producer arms it (both CTAs' bytes)
+      mbar_init(&empty_bar[s], 1);  // one multicast commit per stage use
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 2 * 32 * EPI_WARPS);  // epilogue threads of both CTAs
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mA_hi) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mB_hi) : "memory");
+  }
+  if (warp == 1) {  // same logical warp in both CTAs
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync_all();  // peer barriers initialised before any remote arrive / complete_tx
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem_base = tmem_base_sh;
+  const uint32_t stage_bytes = p.x3 ? (uint32_t)STAGE2_BYTES : (uint32_t)(A_TILE + B2_TILE);
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (both CTAs)
+    if (lane == 0) {
+      const uint64_t a_pol = p.a_evict_last ? policy_evict_last() : policy_evict_normal();
+      const uint64_t b_pol = policy_evict_normal();
+      int s = 0;
+      uint32_t ph = 0;
+      for (int tile = pair; tile < num_tiles; tile += num_pairs) {
+        int mb, nb;
+        tile_coords(p, tile, mb, nb);
+        const int arow = (2 * mb + (int)rank) * BM, brow = nb * BN + (int)rank * (BN / 2);
+        for (int kb = 0; kb < p.num_k; ++kb) {
+          mbar_wait(&empty_bar[s], ph ^ 1);
+          uint8_t* st = smem + s * STAGE2_BYTES;
+          if (rank == 0) mbar_expect_tx(&full_bar[s], 2 * stage_bytes);
+          tma_load_2sm(st, &mA_hi, &full_bar[s], kb * BK, arow, a_pol);
+          tma_load_2sm(st + 2 * A_TILE, &mB_hi, &full_bar[s], kb * BK, brow, b_pol);
+          if (p.x3) {
+            tma_load_2sm(st + A_TILE, &mA_lo, &full_bar[s], kb * BK, arow, a_pol);
+            tma_load_2sm(st + 2 * A_TILE + B2_TILE, &mB_lo, &full_bar[s], kb * BK, brow, b_pol);
+          }
+          if (++s == STAGES2) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader only)
+    if (lane == 0 && rank == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t aph = 0;
+      for (int tile = pair; tile < num_tiles; tile += num_pairs) {
+        mbar_wait(&tempty_bar[acc], aph ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t d = tmem_base + (uint32_t)(acc * BN);
+        for (int kb = 0; kb < p.num_k; ++kb) {
+          mbar_wait(&full_bar[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t st = smem_u32(smem + s * STAGE2_BYTES);
+          const uint32_t a_hi = st, a_lo = st + A_TILE, b_hi = st + 2 * A_TILE, b_lo = st + 2 * A_TILE + B2_TILE;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint32_t ko = k * 32;
+            mma2_bf16(d, sw128_desc(a_hi + ko), sw128_desc(b_hi + ko), (kb | k) ? 1u : 0u);
+            if (p.x3) {
+              mma2_bf16(d, sw128_desc(a_hi + ko), sw128_desc(b_lo + ko), 1u);
+              mma2_bf16(d, sw128_desc(a_lo + ko), sw128_desc(b_hi + ko), 1u);
+            }
+          }
+          mma2_commit_both(&empty_bar[s]);  // both CTAs' stage s free once these retire
+          if (++s == STAGES2) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        mma2_commit_both(&tfull_bar[acc]);  // both CTAs' accumulators ready
+        if (++acc == 2) {
+          acc = 0;
+          aph ^= 1;
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const uint64_t st_pol = policy_evict_first();
+    const int q = warp & 3;
+    const int half = (warp - 2) / 4;
+    uint8_t* stg = smem + STAGES2 * STAGE2_BYTES + (warp - 2) * 4096;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int tile = pair; tile < num_tiles; tile += num_pairs) {
+      int mb, nb;
+      tile_coords(p, tile, mb, nb);
+      const int row0 = (2 * mb + (int)rank) * BM;
+      mbar_wait(&tfull_bar[acc], aph);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll 1
+      for (int c = half; c < BN / 32; c += 2) {
+        uint32_t v[32];
+        const uint32_t taddr = tmem_base + (uint32_t)(acc * BN + c * 32) + ((uint32_t)(q * 32) << 16);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
+              "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+              "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (c >= BN / 32 - 2) {
+          asm volatile("tcgen05.fence::before_thread_sync;");
+          mbar_arrive_leader(&tempty_bar[acc]);
+        }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+        float4* dst = reinterpret_cast<float4*>(stg + lane * 128);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          dst[j ^ (lane & 7)] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                            __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          if (p.accumulate)
+            tma_reduce_add_2d(&mOut, stg, nb * BN + c * 32, row0 + q * 32, st_pol);
+          else
+            tma_store_2d(&mOut, stg, nb * BN + c * 32, row0 + q * 32, st_pol);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      }
+      if (++acc == 2) {
+        acc = 0;
+        aph ^= 1;
+      }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync_all();  // the peer is done with the leader's barriers and the MMAs with both SMEMs
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+}
+
 // ----------------------------------------------------------------------- K4
 __device__ __forceinline__ void split_bf16(float x, __nv_bfloat16& hi, __nv_bfloat16& lo) {
   hi = __float2bfloat16_rn(x);
@@ -549,10 +781,28 @@ inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row
     if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("tc smem attr: ") + cudaGetErrorString(e));
     attr = true;
   }
-  const long long tiles = (long long)p.num_m * p.num_n;
-  const int grid = (int)std::min<long long>(tiles, num_sms());
   CUtensorMap mO = make_out_map((float*)out, rows, 2 * MB);
-  tc::tc_gemm_kernel<<<grid, tc::THREADS, tc::SMEM_BYTES, st>>>(mAh, mAl, mBh, mBl, mO, p);
+  const char* pair_env = std::getenv("HSF_TC_PAIR");
+  const bool pair = rows > tc::BM && !(pair_env && pair_env[0] == '0');
+  if (pair) {
+    // CTA pairs: 256-row M tiles, each CTA loads half of every B tile
+    static bool attr2 = false;
+    if (!attr2) {
+      e = cudaFuncSetAttribute(tc::tc_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM2_BYTES);
+      if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("tc2 smem attr: ") + cudaGetErrorString(e));
+      attr2 = true;
+    }
+    CUtensorMap mBh2 = make_map(t.b_hi, t.d.nrows_b_pad, kcols, tc::BN / 2);
+    CUtensorMap mBl2 = x3 ? make_map(t.b_lo, t.d.nrows_b_pad, kcols, tc::BN / 2) : mBh2;
+    p.num_m = (int)((rows + 2 * tc::BM - 1) / (2 * tc::BM));
+    const long long tiles = (long long)p.num_m * p.num_n;
+    const int grid = 2 * (int)std::min<long long>(tiles, num_sms() / 2);
+    tc::tc_gemm2_kernel<<<grid, tc::THREADS, tc::SMEM2_BYTES, st>>>(mAh, mAl, mBh2, mBl2, mO, p);
+  } else {
+    const long long tiles = (long long)p.num_m * p.num_n;
+    const int grid = (int)std::min<long long>(tiles, num_sms());
+    tc::tc_gemm_kernel<<<grid, tc::THREADS, tc::SMEM_BYTES, st>>>(mAh, mAl, mBh, mBl, mO, p);
+  }
   e = cudaGetLastError();
   if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("tc_gemm: ") + cudaGetErrorString(e));
 }

@@ -15,6 +15,7 @@ struct JitLaunchArgs {
   void* dst;
   const void* coef;
   long long node_first, node_local0, src_first, src_div;
+  unsigned tile0;
 };
 
 // CUDA source of the kernel "hsf_jit_pass" specialised to one tile pass.

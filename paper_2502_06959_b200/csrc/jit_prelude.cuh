@@ -19,6 +19,7 @@ struct JitArgs {
   long long node_local0; // local output-node index of blockIdx.y == 0
   long long src_first;   // global index of the first node of the input level
   long long src_div;     // parent = node_global / src_div
+  unsigned tile0;        // tile index of blockIdx.x == 0 (row-restricted leaf passes)
 };
 
 __device__ __forceinline__ int sw(int e) { return e ^ ((e >> 4) & 15); }

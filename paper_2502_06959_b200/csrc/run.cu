@@ -347,7 +347,23 @@ static void run_half(const Plan& P, DeviceState* d, int h, const Layout& L, cuda
       smem = ((smem + 15) & ~(size_t)15) + (size_t)n_ops * (sizeof(DevOp) + sizeof(void*));
       smem = ((smem + 15) & ~(size_t)15) + (size_t)ps.tbl_elems * sizeof(C);
       pp.tbl_elems = (int)ps.tbl_elems;
-      const uint64_t tiles = 1ull << (H.m - ps.t);
+      uint64_t tiles = 1ull << (H.m - ps.t);
+      pp.tile0 = 0;
+      // Row-restricted leaf pass: in full-output runs only rows [r0, r1) of
+      // half A's leaves reach the path-sum, so the last pass of A's tree
+      // computes only the tiles holding them (ops of a pass stay inside its
+      // tile; tile index = the rows' non-tile bits, monotone in the row)
+      if (h == 0 && !L.bits_mode && last && pi + 1 == tr.passes.size() && ps.t < H.m &&
+          (L.r1 - L.r0) < (1ull << H.m)) {
+        auto tile_of = [&](uint64_t i) {
+          uint64_t tt = 0;
+          for (int j = 0; j < pp.n_nt; ++j) tt |= ((i >> pp.nonT[j]) & 1ull) << j;
+          return tt;
+        };
+        const uint64_t t0 = tile_of(L.r0), t1 = tile_of(L.r1 - 1);
+        pp.tile0 = (unsigned)t0;
+        tiles = t1 - t0 + 1;
+      }
       // narrow levels (few CTAs) use one 1024-thread CTA per (node, tile) to
       // shorten the dependent chain of small launches at the top of the tree
       const bool wide = tiles * n_out < 2ull * (uint64_t)num_sms() && ps.t >= 11;
@@ -374,7 +390,8 @@ static void run_half(const Plan& P, DeviceState* d, int h, const Layout& L, cuda
           pp.src_div = 1;
         }
         if (jf) {
-          JitLaunchArgs ja{pp.src, pp.dst, pp.coef, pp.node_first, pp.node_local0, pp.src_first, pp.src_div};
+          JitLaunchArgs ja{pp.src, pp.dst, pp.coef, pp.node_first, pp.node_local0, pp.src_first, pp.src_div,
+                           pp.tile0};
           jit_launch((*jf)[pass_ord], (unsigned)tiles, (unsigned)ny, jit_smem_bytes(ps, sizeof(R) == 4), st, ja);
         } else {
           dim3 grid((unsigned)tiles, (unsigned)ny);

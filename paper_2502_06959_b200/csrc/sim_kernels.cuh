@@ -100,6 +100,7 @@ struct PassParams {
   int nonT[kMaxNonTile];   // half qubits outside the tile, ascending
   long long state_elems;   // 2^m
   long long node_first;    // global index (at the output level) of blockIdx.y == 0
+  unsigned tile0;          // tile index of blockIdx.x == 0 (row-restricted leaf passes)
   long long node_local0;   // local output-node index of blockIdx.y == 0
   long long src_first;     // global index of the first node of the input level
   long long src_div;       // parent = node_global / src_div
@@ -346,7 +347,7 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? (HEAVY ? 2 : 4) : 1)) hsf_pas
   off = (off + 15) & ~(size_t)15;
   C* stab = reinterpret_cast<C*>(smem_raw + off);  // staged diagonal tables
 
-  const uint32_t tile = blockIdx.x;
+  const uint32_t tile = blockIdx.x + p.tile0;
   const long long node_local = p.node_local0 + blockIdx.y;
   const long long node_g = p.node_first + blockIdx.y;
   const int nel = 1 << p.t;
