@@ -94,6 +94,9 @@ typedef struct {
                                     specialised to its op list (generated CUDA, NVRTC for
                                     sm_100a, compiled at the first hsf_run on a device and
                                     cached per process); 0 => generic interpreter kernel */
+  int32_t graphs;                /* 1 (default) => runs with device buffers are captured once
+                                    into a CUDA graph (both streams, all launches) and replayed
+                                    while pointers, ranges and precision stay the same */
 } hsf_plan_opts;
 
 typedef struct hsf_plan_s hsf_plan_t; /* opaque */

@@ -46,6 +46,13 @@ struct DeviceState {
   uint64_t cp_p0 = ~0ull, cp_p1 = ~0ull;
   int cp_units = -1;
   cudaEvent_t ev[6] = {};
+  cudaEvent_t ev_t0 = nullptr;              // timing start (ev[0] is the fork event)
+  // CUDA graph of the whole run (both streams), replayed while the run's
+  // arguments (pointers, ranges, precision) stay the same
+  cudaStream_t cap = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  std::vector<uint64_t> gkey;
+  bool capturing = false;
   cudaEvent_t evg[2] = {}, evc[2] = {};  // host-output chunks: GEMM done / D2H done
   cudaStream_t side = nullptr;  // half-B stream; D2H stream of host-output chunks
   bool sticky = false;
@@ -67,6 +74,9 @@ void destroy_device(Plan* p) {
   cudaFree(d->cp);
   for (auto& e : d->ev)
     if (e) cudaEventDestroy(e);
+  if (d->ev_t0) cudaEventDestroy(d->ev_t0);
+  if (d->gexec) cudaGraphExecDestroy(d->gexec);
+  if (d->cap) cudaStreamDestroy(d->cap);
   for (int i = 0; i < 2; ++i) {
     if (d->evg[i]) cudaEventDestroy(d->evg[i]);
     if (d->evc[i]) cudaEventDestroy(d->evc[i]);
@@ -140,6 +150,8 @@ static DeviceState* ensure_device(Plan* P, int device) {
     d->jit = true;
   }
   for (auto& e : d->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDefault));
+  CK(cudaEventCreateWithFlags(&d->ev_t0, cudaEventDefault));
+  CK(cudaStreamCreateWithFlags(&d->cap, cudaStreamNonBlocking));
   for (int i = 0; i < 2; ++i) {
     CK(cudaEventCreateWithFlags(&d->evg[i], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&d->evc[i], cudaEventDisableTiming));
@@ -494,19 +506,24 @@ static void run_core_full(Plan* P, DeviceState* d, const Layout& L, cudaStream_t
 template <typename R>
 static void run_all(Plan* P, DeviceState* d, const Layout& L, const hsf_run_args& a, cudaStream_t st, bool timed) {
   using C = typename cplx<R>::T;
+  // timing events become graph nodes when the run is being captured
+  auto rec = [&](cudaEvent_t e, cudaStream_t s) {
+    CK(cudaEventRecordWithFlags(e, s, d->capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+  };
+  if (timed) rec(d->ev_t0, st);
   // half B (and its operand prep) on the side stream, half A on the caller's
   // stream; the two path trees are independent until the path-sum
   CK(cudaEventRecord(d->ev[0], st));
   CK(cudaStreamWaitEvent(d->side, d->ev[0], 0));
   run_half<R>(*P, d, 1, L, d->side);
-  if (timed) CK(cudaEventRecord(d->ev[2], d->side));
+  if (timed) rec(d->ev[2], d->side);
   prep_half<R>(P, d, L, 1, d->side);
   CK(cudaEventRecord(d->ev[5], d->side));
   run_half<R>(*P, d, 0, L, st);
-  if (timed) CK(cudaEventRecord(d->ev[1], st));
+  if (timed) rec(d->ev[1], st);
   prep_half<R>(P, d, L, 0, st);
   CK(cudaStreamWaitEvent(st, d->ev[5], 0));
-  if (timed) CK(cudaEventRecord(d->ev[3], st));
+  if (timed) rec(d->ev[3], st);
   char* ws = (char*)d->ws;
   if (L.bits_mode) {
     C* out = a.out_on_device ? (C*)a.out : (C*)(ws + L.off_out);
@@ -532,7 +549,7 @@ static void run_all(Plan* P, DeviceState* d, const Layout& L, const hsf_run_args
     }
     for (int i = 0; i < std::min(c, 2); ++i) CK(cudaStreamWaitEvent(st, d->evc[i], 0));
   }
-  if (timed) CK(cudaEventRecord(d->ev[4], st));
+  if (timed) rec(d->ev[4], st);
 }
 
 static void run(Plan* P, const hsf_run_args& a) {
@@ -545,18 +562,53 @@ static void run(Plan* P, const hsf_run_args& a) {
   ensure_cp(P, d, L.p0, L.p1, L.U_tree, st);
   const bool timed = a.phase_ms != nullptr;
   try {
-    if (P->opts.dtype == HSF_C64)
+    const char* ng = std::getenv("HSF_NO_GRAPH");
+    const bool graph = P->opts.graphs && a.out_on_device && (!L.bits_mode || a.bits_on_device) && !(ng && ng[0] == '1');
+    if (graph) {
+      // the key holds everything the captured launches depend on
+      std::vector<uint64_t> key = {(uint64_t)(uintptr_t)a.out, (uint64_t)(uintptr_t)a.bitstrings, a.n_bitstrings,
+                                   L.p0, L.p1, L.r0, L.r1, (uint64_t)L.prec, (uint64_t)a.accumulate,
+                                   (uint64_t)timed, (uint64_t)L.fold, (uint64_t)(uintptr_t)d->ws,
+                                   (uint64_t)(uintptr_t)d->cp, (uint64_t)L.total};
+      if (!d->gexec || key != d->gkey) {
+        if (d->gexec) CK(cudaGraphExecDestroy(d->gexec));
+        d->gexec = nullptr;
+        d->gkey.clear();
+        cudaGraph_t g = nullptr;
+        CK(cudaStreamBeginCapture(d->cap, cudaStreamCaptureModeThreadLocal));
+        d->capturing = true;
+        try {
+          if (P->opts.dtype == HSF_C64)
+            run_all<float>(P, d, L, a, d->cap, timed);
+          else
+            run_all<double>(P, d, L, a, d->cap, timed);
+        } catch (...) {
+          d->capturing = false;
+          cudaStreamEndCapture(d->cap, &g);
+          if (g) cudaGraphDestroy(g);
+          throw;
+        }
+        d->capturing = false;
+        CK(cudaStreamEndCapture(d->cap, &g));
+        cudaError_t e = cudaGraphInstantiate(&d->gexec, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
+        d->gkey = key;
+      }
+      CK(cudaGraphLaunch(d->gexec, st));
+    } else if (P->opts.dtype == HSF_C64) {
       run_all<float>(P, d, L, a, st, timed);
-    else
+    } else {
       run_all<double>(P, d, L, a, st, timed);
+    }
     if (timed || !a.out_on_device) CK(cudaStreamSynchronize(st));
     if (timed) {
       float tA, tB, tprep, tcore, ttot;
-      CK(cudaEventElapsedTime(&tA, d->ev[0], d->ev[1]));
-      CK(cudaEventElapsedTime(&tB, d->ev[0], d->ev[2]));
-      CK(cudaEventElapsedTime(&tprep, d->ev[0], d->ev[3]));
+      CK(cudaEventElapsedTime(&tA, d->ev_t0, d->ev[1]));
+      CK(cudaEventElapsedTime(&tB, d->ev_t0, d->ev[2]));
+      CK(cudaEventElapsedTime(&tprep, d->ev_t0, d->ev[3]));
       CK(cudaEventElapsedTime(&tcore, d->ev[3], d->ev[4]));
-      CK(cudaEventElapsedTime(&ttot, d->ev[0], d->ev[4]));
+      CK(cudaEventElapsedTime(&ttot, d->ev_t0, d->ev[4]));
       a.phase_ms[0] = tA;
       a.phase_ms[1] = tB;
       a.phase_ms[2] = tprep - std::max(tA, tB);
@@ -605,6 +657,7 @@ hsf_status hsf_plan_opts_default(hsf_plan_opts* o) {
   o->hoist_gates = 1;
   o->fold_trailing_diag = 1;
   o->jit = 1;
+  o->graphs = 1;
   return HSF_OK;
 }
 

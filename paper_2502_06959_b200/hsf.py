@@ -31,7 +31,7 @@ class _Opts(C.Structure):
     _fields_ = [("dtype", C.c_int), ("svd_rel_tol", C.c_double), ("max_dense_block_qubits", C.c_int32),
                 ("log2_path_budget", C.c_double), ("individual", C.c_int32), ("tile_qubits", C.c_int32),
                 ("fuse_gates", C.c_int32), ("hoist_gates", C.c_int32), ("fold_trailing_diag", C.c_int32),
-                ("jit", C.c_int32)]
+                ("jit", C.c_int32), ("graphs", C.c_int32)]
 
 
 class _Info(C.Structure):
@@ -110,7 +110,7 @@ class Plan:
     def __init__(self, circuit_text: str, n_low: int, blocks=None, dtype: str = "c64", individual: bool = False,
                  svd_rel_tol: float = 1e-12, tile_qubits: int = 0, fuse_gates: bool = True,
                  log2_path_budget: float = 26.0, max_dense_block_qubits: int = 10, hoist_gates: bool = True,
-                 fold_trailing_diag: bool = True, jit: bool = True):
+                 fold_trailing_diag: bool = True, jit: bool = True, graphs: bool = True):
         L = lib()
         o = _Opts()
         _check(L.hsf_plan_opts_default(C.byref(o)))
@@ -122,6 +122,7 @@ class Plan:
         o.hoist_gates = int(hoist_gates)
         o.fold_trailing_diag = int(fold_trailing_diag)
         o.jit = int(jit)
+        o.graphs = int(graphs)
         o.log2_path_budget = log2_path_budget
         o.max_dense_block_qubits = max_dense_block_qubits
         auto = isinstance(blocks, str)

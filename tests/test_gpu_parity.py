@@ -470,3 +470,27 @@ def test_row_restricted_leaf_pass(torch, rr):
     part, _ = gpu_full(torch, inst, precision="simt", tile_qubits=11, row_range=rr)
     nb = P.n_b
     assert np.array_equal(part, full[rr[0] << nb:rr[1] << nb])
+
+
+@pytest.mark.parametrize("name", ["c1", "c5"])
+def test_graph_replay_matches_direct(torch, name):
+    # graphs=True captures the run once and replays it; results equal the
+    # directly launched run (graphs=False), bitwise, across replays
+    from paper_2502_06959_b200 import Plan
+    inst = make_config(name, twin=True)
+    outs = []
+    for graphs in (True, False):
+        P = Plan(inst.text, inst.n_low, inst.blocks, dtype=inst.dtype, graphs=graphs)
+        cdt = _cdt(torch, inst.dtype)
+        if inst.bitstrings is None:
+            out, kw = torch.empty(1 << inst.n, dtype=cdt, device="cuda"), {}
+        else:
+            out = torch.empty(len(inst.bitstrings), dtype=cdt, device="cuda")
+            kw = {"bitstrings": torch.from_numpy(inst.bitstrings.view(np.int64)).cuda()}
+        for _ in range(3):
+            out.zero_()
+            ph = P.run(out, timings=True, **kw)
+            torch.cuda.synchronize()
+            assert all(x >= 0 for x in ph) and ph[4] > 0
+            outs.append(out.cpu().numpy().copy())
+    assert all(np.array_equal(outs[0], o) for o in outs[1:])
