@@ -494,3 +494,53 @@ def test_graph_replay_matches_direct(torch, name):
             assert all(x >= 0 for x in ph) and ph[4] > 0
             outs.append(out.cpu().numpy().copy())
     assert all(np.array_equal(outs[0], o) for o in outs[1:])
+
+
+# ------------------------------------------------------------- edge cases
+def test_minimal_two_qubit_bell_across_cut(torch):
+    # n = 2, cut between the qubits: the Bell circuit of the paper's Example 1
+    # has one crossing CNOT (rank 2) -> 2 paths
+    from paper_2502_06959_b200 import Plan
+    txt = "qubits 2\nh 1\ncx 1 0\n"
+    for dtype in ("c64", "c128"):
+        P = Plan(txt, 1, [], dtype=dtype)
+        assert P.n_paths == 2
+        out = torch.empty(4, dtype=_cdt(torch, dtype), device="cuda")
+        P.run(out, precision="simt")
+        torch.cuda.synchronize()
+        np.testing.assert_allclose(out.cpu().numpy(), np.array([1, 0, 0, 1]) / np.sqrt(2), atol=1e-7)
+
+
+def test_single_path_single_row_single_sample(torch):
+    inst = make_config("c5", twin=True)
+    n, g = O.parse_circuit(inst.text)
+    P = O.plan(n, g, inst.n_low, inst.blocks)
+    A, B, c = O.half_states(P, 7, 8)
+    # one path, one bitstring (repeated), extreme indices 0 and 2^n - 1
+    bits = np.array([0, (1 << n) - 1, 5, 5], dtype=np.uint64)
+    ref = O.recombine_bits(A, B, c, bits, inst.n_low)
+    got, _ = gpu_bits(torch, inst, bits, path_range=(7, 8))
+    check(got, ref, "c64")
+    assert got[2] == got[3]  # duplicates allowed, identical
+    full = O.recombine_full(A, B, c)
+    for prec in ("simt", "bf16x3"):
+        got, _ = gpu_full(torch, inst, precision=prec, path_range=(7, 8), row_range=(3, 4))
+        np.testing.assert_allclose(got, full[3 << inst.n_low:4 << inst.n_low], atol=1e-6)
+
+
+def test_empty_and_invalid_requests(torch):
+    from paper_2502_06959_b200 import HsfError, Plan
+    inst = make_config("c1")
+    P = Plan(inst.text, inst.n_low, inst.blocks)
+    out = torch.empty(1 << 12, dtype=torch.complex64, device="cuda")
+    for kw in (dict(path_range=(3, 3)), dict(path_range=(0, 17)), dict(row_range=(0, 65)),
+               dict(row_range=(4, 4))):
+        with pytest.raises(HsfError):
+            P.run(out, **kw)
+    with pytest.raises(HsfError):  # accumulate needs a device buffer
+        P.run(np.zeros(1 << 12, dtype=np.complex64), accumulate=True)
+    # the plan stays usable after argument errors
+    P.run(out)
+    torch.cuda.synchronize()
+    n, g = O.parse_circuit(inst.text)
+    check(out.cpu().numpy(), O.schrodinger(n, g), "c64")
