@@ -53,6 +53,7 @@ struct Params {
   int n_fastest;            // tile raster: 1 => consecutive tiles walk N
   int a_evict_last;         // 1 => A operand loads carry an L2 evict-last hint
   int accumulate;           // 1 => out += D (TMA reduce-add) instead of out = D
+
   int x3;
   float* out;               // D, row-major, ld = ldo floats
   long long ldo;
@@ -351,8 +352,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 // thread of both CTAs arrives on the leader's accumulator-empty barrier.
 constexpr int B2_TILE = (BN / 2) * BK * 2;               // 16 KB: this CTA's half of B
 constexpr int STAGE2_BYTES = 2 * A_TILE + 2 * B2_TILE;   // 64 KB
-constexpr int STAGES2 = 3;
-constexpr int SMEM2_BYTES = STAGES2 * STAGE2_BYTES + EPI_BYTES + 1024;
+constexpr int smem2_bytes(int nst, int ebuf) { return nst * STAGE2_BYTES + ebuf * EPI_BYTES + 1024; }
 constexpr uint32_t IDESC2 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                             ((uint32_t)((2 * BM) >> 4) << 24);
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // shared::cluster address -> the pair's rank-0 CTA
@@ -397,12 +397,16 @@ __device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
 }
 
 // p.num_m counts 256-row PAIR tiles here
+// NST SMEM stages, EBUF staging boxes per epilogue warp: <3,1> for long K
+// (c2: deep operand pipeline), <2,2> for short K (c4: num_k <= 2, the kernel
+// is output-write-bound, so a second box keeps two TMA stores per warp in flight)
+template <int NST, int EBUF>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     tc_gemm2_kernel(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUtensorMap mA_lo,
                     const __grid_constant__ CUtensorMap mB_hi, const __grid_constant__ CUtensorMap mB_lo,
                     const __grid_constant__ CUtensorMap mOut, const Params p) {
   extern __shared__ uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t full_bar[STAGES2], empty_bar[STAGES2], tfull_bar[2], tempty_bar[2];
+  __shared__ __align__(8) uint64_t full_bar[NST], empty_bar[NST], tfull_bar[2], tempty_bar[2];
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -412,7 +416,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   const int pair = blockIdx.x >> 1, num_pairs = gridDim.x >> 1;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES2; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(&full_bar[s], 1);   // the leader's producer arms it (both CTAs' bytes)
       mbar_init(&empty_bar[s], 1);  // one multicast commit per stage use
     }
@@ -457,7 +461,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             tma_load_2sm(st + A_TILE, &mA_lo, &full_bar[s], kb * BK, arow, a_pol);
             tma_load_2sm(st + 2 * A_TILE + B2_TILE, &mB_lo, &full_bar[s], kb * BK, brow, b_pol);
           }
-          if (++s == STAGES2) {
+          if (++s == NST) {
             s = 0;
             ph ^= 1;
           }
@@ -490,7 +494,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             }
           }
           mma2_commit_both(&empty_bar[s]);  // both CTAs' stage s free once these retire
-          if (++s == STAGES2) {
+          if (++s == NST) {
             s = 0;
             ph ^= 1;
           }
@@ -507,7 +511,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const uint64_t st_pol = policy_evict_first();
     const int q = warp & 3;
     const int half = (warp - 2) / 4;
-    uint8_t* stg = smem + STAGES2 * STAGE2_BYTES + (warp - 2) * 4096;
+    uint8_t* stg0 = smem + NST * STAGE2_BYTES + (warp - 2) * 4096 * EBUF;
+    int buf = 0;
     int acc = 0;
     uint32_t aph = 0;
     for (int tile = pair; tile < num_tiles; tile += num_pairs) {
@@ -534,8 +539,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           asm volatile("tcgen05.fence::before_thread_sync;");
           mbar_arrive_leader(&tempty_bar[acc]);
         }
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        // the TMA store issued EBUF chunks ago from this box must have read it
+        if (lane == 0) {
+          if (EBUF == 1)
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          else
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        }
         __syncwarp();
+        uint8_t* stg = stg0 + buf * 4096;
+        buf = (buf + 1) % EBUF;
         float4* dst = reinterpret_cast<float4*>(stg + lane * 128);
 #pragma unroll
         for (int j = 0; j < 8; ++j)
@@ -769,6 +782,7 @@ inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row
   // (N-fastest re-reads all of B per row block: 7 GB of DRAM reads per 1/16
   // of c4, ncu profiles/r01.)
   p.n_fastest = 0;
+
   p.a_evict_last = ((x3 ? 2 : 1) * rpad * kcols * 2 <= (64ll << 20)) ? 1 : 0;
   p.out = (float*)out;
   p.ldo = 2 * MB;
@@ -788,7 +802,11 @@ inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row
     // CTA pairs: 256-row M tiles, each CTA loads half of every B tile
     static bool attr2 = false;
     if (!attr2) {
-      e = cudaFuncSetAttribute(tc::tc_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM2_BYTES);
+      e = cudaFuncSetAttribute(tc::tc_gemm2_kernel<3, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               tc::smem2_bytes(3, 1));
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(tc::tc_gemm2_kernel<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 tc::smem2_bytes(2, 2));
       if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("tc2 smem attr: ") + cudaGetErrorString(e));
       attr2 = true;
     }
@@ -797,7 +815,10 @@ inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row
     p.num_m = (int)((rows + 2 * tc::BM - 1) / (2 * tc::BM));
     const long long tiles = (long long)p.num_m * p.num_n;
     const int grid = 2 * (int)std::min<long long>(tiles, num_sms() / 2);
-    tc::tc_gemm2_kernel<<<grid, tc::THREADS, tc::SMEM2_BYTES, st>>>(mAh, mAl, mBh2, mBl2, mO, p);
+    if (p.num_k <= 2)
+      tc::tc_gemm2_kernel<2, 2><<<grid, tc::THREADS, tc::smem2_bytes(2, 2), st>>>(mAh, mAl, mBh2, mBl2, mO, p);
+    else
+      tc::tc_gemm2_kernel<3, 1><<<grid, tc::THREADS, tc::smem2_bytes(3, 1), st>>>(mAh, mAl, mBh2, mBl2, mO, p);
   } else {
     const long long tiles = (long long)p.num_m * p.num_n;
     const int grid = (int)std::min<long long>(tiles, num_sms());
