@@ -26,6 +26,9 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 METRIC = "HSF paths/s"
+# dram bytes read + written per launch of the dominant kernel, from one
+# `ncu --set full` capture of the same workload (profiles/r01/*details.txt)
+NCU_TRAFFIC = {("c2", "gemm"): 1.2618e9 + 0.1166e9}
 
 
 def _args():
@@ -358,13 +361,20 @@ def main():
         if t_tensor >= t_hbm:
             ach = tflop / (core_ms * 1e-3) / 1e12
             roof = {"bound": "tensor", "achieved": ach, "peak": bf16, "unit": "TFLOP/s", "frac": ach / bf16,
-                    "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst); sustained %.1f" %
-                                   peaks.get("bf16_tflops_sustained", 0.0)}
+                    "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst: torch/cuBLAS bf16 8192^3, itself "
+                                   "%.0f%% of the 2250 TFLOP/s nominal dense peak); sustained %.1f" %
+                                   (100.0 * bf16 / 2250.0, peaks.get("bf16_tflops_sustained", 0.0)),
+                    "frac_of_nominal_2250": ach / 2250.0}
         else:
             ach = obytes / (core_ms * 1e-3) / 1e9
             roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
-        roof.update({"kernel": "tc_gemm_kernel (tcgen05 bf16, split x%d)" % nprod, "traffic": None,
+        pair = MA > 128
+        roof.update({"kernel": "%s (tcgen05 bf16, split x%d)" % ("tc_gemm2_kernel CTA pairs" if pair else
+                                                                 "tc_gemm_kernel", nprod),
+                     "traffic": NCU_TRAFFIC.get((a.config, "gemm")),
+                     "traffic_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum per launch "
+                                       "(profiles/r01)" if (a.config, "gemm") in NCU_TRAFFIC else None,
                      "flops_per_launch": tflop, "bytes_per_launch": obytes,
                      "useful_complex_flops": 8.0 * MA * MB * K, "kernel_ms": core_ms})
     elif full:

@@ -14,6 +14,7 @@
 //   H8 per-half programs: fixed local gates + factor slots, gate fusion
 //      (P:282), path-tree levels, SMEM tile passes
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -292,10 +293,18 @@ static void decompose_unit(const std::vector<Gate>& gates, Unit& u, int n_low, c
       for (int j = 0; j < g.k; ++j)
         pos[j] = (int)(std::find(u.support.begin(), u.support.end(), g.q[j]) - u.support.begin());
       const int dg = 1 << g.k;
-      for (size_t i = 0; i < N; ++i) {
-        int il = 0;
-        for (int j = 0; j < g.k; ++j) il = (il << 1) | (int)((i >> pos[j]) & 1);
-        d[i] *= g.U[(size_t)il * dg + il];
+      std::vector<cd> diag(dg);
+      for (int il = 0; il < dg; ++il) diag[il] = g.U[(size_t)il * dg + il];
+      if (g.k == 1) {
+        for (size_t i = 0; i < N; ++i) d[i] *= diag[(i >> pos[0]) & 1];
+      } else if (g.k == 2) {  // first-listed qubit = MSB of the gate-local index
+        for (size_t i = 0; i < N; ++i) d[i] *= diag[(((i >> pos[0]) & 1) << 1) | ((i >> pos[1]) & 1)];
+      } else {
+        for (size_t i = 0; i < N; ++i) {
+          int il = 0;
+          for (int j = 0; j < g.k; ++j) il = (il << 1) | (int)((i >> pos[j]) & 1);
+          d[i] *= diag[il];
+        }
       }
     }
     // M[i^b, i^a] = u(i^a, i^b): the diagonal operator's operator-Schmidt matrix
@@ -1070,7 +1079,16 @@ Plan* build_plan(const char* text, size_t len, int n_low, int64_t n_blocks, cons
                  const hsf_plan_opts& opts) {
   auto P = std::make_unique<Plan>();
   P->opts = opts;
+  const bool dbg = std::getenv("HSF_DEBUG_PLAN_TIME") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!dbg) return;
+    auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "plan %-12s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(now - t_last).count());
+    t_last = now;
+  };
   P->gates = parse(text, len, &P->n);
+  lap("parse");
   P->n_low = n_low;
   if (n_low < 1 || n_low >= P->n) fail(HSF_ERR_INVALID_ARG, "n_low must satisfy 1 <= n_low < n");
   const int G = (int)P->gates.size();
@@ -1113,6 +1131,7 @@ Plan* build_plan(const char* text, size_t len, int n_low, int64_t n_blocks, cons
   for (int gi = 0; gi < G; ++gi)
     if (!in_block[gi] && crossing(gi)) units.push_back({gi});
   auto order = schedule(P->gates, units);
+  lap("schedule");
   // renumber units in schedule order
   std::vector<int> remap(units.size(), -1);
   int nu = 0;
@@ -1130,6 +1149,7 @@ Plan* build_plan(const char* text, size_t len, int n_low, int64_t n_blocks, cons
     log2_np += std::log2((double)u.rank);
   }
   // individual-cut count n_p^t: product of the individual crossing-gate ranks
+  lap("decompose");
   P->log2_individual = 0;
   {
     hsf_plan_opts o2 = opts;
@@ -1141,6 +1161,7 @@ Plan* build_plan(const char* text, size_t len, int n_low, int64_t n_blocks, cons
         P->log2_individual += std::log2((double)tmp.rank);
       }
   }
+  lap("individual");
   // H7
   if (log2_np > opts.log2_path_budget + 1e-9)
     fail(HSF_ERR_PATH_BUDGET, "n_p = 2^" + std::to_string(log2_np) + " exceeds the path budget");
@@ -1157,7 +1178,9 @@ Plan* build_plan(const char* text, size_t len, int n_low, int64_t n_blocks, cons
   // H8
   const int U = (int)P->units.size();
   build_half(*P, 0, order, U, P->half[0]);
+  lap("half A");
   build_half(*P, 1, order, U, P->half[1]);
+  lap("half B");
   // Trailing-diagonal fold (bitstring runs): when the last units are all
   // diagonal and no gate follows them in either half (after hoisting), their
   // factors commute to the end of both half-circuits, so for an output sample
