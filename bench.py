@@ -439,6 +439,7 @@ def main():
                 "gpu_launches": n_launch, "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:
+        dist.barrier()  # rank 0 ran the e2e / CPU legs alone; leave together
         dist.destroy_process_group()
     return 0
 
