@@ -421,7 +421,11 @@ def main():
         r, sample, thr, _ = cpu_oracle_rate(inst, budget_s=15.0)
         cpu = {"value": r, "unit": "paths/s", "cores": thr, "kind": "oracle", "sample": sample}
 
-    n_launch = P.passes[0] + P.passes[1] + (1 if (full and eff_prec == "simt") else 3)
+    # our kernels per step: simulator passes of both halves, then the path-sum:
+    # full output = split_a + split_b + GEMM (SIMT: 1 kernel); bitstrings =
+    # 2 transposes + gather (folded tree when the trailing units fold)
+    sim_launches = sum(P.fold_passes) if used_fold else sum(P.passes)
+    n_launch = sim_launches + (1 if (full and eff_prec == "simt") else 3)
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "paths/s", "n_gpus": world, "steps": a.steps,
                 "warmup": max(3, a.warmup), "ms_per_step": t_step, "higher_is_better": True, "scaling": "strong",

@@ -149,6 +149,7 @@ typedef struct {
   double tree_bytes_a, tree_bytes_b; /* state bytes the simulator tile passes read + write
                                    for all paths (full tree; roofline numerator) */
   double fold_tree_bytes_a, fold_tree_bytes_b; /* same for the folded tree (0 if none) */
+  int32_t fold_passes_a, fold_passes_b;        /* device passes of the folded tree (0 if none) */
 } hsf_plan_info;
 
 /* Pointers in *info stay valid until hsf_plan_free. */

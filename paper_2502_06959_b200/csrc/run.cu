@@ -706,6 +706,8 @@ hsf_status hsf_plan_info_get(const hsf_plan_t* plan, hsf_plan_info* info) {
     info->tree_bytes_b = P->half[1].tree_bytes;
     info->fold_tree_bytes_a = P->fold_u0 >= 0 ? P->half_fold[0].tree_bytes : 0.0;
     info->fold_tree_bytes_b = P->fold_u0 >= 0 ? P->half_fold[1].tree_bytes : 0.0;
+    info->fold_passes_a = P->fold_u0 >= 0 ? P->half_fold[0].n_passes : 0;
+    info->fold_passes_b = P->fold_u0 >= 0 ? P->half_fold[1].n_passes : 0;
     info->n_joint_blocks = 0;
     for (const auto& un : P->units) info->n_joint_blocks += un.gids.size() > 1 ? 1 : 0;
   })

@@ -43,7 +43,8 @@ class _Info(C.Structure):
                 ("passes_a", C.c_int32), ("passes_b", C.c_int32), ("ops_a", C.c_int32), ("ops_b", C.c_int32),
                 ("plan_hash", C.c_uint64), ("fold_units", C.c_int32),
                 ("n_joint_blocks", C.c_int32), ("tree_bytes_a", C.c_double), ("tree_bytes_b", C.c_double),
-                ("fold_tree_bytes_a", C.c_double), ("fold_tree_bytes_b", C.c_double)]
+                ("fold_tree_bytes_a", C.c_double), ("fold_tree_bytes_b", C.c_double),
+                ("fold_passes_a", C.c_int32), ("fold_passes_b", C.c_int32)]
 
 
 class _RunArgs(C.Structure):
@@ -158,6 +159,7 @@ class Plan:
         self.n_units = int(i.n_units)
         self.tree_bytes = (float(i.tree_bytes_a), float(i.tree_bytes_b))
         self.fold_tree_bytes = (float(i.fold_tree_bytes_a), float(i.fold_tree_bytes_b))
+        self.fold_passes = (int(i.fold_passes_a), int(i.fold_passes_b))
 
     def __del__(self):
         h = getattr(self, "_h", None)

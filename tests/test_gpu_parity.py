@@ -544,3 +544,18 @@ def test_empty_and_invalid_requests(torch):
     torch.cuda.synchronize()
     n, g = O.parse_circuit(inst.text)
     check(out.cpu().numpy(), O.schrodinger(n, g), "c64")
+
+
+def test_c3_full_size_all_paths_sampled(torch):
+    # c3 exactly as bench.py runs it (all 256 joint-cut paths, 2^15-amplitude
+    # halves through the tiled tier, JIT passes, CUDA graph), checked on 4096
+    # of its 2^20 bitstrings that the oracle recombines one by one
+    inst = make_config("c3")
+    n, g = O.parse_circuit(inst.text)
+    P = O.plan(n, g, inst.n_low, inst.blocks)
+    A, B, c = O.half_states(P)
+    sel = inst.bitstrings[:4096]
+    ref = O.recombine_bits(A, B, c, sel, inst.n_low)
+    got, Pg = gpu_bits(torch, inst, inst.bitstrings)
+    check(got[:4096], ref, "c64")
+    assert Pg.n_paths == 256
