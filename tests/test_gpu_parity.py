@@ -559,3 +559,33 @@ def test_c3_full_size_all_paths_sampled(torch):
     got, Pg = gpu_bits(torch, inst, inst.bitstrings)
     check(got[:4096], ref, "c64")
     assert Pg.n_paths == 256
+
+
+def test_maximum_half_size_closed_form(torch):
+    # the largest halves the library takes: n = 60 cut 30|30 (2^30 amplitudes
+    # = 8 GiB complex64 per half-state) through the tiled tier.  Circuit with a
+    # closed form: H on every qubit, then CZ(29, 30) across the cut and
+    # CP(theta)(10, 50) across the cut: amp(x) = 2^-30 (-1)^(x29 x30)
+    # exp(i theta x10 x50); two rank-2 cuts = 4 paths (both trailing diagonal
+    # units fold into the per-sample weight in this bitstring run)
+    free, _ = torch.cuda.mem_get_info()
+    if free < (96 << 30):
+        pytest.skip("needs ~96 GB of free device memory")
+    n, nb, th = 60, 30, 0.8125
+    txt = f"qubits {n}\n" + "".join(f"h {q}\n" for q in range(n)) + f"cz 29 30\ncp {th.hex()} 10 50\n"
+    rng = np.random.default_rng(606)
+    bits = rng.integers(0, 1 << 62, size=1000, dtype=np.int64).astype(np.uint64) & np.uint64((1 << n) - 1)
+    bits[:3] = [0, (1 << n) - 1, (1 << 29) | (1 << 30)]
+    from paper_2502_06959_b200 import Plan
+    P = Plan(txt, nb, [])
+    assert P.n_paths == 4
+    b = torch.from_numpy(bits.view(np.int64)).cuda()
+    out = torch.empty(len(bits), dtype=torch.complex64, device="cuda")
+    P.run(out, bitstrings=b)
+    torch.cuda.synchronize()
+    x = bits
+    bit = lambda q: ((x >> np.uint64(q)) & np.uint64(1)).astype(np.int64)
+    ref = 2.0 ** -30 * (-1.0) ** (bit(29) * bit(30)) * np.exp(1j * th * bit(10) * bit(50))
+    got = out.cpu().numpy()
+    assert np.abs(got - ref).max() <= 1e-5 * 2.0 ** -30 * 100  # relative to |amp| = 2^-30
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 2e-5
