@@ -94,6 +94,13 @@ typedef struct {
                                     specialised to its op list (generated CUDA, NVRTC for
                                     sm_100a, compiled at the first hsf_run on a device and
                                     cached per process); 0 => generic interpreter kernel */
+  uint64_t partition_b;          /* 0 (default) => contiguous cut: half B = qubits [0, n_low).
+                                    Otherwise the bit mask of half B's qubits (any subset,
+                                    popcount == n_low): qubits are relabelled internally (B
+                                    qubits keep their order at [0, n_low), A qubits at
+                                    [n_low, n)); bitstrings and full outputs stay in the
+                                    caller's qubit order.  Full-output runs then need a device
+                                    output and all rows. */
   int32_t graphs;                /* 1 (default) => runs with device buffers are captured once
                                     into a CUDA graph (both streams, all launches) and replayed
                                     while pointers, ranges and precision stay the same */

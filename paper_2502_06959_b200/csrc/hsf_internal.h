@@ -116,6 +116,9 @@ struct Half {
 
 struct Plan {
   int n = 0, n_low = 0;
+  // non-contiguous partition: new index of caller qubit q (identity if none)
+  std::vector<int> relabel;
+  bool permuted = false;
   hsf_plan_opts opts{};
   std::vector<Gate> gates;
   std::vector<Unit> units;          // schedule order

@@ -1091,6 +1091,20 @@ Plan* build_plan(const char* text, size_t len, int n_low, int64_t n_blocks, cons
   lap("parse");
   P->n_low = n_low;
   if (n_low < 1 || n_low >= P->n) fail(HSF_ERR_INVALID_ARG, "n_low must satisfy 1 <= n_low < n");
+  // arbitrary partition: relabel so half B is [0, n_low)
+  P->relabel.resize(P->n);
+  for (int q = 0; q < P->n; ++q) P->relabel[q] = q;
+  if (opts.partition_b) {
+    if (P->n < 64 && (opts.partition_b >> P->n))
+      fail(HSF_ERR_INVALID_ARG, "partition_b names a qubit beyond the circuit");
+    if (__builtin_popcountll(opts.partition_b) != n_low)
+      fail(HSF_ERR_INVALID_ARG, "popcount(partition_b) must equal n_low");
+    int nb = 0, na = n_low;
+    for (int q = 0; q < P->n; ++q) P->relabel[q] = ((opts.partition_b >> q) & 1ull) ? nb++ : na++;
+    for (int q = 0; q < P->n; ++q) P->permuted = P->permuted || P->relabel[q] != q;
+    for (auto& g : P->gates)
+      for (int& q : g.q) q = P->relabel[q];
+  }
   const int G = (int)P->gates.size();
   auto crossing = [&](int gi) {
     bool lo = false, hi = false;
@@ -1226,6 +1240,7 @@ Plan* build_plan(const char* text, size_t len, int n_low, int64_t n_blocks, cons
     h = fnv(h, P->half_fold[s].dev_ops.data(), P->half_fold[s].dev_ops.size() * sizeof(DevOp));
   }
   h = fnv(h, P->trail_tab.data(), P->trail_tab.size() * sizeof(cd));
+  h = fnv(h, P->relabel.data(), P->relabel.size() * sizeof(int));
   h = fnv(h, P->coef.data(), P->coef.size() * sizeof(cd));
   h = fnv(h, P->ranks.data(), P->ranks.size() * sizeof(int32_t));
   P->hash = h;

@@ -37,6 +37,7 @@ struct DeviceState {
   DevOp* ops_fold[2] = {nullptr, nullptr};  // trailing-diagonal fold variant
   void* trail = nullptr;                    // folded units' block diagonals (run dtype)
   bool jit = false;                         // specialised pass kernels loaded
+  unsigned long long* perm_tab = nullptr;   // caller -> internal index bits (partitions)
   std::vector<void*> jit_fn[2][2];          // [variant][half] per flattened pass
   void* ws = nullptr;
   size_t ws_bytes = 0;
@@ -70,6 +71,7 @@ void destroy_device(Plan* p) {
   cudaFree(d->ops_fold[0]);
   cudaFree(d->ops_fold[1]);
   cudaFree(d->trail);
+  cudaFree(d->perm_tab);
   cudaFree(d->ws);
   cudaFree(d->cp);
   for (auto& e : d->ev)
@@ -130,6 +132,20 @@ static DeviceState* ensure_device(Plan* P, int device) {
       CK(cudaMemcpy(d->trail, P->trail_tab.data(), nt * 16, cudaMemcpyHostToDevice));
     }
   }
+  if (P->permuted) {
+    std::vector<unsigned long long> tab(4 * 65536, 0);
+    for (int k = 0; k < 4; ++k)
+      for (unsigned v = 0; v < 65536; ++v) {
+        unsigned long long x = 0;
+        for (int b = 0; b < 16; ++b) {
+          const int q = 16 * k + b;
+          if (q < P->n && ((v >> b) & 1u)) x |= 1ull << P->relabel[q];
+        }
+        tab[(size_t)k * 65536 + v] = x;
+      }
+    CK(cudaMalloc(&d->perm_tab, tab.size() * 8));
+    CK(cudaMemcpy(d->perm_tab, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice));
+  }
   if (P->opts.jit) {
     // one specialised kernel per tile pass (jit.cpp), compiled once per process
     std::vector<std::string> src;
@@ -175,6 +191,7 @@ struct Layout {
   size_t off_leaves[2] = {0, 0};
   size_t off_T[2] = {0, 0};    // transposed operands (bitstring mode)
   size_t off_bits = 0, off_out = 0, off_tc = 0;
+  size_t off_pbits = 0, off_pout = 0;  // relabelled bitstrings / internal-order output (partitions)
   size_t tc_bytes = 0;
   uint64_t chunk_rows = 0;     // full mode, host output: rows per staged D2H chunk
   size_t chunk_bytes = 0;
@@ -246,7 +263,17 @@ static Layout make_layout(const Plan& P, const hsf_run_args& a, size_t elem) {
       L.off_out = off;
       off = align_up(off + a.n_bitstrings * elem);
     }
+    if (P.permuted) {
+      L.off_pbits = off;
+      off = align_up(off + a.n_bitstrings * 8);
+    }
   } else {
+    if (P.permuted) {
+      if (!a.out_on_device || L.r0 != 0 || L.r1 != (1ull << nA))
+        fail(HSF_ERR_UNSUPPORTED, "non-contiguous partitions need a device output and all rows in full-output runs");
+      L.off_pout = off;
+      off = align_up(off + ((size_t)1 << P.n) * elem);
+    }
     if (L.prec == HSF_PREC_BF16X3 || L.prec == HSF_PREC_BF16X1) {
       L.tc_bytes = tc_workspace_bytes((long long)L.K, (long long)(L.r1 - L.r0), 1ll << nB, L.prec == HSF_PREC_BF16X3);
       L.off_tc = off;
@@ -460,6 +487,13 @@ static void run_core_bits(Plan* P, DeviceState* d, const Layout& L, const hsf_ru
   }
   const long long ns = (long long)a.n_bitstrings;
   long long blocks = std::min<long long>((ns + 7) / 8, 148ll * 64);
+  if (P->permuted) {  // caller bit order -> internal (relabelled) bit order
+    unsigned long long* pb = (unsigned long long*)(ws + L.off_pbits);
+    permute_bits_kernel<<<(unsigned)std::min<long long>((ns + 255) / 256, 148ll * 8), 256, 0, st>>>(bits, pb, ns,
+                                                                                                 d->perm_tab);
+    CK(cudaGetLastError());
+    bits = pb;
+  }
   TrailParams tw{};
   if (L.fold) {
     tw.n = (int)P->trail_mask.size();
@@ -530,6 +564,14 @@ static void run_all(Plan* P, DeviceState* d, const Layout& L, const hsf_run_args
     run_core_bits<R>(P, d, L, a, st, out);
     if (!a.out_on_device)
       CK(cudaMemcpyAsync(a.out, out, (size_t)a.n_bitstrings * sizeof(C), cudaMemcpyDeviceToHost, st));
+  } else if (a.out_on_device && P->permuted) {
+    // internal-order result into the workspace, then back to the caller's qubit order
+    C* tmp = (C*)(ws + L.off_pout);
+    run_core_full<R>(P, d, L, st, 0, L.r1 - L.r0, tmp, false);
+    const long long nout = 1ll << P->n;
+    permute_out_kernel<C><<<(unsigned)std::min<long long>((nout + 255) / 256, 148ll * 32), 256, 0, st>>>(
+        tmp, (C*)a.out, nout, d->perm_tab, a.accumulate);
+    CK(cudaGetLastError());
   } else if (a.out_on_device) {
     run_core_full<R>(P, d, L, st, 0, L.r1 - L.r0, (C*)a.out, a.accumulate != 0);
   } else {
@@ -658,6 +700,7 @@ hsf_status hsf_plan_opts_default(hsf_plan_opts* o) {
   o->fold_trailing_diag = 1;
   o->jit = 1;
   o->graphs = 1;
+  o->partition_b = 0;
   return HSF_OK;
 }
 

@@ -40,6 +40,36 @@ __global__ void transpose_fold_kernel(const C* __restrict__ in, C* __restrict__ 
   }
 }
 
+// --------------------------------------------- qubit relabelling (partitions)
+// caller index <-> internal index for a non-contiguous partition: bit q of the
+// caller's index is bit relabel[q] of the internal one.  tab[16*k .. ] holds,
+// for each 16-bit chunk k of the source index, the mapped bits (4 x 2^16).
+__device__ __forceinline__ unsigned long long permute_index(unsigned long long x,
+                                                            const unsigned long long* __restrict__ tab) {
+  return __ldg(&tab[x & 0xFFFFull]) | __ldg(&tab[65536 + ((x >> 16) & 0xFFFFull)]) |
+         __ldg(&tab[131072 + ((x >> 32) & 0xFFFFull)]) | __ldg(&tab[196608 + (x >> 48)]);
+}
+
+__global__ void permute_bits_kernel(const unsigned long long* __restrict__ in, unsigned long long* __restrict__ out,
+                                    long long n, const unsigned long long* __restrict__ tab) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = permute_index(in[i], tab);
+}
+
+// out[j] (caller order) = in[map(j)] (internal order), or += with accumulate
+template <typename C>
+__global__ void permute_out_kernel(const C* __restrict__ in, C* __restrict__ out, long long n,
+                                   const unsigned long long* __restrict__ tab, int accumulate) {
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
+    C v = in[permute_index((unsigned long long)j, tab)];
+    if (accumulate) {
+      v.x += out[j].x;
+      v.y += out[j].y;
+    }
+    out[j] = v;
+  }
+}
+
 // ------------------------------------------------------------------- K6
 // Folded trailing diagonal units: amp(s) *= prod_u D_u[s's bits on supp(u)]
 // (block-local index, LSB = smallest support qubit; see plan.cpp).

@@ -31,7 +31,8 @@ class _Opts(C.Structure):
     _fields_ = [("dtype", C.c_int), ("svd_rel_tol", C.c_double), ("max_dense_block_qubits", C.c_int32),
                 ("log2_path_budget", C.c_double), ("individual", C.c_int32), ("tile_qubits", C.c_int32),
                 ("fuse_gates", C.c_int32), ("hoist_gates", C.c_int32), ("fold_trailing_diag", C.c_int32),
-                ("jit", C.c_int32), ("graphs", C.c_int32)]
+                ("jit", C.c_int32), ("partition_b", C.c_uint64),
+                ("graphs", C.c_int32)]
 
 
 class _Info(C.Structure):
@@ -104,7 +105,9 @@ def version() -> str:
 
 
 class Plan:
-    """hsf_plan(): host-side joint-cut plan.  `blocks` is a list of
+    """hsf_plan(): host-side joint-cut plan.  `n_low` is the size
+    of half B = qubits [0, n_low), or a list of the qubits forming half B (any
+    partition; relabelled internally, results in the caller's order).  `blocks` is a list of
     gate-index lists, or "auto" (automatic cascades of commuting diagonal
     crossing gates); `individual=True` cuts every crossing gate alone."""
 
@@ -115,6 +118,10 @@ class Plan:
         L = lib()
         o = _Opts()
         _check(L.hsf_plan_opts_default(C.byref(o)))
+        if isinstance(n_low, (list, tuple, set, frozenset)):  # half B = these qubits (any subset)
+            qs = sorted(set(int(q) for q in n_low))
+            o.partition_b = sum(1 << q for q in qs)
+            n_low = len(qs)
         o.dtype = HSF_C64 if dtype == "c64" else HSF_C128
         o.svd_rel_tol = svd_rel_tol
         o.individual = int(individual)

@@ -186,3 +186,15 @@ def test_auto_blocks_match_oracle_finder(hsf, seed):
     assert P.n_units == len(Po.units) == ncasc
     assert P.n_paths == Po.n_paths
     assert P.n_joint_blocks == len(blocks)
+
+
+def test_partition_mask_validation_and_counts(hsf):
+    from paper_2502_06959_b200 import HsfError, Plan
+    # GHZ-like chain: cutting between {0,2} and {1,3} crosses 3 CNOTs, the
+    # contiguous cut {0,1}|{2,3} only one
+    txt = "qubits 4\nh 0\ncx 0 1\ncx 1 2\ncx 2 3\n"
+    assert Plan(txt, 2, []).n_units == 1
+    assert Plan(txt, [0, 2], []).n_units == 3
+    assert Plan(txt, [0, 1], []).plan_hash == Plan(txt, 2, []).plan_hash
+    with pytest.raises(HsfError):
+        Plan(txt, [0, 9], [])  # qubit beyond the circuit

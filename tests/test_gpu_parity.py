@@ -286,6 +286,7 @@ def test_c4_full_size_sampled(torch):
     # half-states and recombines 2^16 sampled output indices one by one; the
     # whole output must carry unit norm (sum over every amplitude).
     inst = make_config("c4")
+    torch.cuda.empty_cache()
     free, _ = torch.cuda.mem_get_info()
     if free < (140 << 30):
         pytest.skip("needs ~140 GB of free device memory")
@@ -308,7 +309,8 @@ def test_c4_full_size_sampled(torch):
     idx[:4] = [0, (1 << n) - 1, (1 << inst.n_low) - 1, 1 << inst.n_low]
     ref = O.recombine_bits(A, B, c, idx.astype(np.uint64), inst.n_low)
     got = out[torch.from_numpy(idx).cuda()].cpu().numpy()
-    del out
+    del out, P
+    torch.cuda.empty_cache()
     check(got, ref, "c64")
     assert abs(norm - 1.0) < 1e-4, norm
 
@@ -568,6 +570,7 @@ def test_maximum_half_size_closed_form(torch):
     # CP(theta)(10, 50) across the cut: amp(x) = 2^-30 (-1)^(x29 x30)
     # exp(i theta x10 x50); two rank-2 cuts = 4 paths (both trailing diagonal
     # units fold into the per-sample weight in this bitstring run)
+    torch.cuda.empty_cache()
     free, _ = torch.cuda.mem_get_info()
     if free < (96 << 30):
         pytest.skip("needs ~96 GB of free device memory")
@@ -589,3 +592,26 @@ def test_maximum_half_size_closed_form(torch):
     got = out.cpu().numpy()
     assert np.abs(got - ref).max() <= 1e-5 * 2.0 ** -30 * 100  # relative to |amp| = 2^-30
     assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 2e-5
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_noncontiguous_partition(torch, seed):
+    # half B = an arbitrary qubit subset (relabelled internally): full output
+    # and bitstrings in the caller's qubit order equal the Schroedinger state
+    inst = random_small_circuit(300 + seed, n=10, n_gates=30, with_u=True)
+    n, g = O.parse_circuit(inst.text)
+    ref = O.schrodinger(n, g)
+    rng = np.random.default_rng(seed)
+    part = sorted(int(q) for q in rng.choice(n, size=int(rng.integers(2, n - 1)), replace=False))
+    from paper_2502_06959_b200 import Plan
+    P = Plan(inst.text, part, [], dtype="c128", log2_path_budget=30)
+    out = torch.empty(1 << n, dtype=torch.complex128, device="cuda")
+    P.run(out, precision="simt")
+    torch.cuda.synchronize()
+    check(out.cpu().numpy(), ref, "c128")
+    bits = rng.integers(0, 1 << n, size=777).astype(np.uint64)
+    b = torch.from_numpy(bits.view(np.int64)).cuda()
+    ob = torch.empty(len(bits), dtype=torch.complex128, device="cuda")
+    P.run(ob, bitstrings=b)
+    torch.cuda.synchronize()
+    check(ob.cpu().numpy(), ref[bits.astype(np.int64)], "c128")
