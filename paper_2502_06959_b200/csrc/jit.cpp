@@ -96,9 +96,10 @@ struct Gen {
   }
 
   void header(const std::string& name, int minb) {
-    o << "extern \"C\" __global__ void __launch_bounds__(256, " << minb << ") " << name << "(const JitArgs a) {\n";
+    o << "extern \"C\" __global__ void __launch_bounds__(" << nt << ", " << minb << ") " << name
+      << "(const JitArgs a) {\n";
     o << "  typedef " << (c64 ? "float2" : "double2") << " C;\n";
-    o << "  constexpr u32 NT = 256u, NEL = 1u << " << t << ";\n";
+    o << "  constexpr u32 NT = " << nt << "u, NEL = 1u << " << t << ";\n";
     o << "  extern __shared__ __align__(128) unsigned char smem_raw[];\n";
     o << "  C* s = reinterpret_cast<C*>(smem_raw);\n";
     o << "  C* stab = reinterpret_cast<C*>(smem_raw + (sizeof(C) << " << t << "));\n";
@@ -243,10 +244,13 @@ struct Gen {
     o << "      s[sw(e)] = v; } }\n  }\n";
   }
 
-  std::string build(const std::string& name) {
+  int nt = 256;  // threads per CTA (512 for narrow tree levels)
+
+  std::string build(const std::string& name, int threads) {
+    nt = threads;
     bool heavy = false;
     for (auto& d : ops) heavy = heavy || d.kind == OP_RPASS || (d.kind == OP_DENSE && d.k > 2);
-    header(name, heavy ? 2 : 3);
+    header(name, nt > 256 ? 1 : (heavy ? 2 : 3));
     size_t i = 0;
     while (i < ops.size()) {
       const DevOp& d = ops[i];
@@ -339,9 +343,9 @@ std::vector<char> nvrtc_compile(const std::string& src, std::string& log) {
 
 }  // namespace
 
-std::string jit_pass_source(const Half& H, const Pass& ps, bool c64) {
+std::string jit_pass_source(const Half& H, const Pass& ps, bool c64, int threads) {
   Gen g(H, ps, c64);
-  return std::string(kPrelude) + "\n" + g.build("hsf_jit_pass");
+  return std::string(kPrelude) + "\n" + g.build("hsf_jit_pass", threads);
 }
 
 size_t jit_smem_bytes(const Pass& ps, bool c64) {
@@ -392,10 +396,11 @@ std::vector<void*> jit_compile_all(int device, const std::vector<std::string>& s
   return fns;
 }
 
-void jit_launch(void* fn, unsigned gx, unsigned gy, size_t smem, void* stream, const JitLaunchArgs& a) {
+void jit_launch(void* fn, unsigned gx, unsigned gy, unsigned threads, size_t smem, void* stream,
+                const JitLaunchArgs& a) {
   JitLaunchArgs args = a;
   void* params[] = {&args};
-  if (drv().launchKernel((CUfunction)fn, gx, gy, 1, 256, 1, 1, (unsigned)smem, (CUstream)stream, params, nullptr) !=
+  if (drv().launchKernel((CUfunction)fn, gx, gy, 1, threads, 1, 1, (unsigned)smem, (CUstream)stream, params, nullptr) !=
       CUDA_SUCCESS)
     fail(HSF_ERR_CUDA, "cuLaunchKernel (specialised pass) failed");
 }

@@ -39,6 +39,7 @@ struct DeviceState {
   bool jit = false;                         // specialised pass kernels loaded
   unsigned long long* perm_tab = nullptr;   // caller -> internal index bits (partitions)
   std::vector<void*> jit_fn[2][2];          // [variant][half] per flattened pass
+  std::vector<int> jit_nt[2][2];            //   and its threads per CTA
   void* ws = nullptr;
   size_t ws_bytes = 0;
   // cached per-range path coefficients
@@ -154,11 +155,19 @@ static DeviceState* ensure_device(Plan* P, int device) {
       if (v == 1 && P->fold_u0 < 0) continue;
       for (int h = 0; h < 2; ++h) {
         const Half& H = v ? P->half_fold[h] : P->half[h];
-        for (const auto& tr : H.trans)
+        for (const auto& tr : H.trans) {
+          // narrow levels (few nodes x tiles, e.g. a root that hoisting made
+          // heavy) get 512-thread CTAs: twice the threads on the few SMs busy
+          const double ctas = (double)range_prod(v ? std::vector<int32_t>(P->ranks.begin(), P->ranks.begin() + P->fold_u0)
+                                                   : P->ranks, 0, tr.level_out);
           for (const auto& ps : tr.passes) {
-            src.push_back(jit_pass_source(H, ps, c64));
+            const double n_cta = ctas * std::ldexp(1.0, H.m - ps.t);
+            const int nt = n_cta < 2.0 * num_sms() ? 512 : 256;
+            src.push_back(jit_pass_source(H, ps, c64, nt));
             owner.push_back({v, h});
+            d->jit_nt[v][h].push_back(nt);
           }
+        }
       }
     }
     std::vector<void*> fns = jit_compile_all(device, src);
@@ -431,7 +440,8 @@ static void run_half(const Plan& P, DeviceState* d, int h, const Layout& L, cuda
         if (jf) {
           JitLaunchArgs ja{pp.src, pp.dst, pp.coef, pp.node_first, pp.node_local0, pp.src_first, pp.src_div,
                            pp.tile0};
-          jit_launch((*jf)[pass_ord], (unsigned)tiles, (unsigned)ny, jit_smem_bytes(ps, sizeof(R) == 4), st, ja);
+          jit_launch((*jf)[pass_ord], (unsigned)tiles, (unsigned)ny, (unsigned)d->jit_nt[L.fold ? 1 : 0][h][pass_ord],
+                     jit_smem_bytes(ps, sizeof(R) == 4), st, ja);
         } else {
           dim3 grid((unsigned)tiles, (unsigned)ny);
           kern<<<grid, nthr, smem, st>>>(pp);
