@@ -172,7 +172,7 @@ typedef struct {
   int32_t bits_on_device;       /* 1 => device pointer, 0 => host pointer */
   void* out;                    /* caller-owned, plan dtype */
   int32_t out_on_device;        /* 1 => device pointer, 0 => host pointer: full-mode
-                                   rows are computed in chunks of <= 256 MiB into two
+                                   rows are computed in chunks of <= 32 MiB into two
                                    device staging buffers and copied back while the
                                    next chunk is computed (bounded device memory);
                                    pinned host memory gives overlapped copies */

@@ -208,7 +208,7 @@ struct Layout {
 };
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
-constexpr size_t kHostChunkBytes = (size_t)256 << 20;
+constexpr size_t kHostChunkBytes = (size_t)32 << 20;  // D2H of chunk i overlaps the path-sum of chunk i+1
 
 static uint64_t nodes_at(const Layout& Y, int L, uint64_t p0, uint64_t p1) {
   uint64_t S = suffix_prod(Y.ranks, L);
