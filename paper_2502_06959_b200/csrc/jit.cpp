@@ -74,7 +74,9 @@ struct Gen {
   std::vector<DevOp> ops;
   std::vector<int> pos2q;  // tile position -> half qubit
 
-  Gen(const Half& h, const Pass& p, bool c) : H(h), ps(p), c64(c) {
+  const std::vector<cd>* coef = nullptr;  // plan master table (fp64): fixed-gate literals
+
+  Gen(const Half& h, const Pass& p, bool c, const std::vector<cd>* cf) : H(h), ps(p), c64(c), coef(cf) {
     t = p.t;
     m = h.m;
     whole = (t == m);
@@ -84,6 +86,21 @@ struct Gen {
   }
 
   std::string table(int i) const { return "M" + std::to_string(i); }
+  // fixed (non-factor) gate entries become literals in the generated code: no
+  // dependent table loads on the gate chain (exact: %a of the run-dtype value)
+  bool literal(const DevOp& d) const { return coef && d.radix <= 1 && (d.kind == OP_R1 || d.kind == OP_DENSE); }
+  std::string lit(int64_t idx) const {
+    const cd v = (*coef)[(size_t)idx];
+    char b[128];
+    if (c64)
+      std::snprintf(b, sizeof b, "make_float2(%af, %af)", (double)(float)v.real(), (double)(float)v.imag());
+    else
+      std::snprintf(b, sizeof b, "make_double2(%a, %a)", v.real(), v.imag());
+    return b;
+  }
+  std::string mat(const DevOp& d, int i, int e) const {
+    return literal(d) ? lit(d.table + e) : "__ldg(&" + table(i) + "[" + std::to_string(e) + "])";
+  }
   std::string didx(const DevOp& d, const std::string& g) const {
     std::vector<int> from(d.q, d.q + d.k), to(d.k);
     for (int j = 0; j < d.k; ++j) to[j] = j;
@@ -100,9 +117,21 @@ struct Gen {
       << "(const JitArgs a) {\n";
     o << "  typedef " << (c64 ? "float2" : "double2") << " C;\n";
     o << "  constexpr u32 NT = " << nt << "u, NEL = 1u << " << t << ";\n";
+    // cluster tier (cb > 0): the tile is split over 2^cb CTAs of a cluster by
+    // its top cb tile positions; CTA `RANK` holds elements [RANK << LB, +LNEL)
+    o << "  constexpr u32 CB = " << cb << "u, LB = " << (t - cb) << "u, LNEL = 1u << LB;\n";
+    o << "  (void)CB;\n";
     o << "  extern __shared__ __align__(128) unsigned char smem_raw[];\n";
     o << "  C* s = reinterpret_cast<C*>(smem_raw);\n";
-    o << "  C* stab = reinterpret_cast<C*>(smem_raw + (sizeof(C) << " << t << "));\n";
+    o << "  C* stab = reinterpret_cast<C*>(smem_raw + (sizeof(C) << " << (t - cb) << "));\n";
+    if (cb) {
+      o << "  const u32 RANK = cluster_rank();\n";
+      o << "  C* sr[" << (1 << cb) << "];\n";
+      o << "#pragma unroll\n  for (u32 r = 0; r < " << (1 << cb) << "u; ++r) sr[r] = map_rank(s, r);\n";
+      o << "  auto P = [&](u32 e) -> C& { return sr[e >> LB][sw(e & (LNEL - 1u))]; };\n";
+    } else {
+      o << "  constexpr u32 RANK = 0u;\n";
+    }
     o << "  (void)stab;\n";
     o << "  const long long node_g = a.node_first + blockIdx.y;\n";
     o << "  const C* coef = reinterpret_cast<const C*>(a.coef);\n";
@@ -118,7 +147,7 @@ struct Gen {
         if (std::find(ps.T.begin(), ps.T.end(), q) == ps.T.end()) nonT.push_back(q);
       std::vector<int> from(nonT.size()), to = nonT;
       for (size_t j = 0; j < nonT.size(); ++j) from[j] = (int)j;
-      o << "  const u32 tile = blockIdx.x + a.tile0;\n";
+      o << "  const u32 tile = (blockIdx.x >> CB) + a.tile0;\n";
       o << "  const u32 base = " << gather_expr("tile", from, to) << ";\n";
       std::vector<int> pf, pt;
       for (int i = 0; i < t; ++i) {
@@ -146,35 +175,56 @@ struct Gen {
     // load (or |0...0>)
     o << "  if (src) {\n";
     o << "#pragma unroll 4\n";
-    o << "    for (u32 e = 2u * threadIdx.x; e < NEL; e += 2u * NT) { C x_, y_; ld2(src + G(e), x_, y_); "
+    o << "    for (u32 e = 2u * threadIdx.x; e < LNEL; e += 2u * NT) { C x_, y_; ld2(src + G((RANK << LB) | e), x_, y_); "
          "s[sw(e)] = x_; s[sw(e + 1)] = y_; }\n";
     o << "  } else {\n";
-    o << "    for (u32 e = threadIdx.x; e < NEL; e += NT) { C v_ = czero<C>(); if (G(e) == 0u) v_.x = 1; s[sw(e)] = v_; }\n";
-    o << "  }\n  __syncthreads();\n";
+    o << "    for (u32 e = threadIdx.x; e < LNEL; e += NT) { C v_ = czero<C>(); if (G((RANK << LB) | e) == 0u) v_.x = 1; "
+         "s[sw(e)] = v_; }\n";
+    o << "  }\n";
+    o << (cb ? "  cluster_sync();\n" : "  __syncthreads();\n");
+  }
+
+  bool cross(const int* pos, int k) const {
+    for (int j = 0; j < k; ++j)
+      if (pos[j] >= t - cb) return true;
+    return false;
+  }
+  // element access: local op -> this CTA's SMEM, cross op -> any CTA's (DSMEM)
+  std::string el(bool x, const std::string& e) const { return x ? "P(" + e + ")" : "s[sw(" + e + ")]"; }
+  void sync_pre(bool x) { o << (x ? "  cluster_sync();\n" : "  __syncthreads();\n"); }
+  // loop over groups: local ops walk this CTA's groups, cross ops the whole tile's
+  void group_loop(bool x, const std::string& var, int shift) {
+    if (x)
+      o << "  for (u32 " << var << " = RANK * NT + threadIdx.x; " << var << " < (NEL >> " << shift << "); " << var
+        << " += (NT << CB)) {\n";
+    else
+      o << "  for (u32 " << var << " = threadIdx.x; " << var << " < (LNEL >> " << shift << "); " << var
+        << " += NT) {\n";
   }
 
   void dense(const DevOp& d, int i) {
     const int K = d.k, D = 1 << K;
+    const bool x = cross(d.q, K);
     std::vector<int> sorted(d.q, d.q + K);
     std::sort(sorted.begin(), sorted.end());
-    o << "  __syncthreads();\n";
-    o << "  for (u32 g = threadIdx.x; g < (NEL >> " << K << "); g += NT) {\n";
+    sync_pre(x);
+    group_loop(x, "g", K);
     o << "    u32 b = g;";
     for (int p : sorted) o << " b = ins0<" << p << ">(b);";
     o << "\n    C v[" << D << "];\n";
     std::vector<uint32_t> off(D);
     for (int r = 0; r < D; ++r) {
-      uint32_t x = 0;
+      uint32_t xo = 0;
       for (int j = 0; j < K; ++j)
-        if ((r >> j) & 1) x |= 1u << d.q[j];
-      off[r] = x;
-      o << "    v[" << r << "] = s[sw(b + " << x << "u)];\n";
+        if ((r >> j) & 1) xo |= 1u << d.q[j];
+      off[r] = xo;
+      o << "    v[" << r << "] = " << el(x, "b + " + std::to_string(xo) + "u") << ";\n";
     }
     if (K <= 3) {
       for (int r = 0; r < D; ++r) {
         o << "    { C acc = czero<C>();";
-        for (int c = 0; c < D; ++c) o << " acc = cfma(__ldg(&" << table(i) << "[" << r * D + c << "]), v[" << c << "], acc);";
-        o << " s[sw(b + " << off[r] << "u)] = acc; }\n";
+        for (int c = 0; c < D; ++c) o << " acc = cfma(" << mat(d, i, r * D + c) << ", v[" << c << "], acc);";
+        o << " " << el(x, "b + " + std::to_string(off[r]) + "u") << " = acc; }\n";
       }
     } else {
       o << "    const u32 offs[" << D << "] = {";
@@ -183,9 +233,10 @@ struct Gen {
       o << "#pragma unroll 1\n    for (int r = 0; r < " << D << "; ++r) { C acc = czero<C>();\n";
       o << "#pragma unroll\n      for (int c = 0; c < " << D << "; ++c) acc = cfma(__ldg(&" << table(i) << "[r * " << D
         << " + c]), v[c], acc);\n";
-      o << "      s[sw(b + offs[r])] = acc; }\n";
+      o << "      " << el(x, "b + offs[r]") << " = acc; }\n";
     }
-    o << "  }\n  __syncthreads();\n";
+    o << "  }\n";
+    sync_pre(x);
   }
 
   // register pass: header at ops[i], then ops[i+1 .. i+n]
@@ -199,23 +250,28 @@ struct Gen {
     }
     std::vector<int> sorted(pos, pos + 4);
     std::sort(sorted.begin(), sorted.end());
-    o << "  __syncthreads();\n";
-    o << "  for (u32 gi = threadIdx.x; gi < (NEL >> 4); gi += NT) {\n";
+    const bool x = cross(pos, 4);
+    sync_pre(x);
+    group_loop(x, "gi", 4);
     o << "    u32 b = gi;";
     for (int p : sorted) o << " b = ins0<" << p << ">(b);";
-    o << "\n    const u32 gb = G(b); (void)gb;\n    C v[16];\n";
+    o << "\n    const u32 gb = G(" << (x ? "b" : "(RANK << LB) | b") << "); (void)gb;\n    C v[16];\n";
     uint32_t ek[16];
     for (int k = 0; k < 16; ++k) {
       uint32_t e = 0;
       for (int j = 0; j < 4; ++j)
         if ((k >> j) & 1) e |= 1u << pos[j];
       ek[k] = e;
-      o << "    v[" << k << "] = s[sw(b | " << e << "u)];\n";
+      o << "    v[" << k << "] = " << el(x, "(b | " + std::to_string(e) + "u)") << ";\n";
     }
     for (size_t r = i + 1; r <= i + (size_t)n; ++r) {
       const DevOp& d = ops[r];
       if (d.kind == OP_R1) {
-        o << "    r1<" << d.q[0] << ">(v, " << table((int)r) << ");\n";
+        if (literal(d))
+          o << "    r1c<" << d.q[0] << ">(v, " << lit(d.table) << ", " << lit(d.table + 1) << ", " << lit(d.table + 2)
+            << ", " << lit(d.table + 3) << ");\n";
+        else
+          o << "    r1<" << d.q[0] << ">(v, " << table((int)r) << ");\n";
       } else {  // diagonal: index of element k = i0 | IK[k]
         o << "    { const u32 i0 = " << didx(d, "gb") << ";\n";
         for (int k = 0; k < 16; ++k) {
@@ -230,24 +286,27 @@ struct Gen {
         o << "    }\n";
       }
     }
-    for (int k = 0; k < 16; ++k) o << "    s[sw(b | " << ek[k] << "u)] = v[" << k << "];\n";
-    o << "  }\n  __syncthreads();\n";
+    for (int k = 0; k < 16; ++k) o << "    " << el(x, "(b | " + std::to_string(ek[k]) + "u)") << " = v[" << k << "];\n";
+    o << "  }\n";
+    sync_pre(x);
   }
 
   // run of standalone diagonal ops [i, j): element-owner mapping, 4 per thread
   void diag_run(size_t i, size_t j) {
-    o << "  for (u32 e0 = threadIdx.x; e0 < NEL; e0 += 4u * NT) {\n";
+    o << "  for (u32 e0 = threadIdx.x; e0 < LNEL; e0 += 4u * NT) {\n";
     o << "#pragma unroll\n    for (u32 w = 0; w < 4u; ++w) { const u32 e = e0 + w * NT;";
-    o << " if (e < NEL) { const u32 g = G(e); C v = s[sw(e)];\n";
+    o << " if (e < LNEL) { const u32 g = G((RANK << LB) | e); C v = s[sw(e)];\n";
     for (size_t r = i; r < j; ++r)
       o << "      v = cmul(v, " << tload(ops[r], (int)r, didx(ops[r], "g")) << ");\n";
     o << "      s[sw(e)] = v; } }\n  }\n";
   }
 
   int nt = 256;  // threads per CTA (512 for narrow tree levels)
+  int cb = 0;    // cluster tier: log2 CTAs per tile (0 = one CTA per tile)
 
-  std::string build(const std::string& name, int threads) {
+  std::string build(const std::string& name, int threads, int cluster_bits) {
     nt = threads;
+    cb = whole ? 0 : cluster_bits;
     bool heavy = false;
     for (auto& d : ops) heavy = heavy || d.kind == OP_RPASS || (d.kind == OP_DENSE && d.k > 2);
     header(name, nt > 256 ? 1 : (heavy ? 2 : 3));
@@ -270,7 +329,7 @@ struct Gen {
     }
     o << "  __syncthreads();\n";
     o << "#pragma unroll 4\n";
-    o << "  for (u32 e = 2u * threadIdx.x; e < NEL; e += 2u * NT) st2(dst + G(e), s[sw(e)], s[sw(e + 1)]);\n";
+    o << "  for (u32 e = 2u * threadIdx.x; e < LNEL; e += 2u * NT) st2(dst + G((RANK << LB) | e), s[sw(e)], s[sw(e + 1)]);\n";
     o << "}\n";
     return o.str();
   }
@@ -283,6 +342,7 @@ struct Drv {
   CUresult (*funcSetAttribute)(CUfunction, CUfunction_attribute, int) = nullptr;
   CUresult (*launchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
                            CUstream, void**, void**) = nullptr;
+  CUresult (*launchKernelEx)(const CUlaunchConfig*, CUfunction, void**, void**) = nullptr;
 };
 
 template <typename F>
@@ -302,6 +362,7 @@ Drv& drv() {
     load_sym(d.moduleGetFunction, "cuModuleGetFunction");
     load_sym(d.funcSetAttribute, "cuFuncSetAttribute");
     load_sym(d.launchKernel, "cuLaunchKernel");
+    load_sym(d.launchKernelEx, "cuLaunchKernelEx");
   });
   return d;
 }
@@ -343,14 +404,15 @@ std::vector<char> nvrtc_compile(const std::string& src, std::string& log) {
 
 }  // namespace
 
-std::string jit_pass_source(const Half& H, const Pass& ps, bool c64, int threads) {
-  Gen g(H, ps, c64);
-  return std::string(kPrelude) + "\n" + g.build("hsf_jit_pass", threads);
+std::string jit_pass_source(const Half& H, const Pass& ps, bool c64, int threads, int cluster_bits,
+                            const std::vector<cd>* coef) {
+  Gen g(H, ps, c64, coef);
+  return std::string(kPrelude) + "\n" + g.build("hsf_jit_pass", threads, cluster_bits);
 }
 
-size_t jit_smem_bytes(const Pass& ps, bool c64) {
+size_t jit_smem_bytes(const Pass& ps, bool c64, int cluster_bits) {
   const size_t elem = c64 ? 8 : 16;
-  return (elem << ps.t) + (size_t)ps.tbl_elems * elem;
+  return (elem << (ps.t - cluster_bits)) + (size_t)ps.tbl_elems * elem;
 }
 
 std::vector<void*> jit_compile_all(int device, const std::vector<std::string>& sources) {
@@ -397,9 +459,32 @@ std::vector<void*> jit_compile_all(int device, const std::vector<std::string>& s
 }
 
 void jit_launch(void* fn, unsigned gx, unsigned gy, unsigned threads, size_t smem, void* stream,
-                const JitLaunchArgs& a) {
+                const JitLaunchArgs& a, int cluster_bits) {
   JitLaunchArgs args = a;
   void* params[] = {&args};
+  if (cluster_bits > 0) {  // cluster tier: 2^cb CTAs per tile, one (2^cb, 1, 1) cluster each
+    CUlaunchAttribute attr[1];
+    std::memset(attr, 0, sizeof(attr));
+    attr[0].id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
+    attr[0].value.clusterDim.x = 1u << cluster_bits;
+    attr[0].value.clusterDim.y = 1;
+    attr[0].value.clusterDim.z = 1;
+    CUlaunchConfig cfg;
+    std::memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDimX = gx << cluster_bits;
+    cfg.gridDimY = gy;
+    cfg.gridDimZ = 1;
+    cfg.blockDimX = threads;
+    cfg.blockDimY = 1;
+    cfg.blockDimZ = 1;
+    cfg.sharedMemBytes = (unsigned)smem;
+    cfg.hStream = (CUstream)stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (drv().launchKernelEx(&cfg, (CUfunction)fn, params, nullptr) != CUDA_SUCCESS)
+      fail(HSF_ERR_CUDA, "cuLaunchKernelEx (cluster-tier pass) failed");
+    return;
+  }
   if (drv().launchKernel((CUfunction)fn, gx, gy, 1, threads, 1, 1, (unsigned)smem, (CUstream)stream, params, nullptr) !=
       CUDA_SUCCESS)
     fail(HSF_ERR_CUDA, "cuLaunchKernel (specialised pass) failed");

@@ -19,13 +19,15 @@ struct JitLaunchArgs {
 };
 
 // CUDA source of the kernel "hsf_jit_pass" specialised to one tile pass.
-std::string jit_pass_source(const Half& H, const Pass& ps, bool c64, int threads = 256);
+// coef (plan master table, optional): fixed gate matrices become literals
+std::string jit_pass_source(const Half& H, const Pass& ps, bool c64, int threads = 256, int cluster_bits = 0,
+                            const std::vector<cd>* coef = nullptr);
 // dynamic shared memory of that kernel (tile + staged diagonal tables)
-size_t jit_smem_bytes(const Pass& ps, bool c64);
+size_t jit_smem_bytes(const Pass& ps, bool c64, int cluster_bits = 0);
 // NVRTC-compile (cached per device and source, parallel) and load; returns CUfunctions
 std::vector<void*> jit_compile_all(int device, const std::vector<std::string>& sources);
 void jit_launch(void* fn, unsigned gx, unsigned gy, unsigned threads, size_t smem, void* stream,
-                const JitLaunchArgs& a);
+                const JitLaunchArgs& a, int cluster_bits = 0);
 uint64_t jit_source_hash(const std::string& s);
 
 }  // namespace hsf

@@ -78,6 +78,35 @@ __device__ __forceinline__ void r1(C (&v)[16], const C* __restrict__ M) {
   }
 }
 
+// cluster tier helpers: rank in the cluster, generic pointer to the same
+// shared-memory variable in CTA `r` of the cluster (DSMEM), cluster barrier
+__device__ __forceinline__ u32 cluster_rank() {
+  u32 r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+template <typename T>
+__device__ __forceinline__ T* map_rank(T* p, u32 r) {
+  u64 out;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(out) : "l"(reinterpret_cast<u64>(p)), "r"(r));
+  return reinterpret_cast<T*>(out);
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// same with the matrix entries as compile-time literals (fixed gates)
+template <int J, typename C>
+__device__ __forceinline__ void r1c(C (&v)[16], const C m00, const C m01, const C m10, const C m11) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    if (i & (1 << J)) continue;
+    const C a = v[i], b = v[i | (1 << J)];
+    v[i] = cfma(m01, b, cmul(m00, a));
+    v[i | (1 << J)] = cfma(m11, b, cmul(m10, a));
+  }
+}
+
 // insert a zero bit at position P (ascending use: smallest position first)
 template <int P>
 __device__ __forceinline__ u32 ins0(u32 b) {

@@ -40,6 +40,7 @@ struct DeviceState {
   unsigned long long* perm_tab = nullptr;   // caller -> internal index bits (partitions)
   std::vector<void*> jit_fn[2][2];          // [variant][half] per flattened pass
   std::vector<int> jit_nt[2][2];            //   and its threads per CTA
+  std::vector<int> jit_cb[2][2];            //   and its cluster bits (cluster tier, narrow levels)
   void* ws = nullptr;
   size_t ws_bytes = 0;
   // cached per-range path coefficients
@@ -162,10 +163,19 @@ static DeviceState* ensure_device(Plan* P, int device) {
                                                    : P->ranks, 0, tr.level_out);
           for (const auto& ps : tr.passes) {
             const double n_cta = ctas * std::ldexp(1.0, H.m - ps.t);
-            const int nt = n_cta < 2.0 * num_sms() ? 512 : 256;
-            src.push_back(jit_pass_source(H, ps, c64, nt));
+            // very narrow tiled levels: split each tile over a cluster of 2 or
+            // 4 CTAs (DSMEM for the ops on the top tile positions) so more SMs
+            // share one tile's op list; otherwise 512 threads for narrow levels
+            const char* ce = std::getenv("HSF_NO_CLUSTER");
+            const bool tiled = ps.t < H.m && ps.t >= 12 && !(ce && ce[0] == '1');
+            int cb = 0;
+            if (tiled && n_cta * 4 <= num_sms()) cb = 2;
+            else if (tiled && n_cta * 2 <= num_sms()) cb = 1;
+            const int nt = cb ? std::max(128, 1 << (ps.t - cb - 4)) : (n_cta < 2.0 * num_sms() ? 512 : 256);
+            src.push_back(jit_pass_source(H, ps, c64, nt, cb, &P->coef));
             owner.push_back({v, h});
             d->jit_nt[v][h].push_back(nt);
+            d->jit_cb[v][h].push_back(cb);
           }
         }
       }
@@ -440,8 +450,10 @@ static void run_half(const Plan& P, DeviceState* d, int h, const Layout& L, cuda
         if (jf) {
           JitLaunchArgs ja{pp.src, pp.dst, pp.coef, pp.node_first, pp.node_local0, pp.src_first, pp.src_div,
                            pp.tile0};
-          jit_launch((*jf)[pass_ord], (unsigned)tiles, (unsigned)ny, (unsigned)d->jit_nt[L.fold ? 1 : 0][h][pass_ord],
-                     jit_smem_bytes(ps, sizeof(R) == 4), st, ja);
+          const int vi = L.fold ? 1 : 0;
+          const int cb = d->jit_cb[vi][h][pass_ord];
+          jit_launch((*jf)[pass_ord], (unsigned)tiles, (unsigned)ny, (unsigned)d->jit_nt[vi][h][pass_ord],
+                     jit_smem_bytes(ps, sizeof(R) == 4, cb), st, ja, cb);
         } else {
           dim3 grid((unsigned)tiles, (unsigned)ny);
           kern<<<grid, nthr, smem, st>>>(pp);
@@ -826,13 +838,17 @@ size_t hsf_debug_pass_source(const hsf_plan_t* plan, int32_t variant, int32_t ha
                              size_t len) {
   try {
     const Plan* P = reinterpret_cast<const Plan*>(plan);
-    if (!P || half < 0 || half > 1 || variant < 0 || variant > 1 || (variant == 1 && P->fold_u0 < 0)) return 0;
+    const int cbq = (variant >> 2) & 3;  // bits 2-3: cluster-tier variant with 2^cb CTAs per tile
+    variant &= 1;
+    if (!P || half < 0 || half > 1 || variant < 0 || (variant == 1 && P->fold_u0 < 0)) return 0;
     const Half& H = variant ? P->half_fold[half] : P->half[half];
     int k = 0;
     for (const auto& tr : H.trans)
       for (const auto& ps : tr.passes)
         if (k++ == pass) {
-          const std::string s = jit_pass_source(H, ps, P->opts.dtype == HSF_C64);
+          const int nt = cbq ? std::max(128, 1 << (ps.t - cbq - 4)) : 256;
+          const std::string s =
+              jit_pass_source(H, ps, P->opts.dtype == HSF_C64, nt, ps.t < H.m ? cbq : 0, &P->coef);
           if (buf && len) {
             const size_t n = std::min(len - 1, s.size());
             std::memcpy(buf, s.data(), n);
