@@ -163,11 +163,13 @@ static DeviceState* ensure_device(Plan* P, int device) {
                                                    : P->ranks, 0, tr.level_out);
           for (const auto& ps : tr.passes) {
             const double n_cta = ctas * std::ldexp(1.0, H.m - ps.t);
-            // very narrow tiled levels: split each tile over a cluster of 2 or
-            // 4 CTAs (DSMEM for the ops on the top tile positions) so more SMs
-            // share one tile's op list; otherwise 512 threads for narrow levels
-            const char* ce = std::getenv("HSF_NO_CLUSTER");
-            const bool tiled = ps.t < H.m && ps.t >= 12 && !(ce && ce[0] == '1');
+            // Cluster tier (opt-in, HSF_CLUSTER=1): very narrow tiled levels split
+            // each tile over a cluster of 2 or 4 CTAs (DSMEM for the ops on the
+            // top tile positions).  Parity-tested, but measured no faster on c3's
+            // narrow roots (their passes are bound by each thread's op chain, not
+            // by one SM's issue rate), so the default is 512-thread CTAs there.
+            const char* ce = std::getenv("HSF_CLUSTER");
+            const bool tiled = ps.t < H.m && ps.t >= 12 && ce && ce[0] == '1';
             int cb = 0;
             if (tiled && n_cta * 4 <= num_sms()) cb = 2;
             else if (tiled && n_cta * 2 <= num_sms()) cb = 1;

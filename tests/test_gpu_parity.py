@@ -615,3 +615,17 @@ def test_noncontiguous_partition(torch, seed):
     P.run(ob, bitstrings=b)
     torch.cuda.synchronize()
     check(ob.cpu().numpy(), ref[bits.astype(np.int64)], "c128")
+
+
+def test_cluster_tier_optin(torch, monkeypatch):
+    # HSF_CLUSTER=1: narrow tiled levels run as 2/4-CTA clusters sharing one
+    # tile over DSMEM; c3 at full size (narrow roots) against the oracle
+    monkeypatch.setenv("HSF_CLUSTER", "1")
+    inst = make_config("c3")
+    n, g = O.parse_circuit(inst.text)
+    P = O.plan(n, g, inst.n_low, inst.blocks)
+    A, B, c = O.half_states(P, 0, 16)
+    bits = inst.bitstrings[:4096]
+    ref = O.recombine_bits(A, B, c, bits, inst.n_low)
+    got, _ = gpu_bits(torch, inst, bits, path_range=(0, 16))
+    check(got, ref, "c64")
