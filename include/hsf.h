@@ -89,7 +89,11 @@ typedef struct {
   int32_t fold_trailing_diag;    /* 1 (default) => bitstring runs fold trailing all-diagonal
                                     units with no gate after them into a per-sample weight
                                     (the block's diagonal at the sample's bits) instead of
-                                    extending the path tree; results are identical */
+                                    extending the path tree; and full-output tensor-core runs
+                                    fold trailing units whose factors on one half are diagonal
+                                    with no gate of that half after them into that half's
+                                    operand prep (leaf = prefix leaf x diagonal factors);
+                                    results are identical up to rounding */
   int32_t jit;                   /* 1 (default) => every simulator tile pass runs as a kernel
                                     specialised to its op list (generated CUDA, NVRTC for
                                     sm_100a, compiled at the first hsf_run on a device and
@@ -157,6 +161,11 @@ typedef struct {
                                    for all paths (full tree; roofline numerator) */
   double fold_tree_bytes_a, fold_tree_bytes_b; /* same for the folded tree (0 if none) */
   int32_t fold_passes_a, fold_passes_b;        /* device passes of the folded tree (0 if none) */
+  int32_t tail_units_a, tail_units_b;          /* trailing units whose diagonal factors on that half
+                                                  are applied in the full-output operand prep
+                                                  (half-sided fold; 0 = none) */
+  int32_t tail_passes_a, tail_passes_b;        /* device passes of that half's shortened tree */
+  double tail_tree_bytes_a, tail_tree_bytes_b; /* tree_bytes of the shortened trees (0 if none) */
 } hsf_plan_info;
 
 /* Pointers in *info stay valid until hsf_plan_free. */
@@ -216,7 +225,9 @@ size_t hsf_last_error(char* buf, size_t len);
 
 /* Debug/inspection: CUDA source of the specialised kernel of tile pass `pass`
  * (flattened over transitions) of half `half` (0 = A, 1 = B) of tree variant
- * `variant` (0 = full tree, 1 = trailing-diagonal fold).  Copies at most
+ * `variant` (0 = full tree, 1 = bitstring trailing-diagonal fold, 2 = the
+ * half-sided trailing fold of full-output runs; + 4·cb for the cluster tier
+ * with 2^cb CTAs per tile).  Copies at most
  * len-1 bytes + NUL into buf (may be NULL) and returns the full length; 0 if
  * the pass does not exist.  Host only. */
 size_t hsf_debug_pass_source(const hsf_plan_t* plan, int32_t variant, int32_t half, int32_t pass, char* buf,

@@ -53,6 +53,7 @@ struct Params {
   int n_fastest;            // tile raster: 1 => consecutive tiles walk N
   int a_evict_last;         // 1 => A operand loads carry an L2 evict-last hint
   int accumulate;           // 1 => out += D (TMA reduce-add) instead of out = D
+  int b_mn;                 // 1 => B operand stored MN-major ([2*Kpad][nrows_b_pad], see split_b_mn_kernel)
 
   int x3;
   float* out;               // D, row-major, ld = ldo floats
@@ -137,18 +138,27 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
+// MN-major operand, SWIZZLE_128B: 64-element (128 B) rows along M/N, one row
+// per k; LBO = 8 KB between 64-wide MN atoms (TMA boxes of 64 x BK),
+// SBO = 1024 B between 8-row k groups
+__device__ __forceinline__ uint64_t sw128_desc_mn(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(8192 >> 4) << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+constexpr uint32_t kBMajorMN = 1u << 16;  // instruction descriptor: B is MN-major
 // kind::f16 instruction descriptor: D=F32, A=B=BF16, K-major both, N=BN, M=BM
 constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                            ((uint32_t)(BM >> 4) << 24);
 
-__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accum,
+                                         uint32_t idesc = IDESC) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
       "setp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
       "}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accum));
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
@@ -222,10 +232,15 @@ __global__ void __launch_bounds__(THREADS, 1)
           uint8_t* st = smem + s * STAGE_BYTES;
           mbar_expect_tx(&full_bar[s], stage_bytes);
           tma_load_2d_hint(st, &mA_hi, &full_bar[s], kb * BK, mb * BM, a_pol);
-          tma_load_2d(st + 2 * A_TILE, &mB_hi, &full_bar[s], kb * BK, nb * BN);
-          if (p.x3) {
-            tma_load_2d_hint(st + A_TILE, &mA_lo, &full_bar[s], kb * BK, mb * BM, a_pol);
-            tma_load_2d(st + 2 * A_TILE + B_TILE, &mB_lo, &full_bar[s], kb * BK, nb * BN);
+          if (p.x3) tma_load_2d_hint(st + A_TILE, &mA_lo, &full_bar[s], kb * BK, mb * BM, a_pol);
+          if (p.b_mn) {  // four 64(n) x BK(k) boxes per operand
+            for (int j = 0; j < BN / 64; ++j) {
+              tma_load_2d(st + 2 * A_TILE + j * 8192, &mB_hi, &full_bar[s], nb * BN + j * 64, kb * BK);
+              if (p.x3) tma_load_2d(st + 2 * A_TILE + B_TILE + j * 8192, &mB_lo, &full_bar[s], nb * BN + j * 64, kb * BK);
+            }
+          } else {
+            tma_load_2d(st + 2 * A_TILE, &mB_hi, &full_bar[s], kb * BK, nb * BN);
+            if (p.x3) tma_load_2d(st + 2 * A_TILE + B_TILE, &mB_lo, &full_bar[s], kb * BK, nb * BN);
           }
           if (++s == STAGES) {
             s = 0;
@@ -250,13 +265,26 @@ __global__ void __launch_bounds__(THREADS, 1)
           asm volatile("tcgen05.fence::after_thread_sync;");
           const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
           const uint32_t a_hi = st, a_lo = st + A_TILE, b_hi = st + 2 * A_TILE, b_lo = st + 2 * A_TILE + B_TILE;
+          if (p.b_mn) {
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint32_t ko = k * 32;  // 16 bf16 = 32 B inside the 128 B swizzle row
-            mma_bf16(d, sw128_desc(a_hi + ko), sw128_desc(b_hi + ko), (kb | k) ? 1u : 0u);
-            if (p.x3) {
-              mma_bf16(d, sw128_desc(a_hi + ko), sw128_desc(b_lo + ko), 1u);
-              mma_bf16(d, sw128_desc(a_lo + ko), sw128_desc(b_hi + ko), 1u);
+            for (int k = 0; k < BK / 16; ++k) {
+              const uint32_t ko = k * 32, kr = k * 2048;  // B: 16 k rows of 128 B
+              const uint32_t id = IDESC | kBMajorMN;
+              mma_bf16(d, sw128_desc(a_hi + ko), sw128_desc_mn(b_hi + kr), (kb | k) ? 1u : 0u, id);
+              if (p.x3) {
+                mma_bf16(d, sw128_desc(a_hi + ko), sw128_desc_mn(b_lo + kr), 1u, id);
+                mma_bf16(d, sw128_desc(a_lo + ko), sw128_desc_mn(b_hi + kr), 1u, id);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k) {
+              const uint32_t ko = k * 32;  // 16 bf16 = 32 B inside the 128 B swizzle row
+              mma_bf16(d, sw128_desc(a_hi + ko), sw128_desc(b_hi + ko), (kb | k) ? 1u : 0u);
+              if (p.x3) {
+                mma_bf16(d, sw128_desc(a_hi + ko), sw128_desc(b_lo + ko), 1u);
+                mma_bf16(d, sw128_desc(a_lo + ko), sw128_desc(b_hi + ko), 1u);
+              }
             }
           }
           mma_commit(&empty_bar[s]);  // frees the smem stage when these MMAs retire
@@ -373,14 +401,15 @@ __device__ __forceinline__ void tma_load_2sm(void* dst, const CUtensorMap* map, 
       "l"(map), "r"(smem_u32(bar) & kPeerMask), "r"(c0), "r"(c1), "l"(policy)
       : "memory");
 }
-__device__ __forceinline__ void mma2_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
+__device__ __forceinline__ void mma2_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accum,
+                                          uint32_t idesc = IDESC2) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
       "setp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
       "}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(IDESC2), "r"(accum));
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
 }
 __device__ __forceinline__ void mma2_commit_both(uint64_t* bar) {
   asm volatile(
@@ -456,10 +485,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           uint8_t* st = smem + s * STAGE2_BYTES;
           if (rank == 0) mbar_expect_tx(&full_bar[s], 2 * stage_bytes);
           tma_load_2sm(st, &mA_hi, &full_bar[s], kb * BK, arow, a_pol);
-          tma_load_2sm(st + 2 * A_TILE, &mB_hi, &full_bar[s], kb * BK, brow, b_pol);
-          if (p.x3) {
-            tma_load_2sm(st + A_TILE, &mA_lo, &full_bar[s], kb * BK, arow, a_pol);
-            tma_load_2sm(st + 2 * A_TILE + B2_TILE, &mB_lo, &full_bar[s], kb * BK, brow, b_pol);
+          if (p.x3) tma_load_2sm(st + A_TILE, &mA_lo, &full_bar[s], kb * BK, arow, a_pol);
+          if (p.b_mn) {  // two 64(n) x BK(k) boxes per operand half
+            for (int j = 0; j < BN / 128; ++j) {
+              tma_load_2sm(st + 2 * A_TILE + j * 8192, &mB_hi, &full_bar[s], brow + j * 64, kb * BK, b_pol);
+              if (p.x3)
+                tma_load_2sm(st + 2 * A_TILE + B2_TILE + j * 8192, &mB_lo, &full_bar[s], brow + j * 64, kb * BK, b_pol);
+            }
+          } else {
+            tma_load_2sm(st + 2 * A_TILE, &mB_hi, &full_bar[s], kb * BK, brow, b_pol);
+            if (p.x3) tma_load_2sm(st + 2 * A_TILE + B2_TILE, &mB_lo, &full_bar[s], kb * BK, brow, b_pol);
           }
           if (++s == NST) {
             s = 0;
@@ -484,13 +519,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           asm volatile("tcgen05.fence::after_thread_sync;");
           const uint32_t st = smem_u32(smem + s * STAGE2_BYTES);
           const uint32_t a_hi = st, a_lo = st + A_TILE, b_hi = st + 2 * A_TILE, b_lo = st + 2 * A_TILE + B2_TILE;
+          if (p.b_mn) {
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint32_t ko = k * 32;
-            mma2_bf16(d, sw128_desc(a_hi + ko), sw128_desc(b_hi + ko), (kb | k) ? 1u : 0u);
-            if (p.x3) {
-              mma2_bf16(d, sw128_desc(a_hi + ko), sw128_desc(b_lo + ko), 1u);
-              mma2_bf16(d, sw128_desc(a_lo + ko), sw128_desc(b_hi + ko), 1u);
+            for (int k = 0; k < BK / 16; ++k) {
+              const uint32_t ko = k * 32, kr = k * 2048;
+              const uint32_t id = IDESC2 | kBMajorMN;
+              mma2_bf16(d, sw128_desc(a_hi + ko), sw128_desc_mn(b_hi + kr), (kb | k) ? 1u : 0u, id);
+              if (p.x3) {
+                mma2_bf16(d, sw128_desc(a_hi + ko), sw128_desc_mn(b_lo + kr), 1u, id);
+                mma2_bf16(d, sw128_desc(a_lo + ko), sw128_desc_mn(b_hi + kr), 1u, id);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k) {
+              const uint32_t ko = k * 32;
+              mma2_bf16(d, sw128_desc(a_hi + ko), sw128_desc(b_hi + ko), (kb | k) ? 1u : 0u);
+              if (p.x3) {
+                mma2_bf16(d, sw128_desc(a_hi + ko), sw128_desc(b_lo + ko), 1u);
+                mma2_bf16(d, sw128_desc(a_lo + ko), sw128_desc(b_hi + ko), 1u);
+              }
             }
           }
           mma2_commit_both(&empty_bar[s]);  // both CTAs' stage s free once these retire
@@ -579,23 +627,82 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 }
 
 // ----------------------------------------------------------------------- K4
+__device__ __forceinline__ float2 cmul_f(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
 __device__ __forceinline__ void split_bf16(float x, __nv_bfloat16& hi, __nv_bfloat16& lo) {
   hi = __float2bfloat16_rn(x);
   lo = __float2bfloat16_rn(x - __bfloat162float(hi));
 }
 
+// Half-sided trailing fold (plan.cpp, Plan::Tail): the leaf of path p is the
+// tree leaf of p / T times prod_u F_{u,d_u}[i's bits on mask_u], the folded
+// units [u0, U) being the fastest digits of p (n == 0 => no fold, T == 1).
+struct TailParams {
+  int n;
+  int radix[kMaxTail];
+  unsigned mask[kMaxTail];     // half-local support bits of unit u0 + j
+  long long off[kMaxTail];     // digit-0 diagonal of unit u0 + j in the tail table
+  long long stride[kMaxTail];  // digit d_j = (p / stride[j]) % radix[j]
+  long long T;                 // prod of the folded radices
+  long long p0;                // global path of operand column 0
+};
+
+// Per 32-path x 32-amplitude tile: the leaf row of each path and, per folded
+// unit, each path's diagonal (table offset) and each amplitude's index in it
+struct TailTile {
+  long long node[32];
+  int base[kMaxTail][32];
+  int idx[kMaxTail][32];
+};
+
+__device__ __forceinline__ void tail_tile_setup(TailTile& tt, const TailParams& tp, long long pb, long long ib) {
+  const int tid = threadIdx.y * 32 + threadIdx.x;  // 256 threads
+  if (tid < 32) tt.node[tid] = (tp.p0 + pb + tid) / tp.T - tp.p0 / tp.T;
+  for (int e = tid; e < tp.n * 32; e += 256) {
+    const int u = e >> 5, r = e & 31;
+    const long long p = tp.p0 + pb + r;
+    const int d = (int)((p / tp.stride[u]) % tp.radix[u]);
+    tt.base[u][r] = (int)(tp.off[u] + ((long long)d << __popc(tp.mask[u])));
+    const unsigned i = (unsigned)(ib + r);
+    unsigned mk = tp.mask[u], x = 0;
+    for (int j = 0; mk; ++j, mk &= mk - 1) x |= ((i >> (__ffs(mk) - 1)) & 1u) << j;
+    tt.idx[u][r] = (int)x;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ float2 tail_weight(const TailTile& tt, int n, const float2* __restrict__ tab, int r, int c) {
+  float2 w = __ldg(&tab[tt.base[0][r] + tt.idx[0][c]]);
+  for (int u = 1; u < n; ++u) {
+    const float2 f = __ldg(&tab[tt.base[u][r] + tt.idx[u][c]]);
+    w = make_float2(w.x * f.x - w.y * f.y, w.x * f.y + w.y * f.x);
+  }
+  return w;
+}
+
 // A'' rows [0, rows_pad): row i <- (re, im) of c_p * A[p][r0 + i]; zero padding
 __global__ void split_a_kernel(const float2* __restrict__ leaves, const float2* __restrict__ cp,
                                __nv_bfloat162* __restrict__ hi, __nv_bfloat162* __restrict__ lo, long long K,
-                               long long Kpad, long long MA, long long r0, long long rows) {
+                               long long Kpad, long long MA, long long r0, long long rows, const TailParams tp,
+                               const float2* __restrict__ ttab) {
   __shared__ float2 t[32][33];
+  __shared__ TailTile tt;
   const long long i0 = (long long)blockIdx.x * 32, p0 = (long long)blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  if (tp.n) tail_tile_setup(tt, tp, p0, r0 + i0);
   for (int r = ty; r < 32; r += 8) {
     long long p = p0 + r, i = i0 + tx;
     float2 v = make_float2(0.f, 0.f);
     if (p < K && i < rows) {
-      float2 a = leaves[p * MA + r0 + i], c = cp[p];
+      float2 a, c = cp[p];
+      if (tp.n) {
+        a = leaves[tt.node[r] * MA + r0 + i];
+        c = cmul_f(c, tail_weight(tt, tp.n, ttab, r, tx));
+      } else {
+        a = leaves[p * MA + r0 + i];
+      }
       v = make_float2(a.x * c.x - a.y * c.y, a.x * c.y + a.y * c.x);
     }
     t[r][tx] = v;
@@ -614,14 +721,23 @@ __global__ void split_a_kernel(const float2* __restrict__ leaves, const float2* 
 
 // B'' rows [0, 2*MB_pad): row 2j <- (re, -im), row 2j+1 <- (im, re) of B[p][j]
 __global__ void split_b_kernel(const float2* __restrict__ leaves, __nv_bfloat162* __restrict__ hi,
-                               __nv_bfloat162* __restrict__ lo, long long K, long long Kpad, long long MB) {
+                               __nv_bfloat162* __restrict__ lo, long long K, long long Kpad, long long MB,
+                               const TailParams tp, const float2* __restrict__ ttab) {
   __shared__ float2 t[32][33];
   const long long j0 = (long long)blockIdx.x * 32, p0 = (long long)blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;
+  __shared__ TailTile tt;
+  if (tp.n) tail_tile_setup(tt, tp, p0, j0);
   for (int r = ty; r < 32; r += 8) {
     long long p = p0 + r, j = j0 + tx;
     float2 v = make_float2(0.f, 0.f);
-    if (p < K && j < MB) v = leaves[p * MB + j];
+    if (p < K && j < MB) {
+      if (tp.n) {
+        v = cmul_f(leaves[tt.node[r] * MB + j], tail_weight(tt, tp.n, ttab, r, tx));
+      } else {
+        v = leaves[p * MB + j];
+      }
+    }
     t[r][tx] = v;
   }
   __syncthreads();
@@ -639,6 +755,70 @@ __global__ void split_b_kernel(const float2* __restrict__ leaves, __nv_bfloat162
       lo[(2 * j) * Kpad + p] = l0;
       lo[(2 * j + 1) * Kpad + p] = l1;
     }
+  }
+}
+
+// MN-major B'' (p.b_mn): row 2p <- (re, im) of B[p][j] at columns (2j, 2j+1),
+// row 2p+1 <- (-im, re): the same operand as split_b_kernel's, transposed, so
+// each row is one leaf, written elementwise.  One CTA per (path, 512 amplitudes).
+__global__ void split_b_mn_kernel(const float2* __restrict__ leaves, __nv_bfloat16* __restrict__ hi,
+                                  __nv_bfloat16* __restrict__ lo, long long K, long long ldb, long long MB,
+                                  const TailParams tp, const float2* __restrict__ ttab) {
+  __shared__ int base[kMaxTail];
+  __shared__ long long node;
+  const long long p = blockIdx.y;
+  const long long j = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 2;
+  if (tp.n) {
+    if (threadIdx.x < tp.n) {
+      const int u = threadIdx.x;
+      const int d = (int)(((tp.p0 + p) / tp.stride[u]) % tp.radix[u]);
+      base[u] = (int)(tp.off[u] + ((long long)d << __popc(tp.mask[u])));
+    }
+    if (threadIdx.x == 0) node = (tp.p0 + p) / tp.T - tp.p0 / tp.T;
+    __syncthreads();
+  }
+  if (j >= ldb / 2) return;
+  float2 a = make_float2(0.f, 0.f), b = a;
+  if (p < K && j < MB) {
+    const long long row = tp.n ? node : p;
+    if (j + 1 < MB) {
+      const float4 x = *reinterpret_cast<const float4*>(leaves + row * MB + j);
+      a = make_float2(x.x, x.y);
+      b = make_float2(x.z, x.w);
+    } else {
+      a = leaves[row * MB + j];
+    }
+    if (tp.n) {
+      float2 w[2];
+      for (int e = 0; e < 2; ++e) {
+        const unsigned i = (unsigned)(j + e);
+        float2 acc = make_float2(1.f, 0.f);
+        for (int u = 0; u < tp.n; ++u) {
+          unsigned mk = tp.mask[u], x = 0;
+          for (int q = 0; mk; ++q, mk &= mk - 1) x |= ((i >> (__ffs(mk) - 1)) & 1u) << q;
+          acc = cmul_f(acc, __ldg(&ttab[base[u] + x]));
+        }
+        w[e] = acc;
+      }
+      a = cmul_f(a, w[0]);
+      b = cmul_f(b, w[1]);
+    }
+  }
+  __nv_bfloat16 h[8], l[8];
+  split_bf16(a.x, h[0], l[0]);
+  split_bf16(a.y, h[1], l[1]);
+  split_bf16(b.x, h[2], l[2]);
+  split_bf16(b.y, h[3], l[3]);
+  split_bf16(-a.y, h[4], l[4]);
+  split_bf16(a.x, h[5], l[5]);
+  split_bf16(-b.y, h[6], l[6]);
+  split_bf16(b.x, h[7], l[7]);
+  const long long o0 = (2 * p) * ldb + 2 * j, o1 = o0 + ldb;
+  *reinterpret_cast<uint2*>(hi + o0) = *reinterpret_cast<const uint2*>(h);
+  *reinterpret_cast<uint2*>(hi + o1) = *reinterpret_cast<const uint2*>(h + 4);
+  if (lo) {
+    *reinterpret_cast<uint2*>(lo + o0) = *reinterpret_cast<const uint2*>(l);
+    *reinterpret_cast<uint2*>(lo + o1) = *reinterpret_cast<const uint2*>(l + 4);
   }
 }
 
@@ -682,10 +862,12 @@ inline PFN_encodeTiled get_encode() {
   return fn;
 }
 
-inline CUtensorMap make_map(void* base, long long rows, long long cols_bf16, int box_rows) {
+// bf16 [rows][cols_bf16] with row stride ld_bf16 (>= cols; boxes past the
+// extent read zeros), boxes of BK x box_rows, 128B swizzle
+inline CUtensorMap make_map(void* base, long long rows, long long cols_bf16, int box_rows, long long ld_bf16 = 0) {
   CUtensorMap m;
   cuuint64_t dims[2] = {(cuuint64_t)cols_bf16, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)cols_bf16 * 2};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld_bf16 ? ld_bf16 : cols_bf16) * 2};
   cuuint32_t box[2] = {(cuuint32_t)tc::BK, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr,
@@ -722,7 +904,18 @@ inline int num_sms() {
 struct TcBuffers {
   TcDims d;
   __nv_bfloat162 *a_hi, *a_lo, *b_hi, *b_lo;
+  bool b_mn = false;  // B'' stored MN-major: [2*Kpad][nrows_b_pad] bf16
+  long long K = 0;    // paths (operand k extent before padding)
 };
+
+// B operand layout: MN-major (elementwise prep, fusable into half B's last
+// pass) for long K; K-major when the GEMM has <= 2 k-blocks (c4: write-bound,
+// measured 37.2 vs 40.0 ms with MN-major).  HSF_TC_BMN=0/1 forces either.
+inline bool tc_b_mn(long long K) {
+  const char* e = std::getenv("HSF_TC_BMN");
+  if (e && (e[0] == '0' || e[0] == '1')) return e[0] == '1';
+  return 2 * ((K + 31) / 32 * 32) > 2 * tc::BK;
+}
 
 inline TcBuffers tc_buffers(long long K, long long rows, long long MB, bool x3, void* ws, size_t ws_bytes) {
   TcBuffers t;
@@ -738,22 +931,33 @@ inline TcBuffers tc_buffers(long long K, long long rows, long long MB, bool x3, 
   t.b_hi = (__nv_bfloat162*)take(t.d.b_bytes);
   t.a_lo = x3 ? (__nv_bfloat162*)take(t.d.a_bytes) : nullptr;
   t.b_lo = x3 ? (__nv_bfloat162*)take(t.d.b_bytes) : nullptr;
+  t.b_mn = tc_b_mn(K);
+  t.K = K;
   return t;
 }
 
 // K4 for half A (c_p folded) — may run on its own stream
 inline void tc_prep_a(const TcBuffers& t, const float2* leavesA, const float2* cp, long long K, long long MA,
-                      long long r0, long long rows, cudaStream_t st) {
+                      long long r0, long long rows, const tc::TailParams& tp, const float2* ttab, cudaStream_t st) {
   tc::split_a_kernel<<<dim3((unsigned)(t.d.rows_pad / 32), (unsigned)(t.d.Kpad / 32)), dim3(32, 8), 0, st>>>(
-      leavesA, cp, t.a_hi, t.a_lo, K, t.d.Kpad, MA, r0, rows);
+      leavesA, cp, t.a_hi, t.a_lo, K, t.d.Kpad, MA, r0, rows, tp, ttab);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("split_a: ") + cudaGetErrorString(e));
 }
 
 // K4 for half B — may run on its own stream
-inline void tc_prep_b(const TcBuffers& t, const float2* leavesB, long long K, long long MB, cudaStream_t st) {
+inline void tc_prep_b(const TcBuffers& t, const float2* leavesB, long long K, long long MB,
+                      const tc::TailParams& tp, const float2* ttab, cudaStream_t st) {
+  if (t.b_mn) {
+    const long long ldb = t.d.nrows_b_pad;
+    tc::split_b_mn_kernel<<<dim3((unsigned)((ldb / 2 + 255) / 256), (unsigned)t.d.Kpad), 256, 0, st>>>(
+        leavesB, (__nv_bfloat16*)t.b_hi, (__nv_bfloat16*)t.b_lo, K, ldb, MB, tp, ttab);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("split_b_mn: ") + cudaGetErrorString(e));
+    return;
+  }
   tc::split_b_kernel<<<dim3((unsigned)(t.d.nrows_b_pad / 64), (unsigned)(t.d.Kpad / 32)), dim3(32, 8), 0, st>>>(
-      leavesB, t.b_hi, t.b_lo, K, t.d.Kpad, MB);
+      leavesB, t.b_hi, t.b_lo, K, t.d.Kpad, MB, tp, ttab);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("split_b: ") + cudaGetErrorString(e));
 }
@@ -767,15 +971,22 @@ inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row
   const long long rpad = (rows + tc::BM - 1) / tc::BM * tc::BM;
   if (row0 + rpad > t.d.rows_pad) fail(HSF_ERR_INVALID_ARG, "tc_gemm rows out of range");
   CUtensorMap mAh = make_map(t.a_hi + row0 * t.d.Kpad, rpad, kcols, tc::BM);
-  CUtensorMap mBh = make_map(t.b_hi, t.d.nrows_b_pad, kcols, tc::BN);
+  // MN-major B: [2K][2MB] valid of [kcols][nrows_b_pad] storage, 64 x BK
+  // boxes; the padding rows / columns are read as zeros (TMA OOB fill), so
+  // producers need not write them (operand-store passes do not)
+  CUtensorMap mBh = t.b_mn ? make_map(t.b_hi, 2 * t.K, 2 * MB, tc::BK, t.d.nrows_b_pad)
+                           : make_map(t.b_hi, t.d.nrows_b_pad, kcols, tc::BN);
   CUtensorMap mAl = x3 ? make_map(t.a_lo + row0 * t.d.Kpad, rpad, kcols, tc::BM) : mAh;
-  CUtensorMap mBl = x3 ? make_map(t.b_lo, t.d.nrows_b_pad, kcols, tc::BN) : mBh;
+  CUtensorMap mBl = !x3 ? mBh
+                   : t.b_mn ? make_map(t.b_lo, 2 * t.K, 2 * MB, tc::BK, t.d.nrows_b_pad)
+                            : make_map(t.b_lo, t.d.nrows_b_pad, kcols, tc::BN);
   tc::Params p;
   p.num_m = (int)(rpad / tc::BM);
   p.num_n = (int)(t.d.nrows_b_pad / tc::BN);
   p.num_k = (int)(kcols / tc::BK);
   p.x3 = x3 ? 1 : 0;
   p.accumulate = accumulate ? 1 : 0;
+  p.b_mn = t.b_mn ? 1 : 0;
   // M-fastest raster: the ~148 concurrent tiles share one B tile (read once
   // from DRAM) and sweep A; A stays L2-resident (evict-last) when it is small
   // (c4: 64 MiB for hi+lo), while the streaming output stores are evict-first.
@@ -810,8 +1021,8 @@ inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row
       if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("tc2 smem attr: ") + cudaGetErrorString(e));
       attr2 = true;
     }
-    CUtensorMap mBh2 = make_map(t.b_hi, t.d.nrows_b_pad, kcols, tc::BN / 2);
-    CUtensorMap mBl2 = x3 ? make_map(t.b_lo, t.d.nrows_b_pad, kcols, tc::BN / 2) : mBh2;
+    CUtensorMap mBh2 = t.b_mn ? mBh : make_map(t.b_hi, t.d.nrows_b_pad, kcols, tc::BN / 2);
+    CUtensorMap mBl2 = t.b_mn ? mBl : x3 ? make_map(t.b_lo, t.d.nrows_b_pad, kcols, tc::BN / 2) : mBh2;
     p.num_m = (int)((rows + 2 * tc::BM - 1) / (2 * tc::BM));
     const long long tiles = (long long)p.num_m * p.num_n;
     const int grid = 2 * (int)std::min<long long>(tiles, num_sms() / 2);

@@ -58,6 +58,8 @@ constexpr int kSmemTableBytes = 48 * 1024;  // per-pass cap on staged tables
 constexpr int kMaxOpQ = 13;      // widest diagonal op (2^13 entries)
 constexpr int kMaxDenseQ = 5;    // widest dense op in the SMEM kernels
 constexpr int kMaxTrail = 8;     // folded trailing diagonal units (bitstring runs)
+constexpr int kMaxTail = 16;     // half-sided trailing diagonal factors (full-output operand prep)
+constexpr double kTailPrefixBytes = 16.0 * (1 << 20);  // prefix leaves of a half-sided fold
 
 // One operation of a half-circuit program (half-local qubits, LSB-first:
 // q[j] is bit j of the op's local index).
@@ -136,6 +138,18 @@ struct Plan {
   std::vector<uint64_t> trail_mask; // per folded unit: global support bits
   std::vector<int64_t> trail_off;   // per folded unit: offset into trail_tab
   std::vector<cd> trail_tab;        // per folded unit: block diagonal D_u over its support
+  // half-sided trailing fold (full-output tensor-core runs; see build_plan):
+  // units [u0, U) whose half-h factors are diagonal with no gate of half h
+  // after them are applied while the GEMM operand is prepared
+  struct Tail {
+    int u0 = -1;                    // tree depth of half h, -1 => none
+    uint64_t T = 1;                 // product of the folded units' ranks
+    Half half;                      // half h's tree over units [0, u0)
+    std::vector<uint32_t> mask;     // per folded unit: half-local support bits
+    std::vector<int32_t> radix;     // per folded unit: rank
+    std::vector<int64_t> off;       // per folded unit: offset of digit 0 in tail_tab
+  } tail[2];
+  std::vector<cd> tail_tab;         // diagonal factors (X for A, Y for B), 2^|S_h| per digit
   uint64_t hash = 0;
   void* dev = nullptr;              // device state (run.cu)
 };

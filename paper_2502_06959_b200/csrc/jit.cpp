@@ -136,6 +136,7 @@ struct Gen {
     o << "  const long long node_g = a.node_first + blockIdx.y;\n";
     o << "  const C* coef = reinterpret_cast<const C*>(a.coef);\n";
     o << "  C* dst = reinterpret_cast<C*>(a.dst) + (a.node_local0 + blockIdx.y) * " << (1ll << m) << "ll;\n";
+    o << "  (void)dst;\n";
     o << "  const C* src = a.src ? reinterpret_cast<const C*>(a.src) + (node_g / a.src_div - a.src_first) * "
       << (1ll << m) << "ll : nullptr;\n";
     // tile -> state index map
@@ -304,7 +305,7 @@ struct Gen {
   int nt = 256;  // threads per CTA (512 for narrow tree levels)
   int cb = 0;    // cluster tier: log2 CTAs per tile (0 = one CTA per tile)
 
-  std::string build(const std::string& name, int threads, int cluster_bits) {
+  std::string build(const std::string& name, int threads, int cluster_bits, bool operand_store = false) {
     nt = threads;
     cb = whole ? 0 : cluster_bits;
     bool heavy = false;
@@ -329,7 +330,11 @@ struct Gen {
     }
     o << "  __syncthreads();\n";
     o << "#pragma unroll 4\n";
-    o << "  for (u32 e = 2u * threadIdx.x; e < LNEL; e += 2u * NT) st2(dst + G((RANK << LB) | e), s[sw(e)], s[sw(e + 1)]);\n";
+    if (operand_store)
+      o << "  for (u32 e = 2u * threadIdx.x; e < LNEL; e += 2u * NT) st_bop(a, a.node_local0 + blockIdx.y, "
+           "G((RANK << LB) | e), s[sw(e)], s[sw(e + 1)]);\n";
+    else
+      o << "  for (u32 e = 2u * threadIdx.x; e < LNEL; e += 2u * NT) st2(dst + G((RANK << LB) | e), s[sw(e)], s[sw(e + 1)]);\n";
     o << "}\n";
     return o.str();
   }
@@ -405,9 +410,9 @@ std::vector<char> nvrtc_compile(const std::string& src, std::string& log) {
 }  // namespace
 
 std::string jit_pass_source(const Half& H, const Pass& ps, bool c64, int threads, int cluster_bits,
-                            const std::vector<cd>* coef) {
+                            const std::vector<cd>* coef, bool operand_store) {
   Gen g(H, ps, c64, coef);
-  return std::string(kPrelude) + "\n" + g.build("hsf_jit_pass", threads, cluster_bits);
+  return std::string(kPrelude) + "\n" + g.build("hsf_jit_pass", threads, cluster_bits, operand_store);
 }
 
 size_t jit_smem_bytes(const Pass& ps, bool c64, int cluster_bits) {

@@ -16,12 +16,16 @@ struct JitLaunchArgs {
   const void* coef;
   long long node_first, node_local0, src_first, src_div;
   unsigned tile0;
+  void* dst_lo = nullptr;
+  long long ldw = 0;
 };
 
 // CUDA source of the kernel "hsf_jit_pass" specialised to one tile pass.
 // coef (plan master table, optional): fixed gate matrices become literals
+// operand_store: write the MN-major split-bf16 B operand instead of the leaf
+// (JitArgs dst / dst_lo / ldw; row pair 2k, 2k+1 for output node k)
 std::string jit_pass_source(const Half& H, const Pass& ps, bool c64, int threads = 256, int cluster_bits = 0,
-                            const std::vector<cd>* coef = nullptr);
+                            const std::vector<cd>* coef = nullptr, bool operand_store = false);
 // dynamic shared memory of that kernel (tile + staged diagonal tables)
 size_t jit_smem_bytes(const Pass& ps, bool c64, int cluster_bits = 0);
 // NVRTC-compile (cached per device and source, parallel) and load; returns CUfunctions

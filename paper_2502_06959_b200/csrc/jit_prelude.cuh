@@ -20,6 +20,8 @@ struct JitArgs {
   long long src_first;   // global index of the first node of the input level
   long long src_div;     // parent = node_global / src_div
   unsigned tile0;        // tile index of blockIdx.x == 0 (row-restricted leaf passes)
+  void* dst_lo;          // operand-store passes: lo plane of the split-bf16 B operand (nullptr => hi only)
+  long long ldw;         //   and its row stride in 32-bit words (bf16 pairs)
 };
 
 __device__ __forceinline__ int sw(int e) { return e ^ ((e >> 4) & 15); }
@@ -64,6 +66,33 @@ __device__ __forceinline__ void st2(double2* p, double2 a, double2 b) {
   p[0] = a;
   p[1] = b;
 }
+
+// Operand-store passes (half B's last pass of a full-output tensor-core run):
+// instead of the leaf, write rows 2k and 2k+1 of the MN-major split-bf16 B
+// operand -- (re, im) and (-im, re) of each amplitude at word G -- hi plane
+// and, if present, the lo plane (x - bf16(x)), RNE conversions (cvt.rn)
+__device__ __forceinline__ u32 bf2(float lo_half, float hi_half) {
+  u32 d;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi_half), "f"(lo_half));
+  return d;
+}
+__device__ __forceinline__ float bf_lo(u32 d) { return __uint_as_float(d << 16); }
+__device__ __forceinline__ float bf_hi(u32 d) { return __uint_as_float(d & 0xFFFF0000u); }
+__device__ __forceinline__ void st_bop(const JitArgs& a, long long k, u32 g, float2 x, float2 y) {
+  u32* hi = reinterpret_cast<u32*>(a.dst);
+  const long long o0 = 2 * k * a.ldw + g, o1 = o0 + a.ldw;
+  const u32 h0 = bf2(x.x, x.y), h1 = bf2(y.x, y.y), r0 = bf2(-x.y, x.x), r1 = bf2(-y.y, y.x);
+  *reinterpret_cast<uint2*>(hi + o0) = make_uint2(h0, h1);
+  *reinterpret_cast<uint2*>(hi + o1) = make_uint2(r0, r1);
+  if (a.dst_lo) {
+    u32* lo = reinterpret_cast<u32*>(a.dst_lo);
+    *reinterpret_cast<uint2*>(lo + o0) =
+        make_uint2(bf2(x.x - bf_lo(h0), x.y - bf_hi(h0)), bf2(y.x - bf_lo(h1), y.y - bf_hi(h1)));
+    *reinterpret_cast<uint2*>(lo + o1) =
+        make_uint2(bf2(-x.y - bf_lo(r0), x.x - bf_hi(r0)), bf2(-y.y - bf_lo(r1), y.x - bf_hi(r1)));
+  }
+}
+__device__ __forceinline__ void st_bop(const JitArgs&, long long, u32, double2, double2) {}
 
 // 1-qubit gate on register slot J of 16 amplitudes held by one thread
 template <int J, typename C>

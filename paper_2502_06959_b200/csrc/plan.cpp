@@ -1231,6 +1231,50 @@ Plan* build_plan(const char* text, size_t len, int n_low, int64_t n_blocks, cons
       }
     }
   }
+  // Half-sided trailing fold (full-output runs on the tensor cores): when the
+  // last units' half-h factors are diagonal and no gate of half h follows them
+  // (after hoisting), they commute to the end of half h's circuit, so half h's
+  // leaf of path p is its leaf of the prefix path p / T times the product of
+  // those diagonals at the amplitude's support bits (P:104-109 with the
+  // factors moved last).  Half h's tree then stops at level u0 and the
+  // product is taken while the split-bf16 GEMM operand is written.
+  // The shortened tree shares the folded factors' products across siblings no
+  // more, so the fold stops where the prefix leaves fit comfortably in L2
+  // (kTailPrefixBytes): u0 = the deepest such level, or the shallowest level
+  // the half's gates allow if that is deeper.
+  if (opts.fold_trailing_diag && U > 0) {
+    const double elem = (opts.dtype == HSF_C64) ? 8.0 : 16.0;
+    double budget = kTailPrefixBytes;
+    if (const char* e = std::getenv("HSF_TAIL_PREFIX_BYTES")) budget = std::strtod(e, nullptr);  // tests: 0 => longest fold
+    for (int hh = 0; hh < 2; ++hh) {
+      int u_fit = 0;
+      for (int u = 1; u < U; ++u)
+        if ((double)range_prod(P->ranks, 0, u) * std::ldexp(elem, P->half[hh].m) <= budget) u_fit = u;
+      int u0 = std::max({P->half[hh].last_gate_level, U - kMaxTail, u_fit});
+      for (int u = U - 1; u >= u0; --u)
+        if (!P->units[u].diag_route) {
+          u0 = u + 1;
+          break;
+        }
+      if (u0 >= U) continue;
+      Plan::Tail& T = P->tail[hh];
+      T.u0 = u0;
+      T.T = range_prod(P->ranks, u0, U);
+      build_half(*P, hh, order, u0, T.half);
+      const int first = P->half[hh].first_qubit;
+      for (int u = u0; u < U; ++u) {
+        const Unit& un = P->units[u];
+        const std::vector<int>& S = hh == 0 ? un.Sa : un.Sb;
+        const auto& F = hh == 0 ? un.X : un.Y;
+        uint32_t mask = 0;
+        for (int q : S) mask |= 1u << (q - first);
+        T.mask.push_back(mask);
+        T.radix.push_back(un.rank);
+        T.off.push_back((int64_t)P->tail_tab.size());
+        for (const auto& f : F) P->tail_tab.insert(P->tail_tab.end(), f.begin(), f.end());
+      }
+    }
+  }
   // hash
   uint64_t h = 1469598103934665603ull;
   h = fnv(h, &P->n, sizeof(int));
@@ -1240,6 +1284,8 @@ Plan* build_plan(const char* text, size_t len, int n_low, int64_t n_blocks, cons
     h = fnv(h, P->half_fold[s].dev_ops.data(), P->half_fold[s].dev_ops.size() * sizeof(DevOp));
   }
   h = fnv(h, P->trail_tab.data(), P->trail_tab.size() * sizeof(cd));
+  for (int s = 0; s < 2; ++s) h = fnv(h, P->tail[s].half.dev_ops.data(), P->tail[s].half.dev_ops.size() * sizeof(DevOp));
+  h = fnv(h, P->tail_tab.data(), P->tail_tab.size() * sizeof(cd));
   h = fnv(h, P->relabel.data(), P->relabel.size() * sizeof(int));
   h = fnv(h, P->coef.data(), P->coef.size() * sizeof(cd));
   h = fnv(h, P->ranks.data(), P->ranks.size() * sizeof(int32_t));

@@ -35,12 +35,19 @@ struct DeviceState {
   void* coef = nullptr;     // complex table (run dtype)
   DevOp* ops[2] = {nullptr, nullptr};
   DevOp* ops_fold[2] = {nullptr, nullptr};  // trailing-diagonal fold variant
+  DevOp* ops_tail[2] = {nullptr, nullptr};  // half-sided trailing fold variant (full output)
   void* trail = nullptr;                    // folded units' block diagonals (run dtype)
+  void* tail = nullptr;                     // half-sided folded diagonal factors (run dtype)
+  // half B's last pass (full tree) writing the MN-major split-bf16 GEMM
+  // operand directly (full-output tensor-core runs; K4 fused into the leaf pass)
+  void* jit_bop = nullptr;
+  int jit_bop_nt = 256;
   bool jit = false;                         // specialised pass kernels loaded
   unsigned long long* perm_tab = nullptr;   // caller -> internal index bits (partitions)
-  std::vector<void*> jit_fn[2][2];          // [variant][half] per flattened pass
-  std::vector<int> jit_nt[2][2];            //   and its threads per CTA
-  std::vector<int> jit_cb[2][2];            //   and its cluster bits (cluster tier, narrow levels)
+  // [variant: 0 full tree, 1 bitstring fold, 2 half-sided tail][half] per flattened pass
+  std::vector<void*> jit_fn[3][2];
+  std::vector<int> jit_nt[3][2];            //   and its threads per CTA
+  std::vector<int> jit_cb[3][2];            //   and its cluster bits (cluster tier, narrow levels)
   void* ws = nullptr;
   size_t ws_bytes = 0;
   // cached per-range path coefficients
@@ -72,7 +79,10 @@ void destroy_device(Plan* p) {
   cudaFree(d->ops[1]);
   cudaFree(d->ops_fold[0]);
   cudaFree(d->ops_fold[1]);
+  cudaFree(d->ops_tail[0]);
+  cudaFree(d->ops_tail[1]);
   cudaFree(d->trail);
+  cudaFree(d->tail);
   cudaFree(d->perm_tab);
   cudaFree(d->ws);
   cudaFree(d->cp);
@@ -122,18 +132,21 @@ static DeviceState* ensure_device(Plan* P, int device) {
   for (int h = 0; h < 2; ++h) {
     upload_ops(P->half[h], &d->ops[h]);
     if (P->fold_u0 >= 0) upload_ops(P->half_fold[h], &d->ops_fold[h]);
+    if (P->tail[h].u0 >= 0) upload_ops(P->tail[h].half, &d->ops_tail[h]);
   }
-  if (P->fold_u0 >= 0) {
-    const size_t nt = P->trail_tab.size();
-    CK(cudaMalloc(&d->trail, nt * d->elem));
+  auto upload_tab = [&](const std::vector<cd>& tab, void** dst) {
+    const size_t nt = tab.size();
+    CK(cudaMalloc(dst, std::max<size_t>(nt, 1) * d->elem));
     if (c64) {
       std::vector<float2> h(nt);
-      for (size_t i = 0; i < nt; ++i) h[i] = make_float2((float)P->trail_tab[i].real(), (float)P->trail_tab[i].imag());
-      CK(cudaMemcpy(d->trail, h.data(), nt * 8, cudaMemcpyHostToDevice));
+      for (size_t i = 0; i < nt; ++i) h[i] = make_float2((float)tab[i].real(), (float)tab[i].imag());
+      CK(cudaMemcpy(*dst, h.data(), nt * 8, cudaMemcpyHostToDevice));
     } else {
-      CK(cudaMemcpy(d->trail, P->trail_tab.data(), nt * 16, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(*dst, tab.data(), nt * 16, cudaMemcpyHostToDevice));
     }
-  }
+  };
+  if (P->fold_u0 >= 0) upload_tab(P->trail_tab, &d->trail);
+  if (!P->tail_tab.empty()) upload_tab(P->tail_tab, &d->tail);
   if (P->permuted) {
     std::vector<unsigned long long> tab(4 * 65536, 0);
     for (int k = 0; k < 4; ++k)
@@ -152,15 +165,15 @@ static DeviceState* ensure_device(Plan* P, int device) {
     // one specialised kernel per tile pass (jit.cpp), compiled once per process
     std::vector<std::string> src;
     std::vector<std::pair<int, int>> owner;
-    for (int v = 0; v < 2; ++v) {
+    for (int v = 0; v < 3; ++v) {
       if (v == 1 && P->fold_u0 < 0) continue;
       for (int h = 0; h < 2; ++h) {
-        const Half& H = v ? P->half_fold[h] : P->half[h];
+        if (v == 2 && P->tail[h].u0 < 0) continue;
+        const Half& H = v == 0 ? P->half[h] : v == 1 ? P->half_fold[h] : P->tail[h].half;
         for (const auto& tr : H.trans) {
           // narrow levels (few nodes x tiles, e.g. a root that hoisting made
           // heavy) get 512-thread CTAs: twice the threads on the few SMs busy
-          const double ctas = (double)range_prod(v ? std::vector<int32_t>(P->ranks.begin(), P->ranks.begin() + P->fold_u0)
-                                                   : P->ranks, 0, tr.level_out);
+          const double ctas = (double)range_prod(P->ranks, 0, tr.level_out);
           for (const auto& ps : tr.passes) {
             const double n_cta = ctas * std::ldexp(1.0, H.m - ps.t);
             // Cluster tier (opt-in, HSF_CLUSTER=1): very narrow tiled levels split
@@ -182,8 +195,21 @@ static DeviceState* ensure_device(Plan* P, int device) {
         }
       }
     }
+    // operand-store variant of half B's last pass (same launch shape)
+    const Half& HB = P->half[1];
+    const bool bop = c64 && !d->jit_cb[0][1].empty() && d->jit_cb[0][1].back() == 0;
+    if (bop) {
+      d->jit_bop_nt = d->jit_nt[0][1].back();
+      src.push_back(jit_pass_source(HB, HB.trans.back().passes.back(), c64, d->jit_bop_nt, 0, &P->coef, true));
+      owner.push_back({-1, 1});
+    }
     std::vector<void*> fns = jit_compile_all(device, src);
-    for (size_t i = 0; i < fns.size(); ++i) d->jit_fn[owner[i].first][owner[i].second].push_back(fns[i]);
+    for (size_t i = 0; i < fns.size(); ++i) {
+      if (owner[i].first < 0)
+        d->jit_bop = fns[i];
+      else
+        d->jit_fn[owner[i].first][owner[i].second].push_back(fns[i]);
+    }
     d->jit = true;
   }
   for (auto& e : d->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDefault));
@@ -199,11 +225,17 @@ static DeviceState* ensure_device(Plan* P, int device) {
 
 // ----------------------------------------------------------- workspace
 struct Layout {
-  uint64_t p0, p1, K;          // TREE path range (folded runs: full range / fold_T)
+  uint64_t p0, p1, K;          // path range of the path-sum (folded runs: full range / fold_T)
   bool fold = false;           // trailing-diagonal fold active (bitstring runs)
-  int U_tree = 0;              // units in the evaluated tree
+  int U_tree = 0;              // units behind p0, p1 (c_p table)
   std::vector<int32_t> ranks;  // their radices
+  // per half: evaluated tree (0 full, 1 bitstring fold, 2 half-sided tail),
+  // its units' radices and its node range at the leaf level
+  int var[2] = {0, 0};
+  std::vector<int32_t> hranks[2];
+  uint64_t hp0[2] = {0, 0}, hp1[2] = {0, 0};
   const Half* half[2] = {nullptr, nullptr};
+  bool bop = false;            // half B's last pass writes the MN-major GEMM operand (with a JIT kernel)
   bool bits_mode;
   uint64_t r0, r1;
   hsf_precision prec;
@@ -222,8 +254,8 @@ struct Layout {
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 constexpr size_t kHostChunkBytes = (size_t)32 << 20;  // D2H of chunk i overlaps the path-sum of chunk i+1
 
-static uint64_t nodes_at(const Layout& Y, int L, uint64_t p0, uint64_t p1) {
-  uint64_t S = suffix_prod(Y.ranks, L);
+static uint64_t nodes_at(const std::vector<int32_t>& ranks, int L, uint64_t p0, uint64_t p1) {
+  uint64_t S = suffix_prod(ranks, L);
   return (p1 - 1) / S - p0 / S + 1;
 }
 
@@ -245,6 +277,28 @@ static Layout make_layout(const Plan& P, const hsf_run_args& a, size_t elem) {
     L.p1 /= P.fold_T;
   }
   L.K = L.p1 - L.p0;
+  L.prec = a.precision;
+  if (L.prec == HSF_PREC_AUTO) L.prec = (P.opts.dtype == HSF_C64) ? HSF_PREC_BF16X3 : HSF_PREC_SIMT;
+  if (P.opts.dtype == HSF_C128 && L.prec != HSF_PREC_SIMT) fail(HSF_ERR_UNSUPPORTED, "complex128 path-sum is SIMT fp64 only");
+  // half-sided trailing fold: full-output tensor-core runs whose path range
+  // holds whole groups of T consecutive paths (the folded units are the
+  // fastest digits)
+  for (int h = 0; h < 2; ++h) {
+    const Plan::Tail& T = P.tail[h];
+    const bool tail = !L.bits_mode && L.prec != HSF_PREC_SIMT && T.u0 >= 0 && L.p0 % T.T == 0 && L.p1 % T.T == 0;
+    L.var[h] = L.fold ? 1 : tail ? 2 : 0;
+    if (tail) {
+      L.half[h] = &T.half;
+      L.hranks[h].assign(P.ranks.begin(), P.ranks.begin() + T.u0);
+      L.hp0[h] = L.p0 / T.T;
+      L.hp1[h] = L.p1 / T.T;
+    } else {
+      L.hranks[h] = L.ranks;
+      L.hp0[h] = L.p0;
+      L.hp1[h] = L.p1;
+    }
+  }
+  L.bop = !L.bits_mode && L.prec != HSF_PREC_SIMT && P.opts.dtype == HSF_C64 && L.var[1] == 0 && tc_b_mn((long long)L.K);
   if (!L.bits_mode && a.bitstrings) fail(HSF_ERR_INVALID_ARG, "bitstrings given with n_bitstrings == 0");
   if (L.bits_mode && !a.bitstrings) fail(HSF_ERR_INVALID_ARG, "n_bitstrings > 0 but bitstrings is NULL");
   if (L.bits_mode && P.n > 63) fail(HSF_ERR_INVALID_ARG, "bitstring runs need n <= 63");
@@ -253,15 +307,13 @@ static Layout make_layout(const Plan& P, const hsf_run_args& a, size_t elem) {
   L.r1 = a.row_end;
   if (L.r0 == 0 && L.r1 == 0) L.r1 = 1ull << nA;
   if (!L.bits_mode && (L.r0 >= L.r1 || L.r1 > (1ull << nA))) fail(HSF_ERR_INVALID_ARG, "bad row range");
-  L.prec = a.precision;
-  if (L.prec == HSF_PREC_AUTO) L.prec = (P.opts.dtype == HSF_C64) ? HSF_PREC_BF16X3 : HSF_PREC_SIMT;
-  if (P.opts.dtype == HSF_C128 && L.prec != HSF_PREC_SIMT) fail(HSF_ERR_UNSUPPORTED, "complex128 path-sum is SIMT fp64 only");
   size_t off = 0;
   for (int h = 0; h < 2; ++h) {
     const Half& H = *L.half[h];
     const size_t st = (size_t)1 << H.m;
     for (size_t i = 0; i + 1 < H.trans.size(); ++i)
-      L.scratch_elems[h] = std::max(L.scratch_elems[h], (size_t)nodes_at(L, H.trans[i].level_out, L.p0, L.p1) * st);
+      L.scratch_elems[h] =
+          std::max(L.scratch_elems[h], (size_t)nodes_at(L.hranks[h], H.trans[i].level_out, L.hp0[h], L.hp1[h]) * st);
     for (int b = 0; b < 2; ++b) {
       L.off_scratch[h][b] = off;
       off = align_up(off + L.scratch_elems[h] * elem);
@@ -269,7 +321,7 @@ static Layout make_layout(const Plan& P, const hsf_run_args& a, size_t elem) {
   }
   for (int h = 0; h < 2; ++h) {
     L.off_leaves[h] = off;
-    off = align_up(off + ((size_t)L.K << L.half[h]->m) * elem);
+    off = align_up(off + ((size_t)(L.hp1[h] - L.hp0[h]) << L.half[h]->m) * elem);
   }
   if (L.bits_mode) {
     for (int h = 0; h < 2; ++h) {
@@ -370,20 +422,23 @@ template <typename R>
 static void run_half(const Plan& P, DeviceState* d, int h, const Layout& L, cudaStream_t st) {
   using C = typename cplx<R>::T;
   const Half& H = *L.half[h];
-  DevOp* dops = L.fold ? d->ops_fold[h] : d->ops[h];
+  const int var = L.var[h];
+  DevOp* dops = var == 0 ? d->ops[h] : var == 1 ? d->ops_fold[h] : d->ops_tail[h];
+  const std::vector<int32_t>& ranks = L.hranks[h];
+  const uint64_t hp0 = L.hp0[h], hp1 = L.hp1[h];
   char* ws = (char*)d->ws;
   const size_t st_elems = (size_t)1 << H.m;
   const void* prev_buf = nullptr;
   int prev_level = -1;
   size_t pass_ord = 0;
-  const std::vector<void*>* jf = d->jit ? &d->jit_fn[L.fold ? 1 : 0][h] : nullptr;
+  const std::vector<void*>* jf = d->jit ? &d->jit_fn[var][h] : nullptr;
   for (size_t ti = 0; ti < H.trans.size(); ++ti) {
     const Transition& tr = H.trans[ti];
     const bool last = (ti + 1 == H.trans.size());
     void* out = ws + (last ? L.off_leaves[h] : L.off_scratch[h][ti & 1]);
-    const uint64_t S_out = suffix_prod(L.ranks, tr.level_out);
-    const uint64_t first_out = L.p0 / S_out;
-    const uint64_t n_out = (L.p1 - 1) / S_out - first_out + 1;
+    const uint64_t S_out = suffix_prod(ranks, tr.level_out);
+    const uint64_t first_out = hp0 / S_out;
+    const uint64_t n_out = (hp1 - 1) / S_out - first_out + 1;
     for (size_t pi = 0; pi < tr.passes.size(); ++pi, ++pass_ord) {
       const Pass& ps = tr.passes[pi];
       PassParams pp{};
@@ -440,21 +495,28 @@ static void run_half(const Plan& P, DeviceState* d, int h, const Layout& L, cuda
             pp.src = nullptr;
           } else {
             pp.src = prev_buf;
-            const uint64_t S_in = suffix_prod(L.ranks, prev_level);
-            pp.src_first = (long long)(L.p0 / S_in);
-            pp.src_div = (long long)range_prod(L.ranks, prev_level, tr.level_out);
+            const uint64_t S_in = suffix_prod(ranks, prev_level);
+            pp.src_first = (long long)(hp0 / S_in);
+            pp.src_div = (long long)range_prod(ranks, prev_level, tr.level_out);
           }
         } else {  // in place on this level's buffer
           pp.src = out;
           pp.src_first = (long long)first_out;
           pp.src_div = 1;
         }
-        if (jf) {
+        const bool bop = h == 1 && L.bop && d->jit_bop && last && pi + 1 == tr.passes.size();
+        if (bop) {  // K4 fused: write the MN-major split-bf16 B operand instead of the leaves
+          TcBuffers t = tc_buffers((long long)L.K, (long long)(L.r1 - L.r0), 1ll << H.m, L.prec == HSF_PREC_BF16X3,
+                                   ws + L.off_tc, L.tc_bytes);
+          JitLaunchArgs ja{pp.src, t.b_hi, pp.coef, pp.node_first, pp.node_local0, pp.src_first, pp.src_div, pp.tile0,
+                           t.b_lo, t.d.nrows_b_pad / 2};
+          jit_launch(d->jit_bop, (unsigned)tiles, (unsigned)ny, (unsigned)d->jit_bop_nt, jit_smem_bytes(ps, true, 0), st,
+                     ja, 0);
+        } else if (jf) {
           JitLaunchArgs ja{pp.src, pp.dst, pp.coef, pp.node_first, pp.node_local0, pp.src_first, pp.src_div,
                            pp.tile0};
-          const int vi = L.fold ? 1 : 0;
-          const int cb = d->jit_cb[vi][h][pass_ord];
-          jit_launch((*jf)[pass_ord], (unsigned)tiles, (unsigned)ny, (unsigned)d->jit_nt[vi][h][pass_ord],
+          const int cb = d->jit_cb[var][h][pass_ord];
+          jit_launch((*jf)[pass_ord], (unsigned)tiles, (unsigned)ny, (unsigned)d->jit_nt[var][h][pass_ord],
                      jit_smem_bytes(ps, sizeof(R) == 4, cb), st, ja, cb);
         } else {
           dim3 grid((unsigned)tiles, (unsigned)ny);
@@ -487,10 +549,27 @@ static void prep_half(Plan* P, DeviceState* d, const Layout& L, int h, cudaStrea
   } else if (L.prec != HSF_PREC_SIMT) {
     const int nB = P->n_low;
     TcBuffers t = tc_buffers(K, (long long)(L.r1 - L.r0), 1ll << nB, L.prec == HSF_PREC_BF16X3, ws + L.off_tc, L.tc_bytes);
+    tc::TailParams tp{};
+    tp.T = 1;
+    tp.p0 = (long long)L.p0;
+    if (L.var[h] == 2) {
+      const Plan::Tail& T = P->tail[h];
+      tp.n = (int)T.mask.size();
+      tp.T = (long long)T.T;
+      long long stride = 1;
+      for (int u = tp.n - 1; u >= 0; --u) {
+        tp.mask[u] = T.mask[u];
+        tp.radix[u] = T.radix[u];
+        tp.off[u] = T.off[u];
+        tp.stride[u] = stride;
+        stride *= T.radix[u];
+      }
+    }
     if (h == 0)
-      tc_prep_a(t, (const float2*)leaves, (const float2*)d->cp, K, 1ll << m, (long long)L.r0, (long long)(L.r1 - L.r0), st);
-    else
-      tc_prep_b(t, (const float2*)leaves, K, 1ll << m, st);
+      tc_prep_a(t, (const float2*)leaves, (const float2*)d->cp, K, 1ll << m, (long long)L.r0, (long long)(L.r1 - L.r0),
+                tp, (const float2*)d->tail, st);
+    else if (!(L.bop && d->jit_bop))  // else written by half B's last pass
+      tc_prep_b(t, (const float2*)leaves, K, 1ll << m, tp, (const float2*)d->tail, st);
   }
 }
 
@@ -775,6 +854,13 @@ hsf_status hsf_plan_info_get(const hsf_plan_t* plan, hsf_plan_info* info) {
     info->fold_tree_bytes_b = P->fold_u0 >= 0 ? P->half_fold[1].tree_bytes : 0.0;
     info->fold_passes_a = P->fold_u0 >= 0 ? P->half_fold[0].n_passes : 0;
     info->fold_passes_b = P->fold_u0 >= 0 ? P->half_fold[1].n_passes : 0;
+    for (int h = 0; h < 2; ++h) {
+      const Plan::Tail& T = P->tail[h];
+      const int nu = T.u0 >= 0 ? (int)P->units.size() - T.u0 : 0;
+      (h ? info->tail_units_b : info->tail_units_a) = nu;
+      (h ? info->tail_passes_b : info->tail_passes_a) = nu ? T.half.n_passes : 0;
+      (h ? info->tail_tree_bytes_b : info->tail_tree_bytes_a) = nu ? T.half.tree_bytes : 0.0;
+    }
     info->n_joint_blocks = 0;
     for (const auto& un : P->units) info->n_joint_blocks += un.gids.size() > 1 ? 1 : 0;
   })
@@ -841,9 +927,11 @@ size_t hsf_debug_pass_source(const hsf_plan_t* plan, int32_t variant, int32_t ha
   try {
     const Plan* P = reinterpret_cast<const Plan*>(plan);
     const int cbq = (variant >> 2) & 3;  // bits 2-3: cluster-tier variant with 2^cb CTAs per tile
-    variant &= 1;
-    if (!P || half < 0 || half > 1 || variant < 0 || (variant == 1 && P->fold_u0 < 0)) return 0;
-    const Half& H = variant ? P->half_fold[half] : P->half[half];
+    variant &= 3;                        // 0 full tree, 1 bitstring fold, 2 half-sided tail
+    if (!P || half < 0 || half > 1 || variant > 2 || (variant == 1 && P->fold_u0 < 0) ||
+        (variant == 2 && P->tail[half].u0 < 0))
+      return 0;
+    const Half& H = variant == 0 ? P->half[half] : variant == 1 ? P->half_fold[half] : P->tail[half].half;
     int k = 0;
     for (const auto& tr : H.trans)
       for (const auto& ps : tr.passes)

@@ -45,7 +45,10 @@ class _Info(C.Structure):
                 ("plan_hash", C.c_uint64), ("fold_units", C.c_int32),
                 ("n_joint_blocks", C.c_int32), ("tree_bytes_a", C.c_double), ("tree_bytes_b", C.c_double),
                 ("fold_tree_bytes_a", C.c_double), ("fold_tree_bytes_b", C.c_double),
-                ("fold_passes_a", C.c_int32), ("fold_passes_b", C.c_int32)]
+                ("fold_passes_a", C.c_int32), ("fold_passes_b", C.c_int32),
+                ("tail_units_a", C.c_int32), ("tail_units_b", C.c_int32),
+                ("tail_passes_a", C.c_int32), ("tail_passes_b", C.c_int32),
+                ("tail_tree_bytes_a", C.c_double), ("tail_tree_bytes_b", C.c_double)]
 
 
 class _RunArgs(C.Structure):
@@ -167,6 +170,9 @@ class Plan:
         self.tree_bytes = (float(i.tree_bytes_a), float(i.tree_bytes_b))
         self.fold_tree_bytes = (float(i.fold_tree_bytes_a), float(i.fold_tree_bytes_b))
         self.fold_passes = (int(i.fold_passes_a), int(i.fold_passes_b))
+        self.tail_units = (int(i.tail_units_a), int(i.tail_units_b))
+        self.tail_passes = (int(i.tail_passes_a), int(i.tail_passes_b))
+        self.tail_tree_bytes = (float(i.tail_tree_bytes_a), float(i.tail_tree_bytes_b))
 
     def __del__(self):
         h = getattr(self, "_h", None)

@@ -170,6 +170,39 @@ def test_trailing_fold_detection(hsf):
     assert Plan(txt + "h 3\n", 2, []).fold_units == 0
 
 
+def test_half_sided_tail_detection(hsf, monkeypatch):
+    # full-output runs fold, per half, the trailing units whose factors on that
+    # half are diagonal with no gate of that half after them (hoisting moves
+    # commuting gates above them)
+    from paper_2502_06959_b200 import Plan
+    # default: the fold stops where the prefix leaves fit in 16 MiB (c2: 2^9
+    # prefixes x 32 KiB), or where the half's gates end
+    for name, twin, tail in [("c1", True, (1, 1)), ("c2", True, (1, 0)), ("c2", False, (3, 0)),
+                             ("c3", True, (0, 0)), ("c4", True, (0, 0)), ("c5", True, (1, 1))]:
+        inst = make_config(name, twin=twin)
+        assert Plan(inst.text, inst.n_low, inst.blocks).tail_units == tail, name
+    # longest fold the gates allow
+    monkeypatch.setenv("HSF_TAIL_PREFIX_BYTES", "0")
+    for name, twin, tail in [("c1", True, (1, 1)), ("c2", True, (8, 0)), ("c2", False, (12, 0)),
+                             ("c3", True, (0, 0)), ("c4", True, (0, 0)), ("c5", True, (1, 1))]:
+        inst = make_config(name, twin=twin)
+        P = Plan(inst.text, inst.n_low, inst.blocks)
+        assert P.tail_units == tail, name
+        assert Plan(inst.text, inst.n_low, inst.blocks, fold_trailing_diag=False).tail_units == (0, 0)
+    # c2: every A factor is a 1-qubit phase that commutes with all later A gates,
+    # so A's tree is the root alone
+    inst = make_config("c2")
+    assert Plan(inst.text, inst.n_low, inst.blocks).tail_passes[0] == 1
+    txt = "qubits 4\nh 0\nh 1\nh 2\nh 3\ncz 1 2\ncz 0 3\ncz 1 3\n"
+    assert Plan(txt, 2, []).tail_units == (3, 3)
+    # H on qubit 2 (half A) after unit 0 pins A's tree to level 1; H on qubit 3
+    # after every unit blocks A's tail; H on qubit 0 (half B) after unit 1
+    # leaves only unit 2 in B's tail
+    assert Plan(txt + "h 2\n", 2, []).tail_units == (2, 3)
+    assert Plan(txt + "h 3\n", 2, []).tail_units == (0, 3)
+    assert Plan(txt + "h 0\n", 2, []).tail_units == (3, 1)
+
+
 @pytest.mark.parametrize("seed", range(8))
 def test_auto_blocks_match_oracle_finder(hsf, seed):
     # the C++ cascade finder (hsf_plan n_blocks = -1) and the oracle's

@@ -240,8 +240,13 @@ def test_bf16x1_is_lower_precision(torch):
     assert e1 < 2e-2 and e3 < 2e-5 and e3 < e1 / 20, (e1, e3)
 
 
-def test_bf16x3_ragged_rows_and_paths(torch):
-    # K not a multiple of 32, row range not a multiple of 128, 2*MB < 256
+@pytest.mark.parametrize("b_layout", ["auto", "0", "1"])
+def test_bf16x3_ragged_rows_and_paths(torch, b_layout, monkeypatch):
+    # K not a multiple of 32, row range not a multiple of 128, 2*MB < 256;
+    # B operand K-major ("0", split_b), MN-major ("1": split_b_mn, or half B's
+    # last pass writing it) or chosen by K ("auto")
+    if b_layout != "auto":
+        monkeypatch.setenv("HSF_TC_BMN", b_layout)
     inst = make_config("c5", twin=True)
     full, P = gpu_full(torch, inst, precision="simt")
     rows = 1 << P.n_a
@@ -363,6 +368,40 @@ def test_trailing_diagonal_fold(torch, path_range):
         check(got, ref, "c64")
     got, _ = gpu_bits(torch, inst, inst.bitstrings, dtype="c128", path_range=path_range)
     check(got, ref, "c128")
+
+
+@pytest.mark.parametrize("case", ["c2", "c5", "toy", "toy_h2", "toy_h0"])
+@pytest.mark.parametrize("longest", [False, True])
+def test_half_sided_tail_fold(torch, case, longest, monkeypatch):
+    # full-output tensor-core runs apply each half's trailing diagonal factors
+    # in the operand prep (prefix leaf x diagonals) instead of extending that
+    # half's tree; folded and unfolded runs match the oracle's partial sums for
+    # aligned and unaligned path ranges (the latter fall back to the full
+    # tree) and row ranges
+    if longest:  # fold every unit the gates allow (default: stop at L2-sized prefixes)
+        monkeypatch.setenv("HSF_TAIL_PREFIX_BYTES", "0")
+    toy = "qubits 4\nh 0\nh 1\nh 2\nh 3\ncz 1 2\ncz 0 3\ncz 1 3\nrx 0x1.8p-1 2\nrx 0x1.4p-2 0\n"
+    if case.startswith("toy"):
+        from types import SimpleNamespace
+        txt = toy + {"toy": "", "toy_h2": "h 2\n", "toy_h0": "h 0\n"}[case]
+        inst = SimpleNamespace(text=txt, n_low=2, blocks=[], dtype="c64")
+    else:
+        inst = make_config(case, twin=True)
+    n, g = O.parse_circuit(inst.text)
+    P = O.plan(n, g, inst.n_low, inst.blocks)
+    rows = 1 << (n - inst.n_low)
+    ranges = [(None, None), ((0, P.n_paths // 2), (1, rows - 1)), ((1, P.n_paths - 1), None)]
+    for pr, rr in ranges:
+        p0, p1 = pr or (0, P.n_paths)
+        A, B, c = O.half_states(P, p0, p1)
+        ref = O.recombine_full(A, B, c)
+        if rr:
+            ref = ref[rr[0] << inst.n_low:rr[1] << inst.n_low]
+        for fold in (True, False):
+            got, Pg = gpu_full(torch, inst, precision="bf16x3", path_range=pr, row_range=rr,
+                               fold_trailing_diag=fold)
+            assert (sum(Pg.tail_units) > 0) == fold
+            check(got, ref, "c64")
 
 
 @pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
