@@ -164,8 +164,12 @@ typedef struct {
   int32_t tail_units_a, tail_units_b;          /* trailing units whose diagonal factors on that half
                                                   are applied in the full-output operand prep
                                                   (half-sided fold; 0 = none) */
-  int32_t tail_passes_a, tail_passes_b;        /* device passes of that half's shortened tree */
+  int32_t tail_passes_a, tail_passes_b;        /* device passes of that half's shortened tree
+                                                  (head and tail folds) */
   double tail_tree_bytes_a, tail_tree_bytes_b; /* tree_bytes of the shortened trees (0 if none) */
+  int32_t head_units_a, head_units_b;          /* leading units whose factors on that half act on
+                                                  computational-basis qubits: scalars folded into
+                                                  c_p in full-output tensor-core runs (head fold) */
 } hsf_plan_info;
 
 /* Pointers in *info stay valid until hsf_plan_free. */

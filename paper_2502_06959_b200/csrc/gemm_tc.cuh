@@ -53,7 +53,8 @@ struct Params {
   int n_fastest;            // tile raster: 1 => consecutive tiles walk N
   int a_evict_last;         // 1 => A operand loads carry an L2 evict-last hint
   int accumulate;           // 1 => out += D (TMA reduce-add) instead of out = D
-  int b_mn;                 // 1 => B operand stored MN-major ([2*Kpad][nrows_b_pad], see split_b_mn_kernel)
+  int mn;                   // 1 => both operands MN-major (A''^T [2*Kpad][rows_pad], B''^T [2*Kpad][nrows_b_pad];
+                            //      split_a_mn_kernel / split_b_mn_kernel)
 
   int x3;
   float* out;               // D, row-major, ld = ldo floats
@@ -145,7 +146,7 @@ __device__ __forceinline__ uint64_t sw128_desc_mn(uint32_t saddr) {
   return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(8192 >> 4) << 16) | ((uint64_t)(1024 >> 4) << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
-constexpr uint32_t kBMajorMN = 1u << 16;  // instruction descriptor: B is MN-major
+constexpr uint32_t kMajorMN = (1u << 15) | (1u << 16);  // instruction descriptor: A and B MN-major
 // kind::f16 instruction descriptor: D=F32, A=B=BF16, K-major both, N=BN, M=BM
 constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                            ((uint32_t)(BM >> 4) << 24);
@@ -231,14 +232,18 @@ __global__ void __launch_bounds__(THREADS, 1)
           mbar_wait(&empty_bar[s], ph ^ 1);
           uint8_t* st = smem + s * STAGE_BYTES;
           mbar_expect_tx(&full_bar[s], stage_bytes);
-          tma_load_2d_hint(st, &mA_hi, &full_bar[s], kb * BK, mb * BM, a_pol);
-          if (p.x3) tma_load_2d_hint(st + A_TILE, &mA_lo, &full_bar[s], kb * BK, mb * BM, a_pol);
-          if (p.b_mn) {  // four 64(n) x BK(k) boxes per operand
+          if (p.mn) {  // 64(m|n) x BK(k) boxes: two per A operand, four per B operand
+            for (int j = 0; j < BM / 64; ++j) {
+              tma_load_2d_hint(st + j * 8192, &mA_hi, &full_bar[s], mb * BM + j * 64, kb * BK, a_pol);
+              if (p.x3) tma_load_2d_hint(st + A_TILE + j * 8192, &mA_lo, &full_bar[s], mb * BM + j * 64, kb * BK, a_pol);
+            }
             for (int j = 0; j < BN / 64; ++j) {
               tma_load_2d(st + 2 * A_TILE + j * 8192, &mB_hi, &full_bar[s], nb * BN + j * 64, kb * BK);
               if (p.x3) tma_load_2d(st + 2 * A_TILE + B_TILE + j * 8192, &mB_lo, &full_bar[s], nb * BN + j * 64, kb * BK);
             }
           } else {
+            tma_load_2d_hint(st, &mA_hi, &full_bar[s], kb * BK, mb * BM, a_pol);
+            if (p.x3) tma_load_2d_hint(st + A_TILE, &mA_lo, &full_bar[s], kb * BK, mb * BM, a_pol);
             tma_load_2d(st + 2 * A_TILE, &mB_hi, &full_bar[s], kb * BK, nb * BN);
             if (p.x3) tma_load_2d(st + 2 * A_TILE + B_TILE, &mB_lo, &full_bar[s], kb * BK, nb * BN);
           }
@@ -265,15 +270,15 @@ __global__ void __launch_bounds__(THREADS, 1)
           asm volatile("tcgen05.fence::after_thread_sync;");
           const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
           const uint32_t a_hi = st, a_lo = st + A_TILE, b_hi = st + 2 * A_TILE, b_lo = st + 2 * A_TILE + B_TILE;
-          if (p.b_mn) {
+          if (p.mn) {
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
-              const uint32_t ko = k * 32, kr = k * 2048;  // B: 16 k rows of 128 B
-              const uint32_t id = IDESC | kBMajorMN;
-              mma_bf16(d, sw128_desc(a_hi + ko), sw128_desc_mn(b_hi + kr), (kb | k) ? 1u : 0u, id);
+              const uint32_t kr = k * 2048;  // 16 k rows of 128 B
+              const uint32_t id = IDESC | kMajorMN;
+              mma_bf16(d, sw128_desc_mn(a_hi + kr), sw128_desc_mn(b_hi + kr), (kb | k) ? 1u : 0u, id);
               if (p.x3) {
-                mma_bf16(d, sw128_desc(a_hi + ko), sw128_desc_mn(b_lo + kr), 1u, id);
-                mma_bf16(d, sw128_desc(a_lo + ko), sw128_desc_mn(b_hi + kr), 1u, id);
+                mma_bf16(d, sw128_desc_mn(a_hi + kr), sw128_desc_mn(b_lo + kr), 1u, id);
+                mma_bf16(d, sw128_desc_mn(a_lo + kr), sw128_desc_mn(b_hi + kr), 1u, id);
               }
             }
           } else {
@@ -484,15 +489,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           mbar_wait(&empty_bar[s], ph ^ 1);
           uint8_t* st = smem + s * STAGE2_BYTES;
           if (rank == 0) mbar_expect_tx(&full_bar[s], 2 * stage_bytes);
-          tma_load_2sm(st, &mA_hi, &full_bar[s], kb * BK, arow, a_pol);
-          if (p.x3) tma_load_2sm(st + A_TILE, &mA_lo, &full_bar[s], kb * BK, arow, a_pol);
-          if (p.b_mn) {  // two 64(n) x BK(k) boxes per operand half
+          if (p.mn) {  // 64(m|n) x BK(k) boxes: two per A operand, two per B operand half
+            for (int j = 0; j < BM / 64; ++j) {
+              tma_load_2sm(st + j * 8192, &mA_hi, &full_bar[s], arow + j * 64, kb * BK, a_pol);
+              if (p.x3) tma_load_2sm(st + A_TILE + j * 8192, &mA_lo, &full_bar[s], arow + j * 64, kb * BK, a_pol);
+            }
             for (int j = 0; j < BN / 128; ++j) {
               tma_load_2sm(st + 2 * A_TILE + j * 8192, &mB_hi, &full_bar[s], brow + j * 64, kb * BK, b_pol);
               if (p.x3)
                 tma_load_2sm(st + 2 * A_TILE + B2_TILE + j * 8192, &mB_lo, &full_bar[s], brow + j * 64, kb * BK, b_pol);
             }
           } else {
+            tma_load_2sm(st, &mA_hi, &full_bar[s], kb * BK, arow, a_pol);
+            if (p.x3) tma_load_2sm(st + A_TILE, &mA_lo, &full_bar[s], kb * BK, arow, a_pol);
             tma_load_2sm(st + 2 * A_TILE, &mB_hi, &full_bar[s], kb * BK, brow, b_pol);
             if (p.x3) tma_load_2sm(st + 2 * A_TILE + B2_TILE, &mB_lo, &full_bar[s], kb * BK, brow, b_pol);
           }
@@ -519,15 +528,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           asm volatile("tcgen05.fence::after_thread_sync;");
           const uint32_t st = smem_u32(smem + s * STAGE2_BYTES);
           const uint32_t a_hi = st, a_lo = st + A_TILE, b_hi = st + 2 * A_TILE, b_lo = st + 2 * A_TILE + B2_TILE;
-          if (p.b_mn) {
+          if (p.mn) {
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
-              const uint32_t ko = k * 32, kr = k * 2048;
-              const uint32_t id = IDESC2 | kBMajorMN;
-              mma2_bf16(d, sw128_desc(a_hi + ko), sw128_desc_mn(b_hi + kr), (kb | k) ? 1u : 0u, id);
+              const uint32_t kr = k * 2048;
+              const uint32_t id = IDESC2 | kMajorMN;
+              mma2_bf16(d, sw128_desc_mn(a_hi + kr), sw128_desc_mn(b_hi + kr), (kb | k) ? 1u : 0u, id);
               if (p.x3) {
-                mma2_bf16(d, sw128_desc(a_hi + ko), sw128_desc_mn(b_lo + kr), 1u, id);
-                mma2_bf16(d, sw128_desc(a_lo + ko), sw128_desc_mn(b_hi + kr), 1u, id);
+                mma2_bf16(d, sw128_desc_mn(a_hi + kr), sw128_desc_mn(b_lo + kr), 1u, id);
+                mma2_bf16(d, sw128_desc_mn(a_lo + kr), sw128_desc_mn(b_hi + kr), 1u, id);
               }
             }
           } else {
@@ -636,17 +645,23 @@ __device__ __forceinline__ void split_bf16(float x, __nv_bfloat16& hi, __nv_bflo
   lo = __float2bfloat16_rn(x - __bfloat162float(hi));
 }
 
-// Half-sided trailing fold (plan.cpp, Plan::Tail): the leaf of path p is the
-// tree leaf of p / T times prod_u F_{u,d_u}[i's bits on mask_u], the folded
-// units [u0, U) being the fastest digits of p (n == 0 => no fold, T == 1).
+// Half-sided folds (plan.cpp, Plan::Tail): the leaf of path p is the tree leaf
+// ((p / T) mod Tt) times prod_u F_{u,d_u}[i's bits on mask_u], the tail units
+// [u0, U) being the fastest digits of p; head-scalar units [0, v0) are not in
+// the tree (their scalars are in c_p).
 struct TailParams {
   int n;
   int radix[kMaxTail];
   unsigned mask[kMaxTail];     // half-local support bits of unit u0 + j
   long long off[kMaxTail];     // digit-0 diagonal of unit u0 + j in the tail table
   long long stride[kMaxTail];  // digit d_j = (p / stride[j]) % radix[j]
+  int mapped;                  // 1 => half variant active: leaf = ((p / T) mod Tt) - node0 (else leaf = p)
   long long T;                 // prod of the folded radices
+  long long Tt;                // tree paths
+  long long node0;             // first materialised leaf
   long long p0;                // global path of operand column 0
+  const float2* W;             // optional [T][2^m] table of the tail weights (tail_weights_kernel)
+  long long wld;               // its row length 2^m
 };
 
 // Per 32-path x 32-amplitude tile: the leaf row of each path and, per folded
@@ -659,7 +674,7 @@ struct TailTile {
 
 __device__ __forceinline__ void tail_tile_setup(TailTile& tt, const TailParams& tp, long long pb, long long ib) {
   const int tid = threadIdx.y * 32 + threadIdx.x;  // 256 threads
-  if (tid < 32) tt.node[tid] = (tp.p0 + pb + tid) / tp.T - tp.p0 / tp.T;
+  if (tid < 32) tt.node[tid] = ((tp.p0 + pb + tid) / tp.T) % tp.Tt - tp.node0;
   for (int e = tid; e < tp.n * 32; e += 256) {
     const int u = e >> 5, r = e & 31;
     const long long p = tp.p0 + pb + r;
@@ -691,18 +706,15 @@ __global__ void split_a_kernel(const float2* __restrict__ leaves, const float2* 
   __shared__ TailTile tt;
   const long long i0 = (long long)blockIdx.x * 32, p0 = (long long)blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
-  if (tp.n) tail_tile_setup(tt, tp, p0, r0 + i0);
+  if (tp.mapped) tail_tile_setup(tt, tp, p0, r0 + i0);
   for (int r = ty; r < 32; r += 8) {
     long long p = p0 + r, i = i0 + tx;
     float2 v = make_float2(0.f, 0.f);
     if (p < K && i < rows) {
-      float2 a, c = cp[p];
-      if (tp.n) {
-        a = leaves[tt.node[r] * MA + r0 + i];
-        c = cmul_f(c, tail_weight(tt, tp.n, ttab, r, tx));
-      } else {
-        a = leaves[p * MA + r0 + i];
-      }
+      float2 c = cp[p];
+      const float2 a = leaves[(tp.mapped ? tt.node[r] : p) * MA + r0 + i];
+      if (tp.W) c = cmul_f(c, tp.W[((tp.p0 + p) % tp.T) * tp.wld + r0 + i]);
+      else if (tp.n) c = cmul_f(c, tail_weight(tt, tp.n, ttab, r, tx));
       v = make_float2(a.x * c.x - a.y * c.y, a.x * c.y + a.y * c.x);
     }
     t[r][tx] = v;
@@ -727,16 +739,14 @@ __global__ void split_b_kernel(const float2* __restrict__ leaves, __nv_bfloat162
   const long long j0 = (long long)blockIdx.x * 32, p0 = (long long)blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;
   __shared__ TailTile tt;
-  if (tp.n) tail_tile_setup(tt, tp, p0, j0);
+  if (tp.mapped) tail_tile_setup(tt, tp, p0, j0);
   for (int r = ty; r < 32; r += 8) {
     long long p = p0 + r, j = j0 + tx;
     float2 v = make_float2(0.f, 0.f);
     if (p < K && j < MB) {
-      if (tp.n) {
-        v = cmul_f(leaves[tt.node[r] * MB + j], tail_weight(tt, tp.n, ttab, r, tx));
-      } else {
-        v = leaves[p * MB + j];
-      }
+      v = leaves[(tp.mapped ? tt.node[r] : p) * MB + j];
+      if (tp.W) v = cmul_f(v, tp.W[((tp.p0 + p) % tp.T) * tp.wld + j]);
+      else if (tp.n) v = cmul_f(v, tail_weight(tt, tp.n, ttab, r, tx));
     }
     t[r][tx] = v;
   }
@@ -758,67 +768,143 @@ __global__ void split_b_kernel(const float2* __restrict__ leaves, __nv_bfloat162
   }
 }
 
-// MN-major B'' (p.b_mn): row 2p <- (re, im) of B[p][j] at columns (2j, 2j+1),
+// W[t][i] = prod_u F_{u,d_u(t)}[i's bits on mask_u] for the tail digit
+// combinations t in [0, T) (the folded units' digits of p mod T): the split
+// kernels then take one table load per element instead of the per-unit loop
+__global__ void tail_weights_kernel(float2* __restrict__ W, long long wld, const TailParams tp,
+                                    const float2* __restrict__ ttab) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= tp.T * wld) return;
+  const long long t = e / wld;
+  const unsigned i = (unsigned)(e % wld);
+  float2 w = make_float2(1.f, 0.f);
+  for (int u = 0; u < tp.n; ++u) {
+    const int d = (int)((t / tp.stride[u]) % tp.radix[u]);
+    unsigned mk = tp.mask[u], x = 0;
+    for (int q = 0; mk; ++q, mk &= mk - 1) x |= ((i >> (__ffs(mk) - 1)) & 1u) << q;
+    w = cmul_f(w, ttab[tp.off[u] + ((long long)d << __popc(tp.mask[u])) + x]);
+  }
+  W[e] = w;
+}
+
+// MN-major A'' (p.mn): row 2p <- Re, row 2p+1 <- Im of c_p * A[p][r0 + i] over
+// i in [0, rows_pad) (zero past `rows`): split_a_kernel's operand transposed,
+// written elementwise.  One CTA per (path, 2048 rows), 8 rows per thread
+// (16 B stores per plane row).
+__global__ void split_a_mn_kernel(const float2* __restrict__ leaves, const float2* __restrict__ cp,
+                                  __nv_bfloat16* __restrict__ hi, __nv_bfloat16* __restrict__ lo, long long K,
+                                  long long lda, long long MA, long long r0, long long rows, const TailParams tp,
+                                  const float2* __restrict__ ttab) {
+  __shared__ int base[kMaxTail];
+  __shared__ unsigned smask[kMaxTail];
+  __shared__ long long node;
+  const long long p = blockIdx.y;
+  const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (tp.mapped) {
+    if (threadIdx.x < tp.n) {
+      const int u = threadIdx.x;
+      const int d = (int)(((tp.p0 + p) / tp.stride[u]) % tp.radix[u]);
+      base[u] = (int)(tp.off[u] + ((long long)d << __popc(tp.mask[u])));
+      smask[u] = tp.mask[u];
+    }
+    if (threadIdx.x == 0) node = ((tp.p0 + p) / tp.T) % tp.Tt - tp.node0;
+    __syncthreads();
+  }
+  if (i >= lda) return;
+  float re[8], im[8];
+  const float2 c = p < K ? cp[p] : make_float2(0.f, 0.f);
+  const long long row = tp.mapped ? node : p;
+  const float2* __restrict__ wrow = tp.W ? tp.W + ((tp.p0 + p) % tp.T) * tp.wld : nullptr;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    float2 v = make_float2(0.f, 0.f);
+    if (p < K && i + e < rows) {
+      v = cmul_f(leaves[row * MA + r0 + i + e], c);
+      if (tp.W) {
+        v = cmul_f(v, wrow[r0 + i + e]);
+      } else if (tp.n) {
+        const unsigned ii = (unsigned)(r0 + i + e);
+        for (int u = 0; u < tp.n; ++u) {
+          unsigned mk = smask[u], x = 0;
+          for (int q = 0; mk; ++q, mk &= mk - 1) x |= ((ii >> (__ffs(mk) - 1)) & 1u) << q;
+          v = cmul_f(v, __ldg(&ttab[base[u] + x]));
+        }
+      }
+    }
+    re[e] = v.x;
+    im[e] = v.y;
+  }
+  __align__(16) __nv_bfloat16 h[16], l[16];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    split_bf16(re[e], h[e], l[e]);
+    split_bf16(im[e], h[8 + e], l[8 + e]);
+  }
+  const long long o0 = (2 * p) * lda + i, o1 = o0 + lda;
+  *reinterpret_cast<uint4*>(hi + o0) = *reinterpret_cast<const uint4*>(h);
+  *reinterpret_cast<uint4*>(hi + o1) = *reinterpret_cast<const uint4*>(h + 8);
+  if (lo) {
+    *reinterpret_cast<uint4*>(lo + o0) = *reinterpret_cast<const uint4*>(l);
+    *reinterpret_cast<uint4*>(lo + o1) = *reinterpret_cast<const uint4*>(l + 8);
+  }
+}
+
+// MN-major B'' (p.mn): row 2p <- (re, im) of B[p][j] at columns (2j, 2j+1),
 // row 2p+1 <- (-im, re): the same operand as split_b_kernel's, transposed, so
 // each row is one leaf, written elementwise.  One CTA per (path, 512 amplitudes).
 __global__ void split_b_mn_kernel(const float2* __restrict__ leaves, __nv_bfloat16* __restrict__ hi,
                                   __nv_bfloat16* __restrict__ lo, long long K, long long ldb, long long MB,
                                   const TailParams tp, const float2* __restrict__ ttab) {
   __shared__ int base[kMaxTail];
+  __shared__ unsigned smask[kMaxTail];
   __shared__ long long node;
   const long long p = blockIdx.y;
-  const long long j = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 2;
-  if (tp.n) {
+  const long long j = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 4;  // 4 amplitudes per thread
+  if (tp.mapped) {
     if (threadIdx.x < tp.n) {
       const int u = threadIdx.x;
       const int d = (int)(((tp.p0 + p) / tp.stride[u]) % tp.radix[u]);
       base[u] = (int)(tp.off[u] + ((long long)d << __popc(tp.mask[u])));
+      smask[u] = tp.mask[u];
     }
-    if (threadIdx.x == 0) node = (tp.p0 + p) / tp.T - tp.p0 / tp.T;
+    if (threadIdx.x == 0) node = ((tp.p0 + p) / tp.T) % tp.Tt - tp.node0;
     __syncthreads();
   }
-  if (j >= ldb / 2) return;
-  float2 a = make_float2(0.f, 0.f), b = a;
-  if (p < K && j < MB) {
-    const long long row = tp.n ? node : p;
-    if (j + 1 < MB) {
-      const float4 x = *reinterpret_cast<const float4*>(leaves + row * MB + j);
-      a = make_float2(x.x, x.y);
-      b = make_float2(x.z, x.w);
-    } else {
-      a = leaves[row * MB + j];
-    }
-    if (tp.n) {
-      float2 w[2];
-      for (int e = 0; e < 2; ++e) {
-        const unsigned i = (unsigned)(j + e);
-        float2 acc = make_float2(1.f, 0.f);
+  if (2 * j >= ldb) return;
+  float2 v[4];
+  const long long row = tp.mapped ? node : p;
+  const float2* __restrict__ wrow = tp.W ? tp.W + ((tp.p0 + p) % tp.T) * tp.wld : nullptr;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    v[e] = make_float2(0.f, 0.f);
+    if (p < K && j + e < MB) {
+      v[e] = leaves[row * MB + j + e];
+      if (tp.W) {
+        v[e] = cmul_f(v[e], wrow[j + e]);
+      } else if (tp.n) {
+        const unsigned ii = (unsigned)(j + e);
         for (int u = 0; u < tp.n; ++u) {
-          unsigned mk = tp.mask[u], x = 0;
-          for (int q = 0; mk; ++q, mk &= mk - 1) x |= ((i >> (__ffs(mk) - 1)) & 1u) << q;
-          acc = cmul_f(acc, __ldg(&ttab[base[u] + x]));
+          unsigned mk = smask[u], x = 0;
+          for (int q = 0; mk; ++q, mk &= mk - 1) x |= ((ii >> (__ffs(mk) - 1)) & 1u) << q;
+          v[e] = cmul_f(v[e], __ldg(&ttab[base[u] + x]));
         }
-        w[e] = acc;
       }
-      a = cmul_f(a, w[0]);
-      b = cmul_f(b, w[1]);
     }
   }
-  __nv_bfloat16 h[8], l[8];
-  split_bf16(a.x, h[0], l[0]);
-  split_bf16(a.y, h[1], l[1]);
-  split_bf16(b.x, h[2], l[2]);
-  split_bf16(b.y, h[3], l[3]);
-  split_bf16(-a.y, h[4], l[4]);
-  split_bf16(a.x, h[5], l[5]);
-  split_bf16(-b.y, h[6], l[6]);
-  split_bf16(b.x, h[7], l[7]);
+  __align__(16) __nv_bfloat16 h[16], l[16];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    split_bf16(v[e].x, h[2 * e], l[2 * e]);
+    split_bf16(v[e].y, h[2 * e + 1], l[2 * e + 1]);
+    split_bf16(-v[e].y, h[8 + 2 * e], l[8 + 2 * e]);
+    split_bf16(v[e].x, h[8 + 2 * e + 1], l[8 + 2 * e + 1]);
+  }
   const long long o0 = (2 * p) * ldb + 2 * j, o1 = o0 + ldb;
-  *reinterpret_cast<uint2*>(hi + o0) = *reinterpret_cast<const uint2*>(h);
-  *reinterpret_cast<uint2*>(hi + o1) = *reinterpret_cast<const uint2*>(h + 4);
+  *reinterpret_cast<uint4*>(hi + o0) = *reinterpret_cast<const uint4*>(h);
+  *reinterpret_cast<uint4*>(hi + o1) = *reinterpret_cast<const uint4*>(h + 8);
   if (lo) {
-    *reinterpret_cast<uint2*>(lo + o0) = *reinterpret_cast<const uint2*>(l);
-    *reinterpret_cast<uint2*>(lo + o1) = *reinterpret_cast<const uint2*>(l + 4);
+    *reinterpret_cast<uint4*>(lo + o0) = *reinterpret_cast<const uint4*>(l);
+    *reinterpret_cast<uint4*>(lo + o1) = *reinterpret_cast<const uint4*>(l + 8);
   }
 }
 
@@ -904,14 +990,14 @@ inline int num_sms() {
 struct TcBuffers {
   TcDims d;
   __nv_bfloat162 *a_hi, *a_lo, *b_hi, *b_lo;
-  bool b_mn = false;  // B'' stored MN-major: [2*Kpad][nrows_b_pad] bf16
+  bool mn = false;    // operands MN-major: A''^T [2*Kpad][rows_pad], B''^T [2*Kpad][nrows_b_pad] bf16
   long long K = 0;    // paths (operand k extent before padding)
 };
 
-// B operand layout: MN-major (elementwise prep, fusable into half B's last
+// Operand layout: MN-major (elementwise prep, B's fusable into half B's last
 // pass) for long K; K-major when the GEMM has <= 2 k-blocks (c4: write-bound,
-// measured 37.2 vs 40.0 ms with MN-major).  HSF_TC_BMN=0/1 forces either.
-inline bool tc_b_mn(long long K) {
+// measured 37.2 vs 40.0 ms with an MN-major B).  HSF_TC_BMN=0/1 forces either.
+inline bool tc_mn(long long K) {
   const char* e = std::getenv("HSF_TC_BMN");
   if (e && (e[0] == '0' || e[0] == '1')) return e[0] == '1';
   return 2 * ((K + 31) / 32 * 32) > 2 * tc::BK;
@@ -931,7 +1017,7 @@ inline TcBuffers tc_buffers(long long K, long long rows, long long MB, bool x3, 
   t.b_hi = (__nv_bfloat162*)take(t.d.b_bytes);
   t.a_lo = x3 ? (__nv_bfloat162*)take(t.d.a_bytes) : nullptr;
   t.b_lo = x3 ? (__nv_bfloat162*)take(t.d.b_bytes) : nullptr;
-  t.b_mn = tc_b_mn(K);
+  t.mn = tc_mn(K);
   t.K = K;
   return t;
 }
@@ -939,6 +1025,14 @@ inline TcBuffers tc_buffers(long long K, long long rows, long long MB, bool x3, 
 // K4 for half A (c_p folded) — may run on its own stream
 inline void tc_prep_a(const TcBuffers& t, const float2* leavesA, const float2* cp, long long K, long long MA,
                       long long r0, long long rows, const tc::TailParams& tp, const float2* ttab, cudaStream_t st) {
+  if (t.mn) {
+    const long long lda = t.d.rows_pad;
+    tc::split_a_mn_kernel<<<dim3((unsigned)((lda / 8 + 255) / 256), (unsigned)t.d.Kpad), 256, 0, st>>>(
+        leavesA, cp, (__nv_bfloat16*)t.a_hi, (__nv_bfloat16*)t.a_lo, K, lda, MA, r0, rows, tp, ttab);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("split_a_mn: ") + cudaGetErrorString(e));
+    return;
+  }
   tc::split_a_kernel<<<dim3((unsigned)(t.d.rows_pad / 32), (unsigned)(t.d.Kpad / 32)), dim3(32, 8), 0, st>>>(
       leavesA, cp, t.a_hi, t.a_lo, K, t.d.Kpad, MA, r0, rows, tp, ttab);
   cudaError_t e = cudaGetLastError();
@@ -948,9 +1042,9 @@ inline void tc_prep_a(const TcBuffers& t, const float2* leavesA, const float2* c
 // K4 for half B — may run on its own stream
 inline void tc_prep_b(const TcBuffers& t, const float2* leavesB, long long K, long long MB,
                       const tc::TailParams& tp, const float2* ttab, cudaStream_t st) {
-  if (t.b_mn) {
+  if (t.mn) {
     const long long ldb = t.d.nrows_b_pad;
-    tc::split_b_mn_kernel<<<dim3((unsigned)((ldb / 2 + 255) / 256), (unsigned)t.d.Kpad), 256, 0, st>>>(
+    tc::split_b_mn_kernel<<<dim3((unsigned)((ldb / 8 + 255) / 256), (unsigned)t.d.Kpad), 256, 0, st>>>(
         leavesB, (__nv_bfloat16*)t.b_hi, (__nv_bfloat16*)t.b_lo, K, ldb, MB, tp, ttab);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("split_b_mn: ") + cudaGetErrorString(e));
@@ -970,15 +1064,21 @@ inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row
   if (row0 % tc::BM) fail(HSF_ERR_INVALID_ARG, "tc_gemm row offset not tile aligned");
   const long long rpad = (rows + tc::BM - 1) / tc::BM * tc::BM;
   if (row0 + rpad > t.d.rows_pad) fail(HSF_ERR_INVALID_ARG, "tc_gemm rows out of range");
-  CUtensorMap mAh = make_map(t.a_hi + row0 * t.d.Kpad, rpad, kcols, tc::BM);
+  // MN-major A: columns [row0, row0 + rows) of [2K][rows_pad], 64 x BK boxes
+  __nv_bfloat16* a_hi_mn = (__nv_bfloat16*)t.a_hi + row0;
+  __nv_bfloat16* a_lo_mn = x3 ? (__nv_bfloat16*)t.a_lo + row0 : nullptr;
+  CUtensorMap mAh = t.mn ? make_map(a_hi_mn, 2 * t.K, rows, tc::BK, t.d.rows_pad)
+                         : make_map(t.a_hi + row0 * t.d.Kpad, rpad, kcols, tc::BM);
   // MN-major B: [2K][2MB] valid of [kcols][nrows_b_pad] storage, 64 x BK
   // boxes; the padding rows / columns are read as zeros (TMA OOB fill), so
   // producers need not write them (operand-store passes do not)
-  CUtensorMap mBh = t.b_mn ? make_map(t.b_hi, 2 * t.K, 2 * MB, tc::BK, t.d.nrows_b_pad)
+  CUtensorMap mBh = t.mn ? make_map(t.b_hi, 2 * t.K, 2 * MB, tc::BK, t.d.nrows_b_pad)
                            : make_map(t.b_hi, t.d.nrows_b_pad, kcols, tc::BN);
-  CUtensorMap mAl = x3 ? make_map(t.a_lo + row0 * t.d.Kpad, rpad, kcols, tc::BM) : mAh;
+  CUtensorMap mAl = !x3 ? mAh
+                   : t.mn ? make_map(a_lo_mn, 2 * t.K, rows, tc::BK, t.d.rows_pad)
+                          : make_map(t.a_lo + row0 * t.d.Kpad, rpad, kcols, tc::BM);
   CUtensorMap mBl = !x3 ? mBh
-                   : t.b_mn ? make_map(t.b_lo, 2 * t.K, 2 * MB, tc::BK, t.d.nrows_b_pad)
+                   : t.mn ? make_map(t.b_lo, 2 * t.K, 2 * MB, tc::BK, t.d.nrows_b_pad)
                             : make_map(t.b_lo, t.d.nrows_b_pad, kcols, tc::BN);
   tc::Params p;
   p.num_m = (int)(rpad / tc::BM);
@@ -986,7 +1086,7 @@ inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row
   p.num_k = (int)(kcols / tc::BK);
   p.x3 = x3 ? 1 : 0;
   p.accumulate = accumulate ? 1 : 0;
-  p.b_mn = t.b_mn ? 1 : 0;
+  p.mn = t.mn ? 1 : 0;
   // M-fastest raster: the ~148 concurrent tiles share one B tile (read once
   // from DRAM) and sweep A; A stays L2-resident (evict-last) when it is small
   // (c4: 64 MiB for hi+lo), while the streaming output stores are evict-first.
@@ -1021,8 +1121,8 @@ inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row
       if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("tc2 smem attr: ") + cudaGetErrorString(e));
       attr2 = true;
     }
-    CUtensorMap mBh2 = t.b_mn ? mBh : make_map(t.b_hi, t.d.nrows_b_pad, kcols, tc::BN / 2);
-    CUtensorMap mBl2 = t.b_mn ? mBl : x3 ? make_map(t.b_lo, t.d.nrows_b_pad, kcols, tc::BN / 2) : mBh2;
+    CUtensorMap mBh2 = t.mn ? mBh : make_map(t.b_hi, t.d.nrows_b_pad, kcols, tc::BN / 2);
+    CUtensorMap mBl2 = t.mn ? mBl : x3 ? make_map(t.b_lo, t.d.nrows_b_pad, kcols, tc::BN / 2) : mBh2;
     p.num_m = (int)((rows + 2 * tc::BM - 1) / (2 * tc::BM));
     const long long tiles = (long long)p.num_m * p.num_n;
     const int grid = 2 * (int)std::min<long long>(tiles, num_sms() / 2);

@@ -142,9 +142,12 @@ struct Plan {
   // units [u0, U) whose half-h factors are diagonal with no gate of half h
   // after them are applied while the GEMM operand is prepared
   struct Tail {
-    int u0 = -1;                    // tree depth of half h, -1 => none
-    uint64_t T = 1;                 // product of the folded units' ranks
-    Half half;                      // half h's tree over units [0, u0)
+    int u0 = -1;                    // tree depth of half h, -1 => no variant (U => head fold only)
+    int v0 = 0;                     // head-scalar units [0, v0) (radix 1 in this tree)
+    uint64_t T = 1;                 // product of the tail units' ranks
+    uint64_t Tt = 1;                // product of the tree units' ranks [v0, u0)
+    std::vector<std::vector<cd>> head;  // per head unit, per digit: its scalar on half h
+    Half half;                      // half h's tree over units [v0, u0)
     std::vector<uint32_t> mask;     // per folded unit: half-local support bits
     std::vector<int32_t> radix;     // per folded unit: rank
     std::vector<int64_t> off;       // per folded unit: offset of digit 0 in tail_tab

@@ -727,11 +727,81 @@ static void finalize_half(Half& H, size_t elem_bytes) {
   H.dev_ops.swap(out);
 }
 
+// Head fold: while every op of half h so far has kept a qubit in a
+// computational-basis state (diagonal gates, or monomial gates -- one nonzero
+// per column, e.g. X -- on basis qubits), a diagonal Schmidt factor on basis
+// qubits multiplies the half state by the scalar F_{u,d}[bits].  Returns the
+// number v0 of leading units whose half-h factors are such scalars, and each
+// one's diagonal index (LSB = smallest support qubit).  Exact: the factor acts
+// on alpha |b>.
+static int head_units(const Plan& P, int h, const std::vector<SchedItem>& order, std::vector<int64_t>& idx) {
+  const int first = (h == 0) ? P.n_low : 0, m = (h == 0) ? P.n - P.n_low : P.n_low;
+  std::vector<char> cls(m, 1);
+  std::vector<int> bit(m, 0);
+  std::vector<char> cand(P.units.size(), 0);
+  idx.assign(P.units.size(), 0);
+  for (const SchedItem& it : order) {
+    if (it.unit) {
+      const Unit& u = P.units[it.id];
+      const std::vector<int>& S = (h == 0) ? u.Sa : u.Sb;
+      bool all = true;
+      for (int q : S) all = all && cls[q - first];
+      if (u.diag_route && all) {
+        cand[it.id] = 1;
+        int64_t x = 0;
+        for (size_t j = 0; j < S.size(); ++j) x |= (int64_t)bit[S[j] - first] << j;
+        idx[it.id] = x;
+      } else if (!u.diag_route) {
+        for (int q : S) cls[q - first] = 0;
+      }
+      continue;
+    }
+    const Gate& g = P.gates[it.id];
+    bool mine = true;
+    for (int q : g.q) mine = mine && ((h == 0) ? q >= P.n_low : q < P.n_low);
+    if (!mine || g.diag) continue;
+    bool all = true;
+    for (int q : g.q) all = all && cls[q - first];
+    // monomial: exactly one nonzero per column
+    const int D = 1 << g.k;
+    int col_row = -1;
+    bool mono = all;
+    if (all) {
+      int b = 0;  // gate-local input index, q[0] = MSB
+      for (int j = 0; j < g.k; ++j) b = (b << 1) | bit[g.q[j] - first];
+      int nz = 0;
+      for (int r = 0; r < D; ++r)
+        if (g.U[(size_t)r * D + b] != cd(0)) {
+          ++nz;
+          col_row = r;
+        }
+      for (int c = 0; c < D && mono; ++c) {
+        int n = 0;
+        for (int r = 0; r < D; ++r) n += g.U[(size_t)r * D + c] != cd(0);
+        mono = n == 1;
+      }
+      mono = mono && nz == 1;
+    }
+    if (mono) {
+      for (int j = 0; j < g.k; ++j) bit[g.q[j] - first] = (col_row >> (g.k - 1 - j)) & 1;
+    } else {
+      for (int q : g.q) cls[q - first] = 0;
+    }
+  }
+  int v0 = 0;
+  while (v0 < (int)P.units.size() && cand[v0]) ++v0;
+  return v0;
+}
+
 // Builds half h's path-tree program over the first U_tree units (U_tree <
 // n_units only for the trailing-diagonal fold, whose dropped units carry no
 // gate after them).
-static void build_half(Plan& P, int h, const std::vector<SchedItem>& order, int U_tree, Half& H) {
+static void build_half(Plan& P, int h, const std::vector<SchedItem>& order, int U_tree, Half& H, int v0 = 0) {
   const int n_low = P.n_low;
+  // units [0, v0) are scalars on this half (head fold, see head_units): no
+  // factor op, radix 1 in this tree
+  std::vector<int32_t> R = P.ranks;
+  for (int u = 0; u < v0 && u < (int)R.size(); ++u) R[u] = 1;
   H.first_qubit = (h == 0) ? n_low : 0;
   H.m = (h == 0) ? P.n - n_low : n_low;
   if (H.m > 30) fail(HSF_ERR_UNSUPPORTED, "half-states above 30 qubits are not supported (32-bit device indexing)");
@@ -769,7 +839,7 @@ static void build_half(Plan& P, int h, const std::vector<SchedItem>& order, int 
     }
   };
   for (const SchedItem& it : order) {
-    if (it.unit && it.id >= U_tree) continue;  // folded trailing unit (diagonal, nothing after it)
+    if (it.unit && (it.id >= U_tree || it.id < v0)) continue;  // folded trailing / head-scalar unit
     if (it.unit) {
       const Unit& u = P.units[it.id];
       const std::vector<int>& S = (h == 0) ? u.Sa : u.Sb;
@@ -814,7 +884,7 @@ static void build_half(Plan& P, int h, const std::vector<SchedItem>& order, int 
   H.ops.clear();
   H.seg_end.assign(U + 1, 0);
   for (int l = 0; l <= U; ++l) {
-    if (l > 0) H.ops.push_back(factors[l - 1]);
+    if (l > v0) H.ops.push_back(factors[l - 1]);  // head-scalar units have no factor op
     for (auto& op : segs[l]) H.ops.push_back(op);
     H.seg_end[l] = (int64_t)H.ops.size();
   }
@@ -833,7 +903,7 @@ static void build_half(Plan& P, int h, const std::vector<SchedItem>& order, int 
   {
     const double elem = (P.opts.dtype == HSF_C64) ? 8.0 : 16.0;
     const double amps = std::ldexp(1.0, H.m), S = amps * elem;
-    auto nodes = [&](int l) { return (double)range_prod(P.ranks, 0, l); };
+    auto nodes = [&](int l) { return (double)range_prod(R, 0, l); };
     auto cost = [&](int a, int b) {
       const int64_t ob = (a < 0) ? 0 : H.seg_end[a], oe = H.seg_end[b];
       size_t np = 1;
@@ -914,8 +984,8 @@ static void build_half(Plan& P, int h, const std::vector<SchedItem>& order, int 
         DevOp& d = H.dev_ops[i];
         int unit = (int)d.div;
         if (unit >= 0) {
-          d.radix = P.ranks[unit];
-          d.div = (int64_t)range_prod(P.ranks, unit + 1, L);
+          d.radix = R[unit];
+          d.div = (int64_t)range_prod(R, unit + 1, L);
         } else {
           d.radix = 1;
           d.div = 1;
@@ -948,7 +1018,7 @@ static void build_half(Plan& P, int h, const std::vector<SchedItem>& order, int 
   {
     const double S = std::ldexp(1.0, H.m) * (P.opts.dtype == HSF_C64 ? 8.0 : 16.0);
     for (const auto& tr : H.trans) {
-      const double N = (double)range_prod(P.ranks, 0, tr.level_out);
+      const double N = (double)range_prod(R, 0, tr.level_out);
       H.tree_bytes += N * S * (2.0 * (double)tr.passes.size() - (tr.level_in < 0 ? 1.0 : 0.0));
     }
   }
@@ -1242,25 +1312,47 @@ Plan* build_plan(const char* text, size_t len, int n_low, int64_t n_blocks, cons
   // more, so the fold stops where the prefix leaves fit comfortably in L2
   // (kTailPrefixBytes): u0 = the deepest such level, or the shallowest level
   // the half's gates allow if that is deeper.
+  //
+  // Head fold (same runs): leading units whose half-h factors act on basis
+  // qubits are scalars on half h (head_units); they leave half h's tree
+  // (radix 1) and their scalars F_{u,d}[bits] join c_p.  Half h's leaf of
+  // path p is then its tree leaf ((p / T) mod Tt) -- e.g. c2's half B, whose
+  // factors all precede its QFT on the X-prepared basis state, is one state.
   if (opts.fold_trailing_diag && U > 0) {
     const double elem = (opts.dtype == HSF_C64) ? 8.0 : 16.0;
     double budget = kTailPrefixBytes;
     if (const char* e = std::getenv("HSF_TAIL_PREFIX_BYTES")) budget = std::strtod(e, nullptr);  // tests: 0 => longest fold
+    const char* nh = std::getenv("HSF_NO_HEAD_FOLD");
     for (int hh = 0; hh < 2; ++hh) {
+      std::vector<int64_t> hidx;
+      int v0 = (nh && nh[0] == '1') ? 0 : head_units(*P, hh, order, hidx);
+      Half tmp;
+      const Half* base = &P->half[hh];
+      if (v0 > 0) {
+        build_half(*P, hh, order, U, tmp, v0);
+        base = &tmp;
+      }
+      std::vector<int32_t> R = P->ranks;
+      for (int u = 0; u < v0; ++u) R[u] = 1;
       int u_fit = 0;
       for (int u = 1; u < U; ++u)
-        if ((double)range_prod(P->ranks, 0, u) * std::ldexp(elem, P->half[hh].m) <= budget) u_fit = u;
-      int u0 = std::max({P->half[hh].last_gate_level, U - kMaxTail, u_fit});
+        if ((double)range_prod(R, 0, u) * std::ldexp(elem, P->half[hh].m) <= budget) u_fit = u;
+      int u0 = std::max({base->last_gate_level, U - kMaxTail, u_fit, v0});
       for (int u = U - 1; u >= u0; --u)
         if (!P->units[u].diag_route) {
           u0 = u + 1;
           break;
         }
-      if (u0 >= U) continue;
+      if (u0 >= U && v0 == 0) continue;
       Plan::Tail& T = P->tail[hh];
       T.u0 = u0;
+      T.v0 = v0;
       T.T = range_prod(P->ranks, u0, U);
-      build_half(*P, hh, order, u0, T.half);
+      T.Tt = range_prod(P->ranks, v0, u0);
+      if (u0 == U && v0 > 0)
+        T.half = std::move(tmp);
+      else
+        build_half(*P, hh, order, u0, T.half, v0);
       const int first = P->half[hh].first_qubit;
       for (int u = u0; u < U; ++u) {
         const Unit& un = P->units[u];
@@ -1272,6 +1364,14 @@ Plan* build_plan(const char* text, size_t len, int n_low, int64_t n_blocks, cons
         T.radix.push_back(un.rank);
         T.off.push_back((int64_t)P->tail_tab.size());
         for (const auto& f : F) P->tail_tab.insert(P->tail_tab.end(), f.begin(), f.end());
+      }
+      // head scalars: hs[u][d] = F_{u,d}[bits at the factor]
+      for (int u = 0; u < v0; ++u) {
+        const Unit& un = P->units[u];
+        const auto& F = hh == 0 ? un.X : un.Y;
+        std::vector<cd> sc(un.rank);
+        for (int d = 0; d < un.rank; ++d) sc[d] = F[d][(size_t)hidx[u]];
+        T.head.push_back(sc);
       }
     }
   }
@@ -1286,6 +1386,8 @@ Plan* build_plan(const char* text, size_t len, int n_low, int64_t n_blocks, cons
   h = fnv(h, P->trail_tab.data(), P->trail_tab.size() * sizeof(cd));
   for (int s = 0; s < 2; ++s) h = fnv(h, P->tail[s].half.dev_ops.data(), P->tail[s].half.dev_ops.size() * sizeof(DevOp));
   h = fnv(h, P->tail_tab.data(), P->tail_tab.size() * sizeof(cd));
+  for (int s = 0; s < 2; ++s)
+    for (const auto& v : P->tail[s].head) h = fnv(h, v.data(), v.size() * sizeof(cd));
   h = fnv(h, P->relabel.data(), P->relabel.size() * sizeof(int));
   h = fnv(h, P->coef.data(), P->coef.size() * sizeof(cd));
   h = fnv(h, P->ranks.data(), P->ranks.size() * sizeof(int32_t));

@@ -38,6 +38,7 @@ struct DeviceState {
   DevOp* ops_tail[2] = {nullptr, nullptr};  // half-sided trailing fold variant (full output)
   void* trail = nullptr;                    // folded units' block diagonals (run dtype)
   void* tail = nullptr;                     // half-sided folded diagonal factors (run dtype)
+  float2* tailw[2] = {nullptr, nullptr};    // [T][2^m] tail weights per half (tensor-core runs)
   // half B's last pass (full tree) writing the MN-major split-bf16 GEMM
   // operand directly (full-output tensor-core runs; K4 fused into the leaf pass)
   void* jit_bop = nullptr;
@@ -55,6 +56,7 @@ struct DeviceState {
   size_t cp_cap = 0;
   uint64_t cp_p0 = ~0ull, cp_p1 = ~0ull;
   int cp_units = -1;
+  int cp_heads = 0;
   cudaEvent_t ev[6] = {};
   cudaEvent_t ev_t0 = nullptr;              // timing start (ev[0] is the fork event)
   // CUDA graph of the whole run (both streams), replayed while the run's
@@ -83,6 +85,8 @@ void destroy_device(Plan* p) {
   cudaFree(d->ops_tail[1]);
   cudaFree(d->trail);
   cudaFree(d->tail);
+  cudaFree(d->tailw[0]);
+  cudaFree(d->tailw[1]);
   cudaFree(d->perm_tab);
   cudaFree(d->ws);
   cudaFree(d->cp);
@@ -99,6 +103,26 @@ void destroy_device(Plan* p) {
   if (cur >= 0) cudaSetDevice(cur);
   delete d;
   p->dev = nullptr;
+}
+
+// half h's fold variant as seen by the operand-prep kernels (path-range
+// fields p0 / node0 / W filled by the caller)
+static tc::TailParams tail_params(const Plan& P, int h) {
+  const Plan::Tail& T = P.tail[h];
+  tc::TailParams tp{};
+  tp.mapped = 1;
+  tp.n = (int)T.mask.size();
+  tp.T = (long long)T.T;
+  tp.Tt = (long long)T.Tt;
+  long long stride = 1;
+  for (int u = tp.n - 1; u >= 0; --u) {
+    tp.mask[u] = T.mask[u];
+    tp.radix[u] = T.radix[u];
+    tp.off[u] = T.off[u];
+    tp.stride[u] = stride;
+    stride *= T.radix[u];
+  }
+  return tp;
 }
 
 static DeviceState* ensure_device(Plan* P, int device) {
@@ -147,6 +171,20 @@ static DeviceState* ensure_device(Plan* P, int device) {
   };
   if (P->fold_u0 >= 0) upload_tab(P->trail_tab, &d->trail);
   if (!P->tail_tab.empty()) upload_tab(P->tail_tab, &d->tail);
+  // tail weight tables (complex64 tensor-core runs): W[t][i] over the tail
+  // digit combinations, when small (<= 2^22 entries)
+  for (int h = 0; h < 2 && c64; ++h) {
+    const Plan::Tail& T = P->tail[h];
+    const long long wld = 1ll << P->half[h].m;
+    const char* nt = std::getenv("HSF_TAIL_NO_TABLE");  // tests: per-unit weight loop
+    if (T.u0 < 0 || T.mask.empty() || (double)T.T * (double)wld > (double)(1 << 22) || (nt && nt[0] == '1')) continue;
+    CK(cudaMalloc(&d->tailw[h], (size_t)T.T * wld * sizeof(float2)));
+    const tc::TailParams tp = tail_params(*P, h);
+    const long long nel = (long long)T.T * wld;
+    tc::tail_weights_kernel<<<(unsigned)((nel + 255) / 256), 256>>>(d->tailw[h], wld, tp, (const float2*)d->tail);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+  }
   if (P->permuted) {
     std::vector<unsigned long long> tab(4 * 65536, 0);
     for (int k = 0; k < 4; ++k)
@@ -284,21 +322,24 @@ static Layout make_layout(const Plan& P, const hsf_run_args& a, size_t elem) {
   // holds whole groups of T consecutive paths (the folded units are the
   // fastest digits)
   for (int h = 0; h < 2; ++h) {
+    // (head fold: whole periods of T * Tt paths, the tree is evaluated whole)
     const Plan::Tail& T = P.tail[h];
-    const bool tail = !L.bits_mode && L.prec != HSF_PREC_SIMT && T.u0 >= 0 && L.p0 % T.T == 0 && L.p1 % T.T == 0;
+    const uint64_t per = T.v0 > 0 ? T.T * T.Tt : T.T;
+    const bool tail = !L.bits_mode && L.prec != HSF_PREC_SIMT && T.u0 >= 0 && L.p0 % per == 0 && L.p1 % per == 0;
     L.var[h] = L.fold ? 1 : tail ? 2 : 0;
     if (tail) {
       L.half[h] = &T.half;
       L.hranks[h].assign(P.ranks.begin(), P.ranks.begin() + T.u0);
-      L.hp0[h] = L.p0 / T.T;
-      L.hp1[h] = L.p1 / T.T;
+      for (int u = 0; u < T.v0; ++u) L.hranks[h][u] = 1;
+      L.hp0[h] = T.v0 > 0 ? 0 : L.p0 / T.T;
+      L.hp1[h] = T.v0 > 0 ? T.Tt : L.p1 / T.T;
     } else {
       L.hranks[h] = L.ranks;
       L.hp0[h] = L.p0;
       L.hp1[h] = L.p1;
     }
   }
-  L.bop = !L.bits_mode && L.prec != HSF_PREC_SIMT && P.opts.dtype == HSF_C64 && L.var[1] == 0 && tc_b_mn((long long)L.K);
+  L.bop = !L.bits_mode && L.prec != HSF_PREC_SIMT && P.opts.dtype == HSF_C64 && L.var[1] == 0 && tc_mn((long long)L.K);
   if (!L.bits_mode && a.bitstrings) fail(HSF_ERR_INVALID_ARG, "bitstrings given with n_bitstrings == 0");
   if (L.bits_mode && !a.bitstrings) fail(HSF_ERR_INVALID_ARG, "n_bitstrings > 0 but bitstrings is NULL");
   if (L.bits_mode && P.n > 63) fail(HSF_ERR_INVALID_ARG, "bitstring runs need n <= 63");
@@ -386,8 +427,10 @@ static void ensure_ws(DeviceState* d, size_t bytes) {
 
 // c_p = prod_u c_{u,d_u} over the tree's units for tree paths p in [p0, p1),
 // fp64 on the host -> run dtype
-static void ensure_cp(Plan* P, DeviceState* d, uint64_t p0, uint64_t p1, int U_tree, cudaStream_t st) {
-  if (d->cp_p0 == p0 && d->cp_p1 == p1 && d->cp_units == U_tree) return;
+// heads: bit h set => half h's head-scalar units (Plan::Tail::v0) are folded
+// into c_p as well
+static void ensure_cp(Plan* P, DeviceState* d, uint64_t p0, uint64_t p1, int U_tree, int heads, cudaStream_t st) {
+  if (d->cp_p0 == p0 && d->cp_p1 == p1 && d->cp_units == U_tree && d->cp_heads == heads) return;
   const uint64_t K = p1 - p0;
   if (d->cp_cap < K) {
     if (d->cp) CK(cudaFree(d->cp));
@@ -400,7 +443,10 @@ static void ensure_cp(Plan* P, DeviceState* d, uint64_t p0, uint64_t p1, int U_t
     uint64_t x = p;
     cd v = 1.0;
     for (int u = U - 1; u >= 0; --u) {
-      v *= P->units[u].c[x % P->ranks[u]];
+      const int dg = (int)(x % P->ranks[u]);
+      v *= P->units[u].c[dg];
+      for (int h = 0; h < 2; ++h)
+        if (((heads >> h) & 1) && u < P->tail[h].v0) v *= P->tail[h].head[u][dg];
       x /= P->ranks[u];
     }
     c[p - p0] = v;
@@ -416,6 +462,7 @@ static void ensure_cp(Plan* P, DeviceState* d, uint64_t p0, uint64_t p1, int U_t
   d->cp_p0 = p0;
   d->cp_p1 = p1;
   d->cp_units = U_tree;
+  d->cp_heads = heads;
 }
 
 template <typename R>
@@ -549,21 +596,15 @@ static void prep_half(Plan* P, DeviceState* d, const Layout& L, int h, cudaStrea
   } else if (L.prec != HSF_PREC_SIMT) {
     const int nB = P->n_low;
     TcBuffers t = tc_buffers(K, (long long)(L.r1 - L.r0), 1ll << nB, L.prec == HSF_PREC_BF16X3, ws + L.off_tc, L.tc_bytes);
-    tc::TailParams tp{};
-    tp.T = 1;
+    tc::TailParams tp = L.var[h] == 2 ? tail_params(*P, h) : tc::TailParams{};
     tp.p0 = (long long)L.p0;
     if (L.var[h] == 2) {
-      const Plan::Tail& T = P->tail[h];
-      tp.n = (int)T.mask.size();
-      tp.T = (long long)T.T;
-      long long stride = 1;
-      for (int u = tp.n - 1; u >= 0; --u) {
-        tp.mask[u] = T.mask[u];
-        tp.radix[u] = T.radix[u];
-        tp.off[u] = T.off[u];
-        tp.stride[u] = stride;
-        stride *= T.radix[u];
-      }
+      tp.node0 = (long long)L.hp0[h];
+      tp.W = d->tailw[h];
+      tp.wld = 1ll << m;
+    } else {
+      tp.T = 1;
+      tp.Tt = 1;
     }
     if (h == 0)
       tc_prep_a(t, (const float2*)leaves, (const float2*)d->cp, K, 1ll << m, (long long)L.r0, (long long)(L.r1 - L.r0),
@@ -704,7 +745,10 @@ static void run(Plan* P, const hsf_run_args& a) {
   if (a.accumulate && !a.out_on_device) fail(HSF_ERR_INVALID_ARG, "accumulate needs a device output buffer");
   ensure_ws(d, L.total);
   cudaStream_t st = (cudaStream_t)a.cuda_stream;
-  ensure_cp(P, d, L.p0, L.p1, L.U_tree, st);
+  int heads = 0;
+  for (int h = 0; h < 2; ++h)
+    if (L.var[h] == 2 && P->tail[h].v0 > 0) heads |= 1 << h;
+  ensure_cp(P, d, L.p0, L.p1, L.U_tree, heads, st);
   const bool timed = a.phase_ms != nullptr;
   try {
     const char* ng = std::getenv("HSF_NO_GRAPH");
@@ -856,10 +900,12 @@ hsf_status hsf_plan_info_get(const hsf_plan_t* plan, hsf_plan_info* info) {
     info->fold_passes_b = P->fold_u0 >= 0 ? P->half_fold[1].n_passes : 0;
     for (int h = 0; h < 2; ++h) {
       const Plan::Tail& T = P->tail[h];
-      const int nu = T.u0 >= 0 ? (int)P->units.size() - T.u0 : 0;
+      const bool on = T.u0 >= 0;
+      const int nu = on ? (int)P->units.size() - T.u0 : 0;
       (h ? info->tail_units_b : info->tail_units_a) = nu;
-      (h ? info->tail_passes_b : info->tail_passes_a) = nu ? T.half.n_passes : 0;
-      (h ? info->tail_tree_bytes_b : info->tail_tree_bytes_a) = nu ? T.half.tree_bytes : 0.0;
+      (h ? info->head_units_b : info->head_units_a) = on ? T.v0 : 0;
+      (h ? info->tail_passes_b : info->tail_passes_a) = on ? T.half.n_passes : 0;
+      (h ? info->tail_tree_bytes_b : info->tail_tree_bytes_a) = on ? T.half.tree_bytes : 0.0;
     }
     info->n_joint_blocks = 0;
     for (const auto& un : P->units) info->n_joint_blocks += un.gids.size() > 1 ? 1 : 0;

@@ -48,7 +48,8 @@ class _Info(C.Structure):
                 ("fold_passes_a", C.c_int32), ("fold_passes_b", C.c_int32),
                 ("tail_units_a", C.c_int32), ("tail_units_b", C.c_int32),
                 ("tail_passes_a", C.c_int32), ("tail_passes_b", C.c_int32),
-                ("tail_tree_bytes_a", C.c_double), ("tail_tree_bytes_b", C.c_double)]
+                ("tail_tree_bytes_a", C.c_double), ("tail_tree_bytes_b", C.c_double),
+                ("head_units_a", C.c_int32), ("head_units_b", C.c_int32)]
 
 
 class _RunArgs(C.Structure):
@@ -173,6 +174,7 @@ class Plan:
         self.tail_units = (int(i.tail_units_a), int(i.tail_units_b))
         self.tail_passes = (int(i.tail_passes_a), int(i.tail_passes_b))
         self.tail_tree_bytes = (float(i.tail_tree_bytes_a), float(i.tail_tree_bytes_b))
+        self.head_units = (int(i.head_units_a), int(i.head_units_b))
 
     def __del__(self):
         h = getattr(self, "_h", None)

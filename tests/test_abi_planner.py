@@ -203,6 +203,30 @@ def test_half_sided_tail_detection(hsf, monkeypatch):
     assert Plan(txt + "h 0\n", 2, []).tail_units == (3, 1)
 
 
+def test_head_scalar_detection(hsf, monkeypatch):
+    # leading units whose factors act on computational-basis qubits of a half
+    # (only X / diagonal gates before them there) are scalars on that half
+    from paper_2502_06959_b200 import Plan
+    inst = make_config("c2")  # B's 12 factors precede its QFT on the X-prepared input
+    P = Plan(inst.text, inst.n_low, inst.blocks)
+    assert P.head_units == (0, 12) and P.tail_passes[1] == 1
+    for name in ("c1", "c3", "c4", "c5"):  # H / SU(2) layers first: no head
+        inst = make_config(name, twin=True)
+        assert Plan(inst.text, inst.n_low, inst.blocks).head_units == (0, 0), name
+    # B: cz(1,2) and cp(0,3) see basis qubits 1, 0; h 1 ends it before cz(1,3).
+    # A: qubit 3 stays a basis qubit through cz(1,3); h 3 ends it before cz(0,2)
+    t = ("qubits 4\nx 1\nx 3\ncz 1 2\ncp 0x1.8p-1 0 3\nh 1\nh 2\ncz 1 3\nh 0\nh 3\ncz 0 2\n"
+         "rx 0x1.4p-2 1\n")
+    P = Plan(t, 2, [])
+    assert P.n_units == 4 and P.head_units == (3, 2) and P.tail_units == (1, 1)
+    # a superposition gate before the first unit on its qubit ends the head
+    assert Plan("qubits 2\nh 0\ncz 0 1\n", 1, []).head_units == (1, 0)
+    assert Plan("qubits 2\nx 0\ncz 0 1\nh 1\n", 1, []).head_units == (1, 1)
+    assert Plan(t, 2, [], fold_trailing_diag=False).head_units == (0, 0)
+    monkeypatch.setenv("HSF_NO_HEAD_FOLD", "1")
+    assert Plan(t, 2, []).head_units == (0, 0)
+
+
 @pytest.mark.parametrize("seed", range(8))
 def test_auto_blocks_match_oracle_finder(hsf, seed):
     # the C++ cascade finder (hsf_plan n_blocks = -1) and the oracle's

@@ -370,9 +370,9 @@ def test_trailing_diagonal_fold(torch, path_range):
     check(got, ref, "c128")
 
 
-@pytest.mark.parametrize("case", ["c2", "c5", "toy", "toy_h2", "toy_h0"])
-@pytest.mark.parametrize("longest", [False, True])
-def test_half_sided_tail_fold(torch, case, longest, monkeypatch):
+@pytest.mark.parametrize("case", ["c2", "c5", "toy", "toy_h2", "toy_h0", "toy_head", "toy_head_only"])
+@pytest.mark.parametrize("longest,table", [(False, True), (True, True), (True, False)])
+def test_half_sided_tail_fold(torch, case, longest, table, monkeypatch):
     # full-output tensor-core runs apply each half's trailing diagonal factors
     # in the operand prep (prefix leaf x diagonals) instead of extending that
     # half's tree; folded and unfolded runs match the oracle's partial sums for
@@ -380,10 +380,18 @@ def test_half_sided_tail_fold(torch, case, longest, monkeypatch):
     # tree) and row ranges
     if longest:  # fold every unit the gates allow (default: stop at L2-sized prefixes)
         monkeypatch.setenv("HSF_TAIL_PREFIX_BYTES", "0")
+    if not table:  # per-unit weight loop in the split kernels instead of the W[t][i] table
+        monkeypatch.setenv("HSF_TAIL_NO_TABLE", "1")
     toy = "qubits 4\nh 0\nh 1\nh 2\nh 3\ncz 1 2\ncz 0 3\ncz 1 3\nrx 0x1.8p-1 2\nrx 0x1.4p-2 0\n"
+    # toy_head: leading units act on basis qubits of both halves (head fold:
+    # scalars in c_p, leaf = tree leaf (p / T) mod Tt), then a trailing unit
+    head = ("qubits 4\nx 1\nx 3\ncz 1 2\ncp 0x1.8p-1 0 3\nh 1\nh 2\ncz 1 3\nh 0\nh 3\ncz 0 2\n"
+            "rx 0x1.4p-2 1\nrx 0x1.8p-2 2\n")
+    head_only = "qubits 4\nx 0\nx 2\ncz 1 2\ncp 0x1.8p-1 0 3\ncz 0 2\nh 0\nh 1\nh 2\nh 3\nrx 0x1.4p-2 1\n"
     if case.startswith("toy"):
         from types import SimpleNamespace
-        txt = toy + {"toy": "", "toy_h2": "h 2\n", "toy_h0": "h 0\n"}[case]
+        txt = {"toy": toy, "toy_h2": toy + "h 2\n", "toy_h0": toy + "h 0\n", "toy_head": head,
+               "toy_head_only": head_only}[case]
         inst = SimpleNamespace(text=txt, n_low=2, blocks=[], dtype="c64")
     else:
         inst = make_config(case, twin=True)
@@ -400,7 +408,7 @@ def test_half_sided_tail_fold(torch, case, longest, monkeypatch):
         for fold in (True, False):
             got, Pg = gpu_full(torch, inst, precision="bf16x3", path_range=pr, row_range=rr,
                                fold_trailing_diag=fold)
-            assert (sum(Pg.tail_units) > 0) == fold
+            assert (sum(Pg.tail_units) + sum(Pg.head_units) > 0) == fold
             check(got, ref, "c64")
 
 
