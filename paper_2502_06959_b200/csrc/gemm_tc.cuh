@@ -815,6 +815,37 @@ __global__ void split_a_mn_kernel(const float2* __restrict__ leaves, const float
   const float2 c = p < K ? cp[p] : make_float2(0.f, 0.f);
   const long long row = tp.mapped ? node : p;
   const float2* __restrict__ wrow = tp.W ? tp.W + ((tp.p0 + p) % tp.T) * tp.wld : nullptr;
+  if (p < K && i + 8 <= rows && (tp.W || !tp.n)) {
+    // common case: branch-free, all 16 loads in flight together
+    float2 x[8], w[8];
+    const float2* __restrict__ src = leaves + row * MA + r0 + i;
+    if ((r0 & 1) == 0) {  // 16 B loads (L1 wavefronts: 8 B strided loads were 96 % L1-bound)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float4 a4 = *reinterpret_cast<const float4*>(src + 2 * e);
+        x[2 * e] = make_float2(a4.x, a4.y);
+        x[2 * e + 1] = make_float2(a4.z, a4.w);
+        if (tp.W) {
+          const float4 w4 = *reinterpret_cast<const float4*>(wrow + r0 + i + 2 * e);
+          w[2 * e] = make_float2(w4.x, w4.y);
+          w[2 * e + 1] = make_float2(w4.z, w4.w);
+        } else {
+          w[2 * e] = w[2 * e + 1] = make_float2(1.f, 0.f);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) x[e] = src[e];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) w[e] = tp.W ? wrow[r0 + i + e] : make_float2(1.f, 0.f);
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float2 v = cmul_f(cmul_f(x[e], c), w[e]);
+      re[e] = v.x;
+      im[e] = v.y;
+    }
+  } else {
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
     float2 v = make_float2(0.f, 0.f);
@@ -833,6 +864,7 @@ __global__ void split_a_mn_kernel(const float2* __restrict__ leaves, const float
     }
     re[e] = v.x;
     im[e] = v.y;
+  }
   }
   __align__(16) __nv_bfloat16 h[16], l[16];
 #pragma unroll
@@ -874,6 +906,25 @@ __global__ void split_b_mn_kernel(const float2* __restrict__ leaves, __nv_bfloat
   float2 v[4];
   const long long row = tp.mapped ? node : p;
   const float2* __restrict__ wrow = tp.W ? tp.W + ((tp.p0 + p) % tp.T) * tp.wld : nullptr;
+  if (p < K && j + 4 <= MB && (tp.W || !tp.n)) {
+    const float2* __restrict__ src = leaves + row * MB + j;
+    float2 w[4];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const float4 a4 = *reinterpret_cast<const float4*>(src + 2 * e);
+      v[2 * e] = make_float2(a4.x, a4.y);
+      v[2 * e + 1] = make_float2(a4.z, a4.w);
+      if (tp.W) {
+        const float4 w4 = *reinterpret_cast<const float4*>(wrow + j + 2 * e);
+        w[2 * e] = make_float2(w4.x, w4.y);
+        w[2 * e + 1] = make_float2(w4.z, w4.w);
+      } else {
+        w[2 * e] = w[2 * e + 1] = make_float2(1.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) v[e] = cmul_f(v[e], w[e]);
+  } else
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     v[e] = make_float2(0.f, 0.f);
