@@ -416,7 +416,14 @@ def main():
     # the simulator tree (both halves concurrently): algorithmic bytes of its
     # tile passes over this rank's share of the paths / the sim phase
     used_fold = (not full) and P.fold_units > 0
-    tb = P.fold_tree_bytes if used_fold else P.tree_bytes
+    tb = list(P.fold_tree_bytes if used_fold else P.tree_bytes)
+    # full-output tensor-core runs evaluate each half's head/tail-folded tree
+    # when the planner made one (hsf.h fold_trailing_diag)
+    tc_full = full and eff_prec != "simt"
+    halves_var = [tc_full and P.tail_passes[h] > 0 for h in (0, 1)]
+    for h in (0, 1):
+        if halves_var[h]:
+            tb[h] = P.tail_tree_bytes[h]
     sim_ms = max(phase[0], phase[1])
     sim_bytes = (tb[0] + tb[1]) * (K / P.n_paths)
     sim_ach = sim_bytes / (sim_ms * 1e-3) / 1e9
@@ -442,8 +449,14 @@ def main():
     # our kernels per step: simulator passes of both halves, then the path-sum:
     # full output = split_a + split_b + GEMM (SIMT: 1 kernel); bitstrings =
     # 2 transposes + gather (folded tree when the trailing units fold)
-    sim_launches = sum(P.fold_passes) if used_fold else sum(P.passes)
-    n_launch = sim_launches + (1 if (full and eff_prec == "simt") else 3)
+    # (full tensor-core runs: half B's last pass writes the GEMM operand itself
+    # when B has no folded tree and K > 64, see hsf.h / run.cu)
+    if used_fold:
+        sim_launches = sum(P.fold_passes)
+    else:
+        sim_launches = sum(P.tail_passes[h] if halves_var[h] else P.passes[h] for h in (0, 1))
+    fused_b = tc_full and not halves_var[1] and K > 64
+    n_launch = sim_launches + (1 if (full and eff_prec == "simt") else (2 if fused_b else 3))
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "paths/s", "n_gpus": world, "steps": a.steps,
                 "warmup": max(3, a.warmup), "ms_per_step": t_step, "higher_is_better": True, "scaling": "strong",
