@@ -369,12 +369,12 @@ def main():
     eff_prec = ("bf16x3" if inst.dtype == "c64" else "simt") if prec == "auto" else prec
     MA, MB = (rows if full else 1 << (inst.n - inst.n_low)), 1 << inst.n_low
     clk_mhz = peaks.get("clocks_under_load", {}).get("sm_mhz_median", 1305.0)
-    if full and eff_prec in ("bf16x3", "bf16x1"):
-        # executed tensor-core flops: (3 | 1) real GEMMs of rows x 2MB x 2K;
-        # algorithmic bytes: the fp32 output written once (+ bf16 operands)
-        nprod = 3 if eff_prec == "bf16x3" else 1
+    if full and eff_prec in ("bf16x3", "bf16x1", "bf16x6"):
+        # executed tensor-core flops: (6 | 3 | 1) real GEMMs of rows x 2MB x 2K;
+        # algorithmic bytes: the fp32 output written once (+ bf16 operand planes)
+        nprod, planes = {"bf16x6": (6, 3), "bf16x3": (3, 2), "bf16x1": (1, 1)}[eff_prec]
         tflop = nprod * 2.0 * MA * (2 * MB) * (2 * K)
-        obytes = MA * MB * esz + (2 if nprod == 3 else 1) * 4.0 * K * (MA + 2 * MB)
+        obytes = MA * MB * esz + planes * 4.0 * K * (MA + 2 * MB)
         t_tensor, t_hbm = tflop / (bf16 * 1e12), obytes / (hbm * 1e9)
         if t_tensor >= t_hbm:
             ach = tflop / (core_ms * 1e-3) / 1e12

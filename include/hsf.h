@@ -68,7 +68,9 @@ typedef enum {
   HSF_PREC_SIMT = 1,    /* CUDA-core FMA in the plan dtype (fp32 / fp64) */
   HSF_PREC_BF16X3 = 2,  /* tcgen05 bf16 MMA, fp32 accumulate in TMEM, operands
                            split hi+lo, 3 products (hi*hi + hi*lo + lo*hi) */
-  HSF_PREC_BF16X1 = 3   /* tcgen05 bf16 MMA, single product (error study only) */
+  HSF_PREC_BF16X1 = 3,  /* tcgen05 bf16 MMA, single product (error study only) */
+  HSF_PREC_BF16X6 = 4   /* tcgen05 bf16 MMA, operands split hi+lo+lo2, 6 products
+                           (+ lo*lo + hi*lo2 + lo2*hi): ~fp32 accuracy, 2x the MMA work */
 } hsf_precision;
 
 typedef struct {

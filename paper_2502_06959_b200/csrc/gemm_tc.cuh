@@ -58,6 +58,7 @@ struct Params {
                             //      split_a_mn_kernel / split_b_mn_kernel)
 
   int x3;
+  int x6;                   // bf16x6: third operand plane (lo2), 6 products (pair kernel only)
   float* out;               // D, row-major, ld = ldo floats
   long long ldo;
   long long rows, cols;     // valid D extent (rows of this call, 2*MB)
@@ -391,7 +392,9 @@ __global__ void __launch_bounds__(THREADS, 1)
 // thread of both CTAs arrives on the leader's accumulator-empty barrier.
 constexpr int B2_TILE = (BN / 2) * BK * 2;               // 16 KB: this CTA's half of B
 constexpr int STAGE2_BYTES = 2 * A_TILE + 2 * B2_TILE;   // 64 KB
-constexpr int smem2_bytes(int nst, int ebuf) { return nst * STAGE2_BYTES + ebuf * EPI_BYTES + 1024; }
+constexpr int smem2_bytes(int nst, int ebuf, int npl = 2) {
+  return nst * npl * (A_TILE + B2_TILE) + ebuf * EPI_BYTES + 1024;
+}
 constexpr uint32_t IDESC2 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                             ((uint32_t)((2 * BM) >> 4) << 24);
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // shared::cluster address -> the pair's rank-0 CTA
@@ -444,6 +447,7 @@ template <int NST, int EBUF>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     tc_gemm2_kernel(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUtensorMap mA_lo,
                     const __grid_constant__ CUtensorMap mB_hi, const __grid_constant__ CUtensorMap mB_lo,
+                    const __grid_constant__ CUtensorMap mA_l2, const __grid_constant__ CUtensorMap mB_l2,
                     const __grid_constant__ CUtensorMap mOut, const Params p) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[NST], empty_bar[NST], tfull_bar[2], tempty_bar[2];
@@ -478,7 +482,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   cluster_sync_all();  // peer barriers initialised before any remote arrive / complete_tx
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem_base = tmem_base_sh;
-  const uint32_t stage_bytes = p.x3 ? (uint32_t)STAGE2_BYTES : (uint32_t)(A_TILE + B2_TILE);
+  // stage layout: npl A plane slots, then npl B plane slots (hi, lo[, lo2])
+  const int npl = p.x6 ? 3 : 2;
+  const uint32_t SS = (uint32_t)npl * (A_TILE + B2_TILE);
+  const uint32_t stage_bytes = (uint32_t)(p.x6 ? 3 : p.x3 ? 2 : 1) * (A_TILE + B2_TILE);
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
@@ -493,23 +500,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         const int arow = (2 * mb + (int)rank) * BM, brow = nb * BN + (int)rank * (BN / 2);
         for (int kb = 0; kb < p.num_k; ++kb) {
           mbar_wait(&empty_bar[s], ph ^ 1);
-          uint8_t* st = smem + s * STAGE2_BYTES;
+          uint8_t* st = smem + s * SS;
+          uint8_t* sb = st + npl * A_TILE;
           if (rank == 0) mbar_expect_tx(&full_bar[s], 2 * stage_bytes);
           if (p.mn) {  // 64(m|n) x BK(k) boxes: two per A operand, two per B operand half
             for (int j = 0; j < BM / 64; ++j) {
               tma_load_2sm(st + j * 8192, &mA_hi, &full_bar[s], arow + j * 64, kb * BK, a_pol);
               if (p.x3) tma_load_2sm(st + A_TILE + j * 8192, &mA_lo, &full_bar[s], arow + j * 64, kb * BK, a_pol);
+              if (p.x6) tma_load_2sm(st + 2 * A_TILE + j * 8192, &mA_l2, &full_bar[s], arow + j * 64, kb * BK, a_pol);
             }
             for (int j = 0; j < BN / 128; ++j) {
-              tma_load_2sm(st + 2 * A_TILE + j * 8192, &mB_hi, &full_bar[s], brow + j * 64, kb * BK, b_pol);
-              if (p.x3)
-                tma_load_2sm(st + 2 * A_TILE + B2_TILE + j * 8192, &mB_lo, &full_bar[s], brow + j * 64, kb * BK, b_pol);
+              tma_load_2sm(sb + j * 8192, &mB_hi, &full_bar[s], brow + j * 64, kb * BK, b_pol);
+              if (p.x3) tma_load_2sm(sb + B2_TILE + j * 8192, &mB_lo, &full_bar[s], brow + j * 64, kb * BK, b_pol);
+              if (p.x6) tma_load_2sm(sb + 2 * B2_TILE + j * 8192, &mB_l2, &full_bar[s], brow + j * 64, kb * BK, b_pol);
             }
           } else {
             tma_load_2sm(st, &mA_hi, &full_bar[s], kb * BK, arow, a_pol);
             if (p.x3) tma_load_2sm(st + A_TILE, &mA_lo, &full_bar[s], kb * BK, arow, a_pol);
-            tma_load_2sm(st + 2 * A_TILE, &mB_hi, &full_bar[s], kb * BK, brow, b_pol);
-            if (p.x3) tma_load_2sm(st + 2 * A_TILE + B2_TILE, &mB_lo, &full_bar[s], kb * BK, brow, b_pol);
+            if (p.x6) tma_load_2sm(st + 2 * A_TILE, &mA_l2, &full_bar[s], kb * BK, arow, a_pol);
+            tma_load_2sm(sb, &mB_hi, &full_bar[s], kb * BK, brow, b_pol);
+            if (p.x3) tma_load_2sm(sb + B2_TILE, &mB_lo, &full_bar[s], kb * BK, brow, b_pol);
+            if (p.x6) tma_load_2sm(sb + 2 * B2_TILE, &mB_l2, &full_bar[s], kb * BK, brow, b_pol);
           }
           if (++s == NST) {
             s = 0;
@@ -532,8 +543,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         for (int kb = 0; kb < p.num_k; ++kb) {
           mbar_wait(&full_bar[s], ph);
           asm volatile("tcgen05.fence::after_thread_sync;");
-          const uint32_t st = smem_u32(smem + s * STAGE2_BYTES);
-          const uint32_t a_hi = st, a_lo = st + A_TILE, b_hi = st + 2 * A_TILE, b_lo = st + 2 * A_TILE + B2_TILE;
+          const uint32_t st = smem_u32(smem + s * SS);
+          const uint32_t a_hi = st, a_lo = st + A_TILE, a_l2 = st + 2 * A_TILE;
+          const uint32_t b_hi = st + npl * A_TILE, b_lo = b_hi + B2_TILE, b_l2 = b_hi + 2 * B2_TILE;
           if (p.mn) {
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
@@ -544,6 +556,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 mma2_bf16(d, sw128_desc_mn(a_hi + kr), sw128_desc_mn(b_lo + kr), 1u, id);
                 mma2_bf16(d, sw128_desc_mn(a_lo + kr), sw128_desc_mn(b_hi + kr), 1u, id);
               }
+              if (p.x6) {  // bf16x6: + lo*lo + hi*lo2 + lo2*hi
+                mma2_bf16(d, sw128_desc_mn(a_lo + kr), sw128_desc_mn(b_lo + kr), 1u, id);
+                mma2_bf16(d, sw128_desc_mn(a_hi + kr), sw128_desc_mn(b_l2 + kr), 1u, id);
+                mma2_bf16(d, sw128_desc_mn(a_l2 + kr), sw128_desc_mn(b_hi + kr), 1u, id);
+              }
             }
           } else {
 #pragma unroll
@@ -553,6 +570,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               if (p.x3) {
                 mma2_bf16(d, sw128_desc(a_hi + ko), sw128_desc(b_lo + ko), 1u);
                 mma2_bf16(d, sw128_desc(a_lo + ko), sw128_desc(b_hi + ko), 1u);
+              }
+              if (p.x6) {
+                mma2_bf16(d, sw128_desc(a_lo + ko), sw128_desc(b_lo + ko), 1u);
+                mma2_bf16(d, sw128_desc(a_hi + ko), sw128_desc(b_l2 + ko), 1u);
+                mma2_bf16(d, sw128_desc(a_l2 + ko), sw128_desc(b_hi + ko), 1u);
               }
             }
           }
@@ -574,7 +596,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const uint64_t st_pol = policy_evict_first();
     const int q = warp & 3;
     const int half = (warp - 2) / 4;
-    uint8_t* stg0 = smem + NST * STAGE2_BYTES + (warp - 2) * 4096 * EBUF;
+    uint8_t* stg0 = smem + NST * SS + (warp - 2) * 4096 * EBUF;
     int buf = 0;
     int acc = 0;
     uint32_t aph = 0;
@@ -646,6 +668,14 @@ __device__ __forceinline__ float2 cmul_f(float2 a, float2 b) {
   return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 
+// three-way split for bf16x6: x ~ hi + lo + lo2
+__device__ __forceinline__ void split3(float x, __nv_bfloat16& hi, __nv_bfloat16& lo, __nv_bfloat16& lo2) {
+  hi = __float2bfloat16_rn(x);
+  const float r = x - __bfloat162float(hi);
+  lo = __float2bfloat16_rn(r);
+  lo2 = __float2bfloat16_rn(r - __bfloat162float(lo));
+}
+
 __device__ __forceinline__ void split_bf16(float x, __nv_bfloat16& hi, __nv_bfloat16& lo) {
   hi = __float2bfloat16_rn(x);
   lo = __float2bfloat16_rn(x - __bfloat162float(hi));
@@ -707,7 +737,7 @@ __device__ __forceinline__ float2 tail_weight(const TailTile& tt, int n, const f
 __global__ void split_a_kernel(const float2* __restrict__ leaves, const float2* __restrict__ cp,
                                __nv_bfloat162* __restrict__ hi, __nv_bfloat162* __restrict__ lo, long long K,
                                long long Kpad, long long MA, long long r0, long long rows, const TailParams tp,
-                               const float2* __restrict__ ttab) {
+                               const float2* __restrict__ ttab, __nv_bfloat162* __restrict__ lo2) {
   __shared__ float2 t[32][33];
   __shared__ TailTile tt;
   const long long i0 = (long long)blockIdx.x * 32, p0 = (long long)blockIdx.y * 32;
@@ -729,18 +759,20 @@ __global__ void split_a_kernel(const float2* __restrict__ leaves, const float2* 
   for (int r = ty; r < 32; r += 8) {
     long long i = i0 + r, p = p0 + tx;
     float2 v = t[tx][r];
-    __nv_bfloat162 h, l;
-    split_bf16(v.x, h.x, l.x);
-    split_bf16(v.y, h.y, l.y);
+    __nv_bfloat162 h, l, l2;
+    split3(v.x, h.x, l.x, l2.x);
+    split3(v.y, h.y, l.y, l2.y);
     hi[i * Kpad + p] = h;
     if (lo) lo[i * Kpad + p] = l;
+    if (lo2) lo2[i * Kpad + p] = l2;
   }
 }
 
 // B'' rows [0, 2*MB_pad): row 2j <- (re, -im), row 2j+1 <- (im, re) of B[p][j]
 __global__ void split_b_kernel(const float2* __restrict__ leaves, __nv_bfloat162* __restrict__ hi,
                                __nv_bfloat162* __restrict__ lo, long long K, long long Kpad, long long MB,
-                               const TailParams tp, const float2* __restrict__ ttab) {
+                               const TailParams tp, const float2* __restrict__ ttab,
+                               __nv_bfloat162* __restrict__ lo2) {
   __shared__ float2 t[32][33];
   const long long j0 = (long long)blockIdx.x * 32, p0 = (long long)blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -760,11 +792,15 @@ __global__ void split_b_kernel(const float2* __restrict__ leaves, __nv_bfloat162
   for (int r = ty; r < 32; r += 8) {
     long long j = j0 + r, p = p0 + tx;
     float2 v = t[tx][r];
-    __nv_bfloat162 h0, l0, h1, l1;
-    split_bf16(v.x, h0.x, l0.x);
-    split_bf16(-v.y, h0.y, l0.y);
-    split_bf16(v.y, h1.x, l1.x);
-    split_bf16(v.x, h1.y, l1.y);
+    __nv_bfloat162 h0, l0, h1, l1, m0, m1;
+    split3(v.x, h0.x, l0.x, m0.x);
+    split3(-v.y, h0.y, l0.y, m0.y);
+    split3(v.y, h1.x, l1.x, m1.x);
+    split3(v.x, h1.y, l1.y, m1.y);
+    if (lo2) {
+      lo2[(2 * j) * Kpad + p] = m0;
+      lo2[(2 * j + 1) * Kpad + p] = m1;
+    }
     hi[(2 * j) * Kpad + p] = h0;
     hi[(2 * j + 1) * Kpad + p] = h1;
     if (lo) {
@@ -800,7 +836,7 @@ __global__ void tail_weights_kernel(float2* __restrict__ W, long long wld, const
 __global__ void split_a_mn_kernel(const float2* __restrict__ leaves, const float2* __restrict__ cp,
                                   __nv_bfloat16* __restrict__ hi, __nv_bfloat16* __restrict__ lo, long long K,
                                   long long lda, long long MA, long long r0, long long rows, const TailParams tp,
-                                  const float2* __restrict__ ttab) {
+                                  const float2* __restrict__ ttab, __nv_bfloat16* __restrict__ lo2) {
   __shared__ int base[kMaxTail];
   __shared__ unsigned smask[kMaxTail];
   __shared__ long long node;
@@ -872,11 +908,11 @@ __global__ void split_a_mn_kernel(const float2* __restrict__ leaves, const float
     im[e] = v.y;
   }
   }
-  __align__(16) __nv_bfloat16 h[16], l[16];
+  __align__(16) __nv_bfloat16 h[16], l[16], m[16];
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
-    split_bf16(re[e], h[e], l[e]);
-    split_bf16(im[e], h[8 + e], l[8 + e]);
+    split3(re[e], h[e], l[e], m[e]);
+    split3(im[e], h[8 + e], l[8 + e], m[8 + e]);
   }
   const long long o0 = (2 * p) * lda + i, o1 = o0 + lda;
   *reinterpret_cast<uint4*>(hi + o0) = *reinterpret_cast<const uint4*>(h);
@@ -885,6 +921,10 @@ __global__ void split_a_mn_kernel(const float2* __restrict__ leaves, const float
     *reinterpret_cast<uint4*>(lo + o0) = *reinterpret_cast<const uint4*>(l);
     *reinterpret_cast<uint4*>(lo + o1) = *reinterpret_cast<const uint4*>(l + 8);
   }
+  if (lo2) {
+    *reinterpret_cast<uint4*>(lo2 + o0) = *reinterpret_cast<const uint4*>(m);
+    *reinterpret_cast<uint4*>(lo2 + o1) = *reinterpret_cast<const uint4*>(m + 8);
+  }
 }
 
 // MN-major B'' (p.mn): row 2p <- (re, im) of B[p][j] at columns (2j, 2j+1),
@@ -892,7 +932,8 @@ __global__ void split_a_mn_kernel(const float2* __restrict__ leaves, const float
 // each row is one leaf, written elementwise.  One CTA per (path, 512 amplitudes).
 __global__ void split_b_mn_kernel(const float2* __restrict__ leaves, __nv_bfloat16* __restrict__ hi,
                                   __nv_bfloat16* __restrict__ lo, long long K, long long ldb, long long MB,
-                                  const TailParams tp, const float2* __restrict__ ttab) {
+                                  const TailParams tp, const float2* __restrict__ ttab,
+                                  __nv_bfloat16* __restrict__ lo2) {
   __shared__ int base[kMaxTail];
   __shared__ unsigned smask[kMaxTail];
   __shared__ long long node;
@@ -948,13 +989,13 @@ __global__ void split_b_mn_kernel(const float2* __restrict__ leaves, __nv_bfloat
       }
     }
   }
-  __align__(16) __nv_bfloat16 h[16], l[16];
+  __align__(16) __nv_bfloat16 h[16], l[16], m[16];
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    split_bf16(v[e].x, h[2 * e], l[2 * e]);
-    split_bf16(v[e].y, h[2 * e + 1], l[2 * e + 1]);
-    split_bf16(-v[e].y, h[8 + 2 * e], l[8 + 2 * e]);
-    split_bf16(v[e].x, h[8 + 2 * e + 1], l[8 + 2 * e + 1]);
+    split3(v[e].x, h[2 * e], l[2 * e], m[2 * e]);
+    split3(v[e].y, h[2 * e + 1], l[2 * e + 1], m[2 * e + 1]);
+    split3(-v[e].y, h[8 + 2 * e], l[8 + 2 * e], m[8 + 2 * e]);
+    split3(v[e].x, h[8 + 2 * e + 1], l[8 + 2 * e + 1], m[8 + 2 * e + 1]);
   }
   const long long o0 = (2 * p) * ldb + 2 * j, o1 = o0 + ldb;
   *reinterpret_cast<uint4*>(hi + o0) = *reinterpret_cast<const uint4*>(h);
@@ -962,6 +1003,10 @@ __global__ void split_b_mn_kernel(const float2* __restrict__ leaves, __nv_bfloat
   if (lo) {
     *reinterpret_cast<uint4*>(lo + o0) = *reinterpret_cast<const uint4*>(l);
     *reinterpret_cast<uint4*>(lo + o1) = *reinterpret_cast<const uint4*>(l + 8);
+  }
+  if (lo2) {
+    *reinterpret_cast<uint4*>(lo2 + o0) = *reinterpret_cast<const uint4*>(m);
+    *reinterpret_cast<uint4*>(lo2 + o1) = *reinterpret_cast<const uint4*>(m + 8);
   }
 }
 
@@ -983,9 +1028,10 @@ inline TcDims tc_dims(long long K, long long rows, long long MB) {
   return d;
 }
 
-inline size_t tc_workspace_bytes(long long K, long long rows, long long MB, bool x3) {
+// planes: 1 (bf16x1), 2 (bf16x3: hi, lo), 3 (bf16x6: hi, lo, lo2)
+inline size_t tc_workspace_bytes(long long K, long long rows, long long MB, int planes) {
   TcDims d = tc_dims(K, rows, MB);
-  return (x3 ? 2 : 1) * (((d.a_bytes + 1023) & ~(size_t)1023) + ((d.b_bytes + 1023) & ~(size_t)1023));
+  return (size_t)planes * (((d.a_bytes + 1023) & ~(size_t)1023) + ((d.b_bytes + 1023) & ~(size_t)1023));
 }
 
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -1047,6 +1093,8 @@ inline int num_sms() {
 struct TcBuffers {
   TcDims d;
   __nv_bfloat162 *a_hi, *a_lo, *b_hi, *b_lo;
+  __nv_bfloat162 *a_l2 = nullptr, *b_l2 = nullptr;  // bf16x6 third planes
+  int planes = 2;
   bool mn = false;    // operands MN-major: A''^T [2*Kpad][rows_pad], B''^T [2*Kpad][nrows_b_pad] bf16
   long long K = 0;    // paths (operand k extent before padding)
 };
@@ -1060,10 +1108,12 @@ inline bool tc_mn(long long K) {
   return 2 * ((K + 31) / 32 * 32) > 2 * tc::BK;
 }
 
-inline TcBuffers tc_buffers(long long K, long long rows, long long MB, bool x3, void* ws, size_t ws_bytes) {
+inline TcBuffers tc_buffers(long long K, long long rows, long long MB, int planes, void* ws, size_t ws_bytes) {
   TcBuffers t;
   t.d = tc_dims(K, rows, MB);
-  if (tc_workspace_bytes(K, rows, MB, x3) > ws_bytes) fail(HSF_ERR_INVALID_ARG, "tc workspace too small");
+  t.planes = planes;
+  const bool x3 = planes >= 2;
+  if (tc_workspace_bytes(K, rows, MB, planes) > ws_bytes) fail(HSF_ERR_INVALID_ARG, "tc workspace too small");
   char* w = (char*)ws;
   auto take = [&](size_t b) {
     char* r = w;
@@ -1074,6 +1124,8 @@ inline TcBuffers tc_buffers(long long K, long long rows, long long MB, bool x3, 
   t.b_hi = (__nv_bfloat162*)take(t.d.b_bytes);
   t.a_lo = x3 ? (__nv_bfloat162*)take(t.d.a_bytes) : nullptr;
   t.b_lo = x3 ? (__nv_bfloat162*)take(t.d.b_bytes) : nullptr;
+  t.a_l2 = planes >= 3 ? (__nv_bfloat162*)take(t.d.a_bytes) : nullptr;
+  t.b_l2 = planes >= 3 ? (__nv_bfloat162*)take(t.d.b_bytes) : nullptr;
   t.mn = tc_mn(K);
   t.K = K;
   return t;
@@ -1085,13 +1137,14 @@ inline void tc_prep_a(const TcBuffers& t, const float2* leavesA, const float2* c
   if (t.mn) {
     const long long lda = t.d.rows_pad;
     tc::split_a_mn_kernel<<<dim3((unsigned)((lda / 8 + 255) / 256), (unsigned)t.d.Kpad), 256, 0, st>>>(
-        leavesA, cp, (__nv_bfloat16*)t.a_hi, (__nv_bfloat16*)t.a_lo, K, lda, MA, r0, rows, tp, ttab);
+        leavesA, cp, (__nv_bfloat16*)t.a_hi, (__nv_bfloat16*)t.a_lo, K, lda, MA, r0, rows, tp, ttab,
+        (__nv_bfloat16*)t.a_l2);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("split_a_mn: ") + cudaGetErrorString(e));
     return;
   }
   tc::split_a_kernel<<<dim3((unsigned)(t.d.rows_pad / 32), (unsigned)(t.d.Kpad / 32)), dim3(32, 8), 0, st>>>(
-      leavesA, cp, t.a_hi, t.a_lo, K, t.d.Kpad, MA, r0, rows, tp, ttab);
+      leavesA, cp, t.a_hi, t.a_lo, K, t.d.Kpad, MA, r0, rows, tp, ttab, t.a_l2);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("split_a: ") + cudaGetErrorString(e));
 }
@@ -1102,21 +1155,22 @@ inline void tc_prep_b(const TcBuffers& t, const float2* leavesB, long long K, lo
   if (t.mn) {
     const long long ldb = t.d.nrows_b_pad;
     tc::split_b_mn_kernel<<<dim3((unsigned)((ldb / 8 + 255) / 256), (unsigned)t.d.Kpad), 256, 0, st>>>(
-        leavesB, (__nv_bfloat16*)t.b_hi, (__nv_bfloat16*)t.b_lo, K, ldb, MB, tp, ttab);
+        leavesB, (__nv_bfloat16*)t.b_hi, (__nv_bfloat16*)t.b_lo, K, ldb, MB, tp, ttab, (__nv_bfloat16*)t.b_l2);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("split_b_mn: ") + cudaGetErrorString(e));
     return;
   }
   tc::split_b_kernel<<<dim3((unsigned)(t.d.nrows_b_pad / 64), (unsigned)(t.d.Kpad / 32)), dim3(32, 8), 0, st>>>(
-      leavesB, t.b_hi, t.b_lo, K, t.d.Kpad, MB, tp, ttab);
+      leavesB, t.b_hi, t.b_lo, K, t.d.Kpad, MB, tp, ttab, t.b_l2);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("split_b: ") + cudaGetErrorString(e));
 }
 
 // K5: the persistent tcgen05 GEMM over operand rows [row0, row0 + rows)
 // (row0 a multiple of BM) into out[rows][2*MB] fp32
-inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row0, long long rows, bool x3,
+inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row0, long long rows,
                     cudaStream_t st, bool accumulate = false) {
+  const bool x3 = t.planes >= 2, x6 = t.planes >= 3;
   const long long kcols = 2 * t.d.Kpad;  // bf16 per operand row
   if (row0 % tc::BM) fail(HSF_ERR_INVALID_ARG, "tc_gemm row offset not tile aligned");
   const long long rpad = (rows + tc::BM - 1) / tc::BM * tc::BM;
@@ -1137,11 +1191,20 @@ inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row
   CUtensorMap mBl = !x3 ? mBh
                    : t.mn ? make_map(t.b_lo, 2 * t.K, 2 * MB, tc::BK, t.d.nrows_b_pad)
                             : make_map(t.b_lo, t.d.nrows_b_pad, kcols, tc::BN);
+  // bf16x6 third planes (pair kernel only)
+  CUtensorMap mA2 = mAh, mB2 = mBh;
+  if (x6) {
+    mA2 = t.mn ? make_map((__nv_bfloat16*)t.a_l2 + row0, 2 * t.K, rows, tc::BK, t.d.rows_pad)
+               : make_map(t.a_l2 + row0 * t.d.Kpad, rpad, kcols, tc::BM);
+    mB2 = t.mn ? make_map(t.b_l2, 2 * t.K, 2 * MB, tc::BK, t.d.nrows_b_pad)
+               : make_map(t.b_l2, t.d.nrows_b_pad, kcols, tc::BN / 2);
+  }
   tc::Params p;
   p.num_m = (int)(rpad / tc::BM);
   p.num_n = (int)(t.d.nrows_b_pad / tc::BN);
   p.num_k = (int)(kcols / tc::BK);
   p.x3 = x3 ? 1 : 0;
+  p.x6 = x6 ? 1 : 0;
   p.accumulate = accumulate ? 1 : 0;
   p.mn = t.mn ? 1 : 0;
   // M-fastest raster: the ~148 concurrent tiles share one B tile (read once
@@ -1156,7 +1219,7 @@ inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row
   p.group_m = p.num_k <= 2 ? 16 : 0;
   if (const char* g = std::getenv("HSF_TC_GROUP_M")) p.group_m = std::atoi(g);
 
-  p.a_evict_last = ((x3 ? 2 : 1) * rpad * kcols * 2 <= (64ll << 20)) ? 1 : 0;
+  p.a_evict_last = ((long long)t.planes * rpad * kcols * 2 <= (64ll << 20)) ? 1 : 0;
   p.out = (float*)out;
   p.ldo = 2 * MB;
   p.rows = rows;
@@ -1170,7 +1233,8 @@ inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row
   }
   CUtensorMap mO = make_out_map((float*)out, rows, 2 * MB);
   const char* pair_env = std::getenv("HSF_TC_PAIR");
-  const bool pair = rows > tc::BM && !(pair_env && pair_env[0] == '0');
+  // (bf16x6: the pair kernel only -- three planes do not fit two single-CTA stages)
+  const bool pair = x6 || (rows > tc::BM && !(pair_env && pair_env[0] == '0'));
   if (pair) {
     // CTA pairs: 256-row M tiles, each CTA loads half of every B tile
     static bool attr2 = false;
@@ -1180,6 +1244,9 @@ inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row
       if (e == cudaSuccess)
         e = cudaFuncSetAttribute(tc::tc_gemm2_kernel<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  tc::smem2_bytes(2, 2));
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(tc::tc_gemm2_kernel<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 tc::smem2_bytes(2, 1, 3));
       if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("tc2 smem attr: ") + cudaGetErrorString(e));
       attr2 = true;
     }
@@ -1188,10 +1255,15 @@ inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row
     p.num_m = (int)((rows + 2 * tc::BM - 1) / (2 * tc::BM));
     const long long tiles = (long long)p.num_m * p.num_n;
     const int grid = 2 * (int)std::min<long long>(tiles, num_sms() / 2);
-    if (p.num_k <= 2)
-      tc::tc_gemm2_kernel<2, 2><<<grid, tc::THREADS, tc::smem2_bytes(2, 2), st>>>(mAh, mAl, mBh2, mBl2, mO, p);
+    if (x6)  // 2 stages x 96 KB + one staging box per epilogue warp
+      tc::tc_gemm2_kernel<2, 1><<<grid, tc::THREADS, tc::smem2_bytes(2, 1, 3), st>>>(mAh, mAl, mBh2, mBl2, mA2, mB2,
+                                                                                     mO, p);
+    else if (p.num_k <= 2)
+      tc::tc_gemm2_kernel<2, 2><<<grid, tc::THREADS, tc::smem2_bytes(2, 2), st>>>(mAh, mAl, mBh2, mBl2, mAh, mBh2,
+                                                                                  mO, p);
     else
-      tc::tc_gemm2_kernel<3, 1><<<grid, tc::THREADS, tc::smem2_bytes(3, 1), st>>>(mAh, mAl, mBh2, mBl2, mO, p);
+      tc::tc_gemm2_kernel<3, 1><<<grid, tc::THREADS, tc::smem2_bytes(3, 1), st>>>(mAh, mAl, mBh2, mBl2, mAh, mBh2,
+                                                                                  mO, p);
   } else {
     const long long tiles = (long long)p.num_m * p.num_n;
     const int grid = (int)std::min<long long>(tiles, num_sms());

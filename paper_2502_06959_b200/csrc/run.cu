@@ -290,6 +290,8 @@ struct Layout {
 };
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+// split-bf16 operand planes per precision mode
+static int tc_planes(hsf_precision p) { return p == HSF_PREC_BF16X6 ? 3 : p == HSF_PREC_BF16X3 ? 2 : 1; }
 constexpr size_t kHostChunkBytes = (size_t)32 << 20;  // D2H of chunk i overlaps the path-sum of chunk i+1
 
 static uint64_t nodes_at(const std::vector<int32_t>& ranks, int L, uint64_t p0, uint64_t p1) {
@@ -316,6 +318,8 @@ static Layout make_layout(const Plan& P, const hsf_run_args& a, size_t elem) {
   }
   L.K = L.p1 - L.p0;
   L.prec = a.precision;
+  if ((int)L.prec < (int)HSF_PREC_AUTO || (int)L.prec > (int)HSF_PREC_BF16X6)
+    fail(HSF_ERR_INVALID_ARG, "unknown precision mode " + std::to_string((int)L.prec));
   if (L.prec == HSF_PREC_AUTO) L.prec = (P.opts.dtype == HSF_C64) ? HSF_PREC_BF16X3 : HSF_PREC_SIMT;
   if (P.opts.dtype == HSF_C128 && L.prec != HSF_PREC_SIMT) fail(HSF_ERR_UNSUPPORTED, "complex128 path-sum is SIMT fp64 only");
   // half-sided trailing fold: full-output tensor-core runs whose path range
@@ -339,7 +343,8 @@ static Layout make_layout(const Plan& P, const hsf_run_args& a, size_t elem) {
       L.hp1[h] = L.p1;
     }
   }
-  L.bop = !L.bits_mode && L.prec != HSF_PREC_SIMT && P.opts.dtype == HSF_C64 && L.var[1] == 0 && tc_mn((long long)L.K);
+  L.bop = !L.bits_mode && (L.prec == HSF_PREC_BF16X3 || L.prec == HSF_PREC_BF16X1) && P.opts.dtype == HSF_C64 &&
+          L.var[1] == 0 && tc_mn((long long)L.K);
   if (!L.bits_mode && a.bitstrings) fail(HSF_ERR_INVALID_ARG, "bitstrings given with n_bitstrings == 0");
   if (L.bits_mode && !a.bitstrings) fail(HSF_ERR_INVALID_ARG, "n_bitstrings > 0 but bitstrings is NULL");
   if (L.bits_mode && P.n > 63) fail(HSF_ERR_INVALID_ARG, "bitstring runs need n <= 63");
@@ -388,8 +393,8 @@ static Layout make_layout(const Plan& P, const hsf_run_args& a, size_t elem) {
       L.off_pout = off;
       off = align_up(off + ((size_t)1 << P.n) * elem);
     }
-    if (L.prec == HSF_PREC_BF16X3 || L.prec == HSF_PREC_BF16X1) {
-      L.tc_bytes = tc_workspace_bytes((long long)L.K, (long long)(L.r1 - L.r0), 1ll << nB, L.prec == HSF_PREC_BF16X3);
+    if (L.prec == HSF_PREC_BF16X3 || L.prec == HSF_PREC_BF16X1 || L.prec == HSF_PREC_BF16X6) {
+      L.tc_bytes = tc_workspace_bytes((long long)L.K, (long long)(L.r1 - L.r0), 1ll << nB, tc_planes(L.prec));
       L.off_tc = off;
       off = align_up(off + L.tc_bytes);
     }
@@ -553,7 +558,7 @@ static void run_half(const Plan& P, DeviceState* d, int h, const Layout& L, cuda
         }
         const bool bop = h == 1 && L.bop && d->jit_bop && last && pi + 1 == tr.passes.size();
         if (bop) {  // K4 fused: write the MN-major split-bf16 B operand instead of the leaves
-          TcBuffers t = tc_buffers((long long)L.K, (long long)(L.r1 - L.r0), 1ll << H.m, L.prec == HSF_PREC_BF16X3,
+          TcBuffers t = tc_buffers((long long)L.K, (long long)(L.r1 - L.r0), 1ll << H.m, tc_planes(L.prec),
                                    ws + L.off_tc, L.tc_bytes);
           JitLaunchArgs ja{pp.src, t.b_hi, pp.coef, pp.node_first, pp.node_local0, pp.src_first, pp.src_div, pp.tile0,
                            t.b_lo, t.d.nrows_b_pad / 2};
@@ -595,7 +600,7 @@ static void prep_half(Plan* P, DeviceState* d, const Layout& L, int h, cudaStrea
     CK(cudaGetLastError());
   } else if (L.prec != HSF_PREC_SIMT) {
     const int nB = P->n_low;
-    TcBuffers t = tc_buffers(K, (long long)(L.r1 - L.r0), 1ll << nB, L.prec == HSF_PREC_BF16X3, ws + L.off_tc, L.tc_bytes);
+    TcBuffers t = tc_buffers(K, (long long)(L.r1 - L.r0), 1ll << nB, tc_planes(L.prec), ws + L.off_tc, L.tc_bytes);
     tc::TailParams tp = L.var[h] == 2 ? tail_params(*P, h) : tc::TailParams{};
     tp.p0 = (long long)L.p0;
     if (L.var[h] == 2) {
@@ -675,9 +680,9 @@ static void run_core_full(Plan* P, DeviceState* d, const Layout& L, cudaStream_t
     CK(cudaGetLastError());
   } else {
     if (sizeof(R) != 4) fail(HSF_ERR_UNSUPPORTED, "tensor-core path-sum needs complex64");
-    TcBuffers t = tc_buffers(K, (long long)(L.r1 - L.r0), 1ll << nB, L.prec == HSF_PREC_BF16X3, ws + L.off_tc,
+    TcBuffers t = tc_buffers(K, (long long)(L.r1 - L.r0), 1ll << nB, tc_planes(L.prec), ws + L.off_tc,
                              L.tc_bytes);
-    tc_gemm(t, (float2*)out, 1ll << nB, (long long)lo, (long long)nrows, L.prec == HSF_PREC_BF16X3, st, accumulate);
+    tc_gemm(t, (float2*)out, 1ll << nB, (long long)lo, (long long)nrows, st, accumulate);
   }
 }
 

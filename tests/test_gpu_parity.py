@@ -240,6 +240,25 @@ def test_bf16x1_is_lower_precision(torch):
     assert e1 < 2e-2 and e3 < 2e-5 and e3 < e1 / 20, (e1, e3)
 
 
+@pytest.mark.parametrize("name", ["c2", "c4", "c5"])
+def test_bf16x6_precision(torch, name):
+    # three-way split, 6 products (bf16x6 reported beside bf16x3):
+    # the dropped terms are ~2^-24 relative; what remains is the tensor core's
+    # fp32 accumulation over 6 x 2K/16 MMA steps (measured 1.0-1.7e-6 relL2 on
+    # the c2/c4 twins vs 3.8-4.6e-6 for bf16x3 and 3.7e-7 for the fp32 SIMT
+    # path; c5 twin 3.8e-6 vs 4.9e-6)
+    inst = make_config(name, twin=True, n_bits=0) if name == "c5" else make_config(name, twin=True)
+    n, g = O.parse_circuit(inst.text)
+    ref = O.schrodinger(n, g)
+    rel = {}
+    for prec in ("simt", "bf16x3", "bf16x6"):
+        x, _ = gpu_full(torch, inst, dtype="c64", precision=prec)
+        rel[prec] = np.linalg.norm(x - ref) / np.linalg.norm(ref)
+    assert rel["bf16x6"] < 1e-5 and rel["bf16x6"] <= rel["bf16x3"], rel
+    if name != "c5":  # c5's cancelling fan-out sums sit at the accumulation floor for both
+        assert rel["bf16x6"] < 0.6 * rel["bf16x3"], rel
+
+
 @pytest.mark.parametrize("b_layout", ["auto", "0", "1"])
 def test_bf16x3_ragged_rows_and_paths(torch, b_layout, monkeypatch):
     # K not a multiple of 32, row range not a multiple of 128, 2*MB < 256;
@@ -252,8 +271,9 @@ def test_bf16x3_ragged_rows_and_paths(torch, b_layout, monkeypatch):
     rows = 1 << P.n_a
     for pr, rr in [((3, 200), (5, 37)), ((0, 256), (0, rows)), ((17, 18), (1, 2))]:
         ref, _ = gpu_full(torch, inst, precision="simt", path_range=pr, row_range=rr)
-        got, _ = gpu_full(torch, inst, precision="bf16x3", path_range=pr, row_range=rr)
-        assert np.abs(got - ref).max() <= 1e-5 * max(1.0, np.abs(ref).max() * 100)
+        for prec in ("bf16x3", "bf16x6"):
+            got, _ = gpu_full(torch, inst, precision=prec, path_range=pr, row_range=rr)
+            assert np.abs(got - ref).max() <= 1e-5 * max(1.0, np.abs(ref).max() * 100), prec
 
 
 def test_c2_full_size_bf16x3(torch):
