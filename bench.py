@@ -369,20 +369,23 @@ def main():
     eff_prec = ("bf16x3" if inst.dtype == "c64" else "simt") if prec == "auto" else prec
     MA, MB = (rows if full else 1 << (inst.n - inst.n_low)), 1 << inst.n_low
     clk_mhz = peaks.get("clocks_under_load", {}).get("sm_mhz_median", 1305.0)
-    if full and eff_prec in ("bf16x3", "bf16x1", "bf16x6"):
+    if full and eff_prec in ("bf16x3", "bf16x1", "bf16x6", "tf32x3"):
         # executed tensor-core flops: (6 | 3 | 1) real GEMMs of rows x 2MB x 2K;
         # algorithmic bytes: the fp32 output written once (+ bf16 operand planes)
-        nprod, planes = {"bf16x6": (6, 3), "bf16x3": (3, 2), "bf16x1": (1, 1)}[eff_prec]
+        nprod, planes = {"bf16x6": (6, 3), "bf16x3": (3, 2), "bf16x1": (1, 1), "tf32x3": (3, 4)}[eff_prec]
         tflop = nprod * 2.0 * MA * (2 * MB) * (2 * K)
         obytes = MA * MB * esz + planes * 4.0 * K * (MA + 2 * MB)
-        t_tensor, t_hbm = tflop / (bf16 * 1e12), obytes / (hbm * 1e9)
+        # tf32 runs at half the bf16 rate (nominal 1125 vs 2250 TFLOP/s dense)
+        tpeak, tnom = (bf16 / 2, 1125.0) if eff_prec == "tf32x3" else (bf16, 2250.0)
+        t_tensor, t_hbm = tflop / (tpeak * 1e12), obytes / (hbm * 1e9)
         if t_tensor >= t_hbm:
             ach = tflop / (core_ms * 1e-3) / 1e12
-            roof = {"bound": "tensor", "achieved": ach, "peak": bf16, "unit": "TFLOP/s", "frac": ach / bf16,
+            roof = {"bound": "tensor", "achieved": ach, "peak": tpeak, "unit": "TFLOP/s", "frac": ach / tpeak,
                     "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst: torch/cuBLAS bf16 8192^3, itself "
-                                   "%.0f%% of the 2250 TFLOP/s nominal dense peak); sustained %.1f" %
-                                   (100.0 * bf16 / 2250.0, peaks.get("bf16_tflops_sustained", 0.0)),
-                    "frac_of_nominal_2250": ach / 2250.0}
+                                   "%.0f%% of the 2250 TFLOP/s nominal dense peak)%s; sustained %.1f" %
+                                   (100.0 * bf16 / 2250.0, " x 1/2 for tf32" if tnom < 2000 else "",
+                                    peaks.get("bf16_tflops_sustained", 0.0)),
+                    "frac_of_nominal": ach / tnom}
         else:
             ach = obytes / (core_ms * 1e-3) / 1e9
             roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,

@@ -69,8 +69,11 @@ typedef enum {
   HSF_PREC_BF16X3 = 2,  /* tcgen05 bf16 MMA, fp32 accumulate in TMEM, operands
                            split hi+lo, 3 products (hi*hi + hi*lo + lo*hi) */
   HSF_PREC_BF16X1 = 3,  /* tcgen05 bf16 MMA, single product (error study only) */
-  HSF_PREC_BF16X6 = 4   /* tcgen05 bf16 MMA, operands split hi+lo+lo2, 6 products
-                           (+ lo*lo + hi*lo2 + lo2*hi): ~fp32 accuracy, 2x the MMA work */
+  HSF_PREC_BF16X6 = 4,  /* tcgen05 bf16 MMA, operands split hi+lo+lo2, 6 products
+                           (+ lo*lo + hi*lo2 + lo2*hi): 2x the MMA work; the error then
+                           sits at the tensor core's fp32 accumulation floor */
+  HSF_PREC_TF32X3 = 5   /* tcgen05 kind::tf32 MMA (half the bf16 rate), operands split
+                           hi+lo tf32 (cvt.rna), 3 products, K-major fp32 storage */
 } hsf_precision;
 
 typedef struct {

@@ -425,6 +425,19 @@ __device__ __forceinline__ void mma2_bf16(uint32_t tmem_d, uint64_t adesc, uint6
       "}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
 }
+// kind::tf32: D=F32, A=B=TF32 (format 2), K = 8 per instruction (32 B, the
+// same byte step as bf16's K = 16)
+constexpr uint32_t IDESC2_TF32 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                 ((uint32_t)((2 * BM) >> 4) << 24);
+__device__ __forceinline__ void mma2_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(IDESC2_TF32), "r"(accum));
+}
 __device__ __forceinline__ void mma2_commit_both(uint64_t* bar) {
   asm volatile(
       "{\n"
@@ -443,7 +456,9 @@ __device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
 // NST SMEM stages, EBUF staging boxes per epilogue warp: <3,1> for long K
 // (c2: deep operand pipeline), <2,2> for short K (c4: num_k <= 2, the kernel
 // is output-write-bound, so a second box keeps two TMA stores per warp in flight)
-template <int NST, int EBUF>
+// TF32: kind::tf32 on fp32-storage operands (tf32x3; K-major only, boxes of
+// 32 fp32 = the same 128 B rows)
+template <int NST, int EBUF, bool TF32 = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     tc_gemm2_kernel(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUtensorMap mA_lo,
                     const __grid_constant__ CUtensorMap mB_hi, const __grid_constant__ CUtensorMap mB_lo,
@@ -515,12 +530,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               if (p.x6) tma_load_2sm(sb + 2 * B2_TILE + j * 8192, &mB_l2, &full_bar[s], brow + j * 64, kb * BK, b_pol);
             }
           } else {
-            tma_load_2sm(st, &mA_hi, &full_bar[s], kb * BK, arow, a_pol);
-            if (p.x3) tma_load_2sm(st + A_TILE, &mA_lo, &full_bar[s], kb * BK, arow, a_pol);
-            if (p.x6) tma_load_2sm(st + 2 * A_TILE, &mA_l2, &full_bar[s], kb * BK, arow, a_pol);
-            tma_load_2sm(sb, &mB_hi, &full_bar[s], kb * BK, brow, b_pol);
-            if (p.x3) tma_load_2sm(sb + B2_TILE, &mB_lo, &full_bar[s], kb * BK, brow, b_pol);
-            if (p.x6) tma_load_2sm(sb + 2 * B2_TILE, &mB_l2, &full_bar[s], kb * BK, brow, b_pol);
+            const int kc = kb * (TF32 ? BK / 2 : BK);  // element coordinate of this 128 B k block
+            tma_load_2sm(st, &mA_hi, &full_bar[s], kc, arow, a_pol);
+            if (p.x3) tma_load_2sm(st + A_TILE, &mA_lo, &full_bar[s], kc, arow, a_pol);
+            if (p.x6) tma_load_2sm(st + 2 * A_TILE, &mA_l2, &full_bar[s], kc, arow, a_pol);
+            tma_load_2sm(sb, &mB_hi, &full_bar[s], kc, brow, b_pol);
+            if (p.x3) tma_load_2sm(sb + B2_TILE, &mB_lo, &full_bar[s], kc, brow, b_pol);
+            if (p.x6) tma_load_2sm(sb + 2 * B2_TILE, &mB_l2, &full_bar[s], kc, brow, b_pol);
           }
           if (++s == NST) {
             s = 0;
@@ -566,6 +582,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
               const uint32_t ko = k * 32;
+              if constexpr (TF32) {
+                mma2_tf32(d, sw128_desc(a_hi + ko), sw128_desc(b_hi + ko), (kb | k) ? 1u : 0u);
+                mma2_tf32(d, sw128_desc(a_hi + ko), sw128_desc(b_lo + ko), 1u);
+                mma2_tf32(d, sw128_desc(a_lo + ko), sw128_desc(b_hi + ko), 1u);
+                continue;
+              }
               mma2_bf16(d, sw128_desc(a_hi + ko), sw128_desc(b_hi + ko), (kb | k) ? 1u : 0u);
               if (p.x3) {
                 mma2_bf16(d, sw128_desc(a_hi + ko), sw128_desc(b_lo + ko), 1u);
@@ -668,6 +690,24 @@ __device__ __forceinline__ float2 cmul_f(float2 a, float2 b) {
   return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 
+// tf32 (fp32 storage, low 13 mantissa bits zero; RNA as cvt.rna.tf32.f32)
+__device__ __forceinline__ float to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+// pair splitters of the K-major kernels: (re|im) pair -> hi, lo, lo2 pairs
+__device__ __forceinline__ void split3(float x, __nv_bfloat16& hi, __nv_bfloat16& lo, __nv_bfloat16& lo2);
+__device__ __forceinline__ void split_pair(float a, float b, __nv_bfloat162& h, __nv_bfloat162& l, __nv_bfloat162& m) {
+  split3(a, h.x, l.x, m.x);
+  split3(b, h.y, l.y, m.y);
+}
+__device__ __forceinline__ void split_pair(float a, float b, float2& h, float2& l, float2& m) {  // tf32x3
+  h = make_float2(to_tf32(a), to_tf32(b));
+  l = make_float2(to_tf32(a - h.x), to_tf32(b - h.y));
+  m = make_float2(0.f, 0.f);
+}
+
 // three-way split for bf16x6: x ~ hi + lo + lo2
 __device__ __forceinline__ void split3(float x, __nv_bfloat16& hi, __nv_bfloat16& lo, __nv_bfloat16& lo2) {
   hi = __float2bfloat16_rn(x);
@@ -733,11 +773,13 @@ __device__ __forceinline__ float2 tail_weight(const TailTile& tt, int n, const f
   return w;
 }
 
-// A'' rows [0, rows_pad): row i <- (re, im) of c_p * A[p][r0 + i]; zero padding
+// A'' rows [0, rows_pad): row i <- (re, im) of c_p * A[p][r0 + i]; zero padding.
+// T2 = __nv_bfloat162 (bf16 splits) or float2 (tf32x3)
+template <typename T2>
 __global__ void split_a_kernel(const float2* __restrict__ leaves, const float2* __restrict__ cp,
-                               __nv_bfloat162* __restrict__ hi, __nv_bfloat162* __restrict__ lo, long long K,
+                               T2* __restrict__ hi, T2* __restrict__ lo, long long K,
                                long long Kpad, long long MA, long long r0, long long rows, const TailParams tp,
-                               const float2* __restrict__ ttab, __nv_bfloat162* __restrict__ lo2) {
+                               const float2* __restrict__ ttab, T2* __restrict__ lo2) {
   __shared__ float2 t[32][33];
   __shared__ TailTile tt;
   const long long i0 = (long long)blockIdx.x * 32, p0 = (long long)blockIdx.y * 32;
@@ -759,9 +801,8 @@ __global__ void split_a_kernel(const float2* __restrict__ leaves, const float2* 
   for (int r = ty; r < 32; r += 8) {
     long long i = i0 + r, p = p0 + tx;
     float2 v = t[tx][r];
-    __nv_bfloat162 h, l, l2;
-    split3(v.x, h.x, l.x, l2.x);
-    split3(v.y, h.y, l.y, l2.y);
+    T2 h, l, l2;
+    split_pair(v.x, v.y, h, l, l2);
     hi[i * Kpad + p] = h;
     if (lo) lo[i * Kpad + p] = l;
     if (lo2) lo2[i * Kpad + p] = l2;
@@ -769,10 +810,11 @@ __global__ void split_a_kernel(const float2* __restrict__ leaves, const float2* 
 }
 
 // B'' rows [0, 2*MB_pad): row 2j <- (re, -im), row 2j+1 <- (im, re) of B[p][j]
-__global__ void split_b_kernel(const float2* __restrict__ leaves, __nv_bfloat162* __restrict__ hi,
-                               __nv_bfloat162* __restrict__ lo, long long K, long long Kpad, long long MB,
+template <typename T2>
+__global__ void split_b_kernel(const float2* __restrict__ leaves, T2* __restrict__ hi,
+                               T2* __restrict__ lo, long long K, long long Kpad, long long MB,
                                const TailParams tp, const float2* __restrict__ ttab,
-                               __nv_bfloat162* __restrict__ lo2) {
+                               T2* __restrict__ lo2) {
   __shared__ float2 t[32][33];
   const long long j0 = (long long)blockIdx.x * 32, p0 = (long long)blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -792,11 +834,9 @@ __global__ void split_b_kernel(const float2* __restrict__ leaves, __nv_bfloat162
   for (int r = ty; r < 32; r += 8) {
     long long j = j0 + r, p = p0 + tx;
     float2 v = t[tx][r];
-    __nv_bfloat162 h0, l0, h1, l1, m0, m1;
-    split3(v.x, h0.x, l0.x, m0.x);
-    split3(-v.y, h0.y, l0.y, m0.y);
-    split3(v.y, h1.x, l1.x, m1.x);
-    split3(v.x, h1.y, l1.y, m1.y);
+    T2 h0, l0, h1, l1, m0, m1;
+    split_pair(v.x, -v.y, h0, l0, m0);
+    split_pair(v.y, v.x, h1, l1, m1);
     if (lo2) {
       lo2[(2 * j) * Kpad + p] = m0;
       lo2[(2 * j + 1) * Kpad + p] = m1;
@@ -1018,19 +1058,22 @@ struct TcDims {
   size_t a_bytes, b_bytes;
 };
 
-inline TcDims tc_dims(long long K, long long rows, long long MB) {
+// esz: operand element bytes (2 bf16, 4 tf32)
+inline TcDims tc_dims(long long K, long long rows, long long MB, int esz = 2) {
   TcDims d;
-  d.Kpad = (K + 31) / 32 * 32;  // 32 complex = 64 bf16 = one BK block
+  d.Kpad = (K + 31) / 32 * 32;  // 32 complex = 64 elements = one 128 B bf16 row (two tf32 rows)
   d.rows_pad = (rows + tc::BM - 1) / tc::BM * tc::BM;
   d.nrows_b_pad = (2 * MB + tc::BN - 1) / tc::BN * tc::BN;
-  d.a_bytes = (size_t)d.rows_pad * d.Kpad * 4;  // Kpad complex = 2*Kpad bf16
-  d.b_bytes = (size_t)d.nrows_b_pad * d.Kpad * 4;
+  d.a_bytes = (size_t)d.rows_pad * d.Kpad * 2 * esz;  // Kpad complex = 2*Kpad elements
+  d.b_bytes = (size_t)d.nrows_b_pad * d.Kpad * 2 * esz;
   return d;
 }
 
 // planes: 1 (bf16x1), 2 (bf16x3: hi, lo), 3 (bf16x6: hi, lo, lo2)
+// planes 4 = tf32x3 (hi, lo in fp32 storage)
 inline size_t tc_workspace_bytes(long long K, long long rows, long long MB, int planes) {
-  TcDims d = tc_dims(K, rows, MB);
+  TcDims d = tc_dims(K, rows, MB, planes == 4 ? 4 : 2);
+  if (planes == 4) planes = 2;
   return (size_t)planes * (((d.a_bytes + 1023) & ~(size_t)1023) + ((d.b_bytes + 1023) & ~(size_t)1023));
 }
 
@@ -1053,13 +1096,17 @@ inline PFN_encodeTiled get_encode() {
 
 // bf16 [rows][cols_bf16] with row stride ld_bf16 (>= cols; boxes past the
 // extent read zeros), boxes of BK x box_rows, 128B swizzle
-inline CUtensorMap make_map(void* base, long long rows, long long cols_bf16, int box_rows, long long ld_bf16 = 0) {
+// (tf32: fp32 elements, boxes of 32 = the same 128 B rows)
+inline CUtensorMap make_map(void* base, long long rows, long long cols_bf16, int box_rows, long long ld_bf16 = 0,
+                            bool tf32 = false) {
   CUtensorMap m;
+  const int esz = tf32 ? 4 : 2;
   cuuint64_t dims[2] = {(cuuint64_t)cols_bf16, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)(ld_bf16 ? ld_bf16 : cols_bf16) * 2};
-  cuuint32_t box[2] = {(cuuint32_t)tc::BK, (cuuint32_t)box_rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld_bf16 ? ld_bf16 : cols_bf16) * esz};
+  cuuint32_t box[2] = {(cuuint32_t)(128 / esz), (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr,
+  CUresult r = get_encode()(&m, tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base,
+                            dims, strides, box, estr,
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fail(HSF_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
@@ -1095,6 +1142,7 @@ struct TcBuffers {
   __nv_bfloat162 *a_hi, *a_lo, *b_hi, *b_lo;
   __nv_bfloat162 *a_l2 = nullptr, *b_l2 = nullptr;  // bf16x6 third planes
   int planes = 2;
+  bool tf32 = false;  // tf32x3: fp32-storage K-major operands, kind::tf32
   bool mn = false;    // operands MN-major: A''^T [2*Kpad][rows_pad], B''^T [2*Kpad][nrows_b_pad] bf16
   long long K = 0;    // paths (operand k extent before padding)
 };
@@ -1110,10 +1158,12 @@ inline bool tc_mn(long long K) {
 
 inline TcBuffers tc_buffers(long long K, long long rows, long long MB, int planes, void* ws, size_t ws_bytes) {
   TcBuffers t;
-  t.d = tc_dims(K, rows, MB);
+  t.d = tc_dims(K, rows, MB, planes == 4 ? 4 : 2);
+  if (tc_workspace_bytes(K, rows, MB, planes) > ws_bytes) fail(HSF_ERR_INVALID_ARG, "tc workspace too small");
+  t.tf32 = planes == 4;
+  if (t.tf32) planes = 2;
   t.planes = planes;
   const bool x3 = planes >= 2;
-  if (tc_workspace_bytes(K, rows, MB, planes) > ws_bytes) fail(HSF_ERR_INVALID_ARG, "tc workspace too small");
   char* w = (char*)ws;
   auto take = [&](size_t b) {
     char* r = w;
@@ -1126,7 +1176,7 @@ inline TcBuffers tc_buffers(long long K, long long rows, long long MB, int plane
   t.b_lo = x3 ? (__nv_bfloat162*)take(t.d.b_bytes) : nullptr;
   t.a_l2 = planes >= 3 ? (__nv_bfloat162*)take(t.d.a_bytes) : nullptr;
   t.b_l2 = planes >= 3 ? (__nv_bfloat162*)take(t.d.b_bytes) : nullptr;
-  t.mn = tc_mn(K);
+  t.mn = !t.tf32 && tc_mn(K);
   t.K = K;
   return t;
 }
@@ -1143,8 +1193,13 @@ inline void tc_prep_a(const TcBuffers& t, const float2* leavesA, const float2* c
     if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("split_a_mn: ") + cudaGetErrorString(e));
     return;
   }
-  tc::split_a_kernel<<<dim3((unsigned)(t.d.rows_pad / 32), (unsigned)(t.d.Kpad / 32)), dim3(32, 8), 0, st>>>(
-      leavesA, cp, t.a_hi, t.a_lo, K, t.d.Kpad, MA, r0, rows, tp, ttab, t.a_l2);
+  const dim3 ga((unsigned)(t.d.rows_pad / 32), (unsigned)(t.d.Kpad / 32));
+  if (t.tf32)
+    tc::split_a_kernel<float2><<<ga, dim3(32, 8), 0, st>>>(leavesA, cp, (float2*)t.a_hi, (float2*)t.a_lo, K, t.d.Kpad,
+                                                           MA, r0, rows, tp, ttab, nullptr);
+  else
+    tc::split_a_kernel<__nv_bfloat162><<<ga, dim3(32, 8), 0, st>>>(leavesA, cp, t.a_hi, t.a_lo, K, t.d.Kpad, MA, r0,
+                                                                   rows, tp, ttab, t.a_l2);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("split_a: ") + cudaGetErrorString(e));
 }
@@ -1160,8 +1215,13 @@ inline void tc_prep_b(const TcBuffers& t, const float2* leavesB, long long K, lo
     if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("split_b_mn: ") + cudaGetErrorString(e));
     return;
   }
-  tc::split_b_kernel<<<dim3((unsigned)(t.d.nrows_b_pad / 64), (unsigned)(t.d.Kpad / 32)), dim3(32, 8), 0, st>>>(
-      leavesB, t.b_hi, t.b_lo, K, t.d.Kpad, MB, tp, ttab, t.b_l2);
+  const dim3 gb((unsigned)(t.d.nrows_b_pad / 64), (unsigned)(t.d.Kpad / 32));
+  if (t.tf32)
+    tc::split_b_kernel<float2><<<gb, dim3(32, 8), 0, st>>>(leavesB, (float2*)t.b_hi, (float2*)t.b_lo, K, t.d.Kpad, MB,
+                                                           tp, ttab, nullptr);
+  else
+    tc::split_b_kernel<__nv_bfloat162><<<gb, dim3(32, 8), 0, st>>>(leavesB, t.b_hi, t.b_lo, K, t.d.Kpad, MB, tp, ttab,
+                                                                   t.b_l2);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("split_b: ") + cudaGetErrorString(e));
 }
@@ -1170,27 +1230,29 @@ inline void tc_prep_b(const TcBuffers& t, const float2* leavesB, long long K, lo
 // (row0 a multiple of BM) into out[rows][2*MB] fp32
 inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row0, long long rows,
                     cudaStream_t st, bool accumulate = false) {
-  const bool x3 = t.planes >= 2, x6 = t.planes >= 3;
-  const long long kcols = 2 * t.d.Kpad;  // bf16 per operand row
+  const bool x3 = t.planes >= 2, x6 = t.planes >= 3, tf = t.tf32;
+  const long long kcols = 2 * t.d.Kpad;  // elements per K-major operand row
   if (row0 % tc::BM) fail(HSF_ERR_INVALID_ARG, "tc_gemm row offset not tile aligned");
   const long long rpad = (rows + tc::BM - 1) / tc::BM * tc::BM;
   if (row0 + rpad > t.d.rows_pad) fail(HSF_ERR_INVALID_ARG, "tc_gemm rows out of range");
+  // K-major A rows from row0 (bf16 pairs 4 B, tf32 pairs 8 B per complex)
+  auto ka = [&](void* base) { return (void*)((char*)base + (size_t)row0 * t.d.Kpad * (tf ? 8 : 4)); };
   // MN-major A: columns [row0, row0 + rows) of [2K][rows_pad], 64 x BK boxes
   __nv_bfloat16* a_hi_mn = (__nv_bfloat16*)t.a_hi + row0;
   __nv_bfloat16* a_lo_mn = x3 ? (__nv_bfloat16*)t.a_lo + row0 : nullptr;
   CUtensorMap mAh = t.mn ? make_map(a_hi_mn, 2 * t.K, rows, tc::BK, t.d.rows_pad)
-                         : make_map(t.a_hi + row0 * t.d.Kpad, rpad, kcols, tc::BM);
+                         : make_map(ka(t.a_hi), rpad, kcols, tc::BM, 0, tf);
   // MN-major B: [2K][2MB] valid of [kcols][nrows_b_pad] storage, 64 x BK
   // boxes; the padding rows / columns are read as zeros (TMA OOB fill), so
   // producers need not write them (operand-store passes do not)
   CUtensorMap mBh = t.mn ? make_map(t.b_hi, 2 * t.K, 2 * MB, tc::BK, t.d.nrows_b_pad)
-                           : make_map(t.b_hi, t.d.nrows_b_pad, kcols, tc::BN);
+                           : make_map(t.b_hi, t.d.nrows_b_pad, kcols, tc::BN, 0, tf);
   CUtensorMap mAl = !x3 ? mAh
                    : t.mn ? make_map(a_lo_mn, 2 * t.K, rows, tc::BK, t.d.rows_pad)
-                          : make_map(t.a_lo + row0 * t.d.Kpad, rpad, kcols, tc::BM);
+                          : make_map(ka(t.a_lo), rpad, kcols, tc::BM, 0, tf);
   CUtensorMap mBl = !x3 ? mBh
                    : t.mn ? make_map(t.b_lo, 2 * t.K, 2 * MB, tc::BK, t.d.nrows_b_pad)
-                            : make_map(t.b_lo, t.d.nrows_b_pad, kcols, tc::BN);
+                            : make_map(t.b_lo, t.d.nrows_b_pad, kcols, tc::BN, 0, tf);
   // bf16x6 third planes (pair kernel only)
   CUtensorMap mA2 = mAh, mB2 = mBh;
   if (x6) {
@@ -1202,7 +1264,7 @@ inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row
   tc::Params p;
   p.num_m = (int)(rpad / tc::BM);
   p.num_n = (int)(t.d.nrows_b_pad / tc::BN);
-  p.num_k = (int)(kcols / tc::BK);
+  p.num_k = (int)(kcols / (tf ? tc::BK / 2 : tc::BK));
   p.x3 = x3 ? 1 : 0;
   p.x6 = x6 ? 1 : 0;
   p.accumulate = accumulate ? 1 : 0;
@@ -1219,7 +1281,7 @@ inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row
   p.group_m = p.num_k <= 2 ? 16 : 0;
   if (const char* g = std::getenv("HSF_TC_GROUP_M")) p.group_m = std::atoi(g);
 
-  p.a_evict_last = ((long long)t.planes * rpad * kcols * 2 <= (64ll << 20)) ? 1 : 0;
+  p.a_evict_last = ((long long)t.planes * rpad * kcols * (tf ? 4 : 2) <= (64ll << 20)) ? 1 : 0;
   p.out = (float*)out;
   p.ldo = 2 * MB;
   p.rows = rows;
@@ -1234,7 +1296,7 @@ inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row
   CUtensorMap mO = make_out_map((float*)out, rows, 2 * MB);
   const char* pair_env = std::getenv("HSF_TC_PAIR");
   // (bf16x6: the pair kernel only -- three planes do not fit two single-CTA stages)
-  const bool pair = x6 || (rows > tc::BM && !(pair_env && pair_env[0] == '0'));
+  const bool pair = x6 || tf || (rows > tc::BM && !(pair_env && pair_env[0] == '0'));
   if (pair) {
     // CTA pairs: 256-row M tiles, each CTA loads half of every B tile
     static bool attr2 = false;
@@ -1247,15 +1309,27 @@ inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row
       if (e == cudaSuccess)
         e = cudaFuncSetAttribute(tc::tc_gemm2_kernel<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  tc::smem2_bytes(2, 1, 3));
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(tc::tc_gemm2_kernel<3, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 tc::smem2_bytes(3, 1));
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(tc::tc_gemm2_kernel<2, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 tc::smem2_bytes(2, 2));
       if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("tc2 smem attr: ") + cudaGetErrorString(e));
       attr2 = true;
     }
-    CUtensorMap mBh2 = t.mn ? mBh : make_map(t.b_hi, t.d.nrows_b_pad, kcols, tc::BN / 2);
-    CUtensorMap mBl2 = t.mn ? mBl : x3 ? make_map(t.b_lo, t.d.nrows_b_pad, kcols, tc::BN / 2) : mBh2;
+    CUtensorMap mBh2 = t.mn ? mBh : make_map(t.b_hi, t.d.nrows_b_pad, kcols, tc::BN / 2, 0, tf);
+    CUtensorMap mBl2 = t.mn ? mBl : x3 ? make_map(t.b_lo, t.d.nrows_b_pad, kcols, tc::BN / 2, 0, tf) : mBh2;
     p.num_m = (int)((rows + 2 * tc::BM - 1) / (2 * tc::BM));
     const long long tiles = (long long)p.num_m * p.num_n;
     const int grid = 2 * (int)std::min<long long>(tiles, num_sms() / 2);
-    if (x6)  // 2 stages x 96 KB + one staging box per epilogue warp
+    if (tf && p.num_k <= 2)
+      tc::tc_gemm2_kernel<2, 2, true><<<grid, tc::THREADS, tc::smem2_bytes(2, 2), st>>>(mAh, mAl, mBh2, mBl2, mAh, mBh2,
+                                                                                        mO, p);
+    else if (tf)
+      tc::tc_gemm2_kernel<3, 1, true><<<grid, tc::THREADS, tc::smem2_bytes(3, 1), st>>>(mAh, mAl, mBh2, mBl2, mAh, mBh2,
+                                                                                        mO, p);
+    else if (x6)  // 2 stages x 96 KB + one staging box per epilogue warp
       tc::tc_gemm2_kernel<2, 1><<<grid, tc::THREADS, tc::smem2_bytes(2, 1, 3), st>>>(mAh, mAl, mBh2, mBl2, mA2, mB2,
                                                                                      mO, p);
     else if (p.num_k <= 2)

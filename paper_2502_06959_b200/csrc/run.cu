@@ -291,7 +291,10 @@ struct Layout {
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 // split-bf16 operand planes per precision mode
-static int tc_planes(hsf_precision p) { return p == HSF_PREC_BF16X6 ? 3 : p == HSF_PREC_BF16X3 ? 2 : 1; }
+// (4 = tf32x3: hi + lo planes of fp32-storage tf32 values)
+static int tc_planes(hsf_precision p) {
+  return p == HSF_PREC_TF32X3 ? 4 : p == HSF_PREC_BF16X6 ? 3 : p == HSF_PREC_BF16X3 ? 2 : 1;
+}
 constexpr size_t kHostChunkBytes = (size_t)32 << 20;  // D2H of chunk i overlaps the path-sum of chunk i+1
 
 static uint64_t nodes_at(const std::vector<int32_t>& ranks, int L, uint64_t p0, uint64_t p1) {
@@ -318,7 +321,7 @@ static Layout make_layout(const Plan& P, const hsf_run_args& a, size_t elem) {
   }
   L.K = L.p1 - L.p0;
   L.prec = a.precision;
-  if ((int)L.prec < (int)HSF_PREC_AUTO || (int)L.prec > (int)HSF_PREC_BF16X6)
+  if ((int)L.prec < (int)HSF_PREC_AUTO || (int)L.prec > (int)HSF_PREC_TF32X3)
     fail(HSF_ERR_INVALID_ARG, "unknown precision mode " + std::to_string((int)L.prec));
   if (L.prec == HSF_PREC_AUTO) L.prec = (P.opts.dtype == HSF_C64) ? HSF_PREC_BF16X3 : HSF_PREC_SIMT;
   if (P.opts.dtype == HSF_C128 && L.prec != HSF_PREC_SIMT) fail(HSF_ERR_UNSUPPORTED, "complex128 path-sum is SIMT fp64 only");
@@ -393,7 +396,7 @@ static Layout make_layout(const Plan& P, const hsf_run_args& a, size_t elem) {
       L.off_pout = off;
       off = align_up(off + ((size_t)1 << P.n) * elem);
     }
-    if (L.prec == HSF_PREC_BF16X3 || L.prec == HSF_PREC_BF16X1 || L.prec == HSF_PREC_BF16X6) {
+    if (L.prec != HSF_PREC_SIMT) {
       L.tc_bytes = tc_workspace_bytes((long long)L.K, (long long)(L.r1 - L.r0), 1ll << nB, tc_planes(L.prec));
       L.off_tc = off;
       off = align_up(off + L.tc_bytes);

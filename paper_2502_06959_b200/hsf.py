@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libhsf.so")
 
 HSF_C64, HSF_C128 = 0, 1
-PREC = {"auto": 0, "simt": 1, "bf16x3": 2, "bf16x1": 3, "bf16x6": 4}
+PREC = {"auto": 0, "simt": 1, "bf16x3": 2, "bf16x1": 3, "bf16x6": 4, "tf32x3": 5}
 STATUS = {}
 
 

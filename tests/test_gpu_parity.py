@@ -241,7 +241,7 @@ def test_bf16x1_is_lower_precision(torch):
 
 
 @pytest.mark.parametrize("name", ["c2", "c4", "c5"])
-def test_bf16x6_precision(torch, name):
+def test_precision_modes(torch, name):
     # three-way split, 6 products (bf16x6 reported beside bf16x3):
     # the dropped terms are ~2^-24 relative; what remains is the tensor core's
     # fp32 accumulation over 6 x 2K/16 MMA steps (measured 1.0-1.7e-6 relL2 on
@@ -251,9 +251,11 @@ def test_bf16x6_precision(torch, name):
     n, g = O.parse_circuit(inst.text)
     ref = O.schrodinger(n, g)
     rel = {}
-    for prec in ("simt", "bf16x3", "bf16x6"):
+    for prec in ("simt", "bf16x3", "bf16x6", "tf32x3"):
         x, _ = gpu_full(torch, inst, dtype="c64", precision=prec)
         rel[prec] = np.linalg.norm(x - ref) / np.linalg.norm(ref)
+    # tf32x3 (kind::tf32, hi+lo, 3 products): dropped lo*lo ~2^-22
+    assert rel["tf32x3"] < 1e-5 and rel["tf32x3"] <= 1.2 * rel["bf16x3"], rel
     assert rel["bf16x6"] < 1e-5 and rel["bf16x6"] <= rel["bf16x3"], rel
     if name != "c5":  # c5's cancelling fan-out sums sit at the accumulation floor for both
         assert rel["bf16x6"] < 0.6 * rel["bf16x3"], rel
@@ -271,7 +273,7 @@ def test_bf16x3_ragged_rows_and_paths(torch, b_layout, monkeypatch):
     rows = 1 << P.n_a
     for pr, rr in [((3, 200), (5, 37)), ((0, 256), (0, rows)), ((17, 18), (1, 2))]:
         ref, _ = gpu_full(torch, inst, precision="simt", path_range=pr, row_range=rr)
-        for prec in ("bf16x3", "bf16x6"):
+        for prec in ("bf16x3", "bf16x6", "tf32x3"):
             got, _ = gpu_full(torch, inst, precision=prec, path_range=pr, row_range=rr)
             assert np.abs(got - ref).max() <= 1e-5 * max(1.0, np.abs(ref).max() * 100), prec
 
