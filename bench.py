@@ -309,6 +309,30 @@ def main():
     value = P.n_paths / (t_step * 1e-3)
     amps = N_out / (t_step * 1e-3)
 
+    # the full-output GEMM's other precision modes, timed the same way beside
+    # the default (bf16x6 and tf32x3 reported beside bf16x3)
+    prec_alt = None
+    if full and world == 1 and a.precision in ("auto", "bf16x3") and inst.dtype == "c64":
+        prec_alt = {}
+        rr_alt = (0, prefix_rows) if prefix else None
+        for alt in ("bf16x6", "tf32x3"):
+            try:
+                for _ in range(2):
+                    P.run(out, path_range=None, row_range=rr_alt, precision=alt)
+                ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(5)]
+                for i in range(5):
+                    flush.fill_(i & 0xFF)
+                    ev2[i][0].record(stream)
+                    P.run(out, path_range=None, row_range=rr_alt, precision=alt)
+                    ev2[i][1].record(stream)
+                torch.cuda.synchronize()
+                t_alt = statistics.mean(s_.elapsed_time(e_) for s_, e_ in ev2)
+                prec_alt[alt] = {"ms_per_step": t_alt, "value": P.n_paths / (t_alt * 1e-3)}
+            except Exception as ex:  # noqa: BLE001 - reported, not fatal
+                prec_alt[alt] = {"error": str(ex)[:200]}
+        P.run(out, path_range=None, row_range=rr_alt, precision=a.precision)  # restore the default's workspace
+        torch.cuda.synchronize()
+
     # end-to-end through the public API with host buffers: plan (host SVD etc.)
     # + table upload + run + copy of the result to pinned host memory
     e2e = None
@@ -474,7 +498,8 @@ def main():
                 "plan_s": t_plan, "roofline": roof, "roofline_other": roof_other, "cpu_baseline": cpu,
                 "e2e": e2e, "joint_blocks": P.n_joint_blocks, "separate_cuts": P.n_units - P.n_joint_blocks,
                 "folded_units": P.fold_units if not full else 0, "standard_hsf": std,
-                "gpu_launches": n_launch, "clocks": clk.summary()}
+                "gpu_launches": n_launch, "clocks": clk.summary(),
+                "precision_modes": prec_alt}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()  # rank 0 ran the e2e / CPU legs alone; leave together
