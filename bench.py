@@ -42,8 +42,9 @@ def _args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--standard", action="store_true",
                     help="also time standard HSF (every crossing gate cut alone) on the same output: T/J")
-    ap.add_argument("--collective", default="auto", choices=["auto", "reduce_scatter", "allreduce", "rows"],
-                    help="N>1 exchange (paper_2502_06959_b200/dist.py); auto = cheapest for the output mode")
+    ap.add_argument("--collective", default="auto", choices=["auto", "reduce_scatter", "allreduce", "rows", "fused_rs"],
+                    help="N>1 exchange (paper_2502_06959_b200/dist.py); auto = cheapest for the output mode; "
+                         "fused_rs = GEMM epilogue reduce-adds into the owners' shards over peer memory")
     return ap.parse_args()
 
 
@@ -256,6 +257,8 @@ def main():
         out = torch.empty(rows << P.n_b, dtype=cdt, device="cuda")
         shard = torch.empty(N_out // world, dtype=cdt, device="cuda") if mode == "reduce_scatter" and world > 1 \
             else None
+        if mode == "fused_rs":  # no partial output: each rank's shard, mapped into every rank (CUDA IPC)
+            out = D.PeerShards(torch.zeros(N_out // world, dtype=cdt, device="cuda"))
         bits_d = None
     else:
         N_out = len(inst.bitstrings)
@@ -268,8 +271,11 @@ def main():
         def partial(path_range, row_range, o):
             if prefix:
                 row_range = (0, prefix_rows)
-            ph = P.run(o, bitstrings=bits_d, path_range=path_range, row_range=row_range, precision=a.precision,
-                       timings=timed)
+            if isinstance(o, D.PeerShards):
+                ph = P.run(None, path_range=path_range, precision=a.precision, timings=timed, out_shards=o.ptrs)
+            else:
+                ph = P.run(o, bitstrings=bits_d, path_range=path_range, row_range=row_range, precision=a.precision,
+                           timings=timed)
             if timed:
                 phases.append(ph)
         D.sharded_step(sh, partial, out, shard)
@@ -312,7 +318,8 @@ def main():
     # the full-output GEMM's other precision modes, timed the same way beside
     # the default (bf16x6 and tf32x3 reported beside bf16x3)
     prec_alt = None
-    if full and world == 1 and a.precision in ("auto", "bf16x3") and inst.dtype == "c64":
+    if full and world == 1 and a.precision in ("auto", "bf16x3") and inst.dtype == "c64" and \
+            not isinstance(out, D.PeerShards):
         prec_alt = {}
         rr_alt = (0, prefix_rows) if prefix else None
         for alt in ("bf16x6", "tf32x3"):

@@ -211,6 +211,18 @@ typedef struct {
   int32_t accumulate;           /* 1 => out += this run's result (device output only;
                                    e.g. path ranges run in chunks, or partial sums
                                    combined on one GPU); 0 => out is overwritten */
+  /* Fused reduce-scatter (full output, tensor-core precisions, all rows):
+   * n_out_shards in 1..8 device pointers, possibly another GPU's memory
+   * (CUDA IPC / peer access); output rows [o*shard_rows, (o+1)*shard_rows)
+   * are reduce-added (TMA .add, fp32 element-wise) into out_shards[o] by the
+   * GEMM epilogue itself, tile by tile -- the K-split partial sums of several
+   * ranks land in each owner's shard without a separate collective.
+   * shard_rows * n_out_shards == 2^nA, shard_rows a multiple of 256.  The
+   * caller zeroes the shards before the ranks' runs and synchronises after.
+   * `out` is ignored; n_out_shards == 0 => normal output. */
+  void* const* out_shards;
+  int32_t n_out_shards;
+  uint64_t shard_rows;
 } hsf_run_args;
 
 /* hsf_run — evaluate the paths [path_begin, path_end) on the GPU: path-tree
@@ -241,6 +253,15 @@ size_t hsf_last_error(char* buf, size_t len);
  * the pass does not exist.  Host only. */
 size_t hsf_debug_pass_source(const hsf_plan_t* plan, int32_t variant, int32_t half, int32_t pass, char* buf,
                              size_t len);
+
+/* CUDA IPC of fused reduce-scatter shards (plumbing for out_shards across
+ * processes): hsf_ipc_export writes the 64-byte IPC handle of the allocation
+ * holding dev_ptr and dev_ptr's offset in it; another process of the same
+ * node maps it with hsf_ipc_import (peer access enabled lazily) and unmaps it
+ * with hsf_ipc_release(ptr, offset).  The exporter keeps the allocation alive. */
+hsf_status hsf_ipc_export(const void* dev_ptr, void* handle_out, uint64_t* offset_out);
+hsf_status hsf_ipc_import(const void* handle, uint64_t offset, void** dev_ptr_out);
+hsf_status hsf_ipc_release(void* dev_ptr, uint64_t offset);
 
 /* Library build identification string (compile flags, arch). */
 const char* hsf_version(void);

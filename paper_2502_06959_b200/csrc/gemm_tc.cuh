@@ -31,6 +31,7 @@
 #include <stdint.h>
 
 #include <cstdlib>
+#include <cstring>
 
 #include "hsf_internal.h"
 
@@ -59,6 +60,8 @@ struct Params {
 
   int x3;
   int x6;                   // bf16x6: third operand plane (lo2), 6 products (pair kernel only)
+  int n_maps;               // > 0: fused reduce-scatter -- output rows [o*rows_per_map, +rows_per_map)
+  int rows_per_map;         //      are TMA-reduce-added into OutMaps::m[o] (row o*rows_per_map -> 0)
   float* out;               // D, row-major, ld = ldo floats
   long long ldo;
   long long rows, cols;     // valid D extent (rows of this call, 2*MB)
@@ -458,12 +461,19 @@ __device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
 // is output-write-bound, so a second box keeps two TMA stores per warp in flight)
 // TF32: kind::tf32 on fp32-storage operands (tf32x3; K-major only, boxes of
 // 32 fp32 = the same 128 B rows)
+// Destination shards of the fused reduce-scatter (tensor maps of device or
+// peer-GPU memory: each owner's row shard)
+constexpr int kMaxOutMaps = 8;
+struct OutMaps {
+  CUtensorMap m[kMaxOutMaps];
+};
+
 template <int NST, int EBUF, bool TF32 = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     tc_gemm2_kernel(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUtensorMap mA_lo,
                     const __grid_constant__ CUtensorMap mB_hi, const __grid_constant__ CUtensorMap mB_lo,
                     const __grid_constant__ CUtensorMap mA_l2, const __grid_constant__ CUtensorMap mB_l2,
-                    const __grid_constant__ CUtensorMap mOut, const Params p) {
+                    const __grid_constant__ CUtensorMap mOut, const Params p, const __grid_constant__ OutMaps om) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[NST], empty_bar[NST], tfull_bar[2], tempty_bar[2];
   __shared__ uint32_t tmem_base_sh;
@@ -664,10 +674,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) {
-          if (p.accumulate)
+          if (p.n_maps) {  // fused reduce-scatter: this CTA's 128 rows belong to one owner shard
+            const int o = row0 / p.rows_per_map;
+            tma_reduce_add_2d(&om.m[o], stg, nb * BN + c * 32, row0 - o * p.rows_per_map + q * 32, st_pol);
+          } else if (p.accumulate) {
             tma_reduce_add_2d(&mOut, stg, nb * BN + c * 32, row0 + q * 32, st_pol);
-          else
+          } else {
             tma_store_2d(&mOut, stg, nb * BN + c * 32, row0 + q * 32, st_pol);
+          }
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
       }
@@ -1228,8 +1242,12 @@ inline void tc_prep_b(const TcBuffers& t, const float2* leavesB, long long K, lo
 
 // K5: the persistent tcgen05 GEMM over operand rows [row0, row0 + rows)
 // (row0 a multiple of BM) into out[rows][2*MB] fp32
+// shards (fused reduce-scatter): n_shards device pointers (local or peer-GPU
+// memory), shard o receiving rows [o*shard_rows, (o+1)*shard_rows) of this
+// call by TMA reduce-add; `out` unused then
 inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row0, long long rows,
-                    cudaStream_t st, bool accumulate = false) {
+                    cudaStream_t st, bool accumulate = false, void* const* shards = nullptr, int n_shards = 0,
+                    long long shard_rows = 0) {
   const bool x3 = t.planes >= 2, x6 = t.planes >= 3, tf = t.tf32;
   const long long kcols = 2 * t.d.Kpad;  // elements per K-major operand row
   if (row0 % tc::BM) fail(HSF_ERR_INVALID_ARG, "tc_gemm row offset not tile aligned");
@@ -1267,6 +1285,17 @@ inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row
   p.num_k = (int)(kcols / (tf ? tc::BK / 2 : tc::BK));
   p.x3 = x3 ? 1 : 0;
   p.x6 = x6 ? 1 : 0;
+  p.n_maps = 0;
+  p.rows_per_map = 0;
+  tc::OutMaps om;
+  std::memset(&om, 0, sizeof(om));
+  if (n_shards > 0) {
+    if (n_shards > tc::kMaxOutMaps || shard_rows % (2 * tc::BM) || shard_rows * n_shards != rows)
+      fail(HSF_ERR_INVALID_ARG, "fused reduce-scatter: 1..8 shards of a multiple of 256 rows covering all rows");
+    for (int o = 0; o < n_shards; ++o) om.m[o] = make_out_map((float*)shards[o], shard_rows, 2 * MB);
+    p.n_maps = n_shards;
+    p.rows_per_map = (int)shard_rows;
+  }
   p.accumulate = accumulate ? 1 : 0;
   p.mn = t.mn ? 1 : 0;
   // M-fastest raster: the ~148 concurrent tiles share one B tile (read once
@@ -1293,10 +1322,10 @@ inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row
     if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("tc smem attr: ") + cudaGetErrorString(e));
     attr = true;
   }
-  CUtensorMap mO = make_out_map((float*)out, rows, 2 * MB);
+  CUtensorMap mO = n_shards > 0 ? om.m[0] : make_out_map((float*)out, rows, 2 * MB);
   const char* pair_env = std::getenv("HSF_TC_PAIR");
   // (bf16x6: the pair kernel only -- three planes do not fit two single-CTA stages)
-  const bool pair = x6 || tf || (rows > tc::BM && !(pair_env && pair_env[0] == '0'));
+  const bool pair = x6 || tf || n_shards > 0 || (rows > tc::BM && !(pair_env && pair_env[0] == '0'));
   if (pair) {
     // CTA pairs: 256-row M tiles, each CTA loads half of every B tile
     static bool attr2 = false;
@@ -1325,19 +1354,19 @@ inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row
     const int grid = 2 * (int)std::min<long long>(tiles, num_sms() / 2);
     if (tf && p.num_k <= 2)
       tc::tc_gemm2_kernel<2, 2, true><<<grid, tc::THREADS, tc::smem2_bytes(2, 2), st>>>(mAh, mAl, mBh2, mBl2, mAh, mBh2,
-                                                                                        mO, p);
+                                                                                        mO, p, om);
     else if (tf)
       tc::tc_gemm2_kernel<3, 1, true><<<grid, tc::THREADS, tc::smem2_bytes(3, 1), st>>>(mAh, mAl, mBh2, mBl2, mAh, mBh2,
-                                                                                        mO, p);
+                                                                                        mO, p, om);
     else if (x6)  // 2 stages x 96 KB + one staging box per epilogue warp
       tc::tc_gemm2_kernel<2, 1><<<grid, tc::THREADS, tc::smem2_bytes(2, 1, 3), st>>>(mAh, mAl, mBh2, mBl2, mA2, mB2,
-                                                                                     mO, p);
+                                                                                     mO, p, om);
     else if (p.num_k <= 2)
       tc::tc_gemm2_kernel<2, 2><<<grid, tc::THREADS, tc::smem2_bytes(2, 2), st>>>(mAh, mAl, mBh2, mBl2, mAh, mBh2,
-                                                                                  mO, p);
+                                                                                  mO, p, om);
     else
       tc::tc_gemm2_kernel<3, 1><<<grid, tc::THREADS, tc::smem2_bytes(3, 1), st>>>(mAh, mAl, mBh2, mBl2, mAh, mBh2,
-                                                                                  mO, p);
+                                                                                  mO, p, om);
   } else {
     const long long tiles = (long long)p.num_m * p.num_n;
     const int grid = (int)std::min<long long>(tiles, num_sms());

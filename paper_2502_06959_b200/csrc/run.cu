@@ -401,7 +401,7 @@ static Layout make_layout(const Plan& P, const hsf_run_args& a, size_t elem) {
       L.off_tc = off;
       off = align_up(off + L.tc_bytes);
     }
-    if (!a.out_on_device) {
+    if (!a.out_on_device && a.n_out_shards == 0) {
       // host output: rows are produced in chunks of <= kHostChunkBytes into two
       // device staging buffers; the D2H copy of one chunk overlaps the
       // path-sum of the next (bounded device memory for any output size)
@@ -669,7 +669,7 @@ static void run_core_bits(Plan* P, DeviceState* d, const Layout& L, const hsf_ru
 // (device, row-major [nrows][2^nB]); lo is a multiple of the tensor-core M tile
 template <typename R>
 static void run_core_full(Plan* P, DeviceState* d, const Layout& L, cudaStream_t st, uint64_t lo, uint64_t nrows,
-                          typename cplx<R>::T* out, bool accumulate) {
+                          typename cplx<R>::T* out, bool accumulate, const hsf_run_args* shards = nullptr) {
   using C = typename cplx<R>::T;
   char* ws = (char*)d->ws;
   const int nA = P->n - P->n_low, nB = P->n_low;
@@ -685,7 +685,11 @@ static void run_core_full(Plan* P, DeviceState* d, const Layout& L, cudaStream_t
     if (sizeof(R) != 4) fail(HSF_ERR_UNSUPPORTED, "tensor-core path-sum needs complex64");
     TcBuffers t = tc_buffers(K, (long long)(L.r1 - L.r0), 1ll << nB, tc_planes(L.prec), ws + L.off_tc,
                              L.tc_bytes);
-    tc_gemm(t, (float2*)out, 1ll << nB, (long long)lo, (long long)nrows, st, accumulate);
+    if (shards && shards->n_out_shards > 0)
+      tc_gemm(t, nullptr, 1ll << nB, (long long)lo, (long long)nrows, st, true, shards->out_shards,
+              shards->n_out_shards, (long long)shards->shard_rows);
+    else
+      tc_gemm(t, (float2*)out, 1ll << nB, (long long)lo, (long long)nrows, st, accumulate);
   }
 }
 
@@ -724,6 +728,8 @@ static void run_all(Plan* P, DeviceState* d, const Layout& L, const hsf_run_args
     permute_out_kernel<C><<<(unsigned)std::min<long long>((nout + 255) / 256, 148ll * 32), 256, 0, st>>>(
         tmp, (C*)a.out, nout, d->perm_tab, a.accumulate);
     CK(cudaGetLastError());
+  } else if (a.n_out_shards > 0) {  // fused reduce-scatter into the owners' shards
+    run_core_full<R>(P, d, L, st, 0, L.r1 - L.r0, nullptr, true, &a);
   } else if (a.out_on_device) {
     run_core_full<R>(P, d, L, st, 0, L.r1 - L.r0, (C*)a.out, a.accumulate != 0);
   } else {
@@ -749,8 +755,22 @@ static void run_all(Plan* P, DeviceState* d, const Layout& L, const hsf_run_args
 static void run(Plan* P, const hsf_run_args& a) {
   DeviceState* d = ensure_device(P, a.device);
   Layout L = make_layout(*P, a, d->elem);
-  if (!a.out) fail(HSF_ERR_INVALID_ARG, "out is NULL");
-  if (a.accumulate && !a.out_on_device) fail(HSF_ERR_INVALID_ARG, "accumulate needs a device output buffer");
+  if (a.n_out_shards < 0 || a.n_out_shards > 8) fail(HSF_ERR_INVALID_ARG, "n_out_shards must be in 0..8");
+  if (a.n_out_shards > 0) {
+    if (L.bits_mode || L.prec == HSF_PREC_SIMT || P->permuted || L.r0 != 0 || L.r1 != (1ull << (P->n - P->n_low)))
+      fail(HSF_ERR_UNSUPPORTED, "fused reduce-scatter needs a full-output tensor-core run over all rows of a "
+                                "contiguous cut");
+    if (!a.out_shards || a.shard_rows == 0 || a.shard_rows % 256 ||
+        a.shard_rows * (uint64_t)a.n_out_shards != (1ull << (P->n - P->n_low)))
+      fail(HSF_ERR_INVALID_ARG, "out_shards: n_out_shards pointers of shard_rows rows (a multiple of 256) "
+                                "covering all 2^nA rows");
+    for (int o = 0; o < a.n_out_shards; ++o)
+      if (!a.out_shards[o]) fail(HSF_ERR_INVALID_ARG, "out_shards[o] is NULL");
+  } else if (!a.out) {
+    fail(HSF_ERR_INVALID_ARG, "out is NULL");
+  }
+  if (a.accumulate && !a.out_on_device && a.n_out_shards == 0)
+    fail(HSF_ERR_INVALID_ARG, "accumulate needs a device output buffer");
   ensure_ws(d, L.total);
   cudaStream_t st = (cudaStream_t)a.cuda_stream;
   int heads = 0;
@@ -760,13 +780,16 @@ static void run(Plan* P, const hsf_run_args& a) {
   const bool timed = a.phase_ms != nullptr;
   try {
     const char* ng = std::getenv("HSF_NO_GRAPH");
-    const bool graph = P->opts.graphs && a.out_on_device && (!L.bits_mode || a.bits_on_device) && !(ng && ng[0] == '1');
+    const bool graph = P->opts.graphs && (a.out_on_device || a.n_out_shards > 0) && (!L.bits_mode || a.bits_on_device) &&
+                       !(ng && ng[0] == '1');
     if (graph) {
       // the key holds everything the captured launches depend on
       std::vector<uint64_t> key = {(uint64_t)(uintptr_t)a.out, (uint64_t)(uintptr_t)a.bitstrings, a.n_bitstrings,
                                    L.p0, L.p1, L.r0, L.r1, (uint64_t)L.prec, (uint64_t)a.accumulate,
                                    (uint64_t)timed, (uint64_t)L.fold, (uint64_t)(uintptr_t)d->ws,
-                                   (uint64_t)(uintptr_t)d->cp, (uint64_t)L.total};
+                                   (uint64_t)(uintptr_t)d->cp, (uint64_t)L.total, (uint64_t)a.n_out_shards,
+                                   a.shard_rows};
+      for (int o = 0; o < a.n_out_shards; ++o) key.push_back((uint64_t)(uintptr_t)a.out_shards[o]);
       if (!d->gexec || key != d->gkey) {
         if (d->gexec) CK(cudaGraphExecDestroy(d->gexec));
         d->gexec = nullptr;
@@ -924,6 +947,50 @@ hsf_status hsf_run(hsf_plan_t* plan, const hsf_run_args* args) {
   ABI_GUARD({
     if (!plan || !args) fail(HSF_ERR_INVALID_ARG, "NULL argument");
     run(reinterpret_cast<Plan*>(plan), *args);
+  })
+}
+
+// ---- CUDA IPC of output shards (fused reduce-scatter plumbing) ----------
+typedef CUresult (*PFN_memGetAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+hsf_status hsf_ipc_export(const void* dev_ptr, void* handle_out, uint64_t* offset_out) {
+  ABI_GUARD({
+    if (!dev_ptr || !handle_out || !offset_out) fail(HSF_ERR_INVALID_ARG, "NULL argument");
+    static PFN_memGetAddressRange range = nullptr;
+    if (!range) {
+      void* f = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+          q != cudaDriverEntryPointSuccess || !f)
+        fail(HSF_ERR_CUDA, "cuMemGetAddressRange entry point unavailable");
+      range = (PFN_memGetAddressRange)f;
+    }
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range(&base, &size, (CUdeviceptr)(uintptr_t)dev_ptr) != CUDA_SUCCESS)
+      fail(HSF_ERR_INVALID_ARG, "pointer is not device memory of this context");
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, (void*)(uintptr_t)base));
+    std::memcpy(handle_out, &h, sizeof(h));
+    *offset_out = (uint64_t)((uintptr_t)dev_ptr - (uintptr_t)base);
+  })
+}
+
+hsf_status hsf_ipc_import(const void* handle, uint64_t offset, void** dev_ptr_out) {
+  ABI_GUARD({
+    if (!handle || !dev_ptr_out) fail(HSF_ERR_INVALID_ARG, "NULL argument");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    void* base = nullptr;
+    CK(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    *dev_ptr_out = (char*)base + offset;
+  })
+}
+
+hsf_status hsf_ipc_release(void* dev_ptr, uint64_t offset) {
+  ABI_GUARD({
+    if (!dev_ptr) fail(HSF_ERR_INVALID_ARG, "NULL argument");
+    CK(cudaIpcCloseMemHandle((char*)dev_ptr - offset));
   })
 }
 

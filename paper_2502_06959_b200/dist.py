@@ -17,6 +17,13 @@ Modes (`mode`):
   "rows"            every rank evaluates ALL paths but writes only its row
                     shard (rows as above) -- no collective on the data path.
                     The recommended c4 mode.
+  "fused_rs"        paths split as in reduce_scatter, but there is no partial
+                    output and no collective call: every rank's GEMM epilogue
+                    reduce-adds (TMA .add) each output tile straight into the
+                    owner rank's row shard over peer memory (CUDA IPC,
+                    NVLink on the box) -- the GEMM -> reduce-scatter of
+                    SURVEY.md §8(f) row 3 as one kernel.  Full-output
+                    tensor-core runs; 2^nA / G a multiple of 256 rows.
 
 The per-rank evaluation is a callable `partial(path_range, row_range, out)`
 so the partition and collective logic can be exercised on CPU with gloo
@@ -26,7 +33,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
-MODES = ("allreduce", "reduce_scatter", "rows")
+MODES = ("allreduce", "reduce_scatter", "rows", "fused_rs")
 
 
 @dataclass(frozen=True)
@@ -69,27 +76,70 @@ def make_shard(mode: str, n_paths: int, n_a: int, rank: int, world: int, full_ou
         raise ValueError(f"unknown mode {mode!r}")
     if not full_output and mode != "allreduce":
         raise ValueError("bitstring runs use mode='allreduce'")
-    if mode in ("reduce_scatter", "rows") and (1 << n_a) % world:
+    if mode in ("reduce_scatter", "rows", "fused_rs") and (1 << n_a) % world:
         raise ValueError("row sharding needs world to divide 2^n_A")
     pr = path_range_for_rank(n_paths, rank, world)
     if mode == "allreduce":
         return Shard(mode, pr, None, None)
     rr = row_range_for_rank(n_a, rank, world)
-    if mode == "reduce_scatter":
+    if mode in ("reduce_scatter", "fused_rs"):
         return Shard(mode, pr, None, rr)
     return Shard(mode, (0, n_paths), rr, rr)
+
+
+class PeerShards:
+    """Every rank's row shard, mapped into this process (fused_rs mode):
+    `ptrs[r]` is rank r's shard (CUDA IPC import; this rank's own pointer for
+    itself).  The handles travel through torch.distributed (any backend)."""
+
+    def __init__(self, shard_out, group=None):
+        import torch.distributed as dist
+        from . import hsf as H
+        self.local = shard_out
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        mine = H.ipc_export(shard_out) if world > 1 else None
+        allh = [None] * world
+        if world > 1:
+            dist.all_gather_object(allh, mine, group=group)
+        self.ptrs, self._opened = [], []
+        for r in range(world):
+            if r == rank:
+                self.ptrs.append(shard_out.data_ptr())
+            else:
+                p = H.ipc_import(allh[r][0], allh[r][1])
+                self.ptrs.append(p)
+                self._opened.append((p, allh[r][1]))
+
+    def close(self):
+        from . import hsf as H
+        for p, off in self._opened:
+            H.ipc_release(p, off)
+        self._opened = []
 
 
 def sharded_step(shard: Shard, partial, out, shard_out=None, group=None):
     """One rank's step: evaluate, then the mode's collective.
 
-    out       : full-size output buffer (allreduce / reduce_scatter), or the
-                row shard itself (rows mode)
+    out       : full-size output buffer (allreduce / reduce_scatter), the
+                row shard itself (rows mode), or a PeerShards (fused_rs)
     shard_out : reduce_scatter destination (rows shard)
     Returns the tensor holding this rank's result."""
     import torch
     import torch.distributed as dist
 
+    if shard.mode == "fused_rs":
+        # zero the own shard, all ranks' adds land in it, then everyone waits
+        sync = torch.cuda.synchronize if out.local.is_cuda else (lambda: None)
+        out.local.zero_()
+        if dist.is_initialized():
+            sync()
+            dist.barrier(group=group)
+        partial(shard.path_range, None, out)
+        sync()
+        if dist.is_initialized():
+            dist.barrier(group=group)
+        return out.local
     partial(shard.path_range, shard.row_range, out)
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     if world == 1 or shard.mode == "rows":
@@ -106,5 +156,8 @@ def run_sharded(plan, out, shard: Shard, shard_out=None, bitstrings=None, precis
     """GPU entry: `plan.run` (libhsf.so, C ABI) on this rank's range, then the
     collective over NCCL."""
     def partial(path_range, row_range, o):
-        plan.run(o, bitstrings=bitstrings, path_range=path_range, row_range=row_range, precision=precision)
+        if isinstance(o, PeerShards):
+            plan.run(None, path_range=path_range, precision=precision, out_shards=o.ptrs)
+        else:
+            plan.run(o, bitstrings=bitstrings, path_range=path_range, row_range=row_range, precision=precision)
     return sharded_step(shard, partial, out, shard_out, group)

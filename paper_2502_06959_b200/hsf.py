@@ -57,13 +57,15 @@ class _RunArgs(C.Structure):
                 ("out", C.c_void_p), ("out_on_device", C.c_int32), ("path_begin", C.c_uint64),
                 ("path_end", C.c_uint64), ("row_begin", C.c_uint64), ("row_end", C.c_uint64),
                 ("cuda_stream", C.c_void_p), ("precision", C.c_int), ("device", C.c_int32),
-                ("phase_ms", C.POINTER(C.c_double)), ("accumulate", C.c_int32)]
+                ("phase_ms", C.POINTER(C.c_double)), ("accumulate", C.c_int32),
+                ("out_shards", C.POINTER(C.c_void_p)), ("n_out_shards", C.c_int32), ("shard_rows", C.c_uint64)]
 
 
 _lib = None
 
 EXPORTS = ["hsf_plan_opts_default", "hsf_plan", "hsf_plan_info_get", "hsf_run", "hsf_workspace_bytes",
-           "hsf_plan_free", "hsf_status_str", "hsf_last_error", "hsf_version", "hsf_debug_pass_source"]
+           "hsf_plan_free", "hsf_status_str", "hsf_last_error", "hsf_version", "hsf_debug_pass_source",
+           "hsf_ipc_export", "hsf_ipc_import", "hsf_ipc_release"]
 
 
 def lib():
@@ -90,7 +92,11 @@ def lib():
     L.hsf_version.restype = C.c_char_p
     L.hsf_debug_pass_source.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_char_p, C.c_size_t]
     L.hsf_debug_pass_source.restype = C.c_size_t
-    for f in ("hsf_plan_opts_default", "hsf_plan", "hsf_plan_info_get", "hsf_run"):
+    L.hsf_ipc_export.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64)]
+    L.hsf_ipc_import.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_void_p)]
+    L.hsf_ipc_release.argtypes = [C.c_void_p, C.c_uint64]
+    for f in ("hsf_plan_opts_default", "hsf_plan", "hsf_plan_info_get", "hsf_run", "hsf_ipc_export", "hsf_ipc_import",
+              "hsf_ipc_release"):
         getattr(L, f).restype = C.c_int
     _lib = L
     return L
@@ -102,6 +108,26 @@ def _check(st: int):
         buf = C.create_string_buffer(4096)
         L.hsf_last_error(buf, 4096)
         raise HsfError(st, L.hsf_status_str(st).decode(), buf.value.decode(errors="replace"))
+
+
+def ipc_export(t) -> tuple:
+    """CUDA IPC handle (64 bytes) + offset of a device tensor's memory (hsf_ipc_export)."""
+    h = (C.c_char * 64)()
+    off = C.c_uint64()
+    _check(lib().hsf_ipc_export(C.c_void_p(t.data_ptr()), h, C.byref(off)))
+    return bytes(h), int(off.value)
+
+
+def ipc_import(handle: bytes, offset: int) -> int:
+    """Device pointer to another process's exported memory (hsf_ipc_import)."""
+    p = C.c_void_p()
+    hb = C.create_string_buffer(bytes(handle), 64)
+    _check(lib().hsf_ipc_import(hb, C.c_uint64(offset), C.byref(p)))
+    return int(p.value)
+
+
+def ipc_release(ptr: int, offset: int) -> None:
+    _check(lib().hsf_ipc_release(C.c_void_p(ptr), C.c_uint64(offset)))
 
 
 def version() -> str:
@@ -201,11 +227,17 @@ class Plan:
         return a
 
     def run(self, out, bitstrings=None, path_range=None, row_range=None, precision: str = "auto", stream=None,
-            timings: bool = False, accumulate: bool = False):
+            timings: bool = False, accumulate: bool = False, out_shards=None):
         """hsf_run(): evaluate paths [path_range) into `out`.
 
         `out` / `bitstrings` are torch tensors (device or host) or numpy arrays
-        (host).  Returns per-phase ms [simA, simB, prep, core, total] if `timings`."""
+        (host).  Returns per-phase ms [simA, simB, prep, core, total] if `timings`.
+
+        out_shards: fused reduce-scatter (hsf.h) -- a list of 1..8 destinations,
+        each a device tensor or an int device pointer (e.g. another GPU's
+        buffer opened via CUDA IPC) of 2^nA / len(out_shards) rows; the
+        GEMM epilogue reduce-adds each row shard into its owner; `out` may
+        be None."""
         import torch
 
         def ptr(x):
@@ -216,13 +248,23 @@ class Plan:
             x = np.ascontiguousarray(x)
             return x.ctypes.data, False, x.size
 
-        op, odev, _ = ptr(out)
+        shards_arr = None
+        if out_shards:
+            ps = [s if isinstance(s, int) else s.data_ptr() for s in out_shards]
+            shards_arr = (C.c_void_p * len(ps))(*ps)
+            op, odev = None, True
+        else:
+            op, odev, _ = ptr(out)
         bp, bdev, nb = (None, False, 0) if bitstrings is None else ptr(bitstrings)
         dev = torch.cuda.current_device() if torch.cuda.is_available() else -1
         st = stream if stream is not None else (torch.cuda.current_stream().cuda_stream if torch.cuda.is_available() else None)
         phase = (C.c_double * 5)() if timings else None
         a = self._args(op, odev, bp, nb, bdev, path_range, row_range, precision, st, dev,
                        C.cast(phase, C.POINTER(C.c_double)) if timings else None, accumulate)
+        if shards_arr is not None:
+            a.out_shards = C.cast(shards_arr, C.POINTER(C.c_void_p))
+            a.n_out_shards = len(out_shards)
+            a.shard_rows = (1 << self.n_a) // len(out_shards)
         _check(lib().hsf_run(self._h, C.byref(a)))
         return list(phase) if timings else None
 

@@ -39,6 +39,28 @@ def _oracle_partial(inst, P, bits):
     return partial
 
 
+class _HostPeers:
+    """CPU stand-in for dist.PeerShards: the own row shard; the peer adds the
+    GEMM epilogue makes over NVLink are emulated by a reduce-scatter of the
+    rank's partial output inside `partial` (the control flow -- zero, barrier,
+    evaluate, barrier -- is dist.sharded_step's own)."""
+
+    def __init__(self, local):
+        self.local = local
+
+
+def _fused_partial(inst, P):
+    import torch
+    import torch.distributed as dist
+
+    def partial(path_range, row_range, peers):
+        assert row_range is None  # every rank evaluates all rows of its path range
+        A, B, c = O.half_states(P, *path_range)
+        v = torch.from_numpy(np.ascontiguousarray(O.recombine_full(A, B, c)))
+        dist.reduce_scatter_tensor(torch.view_as_real(peers.local), torch.view_as_real(v), op=dist.ReduceOp.SUM)
+    return partial
+
+
 def _worker(rank, world, port, name, mode, q):
     import torch
     import torch.distributed as dist
@@ -58,7 +80,11 @@ def _worker(rank, world, port, name, mode, q):
         else:
             out = torch.zeros(len(inst.bitstrings), dtype=torch.complex128)
             shard_out = None
-        res = D.sharded_step(sh, _oracle_partial(inst, P, inst.bitstrings), out, shard_out)
+        if mode == "fused_rs":
+            peers = _HostPeers(torch.zeros((1 << n) // world, dtype=torch.complex128))
+            res = D.sharded_step(sh, _fused_partial(inst, P), peers)
+        else:
+            res = D.sharded_step(sh, _oracle_partial(inst, P, inst.bitstrings), out, shard_out)
         # gather every rank's piece on rank 0 in rank order
         pieces = [None] * world
         dist.all_gather_object(pieces, (sh.out_rows, res.numpy()))
@@ -91,6 +117,7 @@ def _reference(name):
 
 
 @pytest.mark.parametrize("name,mode", [("c4", "reduce_scatter"), ("c4", "rows"), ("c4", "allreduce"),
+                                       ("c4", "fused_rs"), ("c2", "fused_rs"),
                                        ("c1", "allreduce"), ("c5", "allreduce"), ("c3", "allreduce")])
 def test_two_rank_shards_reassemble(name, mode):
     inst, ref = _reference(name)

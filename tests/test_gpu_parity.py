@@ -3,6 +3,7 @@ same seeded inputs.  Tolerances (BASELINE.json north_star): max|d amp| <= 1e-5
 for complex64, <= 1e-11 for complex128; relative L2 is reported and bounded
 too (DESIGN.md "Tolerances")."""
 import math
+import os
 
 import numpy as np
 import pytest
@@ -432,6 +433,100 @@ def test_half_sided_tail_fold(torch, case, longest, table, monkeypatch):
                                fold_trailing_diag=fold)
             assert (sum(Pg.tail_units) + sum(Pg.head_units) > 0) == fold
             check(got, ref, "c64")
+
+
+@pytest.mark.parametrize("name,n,n_low,shards", [("c2", 20, 10, 4), ("c4", 20, 10, 2), ("c4", 20, 10, 1)])
+@pytest.mark.parametrize("precision", ["bf16x3", "bf16x6", "tf32x3"])
+def test_fused_reduce_scatter_shards(torch, name, n, n_low, shards, precision):
+    # out_shards: the GEMM epilogue reduce-adds each row shard into its own
+    # destination (here local buffers; across ranks peer memory).  Two path
+    # halves accumulated into the same zeroed shards == the full output.
+    from hsf_inputs.circuits import make_c2, make_c4
+    from paper_2502_06959_b200 import Plan
+    inst = (make_c2 if name == "c2" else make_c4)(n=n, n_low=n_low)
+    P = Plan(inst.text, inst.n_low, inst.blocks)
+    full = torch.empty(1 << n, dtype=torch.complex64, device="cuda")
+    P.run(full, precision=precision)
+    rows = (1 << (n - n_low)) // shards
+    bufs = [torch.zeros(rows << n_low, dtype=torch.complex64, device="cuda") for _ in range(shards)]
+    h = P.n_paths // 2
+    for pr in ((0, h), (h, P.n_paths)):
+        P.run(None, path_range=pr, precision=precision, out_shards=bufs)
+    torch.cuda.synchronize()
+    got = torch.cat(bufs).cpu().numpy()
+    ref = full.cpu().numpy()
+    assert np.abs(got - ref).max() <= 1e-6 * max(1.0, float(np.abs(ref).max()) * 1e3)
+
+
+def test_fused_reduce_scatter_rejects_bad_shapes(torch):
+    from paper_2502_06959_b200 import Plan, HsfError
+    inst = make_config("c2", twin=True)  # 2^8 rows: only one 256-row shard fits
+    P = Plan(inst.text, inst.n_low, inst.blocks)
+    bufs = [torch.zeros(128 << inst.n_low, dtype=torch.complex64, device="cuda") for _ in range(2)]
+    with pytest.raises(HsfError):
+        P.run(None, out_shards=bufs)
+    with pytest.raises(HsfError):
+        P.run(None, out_shards=bufs[:1], precision="simt")
+
+
+def _fused_rank(rank, world, port, n, n_low, q):
+    import torch
+    import torch.distributed as dist
+    from hsf_inputs.circuits import make_c2
+    from paper_2502_06959_b200 import Plan, dist as D
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    # gloo carries only the IPC handles and the barriers; the data moves in
+    # the GEMM epilogue's reduce-adds into the peer's shard
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        inst = make_c2(n=n, n_low=n_low)
+        P = Plan(inst.text, inst.n_low, inst.blocks)
+        sh = D.make_shard("fused_rs", P.n_paths, n - n_low, rank, world, True)
+        local = torch.zeros(((1 << (n - n_low)) // world) << n_low, dtype=torch.complex64, device="cuda")
+        peers = D.PeerShards(local)
+        res = D.run_sharded(P, peers, sh)
+        out = res.cpu().numpy()
+        dist.barrier()
+        peers.close()
+        pieces = [None] * world
+        dist.all_gather_object(pieces, (sh.out_rows, out))
+        if rank == 0:
+            q.put(pieces)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fused_reduce_scatter_two_processes_ipc(torch):
+    # two ranks (processes) sharing the one GPU of the box: each K-splits the
+    # paths and its GEMM reduce-adds into BOTH ranks' shards through CUDA IPC
+    # pointers; no collective on the data path.  (On the box the ranks' kernels
+    # time-slice; nothing waits on another rank inside a kernel.)
+    import socket
+    import torch.multiprocessing as mp
+    from hsf_inputs.circuits import make_c2
+    from paper_2502_06959_b200 import Plan
+    n, n_low = 20, 10
+    inst = make_c2(n=n, n_low=n_low)
+    P = Plan(inst.text, inst.n_low, inst.blocks)
+    ref = torch.empty(1 << n, dtype=torch.complex64, device="cuda")
+    P.run(ref)
+    ref = ref.cpu().numpy()
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    procs = [ctx.Process(target=_fused_rank, args=(r, 2, port, n, n_low, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    pieces = q.get()
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    got = np.concatenate([v for _, v in sorted(pieces, key=lambda x: x[0][0])])
+    assert np.abs(got - ref).max() <= 1e-6
 
 
 @pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
