@@ -395,8 +395,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 // thread of both CTAs arrives on the leader's accumulator-empty barrier.
 constexpr int B2_TILE = (BN / 2) * BK * 2;               // 16 KB: this CTA's half of B
 constexpr int STAGE2_BYTES = 2 * A_TILE + 2 * B2_TILE;   // 64 KB
-constexpr int smem2_bytes(int nst, int ebuf, int npl = 2) {
-  return nst * npl * (A_TILE + B2_TILE) + ebuf * EPI_BYTES + 1024;
+constexpr int smem2_bytes(int nst, int ebuf, int npl = 2, int ew = EPI_WARPS) {
+  return nst * npl * (A_TILE + B2_TILE) + ebuf * ew * 4096 + 1024;
 }
 constexpr uint32_t IDESC2 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                             ((uint32_t)((2 * BM) >> 4) << 24);
@@ -468,8 +468,10 @@ struct OutMaps {
   CUtensorMap m[kMaxOutMaps];
 };
 
-template <int NST, int EBUF, bool TF32 = false>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+// EW epilogue warps (8, or 16 for the output-write-bound short-K shape: more
+// 4 KB TMA stores in flight per SM)
+template <int NST, int EBUF, bool TF32 = false, int EW = EPI_WARPS>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * EW, 1)
     tc_gemm2_kernel(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUtensorMap mA_lo,
                     const __grid_constant__ CUtensorMap mB_hi, const __grid_constant__ CUtensorMap mB_lo,
                     const __grid_constant__ CUtensorMap mA_l2, const __grid_constant__ CUtensorMap mB_l2,
@@ -491,7 +493,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 2 * 32 * EPI_WARPS);  // epilogue threads of both CTAs
+      mbar_init(&tempty_bar[a], 2 * 32 * EW);  // epilogue threads of both CTAs
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mA_hi) : "memory");
@@ -627,6 +629,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     // ------------------------------------------------------------ epilogue (both CTAs)
     const uint64_t st_pol = policy_evict_first();
     const int q = warp & 3;
+    constexpr int G = EW / 4;  // warps per TMEM lane quarter, interleaving 32-column chunks
     const int half = (warp - 2) / 4;
     uint8_t* stg0 = smem + NST * SS + (warp - 2) * 4096 * EBUF;
     int buf = 0;
@@ -639,7 +642,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       mbar_wait(&tfull_bar[acc], aph);
       asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll 1
-      for (int c = half; c < BN / 32; c += 2) {
+      for (int c = half; c < BN / 32; c += G) {
         uint32_t v[32];
         const uint32_t taddr = tmem_base + (uint32_t)(acc * BN + c * 32) + ((uint32_t)(q * 32) << 16);
         asm volatile(
@@ -652,7 +655,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               "=r"(v[30]), "=r"(v[31])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (c >= BN / 32 - 2) {
+        if (c >= BN / 32 - G) {
           asm volatile("tcgen05.fence::before_thread_sync;");
           mbar_arrive_leader(&tempty_bar[acc]);
         }
