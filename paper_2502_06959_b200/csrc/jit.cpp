@@ -133,9 +133,14 @@ struct Gen {
       o << "  constexpr u32 RANK = 0u;\n";
     }
     o << "  (void)stab;\n";
-    o << "  const long long node_g = a.node_first + blockIdx.y;\n";
+    // grid: x = tile, y = node; the transposed-store variant swaps them so
+    // that the CTAs of all paths of one tile run together
+    o << "  const u32 NODE_ID = " << (swap_grid ? "blockIdx.x" : "blockIdx.y") << ";\n";
+    o << "  const u32 TILE_ID = " << (swap_grid ? "blockIdx.y" : "blockIdx.x") << ";\n";
+    o << "  (void)TILE_ID;\n";
+    o << "  const long long node_g = a.node_first + NODE_ID;\n";
     o << "  const C* coef = reinterpret_cast<const C*>(a.coef);\n";
-    o << "  C* dst = reinterpret_cast<C*>(a.dst) + (a.node_local0 + blockIdx.y) * " << (1ll << m) << "ll;\n";
+    o << "  C* dst = reinterpret_cast<C*>(a.dst) + (a.node_local0 + NODE_ID) * " << (1ll << m) << "ll;\n";
     o << "  (void)dst;\n";
     o << "  const C* src = a.src ? reinterpret_cast<const C*>(a.src) + (node_g / a.src_div - a.src_first) * "
       << (1ll << m) << "ll : nullptr;\n";
@@ -148,7 +153,7 @@ struct Gen {
         if (std::find(ps.T.begin(), ps.T.end(), q) == ps.T.end()) nonT.push_back(q);
       std::vector<int> from(nonT.size()), to = nonT;
       for (size_t j = 0; j < nonT.size(); ++j) from[j] = (int)j;
-      o << "  const u32 tile = (blockIdx.x >> CB) + a.tile0;\n";
+      o << "  const u32 tile = (TILE_ID >> CB) + a.tile0;\n";
       o << "  const u32 base = " << gather_expr("tile", from, to) << ";\n";
       std::vector<int> pf, pt;
       for (int i = 0; i < t; ++i) {
@@ -305,7 +310,14 @@ struct Gen {
   int nt = 256;  // threads per CTA (512 for narrow tree levels)
   int cb = 0;    // cluster tier: log2 CTAs per tile (0 = one CTA per tile)
 
-  std::string build(const std::string& name, int threads, int cluster_bits, bool operand_store = false) {
+  bool swap_grid = false;  // transposed-store variant: grid x = node, y = tile
+
+  // store_mode: 0 leaf (node-major), 1 MN-major split-bf16 B operand,
+  // 2 transposed leaf: element G of node k to dst[G * ldw + k] (x c_p[k] when
+  // dst_lo carries c_p) -- the bitstring gather operand, no transpose pass
+  std::string build(const std::string& name, int threads, int cluster_bits, int store_mode = 0) {
+    const bool operand_store = store_mode == 1;
+    swap_grid = store_mode == 2;
     nt = threads;
     cb = whole ? 0 : cluster_bits;
     bool heavy = false;
@@ -329,12 +341,22 @@ struct Gen {
       }
     }
     o << "  __syncthreads();\n";
-    o << "#pragma unroll 4\n";
-    if (operand_store)
-      o << "  for (u32 e = 2u * threadIdx.x; e < LNEL; e += 2u * NT) st_bop(a, a.node_local0 + blockIdx.y, "
+    if (operand_store) {
+      o << "#pragma unroll 4\n";
+      o << "  for (u32 e = 2u * threadIdx.x; e < LNEL; e += 2u * NT) st_bop(a, a.node_local0 + NODE_ID, "
            "G((RANK << LB) | e), s[sw(e)], s[sw(e + 1)]);\n";
-    else
+    } else if (swap_grid) {
+      o << "  { const long long kcol = a.node_local0 + NODE_ID;\n";
+      o << "    C cpv = czero<C>(); cpv.x = 1;\n";
+      o << "    if (a.dst_lo) cpv = reinterpret_cast<const C*>(a.dst_lo)[kcol];\n";
+      o << "    C* T = reinterpret_cast<C*>(a.dst);\n";
+      o << "#pragma unroll 4\n";
+      o << "    for (u32 e = threadIdx.x; e < LNEL; e += NT) T[(long long)G((RANK << LB) | e) * a.ldw + kcol] = "
+           "cmul(s[sw(e)], cpv);\n  }\n";
+    } else {
+      o << "#pragma unroll 4\n";
       o << "  for (u32 e = 2u * threadIdx.x; e < LNEL; e += 2u * NT) st2(dst + G((RANK << LB) | e), s[sw(e)], s[sw(e + 1)]);\n";
+    }
     o << "}\n";
     return o.str();
   }
@@ -410,9 +432,9 @@ std::vector<char> nvrtc_compile(const std::string& src, std::string& log) {
 }  // namespace
 
 std::string jit_pass_source(const Half& H, const Pass& ps, bool c64, int threads, int cluster_bits,
-                            const std::vector<cd>* coef, bool operand_store) {
+                            const std::vector<cd>* coef, int store_mode) {
   Gen g(H, ps, c64, coef);
-  return std::string(kPrelude) + "\n" + g.build("hsf_jit_pass", threads, cluster_bits, operand_store);
+  return std::string(kPrelude) + "\n" + g.build("hsf_jit_pass", threads, cluster_bits, store_mode);
 }
 
 size_t jit_smem_bytes(const Pass& ps, bool c64, int cluster_bits) {

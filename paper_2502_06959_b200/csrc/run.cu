@@ -43,6 +43,11 @@ struct DeviceState {
   // operand directly (full-output tensor-core runs; K4 fused into the leaf pass)
   void* jit_bop = nullptr;
   int jit_bop_nt = 256;
+  // bitstring runs: the last pass of each half writing the transposed,
+  // c_p-folded gather operand [2^m][K] directly (no transpose kernel);
+  // [variant 0 full / 1 fold][half]
+  void* jit_tr[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  int jit_tr_nt[2][2] = {{256, 256}, {256, 256}};
   bool jit = false;                         // specialised pass kernels loaded
   unsigned long long* perm_tab = nullptr;   // caller -> internal index bits (partitions)
   // [variant: 0 full tree, 1 bitstring fold, 2 half-sided tail][half] per flattened pass
@@ -241,10 +246,27 @@ static DeviceState* ensure_device(Plan* P, int device) {
       src.push_back(jit_pass_source(HB, HB.trans.back().passes.back(), c64, d->jit_bop_nt, 0, &P->coef, true));
       owner.push_back({-1, 1});
     }
+    // transposed-store variants of each half's last pass (bitstring runs);
+    // opt-in (HSF_TRANSPOSED_STORE=1): its scattered 8 B stores measured slower
+    // than the leaf pass + transpose_fold_kernel (c5 4.99 vs 4.29 ms)
+    const char* tse = std::getenv("HSF_TRANSPOSED_STORE");
+    for (int v = 0; v < 2 && tse && tse[0] == '1'; ++v) {
+      if (v == 1 && P->fold_u0 < 0) continue;
+      for (int h = 0; h < 2; ++h) {
+        const Half& H = v ? P->half_fold[h] : P->half[h];
+        if (H.trans.empty() || H.trans.back().passes.empty() || d->jit_cb[v][h].empty() || d->jit_cb[v][h].back() != 0)
+          continue;
+        d->jit_tr_nt[v][h] = d->jit_nt[v][h].back();
+        src.push_back(jit_pass_source(H, H.trans.back().passes.back(), c64, d->jit_tr_nt[v][h], 0, &P->coef, 2));
+        owner.push_back({-2 - (2 * v + h), 0});
+      }
+    }
     std::vector<void*> fns = jit_compile_all(device, src);
     for (size_t i = 0; i < fns.size(); ++i) {
-      if (owner[i].first < 0)
+      if (owner[i].first == -1)
         d->jit_bop = fns[i];
+      else if (owner[i].first <= -2)
+        d->jit_tr[(-2 - owner[i].first) / 2][(-2 - owner[i].first) % 2] = fns[i];
       else
         d->jit_fn[owner[i].first][owner[i].second].push_back(fns[i]);
     }
@@ -560,7 +582,13 @@ static void run_half(const Plan& P, DeviceState* d, int h, const Layout& L, cuda
           pp.src_div = 1;
         }
         const bool bop = h == 1 && L.bop && d->jit_bop && last && pi + 1 == tr.passes.size();
-        if (bop) {  // K4 fused: write the MN-major split-bf16 B operand instead of the leaves
+        const bool trs = L.bits_mode && var <= 1 && d->jit_tr[var][h] && last && pi + 1 == tr.passes.size();
+        if (trs) {  // K4t fused: write the transposed (c_p-folded for A) gather operand
+          JitLaunchArgs ja{pp.src, ws + L.off_T[h], pp.coef, pp.node_first, pp.node_local0, pp.src_first, pp.src_div,
+                           pp.tile0, h == 0 ? d->cp : nullptr, (long long)L.K};
+          jit_launch(d->jit_tr[var][h], (unsigned)ny, (unsigned)tiles, (unsigned)d->jit_tr_nt[var][h],
+                     jit_smem_bytes(ps, sizeof(R) == 4, 0), st, ja, 0);
+        } else if (bop) {  // K4 fused: write the MN-major split-bf16 B operand instead of the leaves
           TcBuffers t = tc_buffers((long long)L.K, (long long)(L.r1 - L.r0), 1ll << H.m, tc_planes(L.prec),
                                    ws + L.off_tc, L.tc_bytes);
           JitLaunchArgs ja{pp.src, t.b_hi, pp.coef, pp.node_first, pp.node_local0, pp.src_first, pp.src_div, pp.tile0,
@@ -597,6 +625,7 @@ static void prep_half(Plan* P, DeviceState* d, const Layout& L, int h, cudaStrea
   const long long K = (long long)L.K;
   const C* leaves = (const C*)(ws + L.off_leaves[h]);
   if (L.bits_mode) {
+    if (L.var[h] <= 1 && d->jit_tr[L.var[h]][h]) return;  // written by the half's last pass
     C* T = (C*)(ws + L.off_T[h]);
     dim3 g((unsigned)(((1ll << m) + 31) / 32), (unsigned)((K + 31) / 32));
     transpose_fold_kernel<C><<<g, dim3(32, 8), 0, st>>>(leaves, T, h == 0 ? (const C*)d->cp : nullptr, K, 1ll << m);
@@ -1048,6 +1077,7 @@ size_t hsf_debug_pass_source(const hsf_plan_t* plan, int32_t variant, int32_t ha
   try {
     const Plan* P = reinterpret_cast<const Plan*>(plan);
     const int cbq = (variant >> 2) & 3;  // bits 2-3: cluster-tier variant with 2^cb CTAs per tile
+    const int store = (variant >> 4) & 3;  // bits 4-5: store mode (1 B operand, 2 transposed leaf)
     variant &= 3;                        // 0 full tree, 1 bitstring fold, 2 half-sided tail
     if (!P || half < 0 || half > 1 || variant > 2 || (variant == 1 && P->fold_u0 < 0) ||
         (variant == 2 && P->tail[half].u0 < 0))
@@ -1059,7 +1089,7 @@ size_t hsf_debug_pass_source(const hsf_plan_t* plan, int32_t variant, int32_t ha
         if (k++ == pass) {
           const int nt = cbq ? std::max(128, 1 << (ps.t - cbq - 4)) : 256;
           const std::string s =
-              jit_pass_source(H, ps, P->opts.dtype == HSF_C64, nt, ps.t < H.m ? cbq : 0, &P->coef);
+              jit_pass_source(H, ps, P->opts.dtype == HSF_C64, nt, ps.t < H.m ? cbq : 0, &P->coef, store);
           if (buf && len) {
             const size_t n = std::min(len - 1, s.size());
             std::memcpy(buf, s.data(), n);

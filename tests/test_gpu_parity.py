@@ -529,6 +529,23 @@ def test_fused_reduce_scatter_two_processes_ipc(torch):
     assert np.abs(got - ref).max() <= 1e-6
 
 
+@pytest.mark.parametrize("name,path_range", [("c5", None), ("c5", (4, 12)), ("c3", None), ("c1", None)])
+def test_transposed_store_variant(torch, name, path_range, monkeypatch):
+    # opt-in: each half's last pass writes the transposed (c_p-folded for A)
+    # gather operand itself instead of the leaves + transpose_fold_kernel
+    monkeypatch.setenv("HSF_TRANSPOSED_STORE", "1")
+    inst = make_config(name, twin=True)
+    if inst.bitstrings is None:
+        inst.bitstrings = np.random.default_rng(7).integers(0, 1 << inst.n, 4096, dtype=np.uint64)
+    n, g = O.parse_circuit(inst.text)
+    P = O.plan(n, g, inst.n_low, inst.blocks)
+    p0, p1 = path_range or (0, P.n_paths)
+    A, B, c = O.half_states(P, p0, p1)
+    ref = O.recombine_bits(A, B, c, inst.bitstrings, inst.n_low)
+    got, _ = gpu_bits(torch, inst, inst.bitstrings, path_range=path_range)
+    check(got, ref, inst.dtype)
+
+
 @pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
 def test_interpreter_kernel_twins(torch, name):
     # jit=False: the generic interpreter pass kernel (hsf_pass_kernel) instead
