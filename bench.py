@@ -491,6 +491,10 @@ def main():
         sim_launches = sum(P.tail_passes[h] if halves_var[h] else P.passes[h] for h in (0, 1))
     fused_b = tc_full and not halves_var[1] and K > 64
     n_launch = sim_launches + (1 if (full and eff_prec == "simt") else (2 if fused_b else 3))
+    if not full:  # grouped gather (run.cu make_layout): + count, scan, scatter kernels
+        Kt = K // (int(np.prod(P.ranks[len(P.ranks) - P.fold_units:])) if P.fold_units else 1)
+        if inst.dtype == "c64" and Kt % 64 == 0 and Kt <= 512 and N_out >= 8 * (1 << P.n_a):
+            n_launch += 3
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "paths/s", "n_gpus": world, "steps": a.steps,
                 "warmup": max(3, a.warmup), "ms_per_step": t_step, "higher_is_better": True, "scaling": "strong",

@@ -305,6 +305,8 @@ struct Layout {
   size_t off_T[2] = {0, 0};    // transposed operands (bitstring mode)
   size_t off_bits = 0, off_out = 0, off_tc = 0;
   size_t off_pbits = 0, off_pout = 0;  // relabelled bitstrings / internal-order output (partitions)
+  bool grouped = false;        // bitstring gather bucketed by A row (gather_grouped_c64_kernel)
+  size_t off_grp = 0;          // counts[2^nA] | offs[2^nA + 1] | cursor[2^nA] | perm[n] (int32)
   size_t tc_bytes = 0;
   uint64_t chunk_rows = 0;     // full mode, host output: rows per staged D2H chunk
   size_t chunk_bytes = 0;
@@ -410,6 +412,17 @@ static Layout make_layout(const Plan& P, const hsf_run_args& a, size_t elem) {
     if (P.permuted) {
       L.off_pbits = off;
       off = align_up(off + a.n_bitstrings * 8);
+    }
+    // grouped gather: >= 8 samples per A row on average, K a multiple of 64 up
+    // to 512 (the row lives in registers), complex64, rows and samples < 2^31
+    const long long nrowsA = 1ll << nA;
+    const char* gg = std::getenv("HSF_GROUPED_GATHER");
+    const bool want = gg ? gg[0] == '1' : (long long)a.n_bitstrings >= 8 * nrowsA;
+    L.grouped = want && P.opts.dtype == HSF_C64 && L.K % 64 == 0 && L.K <= 512 && nA <= 30 &&
+                a.n_bitstrings < (1ull << 31);
+    if (L.grouped) {
+      L.off_grp = off;
+      off = align_up(off + (size_t)(3 * nrowsA + 1 + (long long)a.n_bitstrings) * 4);
     }
   } else {
     if (P.permuted) {
@@ -683,7 +696,35 @@ static void run_core_bits(Plan* P, DeviceState* d, const Layout& L, const hsf_ru
       tw.off[u] = P->trail_off[u];
     }
   }
-  if (sizeof(R) == 4 && K % 64 == 0) {
+  if (sizeof(R) == 4 && L.grouped) {
+    const long long nrowsA = 1ll << (P->n - nB);
+    int* counts = (int*)(ws + L.off_grp);
+    int* offs = counts + nrowsA;
+    int* cursor = offs + nrowsA + 1;
+    int* perm = cursor + nrowsA;
+    CK(cudaMemsetAsync(counts, 0, (size_t)nrowsA * 4, st));
+    const unsigned gb = (unsigned)std::min<long long>((ns + 255) / 256, 148ll * 16);
+    bucket_count_kernel<<<gb, 256, 0, st>>>(bits, ns, nB, counts);
+    bucket_scan_kernel<<<1, 1024, 0, st>>>(counts, offs, cursor, nrowsA);
+    bucket_scatter_kernel<<<gb, 256, 0, st>>>(bits, ns, nB, cursor, perm);
+    const unsigned gw = (unsigned)std::min<long long>((nrowsA + 7) / 8, 148ll * 64);  // 8 warps per CTA
+    const float4* A4 = (const float4*)AT;
+    const float4* B4 = (const float4*)BT;
+    switch (K / 64) {
+      case 1: gather_grouped_c64_kernel<1><<<gw, 256, 0, st>>>(A4, B4, bits, offs, perm, (float2*)out, nrowsA, nB, tw,
+                                                               (const float2*)d->trail, a.accumulate); break;
+      case 2: gather_grouped_c64_kernel<2><<<gw, 256, 0, st>>>(A4, B4, bits, offs, perm, (float2*)out, nrowsA, nB, tw,
+                                                               (const float2*)d->trail, a.accumulate); break;
+      case 4: gather_grouped_c64_kernel<4><<<gw, 256, 0, st>>>(A4, B4, bits, offs, perm, (float2*)out, nrowsA, nB, tw,
+                                                               (const float2*)d->trail, a.accumulate); break;
+      case 8: gather_grouped_c64_kernel<8><<<gw, 256, 0, st>>>(A4, B4, bits, offs, perm, (float2*)out, nrowsA, nB, tw,
+                                                               (const float2*)d->trail, a.accumulate); break;
+      default: {  // K = 192, 320, 384, 448: the plain vectorised gather
+        gather_dot_c64_vec_kernel<<<(unsigned)blocks, 256, 0, st>>>(A4, B4, bits, (float2*)out, ns, K, nB, tw,
+                                                                    (const float2*)d->trail, a.accumulate);
+      }
+    }
+  } else if (sizeof(R) == 4 && K % 64 == 0) {
     gather_dot_c64_vec_kernel<<<(unsigned)blocks, 256, 0, st>>>((const float4*)AT, (const float4*)BT, bits,
                                                                 (float2*)out, ns, K, nB, tw, (const float2*)d->trail,
                                                                 a.accumulate);

@@ -168,6 +168,116 @@ __global__ void gather_dot_c64_vec_kernel(const float4* __restrict__ AT, const f
   }
 }
 
+// ------------------------------------------------------ K6, grouped by A row
+// When many samples share an A row (c3: 2^20 samples over 2^15 rows, ~32 per
+// row; both operands L2-resident, so the plain gather is bound by L2->SM
+// traffic), the samples are bucketed by A row (counting sort: count, one-CTA
+// scan, scatter of sample indices) and one warp per row keeps the row in
+// registers while it streams its samples' B rows: A traffic drops from one
+// row per sample to one row per distinct row.
+__global__ void bucket_count_kernel(const unsigned long long* __restrict__ bits, long long n, int n_low,
+                                    int* __restrict__ counts) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    atomicAdd(&counts[bits[i] >> n_low], 1);
+}
+
+// exclusive scan of counts[0..n) into offs[0..n] (offs[n] = total); one CTA of 1024
+__global__ void __launch_bounds__(1024) bucket_scan_kernel(const int* __restrict__ counts, int* __restrict__ offs,
+                                                           int* __restrict__ cursor, long long n) {
+  __shared__ int part[1024];
+  const int t = threadIdx.x;
+  const long long per = (n + 1023) / 1024, b = t * per, e = min(n, b + per);
+  int sum = 0;
+  for (long long i = b; i < e; ++i) sum += counts[i];
+  part[t] = sum;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {  // Hillis-Steele inclusive scan of the partials
+    const int v = t >= o ? part[t - o] : 0;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
+  }
+  int run = t ? part[t - 1] : 0;
+  for (long long i = b; i < e; ++i) {
+    offs[i] = run;
+    cursor[i] = run;
+    run += counts[i];
+  }
+  if (t == 1023) offs[n] = part[1023];
+}
+
+__global__ void bucket_scatter_kernel(const unsigned long long* __restrict__ bits, long long n, int n_low,
+                                      int* __restrict__ cursor, int* __restrict__ perm) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    perm[atomicAdd(&cursor[bits[i] >> n_low], 1)] = (int)i;
+}
+
+// one warp per A row r: the row (T float4 per lane, K = 64*T complex) stays in
+// registers; the row's samples are taken two at a time (both B rows in flight)
+template <int T>
+__global__ void gather_grouped_c64_kernel(const float4* __restrict__ AT, const float4* __restrict__ BT,
+                                          const unsigned long long* __restrict__ bits, const int* __restrict__ offs,
+                                          const int* __restrict__ perm, float2* __restrict__ out, long long n_rows,
+                                          int n_low, const TrailParams tw, const float2* __restrict__ trail,
+                                          int accumulate) {
+  constexpr int K2 = 32 * T;  // float4 per operand row
+  const int lane = threadIdx.x & 31;
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const unsigned long long maskB = (1ull << n_low) - 1ull;
+  for (long long r = warp; r < n_rows; r += nwarps) {
+    const int beg = offs[r], end = offs[r + 1];
+    if (beg == end) continue;
+    float4 a[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) a[t] = __ldg(&AT[r * K2 + lane + 32 * t]);
+    for (int j = beg; j < end; j += 2) {
+      const bool two = j + 1 < end;
+      const int i0 = perm[j], i1 = two ? perm[j + 1] : i0;
+      const unsigned long long b0 = bits[i0], b1 = bits[i1];
+      const float4* q0 = BT + (long long)(b0 & maskB) * K2;
+      const float4* q1 = BT + (long long)(b1 & maskB) * K2;
+      float4 y0[T], y1[T];
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        y0[t] = __ldg(&q0[lane + 32 * t]);
+        y1[t] = __ldg(&q1[lane + 32 * t]);
+      }
+      float re0 = 0.f, im0 = 0.f, re1 = 0.f, im1 = 0.f;
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        const float4 x = a[t];
+        re0 = fmaf(x.x, y0[t].x, fmaf(-x.y, y0[t].y, re0));
+        im0 = fmaf(x.x, y0[t].y, fmaf(x.y, y0[t].x, im0));
+        re0 = fmaf(x.z, y0[t].z, fmaf(-x.w, y0[t].w, re0));
+        im0 = fmaf(x.z, y0[t].w, fmaf(x.w, y0[t].z, im0));
+        re1 = fmaf(x.x, y1[t].x, fmaf(-x.y, y1[t].y, re1));
+        im1 = fmaf(x.x, y1[t].y, fmaf(x.y, y1[t].x, im1));
+        re1 = fmaf(x.z, y1[t].z, fmaf(-x.w, y1[t].w, re1));
+        im1 = fmaf(x.z, y1[t].w, fmaf(x.w, y1[t].z, im1));
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        re0 += __shfl_xor_sync(0xffffffffu, re0, o);
+        im0 += __shfl_xor_sync(0xffffffffu, im0, o);
+        re1 += __shfl_xor_sync(0xffffffffu, re1, o);
+        im1 += __shfl_xor_sync(0xffffffffu, im1, o);
+      }
+      if (lane < (two ? 2 : 1)) {  // lane 0 writes sample j, lane 1 sample j+1
+        const int idx = lane ? i1 : i0;
+        const unsigned long long bb = lane ? b1 : b0;
+        const float2 v = lane ? make_float2(re1, im1) : make_float2(re0, im0);
+        float2 res = tw.n ? cmul(v, trail_weight(tw, trail, bb)) : v;
+        if (accumulate) {
+          res.x += out[idx].x;
+          res.y += out[idx].y;
+        }
+        out[idx] = res;
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ K5s
 // out[(i - row0) * MB + j] = sum_p c_p A[p][i] B[p][j]  for i in [row0, row0+rows)
 // A: [K][MA] node-major leaves, B: [K][MB].  64x64 output tile per CTA,

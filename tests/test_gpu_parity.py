@@ -546,6 +546,24 @@ def test_transposed_store_variant(torch, name, path_range, monkeypatch):
     check(got, ref, inst.dtype)
 
 
+@pytest.mark.parametrize("name,path_range", [("c3", None), ("c3", (16, 48)), ("c5", None), ("c5", (3, 9))])
+@pytest.mark.parametrize("grouped", ["0", "1"])
+def test_grouped_gather(torch, name, path_range, grouped, monkeypatch):
+    # bitstring path-sum bucketed by A row (counting sort + one warp per row)
+    # vs the per-sample gather: both against the oracle's partial sums, with
+    # duplicates and unaligned (unfolded) ranges
+    monkeypatch.setenv("HSF_GROUPED_GATHER", grouped)
+    inst = make_config(name, twin=True)
+    bits = np.concatenate([inst.bitstrings, inst.bitstrings[:300]])  # duplicates
+    n, g = O.parse_circuit(inst.text)
+    P = O.plan(n, g, inst.n_low, inst.blocks)
+    p0, p1 = path_range or (0, P.n_paths)
+    A, B, c = O.half_states(P, p0, p1)
+    ref = O.recombine_bits(A, B, c, bits, inst.n_low)
+    got, _ = gpu_bits(torch, inst, bits, path_range=path_range)
+    check(got, ref, inst.dtype)
+
+
 @pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
 def test_interpreter_kernel_twins(torch, name):
     # jit=False: the generic interpreter pass kernel (hsf_pass_kernel) instead
