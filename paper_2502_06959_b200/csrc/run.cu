@@ -296,6 +296,7 @@ struct Layout {
   uint64_t hp0[2] = {0, 0}, hp1[2] = {0, 0};
   const Half* half[2] = {nullptr, nullptr};
   bool bop = false;            // half B's last pass writes the MN-major GEMM operand (with a JIT kernel)
+  bool g3m = false;            // full-output path-sum by the 3M (Gauss) kernel (tc_gemm3m_kernel)
   bool bits_mode;
   uint64_t r0, r1;
   hsf_precision prec;
@@ -370,8 +371,10 @@ static Layout make_layout(const Plan& P, const hsf_run_args& a, size_t elem) {
       L.hp1[h] = L.p1;
     }
   }
-  L.bop = !L.bits_mode && (L.prec == HSF_PREC_BF16X3 || L.prec == HSF_PREC_BF16X1) && P.opts.dtype == HSF_C64 &&
-          L.var[1] == 0 && tc_mn((long long)L.K);
+  L.g3m = !L.bits_mode && L.prec == HSF_PREC_BF16X3 && P.opts.dtype == HSF_C64 && a.n_out_shards == 0 &&
+          !a.accumulate && tc_use_3m((long long)L.K);
+  L.bop = !L.bits_mode && !L.g3m && (L.prec == HSF_PREC_BF16X3 || L.prec == HSF_PREC_BF16X1) &&
+          P.opts.dtype == HSF_C64 && L.var[1] == 0 && tc_mn((long long)L.K);
   if (!L.bits_mode && a.bitstrings) fail(HSF_ERR_INVALID_ARG, "bitstrings given with n_bitstrings == 0");
   if (L.bits_mode && !a.bitstrings) fail(HSF_ERR_INVALID_ARG, "n_bitstrings > 0 but bitstrings is NULL");
   if (L.bits_mode && P.n > 63) fail(HSF_ERR_INVALID_ARG, "bitstring runs need n <= 63");
@@ -432,7 +435,8 @@ static Layout make_layout(const Plan& P, const hsf_run_args& a, size_t elem) {
       off = align_up(off + ((size_t)1 << P.n) * elem);
     }
     if (L.prec != HSF_PREC_SIMT) {
-      L.tc_bytes = tc_workspace_bytes((long long)L.K, (long long)(L.r1 - L.r0), 1ll << nB, tc_planes(L.prec));
+      L.tc_bytes = L.g3m ? tc3_workspace_bytes((long long)L.K, (long long)(L.r1 - L.r0), 1ll << nB)
+                         : tc_workspace_bytes((long long)L.K, (long long)(L.r1 - L.r0), 1ll << nB, tc_planes(L.prec));
       L.off_tc = off;
       off = align_up(off + L.tc_bytes);
     }
@@ -645,7 +649,6 @@ static void prep_half(Plan* P, DeviceState* d, const Layout& L, int h, cudaStrea
     CK(cudaGetLastError());
   } else if (L.prec != HSF_PREC_SIMT) {
     const int nB = P->n_low;
-    TcBuffers t = tc_buffers(K, (long long)(L.r1 - L.r0), 1ll << nB, tc_planes(L.prec), ws + L.off_tc, L.tc_bytes);
     tc::TailParams tp = L.var[h] == 2 ? tail_params(*P, h) : tc::TailParams{};
     tp.p0 = (long long)L.p0;
     if (L.var[h] == 2) {
@@ -656,11 +659,18 @@ static void prep_half(Plan* P, DeviceState* d, const Layout& L, int h, cudaStrea
       tp.T = 1;
       tp.Tt = 1;
     }
-    if (h == 0)
+    if (L.g3m) {
+      const Tc3Buffers t3 = tc3_buffers(K, (long long)(L.r1 - L.r0), 1ll << nB, ws + L.off_tc, L.tc_bytes);
+      tc3_prep(t3, h == 0, (const float2*)leaves, (const float2*)d->cp, 1ll << m, h == 0 ? (long long)L.r0 : 0,
+               h == 0 ? (long long)(L.r1 - L.r0) : (1ll << m), tp, (const float2*)d->tail, st);
+    } else if (h == 0) {
+      TcBuffers t = tc_buffers(K, (long long)(L.r1 - L.r0), 1ll << nB, tc_planes(L.prec), ws + L.off_tc, L.tc_bytes);
       tc_prep_a(t, (const float2*)leaves, (const float2*)d->cp, K, 1ll << m, (long long)L.r0, (long long)(L.r1 - L.r0),
                 tp, (const float2*)d->tail, st);
-    else if (!(L.bop && d->jit_bop))  // else written by half B's last pass
+    } else if (!(L.bop && d->jit_bop)) {  // else written by half B's last pass
+      TcBuffers t = tc_buffers(K, (long long)(L.r1 - L.r0), 1ll << nB, tc_planes(L.prec), ws + L.off_tc, L.tc_bytes);
       tc_prep_b(t, (const float2*)leaves, K, 1ll << m, tp, (const float2*)d->tail, st);
+    }
   }
 }
 
@@ -753,6 +763,11 @@ static void run_core_full(Plan* P, DeviceState* d, const Layout& L, cudaStream_t
     CK(cudaGetLastError());
   } else {
     if (sizeof(R) != 4) fail(HSF_ERR_UNSUPPORTED, "tensor-core path-sum needs complex64");
+    if (L.g3m) {
+      tc_gemm3m(tc3_buffers(K, (long long)(L.r1 - L.r0), 1ll << nB, ws + L.off_tc, L.tc_bytes), (float2*)out,
+                1ll << nB, (long long)lo, (long long)nrows, st);
+      return;
+    }
     TcBuffers t = tc_buffers(K, (long long)(L.r1 - L.r0), 1ll << nB, tc_planes(L.prec), ws + L.off_tc,
                              L.tc_bytes);
     if (shards && shards->n_out_shards > 0)

@@ -564,6 +564,46 @@ def test_grouped_gather(torch, name, path_range, grouped, monkeypatch):
     check(got, ref, inst.dtype)
 
 
+@pytest.mark.parametrize("name", ["c2", "c4", "c5", "toy_head"])
+@pytest.mark.parametrize("mode", ["1", "0"])
+def test_gauss_3m_gemm(torch, name, mode, monkeypatch):
+    # tc_gemm3m_kernel (three real products, Re = T1 - T2, Im = T3 - T1 - T2)
+    # vs the 4-real-GEMM kernel, against the oracle: full, ragged path and row
+    # ranges, host output in chunks
+    monkeypatch.setenv("HSF_TC_3M", mode)
+    if name == "toy_head":
+        from types import SimpleNamespace
+        inst = SimpleNamespace(text="qubits 4\nx 1\nx 3\ncz 1 2\ncp 0x1.8p-1 0 3\nh 1\nh 2\ncz 1 3\nh 0\nh 3\n"
+                                    "cz 0 2\nrx 0x1.4p-2 1\nrx 0x1.8p-2 2\n", n_low=2, blocks=[], dtype="c64")
+    else:
+        inst = make_config(name, twin=True, n_bits=0) if name == "c5" else make_config(name, twin=True)
+    n, g = O.parse_circuit(inst.text)
+    P = O.plan(n, g, inst.n_low, inst.blocks)
+    rows = 1 << (n - inst.n_low)
+    for pr, rr in [(None, None), ((1, P.n_paths - 1), (1, rows - 1))]:
+        p0, p1 = pr or (0, P.n_paths)
+        A, B, c = O.half_states(P, p0, p1)
+        ref = O.recombine_full(A, B, c)
+        if rr:
+            ref = ref[rr[0] << inst.n_low:rr[1] << inst.n_low]
+        got, _ = gpu_full(torch, inst, precision="bf16x3", path_range=pr, row_range=rr)
+        check(got, ref, "c64")
+
+
+def test_gauss_3m_c2_full_size(torch, monkeypatch):
+    monkeypatch.setenv("HSF_TC_3M", "1")
+    inst = make_config("c2")
+    got, P = gpu_full(torch, inst, precision="bf16x3")
+    n, x = inst.n, inst.meta["x"]
+    i = np.arange(1 << n, dtype=np.int64)
+    rev = np.zeros_like(i)
+    for b in range(n):
+        rev |= ((i >> b) & 1) << (n - 1 - b)
+    ref = np.exp(2j * np.pi * ((x * rev) % (1 << n)) / (1 << n)) / 2 ** (n / 2)
+    md, rel = check(got, ref, "c64")
+    print(f"c2 3M max|d|={md:.3e} relL2={rel:.3e}")
+
+
 @pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
 def test_interpreter_kernel_twins(torch, name):
     # jit=False: the generic interpreter pass kernel (hsf_pass_kernel) instead
