@@ -28,6 +28,10 @@ import numpy as np  # noqa: E402
 METRIC = "HSF paths/s"
 # dram bytes read + written per launch of the dominant kernel, from one
 # `ncu --set full` capture of the same workload (profiles/r01/*details.txt)
+# L2-resident read bandwidth measured on the box (scripts/probe/l2bw.cu: 16 B
+# __ldcg loads over a 64 MiB L2-resident buffer, 592 CTAs x 512 threads): the
+# second denominator for kernels whose operands stay in L2 (frac > 1 vs HBM)
+L2_READ_GBS = 19710.0
 NCU_TRAFFIC = {("c2", "gemm"): 1.2576e9 + 0.1205e9}  # profiles/r01/h_c2_gemm_mn_details.txt (MN-major GEMM)
 
 
@@ -445,7 +449,8 @@ def main():
         roof = {"bound": "hbm", "kernel": "gather_dot (bitstring path-sum)", "achieved": ach, "peak": hbm,
                 "unit": "GB/s", "frac": ach / hbm, "traffic": None, "kernel_ms": core_ms,
                 "note": "algorithmic bytes = 2 operand rows of %d tree paths per sample (upper bound; rows "
-                        "shared by samples hit L2, so frac > 1 means L2-resident operands)" % Kt}
+                        "shared by samples hit L2, so frac > 1 means L2-resident operands)" % Kt,
+                "frac_of_l2_read": ach / L2_READ_GBS, "l2_read_peak_gbs": L2_READ_GBS}
 
     # the simulator tree (both halves concurrently): algorithmic bytes of its
     # tile passes over this rank's share of the paths / the sim phase
@@ -463,7 +468,7 @@ def main():
     sim_ach = sim_bytes / (sim_ms * 1e-3) / 1e9
     roof_sim = {"bound": "hbm", "kernel": "simulator tile passes (hsf_jit_pass, both halves)", "achieved": sim_ach,
                 "peak": hbm, "unit": "GB/s", "frac": sim_ach / hbm, "traffic": None, "kernel_ms": sim_ms,
-                "bytes": sim_bytes,
+                "bytes": sim_bytes, "frac_of_l2_read": sim_ach / L2_READ_GBS, "l2_read_peak_gbs": L2_READ_GBS,
                 "note": "algorithmic bytes = every pass reads + writes each output node state once; small "
                         "states stay L2/SMEM-resident, so frac can exceed 1"}
     if sim_ms > core_ms:
