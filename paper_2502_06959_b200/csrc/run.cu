@@ -229,7 +229,8 @@ static DeviceState* ensure_device(Plan* P, int device) {
             int cb = 0;
             if (tiled && n_cta * 4 <= num_sms()) cb = 2;
             else if (tiled && n_cta * 2 <= num_sms()) cb = 1;
-            const int nt = cb ? std::max(128, 1 << (ps.t - cb - 4)) : (n_cta < 2.0 * num_sms() ? 512 : 256);
+            int nt = cb ? std::max(128, 1 << (ps.t - cb - 4)) : (n_cta < 2.0 * num_sms() ? 512 : 256);
+            if (!cb) nt = std::min(nt, std::max(128, 1 << (ps.t - 2)));  // small narrow-level tiles (t = 10, 11)
             src.push_back(jit_pass_source(H, ps, c64, nt, cb, &P->coef));
             owner.push_back({v, h});
             d->jit_nt[v][h].push_back(nt);

@@ -604,6 +604,19 @@ def test_gauss_3m_c2_full_size(torch, monkeypatch):
     print(f"c2 3M max|d|={md:.3e} relL2={rel:.3e}")
 
 
+@pytest.mark.parametrize("name", ["c3", "c5"])
+def test_narrow_level_tiles(torch, name, monkeypatch):
+    # opt-in small tiles on narrow levels (t = 10 / 11 roots), tiled tier
+    monkeypatch.setenv("HSF_NARROW_TILES", "1")
+    inst = make_config(name, twin=True, n=28, n_low=14, n_bits=4096)
+    n, g = O.parse_circuit(inst.text)
+    P = O.plan(n, g, inst.n_low, inst.blocks)
+    A, B, c = O.half_states(P, 0, 8)
+    ref = O.recombine_bits(A, B, c, inst.bitstrings, inst.n_low)
+    got, _ = gpu_bits(torch, inst, inst.bitstrings, path_range=(0, 8))
+    check(got, ref, "c64")
+
+
 @pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
 def test_interpreter_kernel_twins(torch, name):
     # jit=False: the generic interpreter pass kernel (hsf_pass_kernel) instead
