@@ -71,7 +71,32 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
+    def _nvml_loop(self):
+        """NVML polling every 2 ms (an nvidia-smi call takes ~50-100 ms, longer
+        than c2's whole timed region); same fields as the nvidia-smi query."""
+        import pynvml as N
+        N.nvmlInit()
+        try:
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            bits = [getattr(N, "nvmlClocksEventReasonHwSlowdown", 0x8), getattr(N, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+                    getattr(N, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+                    getattr(N, "nvmlClocksEventReasonSwPowerCap", 0x4)]
+            while not self._stop.is_set():
+                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                rs = N.nvmlDeviceGetCurrentClocksEventReasons(h) if hasattr(N, "nvmlDeviceGetCurrentClocksEventReasons") \
+                    else N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                self.rows.append([str(sm), str(mx), hex(rs)] + ["Active" if rs & b else "Not Active" for b in bits])
+                self._stop.wait(0.002)
+        finally:
+            N.nvmlShutdown()
+
     def _loop(self):
+        try:
+            self._nvml_loop()
+            return
+        except Exception:
+            pass
         while not self._stop.is_set():
             try:
                 r = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
@@ -99,7 +124,8 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(self.rows),
+                "source": "NVML every 2 ms" if self.rows and self.rows[0][2].startswith("0x") else "nvidia-smi"}
 
 
 # ------------------------------------------------------------ reference arm
