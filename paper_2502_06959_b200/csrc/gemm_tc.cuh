@@ -1114,11 +1114,13 @@ __global__ void split_a_mn_kernel(const float2* __restrict__ leaves, const float
                                   __nv_bfloat16* __restrict__ hi, __nv_bfloat16* __restrict__ lo, long long K,
                                   long long lda, long long MA, long long r0, long long rows, const TailParams tp,
                                   const float2* __restrict__ ttab, __nv_bfloat16* __restrict__ lo2) {
+  // 4 rounds per thread of 2 consecutive rows: each warp load / store
+  // instruction covers 512 B / 128 B contiguous (coalesced; 8 consecutive rows
+  // per thread left half of every L1 sector unused)
   __shared__ int base[kMaxTail];
   __shared__ unsigned smask[kMaxTail];
   __shared__ long long node;
   const long long p = blockIdx.y;
-  const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 8;
   if (tp.mapped) {
     if (threadIdx.x < tp.n) {
       const int u = threadIdx.x;
@@ -1129,78 +1131,59 @@ __global__ void split_a_mn_kernel(const float2* __restrict__ leaves, const float
     if (threadIdx.x == 0) node = ((tp.p0 + p) / tp.T) % tp.Tt - tp.node0;
     __syncthreads();
   }
-  if (i >= lda) return;
-  float re[8], im[8];
   const float2 c = p < K ? cp[p] : make_float2(0.f, 0.f);
   const long long row = tp.mapped ? node : p;
   const float2* __restrict__ wrow = tp.W ? tp.W + ((tp.p0 + p) % tp.T) * tp.wld : nullptr;
-  if (p < K && i + 8 <= rows && (tp.W || !tp.n)) {
-    // common case: branch-free, all 16 loads in flight together
-    float2 x[8], w[8];
-    const float2* __restrict__ src = leaves + row * MA + r0 + i;
-    if ((r0 & 1) == 0) {  // 16 B loads (L1 wavefronts: 8 B strided loads were 96 % L1-bound)
+  const float2* __restrict__ src = leaves + row * MA + r0;
+  const bool vec = ((r0 & 1) == 0);
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float4 a4 = *reinterpret_cast<const float4*>(src + 2 * e);
-        x[2 * e] = make_float2(a4.x, a4.y);
-        x[2 * e + 1] = make_float2(a4.z, a4.w);
-        if (tp.W) {
-          const float4 w4 = *reinterpret_cast<const float4*>(wrow + r0 + i + 2 * e);
-          w[2 * e] = make_float2(w4.x, w4.y);
-          w[2 * e + 1] = make_float2(w4.z, w4.w);
-        } else {
-          w[2 * e] = w[2 * e + 1] = make_float2(1.f, 0.f);
-        }
+  for (int rd = 0; rd < 4; ++rd) {
+    const long long i = (long long)blockIdx.x * 2048 + rd * 512 + 2 * threadIdx.x;
+    if (i >= lda) break;
+    float2 v[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+    if (p < K && i + 2 <= rows && vec) {
+      const float4 a4 = *reinterpret_cast<const float4*>(src + i);
+      v[0] = cmul_f(make_float2(a4.x, a4.y), c);
+      v[1] = cmul_f(make_float2(a4.z, a4.w), c);
+      if (tp.W) {
+        const float4 w4 = *reinterpret_cast<const float4*>(wrow + r0 + i);
+        v[0] = cmul_f(v[0], make_float2(w4.x, w4.y));
+        v[1] = cmul_f(v[1], make_float2(w4.z, w4.w));
       }
     } else {
-#pragma unroll
-      for (int e = 0; e < 8; ++e) x[e] = src[e];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) w[e] = tp.W ? wrow[r0 + i + e] : make_float2(1.f, 0.f);
+      for (int e = 0; e < 2; ++e)
+        if (p < K && i + e < rows) {
+          v[e] = cmul_f(src[i + e], c);
+          if (tp.W) v[e] = cmul_f(v[e], wrow[r0 + i + e]);
+        }
     }
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const float2 v = cmul_f(cmul_f(x[e], c), w[e]);
-      re[e] = v.x;
-      im[e] = v.y;
-    }
-  } else {
-#pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    float2 v = make_float2(0.f, 0.f);
-    if (p < K && i + e < rows) {
-      v = cmul_f(leaves[row * MA + r0 + i + e], c);
-      if (tp.W) {
-        v = cmul_f(v, wrow[r0 + i + e]);
-      } else if (tp.n) {
+    if (!tp.W && tp.n && p < K) {  // tail weights without the table: per-unit loop
+      for (int e = 0; e < 2; ++e) {
+        if (i + e >= rows) continue;
         const unsigned ii = (unsigned)(r0 + i + e);
         for (int u = 0; u < tp.n; ++u) {
           unsigned mk = smask[u], x = 0;
           for (int q = 0; mk; ++q, mk &= mk - 1) x |= ((ii >> (__ffs(mk) - 1)) & 1u) << q;
-          v = cmul_f(v, __ldg(&ttab[base[u] + x]));
+          v[e] = cmul_f(v[e], __ldg(&ttab[base[u] + x]));
         }
       }
     }
-    re[e] = v.x;
-    im[e] = v.y;
-  }
-  }
-  __align__(16) __nv_bfloat16 h[16], l[16], m[16];
-#pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    split3(re[e], h[e], l[e], m[e]);
-    split3(im[e], h[8 + e], l[8 + e], m[8 + e]);
-  }
-  const long long o0 = (2 * p) * lda + i, o1 = o0 + lda;
-  *reinterpret_cast<uint4*>(hi + o0) = *reinterpret_cast<const uint4*>(h);
-  *reinterpret_cast<uint4*>(hi + o1) = *reinterpret_cast<const uint4*>(h + 8);
-  if (lo) {
-    *reinterpret_cast<uint4*>(lo + o0) = *reinterpret_cast<const uint4*>(l);
-    *reinterpret_cast<uint4*>(lo + o1) = *reinterpret_cast<const uint4*>(l + 8);
-  }
-  if (lo2) {
-    *reinterpret_cast<uint4*>(lo2 + o0) = *reinterpret_cast<const uint4*>(m);
-    *reinterpret_cast<uint4*>(lo2 + o1) = *reinterpret_cast<const uint4*>(m + 8);
+    __nv_bfloat162 h_re, h_im, l_re, l_im, m_re, m_im;
+    split3(v[0].x, h_re.x, l_re.x, m_re.x);
+    split3(v[1].x, h_re.y, l_re.y, m_re.y);
+    split3(v[0].y, h_im.x, l_im.x, m_im.x);
+    split3(v[1].y, h_im.y, l_im.y, m_im.y);
+    const long long o0 = (2 * p) * lda + i, o1 = o0 + lda;
+    *reinterpret_cast<__nv_bfloat162*>(hi + o0) = h_re;
+    *reinterpret_cast<__nv_bfloat162*>(hi + o1) = h_im;
+    if (lo) {
+      *reinterpret_cast<__nv_bfloat162*>(lo + o0) = l_re;
+      *reinterpret_cast<__nv_bfloat162*>(lo + o1) = l_im;
+    }
+    if (lo2) {
+      *reinterpret_cast<__nv_bfloat162*>(lo2 + o0) = m_re;
+      *reinterpret_cast<__nv_bfloat162*>(lo2 + o1) = m_im;
+    }
   }
 }
 
@@ -1487,7 +1470,7 @@ inline void tc_prep_a(const TcBuffers& t, const float2* leavesA, const float2* c
                       long long r0, long long rows, const tc::TailParams& tp, const float2* ttab, cudaStream_t st) {
   if (t.mn) {
     const long long lda = t.d.rows_pad;
-    tc::split_a_mn_kernel<<<dim3((unsigned)((lda / 8 + 255) / 256), (unsigned)t.d.Kpad), 256, 0, st>>>(
+    tc::split_a_mn_kernel<<<dim3((unsigned)((lda + 2047) / 2048), (unsigned)t.d.Kpad), 256, 0, st>>>(
         leavesA, cp, (__nv_bfloat16*)t.a_hi, (__nv_bfloat16*)t.a_lo, K, lda, MA, r0, rows, tp, ttab,
         (__nv_bfloat16*)t.a_l2);
     cudaError_t e = cudaGetLastError();
