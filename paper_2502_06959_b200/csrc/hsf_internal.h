@@ -59,7 +59,8 @@ constexpr int kMaxOpQ = 13;      // widest diagonal op (2^13 entries)
 constexpr int kMaxDenseQ = 5;    // widest dense op in the SMEM kernels
 constexpr int kMaxTrail = 8;     // folded trailing diagonal units (bitstring runs)
 constexpr int kMaxTail = 16;     // half-sided trailing diagonal factors (full-output operand prep)
-constexpr double kTailPrefixBytes = 16.0 * (1 << 20);  // prefix leaves of a half-sided fold
+constexpr double kTailPrefixBytes = 16.0 * (1 << 20);  // prefix-leaf budget (HSF_TAIL_PREFIX_BYTES mode)
+constexpr double kTailTableEntries = 1 << 20;           // default: tail weight table W[T][2^m] cap
 
 // One operation of a half-circuit program (half-local qubits, LSB-first:
 // q[j] is bit j of the op's local index).

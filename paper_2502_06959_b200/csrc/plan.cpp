@@ -1334,10 +1334,11 @@ Plan* build_plan(const char* text, size_t len, int n_low, int64_t n_blocks, cons
   // those diagonals at the amplitude's support bits (P:104-109 with the
   // factors moved last).  Half h's tree then stops at level u0 and the
   // product is taken while the split-bf16 GEMM operand is written.
-  // The shortened tree shares the folded factors' products across siblings no
-  // more, so the fold stops where the prefix leaves fit comfortably in L2
-  // (kTailPrefixBytes): u0 = the deepest such level, or the shallowest level
-  // the half's gates allow if that is deeper.
+  // The operand prep takes the folded diagonals' product from a per-plan table
+  // W[p mod T][i] (one load per element), so the fold reaches as far as that
+  // table stays small (kTailTableEntries; c2's half A: 8 of 12 units, T = 256,
+  // 8 MiB -- measured 0.880 vs 0.890 ms with the 1-3 unit folds of a 16 MiB
+  // prefix-leaf budget), or the shallowest level the half's gates allow.
   //
   // Head fold (same runs): leading units whose half-h factors act on basis
   // qubits are scalars on half h (head_units); they leave half h's tree
@@ -1347,7 +1348,8 @@ Plan* build_plan(const char* text, size_t len, int n_low, int64_t n_blocks, cons
   if (opts.fold_trailing_diag && U > 0) {
     const double elem = (opts.dtype == HSF_C64) ? 8.0 : 16.0;
     double budget = kTailPrefixBytes;
-    if (const char* e = std::getenv("HSF_TAIL_PREFIX_BYTES")) budget = std::strtod(e, nullptr);  // tests: 0 => longest fold
+    const char* budget_env = std::getenv("HSF_TAIL_PREFIX_BYTES");
+    if (budget_env) budget = std::strtod(budget_env, nullptr);  // tests: 0 => longest fold
     const char* nh = std::getenv("HSF_NO_HEAD_FOLD");
     for (int hh = 0; hh < 2; ++hh) {
       std::vector<int64_t> hidx;
@@ -1360,9 +1362,19 @@ Plan* build_plan(const char* text, size_t len, int n_low, int64_t n_blocks, cons
       }
       std::vector<int32_t> R = P->ranks;
       for (int u = 0; u < v0; ++u) R[u] = 1;
+      // default: the longest tail whose weight table W[T][2^m] (one load per
+      // operand element, built once per plan) stays within kTailTableEntries;
+      // HSF_TAIL_PREFIX_BYTES: the deepest level whose prefix leaves fit that budget
       int u_fit = 0;
-      for (int u = 1; u < U; ++u)
-        if ((double)range_prod(R, 0, u) * std::ldexp(elem, P->half[hh].m) <= budget) u_fit = u;
+      if (budget_env) {
+        for (int u = 1; u < U; ++u)
+          if ((double)range_prod(R, 0, u) * std::ldexp(elem, P->half[hh].m) <= budget) u_fit = u;
+      } else {
+        u_fit = U;
+        for (int u = U - 1; u >= 0; --u)
+          if ((double)range_prod(P->ranks, u, U) * std::ldexp(1.0, P->half[hh].m) <= kTailTableEntries) u_fit = u;
+        u_fit = std::min(u_fit, U - 1);
+      }
       int u0 = std::max({base->last_gate_level, U - kMaxTail, u_fit, v0});
       for (int u = U - 1; u >= u0; --u)
         if (!P->units[u].diag_route) {

@@ -175,9 +175,9 @@ def test_half_sided_tail_detection(hsf, monkeypatch):
     # half are diagonal with no gate of that half after them (hoisting moves
     # commuting gates above them)
     from paper_2502_06959_b200 import Plan
-    # default: the fold stops where the prefix leaves fit in 16 MiB (c2: 2^9
-    # prefixes x 32 KiB), or where the half's gates end
-    for name, twin, tail in [("c1", True, (1, 1)), ("c2", True, (1, 0)), ("c2", False, (3, 0)),
+    # default: the longest fold whose weight table W[T][2^m] has <= 2^20
+    # entries (c2: T = 2^8 of its 2^12 paths), or where the half's gates end
+    for name, twin, tail in [("c1", True, (1, 1)), ("c2", True, (8, 0)), ("c2", False, (8, 0)),
                              ("c3", True, (0, 0)), ("c4", True, (0, 0)), ("c5", True, (1, 1))]:
         inst = make_config(name, twin=twin)
         assert Plan(inst.text, inst.n_low, inst.blocks).tail_units == tail, name
