@@ -18,5 +18,6 @@ from .circuits import (  # noqa: F401
     make_table2,
     TABLE2,
     random_small_circuit,
+    random_folding_circuit,
     serialize,
 )

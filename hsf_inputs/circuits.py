@@ -369,6 +369,39 @@ def random_small_circuit(seed: int, n: int | None = None, n_gates: int | None = 
     return Instance(f"rand{seed}", n, n_low, g, blocks, None, "c128", {"seed": seed})
 
 
+def random_folding_circuit(seed: int, n: int | None = None, n_gates: int | None = None) -> Instance:
+    """Random circuit shaped to exercise the half-sided folds: X gates on
+    random qubits, then diagonal crossing gates (cz / cp / rzz, the head: they
+    see computational-basis qubits), then a random body (random_small_circuit's
+    library), then diagonal crossing gates again (the tail) and possibly a few
+    trailing 1-qubit gates.  Blocks: none (every crossing gate its own unit)."""
+    rng = np.random.default_rng([seed, 11])
+    n = n if n is not None else int(rng.integers(4, 10))
+    n_low = int(rng.integers(1, n))
+    body = random_small_circuit(seed + 1000, n=n, n_gates=n_gates if n_gates is not None else int(rng.integers(4, 16)))
+    g = []
+    for q in range(n):
+        if rng.uniform() < 0.5:
+            g.append(("x", (), (q,), None))
+
+    def diag_cross():
+        a = int(rng.integers(0, n_low))
+        b = int(rng.integers(n_low, n))
+        name = ("cz", "cp", "rzz")[int(rng.integers(3))]
+        params = (rng.uniform(0, 2 * math.pi),) if name in ("cp", "rzz") else ()
+        return (name, params, (a, b) if rng.uniform() < 0.5 else (b, a), None)
+
+    for _ in range(int(rng.integers(1, 4))):
+        g.append(diag_cross())
+    g += [x for x in body.gates if x[0] != "u" or len(x[2]) == 1]
+    for _ in range(int(rng.integers(1, 4))):
+        g.append(diag_cross())
+    for _ in range(int(rng.integers(0, 3))):
+        q = int(rng.integers(n))
+        g.append(("h", (), (q,), None))
+    return Instance(f"fold{seed}", n, n_low, g, [], None, "c64", {"seed": seed})
+
+
 # ------------------------------------------------------------------- registry
 CONFIGS = {
     "c1": make_c1,

@@ -100,9 +100,42 @@ def test_random_small_circuits(torch, seed):
     for dtype in ("c64", "c128"):
         got, _ = gpu_full(torch, inst, dtype=dtype, precision="simt")
         check(got, ref, dtype)
+    # the tensor-core path with its head / tail folds and operand layouts
+    for prec in ("bf16x3", "bf16x6"):
+        got, _ = gpu_full(torch, inst, dtype="c64", precision=prec)
+        check(got, ref, "c64")
     got, _ = gpu_full(torch, inst, dtype="c128", precision="simt", individual=True) \
         if O.plan(n, g, inst.n_low, None, "individual").n_paths <= 4096 else (ref, None)
     check(got, ref, "c128")
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_folding_circuits(torch, seed):
+    # X-prepared qubits, diagonal crossing gates before and after a random
+    # body: head and tail folds on random supports, against the Schroedinger
+    # state and the oracle's partial sums over a random aligned / unaligned range
+    from hsf_inputs import random_folding_circuit
+    inst = random_folding_circuit(seed)
+    n, g = O.parse_circuit(inst.text)
+    P = O.plan(n, g, inst.n_low, inst.blocks)
+    if P.n_paths > 4096:
+        pytest.skip("path count above the test budget")
+    ref = O.schrodinger(n, g)
+    got, Pg = gpu_full(torch, inst, dtype="c64", precision="bf16x3")
+    check(got, ref, "c64")
+    # three random consecutive path ranges accumulated into one buffer (partial
+    # sums themselves depend on the SVD basis of degenerate sigma, SURVEY
+    # reading 6, so only their total is compared); unaligned ranges fall back
+    # from the folded trees
+    from paper_2502_06959_b200 import Plan
+    rng = np.random.default_rng(seed)
+    cuts = sorted({0, P.n_paths, *(int(x) for x in rng.integers(1, P.n_paths, 2))})
+    Pr = Plan(inst.text, inst.n_low, inst.blocks)
+    out = torch.zeros(1 << n, dtype=torch.complex64, device="cuda")
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        Pr.run(out, path_range=(a, b), precision="bf16x3", accumulate=True)
+    torch.cuda.synchronize()
+    check(out.cpu().numpy(), ref, "c64")
 
 
 @pytest.mark.parametrize("tile", [10, 11, 12])
