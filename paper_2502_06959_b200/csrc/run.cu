@@ -176,20 +176,6 @@ static DeviceState* ensure_device(Plan* P, int device) {
   };
   if (P->fold_u0 >= 0) upload_tab(P->trail_tab, &d->trail);
   if (!P->tail_tab.empty()) upload_tab(P->tail_tab, &d->tail);
-  // tail weight tables (complex64 tensor-core runs): W[t][i] over the tail
-  // digit combinations, when small (<= 2^22 entries)
-  for (int h = 0; h < 2 && c64; ++h) {
-    const Plan::Tail& T = P->tail[h];
-    const long long wld = 1ll << P->half[h].m;
-    const char* nt = std::getenv("HSF_TAIL_NO_TABLE");  // tests: per-unit weight loop
-    if (T.u0 < 0 || T.mask.empty() || (double)T.T * (double)wld > (double)(1 << 22) || (nt && nt[0] == '1')) continue;
-    CK(cudaMalloc(&d->tailw[h], (size_t)T.T * wld * sizeof(float2)));
-    const tc::TailParams tp = tail_params(*P, h);
-    const long long nel = (long long)T.T * wld;
-    tc::tail_weights_kernel<<<(unsigned)((nel + 255) / 256), 256>>>(d->tailw[h], wld, tp, (const float2*)d->tail);
-    CK(cudaGetLastError());
-    CK(cudaDeviceSynchronize());
-  }
   if (P->permuted) {
     std::vector<unsigned long long> tab(4 * 65536, 0);
     for (int k = 0; k < 4; ++k)
@@ -475,6 +461,24 @@ static void ensure_ws(DeviceState* d, size_t bytes) {
 
 // c_p = prod_u c_{u,d_u} over the tree's units for tree paths p in [p0, p1),
 // fp64 on the host -> run dtype
+// Tail weight table W[t][i] of half h (complex64 tensor-core runs with the
+// half-sided fold), built at the first run that uses it -- outside any graph
+// capture -- when it has <= 2^22 entries; else the operand prep loops over
+// the folded units per element.
+static void ensure_tailw(Plan* P, DeviceState* d, int h) {
+  if (d->tailw[h] || d->elem != 8) return;
+  const Plan::Tail& T = P->tail[h];
+  const long long wld = 1ll << P->half[h].m;
+  const char* nt = std::getenv("HSF_TAIL_NO_TABLE");  // tests: per-unit weight loop
+  if (T.u0 < 0 || T.mask.empty() || (double)T.T * (double)wld > (double)(1 << 22) || (nt && nt[0] == '1')) return;
+  CK(cudaMalloc(&d->tailw[h], (size_t)T.T * wld * sizeof(float2)));
+  const tc::TailParams tp = tail_params(*P, h);
+  const long long nel = (long long)T.T * wld;
+  tc::tail_weights_kernel<<<(unsigned)((nel + 255) / 256), 256>>>(d->tailw[h], wld, tp, (const float2*)d->tail);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+}
+
 // heads: bit h set => half h's head-scalar units (Plan::Tail::v0) are folded
 // into c_p as well
 static void ensure_cp(Plan* P, DeviceState* d, uint64_t p0, uint64_t p1, int U_tree, int heads, cudaStream_t st) {
@@ -863,6 +867,8 @@ static void run(Plan* P, const hsf_run_args& a) {
   for (int h = 0; h < 2; ++h)
     if (L.var[h] == 2 && P->tail[h].v0 > 0) heads |= 1 << h;
   ensure_cp(P, d, L.p0, L.p1, L.U_tree, heads, st);
+  for (int h = 0; h < 2; ++h)
+    if (L.var[h] == 2) ensure_tailw(P, d, h);
   const bool timed = a.phase_ms != nullptr;
   try {
     const char* ng = std::getenv("HSF_NO_GRAPH");
