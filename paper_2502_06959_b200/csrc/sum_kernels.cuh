@@ -181,29 +181,63 @@ __global__ void bucket_count_kernel(const unsigned long long* __restrict__ bits,
     atomicAdd(&counts[bits[i] >> n_low], 1);
 }
 
-// exclusive scan of counts[0..n) into offs[0..n] (offs[n] = total); one CTA of 1024
+// exclusive scan of counts[0..n) into offs[0..n] (offs[n] = total) and
+// cursor[0..n); one CTA of 1024 threads: warp w owns a contiguous span, read
+// in coalesced 32-element chunks with shuffle scans (a per-thread sequential
+// span made every load its own L2 round trip: 80 us for c3's 2^15 rows)
 __global__ void __launch_bounds__(1024) bucket_scan_kernel(const int* __restrict__ counts, int* __restrict__ offs,
                                                            int* __restrict__ cursor, long long n) {
-  __shared__ int part[1024];
-  const int t = threadIdx.x;
-  const long long per = (n + 1023) / 1024, b = t * per, e = min(n, b + per);
-  int sum = 0;
-  for (long long i = b; i < e; ++i) sum += counts[i];
-  part[t] = sum;
+  __shared__ int wsum[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const long long span = (n + 31) / 32, b = w * span, e = min(n, b + span);
+  int tot = 0;  // pass 1: this warp's total (8 chunks of loads in flight)
+  for (long long c0 = b; c0 < e; c0 += 256) {
+    int v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = c0 + 32 * k + lane < e ? counts[c0 + 32 * k + lane] : 0;
+    int sum = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sum += v[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    tot += sum;
+  }
+  if (lane == 0) wsum[w] = tot;
   __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {  // Hillis-Steele inclusive scan of the partials
-    const int v = t >= o ? part[t - o] : 0;
-    __syncthreads();
-    part[t] += v;
-    __syncthreads();
+  if (w == 0) {  // exclusive scan of the 32 warp totals
+    const int x = wsum[lane];
+    int inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    wsum[lane] = inc - x;
+    if (lane == 31) offs[n] = inc;
   }
-  int run = t ? part[t - 1] : 0;
-  for (long long i = b; i < e; ++i) {
-    offs[i] = run;
-    cursor[i] = run;
-    run += counts[i];
+  __syncthreads();
+  int run = wsum[w];  // pass 2: scan each chunk, carry the running total
+  for (long long c0 = b; c0 < e; c0 += 256) {
+    int v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = c0 + 32 * k + lane < e ? counts[c0 + 32 * k + lane] : 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const long long c = c0 + 32 * k;
+      const int x = v[k];
+      int inc = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      if (c + lane < e) {
+        offs[c + lane] = run + inc - x;
+        cursor[c + lane] = run + inc - x;
+      }
+      run += __shfl_sync(0xffffffffu, inc, 31);
+    }
   }
-  if (t == 1023) offs[n] = part[1023];
 }
 
 __global__ void bucket_scatter_kernel(const unsigned long long* __restrict__ bits, long long n, int n_low,
