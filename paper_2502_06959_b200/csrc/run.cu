@@ -72,6 +72,8 @@ struct DeviceState {
   bool capturing = false;
   cudaEvent_t evg[2] = {}, evc[2] = {};  // host-output chunks: GEMM done / D2H done
   cudaStream_t side = nullptr;  // half-B stream; D2H stream of host-output chunks
+  cudaStream_t aux = nullptr;   // bitstring prep (H2D, relabel, bucket sort), overlapping the trees
+  cudaEvent_t ev_aux = nullptr;
   bool sticky = false;
 };
 
@@ -105,6 +107,8 @@ void destroy_device(Plan* p) {
     if (d->evc[i]) cudaEventDestroy(d->evc[i]);
   }
   if (d->side) cudaStreamDestroy(d->side);
+  if (d->aux) cudaStreamDestroy(d->aux);
+  if (d->ev_aux) cudaEventDestroy(d->ev_aux);
   if (cur >= 0) cudaSetDevice(cur);
   delete d;
   p->dev = nullptr;
@@ -267,6 +271,8 @@ static DeviceState* ensure_device(Plan* P, int device) {
     CK(cudaEventCreateWithFlags(&d->evc[i], cudaEventDisableTiming));
   }
   CK(cudaStreamCreateWithFlags(&d->side, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&d->aux, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&d->ev_aux, cudaEventDisableTiming));
   return d;
 }
 
@@ -679,23 +685,20 @@ static void prep_half(Plan* P, DeviceState* d, const Layout& L, int h, cudaStrea
   }
 }
 
-// bitstring path-sum (K6) into `out` (device)
-template <typename R>
-static void run_core_bits(Plan* P, DeviceState* d, const Layout& L, const hsf_run_args& a, cudaStream_t st,
-                          typename cplx<R>::T* out) {
-  using C = typename cplx<R>::T;
+// Bitstring-run input prep, independent of the path trees (runs on the aux
+// stream beside them): H2D of host bitstrings, the relabelling of
+// non-contiguous partitions, and the bucket sort of the grouped gather.
+// Returns the device bitstrings in internal bit order.
+static const unsigned long long* prep_bits(Plan* P, DeviceState* d, const Layout& L, const hsf_run_args& a,
+                                           cudaStream_t st) {
   char* ws = (char*)d->ws;
   const int nB = P->n_low;
-  const long long K = (long long)L.K;
-  const C* AT = (const C*)(ws + L.off_T[0]);
-  const C* BT = (const C*)(ws + L.off_T[1]);
   const unsigned long long* bits = (const unsigned long long*)a.bitstrings;
   if (!a.bits_on_device) {
     bits = (const unsigned long long*)(ws + L.off_bits);
     CK(cudaMemcpyAsync((void*)bits, a.bitstrings, a.n_bitstrings * 8, cudaMemcpyHostToDevice, st));
   }
   const long long ns = (long long)a.n_bitstrings;
-  long long blocks = std::min<long long>((ns + 7) / 8, 148ll * 64);
   if (P->permuted) {  // caller bit order -> internal (relabelled) bit order
     unsigned long long* pb = (unsigned long long*)(ws + L.off_pbits);
     permute_bits_kernel<<<(unsigned)std::min<long long>((ns + 255) / 256, 148ll * 8), 256, 0, st>>>(bits, pb, ns,
@@ -703,15 +706,7 @@ static void run_core_bits(Plan* P, DeviceState* d, const Layout& L, const hsf_ru
     CK(cudaGetLastError());
     bits = pb;
   }
-  TrailParams tw{};
-  if (L.fold) {
-    tw.n = (int)P->trail_mask.size();
-    for (int u = 0; u < tw.n; ++u) {
-      tw.mask[u] = P->trail_mask[u];
-      tw.off[u] = P->trail_off[u];
-    }
-  }
-  if (sizeof(R) == 4 && L.grouped) {
+  if (L.grouped) {
     const long long nrowsA = 1ll << (P->n - nB);
     int* counts = (int*)(ws + L.off_grp);
     int* offs = counts + nrowsA;
@@ -722,6 +717,35 @@ static void run_core_bits(Plan* P, DeviceState* d, const Layout& L, const hsf_ru
     bucket_count_kernel<<<gb, 256, 0, st>>>(bits, ns, nB, counts);
     bucket_scan_kernel<<<1, 1024, 0, st>>>(counts, offs, cursor, nrowsA);
     bucket_scatter_kernel<<<gb, 256, 0, st>>>(bits, ns, nB, cursor, perm);
+    CK(cudaGetLastError());
+  }
+  return bits;
+}
+
+// bitstring path-sum (K6) into `out` (device)
+template <typename R>
+static void run_core_bits(Plan* P, DeviceState* d, const Layout& L, const hsf_run_args& a, cudaStream_t st,
+                          typename cplx<R>::T* out, const unsigned long long* bits) {
+  using C = typename cplx<R>::T;
+  char* ws = (char*)d->ws;
+  const int nB = P->n_low;
+  const long long K = (long long)L.K;
+  const C* AT = (const C*)(ws + L.off_T[0]);
+  const C* BT = (const C*)(ws + L.off_T[1]);
+  const long long ns = (long long)a.n_bitstrings;
+  long long blocks = std::min<long long>((ns + 7) / 8, 148ll * 64);
+  TrailParams tw{};
+  if (L.fold) {
+    tw.n = (int)P->trail_mask.size();
+    for (int u = 0; u < tw.n; ++u) {
+      tw.mask[u] = P->trail_mask[u];
+      tw.off[u] = P->trail_off[u];
+    }
+  }
+  if (sizeof(R) == 4 && L.grouped) {  // bucket sort done by prep_bits
+    const long long nrowsA = 1ll << (P->n - nB);
+    const int* offs = (const int*)(ws + L.off_grp) + nrowsA;
+    const int* perm = offs + 2 * nrowsA + 1;
     const unsigned gw = (unsigned)std::min<long long>((nrowsA + 7) / 8, 148ll * 64);  // 8 warps per CTA
     const float4* A4 = (const float4*)AT;
     const float4* B4 = (const float4*)BT;
@@ -795,6 +819,12 @@ static void run_all(Plan* P, DeviceState* d, const Layout& L, const hsf_run_args
   // stream; the two path trees are independent until the path-sum
   CK(cudaEventRecord(d->ev[0], st));
   CK(cudaStreamWaitEvent(d->side, d->ev[0], 0));
+  const unsigned long long* bits_d = nullptr;
+  if (L.bits_mode) {  // bitstring prep on the aux stream, beside both trees
+    CK(cudaStreamWaitEvent(d->aux, d->ev[0], 0));
+    bits_d = prep_bits(P, d, L, a, d->aux);
+    CK(cudaEventRecord(d->ev_aux, d->aux));
+  }
   run_half<R>(*P, d, 1, L, d->side);
   if (timed) rec(d->ev[2], d->side);
   prep_half<R>(P, d, L, 1, d->side);
@@ -807,7 +837,8 @@ static void run_all(Plan* P, DeviceState* d, const Layout& L, const hsf_run_args
   char* ws = (char*)d->ws;
   if (L.bits_mode) {
     C* out = a.out_on_device ? (C*)a.out : (C*)(ws + L.off_out);
-    run_core_bits<R>(P, d, L, a, st, out);
+    CK(cudaStreamWaitEvent(st, d->ev_aux, 0));
+    run_core_bits<R>(P, d, L, a, st, out, bits_d);
     if (!a.out_on_device)
       CK(cudaMemcpyAsync(a.out, out, (size_t)a.n_bitstrings * sizeof(C), cudaMemcpyDeviceToHost, st));
   } else if (a.out_on_device && P->permuted) {
