@@ -654,6 +654,7 @@ static std::vector<DevOp> regpass_rewrite(const std::vector<DevOp>& ops, int t) 
   std::vector<DevOp> out;
   int hdr = -1;
   std::vector<int> RS;
+  size_t free_start = 0;  // out[free_start..) are standalone diagonals (no group owns them)
   auto close = [&]() {
     if (hdr < 0) return;
     int n_r1 = 0;
@@ -669,6 +670,7 @@ static std::vector<DevOp> regpass_rewrite(const std::vector<DevOp>& ops, int t) 
       out.erase(out.begin() + hdr);
       hdr = -1;
       RS.clear();
+      free_start = out.size();
       return;
     }
     DevOp& h = out[hdr];
@@ -682,6 +684,7 @@ static std::vector<DevOp> regpass_rewrite(const std::vector<DevOp>& ops, int t) 
     h.div = 1;
     hdr = -1;
     RS.clear();
+    free_start = out.size();
   };
   for (const DevOp& d : ops) {
     if (hdr >= 0 && (int)out.size() - hdr >= kMaxPassOps / 2) close();
@@ -690,8 +693,12 @@ static std::vector<DevOp> regpass_rewrite(const std::vector<DevOp>& ops, int t) 
       auto it = std::find(RS.begin(), RS.end(), pos);
       if (hdr >= 0 && it == RS.end() && (int)RS.size() == kRegQ) close();
       if (hdr < 0) {
-        hdr = (int)out.size();
-        out.push_back(DevOp{});
+        // open the group before the standalone diagonals just preceding it:
+        // they run on the registers too (index from the group base + register
+        // bits), saving an element-owner SMEM sweep and a barrier
+        hdr = (int)std::max(free_start, out.size());
+        while ((size_t)hdr > free_start && out[hdr - 1].kind == OP_DIAG) --hdr;
+        out.insert(out.begin() + hdr, DevOp{});
       }
       it = std::find(RS.begin(), RS.end(), pos);
       int slot = (int)(it - RS.begin());
@@ -705,6 +712,7 @@ static std::vector<DevOp> regpass_rewrite(const std::vector<DevOp>& ops, int t) 
     } else {
       close();
       out.push_back(d);
+      free_start = out.size();
     }
   }
   close();
