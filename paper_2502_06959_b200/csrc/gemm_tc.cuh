@@ -60,6 +60,8 @@ struct Params {
 
   int x3;
   int x6;                   // bf16x6: third operand plane (lo2), 6 products (pair kernel only)
+  int bk;                   // 1 (pair kernel, with mn): B K-major [nrows_b_pad][Kpad] instead (swapped path-sum)
+  int bn;                   // pair tile N (multiple of 32, <= BN; < BN only with bk)
   int n_maps;               // > 0: fused reduce-scatter -- output rows [o*rows_per_map, +rows_per_map)
   int rows_per_map;         //      are TMA-reduce-added into OutMaps::m[o] (row o*rows_per_map -> 0)
   float* out;               // D, row-major, ld = ldo floats
@@ -512,7 +514,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * EW, 1)
   // stage layout: npl A plane slots, then npl B plane slots (hi, lo[, lo2])
   const int npl = p.x6 ? 3 : 2;
   const uint32_t SS = (uint32_t)npl * (A_TILE + B2_TILE);
-  const uint32_t stage_bytes = (uint32_t)(p.x6 ? 3 : p.x3 ? 2 : 1) * (A_TILE + B2_TILE);
+  const uint32_t stage_bytes = (uint32_t)(p.x6 ? 3 : p.x3 ? 2 : 1) * (A_TILE + (p.bk ? (p.bn / 2) * 128 : B2_TILE));
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
@@ -524,7 +526,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * EW, 1)
       for (int tile = pair; tile < num_tiles; tile += num_pairs) {
         int mb, nb;
         tile_coords(p, tile, mb, nb);
-        const int arow = (2 * mb + (int)rank) * BM, brow = nb * BN + (int)rank * (BN / 2);
+        const int arow = (2 * mb + (int)rank) * BM, brow = nb * p.bn + (int)rank * (p.bn / 2);
         for (int kb = 0; kb < p.num_k; ++kb) {
           mbar_wait(&empty_bar[s], ph ^ 1);
           uint8_t* st = smem + s * SS;
@@ -536,10 +538,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * EW, 1)
               if (p.x3) tma_load_2sm(st + A_TILE + j * 8192, &mA_lo, &full_bar[s], arow + j * 64, kb * BK, a_pol);
               if (p.x6) tma_load_2sm(st + 2 * A_TILE + j * 8192, &mA_l2, &full_bar[s], arow + j * 64, kb * BK, a_pol);
             }
-            for (int j = 0; j < BN / 128; ++j) {
-              tma_load_2sm(sb + j * 8192, &mB_hi, &full_bar[s], brow + j * 64, kb * BK, b_pol);
-              if (p.x3) tma_load_2sm(sb + B2_TILE + j * 8192, &mB_lo, &full_bar[s], brow + j * 64, kb * BK, b_pol);
-              if (p.x6) tma_load_2sm(sb + 2 * B2_TILE + j * 8192, &mB_l2, &full_bar[s], brow + j * 64, kb * BK, b_pol);
+            if (p.bk) {  // K-major B: one {BK, bn/2} box per plane
+              tma_load_2sm(sb, &mB_hi, &full_bar[s], kb * BK, brow, b_pol);
+              if (p.x3) tma_load_2sm(sb + B2_TILE, &mB_lo, &full_bar[s], kb * BK, brow, b_pol);
+              if (p.x6) tma_load_2sm(sb + 2 * B2_TILE, &mB_l2, &full_bar[s], kb * BK, brow, b_pol);
+            } else {
+              for (int j = 0; j < BN / 128; ++j) {
+                tma_load_2sm(sb + j * 8192, &mB_hi, &full_bar[s], brow + j * 64, kb * BK, b_pol);
+                if (p.x3) tma_load_2sm(sb + B2_TILE + j * 8192, &mB_lo, &full_bar[s], brow + j * 64, kb * BK, b_pol);
+                if (p.x6) tma_load_2sm(sb + 2 * B2_TILE + j * 8192, &mB_l2, &full_bar[s], brow + j * 64, kb * BK, b_pol);
+              }
             }
           } else {
             const int kc = kb * (TF32 ? BK / 2 : BK);  // element coordinate of this 128 B k block
@@ -574,7 +582,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * EW, 1)
           const uint32_t st = smem_u32(smem + s * SS);
           const uint32_t a_hi = st, a_lo = st + A_TILE, a_l2 = st + 2 * A_TILE;
           const uint32_t b_hi = st + npl * A_TILE, b_lo = b_hi + B2_TILE, b_l2 = b_hi + 2 * B2_TILE;
-          if (p.mn) {
+          if (p.mn && p.bk) {  // A MN-major (k step 16 rows = 2 KB), B K-major (k step 32 B), N = bn
+            const uint32_t id = (IDESC2 & ~(0x3Fu << 17)) | ((uint32_t)(p.bn >> 3) << 17) | (1u << 15);
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k) {
+              const uint32_t kr = k * 2048, ko = k * 32;
+              mma2_bf16(d, sw128_desc_mn(a_hi + kr), sw128_desc(b_hi + ko), (kb | k) ? 1u : 0u, id);
+              if (p.x3) {
+                mma2_bf16(d, sw128_desc_mn(a_hi + kr), sw128_desc(b_lo + ko), 1u, id);
+                mma2_bf16(d, sw128_desc_mn(a_lo + kr), sw128_desc(b_hi + ko), 1u, id);
+              }
+              if (p.x6) {
+                mma2_bf16(d, sw128_desc_mn(a_lo + kr), sw128_desc(b_lo + ko), 1u, id);
+                mma2_bf16(d, sw128_desc_mn(a_hi + kr), sw128_desc(b_l2 + ko), 1u, id);
+                mma2_bf16(d, sw128_desc_mn(a_l2 + kr), sw128_desc(b_hi + ko), 1u, id);
+              }
+            }
+          } else if (p.mn) {
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
               const uint32_t kr = k * 2048;
@@ -639,10 +663,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * EW, 1)
       int mb, nb;
       tile_coords(p, tile, mb, nb);
       const int row0 = (2 * mb + (int)rank) * BM;
+      const int nc = p.bn / 32;  // 32-column chunks of the tile
       mbar_wait(&tfull_bar[acc], aph);
       asm volatile("tcgen05.fence::after_thread_sync;");
+      if (half >= nc) {  // narrow tile: no chunk for this warp
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        mbar_arrive_leader(&tempty_bar[acc]);
+      }
 #pragma unroll 1
-      for (int c = half; c < BN / 32; c += G) {
+      for (int c = half; c < nc; c += G) {
         uint32_t v[32];
         const uint32_t taddr = tmem_base + (uint32_t)(acc * BN + c * 32) + ((uint32_t)(q * 32) << 16);
         asm volatile(
@@ -655,7 +684,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * EW, 1)
               "=r"(v[30]), "=r"(v[31])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (c >= BN / 32 - G) {
+        if (c >= nc - G) {
           asm volatile("tcgen05.fence::before_thread_sync;");
           mbar_arrive_leader(&tempty_bar[acc]);
         }
@@ -679,11 +708,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * EW, 1)
         if (lane == 0) {
           if (p.n_maps) {  // fused reduce-scatter: this CTA's 128 rows belong to one owner shard
             const int o = row0 / p.rows_per_map;
-            tma_reduce_add_2d(&om.m[o], stg, nb * BN + c * 32, row0 - o * p.rows_per_map + q * 32, st_pol);
+            tma_reduce_add_2d(&om.m[o], stg, nb * p.bn + c * 32, row0 - o * p.rows_per_map + q * 32, st_pol);
           } else if (p.accumulate) {
-            tma_reduce_add_2d(&mOut, stg, nb * BN + c * 32, row0 + q * 32, st_pol);
+            tma_reduce_add_2d(&mOut, stg, nb * p.bn + c * 32, row0 + q * 32, st_pol);
           } else {
-            tma_store_2d(&mOut, stg, nb * BN + c * 32, row0 + q * 32, st_pol);
+            tma_store_2d(&mOut, stg, nb * p.bn + c * 32, row0 + q * 32, st_pol);
           }
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
@@ -1047,23 +1076,26 @@ __global__ void split_a_kernel(const float2* __restrict__ leaves, const float2* 
 }
 
 // B'' rows [0, 2*MB_pad): row 2j <- (re, -im), row 2j+1 <- (im, re) of B[p][j]
+// (swapped path-sum: the leaves are half A's, columns col0.. of rows of
+// length MS, times c_p when cp is given)
 template <typename T2>
 __global__ void split_b_kernel(const float2* __restrict__ leaves, T2* __restrict__ hi,
                                T2* __restrict__ lo, long long K, long long Kpad, long long MB,
                                const TailParams tp, const float2* __restrict__ ttab,
-                               T2* __restrict__ lo2) {
+                               T2* __restrict__ lo2, const float2* __restrict__ cp, long long col0, long long MS) {
   __shared__ float2 t[32][33];
   const long long j0 = (long long)blockIdx.x * 32, p0 = (long long)blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;
   __shared__ TailTile tt;
-  if (tp.mapped) tail_tile_setup(tt, tp, p0, j0);
+  if (tp.mapped) tail_tile_setup(tt, tp, p0, col0 + j0);
   for (int r = ty; r < 32; r += 8) {
     long long p = p0 + r, j = j0 + tx;
     float2 v = make_float2(0.f, 0.f);
     if (p < K && j < MB) {
-      v = leaves[(tp.mapped ? tt.node[r] : p) * MB + j];
-      if (tp.W) v = cmul_f(v, tp.W[((tp.p0 + p) % tp.T) * tp.wld + j]);
+      v = leaves[(tp.mapped ? tt.node[r] : p) * MS + col0 + j];
+      if (tp.W) v = cmul_f(v, tp.W[((tp.p0 + p) % tp.T) * tp.wld + col0 + j]);
       else if (tp.n) v = cmul_f(v, tail_weight(tt, tp.n, ttab, r, tx));
+      if (cp) v = cmul_f(v, cp[p]);
     }
     t[r][tx] = v;
   }
@@ -1131,7 +1163,7 @@ __global__ void split_a_mn_kernel(const float2* __restrict__ leaves, const float
     if (threadIdx.x == 0) node = ((tp.p0 + p) / tp.T) % tp.Tt - tp.node0;
     __syncthreads();
   }
-  const float2 c = p < K ? cp[p] : make_float2(0.f, 0.f);
+  const float2 c = p < K ? (cp ? cp[p] : make_float2(1.f, 0.f)) : make_float2(0.f, 0.f);  // cp null => 1
   const long long row = tp.mapped ? node : p;
   const float2* __restrict__ wrow = tp.W ? tp.W + ((tp.p0 + p) % tp.T) * tp.wld : nullptr;
   const float2* __restrict__ src = leaves + row * MA + r0;
@@ -1190,10 +1222,13 @@ __global__ void split_a_mn_kernel(const float2* __restrict__ leaves, const float
 // MN-major B'' (p.mn): row 2p <- (re, im) of B[p][j] at columns (2j, 2j+1),
 // row 2p+1 <- (-im, re): the same operand as split_b_kernel's, transposed, so
 // each row is one leaf, written elementwise.  One CTA per (path, 512 amplitudes).
+// (swapped path-sum: the leaves are half A's, columns col0.. of rows of
+// length MS, times c_p when cp is given)
 __global__ void split_b_mn_kernel(const float2* __restrict__ leaves, __nv_bfloat16* __restrict__ hi,
                                   __nv_bfloat16* __restrict__ lo, long long K, long long ldb, long long MB,
                                   const TailParams tp, const float2* __restrict__ ttab,
-                                  __nv_bfloat16* __restrict__ lo2) {
+                                  __nv_bfloat16* __restrict__ lo2, const float2* __restrict__ cp, long long col0,
+                                  long long MS) {
   __shared__ int base[kMaxTail];
   __shared__ unsigned smask[kMaxTail];
   __shared__ long long node;
@@ -1212,9 +1247,10 @@ __global__ void split_b_mn_kernel(const float2* __restrict__ leaves, __nv_bfloat
   if (2 * j >= ldb) return;
   float2 v[4];
   const long long row = tp.mapped ? node : p;
-  const float2* __restrict__ wrow = tp.W ? tp.W + ((tp.p0 + p) % tp.T) * tp.wld : nullptr;
-  if (p < K && j + 4 <= MB && (tp.W || !tp.n)) {
-    const float2* __restrict__ src = leaves + row * MB + j;
+  const float2* __restrict__ wrow = tp.W ? tp.W + ((tp.p0 + p) % tp.T) * tp.wld + col0 : nullptr;
+  const float2 cpv = cp && p < K ? cp[p] : make_float2(1.f, 0.f);
+  if (p < K && j + 4 <= MB && (tp.W || !tp.n) && ((col0 & 1) == 0)) {
+    const float2* __restrict__ src = leaves + row * MS + col0 + j;
     float2 w[4];
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
@@ -1236,11 +1272,11 @@ __global__ void split_b_mn_kernel(const float2* __restrict__ leaves, __nv_bfloat
   for (int e = 0; e < 4; ++e) {
     v[e] = make_float2(0.f, 0.f);
     if (p < K && j + e < MB) {
-      v[e] = leaves[row * MB + j + e];
+      v[e] = leaves[row * MS + col0 + j + e];
       if (tp.W) {
         v[e] = cmul_f(v[e], wrow[j + e]);
       } else if (tp.n) {
-        const unsigned ii = (unsigned)(j + e);
+        const unsigned ii = (unsigned)(col0 + j + e);
         for (int u = 0; u < tp.n; ++u) {
           unsigned mk = smask[u], x = 0;
           for (int q = 0; mk; ++q, mk &= mk - 1) x |= ((ii >> (__ffs(mk) - 1)) & 1u) << q;
@@ -1248,6 +1284,10 @@ __global__ void split_b_mn_kernel(const float2* __restrict__ leaves, __nv_bfloat
         }
       }
     }
+  }
+  if (cp) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) v[e] = cmul_f(v[e], cpv);
   }
   __align__(16) __nv_bfloat16 h[16], l[16], m[16];
 #pragma unroll
@@ -1428,6 +1468,8 @@ struct TcBuffers {
   int planes = 2;
   bool tf32 = false;  // tf32x3: fp32-storage K-major operands, kind::tf32
   bool mn = false;    // operands MN-major: A''^T [2*Kpad][rows_pad], B''^T [2*Kpad][nrows_b_pad] bf16
+  bool bk = false;    // with mn: B K-major instead, pair tiles bn columns wide (tc_swap_buffers)
+  int bn = tc::BN;
   long long K = 0;    // paths (operand k extent before padding)
 };
 
@@ -1462,6 +1504,18 @@ inline TcBuffers tc_buffers(long long K, long long rows, long long MB, int plane
   t.b_l2 = planes >= 3 ? (__nv_bfloat162*)take(t.d.b_bytes) : nullptr;
   t.mn = !t.tf32 && tc_mn(K);
   t.K = K;
+  return t;
+}
+
+// swapped path-sum (few output rows): A'' = half B's leaves MN-major (2^nB
+// GEMM rows), B'' = the MB output rows of half A (c_p, rotation) K-major, one
+// pair tile of bn = 32 * ceil(2 MB / 32) columns -- the big operand is read
+// once and the narrow one stays in L2
+inline TcBuffers tc_swap_buffers(long long K, long long rows, long long MB, int planes, void* ws, size_t ws_bytes) {
+  TcBuffers t = tc_buffers(K, rows, MB, planes, ws, ws_bytes);
+  if (!t.mn || t.tf32) fail(HSF_ERR_UNSUPPORTED, "swapped path-sum needs MN-major bf16 operands");
+  t.bk = true;
+  t.bn = (int)((2 * MB + 31) / 32 * 32);
   return t;
 }
 
@@ -1574,12 +1628,16 @@ inline void tc_gemm3m(const Tc3Buffers& t, float2* out, long long MB, long long 
 }
 
 // K4 for half B — may run on its own stream
+// (swapped path-sum: leavesB are half A's leaves, columns col0.. of rows of
+// length MS, with c_p; MN-major layout only)
 inline void tc_prep_b(const TcBuffers& t, const float2* leavesB, long long K, long long MB,
-                      const tc::TailParams& tp, const float2* ttab, cudaStream_t st) {
-  if (t.mn) {
+                      const tc::TailParams& tp, const float2* ttab, cudaStream_t st, const float2* cp = nullptr,
+                      long long col0 = 0, long long MS = 0) {
+  if (t.mn && !t.bk) {
     const long long ldb = t.d.nrows_b_pad;
     tc::split_b_mn_kernel<<<dim3((unsigned)((ldb / 8 + 255) / 256), (unsigned)t.d.Kpad), 256, 0, st>>>(
-        leavesB, (__nv_bfloat16*)t.b_hi, (__nv_bfloat16*)t.b_lo, K, ldb, MB, tp, ttab, (__nv_bfloat16*)t.b_l2);
+        leavesB, (__nv_bfloat16*)t.b_hi, (__nv_bfloat16*)t.b_lo, K, ldb, MB, tp, ttab, (__nv_bfloat16*)t.b_l2, cp,
+        col0, MS ? MS : MB);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("split_b_mn: ") + cudaGetErrorString(e));
     return;
@@ -1587,10 +1645,10 @@ inline void tc_prep_b(const TcBuffers& t, const float2* leavesB, long long K, lo
   const dim3 gb((unsigned)(t.d.nrows_b_pad / 64), (unsigned)(t.d.Kpad / 32));
   if (t.tf32)
     tc::split_b_kernel<float2><<<gb, dim3(32, 8), 0, st>>>(leavesB, (float2*)t.b_hi, (float2*)t.b_lo, K, t.d.Kpad, MB,
-                                                           tp, ttab, nullptr);
+                                                           tp, ttab, nullptr, cp, col0, MS ? MS : MB);
   else
     tc::split_b_kernel<__nv_bfloat162><<<gb, dim3(32, 8), 0, st>>>(leavesB, t.b_hi, t.b_lo, K, t.d.Kpad, MB, tp, ttab,
-                                                                   t.b_l2);
+                                                                   t.b_l2, cp, col0, MS ? MS : MB);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("split_b: ") + cudaGetErrorString(e));
 }
@@ -1618,12 +1676,16 @@ inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row
   // MN-major B: [2K][2MB] valid of [kcols][nrows_b_pad] storage, 64 x BK
   // boxes; the padding rows / columns are read as zeros (TMA OOB fill), so
   // producers need not write them (operand-store passes do not)
-  CUtensorMap mBh = t.mn ? make_map(t.b_hi, 2 * t.K, 2 * MB, tc::BK, t.d.nrows_b_pad)
+  const bool bk = t.mn && t.bk;  // K-major B of the swapped path-sum, {BK, bn/2} boxes
+  if (bk && (t.bn % 32 || t.bn > tc::BN || 2 * MB > t.bn)) fail(HSF_ERR_INVALID_ARG, "narrow tile too small");
+  CUtensorMap mBh = bk ? make_map(t.b_hi, t.d.nrows_b_pad, kcols, t.bn / 2)
+                  : t.mn ? make_map(t.b_hi, 2 * t.K, 2 * MB, tc::BK, t.d.nrows_b_pad)
                            : make_map(t.b_hi, t.d.nrows_b_pad, kcols, tc::BN, 0, tf);
   CUtensorMap mAl = !x3 ? mAh
                    : t.mn ? make_map(a_lo_mn, 2 * t.K, rows, tc::BK, t.d.rows_pad)
                           : make_map(ka(t.a_lo), rpad, kcols, tc::BM, 0, tf);
   CUtensorMap mBl = !x3 ? mBh
+                   : bk ? make_map(t.b_lo, t.d.nrows_b_pad, kcols, t.bn / 2)
                    : t.mn ? make_map(t.b_lo, 2 * t.K, 2 * MB, tc::BK, t.d.nrows_b_pad)
                             : make_map(t.b_lo, t.d.nrows_b_pad, kcols, tc::BN, 0, tf);
   // bf16x6 third planes (pair kernel only)
@@ -1631,12 +1693,15 @@ inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row
   if (x6) {
     mA2 = t.mn ? make_map((__nv_bfloat16*)t.a_l2 + row0, 2 * t.K, rows, tc::BK, t.d.rows_pad)
                : make_map(t.a_l2 + row0 * t.d.Kpad, rpad, kcols, tc::BM);
-    mB2 = t.mn ? make_map(t.b_l2, 2 * t.K, 2 * MB, tc::BK, t.d.nrows_b_pad)
+    mB2 = bk ? make_map(t.b_l2, t.d.nrows_b_pad, kcols, t.bn / 2)
+        : t.mn ? make_map(t.b_l2, 2 * t.K, 2 * MB, tc::BK, t.d.nrows_b_pad)
                : make_map(t.b_l2, t.d.nrows_b_pad, kcols, tc::BN / 2);
   }
   tc::Params p;
   p.num_m = (int)(rpad / tc::BM);
-  p.num_n = (int)(t.d.nrows_b_pad / tc::BN);
+  p.bk = bk ? 1 : 0;
+  p.bn = bk ? t.bn : tc::BN;
+  p.num_n = bk ? (int)((2 * MB + t.bn - 1) / t.bn) : (int)(t.d.nrows_b_pad / tc::BN);
   p.num_k = (int)(kcols / (tf ? tc::BK / 2 : tc::BK));
   p.x3 = x3 ? 1 : 0;
   p.x6 = x6 ? 1 : 0;
@@ -1680,7 +1745,7 @@ inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row
   CUtensorMap mO = n_shards > 0 ? om.m[0] : make_out_map((float*)out, rows, 2 * MB);
   const char* pair_env = std::getenv("HSF_TC_PAIR");
   // (bf16x6: the pair kernel only -- three planes do not fit two single-CTA stages)
-  const bool pair = x6 || tf || n_shards > 0 || (rows > tc::BM && !(pair_env && pair_env[0] == '0'));
+  const bool pair = bk || x6 || tf || n_shards > 0 || (rows > tc::BM && !(pair_env && pair_env[0] == '0'));
   if (pair) {
     // CTA pairs: 256-row M tiles, each CTA loads half of every B tile
     static bool attr2 = false;

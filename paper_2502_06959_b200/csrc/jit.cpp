@@ -313,10 +313,11 @@ struct Gen {
   bool swap_grid = false;  // transposed-store variant: grid x = node, y = tile
 
   // store_mode: 0 leaf (node-major), 1 MN-major split-bf16 B operand,
+  // 3 MN-major split-bf16 A operand of the swapped path-sum (st_aop),
   // 2 transposed leaf: element G of node k to dst[G * ldw + k] (x c_p[k] when
   // dst_lo carries c_p) -- the bitstring gather operand, no transpose pass
   std::string build(const std::string& name, int threads, int cluster_bits, int store_mode = 0) {
-    const bool operand_store = store_mode == 1;
+    const bool operand_store = store_mode == 1 || store_mode == 3;
     swap_grid = store_mode == 2;
     nt = threads;
     cb = whole ? 0 : cluster_bits;
@@ -343,8 +344,8 @@ struct Gen {
     o << "  __syncthreads();\n";
     if (operand_store) {
       o << "#pragma unroll 4\n";
-      o << "  for (u32 e = 2u * threadIdx.x; e < LNEL; e += 2u * NT) st_bop(a, a.node_local0 + NODE_ID, "
-           "G((RANK << LB) | e), s[sw(e)], s[sw(e + 1)]);\n";
+      o << "  for (u32 e = 2u * threadIdx.x; e < LNEL; e += 2u * NT) " << (store_mode == 3 ? "st_aop" : "st_bop")
+        << "(a, a.node_local0 + NODE_ID, G((RANK << LB) | e), s[sw(e)], s[sw(e + 1)]);\n";
     } else if (swap_grid) {
       o << "  { const long long kcol = a.node_local0 + NODE_ID;\n";
       o << "    C cpv = czero<C>(); cpv.x = 1;\n";

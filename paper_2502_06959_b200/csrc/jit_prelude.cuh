@@ -93,6 +93,22 @@ __device__ __forceinline__ void st_bop(const JitArgs& a, long long k, u32 g, flo
   }
 }
 __device__ __forceinline__ void st_bop(const JitArgs&, long long, u32, double2, double2) {}
+// swapped path-sum: rows 2k (Re) and 2k+1 (Im) of the MN-major split-bf16 M
+// operand (tc_swap_buffers' A''), amplitudes G and G+1 as one bf16 pair per
+// row; a.ldw = the row length in 4 B words
+__device__ __forceinline__ void st_aop(const JitArgs& a, long long k, u32 g, float2 x, float2 y) {
+  u32* hi = reinterpret_cast<u32*>(a.dst);
+  const long long o0 = 2 * k * a.ldw + (g >> 1), o1 = o0 + a.ldw;
+  const u32 hr = bf2(x.x, y.x), hm = bf2(x.y, y.y);
+  hi[o0] = hr;
+  hi[o1] = hm;
+  if (a.dst_lo) {
+    u32* lo = reinterpret_cast<u32*>(a.dst_lo);
+    lo[o0] = bf2(x.x - bf_lo(hr), y.x - bf_hi(hr));
+    lo[o1] = bf2(x.y - bf_lo(hm), y.y - bf_hi(hm));
+  }
+}
+__device__ __forceinline__ void st_aop(const JitArgs&, long long, u32, double2, double2) {}
 
 // 1-qubit gate on register slot J of 16 amplitudes held by one thread
 template <int J, typename C>

@@ -43,6 +43,8 @@ struct DeviceState {
   // operand directly (full-output tensor-core runs; K4 fused into the leaf pass)
   void* jit_bop = nullptr;
   int jit_bop_nt = 256;
+  void* jit_aop = nullptr;  // the same pass writing the swapped path-sum's M operand
+
   // bitstring runs: the last pass of each half writing the transposed,
   // c_p-folded gather operand [2^m][K] directly (no transpose kernel);
   // [variant 0 full / 1 fold][half]
@@ -234,8 +236,12 @@ static DeviceState* ensure_device(Plan* P, int device) {
     const bool bop = c64 && !d->jit_cb[0][1].empty() && d->jit_cb[0][1].back() == 0;
     if (bop) {
       d->jit_bop_nt = d->jit_nt[0][1].back();
-      src.push_back(jit_pass_source(HB, HB.trans.back().passes.back(), c64, d->jit_bop_nt, 0, &P->coef, true));
+      src.push_back(jit_pass_source(HB, HB.trans.back().passes.back(), c64, d->jit_bop_nt, 0, &P->coef, 1));
       owner.push_back({-1, 1});
+      if (P->n_low >= 8) {
+        src.push_back(jit_pass_source(HB, HB.trans.back().passes.back(), c64, d->jit_bop_nt, 0, &P->coef, 3));
+        owner.push_back({-1, 3});
+      }
     }
     // transposed-store variants of each half's last pass (bitstring runs);
     // opt-in (HSF_TRANSPOSED_STORE=1): its scattered 8 B stores measured slower
@@ -255,7 +261,7 @@ static DeviceState* ensure_device(Plan* P, int device) {
     std::vector<void*> fns = jit_compile_all(device, src);
     for (size_t i = 0; i < fns.size(); ++i) {
       if (owner[i].first == -1)
-        d->jit_bop = fns[i];
+        (owner[i].second == 3 ? d->jit_aop : d->jit_bop) = fns[i];
       else if (owner[i].first <= -2)
         d->jit_tr[(-2 - owner[i].first) / 2][(-2 - owner[i].first) % 2] = fns[i];
       else
@@ -290,6 +296,10 @@ struct Layout {
   const Half* half[2] = {nullptr, nullptr};
   bool bop = false;            // half B's last pass writes the MN-major GEMM operand (with a JIT kernel)
   bool g3m = false;            // full-output path-sum by the 3M (Gauss) kernel (tc_gemm3m_kernel)
+  bool swap = false;           // few output rows: GEMM with the roles swapped (half B's 2^nB rows as M,
+                               // half A's rows as N with the complex rotation), then a transpose
+  size_t off_swapT = 0;        // its [2^nB][swap_cols] complex64 output
+  bool aop = false;            // swapped: M operand stored by half B's last pass (jit_aop)
   bool bits_mode;
   uint64_t r0, r1;
   hsf_precision prec;
@@ -319,6 +329,10 @@ static uint64_t nodes_at(const std::vector<int32_t>& ranks, int L, uint64_t p0, 
   uint64_t S = suffix_prod(ranks, L);
   return (p1 - 1) / S - p0 / S + 1;
 }
+
+// swapped path-sum: GEMM columns = the run's output rows, padded to even (16 B
+// rows of the fp32 [2^nB][2 * cols] GEMM output)
+static long long swap_cols(const Layout& L) { return (long long)((L.r1 - L.r0 + 1) & ~1ull); }
 
 static Layout make_layout(const Plan& P, const hsf_run_args& a, size_t elem) {
   Layout L{};
@@ -366,8 +380,26 @@ static Layout make_layout(const Plan& P, const hsf_run_args& a, size_t elem) {
   }
   L.g3m = !L.bits_mode && L.prec == HSF_PREC_BF16X3 && P.opts.dtype == HSF_C64 && a.n_out_shards == 0 &&
           !a.accumulate && tc_use_3m((long long)L.K);
-  L.bop = !L.bits_mode && !L.g3m && (L.prec == HSF_PREC_BF16X3 || L.prec == HSF_PREC_BF16X1) &&
+  {
+    // swapped path-sum for prefix outputs (<= 128 rows of A): half B's leaves
+    // become the un-rotated (re, im planes) MN-major M operand, stored by B's
+    // last pass, and the few A rows the rotated K-major N operand of one
+    // narrow pair tile (tc_swap_buffers).  The big operand is half the bytes
+    // of the rotated one and streams once instead of 16x-padded M tiles
+    // re-reading it (q33-3 9.40 -> 7.09 ms); HSF_TC_SWAP=0 / 1 forces off / on
+    const uint64_t nr = (a.row_end > a.row_begin ? a.row_end - a.row_begin : 1ull << (P.n - P.n_low));
+    const char* sw = std::getenv("HSF_TC_SWAP");
+    const bool want = sw ? sw[0] == '1' : true;
+    L.swap = want && nr <= 128 && !L.bits_mode && !L.g3m && P.opts.dtype == HSF_C64 && L.prec != HSF_PREC_SIMT &&
+             L.prec != HSF_PREC_TF32X3 && a.n_out_shards == 0 && !P.permuted && tc_mn((long long)L.K) &&
+             P.n_low >= 8;
+  }
+  L.bop = !L.bits_mode && !L.g3m && !L.swap && (L.prec == HSF_PREC_BF16X3 || L.prec == HSF_PREC_BF16X1) &&
           P.opts.dtype == HSF_C64 && L.var[1] == 0 && tc_mn((long long)L.K);
+  // the swapped path-sum's M operand written by half B's last pass (HSF_TC_AOP=0 disables)
+  const char* aop_env = std::getenv("HSF_TC_AOP");
+  L.aop = L.swap && (L.prec == HSF_PREC_BF16X3 || L.prec == HSF_PREC_BF16X1) && L.var[1] == 0 &&
+          !(aop_env && aop_env[0] == '0');
   if (!L.bits_mode && a.bitstrings) fail(HSF_ERR_INVALID_ARG, "bitstrings given with n_bitstrings == 0");
   if (L.bits_mode && !a.bitstrings) fail(HSF_ERR_INVALID_ARG, "n_bitstrings > 0 but bitstrings is NULL");
   if (L.bits_mode && P.n > 63) fail(HSF_ERR_INVALID_ARG, "bitstring runs need n <= 63");
@@ -428,10 +460,15 @@ static Layout make_layout(const Plan& P, const hsf_run_args& a, size_t elem) {
       off = align_up(off + ((size_t)1 << P.n) * elem);
     }
     if (L.prec != HSF_PREC_SIMT) {
-      L.tc_bytes = L.g3m ? tc3_workspace_bytes((long long)L.K, (long long)(L.r1 - L.r0), 1ll << nB)
-                         : tc_workspace_bytes((long long)L.K, (long long)(L.r1 - L.r0), 1ll << nB, tc_planes(L.prec));
+      L.tc_bytes = L.g3m    ? tc3_workspace_bytes((long long)L.K, (long long)(L.r1 - L.r0), 1ll << nB)
+                   : L.swap ? tc_workspace_bytes((long long)L.K, 1ll << nB, swap_cols(L), tc_planes(L.prec))
+                            : tc_workspace_bytes((long long)L.K, (long long)(L.r1 - L.r0), 1ll << nB, tc_planes(L.prec));
       L.off_tc = off;
       off = align_up(off + L.tc_bytes);
+      if (L.swap) {
+        L.off_swapT = off;
+        off = align_up(off + ((size_t)swap_cols(L) << nB) * elem);
+      }
     }
     if (!a.out_on_device && a.n_out_shards == 0) {
       // host output: rows are produced in chunks of <= kHostChunkBytes into two
@@ -441,7 +478,7 @@ static Layout make_layout(const Plan& P, const hsf_run_args& a, size_t elem) {
       size_t chunk = kHostChunkBytes;
       if (const char* e = std::getenv("HSF_HOST_CHUNK_BYTES")) chunk = std::max<size_t>(1, std::strtoull(e, nullptr, 10));
       uint64_t cr = std::max<uint64_t>(1, chunk / row_bytes);
-      if (L.prec != HSF_PREC_SIMT) cr = std::max<uint64_t>(128, cr / 128 * 128);  // whole tensor-core M tiles
+      if (L.prec != HSF_PREC_SIMT && !L.swap) cr = std::max<uint64_t>(128, cr / 128 * 128);  // whole tensor-core M tiles
       L.chunk_rows = std::min<uint64_t>(cr, L.r1 - L.r0);
       L.chunk_bytes = align_up(L.chunk_rows * row_bytes);
       L.off_out = off;
@@ -610,12 +647,20 @@ static void run_half(const Plan& P, DeviceState* d, int h, const Layout& L, cuda
           pp.src_div = 1;
         }
         const bool bop = h == 1 && L.bop && d->jit_bop && last && pi + 1 == tr.passes.size();
+        const bool aop = h == 1 && L.aop && d->jit_aop && last && pi + 1 == tr.passes.size();
         const bool trs = L.bits_mode && var <= 1 && d->jit_tr[var][h] && last && pi + 1 == tr.passes.size();
         if (trs) {  // K4t fused: write the transposed (c_p-folded for A) gather operand
           JitLaunchArgs ja{pp.src, ws + L.off_T[h], pp.coef, pp.node_first, pp.node_local0, pp.src_first, pp.src_div,
                            pp.tile0, h == 0 ? d->cp : nullptr, (long long)L.K};
           jit_launch(d->jit_tr[var][h], (unsigned)ny, (unsigned)tiles, (unsigned)d->jit_tr_nt[var][h],
                      jit_smem_bytes(ps, sizeof(R) == 4, 0), st, ja, 0);
+        } else if (aop) {  // swapped path-sum: write the MN-major M operand instead of the leaves
+          TcBuffers t = tc_swap_buffers((long long)L.K, 1ll << H.m, swap_cols(L), tc_planes(L.prec), ws + L.off_tc,
+                                        L.tc_bytes);
+          JitLaunchArgs ja{pp.src, t.a_hi, pp.coef, pp.node_first, pp.node_local0, pp.src_first, pp.src_div, pp.tile0,
+                           t.b_lo == nullptr ? nullptr : t.a_lo, t.d.rows_pad / 2};
+          jit_launch(d->jit_aop, (unsigned)tiles, (unsigned)ny, (unsigned)d->jit_bop_nt, jit_smem_bytes(ps, true, 0), st,
+                     ja, 0);
         } else if (bop) {  // K4 fused: write the MN-major split-bf16 B operand instead of the leaves
           TcBuffers t = tc_buffers((long long)L.K, (long long)(L.r1 - L.r0), 1ll << H.m, tc_planes(L.prec),
                                    ws + L.off_tc, L.tc_bytes);
@@ -674,6 +719,14 @@ static void prep_half(Plan* P, DeviceState* d, const Layout& L, int h, cudaStrea
       const Tc3Buffers t3 = tc3_buffers(K, (long long)(L.r1 - L.r0), 1ll << nB, ws + L.off_tc, L.tc_bytes);
       tc3_prep(t3, h == 0, (const float2*)leaves, (const float2*)d->cp, 1ll << m, h == 0 ? (long long)L.r0 : 0,
                h == 0 ? (long long)(L.r1 - L.r0) : (1ll << m), tp, (const float2*)d->tail, st);
+    } else if (L.swap) {  // roles swapped: B's leaves -> M operand, A's rows (rotated, c_p) -> N operand
+      TcBuffers t = tc_swap_buffers(K, 1ll << nB, swap_cols(L), tc_planes(L.prec), ws + L.off_tc, L.tc_bytes);
+      if (h == 1) {
+        if (!(L.aop && d->jit_aop))  // else written by half B's last pass
+          tc_prep_a(t, (const float2*)leaves, nullptr, K, 1ll << m, 0, 1ll << m, tp, (const float2*)d->tail, st);
+      } else
+        tc_prep_b(t, (const float2*)leaves, K, (long long)(L.r1 - L.r0), tp, (const float2*)d->tail, st,
+                  (const float2*)d->cp, (long long)L.r0, 1ll << m);
     } else if (h == 0) {
       TcBuffers t = tc_buffers(K, (long long)(L.r1 - L.r0), 1ll << nB, tc_planes(L.prec), ws + L.off_tc, L.tc_bytes);
       tc_prep_a(t, (const float2*)leaves, (const float2*)d->cp, K, 1ll << m, (long long)L.r0, (long long)(L.r1 - L.r0),
@@ -797,6 +850,17 @@ static void run_core_full(Plan* P, DeviceState* d, const Layout& L, cudaStream_t
                 1ll << nB, (long long)lo, (long long)nrows, st);
       return;
     }
+    if (L.swap) {  // outT[j][i] over all 2^nB columns and the run's rows, then out[i][j]
+      // (host-output chunks: the GEMM runs with the first chunk, each chunk transposes its rows)
+      const long long Rw = swap_cols(L), MBl = 1ll << nB;
+      float2* outT = (float2*)(ws + L.off_swapT);
+      if (lo == 0)
+        tc_gemm(tc_swap_buffers(K, MBl, Rw, tc_planes(L.prec), ws + L.off_tc, L.tc_bytes), outT, Rw, 0, MBl, st);
+      swap_transpose_kernel<<<dim3((unsigned)((MBl + 31) / 32), (unsigned)((nrows + 31) / 32)), dim3(32, 8), 0, st>>>(
+          outT + lo, (float2*)out, (long long)nrows, MBl, Rw, accumulate ? 1 : 0);
+      CK(cudaGetLastError());
+      return;
+    }
     TcBuffers t = tc_buffers(K, (long long)(L.r1 - L.r0), 1ll << nB, tc_planes(L.prec), ws + L.off_tc,
                              L.tc_bytes);
     if (shards && shards->n_out_shards > 0)
@@ -911,7 +975,7 @@ static void run(Plan* P, const hsf_run_args& a) {
                                    L.p0, L.p1, L.r0, L.r1, (uint64_t)L.prec, (uint64_t)a.accumulate,
                                    (uint64_t)timed, (uint64_t)L.fold, (uint64_t)(uintptr_t)d->ws,
                                    (uint64_t)(uintptr_t)d->cp, (uint64_t)L.total, (uint64_t)a.n_out_shards,
-                                   a.shard_rows};
+                                   a.shard_rows, (uint64_t)L.swap, (uint64_t)L.g3m, (uint64_t)L.bop};
       for (int o = 0; o < a.n_out_shards; ++o) key.push_back((uint64_t)(uintptr_t)a.out_shards[o]);
       if (!d->gexec || key != d->gkey) {
         if (d->gexec) CK(cudaGraphExecDestroy(d->gexec));

@@ -312,6 +312,33 @@ __global__ void gather_grouped_c64_kernel(const float4* __restrict__ AT, const f
   }
 }
 
+// Swapped path-sum (prefix outputs): the GEMM wrote outT[j][i] (j < MB
+// columns of half B, i < rows of half A); out[i][j] = outT[j][i] (+= out).
+// 32 x 32 tiles through SMEM, coalesced on both sides.
+__global__ void swap_transpose_kernel(const float2* __restrict__ outT, float2* __restrict__ out, long long rows,
+                                      long long MB, long long ldT, int accumulate) {
+  __shared__ float2 t[32][33];
+  const long long j0 = (long long)blockIdx.x * 32, i0 = (long long)blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int r = ty; r < 32; r += 8) {
+    const long long j = j0 + r, i = i0 + tx;
+    t[r][tx] = (j < MB && i < rows) ? outT[j * ldT + i] : make_float2(0.f, 0.f);
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const long long i = i0 + r, j = j0 + tx;
+    if (i < rows && j < MB) {
+      float2 v = t[tx][r];
+      if (accumulate) {
+        const float2 o = out[i * MB + j];
+        v.x += o.x;
+        v.y += o.y;
+      }
+      out[i * MB + j] = v;
+    }
+  }
+}
+
 // ------------------------------------------------------------------ K5s
 // out[(i - row0) * MB + j] = sum_p c_p A[p][i] B[p][j]  for i in [row0, row0+rows)
 // A: [K][MA] node-major leaves, B: [K][MB].  64x64 output tile per CTA,

@@ -914,3 +914,45 @@ def test_cluster_tier_optin(torch, monkeypatch):
     ref = O.recombine_bits(A, B, c, bits, inst.n_low)
     got, _ = gpu_bits(torch, inst, bits, path_range=(0, 16))
     check(got, ref, "c64")
+
+
+@pytest.mark.parametrize("name", ["c2", "c4", "c5"])
+@pytest.mark.parametrize("precision", ["bf16x3", "bf16x1", "bf16x6"])
+@pytest.mark.parametrize("aop", ["1", "0"])
+def test_swapped_prefix_path_sum(torch, name, precision, aop, monkeypatch):
+    # few output rows: the GEMM with the roles swapped (half B's leaves as the
+    # MN-major M operand -- stored by half B's last pass, or split from the
+    # leaves -- half A's rows rotated and times c_p as a narrow K-major N
+    # operand) and a transpose; forced on for every row range (odd counts
+    # included), ragged path ranges, host output chunks
+    monkeypatch.setenv("HSF_TC_SWAP", "1")
+    monkeypatch.setenv("HSF_TC_AOP", aop)
+    inst = make_config(name, twin=True, n_bits=0) if name == "c5" else make_config(name, twin=True)
+    n, g = O.parse_circuit(inst.text)
+    P = O.plan(n, g, inst.n_low, inst.blocks)
+    rows = 1 << (n - inst.n_low)
+    tol = dict(TOL, c64=TOL["c64"] * (30 if precision == "bf16x1" else 1))
+    rel = dict(REL, c64=REL["c64"] * (300 if precision == "bf16x1" else 1))
+    for pr, rr in [(None, (0, 16)), ((1, P.n_paths - 1), (3, 40)), (None, (rows - 5, rows)), (None, (0, min(128, rows))), (None, None)]:
+        p0, p1 = pr or (0, P.n_paths)
+        A, B, c = O.half_states(P, p0, p1)
+        ref = O.recombine_full(A, B, c)
+        if rr:
+            ref = ref[rr[0] << inst.n_low:rr[1] << inst.n_low]
+        got, _ = gpu_full(torch, inst, precision=precision, path_range=pr, row_range=rr)
+        d = np.abs(got - ref)
+        assert d.max() <= tol["c64"] and np.linalg.norm(got - ref) / np.linalg.norm(ref) <= rel["c64"], (pr, rr, d.max())
+    # host output in chunks of 2 rows, and accumulate into a device buffer
+    from paper_2502_06959_b200 import Plan
+    monkeypatch.setenv("HSF_HOST_CHUNK_BYTES", str(2 << inst.n_low << 3))
+    Pg = Plan(inst.text, inst.n_low, inst.blocks)
+    A, B, c = O.half_states(P)
+    ref = O.recombine_full(A, B, c)[:11 << inst.n_low]
+    host = np.zeros(11 << inst.n_low, dtype=np.complex64)
+    Pg.run(host, row_range=(0, 11), precision=precision)
+    assert np.abs(host - ref).max() <= tol["c64"]
+    out = torch.zeros(11 << inst.n_low, dtype=torch.complex64, device="cuda")
+    Pg.run(out, row_range=(0, 11), precision=precision, path_range=(0, P.n_paths // 2))
+    Pg.run(out, row_range=(0, 11), precision=precision, path_range=(P.n_paths // 2, P.n_paths), accumulate=True)
+    torch.cuda.synchronize()
+    assert np.abs(out.cpu().numpy() - ref).max() <= tol["c64"]
