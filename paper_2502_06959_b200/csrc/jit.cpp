@@ -153,7 +153,7 @@ struct Gen {
         if (std::find(ps.T.begin(), ps.T.end(), q) == ps.T.end()) nonT.push_back(q);
       std::vector<int> from(nonT.size()), to = nonT;
       for (size_t j = 0; j < nonT.size(); ++j) from[j] = (int)j;
-      o << "  const u32 tile = (TILE_ID >> CB) + a.tile0;\n";
+      o << "  const u32 tile = restricted_tile(TILE_ID >> CB, a.tile0, a.tile_free);\n";
       o << "  const u32 base = " << gather_expr("tile", from, to) << ";\n";
       std::vector<int> pf, pt;
       for (int i = 0; i < t; ++i) {

@@ -18,6 +18,7 @@ struct JitLaunchArgs {
   unsigned tile0;
   void* dst_lo = nullptr;
   long long ldw = 0;
+  unsigned tile_free = 0xFFFFFFFFu;  // see PassParams::tile_free
 };
 
 // CUDA source of the kernel "hsf_jit_pass" specialised to one tile pass.

@@ -22,7 +22,14 @@ struct JitArgs {
   unsigned tile0;        // tile index of blockIdx.x == 0 (row-restricted leaf passes)
   void* dst_lo;          // operand-store passes: lo plane of the split-bf16 B operand (nullptr => hi only)
   long long ldw;         //   and its row stride in 32-bit words (bf16 pairs)
+  unsigned tile_free;    // ~0u: tile = tile0 + blockIdx; else deposit(blockIdx into its set bits) | tile0
 };
+__device__ __forceinline__ u32 restricted_tile(u32 id, u32 tile0, u32 free_mask) {
+  if (free_mask == 0xFFFFFFFFu) return id + tile0;
+  u32 t = tile0;
+  for (u32 m = free_mask; m; m &= m - 1, id >>= 1) t |= (id & 1u) ? (m & (0u - m)) : 0u;
+  return t;
+}
 
 __device__ __forceinline__ int sw(int e) { return e ^ ((e >> 4) & 15); }
 

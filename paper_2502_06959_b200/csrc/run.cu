@@ -574,6 +574,36 @@ static void run_half(const Plan& P, DeviceState* d, int h, const Layout& L, cuda
   int prev_level = -1;
   size_t pass_ord = 0;
   const std::vector<void*>* jf = d->jit ? &d->jit_fn[var][h] : nullptr;
+  // Row light cone (full-output runs of half A over a row range): the rows'
+  // constant index bits F (values those of r0) are all the path-sum reads.
+  // A pass computes an output element from input elements with the same
+  // non-tile bits (its ops stay inside its tile), so pass k needs only the
+  // tiles whose non-tile bits in N_k agree with r0, N_last = F and
+  // N_{k-1} = N_k minus pass k's tile qubits: need[k] = N_k.  (q33-3, 16
+  // rows: the leaf level's first pass computes 4 of 32 tiles per node.)
+  std::vector<uint32_t> need;
+  const bool cone = h == 0 && !L.bits_mode && (L.r1 - L.r0) < (1ull << H.m);
+  if (cone) {
+    size_t np = 0;
+    for (const Transition& tr : H.trans) np += tr.passes.size();
+    need.assign(np, 0);
+    const uint64_t diff = L.r0 ^ (L.r1 - 1);
+    int hb = 0;
+    while (hb < 64 && (diff >> hb) != 0) ++hb;
+    uint32_t N = (uint32_t)(((1ull << H.m) - 1) & ~((1ull << hb) - 1));
+    size_t k = np;
+    for (size_t ti = H.trans.size(); ti-- > 0;)
+      for (size_t pi = H.trans[ti].passes.size(); pi-- > 0;) {
+        need[--k] = N;
+        const Pass& ps = H.trans[ti].passes[pi];
+        uint32_t tm = 0;
+        if (ps.t < H.m)
+          for (int q : ps.T) tm |= 1u << q;
+        else
+          tm = ~0u;
+        N &= ~tm;
+      }
+  }
   for (size_t ti = 0; ti < H.trans.size(); ++ti) {
     const Transition& tr = H.trans[ti];
     const bool last = (ti + 1 == H.trans.size());
@@ -606,6 +636,22 @@ static void run_half(const Plan& P, DeviceState* d, int h, const Layout& L, cuda
       pp.tbl_elems = (int)ps.tbl_elems;
       uint64_t tiles = 1ull << (H.m - ps.t);
       pp.tile0 = 0;
+      pp.tile_free = 0xFFFFFFFFu;
+      if (cone && ps.t < H.m && need[pass_ord] && !(last && pi + 1 == tr.passes.size())) {
+        uint32_t t0 = 0, fm = 0;
+        for (int j = 0; j < pp.n_nt; ++j) {
+          const int q = pp.nonT[j];
+          if ((need[pass_ord] >> q) & 1u)
+            t0 |= (uint32_t)((L.r0 >> q) & 1ull) << j;
+          else
+            fm |= 1u << j;
+        }
+        if (fm != (1u << pp.n_nt) - 1) {
+          pp.tile0 = t0;
+          pp.tile_free = fm;
+          tiles = 1ull << __builtin_popcount(fm);
+        }
+      }
       // Row-restricted leaf pass: in full-output runs only rows [r0, r1) of
       // half A's leaves reach the path-sum, so the last pass of A's tree
       // computes only the tiles holding them (ops of a pass stay inside its
@@ -671,6 +717,7 @@ static void run_half(const Plan& P, DeviceState* d, int h, const Layout& L, cuda
         } else if (jf) {
           JitLaunchArgs ja{pp.src, pp.dst, pp.coef, pp.node_first, pp.node_local0, pp.src_first, pp.src_div,
                            pp.tile0};
+          ja.tile_free = pp.tile_free;
           const int cb = d->jit_cb[var][h][pass_ord];
           jit_launch((*jf)[pass_ord], (unsigned)tiles, (unsigned)ny, (unsigned)d->jit_nt[var][h][pass_ord],
                      jit_smem_bytes(ps, sizeof(R) == 4, cb), st, ja, cb);

@@ -105,7 +105,17 @@ struct PassParams {
   long long src_first;     // global index of the first node of the input level
   long long src_div;       // parent = node_global / src_div
   int tbl_elems;           // SMEM diagonal-table area (complex elements)
+  unsigned tile_free;      // ~0u: tiles tile0 + blockIdx.x; else tile = deposit(blockIdx.x into
+                           // the set bits of tile_free) | tile0 (row light-cone of earlier passes)
 };
+
+// the blockIdx.x-th tile of a row-restricted pass (see tile_free)
+__device__ __forceinline__ uint32_t restricted_tile(uint32_t id, uint32_t tile0, uint32_t free_mask) {
+  if (free_mask == 0xFFFFFFFFu) return id + tile0;
+  uint32_t t = tile0;
+  for (uint32_t m = free_mask; m; m &= m - 1, id >>= 1) t |= (id & 1u) ? (m & (0u - m)) : 0u;
+  return t;
+}
 
 template <int K, typename C>
 __device__ __forceinline__ void apply_dense_k(C* s, int t, const DevOp& op, const C* __restrict__ M) {
@@ -347,7 +357,7 @@ __global__ void __launch_bounds__(NT, (NT == 256 ? (HEAVY ? 2 : 4) : 1)) hsf_pas
   off = (off + 15) & ~(size_t)15;
   C* stab = reinterpret_cast<C*>(smem_raw + off);  // staged diagonal tables
 
-  const uint32_t tile = blockIdx.x + p.tile0;
+  const uint32_t tile = restricted_tile(blockIdx.x, p.tile0, p.tile_free);
   const long long node_local = p.node_local0 + blockIdx.y;
   const long long node_g = p.node_first + blockIdx.y;
   const int nel = 1 << p.t;

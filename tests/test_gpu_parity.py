@@ -748,13 +748,15 @@ def test_table2_q30_prefix_full_paths(torch):
     assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 5e-4
 
 
-@pytest.mark.parametrize("rr", [(0, 3), (5, 37), (64, 65)])
-def test_row_restricted_leaf_pass(torch, rr):
+@pytest.mark.parametrize("rr", [(0, 3), (5, 37), (64, 65), (4096, 4100), (8190, 8192)])
+@pytest.mark.parametrize("jit", [True, False])
+def test_row_restricted_leaf_pass(torch, rr, jit):
     # tiled half A (2^14, 2^11 tiles): a row range computes only the leaf
-    # tiles holding those rows; the rows must equal the full run's rows
+    # tiles holding those rows, and every earlier pass only the tiles in the
+    # rows' light cone (tile_free); the rows must equal the full run's rows
     inst = make_config("c4", twin=True, n=28, n_low=14)
-    full, P = gpu_full(torch, inst, precision="simt", tile_qubits=11)
-    part, _ = gpu_full(torch, inst, precision="simt", tile_qubits=11, row_range=rr)
+    full, P = gpu_full(torch, inst, precision="simt", tile_qubits=11, jit=jit)
+    part, _ = gpu_full(torch, inst, precision="simt", tile_qubits=11, row_range=rr, jit=jit)
     nb = P.n_b
     assert np.array_equal(part, full[rr[0] << nb:rr[1] << nb])
 
