@@ -430,7 +430,29 @@ def main():
     eff_prec = ("bf16x3" if inst.dtype == "c64" else "simt") if prec == "auto" else prec
     MA, MB = (rows if full else 1 << (inst.n - inst.n_low)), 1 << inst.n_low
     clk_mhz = peaks.get("clocks_under_load", {}).get("sm_mhz_median", 1305.0)
-    if full and eff_prec in ("bf16x3", "bf16x1", "bf16x6", "tf32x3"):
+    # swapped path-sum (run.cu make_layout: <= 128 output rows, bf16 modes,
+    # K > 64, n_low >= 8): GEMM M = 2^n_low (half B's leaves, MN-major), one
+    # narrow N tile of the rows, then a transpose -- the M operand streams once
+    Kp = (K + 31) // 32 * 32
+    swap = (full and eff_prec in ("bf16x3", "bf16x1", "bf16x6") and MA <= 128 and inst.n_low >= 8
+            and 2 * Kp > 128 and inst.dtype == "c64" and os.environ.get("HSF_TC_SWAP", "") != "0")
+    if swap:
+        nprod, planes = {"bf16x6": (6, 3), "bf16x3": (3, 2), "bf16x1": (1, 1)}[eff_prec]
+        Rp = (MA + 1) // 2 * 2
+        bn = (2 * Rp + 31) // 32 * 32
+        tflop = nprod * 2.0 * MB * bn * (2 * K)  # executed (narrow tile incl. padding)
+        obytes = planes * 2.0 * (2 * K) * (MB + bn) + MB * 2 * Rp * 4 + MA * MB * esz * 2
+        t_tensor, t_hbm = tflop / (bf16 * 1e12), obytes / (hbm * 1e9)
+        ach = obytes / (core_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                "kernel": "tc_gemm2_kernel narrow-N swapped path-sum (tcgen05 bf16, split x%d) + transpose" % nprod,
+                "traffic": None, "flops_per_launch": tflop, "bytes_per_launch": obytes,
+                "tensor_time_fraction": t_tensor / (core_ms * 1e-3),
+                "useful_complex_flops": 8.0 * MA * MB * K, "kernel_ms": core_ms,
+                "note": "algorithmic bytes = M operand planes (half B's leaves, 2K x 2^n_low bf16 each) read "
+                        "once + the fp32 [2^n_low][2 rows] GEMM output written + the transposed output"}
+    elif full and eff_prec in ("bf16x3", "bf16x1", "bf16x6", "tf32x3"):
         # executed tensor-core flops: (6 | 3 | 1) real GEMMs of rows x 2MB x 2K;
         # algorithmic bytes: the fp32 output written once (+ bf16 operand planes)
         nprod, planes = {"bf16x6": (6, 3), "bf16x3": (3, 2), "bf16x1": (1, 1), "tf32x3": (3, 4)}[eff_prec]
@@ -496,7 +518,9 @@ def main():
                 "peak": hbm, "unit": "GB/s", "frac": sim_ach / hbm, "traffic": None, "kernel_ms": sim_ms,
                 "bytes": sim_bytes, "frac_of_l2_read": sim_ach / L2_READ_GBS, "l2_read_peak_gbs": L2_READ_GBS,
                 "note": "algorithmic bytes = every pass reads + writes each output node state once; small "
-                        "states stay L2/SMEM-resident, so frac can exceed 1"}
+                        "states stay L2/SMEM-resident, so frac can exceed 1" +
+                        ("; row-range runs compute only the rows' light cone of half A (run.cu run_half), "
+                         "so these bytes are an upper bound" if full and MA < (1 << (inst.n - inst.n_low)) else "")}
     if sim_ms > core_ms:
         roof, roof_other = roof_sim, roof
     else:
@@ -522,6 +546,8 @@ def main():
         sim_launches = sum(P.tail_passes[h] if halves_var[h] else P.passes[h] for h in (0, 1))
     fused_b = tc_full and not halves_var[1] and K > 64
     n_launch = sim_launches + (1 if (full and eff_prec == "simt") else (2 if fused_b else 3))
+    if swap:  # split of A's rows (N operand) + GEMM + transpose (+ split of B's leaves unless fused)
+        n_launch = sim_launches + (3 if (not halves_var[1] and eff_prec != "bf16x6") else 4)
     if not full:  # grouped gather (run.cu make_layout): + count, scan, scatter kernels
         Kt = K // (int(np.prod(P.ranks[len(P.ranks) - P.fold_units:])) if P.fold_units else 1)
         if inst.dtype == "c64" and Kt % 64 == 0 and Kt <= 512 and N_out >= 8 * (1 << P.n_a):

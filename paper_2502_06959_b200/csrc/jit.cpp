@@ -22,6 +22,7 @@
 #include <map>
 #include <mutex>
 #include <sstream>
+#include <cstdlib>
 #include <string>
 #include <thread>
 #include <vector>
@@ -323,7 +324,15 @@ struct Gen {
     cb = whole ? 0 : cluster_bits;
     bool heavy = false;
     for (auto& d : ops) heavy = heavy || d.kind == OP_RPASS || (d.kind == OP_DENSE && d.k > 2);
-    header(name, nt > 256 ? 1 : (heavy ? 2 : 3));
+    // __launch_bounds__ min CTAs per SM (256 threads): 4 for heavy passes
+    // (register passes, dense k > 2; <= 64 registers) -- measured against 2 / 3
+    // / 5: q33-3 6.19 / 5.67 / 5.32 / 5.43 ms, q32-1 1.85 / 1.69 / 1.54 / 1.58,
+    // c5 4.10 / 3.95 / 3.88 / 4.02 (latency-bound at 25 % occupancy with 86
+    // registers); light passes insensitive 3 .. 5
+    int heavy_minb = 4, light_minb = 3;
+    if (const char* e = std::getenv("HSF_JIT_HEAVY_MINB")) heavy_minb = std::atoi(e);
+    if (const char* e = std::getenv("HSF_JIT_LIGHT_MINB")) light_minb = std::atoi(e);
+    header(name, nt > 256 ? 1 : (heavy ? heavy_minb : light_minb));
     size_t i = 0;
     while (i < ops.size()) {
       const DevOp& d = ops[i];

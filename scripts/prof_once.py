@@ -20,6 +20,8 @@ cdt = torch.complex64 if inst.dtype == "c64" else torch.complex128
 rr = None
 if inst.bitstrings is None:
     rows = (1 << P.n_a) // row_div
+    if "prefix" in (inst.meta or {}):  # Table II shapes: the first `prefix` amplitudes
+        rows = -(-inst.meta["prefix"] // (1 << inst.n_low))
     rr = (0, rows)
     out = torch.empty(rows << P.n_b, dtype=cdt, device="cuda")
     bits = None
