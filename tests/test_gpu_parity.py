@@ -916,6 +916,12 @@ def test_cluster_tier_optin(torch, monkeypatch):
     ref = O.recombine_bits(A, B, c, bits, inst.n_low)
     got, _ = gpu_bits(torch, inst, bits, path_range=(0, 16))
     check(got, ref, "c64")
+    # full output over a few rows: the row light cone restricts the clustered
+    # passes' tiles too
+    for rr in [(0, 4), (9, 13)]:
+        reff = O.recombine_full(A[rr[0]:rr[1]], B, c)
+        got, _ = gpu_full(torch, inst, precision="simt", path_range=(0, 16), row_range=rr)
+        check(got, reff, "c64")
 
 
 @pytest.mark.parametrize("name", ["c2", "c4", "c5"])
