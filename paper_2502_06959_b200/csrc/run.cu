@@ -1014,15 +1014,29 @@ static void run(Plan* P, const hsf_run_args& a) {
   const bool timed = a.phase_ms != nullptr;
   try {
     const char* ng = std::getenv("HSF_NO_GRAPH");
-    const bool graph = P->opts.graphs && (a.out_on_device || a.n_out_shards > 0) && (!L.bits_mode || a.bits_on_device) &&
-                       !(ng && ng[0] == '1');
+    // page-locked host buffers of a bitstring run (H2D of the samples, D2H of
+    // the amplitudes) are captured as graph memcpy nodes too; pageable ones
+    // are not capturable, those runs launch directly
+    auto pinned = [](const void* ptr) {
+      if (!ptr) return false;
+      cudaPointerAttributes at{};
+      if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return false;
+      }
+      return at.type == cudaMemoryTypeHost;
+    };
+    const bool out_ok = a.out_on_device || a.n_out_shards > 0 || (L.bits_mode && pinned(a.out));
+    const bool bits_ok = !L.bits_mode || a.bits_on_device || pinned(a.bitstrings);
+    const bool graph = P->opts.graphs && out_ok && bits_ok && !(ng && ng[0] == '1');
     if (graph) {
       // the key holds everything the captured launches depend on
       std::vector<uint64_t> key = {(uint64_t)(uintptr_t)a.out, (uint64_t)(uintptr_t)a.bitstrings, a.n_bitstrings,
                                    L.p0, L.p1, L.r0, L.r1, (uint64_t)L.prec, (uint64_t)a.accumulate,
                                    (uint64_t)timed, (uint64_t)L.fold, (uint64_t)(uintptr_t)d->ws,
                                    (uint64_t)(uintptr_t)d->cp, (uint64_t)L.total, (uint64_t)a.n_out_shards,
-                                   a.shard_rows, (uint64_t)L.swap, (uint64_t)L.g3m, (uint64_t)L.bop};
+                                   a.shard_rows, (uint64_t)L.swap, (uint64_t)L.g3m, (uint64_t)L.bop,
+                                   (uint64_t)a.out_on_device, (uint64_t)a.bits_on_device};
       for (int o = 0; o < a.n_out_shards; ++o) key.push_back((uint64_t)(uintptr_t)a.out_shards[o]);
       if (!d->gexec || key != d->gkey) {
         if (d->gexec) CK(cudaGraphExecDestroy(d->gexec));

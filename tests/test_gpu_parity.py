@@ -785,6 +785,32 @@ def test_graph_replay_matches_direct(torch, name):
     assert all(np.array_equal(outs[0], o) for o in outs[1:])
 
 
+@pytest.mark.parametrize("name", ["c3", "c5"])
+def test_graph_pinned_host_bitstrings(torch, name):
+    # page-locked host bitstrings and output: the run (H2D, trees, gather,
+    # D2H) is captured and replayed; each replay reads the host samples' current
+    # contents and writes the host output, equal to the device-buffer run
+    from paper_2502_06959_b200 import Plan
+    inst = make_config(name, twin=True)
+    P = Plan(inst.text, inst.n_low, inst.blocks, dtype=inst.dtype)
+    nb = len(inst.bitstrings)
+    hb = torch.from_numpy(inst.bitstrings.view(np.int64).copy()).pin_memory()
+    ho = torch.empty(nb, dtype=torch.complex64).pin_memory()
+    rng = np.random.default_rng(5)
+    for it in range(3):
+        if it:
+            hb.copy_(torch.from_numpy(rng.permutation(inst.bitstrings).view(np.int64)))
+        ho.zero_()
+        P.run(ho, bitstrings=hb)
+        dev = torch.empty(nb, dtype=torch.complex64, device="cuda")
+        P.run(dev, bitstrings=hb.cuda())
+        torch.cuda.synchronize()
+        assert np.array_equal(ho.numpy(), dev.cpu().numpy())
+    n, g = O.parse_circuit(inst.text)
+    ref = O.schrodinger(n, g)[hb.numpy().view(np.uint64).astype(np.int64)]
+    check(ho.numpy(), ref, "c64")
+
+
 # ------------------------------------------------------------- edge cases
 def test_minimal_two_qubit_bell_across_cut(torch):
     # n = 2, cut between the qubits: the Bell circuit of the paper's Example 1
