@@ -556,7 +556,7 @@ def main():
         n_launch = sim_launches + (3 if (not halves_var[1] and eff_prec != "bf16x6") else 4)
     if not full:  # grouped gather (run.cu make_layout): + count, scan, scatter kernels
         Kt = K // (int(np.prod(P.ranks[len(P.ranks) - P.fold_units:])) if P.fold_units else 1)
-        if inst.dtype == "c64" and Kt % 64 == 0 and Kt <= 512 and N_out >= 8 * (1 << P.n_a):
+        if inst.dtype == "c64" and Kt % 64 == 0 and Kt <= 512 and N_out >= 4 * (1 << P.n_a):
             n_launch += 3
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "paths/s", "n_gpus": world, "steps": a.steps,

@@ -441,11 +441,13 @@ static Layout make_layout(const Plan& P, const hsf_run_args& a, size_t elem) {
       L.off_pbits = off;
       off = align_up(off + a.n_bitstrings * 8);
     }
-    // grouped gather: >= 8 samples per A row on average, K a multiple of 64 up
+    // grouped gather: >= 4 samples per A row on average, K a multiple of 64 up
     // to 512 (the row lives in registers), complex64, rows and samples < 2^31
+    // (c5, 4 per row: gather 1.65 -> 1.41 ms, step 3.87 -> 3.74 ms with the
+    // sort beside the trees; c3, 32 per row: 0.35 -> 0.23 ms)
     const long long nrowsA = 1ll << nA;
     const char* gg = std::getenv("HSF_GROUPED_GATHER");
-    const bool want = gg ? gg[0] == '1' : (long long)a.n_bitstrings >= 8 * nrowsA;
+    const bool want = gg ? gg[0] == '1' : (long long)a.n_bitstrings >= 4 * nrowsA;
     L.grouped = want && P.opts.dtype == HSF_C64 && L.K % 64 == 0 && L.K <= 512 && nA <= 30 &&
                 a.n_bitstrings < (1ull << 31);
     if (L.grouped) {
