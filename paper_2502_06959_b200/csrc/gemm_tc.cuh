@@ -513,7 +513,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * EW, 1)
   const uint32_t tmem_base = tmem_base_sh;
   // stage layout: npl A plane slots, then npl B plane slots (hi, lo[, lo2])
   const int npl = p.x6 ? 3 : 2;
-  const uint32_t SS = (uint32_t)npl * (A_TILE + B2_TILE);
+  // (narrow K-major B: a bn/2-row slot per plane, so more stages fit)
+  const uint32_t BSL = p.bk ? (((uint32_t)(p.bn / 2) * 128u + 1023u) & ~1023u) : (uint32_t)B2_TILE;
+  const uint32_t SS = (uint32_t)npl * (A_TILE + BSL);
   const uint32_t stage_bytes = (uint32_t)(p.x6 ? 3 : p.x3 ? 2 : 1) * (A_TILE + (p.bk ? (p.bn / 2) * 128 : B2_TILE));
 
   if (warp == 0) {
@@ -540,8 +542,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * EW, 1)
             }
             if (p.bk) {  // K-major B: one {BK, bn/2} box per plane
               tma_load_2sm(sb, &mB_hi, &full_bar[s], kb * BK, brow, b_pol);
-              if (p.x3) tma_load_2sm(sb + B2_TILE, &mB_lo, &full_bar[s], kb * BK, brow, b_pol);
-              if (p.x6) tma_load_2sm(sb + 2 * B2_TILE, &mB_l2, &full_bar[s], kb * BK, brow, b_pol);
+              if (p.x3) tma_load_2sm(sb + BSL, &mB_lo, &full_bar[s], kb * BK, brow, b_pol);
+              if (p.x6) tma_load_2sm(sb + 2 * BSL, &mB_l2, &full_bar[s], kb * BK, brow, b_pol);
             } else {
               for (int j = 0; j < BN / 128; ++j) {
                 tma_load_2sm(sb + j * 8192, &mB_hi, &full_bar[s], brow + j * 64, kb * BK, b_pol);
@@ -581,7 +583,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * EW, 1)
           asm volatile("tcgen05.fence::after_thread_sync;");
           const uint32_t st = smem_u32(smem + s * SS);
           const uint32_t a_hi = st, a_lo = st + A_TILE, a_l2 = st + 2 * A_TILE;
-          const uint32_t b_hi = st + npl * A_TILE, b_lo = b_hi + B2_TILE, b_l2 = b_hi + 2 * B2_TILE;
+          const uint32_t b_hi = st + npl * A_TILE, b_lo = b_hi + BSL, b_l2 = b_hi + 2 * BSL;
           if (p.mn && p.bk) {  // A MN-major (k step 16 rows = 2 KB), B K-major (k step 32 B), N = bn
             const uint32_t id = (IDESC2 & ~(0x3Fu << 17)) | ((uint32_t)(p.bn >> 3) << 17) | (1u << 15);
 #pragma unroll
@@ -1772,7 +1774,32 @@ inline void tc_gemm(const TcBuffers& t, float2* out, long long MB, long long row
     p.num_m = (int)((rows + 2 * tc::BM - 1) / (2 * tc::BM));
     const long long tiles = (long long)p.num_m * p.num_n;
     const int grid = 2 * (int)std::min<long long>(tiles, num_sms() / 2);
-    if (tf && p.num_k <= 2)
+    if (bk) {  // narrow B slots: as many stages of the M operand in flight as fit (5 for bn <= 128 at x3)
+      const int bsl = (t.bn / 2 * 128 + 1023) / 1024 * 1024, npl = x6 ? 3 : 2;
+      // (227 KB opt-in limit less the kernel's static barriers)
+      const int budget = 232448 - 1024 - tc::EPI_WARPS * 4096 - 1024;
+      const int fit = budget / (npl * (tc::A_TILE + bsl));
+      const int nst = fit >= 5 ? 5 : fit >= 3 ? 3 : 2;
+      const int smem = nst * npl * (tc::A_TILE + bsl) + tc::EPI_WARPS * 4096 + 1024;
+      static int attr5 = 0, attr3 = 0, attr2n = 0;
+      int& cur = nst == 5 ? attr5 : nst == 3 ? attr3 : attr2n;
+      if (smem > cur) {
+        e = cudaFuncSetAttribute(nst == 5 ? (const void*)tc::tc_gemm2_kernel<5, 1>
+                                 : nst == 3 ? (const void*)tc::tc_gemm2_kernel<3, 1>
+                                            : (const void*)tc::tc_gemm2_kernel<2, 1>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("tc2 narrow smem attr: ") + cudaGetErrorString(e));
+        cur = smem;
+      }
+      const CUtensorMap& a2 = x6 ? mA2 : mAh;
+      const CUtensorMap& b2 = x6 ? mB2 : mBh2;
+      if (nst == 5)
+        tc::tc_gemm2_kernel<5, 1><<<grid, tc::THREADS, smem, st>>>(mAh, mAl, mBh2, mBl2, a2, b2, mO, p, om);
+      else if (nst == 3)
+        tc::tc_gemm2_kernel<3, 1><<<grid, tc::THREADS, smem, st>>>(mAh, mAl, mBh2, mBl2, a2, b2, mO, p, om);
+      else
+        tc::tc_gemm2_kernel<2, 1><<<grid, tc::THREADS, smem, st>>>(mAh, mAl, mBh2, mBl2, a2, b2, mO, p, om);
+    } else if (tf && p.num_k <= 2)
       tc::tc_gemm2_kernel<2, 2, true><<<grid, tc::THREADS, tc::smem2_bytes(2, 2), st>>>(mAh, mAl, mBh2, mBl2, mAh, mBh2,
                                                                                         mO, p, om);
     else if (tf)
