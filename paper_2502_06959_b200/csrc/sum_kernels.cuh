@@ -40,6 +40,57 @@ __global__ void transpose_fold_kernel(const C* __restrict__ in, C* __restrict__ 
   }
 }
 
+// complex64 K4t with 16 B accesses: a 32 (k) x 64 (m) tile per CTA, loads of
+// two consecutive m per thread (512 B per warp row), stores of two
+// consecutive k per thread (256 B per output row). SMEM [m][16 slots][2]:
+// the (k, k+1) pair of row m sits in slot (k / 2) ^ ((m / 2) & 15), so both
+// the load-side 8 B writes and the store-side 16 B reads run at the minimum
+// wavefront count.
+__global__ void transpose_fold_c64_kernel(const float2* __restrict__ in, float2* __restrict__ out,
+                                          const float2* __restrict__ cp, long long K, long long M) {
+  __shared__ __align__(16) float2 S[64][32];
+  const long long m0 = (long long)blockIdx.x * 64, k0 = (long long)blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = ty + 8 * i;  // k offset
+    const long long k = k0 + r, m = m0 + 2 * tx;
+    float2 v0 = make_float2(0.f, 0.f), v1 = v0;
+    if (k < K) {
+      if (m + 1 < M) {
+        const float4 a = *reinterpret_cast<const float4*>(in + k * M + m);
+        v0 = make_float2(a.x, a.y);
+        v1 = make_float2(a.z, a.w);
+      } else if (m < M) {
+        v0 = in[k * M + m];
+      }
+      if (cp) {
+        const float2 c = cp[k];
+        v0 = cmul(v0, c);
+        v1 = cmul(v1, c);
+      }
+    }
+    const int slot = (r >> 1) ^ (tx & 15);  // rows 2tx, 2tx+1: (m / 2) & 15 = tx & 15
+    S[2 * tx][2 * slot + (r & 1)] = v0;
+    S[2 * tx + 1][2 * slot + (r & 1)] = v1;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int mr = 16 * i + 2 * ty + (tx >> 4), kp = tx & 15;
+    const long long m = m0 + mr, k = k0 + 2 * kp;
+    const float4 v = *reinterpret_cast<const float4*>(&S[mr][2 * (kp ^ ((mr >> 1) & 15))]);
+    if (m < M) {
+      if (k + 1 < K && (K & 1) == 0)
+        *reinterpret_cast<float4*>(out + m * K + k) = v;
+      else {
+        if (k < K) out[m * K + k] = make_float2(v.x, v.y);
+        if (k + 1 < K) out[m * K + k + 1] = make_float2(v.z, v.w);
+      }
+    }
+  }
+}
+
 // --------------------------------------------- qubit relabelling (partitions)
 // caller index <-> internal index for a non-contiguous partition: bit q of the
 // caller's index is bit relabel[q] of the internal one.  tab[16*k .. ] holds,
