@@ -316,10 +316,22 @@ __global__ void gather_grouped_c64_kernel(const float4* __restrict__ AT, const f
     float4 a[T];
 #pragma unroll
     for (int t = 0; t < T; ++t) a[t] = __ldg(&AT[r * K2 + lane + 32 * t]);
-    for (int j = beg; j < end; j += 2) {
-      const bool two = j + 1 < end;
-      const int i0 = perm[j], i1 = two ? perm[j + 1] : i0;
-      const unsigned long long b0 = bits[i0], b1 = bits[i1];
+    // the row's sample indices and bitstrings, up to 32 at a time, loaded by
+    // the lanes in parallel and broadcast (no dependent perm -> bits -> B
+    // chain per sample pair)
+    for (int jb = beg; jb < end; jb += 32) {
+    const int nb = end - jb < 32 ? end - jb : 32;
+    int pl = 0;
+    unsigned long long bl = 0;
+    if (lane < nb) {
+      pl = perm[jb + lane];
+      bl = bits[pl];
+    }
+    for (int jj = 0; jj < nb; jj += 2) {
+      const bool two = jj + 1 < nb;
+      const int i0 = __shfl_sync(0xffffffffu, pl, jj), i1 = __shfl_sync(0xffffffffu, pl, two ? jj + 1 : jj);
+      const unsigned long long b0 = __shfl_sync(0xffffffffu, bl, jj);
+      const unsigned long long b1 = __shfl_sync(0xffffffffu, bl, two ? jj + 1 : jj);
       const float4* q0 = BT + (long long)(b0 & maskB) * K2;
       const float4* q1 = BT + (long long)(b1 & maskB) * K2;
       float4 y0[T], y1[T];
@@ -359,6 +371,7 @@ __global__ void gather_grouped_c64_kernel(const float4* __restrict__ AT, const f
         }
         out[idx] = res;
       }
+    }
     }
   }
 }
