@@ -327,44 +327,54 @@ __global__ void gather_grouped_c64_kernel(const float4* __restrict__ AT, const f
       pl = perm[jb + lane];
       bl = bits[pl];
     }
-    for (int jj = 0; jj < nb; jj += 2) {
-      const bool two = jj + 1 < nb;
-      const int i0 = __shfl_sync(0xffffffffu, pl, jj), i1 = __shfl_sync(0xffffffffu, pl, two ? jj + 1 : jj);
-      const unsigned long long b0 = __shfl_sync(0xffffffffu, bl, jj);
-      const unsigned long long b1 = __shfl_sync(0xffffffffu, bl, two ? jj + 1 : jj);
-      const float4* q0 = BT + (long long)(b0 & maskB) * K2;
-      const float4* q1 = BT + (long long)(b1 & maskB) * K2;
-      float4 y0[T], y1[T];
+    // 4 samples per step: 4 B rows in flight per warp
+    for (int jj = 0; jj < nb; jj += 4) {
+      int ii[4];
+      unsigned long long bb[4];
+      float4 y[4][T];
 #pragma unroll
-      for (int t = 0; t < T; ++t) {
-        y0[t] = __ldg(&q0[lane + 32 * t]);
-        y1[t] = __ldg(&q1[lane + 32 * t]);
-      }
-      float re0 = 0.f, im0 = 0.f, re1 = 0.f, im1 = 0.f;
+      for (int u = 0; u < 4; ++u) {
+        const int src = jj + u < nb ? jj + u : jj;  // warp-uniform
+        ii[u] = __shfl_sync(0xffffffffu, pl, src);
+        bb[u] = __shfl_sync(0xffffffffu, bl, src);
+        const float4* q = BT + (long long)(bb[u] & maskB) * K2;
 #pragma unroll
-      for (int t = 0; t < T; ++t) {
-        const float4 x = a[t];
-        re0 = fmaf(x.x, y0[t].x, fmaf(-x.y, y0[t].y, re0));
-        im0 = fmaf(x.x, y0[t].y, fmaf(x.y, y0[t].x, im0));
-        re0 = fmaf(x.z, y0[t].z, fmaf(-x.w, y0[t].w, re0));
-        im0 = fmaf(x.z, y0[t].w, fmaf(x.w, y0[t].z, im0));
-        re1 = fmaf(x.x, y1[t].x, fmaf(-x.y, y1[t].y, re1));
-        im1 = fmaf(x.x, y1[t].y, fmaf(x.y, y1[t].x, im1));
-        re1 = fmaf(x.z, y1[t].z, fmaf(-x.w, y1[t].w, re1));
-        im1 = fmaf(x.z, y1[t].w, fmaf(x.w, y1[t].z, im1));
+        for (int t = 0; t < T; ++t) y[u][t] = __ldg(&q[lane + 32 * t]);
+      }
+      float re[4], im[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        re[u] = 0.f;
+        im[u] = 0.f;
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+          const float4 x = a[t];
+          re[u] = fmaf(x.x, y[u][t].x, fmaf(-x.y, y[u][t].y, re[u]));
+          im[u] = fmaf(x.x, y[u][t].y, fmaf(x.y, y[u][t].x, im[u]));
+          re[u] = fmaf(x.z, y[u][t].z, fmaf(-x.w, y[u][t].w, re[u]));
+          im[u] = fmaf(x.z, y[u][t].w, fmaf(x.w, y[u][t].z, im[u]));
+        }
       }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        re0 += __shfl_xor_sync(0xffffffffu, re0, o);
-        im0 += __shfl_xor_sync(0xffffffffu, im0, o);
-        re1 += __shfl_xor_sync(0xffffffffu, re1, o);
-        im1 += __shfl_xor_sync(0xffffffffu, im1, o);
-      }
-      if (lane < (two ? 2 : 1)) {  // lane 0 writes sample j, lane 1 sample j+1
-        const int idx = lane ? i1 : i0;
-        const unsigned long long bb = lane ? b1 : b0;
-        const float2 v = lane ? make_float2(re1, im1) : make_float2(re0, im0);
-        float2 res = tw.n ? cmul(v, trail_weight(tw, trail, bb)) : v;
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          re[u] += __shfl_xor_sync(0xffffffffu, re[u], o);
+          im[u] += __shfl_xor_sync(0xffffffffu, im[u], o);
+        }
+      const int nv = nb - jj < 4 ? nb - jj : 4;
+      if (lane < nv) {  // lane u writes sample jj + u
+        int idx = ii[0];
+        unsigned long long bs = bb[0];
+        float2 v = make_float2(re[0], im[0]);
+#pragma unroll
+        for (int u = 1; u < 4; ++u)
+          if (lane == u) {
+            idx = ii[u];
+            bs = bb[u];
+            v = make_float2(re[u], im[u]);
+          }
+        float2 res = tw.n ? cmul(v, trail_weight(tw, trail, bs)) : v;
         if (accumulate) {
           res.x += out[idx].x;
           res.y += out[idx].y;
