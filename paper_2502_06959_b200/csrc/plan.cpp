@@ -723,7 +723,7 @@ static std::vector<DevOp> regpass_rewrite(const std::vector<DevOp>& ops, int t) 
 // on a narrow level becomes several kernels of smaller code, each an L2
 // round trip of a few MB -- c3's root passes (127 ops, instruction-fetch
 // bound) at 40: 0.578 -> 0.542-0.553 ms (32 / 40 / 48 / 64 / 80 / 128:
-// 0.54 / 0.55 / 0.55 / 0.56 / 0.57 / 0.58); c2, c5, q32-1 unchanged.
+// 0.54 / 0.55 / 0.55 / 0.56 / 0.57 / 0.58); c5, q32-1 unchanged. Tiled passes only.
 // HSF_MAX_PASS_OPS=n overrides (n >= 128: no split below kMaxPassOps).
 static size_t max_pass_ops() {
   static const size_t v = [] {
@@ -750,7 +750,11 @@ static void finalize_half(Half& H, size_t elem_bytes) {
         size_t n = 0;
         while (i < rw.size()) {
           size_t w = (rw[i].kind == OP_RPASS) ? (size_t)rw[i].k + 1 : 1;
-          if (n + w > max_pass_ops() && n > 0) break;
+          // (tiled passes only: splitting a whole-state K1 pass costs a
+          // relaunch and an SMEM reload of the state -- c2's half A 0.903 vs
+          // 0.907 ms)
+          const size_t cap = p.t < H.m ? max_pass_ops() : (size_t)kMaxPassOps;
+          if (n + w > cap && n > 0) break;
           for (size_t j = 0; j < w; ++j) out.push_back(rw[i + j]);
           n += w;
           i += w;
