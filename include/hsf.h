@@ -190,9 +190,10 @@ typedef struct {
   int32_t bits_on_device;       /* 1 => device pointer, 0 => host pointer */
   void* out;                    /* caller-owned, plan dtype */
   int32_t out_on_device;        /* 1 => device pointer, 0 => host pointer: full-mode
-                                   rows are computed in chunks of <= 32 MiB into two
-                                   device staging buffers and copied back while the
-                                   next chunk is computed (bounded device memory);
+                                   rows are computed in chunks of <= 16 MiB (env
+                                   HSF_HOST_CHUNK_BYTES overrides) into two device
+                                   staging buffers and copied back while the next
+                                   chunk is computed (bounded device memory);
                                    pinned host memory gives overlapped copies */
   uint64_t path_begin, path_end;/* paths evaluated [begin,end); 0,0 => all.  The
                                    result is the partial sum over this range. */
@@ -249,7 +250,7 @@ size_t hsf_last_error(char* buf, size_t len);
  * `variant` (0 = full tree, 1 = bitstring trailing-diagonal fold, 2 = the
  * half-sided trailing fold of full-output runs; + 4·cb for the cluster tier
  * with 2^cb CTAs per tile; + 16·s for the store variant s: 1 = split-bf16 B
- * operand, 2 = transposed gather operand).  Copies at most
+ * operand, 3 = the swapped path-sum's M operand).  Copies at most
  * len-1 bytes + NUL into buf (may be NULL) and returns the full length; 0 if
  * the pass does not exist.  Host only. */
 size_t hsf_debug_pass_source(const hsf_plan_t* plan, int32_t variant, int32_t half, int32_t pass, char* buf,

@@ -733,226 +733,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * EW, 1)
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
 }
 
-// --------------------------------------------- K5g: 3M (Gauss) complex GEMM
-// The complex contraction D = A'B^T (A' = c_p A) with three real
-// products instead of four (the 4-real-GEMM form above):
-//   T1 = Ar Br^T, T2 = Ai Bi^T, T3 = (Ar + Ai)(Br + Bi)^T,
-//   Re D = T1 - T2,  Im D = T3 - T1 - T2,
-// each real product split bf16 hi/lo with 3 MMAs (x3).  25 % fewer MMA flops
-// for 1.125x the operand bytes per path (6 planes per side instead of the
-// duplicated (re, im) / (-im, re) B rows).  CTA pair, M = 256 (each CTA its
-// 128 A rows), N = 128 complex columns (each CTA half of them); the three
-// fp32 accumulators (3 x 128 TMEM columns) are single-buffered, the epilogue
-// combining them into interleaved complex64.  MN-major operands, stages of 32
-// paths (k rows); the 6 planes of a side are one 3-D TMA box {64, 32, 6}
-// (3 TMA ops per stage: two 64-row A boxes, one 64-column B box).
-constexpr int N3 = 128;              // complex output columns per pair tile
-constexpr int BK3 = 16;              // paths per stage (3 TMA ops of 12 KB each per CTA)
-constexpr int NST3 = 5;              // deep pipeline: the operand stream is latency-bound
-constexpr int P3 = 64 * BK3 * 2;     // 4 KB: one plane of one 64-wide MN box
-constexpr int BOX3 = 6 * P3;         // 24 KB: a 3-D box (6 planes)
-constexpr int STAGE3_BYTES = 3 * BOX3;  // 72 KB: A m-boxes 0, 1 and the B box
-constexpr int EBUF3 = 1;
-constexpr int SMEM3_BYTES = NST3 * STAGE3_BYTES + EBUF3 * EPI_WARPS * 4096 + 1024;
-constexpr uint32_t IDESC3 = (1u << 4) | (1u << 7) | (1u << 10) | kMajorMN | ((uint32_t)(N3 >> 3) << 17) |
-                            ((uint32_t)((2 * BM) >> 4) << 24);
-
-struct Maps3 {
-  CUtensorMap a;  // 3-D {rows, K, 6 planes: Ar hi, Ar lo, Ai hi, Ai lo, As hi, As lo}, MN-major
-  CUtensorMap b;  // 3-D {MB, K, 6 planes: Br, Bi, Bs hi/lo}
-};
-__device__ __forceinline__ void tma_load_3d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
-                                                uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
-      "[%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(smem_u32(bar) & kPeerMask), "r"(c0), "r"(c1), "r"(0), "l"(policy)
-      : "memory");
-}
-
-// MN-major SW128 descriptor with a given stride between 64-wide MN atoms
-__device__ __forceinline__ uint64_t sw128_desc_mn_lbo(uint32_t saddr, uint32_t lbo) {
-  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(lbo >> 4) << 16) | ((uint64_t)(1024 >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
-}
-__device__ __forceinline__ void mma3(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(IDESC3), "r"(accum));
-}
-
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
-    tc_gemm3m_kernel(const __grid_constant__ Maps3 mp, const __grid_constant__ CUtensorMap mOut, const Params p) {
-  extern __shared__ uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t full_bar[NST3], empty_bar[NST3], tfull_bar, tempty_bar;
-  __shared__ uint32_t tmem_base_sh;
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  const int num_tiles = p.num_m * p.num_n;
-  const uint32_t rank = cluster_rank();
-  const int cl = blockIdx.x >> 1, num_cl = gridDim.x >> 1;  // CTA pairs
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < NST3; ++s) {
-      mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
-    }
-    mbar_init(&tfull_bar, 1);
-    mbar_init(&tempty_bar, 2 * 32 * EPI_WARPS);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  cluster_sync_all();
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  const uint32_t tmem_base = tmem_base_sh;
-
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer (both CTAs)
-    if (lane == 0) {
-      const uint64_t a_pol = p.a_evict_last ? policy_evict_last() : policy_evict_normal();
-      const uint64_t b_pol = policy_evict_normal();
-      int s = 0;
-      uint32_t ph = 0;
-      for (int tile = cl; tile < num_tiles; tile += num_cl) {
-        int mb, nb;
-        tile_coords(p, tile, mb, nb);
-        const int arow = (2 * mb + (int)rank) * BM, bcol = nb * N3 + (int)rank * (N3 / 2);
-        for (int kb = 0; kb < p.num_k; ++kb) {
-          mbar_wait(&empty_bar[s], ph ^ 1);
-          uint8_t* st = smem + s * STAGE3_BYTES;
-          if (rank == 0) mbar_expect_tx(&full_bar[s], 2 * STAGE3_BYTES);
-          tma_load_3d_2sm(st, &mp.a, &full_bar[s], arow, kb * BK3, a_pol);
-          tma_load_3d_2sm(st + BOX3, &mp.a, &full_bar[s], arow + 64, kb * BK3, a_pol);
-          tma_load_3d_2sm(st + 2 * BOX3, &mp.b, &full_bar[s], bcol, kb * BK3, b_pol);
-          if (++s == NST3) {
-            s = 0;
-            ph ^= 1;
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer (leader only)
-    if (lane == 0 && rank == 0) {
-      int s = 0;
-      uint32_t ph = 0, aph = 0;
-      for (int tile = cl; tile < num_tiles; tile += num_cl) {
-        mbar_wait(&tempty_bar, aph ^ 1);  // the epilogue has read the previous tile's accumulators
-        aph ^= 1;
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t t1 = tmem_base, t2 = tmem_base + N3, t3 = tmem_base + 2 * N3;
-        for (int kb = 0; kb < p.num_k; ++kb) {
-          mbar_wait(&full_bar[s], ph);
-          asm volatile("tcgen05.fence::after_thread_sync;");
-          const uint32_t st = smem_u32(smem + s * STAGE3_BYTES);
-#pragma unroll
-          for (int k = 0; k < BK3 / 16; ++k) {  // 16 k rows = 2 KB into each plane
-            auto ad = [&](int q) { return sw128_desc_mn_lbo(st + q * P3 + k * 2048, BOX3); };
-            auto bd = [&](int q) { return sw128_desc_mn_lbo(st + 2 * BOX3 + q * P3 + k * 2048, BOX3); };
-            const uint32_t acc = (kb | k) ? 1u : 0u;
-            // T1 = Ar Br, T2 = Ai Bi, T3 = As Bs; each hi*hi + hi*lo + lo*hi
-            mma3(t1, ad(0), bd(0), acc);
-            mma3(t1, ad(0), bd(1), 1u);
-            mma3(t1, ad(1), bd(0), 1u);
-            mma3(t2, ad(2), bd(2), acc);
-            mma3(t2, ad(2), bd(3), 1u);
-            mma3(t2, ad(3), bd(2), 1u);
-            mma3(t3, ad(4), bd(4), acc);
-            mma3(t3, ad(4), bd(5), 1u);
-            mma3(t3, ad(5), bd(4), 1u);
-          }
-          mma2_commit_both(&empty_bar[s]);
-          if (++s == NST3) {
-            s = 0;
-            ph ^= 1;
-          }
-        }
-        mma2_commit_both(&tfull_bar);
-      }
-    }
-  } else {
-    // ------------------------------------------------------------ epilogue (both CTAs)
-    // warp: lane quarter q (rows 32q..), half h (complex columns 64h..64h+63),
-    // 4 sub-chunks of 16 complex = one 32 x 32 fp32 box of interleaved output
-    const uint64_t st_pol = policy_evict_first();
-    const int q = warp & 3;
-    const int half = (warp - 2) / 4;
-    uint8_t* stg0 = smem + NST3 * STAGE3_BYTES + (warp - 2) * 4096 * EBUF3;
-    int buf = 0;
-    uint32_t aph = 0;
-    for (int tile = cl; tile < num_tiles; tile += num_cl) {
-      int mb, nb;
-      tile_coords(p, tile, mb, nb);
-      const int row0 = (2 * mb + (int)rank) * BM;
-      mbar_wait(&tfull_bar, aph);
-      aph ^= 1;
-      asm volatile("tcgen05.fence::after_thread_sync;");
-#pragma unroll 1
-      for (int sc = 0; sc < 4; ++sc) {
-        const int c0 = 64 * half + 16 * sc;  // first complex column of this sub-chunk
-        uint32_t v1[16], v2[16], v3[16];
-        const uint32_t lanes = (uint32_t)(q * 32) << 16;
-#define HSF_LD16(dst, col)                                                                                      \
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, " \
-               "[%16];"                                                                                         \
-               : "=r"(dst[0]), "=r"(dst[1]), "=r"(dst[2]), "=r"(dst[3]), "=r"(dst[4]), "=r"(dst[5]), "=r"(dst[6]),  \
-                 "=r"(dst[7]), "=r"(dst[8]), "=r"(dst[9]), "=r"(dst[10]), "=r"(dst[11]), "=r"(dst[12]),           \
-                 "=r"(dst[13]), "=r"(dst[14]), "=r"(dst[15])                                                     \
-               : "r"(col))
-        HSF_LD16(v1, tmem_base + (uint32_t)c0 + lanes);
-        HSF_LD16(v2, tmem_base + (uint32_t)(N3 + c0) + lanes);
-        HSF_LD16(v3, tmem_base + (uint32_t)(2 * N3 + c0) + lanes);
-#undef HSF_LD16
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (sc == 3) {  // all three accumulators read: the next tile's MMAs may start
-          asm volatile("tcgen05.fence::before_thread_sync;");
-          mbar_arrive_leader(&tempty_bar);
-        }
-        if (lane == 0) {  // the staging box's previous TMA store must have read it
-          if (EBUF3 == 1)
-            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-          else
-            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-        }
-        __syncwarp();
-        uint8_t* stg = stg0 + buf * 4096;
-        buf = (buf + 1) % EBUF3;
-        float4* dst = reinterpret_cast<float4*>(stg + lane * 128);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {  // complex columns 2j, 2j+1 -> (re, im, re, im)
-          const float a1 = __uint_as_float(v1[2 * j]), b1 = __uint_as_float(v2[2 * j]), s1 = __uint_as_float(v3[2 * j]);
-          const float a2 = __uint_as_float(v1[2 * j + 1]), b2 = __uint_as_float(v2[2 * j + 1]),
-                      s2 = __uint_as_float(v3[2 * j + 1]);
-          dst[j ^ (lane & 7)] = make_float4(a1 - b1, s1 - a1 - b1, a2 - b2, s2 - a2 - b2);
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) {
-          tma_store_2d(&mOut, stg, nb * (2 * N3) + 2 * c0, row0 + q * 32, st_pol);
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        }
-      }
-    }
-    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  cluster_sync_all();
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
-}
-
 // ----------------------------------------------------------------------- K4
 __device__ __forceinline__ float2 cmul_f(float2 a, float2 b) {
   return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
@@ -1312,70 +1092,6 @@ __global__ void split_b_mn_kernel(const float2* __restrict__ leaves, __nv_bfloat
   }
 }
 
-// 3M operand planes (tc_gemm3m_kernel): for path p and amplitude i,
-// plane rows p of Re, Im and Re + Im of c_p * A_p(i) (A side, with the tail
-// weights / leaf map of the half's folded tree) or of B_p(j) (B side), each
-// split bf16 hi/lo: planes [Re hi, Re lo, Im hi, Im lo, S hi, S lo], plane
-// stride `ps` elements, row length `ld`.  8 amplitudes per thread, 16 B stores.
-template <bool SIDE_A>
-__global__ void split_3m_kernel(const float2* __restrict__ leaves, const float2* __restrict__ cp,
-                                __nv_bfloat16* __restrict__ planes, long long K, long long ld, long long ps,
-                                long long MS, long long r0, long long rows, const TailParams tp,
-                                const float2* __restrict__ ttab) {
-  __shared__ long long node;
-  __shared__ int base[kMaxTail];
-  __shared__ unsigned smask[kMaxTail];
-  const long long p = blockIdx.y;
-  const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 8;
-  if (tp.mapped) {
-    if (threadIdx.x < tp.n) {
-      const int u = threadIdx.x;
-      const int d = (int)(((tp.p0 + p) / tp.stride[u]) % tp.radix[u]);
-      base[u] = (int)(tp.off[u] + ((long long)d << __popc(tp.mask[u])));
-      smask[u] = tp.mask[u];
-    }
-    if (threadIdx.x == 0) node = ((tp.p0 + p) / tp.T) % tp.Tt - tp.node0;
-    __syncthreads();
-  }
-  if (i >= ld) return;
-  const float2 c = SIDE_A ? (p < K ? cp[p] : make_float2(0.f, 0.f)) : make_float2(1.f, 0.f);
-  const long long row = tp.mapped ? node : p;
-  const float2* __restrict__ wrow = tp.W ? tp.W + ((tp.p0 + p) % tp.T) * tp.wld : nullptr;
-  float re[8], im[8];
-#pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    float2 v = make_float2(0.f, 0.f);
-    if (p < K && i + e < rows) {
-      v = cmul_f(leaves[row * MS + r0 + i + e], c);
-      if (tp.W) {
-        v = cmul_f(v, wrow[r0 + i + e]);
-      } else if (tp.n) {  // tail weights without the W table: per-unit loop
-        const unsigned ii = (unsigned)(r0 + i + e);
-        for (int u = 0; u < tp.n; ++u) {
-          unsigned mk = smask[u], x = 0;
-          for (int qq = 0; mk; ++qq, mk &= mk - 1) x |= ((ii >> (__ffs(mk) - 1)) & 1u) << qq;
-          v = cmul_f(v, __ldg(&ttab[base[u] + x]));
-        }
-      }
-    }
-    re[e] = v.x;
-    im[e] = v.y;
-  }
-  __align__(16) __nv_bfloat16 h[3][8], l[3][8];
-#pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    split_bf16(re[e], h[0][e], l[0][e]);
-    split_bf16(im[e], h[1][e], l[1][e]);
-    split_bf16(re[e] + im[e], h[2][e], l[2][e]);
-  }
-  const long long o = p * ld + i;
-#pragma unroll
-  for (int q = 0; q < 3; ++q) {
-    *reinterpret_cast<uint4*>(planes + (2 * q) * ps + o) = *reinterpret_cast<const uint4*>(h[q]);
-    *reinterpret_cast<uint4*>(planes + (2 * q + 1) * ps + o) = *reinterpret_cast<const uint4*>(l[q]);
-  }
-}
-
 }  // namespace tc
 
 // ------------------------------------------------------------------ host side
@@ -1542,91 +1258,6 @@ inline void tc_prep_a(const TcBuffers& t, const float2* leavesA, const float2* c
                                                                    rows, tp, ttab, t.a_l2);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("split_a: ") + cudaGetErrorString(e));
-}
-
-// ---- 3M (Gauss) path: operand planes and launch (tc_gemm3m_kernel) ---------
-// 6 bf16 planes [6][Kpad][ld] as one 3-D tensor {cols, K, 6}; boxes {64, BK3, 6}
-inline CUtensorMap make_map3(void* base, long long cols, long long K, long long ld, long long plane_stride) {
-  CUtensorMap m;
-  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)K, 6};
-  cuuint64_t strides[2] = {(cuuint64_t)ld * 2, (cuuint64_t)plane_stride * 2};
-  cuuint32_t box[3] = {64, (cuuint32_t)tc::BK3, 6};
-  cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides, box, estr,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) fail(HSF_ERR_CUDA, "cuTensorMapEncodeTiled (3-D planes) failed (" + std::to_string((int)r) + ")");
-  return m;
-}
-// Opt-in (HSF_TC_3M=1, K >= 64): on B200 both complex GEMM forms are bound by
-// the per-SM operand ingest (~39 B/clk of TMA traffic per SM, ~10.8 TB/s in
-// total), which the 4-real-GEMM kernel reaches at 96 % tensor activity; 3M
-// needs 1.5x the operand bytes per flop, so it is slower there (c2: 0.896 vs
-// 0.803 ms; a 4-CTA-cluster variant multicasting A was 1.76 ms -- multicast
-// does not reduce per-SM ingest and couples the pairs' pipelines).
-inline bool tc_use_3m(long long K) {
-  const char* e = std::getenv("HSF_TC_3M");
-  return e && e[0] == '1' && K >= 64;
-}
-struct Tc3Buffers {
-  long long Kpad, lda, ldb;  // lda = rows_pad (multiple of 256), ldb = MB_pad (multiple of 8)
-  __nv_bfloat16 *a, *b;      // 6 planes each, plane strides Kpad*lda / Kpad*ldb
-  long long K;
-};
-inline size_t tc3_workspace_bytes(long long K, long long rows, long long MB) {
-  const long long Kpad = (K + tc::BK3 - 1) / tc::BK3 * tc::BK3;
-  const long long lda = (rows + 255) / 256 * 256, ldb = (MB + 7) / 8 * 8;
-  return (((size_t)6 * Kpad * lda * 2 + 1023) & ~(size_t)1023) + (((size_t)6 * Kpad * ldb * 2 + 1023) & ~(size_t)1023);
-}
-inline Tc3Buffers tc3_buffers(long long K, long long rows, long long MB, void* ws, size_t ws_bytes) {
-  if (tc3_workspace_bytes(K, rows, MB) > ws_bytes) fail(HSF_ERR_INVALID_ARG, "tc3 workspace too small");
-  Tc3Buffers t;
-  t.K = K;
-  t.Kpad = (K + tc::BK3 - 1) / tc::BK3 * tc::BK3;
-  t.lda = (rows + 255) / 256 * 256;
-  t.ldb = (MB + 7) / 8 * 8;
-  t.a = (__nv_bfloat16*)ws;
-  t.b = (__nv_bfloat16*)((char*)ws + (((size_t)6 * t.Kpad * t.lda * 2 + 1023) & ~(size_t)1023));
-  return t;
-}
-inline void tc3_prep(const Tc3Buffers& t, bool side_a, const float2* leaves, const float2* cp, long long MS,
-                     long long r0, long long rows, const tc::TailParams& tp, const float2* ttab, cudaStream_t st) {
-  const long long ld = side_a ? t.lda : t.ldb;
-  const dim3 g((unsigned)((ld / 8 + 255) / 256), (unsigned)t.Kpad);
-  if (side_a)
-    tc::split_3m_kernel<true><<<g, 256, 0, st>>>(leaves, cp, t.a, t.K, ld, t.Kpad * ld, MS, r0, rows, tp, ttab);
-  else
-    tc::split_3m_kernel<false><<<g, 256, 0, st>>>(leaves, nullptr, t.b, t.K, ld, t.Kpad * ld, MS, 0, MS, tp, ttab);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("split_3m: ") + cudaGetErrorString(e));
-}
-// rows [row0, row0 + rows) of the output (row0 a multiple of 256) into out[rows][2*MB]
-inline void tc_gemm3m(const Tc3Buffers& t, float2* out, long long MB, long long row0, long long rows, cudaStream_t st) {
-  if (row0 % 256) fail(HSF_ERR_INVALID_ARG, "tc_gemm3m row offset not pair-tile aligned");
-  tc::Maps3 mp;
-  mp.a = make_map3(t.a + row0, rows, t.K, t.lda, t.Kpad * t.lda);
-  mp.b = make_map3(t.b, MB, t.K, t.ldb, t.Kpad * t.ldb);
-  tc::Params p;
-  std::memset(&p, 0, sizeof(p));
-  p.num_m = (int)((rows + 255) / 256);
-  p.num_n = (int)((MB + tc::N3 - 1) / tc::N3);
-  p.num_k = (int)(t.Kpad / tc::BK3);
-  p.a_evict_last = ((long long)6 * rows * t.Kpad * 2 <= (64ll << 20)) ? 1 : 0;
-  p.rows = rows;
-  p.cols = 2 * MB;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc::tc_gemm3m_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         tc::SMEM3_BYTES);
-    if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("tc3 smem attr: ") + cudaGetErrorString(e));
-    attr = true;
-  }
-  CUtensorMap mO = make_out_map((float*)out, rows, 2 * MB);
-  const long long tiles = (long long)p.num_m * p.num_n;
-  const int grid = 2 * (int)std::min<long long>(tiles, num_sms() / 2);
-  tc::tc_gemm3m_kernel<<<grid, tc::THREADS, tc::SMEM3_BYTES, st>>>(mp, mO, p);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("tc_gemm3m: ") + cudaGetErrorString(e));
 }
 
 // K4 for half B — may run on its own stream

@@ -134,10 +134,9 @@ struct Gen {
       o << "  constexpr u32 RANK = 0u;\n";
     }
     o << "  (void)stab;\n";
-    // grid: x = tile, y = node; the transposed-store variant swaps them so
-    // that the CTAs of all paths of one tile run together
-    o << "  const u32 NODE_ID = " << (swap_grid ? "blockIdx.x" : "blockIdx.y") << ";\n";
-    o << "  const u32 TILE_ID = " << (swap_grid ? "blockIdx.y" : "blockIdx.x") << ";\n";
+    // grid: x = tile, y = node
+    o << "  const u32 NODE_ID = blockIdx.y;\n";
+    o << "  const u32 TILE_ID = blockIdx.x;\n";
     o << "  (void)TILE_ID;\n";
     o << "  const long long node_g = a.node_first + NODE_ID;\n";
     o << "  const C* coef = reinterpret_cast<const C*>(a.coef);\n";
@@ -311,15 +310,10 @@ struct Gen {
   int nt = 256;  // threads per CTA (512 for narrow tree levels)
   int cb = 0;    // cluster tier: log2 CTAs per tile (0 = one CTA per tile)
 
-  bool swap_grid = false;  // transposed-store variant: grid x = node, y = tile
-
   // store_mode: 0 leaf (node-major), 1 MN-major split-bf16 B operand,
-  // 3 MN-major split-bf16 A operand of the swapped path-sum (st_aop),
-  // 2 transposed leaf: element G of node k to dst[G * ldw + k] (x c_p[k] when
-  // dst_lo carries c_p) -- the bitstring gather operand, no transpose pass
+  // 3 MN-major split-bf16 A operand of the swapped path-sum (st_aop)
   std::string build(const std::string& name, int threads, int cluster_bits, int store_mode = 0) {
     const bool operand_store = store_mode == 1 || store_mode == 3;
-    swap_grid = store_mode == 2;
     nt = threads;
     cb = whole ? 0 : cluster_bits;
     bool heavy = false;
@@ -355,14 +349,6 @@ struct Gen {
       o << "#pragma unroll 4\n";
       o << "  for (u32 e = 2u * threadIdx.x; e < LNEL; e += 2u * NT) " << (store_mode == 3 ? "st_aop" : "st_bop")
         << "(a, a.node_local0 + NODE_ID, G((RANK << LB) | e), s[sw(e)], s[sw(e + 1)]);\n";
-    } else if (swap_grid) {
-      o << "  { const long long kcol = a.node_local0 + NODE_ID;\n";
-      o << "    C cpv = czero<C>(); cpv.x = 1;\n";
-      o << "    if (a.dst_lo) cpv = reinterpret_cast<const C*>(a.dst_lo)[kcol];\n";
-      o << "    C* T = reinterpret_cast<C*>(a.dst);\n";
-      o << "#pragma unroll 4\n";
-      o << "    for (u32 e = threadIdx.x; e < LNEL; e += NT) T[(long long)G((RANK << LB) | e) * a.ldw + kcol] = "
-           "cmul(s[sw(e)], cpv);\n  }\n";
     } else {
       o << "#pragma unroll 4\n";
       o << "  for (u32 e = 2u * threadIdx.x; e < LNEL; e += 2u * NT) st2(dst + G((RANK << LB) | e), s[sw(e)], s[sw(e + 1)]);\n";

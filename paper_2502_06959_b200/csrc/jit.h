@@ -25,8 +25,7 @@ struct JitLaunchArgs {
 // coef (plan master table, optional): fixed gate matrices become literals
 // store_mode 1: write the MN-major split-bf16 B operand instead of the leaf
 // (JitArgs dst / dst_lo / ldw; row pair 2k, 2k+1 for output node k);
-// store_mode 2: transposed leaf dst[G * ldw + k] (x c_p[k] if dst_lo), launched
-// with grid (nodes, tiles)
+// store_mode 3: the swapped path-sum's MN-major M operand (st_aop)
 std::string jit_pass_source(const Half& H, const Pass& ps, bool c64, int threads = 256, int cluster_bits = 0,
                             const std::vector<cd>* coef = nullptr, int store_mode = 0);
 // dynamic shared memory of that kernel (tile + staged diagonal tables)

@@ -591,49 +591,25 @@ static std::vector<PassChoice> greedy_passes(const Half& H, int64_t ob, int64_t 
   return out;
 }
 
-// Tile size per transition: t, or up to t_max (tile_qubits == 0 => auto: 12,
-// or 13 for complex64 = 64 KiB tiles) when a wider tile needs fewer HBM passes
-// over the level.
-// Tile size of a transition's passes.  Wide levels: the fewest passes over
-// t in [t, t_max] (each pass is an HBM/L2 round trip of every node).  Narrow
-// levels (fewer than 2 CTAs per SM at t, e.g. the roots): the time estimate
-//   passes x 3 us + amplitude-ops / (2.5e13 FMA/s x min(1, CTAs / 296)),
-// over t down to 10 -- more, smaller tiles spread a long op chain over more
-// SMs (c3's roots ran on 4 CTAs, bound by one SM's instruction fetch).
-static double ops_fma(const Half& H, int64_t ob, int64_t oe) {
-  double fma = 0;
-  for (int64_t i = ob; i < oe; ++i) {
-    const HostOp& op = H.ops[i];
-    fma += op.kind == OP_DIAG ? 6.0 : 4.0 * std::ldexp(1.0, op.k);
-  }
-  return fma;
-}
-static std::vector<PassChoice> choose_passes(const Half& H, int64_t ob, int64_t oe, int t, int t_max, double nodes,
-                                             bool narrow_ok, int& bt) {
-  const double amps = std::ldexp(1.0, H.m), full = 2.0 * 148;
-  const double work = ops_fma(H, ob, oe) * amps * nodes / 2.5e13;
-  const bool narrow = narrow_ok && nodes * std::ldexp(1.0, H.m - t) < full;
-  const int lo = narrow ? std::min(t, 10) : t;
+// Tile size of a transition's passes: the fewest passes over t in [t, t_max]
+// (tile_qubits == 0 => auto: 12, or 13 for complex64 = 64 KiB tiles); each
+// pass is an HBM/L2 round trip of every node.
+static std::vector<PassChoice> choose_passes(const Half& H, int64_t ob, int64_t oe, int t, int t_max, int& bt) {
   std::vector<PassChoice> best;
-  double best_est = 1e300;
   bt = t;
-  for (int t2 = lo; t2 <= t_max && t2 <= H.m; ++t2) {
+  for (int t2 = t; t2 <= t_max && t2 <= H.m; ++t2) {
     std::vector<PassChoice> c = greedy_passes(H, ob, oe, t2);
-    const double ctas = nodes * std::ldexp(1.0, H.m - t2);
-    const double est = narrow ? 3e-6 * (double)c.size() + work / std::min(1.0, ctas / full) : (double)c.size();
-    if (best.empty() || est < best_est) {
+    if (best.empty() || c.size() < best.size()) {
       best.swap(c);
-      best_est = est;
       bt = t2;
     }
   }
   return best;
 }
 
-static void plan_passes(Half& H, Transition& tr, int64_t ob, int64_t oe, int t, int t_max, double nodes = 1e9,
-                        bool narrow_ok = false) {
+static void plan_passes(Half& H, Transition& tr, int64_t ob, int64_t oe, int t, int t_max) {
   int bt = t;
-  std::vector<PassChoice> best = choose_passes(H, ob, oe, t, t_max, nodes, narrow_ok, bt);
+  std::vector<PassChoice> best = choose_passes(H, ob, oe, t, t_max, bt);
   for (auto& pc : best) {
     Pass p;
     p.t = bt;
@@ -957,10 +933,6 @@ static void build_half(Plan& P, int h, const std::vector<SchedItem>& order, int 
   const int t = std::min(H.m, P.opts.tile_qubits > 0 ? P.opts.tile_qubits : 12);
   const int t_max = (P.opts.tile_qubits == 0 && P.opts.dtype == HSF_C64) ? 13 : t;
   const bool whole = H.m <= smem_limit;
-  // narrow-level tile choice (choose_passes): opt-in (HSF_NARROW_TILES=1) --
-  // measured neutral (c3 0.651 vs 0.661 ms, c5 / q32-1 / q33-3 within noise)
-  const char* nn = std::getenv("HSF_NARROW_TILES");
-  const bool narrow_ok = P.opts.tile_qubits == 0 && nn && nn[0] == '1';
   {
     const double elem = (P.opts.dtype == HSF_C64) ? 8.0 : 16.0;
     const double amps = std::ldexp(1.0, H.m), S = amps * elem;
@@ -970,7 +942,7 @@ static void build_half(Plan& P, int h, const std::vector<SchedItem>& order, int 
       size_t np = 1;
       int tt = H.m;
       const double Nb = nodes(b), Na = (a < 0) ? 0.0 : nodes(a);
-      if (!whole) np = choose_passes(H, ob, oe, t, t_max, Nb, narrow_ok, tt).size();
+      if (!whole) np = choose_passes(H, ob, oe, t, t_max, tt).size();
       double bytes = 0;
       for (size_t i = 0; i < np; ++i) {
         const double rd = (i == 0) ? ((a < 0) ? 0.0 : S * (Na + 0.3 * (Nb - Na))) : S * Nb;
@@ -1029,7 +1001,7 @@ static void build_half(Plan& P, int h, const std::vector<SchedItem>& order, int 
       p.op_end = (int64_t)H.dev_ops.size();
       tr.passes.push_back(p);
     } else {
-      plan_passes(H, tr, ob, oe, t, t_max, (double)range_prod(R, 0, L), narrow_ok);
+      plan_passes(H, tr, ob, oe, t, t_max);
     }
     // resolve factor digits for this transition's output level
     for (auto& p : tr.passes)

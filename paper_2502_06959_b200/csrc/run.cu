@@ -45,11 +45,6 @@ struct DeviceState {
   int jit_bop_nt = 256;
   void* jit_aop = nullptr;  // the same pass writing the swapped path-sum's M operand
 
-  // bitstring runs: the last pass of each half writing the transposed,
-  // c_p-folded gather operand [2^m][K] directly (no transpose kernel);
-  // [variant 0 full / 1 fold][half]
-  void* jit_tr[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
-  int jit_tr_nt[2][2] = {{256, 256}, {256, 256}};
   bool jit = false;                         // specialised pass kernels loaded
   unsigned long long* perm_tab = nullptr;   // caller -> internal index bits (partitions)
   // [variant: 0 full tree, 1 bitstring fold, 2 half-sided tail][half] per flattened pass
@@ -243,27 +238,10 @@ static DeviceState* ensure_device(Plan* P, int device) {
         owner.push_back({-1, 3});
       }
     }
-    // transposed-store variants of each half's last pass (bitstring runs);
-    // opt-in (HSF_TRANSPOSED_STORE=1): its scattered 8 B stores measured slower
-    // than the leaf pass + transpose_fold_kernel (c5 4.99 vs 4.29 ms)
-    const char* tse = std::getenv("HSF_TRANSPOSED_STORE");
-    for (int v = 0; v < 2 && tse && tse[0] == '1'; ++v) {
-      if (v == 1 && P->fold_u0 < 0) continue;
-      for (int h = 0; h < 2; ++h) {
-        const Half& H = v ? P->half_fold[h] : P->half[h];
-        if (H.trans.empty() || H.trans.back().passes.empty() || d->jit_cb[v][h].empty() || d->jit_cb[v][h].back() != 0)
-          continue;
-        d->jit_tr_nt[v][h] = d->jit_nt[v][h].back();
-        src.push_back(jit_pass_source(H, H.trans.back().passes.back(), c64, d->jit_tr_nt[v][h], 0, &P->coef, 2));
-        owner.push_back({-2 - (2 * v + h), 0});
-      }
-    }
     std::vector<void*> fns = jit_compile_all(device, src);
     for (size_t i = 0; i < fns.size(); ++i) {
       if (owner[i].first == -1)
         (owner[i].second == 3 ? d->jit_aop : d->jit_bop) = fns[i];
-      else if (owner[i].first <= -2)
-        d->jit_tr[(-2 - owner[i].first) / 2][(-2 - owner[i].first) % 2] = fns[i];
       else
         d->jit_fn[owner[i].first][owner[i].second].push_back(fns[i]);
     }
@@ -295,7 +273,6 @@ struct Layout {
   uint64_t hp0[2] = {0, 0}, hp1[2] = {0, 0};
   const Half* half[2] = {nullptr, nullptr};
   bool bop = false;            // half B's last pass writes the MN-major GEMM operand (with a JIT kernel)
-  bool g3m = false;            // full-output path-sum by the 3M (Gauss) kernel (tc_gemm3m_kernel)
   bool swap = false;           // few output rows: GEMM with the roles swapped (half B's 2^nB rows as M,
                                // half A's rows as N with the complex rotation), then a transpose
   size_t off_swapT = 0;        // its [2^nB][swap_cols] complex64 output
@@ -378,8 +355,6 @@ static Layout make_layout(const Plan& P, const hsf_run_args& a, size_t elem) {
       L.hp1[h] = L.p1;
     }
   }
-  L.g3m = !L.bits_mode && L.prec == HSF_PREC_BF16X3 && P.opts.dtype == HSF_C64 && a.n_out_shards == 0 &&
-          !a.accumulate && tc_use_3m((long long)L.K);
   {
     // swapped path-sum for prefix outputs (<= 128 rows of A): half B's leaves
     // become the un-rotated (re, im planes) MN-major M operand, stored by B's
@@ -390,11 +365,11 @@ static Layout make_layout(const Plan& P, const hsf_run_args& a, size_t elem) {
     const uint64_t nr = (a.row_end > a.row_begin ? a.row_end - a.row_begin : 1ull << (P.n - P.n_low));
     const char* sw = std::getenv("HSF_TC_SWAP");
     const bool want = sw ? sw[0] == '1' : true;
-    L.swap = want && nr <= 128 && !L.bits_mode && !L.g3m && P.opts.dtype == HSF_C64 && L.prec != HSF_PREC_SIMT &&
+    L.swap = want && nr <= 128 && !L.bits_mode && P.opts.dtype == HSF_C64 && L.prec != HSF_PREC_SIMT &&
              L.prec != HSF_PREC_TF32X3 && a.n_out_shards == 0 && !P.permuted && tc_mn((long long)L.K) &&
              P.n_low >= 8;
   }
-  L.bop = !L.bits_mode && !L.g3m && !L.swap && (L.prec == HSF_PREC_BF16X3 || L.prec == HSF_PREC_BF16X1) &&
+  L.bop = !L.bits_mode && !L.swap && (L.prec == HSF_PREC_BF16X3 || L.prec == HSF_PREC_BF16X1) &&
           P.opts.dtype == HSF_C64 && L.var[1] == 0 && tc_mn((long long)L.K);
   // the swapped path-sum's M operand written by half B's last pass (HSF_TC_AOP=0 disables)
   const char* aop_env = std::getenv("HSF_TC_AOP");
@@ -462,8 +437,7 @@ static Layout make_layout(const Plan& P, const hsf_run_args& a, size_t elem) {
       off = align_up(off + ((size_t)1 << P.n) * elem);
     }
     if (L.prec != HSF_PREC_SIMT) {
-      L.tc_bytes = L.g3m    ? tc3_workspace_bytes((long long)L.K, (long long)(L.r1 - L.r0), 1ll << nB)
-                   : L.swap ? tc_workspace_bytes((long long)L.K, 1ll << nB, swap_cols(L), tc_planes(L.prec))
+      L.tc_bytes = L.swap ? tc_workspace_bytes((long long)L.K, 1ll << nB, swap_cols(L), tc_planes(L.prec))
                             : tc_workspace_bytes((long long)L.K, (long long)(L.r1 - L.r0), 1ll << nB, tc_planes(L.prec));
       L.off_tc = off;
       off = align_up(off + L.tc_bytes);
@@ -696,13 +670,7 @@ static void run_half(const Plan& P, DeviceState* d, int h, const Layout& L, cuda
         }
         const bool bop = h == 1 && L.bop && d->jit_bop && last && pi + 1 == tr.passes.size();
         const bool aop = h == 1 && L.aop && d->jit_aop && last && pi + 1 == tr.passes.size();
-        const bool trs = L.bits_mode && var <= 1 && d->jit_tr[var][h] && last && pi + 1 == tr.passes.size();
-        if (trs) {  // K4t fused: write the transposed (c_p-folded for A) gather operand
-          JitLaunchArgs ja{pp.src, ws + L.off_T[h], pp.coef, pp.node_first, pp.node_local0, pp.src_first, pp.src_div,
-                           pp.tile0, h == 0 ? d->cp : nullptr, (long long)L.K};
-          jit_launch(d->jit_tr[var][h], (unsigned)ny, (unsigned)tiles, (unsigned)d->jit_tr_nt[var][h],
-                     jit_smem_bytes(ps, sizeof(R) == 4, 0), st, ja, 0);
-        } else if (aop) {  // swapped path-sum: write the MN-major M operand instead of the leaves
+        if (aop) {  // swapped path-sum: write the MN-major M operand instead of the leaves
           TcBuffers t = tc_swap_buffers((long long)L.K, 1ll << H.m, swap_cols(L), tc_planes(L.prec), ws + L.off_tc,
                                         L.tc_bytes);
           JitLaunchArgs ja{pp.src, t.a_hi, pp.coef, pp.node_first, pp.node_local0, pp.src_first, pp.src_div, pp.tile0,
@@ -747,7 +715,6 @@ static void prep_half(Plan* P, DeviceState* d, const Layout& L, int h, cudaStrea
   const long long K = (long long)L.K;
   const C* leaves = (const C*)(ws + L.off_leaves[h]);
   if (L.bits_mode) {
-    if (L.var[h] <= 1 && d->jit_tr[L.var[h]][h]) return;  // written by the half's last pass
     C* T = (C*)(ws + L.off_T[h]);
     const char* tv = std::getenv("HSF_TRANSPOSE_V1");
     if (sizeof(R) == 4 && m >= 1 && !(tv && tv[0] == '1')) {  // 16 B accesses (c5: 0.43 ms per half before)
@@ -771,11 +738,7 @@ static void prep_half(Plan* P, DeviceState* d, const Layout& L, int h, cudaStrea
       tp.T = 1;
       tp.Tt = 1;
     }
-    if (L.g3m) {
-      const Tc3Buffers t3 = tc3_buffers(K, (long long)(L.r1 - L.r0), 1ll << nB, ws + L.off_tc, L.tc_bytes);
-      tc3_prep(t3, h == 0, (const float2*)leaves, (const float2*)d->cp, 1ll << m, h == 0 ? (long long)L.r0 : 0,
-               h == 0 ? (long long)(L.r1 - L.r0) : (1ll << m), tp, (const float2*)d->tail, st);
-    } else if (L.swap) {  // roles swapped: B's leaves -> M operand, A's rows (rotated, c_p) -> N operand
+    if (L.swap) {  // roles swapped: B's leaves -> M operand, A's rows (rotated, c_p) -> N operand
       TcBuffers t = tc_swap_buffers(K, 1ll << nB, swap_cols(L), tc_planes(L.prec), ws + L.off_tc, L.tc_bytes);
       if (h == 1) {
         if (!(L.aop && d->jit_aop))  // else written by half B's last pass
@@ -901,11 +864,6 @@ static void run_core_full(Plan* P, DeviceState* d, const Layout& L, cudaStream_t
     CK(cudaGetLastError());
   } else {
     if (sizeof(R) != 4) fail(HSF_ERR_UNSUPPORTED, "tensor-core path-sum needs complex64");
-    if (L.g3m) {
-      tc_gemm3m(tc3_buffers(K, (long long)(L.r1 - L.r0), 1ll << nB, ws + L.off_tc, L.tc_bytes), (float2*)out,
-                1ll << nB, (long long)lo, (long long)nrows, st);
-      return;
-    }
     if (L.swap) {  // outT[j][i] over all 2^nB columns and the run's rows, then out[i][j]
       // (host-output chunks: the GEMM runs with the first chunk, each chunk transposes its rows)
       const long long Rw = swap_cols(L), MBl = 1ll << nB;
@@ -1044,7 +1002,7 @@ static void run(Plan* P, const hsf_run_args& a) {
                                    L.p0, L.p1, L.r0, L.r1, (uint64_t)L.prec, (uint64_t)a.accumulate,
                                    (uint64_t)timed, (uint64_t)L.fold, (uint64_t)(uintptr_t)d->ws,
                                    (uint64_t)(uintptr_t)d->cp, (uint64_t)L.total, (uint64_t)a.n_out_shards,
-                                   a.shard_rows, (uint64_t)L.swap, (uint64_t)L.g3m, (uint64_t)L.bop,
+                                   a.shard_rows, (uint64_t)L.swap, (uint64_t)L.bop,
                                    (uint64_t)a.out_on_device, (uint64_t)a.bits_on_device};
       for (int o = 0; o < a.n_out_shards; ++o) key.push_back((uint64_t)(uintptr_t)a.out_shards[o]);
       if (!d->gexec || key != d->gkey) {

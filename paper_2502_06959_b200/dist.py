@@ -47,7 +47,8 @@ class Shard:
 def path_range_for_rank(n_paths: int, rank: int, world: int):
     """Contiguous range of the linear (mixed-radix, last unit fastest) path
     index: whole subtrees of the path tree when `world` divides the leading
-    radices (true for c1..c5 at 1/2/4/8)."""
+    radices (true for c1..c5 at 1/2/4/8).  Empty (p0 == p1) for some ranks
+    when world > n_paths; `sharded_step` then skips the evaluation."""
     return (n_paths * rank // world, n_paths * (rank + 1) // world)
 
 
@@ -135,12 +136,16 @@ def sharded_step(shard: Shard, partial, out, shard_out=None, group=None):
         if dist.is_initialized():
             sync()
             dist.barrier(group=group)
-        partial(shard.path_range, None, out)
+        if shard.path_range[0] < shard.path_range[1]:
+            partial(shard.path_range, None, out)
         sync()
         if dist.is_initialized():
             dist.barrier(group=group)
         return out.local
-    partial(shard.path_range, shard.row_range, out)
+    if shard.path_range[0] < shard.path_range[1]:
+        partial(shard.path_range, shard.row_range, out)
+    else:  # more ranks than paths: this rank contributes nothing to the sum
+        out.zero_()
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     if world == 1 or shard.mode == "rows":
         return out

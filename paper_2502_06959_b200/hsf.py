@@ -240,23 +240,61 @@ class Plan:
         be None."""
         import torch
 
-        def ptr(x):
+        keep = []  # host arrays converted here stay alive until hsf_run returns
+        cdt = {"c64": (torch.complex64, np.complex64), "c128": (torch.complex128, np.complex128)}[self.dtype]
+
+        def ptr(x, kind):
             if isinstance(x, torch.Tensor):
                 if not x.is_contiguous():
-                    raise ValueError("tensor must be contiguous")
+                    raise ValueError(f"{kind} tensor must be contiguous")
+                if kind == "out" and x.dtype != cdt[0]:
+                    raise TypeError(f"out must be {cdt[0]} for a {self.dtype} plan, got {x.dtype}")
+                if kind == "bitstrings" and x.dtype not in (torch.int64, torch.uint64):
+                    raise TypeError(f"bitstrings must be int64 / uint64, got {x.dtype}")
+                if x.is_cuda and torch.cuda.is_available() and x.device.index != dev:
+                    raise ValueError(f"{kind} is on {x.device}, the run on cuda:{dev}")
                 return x.data_ptr(), x.is_cuda, x.numel()
-            x = np.ascontiguousarray(x)
+            if not isinstance(x, np.ndarray):
+                raise TypeError(f"{kind} must be a torch tensor or a numpy array")
+            if kind == "out":
+                if x.dtype != cdt[1]:
+                    raise TypeError(f"out must be {np.dtype(cdt[1])} for a {self.dtype} plan, got {x.dtype}")
+                if not x.flags.c_contiguous or not x.flags.writeable:
+                    raise ValueError("out must be a writeable C-contiguous array")
+            else:
+                if x.dtype not in (np.int64, np.uint64):
+                    raise TypeError(f"bitstrings must be int64 / uint64, got {x.dtype}")
+                x = np.ascontiguousarray(x)
+                keep.append(x)
             return x.ctypes.data, False, x.size
 
+        dev = torch.cuda.current_device() if torch.cuda.is_available() else -1
+        if path_range is not None:
+            p0, p1 = int(path_range[0]), int(path_range[1])
+            if not 0 <= p0 < p1 <= self.n_paths:
+                raise ValueError(f"path_range {path_range} must be non-empty within [0, {self.n_paths})")
         shards_arr = None
         if out_shards:
             ps = [s if isinstance(s, int) else s.data_ptr() for s in out_shards]
             shards_arr = (C.c_void_p * len(ps))(*ps)
             op, odev = None, True
         else:
-            op, odev, _ = ptr(out)
-        bp, bdev, nb = (None, False, 0) if bitstrings is None else ptr(bitstrings)
-        dev = torch.cuda.current_device() if torch.cuda.is_available() else -1
+            if out is None:
+                raise ValueError("out is None")
+            op, odev, n_out = ptr(out, "out")
+        bp, bdev, nb = (None, False, 0) if bitstrings is None else ptr(bitstrings, "bitstrings")
+        if bitstrings is not None and not bdev:  # host samples: checked here (device ones in the library)
+            hb = bitstrings.numpy() if isinstance(bitstrings, torch.Tensor) else bitstrings
+            if nb and self.n < 64 and int(np.bitwise_or.reduce(hb.view(np.uint64).ravel())) >> self.n:
+                raise ValueError(f"bitstrings must be < 2^{self.n}")
+        if not out_shards:
+            if bitstrings is not None:
+                need = nb
+            else:
+                r0, r1 = row_range if row_range else (0, 1 << self.n_a)
+                need = (r1 - r0) << self.n_b
+            if n_out < need:
+                raise ValueError(f"out holds {n_out} amplitudes, the run writes {need}")
         st = stream if stream is not None else (torch.cuda.current_stream().cuda_stream if torch.cuda.is_available() else None)
         phase = (C.c_double * 5)() if timings else None
         a = self._args(op, odev, bp, nb, bdev, path_range, row_range, precision, st, dev,

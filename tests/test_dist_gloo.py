@@ -61,13 +61,22 @@ def _fused_partial(inst, P):
     return partial
 
 
+def _inst(name):
+    if name == "single_path":  # no crossing gate: n_p = 1 < world (rank 0's range is empty)
+        from types import SimpleNamespace
+        bits = np.arange(16, dtype=np.uint64)
+        return SimpleNamespace(text="qubits 4\nh 0\nh 2\ncz 0 1\nrx 0x1.8p-1 3\ncz 2 3\n", n=4, n_low=2,
+                               blocks=[], bitstrings=bits)
+    return make_config(name, twin=True)
+
+
 def _worker(rank, world, port, name, mode, q):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        inst = make_config(name, twin=True)
+        inst = _inst(name)
         n, g = O.parse_circuit(inst.text)
         P = O.plan(n, g, inst.n_low, inst.blocks)
         full = inst.bitstrings is None
@@ -110,7 +119,7 @@ def _run(name, mode, world=2):
 
 
 def _reference(name):
-    inst = make_config(name, twin=True)
+    inst = _inst(name)
     n, g = O.parse_circuit(inst.text)
     psi = O.schrodinger(n, g)
     return inst, psi if inst.bitstrings is None else psi[inst.bitstrings.astype(np.int64)]
@@ -118,7 +127,8 @@ def _reference(name):
 
 @pytest.mark.parametrize("name,mode", [("c4", "reduce_scatter"), ("c4", "rows"), ("c4", "allreduce"),
                                        ("c4", "fused_rs"), ("c2", "fused_rs"),
-                                       ("c1", "allreduce"), ("c5", "allreduce"), ("c3", "allreduce")])
+                                       ("c1", "allreduce"), ("c5", "allreduce"), ("c3", "allreduce"),
+                                       ("single_path", "allreduce")])
 def test_two_rank_shards_reassemble(name, mode):
     inst, ref = _reference(name)
     pieces = _run(name, mode)
@@ -129,6 +139,19 @@ def test_two_rank_shards_reassemble(name, mode):
         got = np.concatenate([v for _, v in sorted(pieces, key=lambda x: x[0][0])])
         assert [r for r, _ in pieces] == [D.row_range_for_rank(inst.n - inst.n_low, r, 2) for r in range(2)]
         assert np.abs(got - ref).max() <= 1e-12
+
+
+def test_more_ranks_than_paths():
+    # ranks whose range is empty must not evaluate (hsf_run reads 0,0 as "all paths")
+    rs = [D.path_range_for_rank(1, r, 2) for r in range(2)]
+    assert rs == [(0, 0), (0, 1)]
+    calls = []
+
+    class Z:
+        def zero_(self):
+            calls.append("zero")
+    D.sharded_step(D.make_shard("allreduce", 1, 2, 0, 2, False), lambda *a: calls.append("run"), Z())
+    assert calls == ["zero"]
 
 
 @pytest.mark.parametrize("world", [1, 2, 4, 8])

@@ -562,23 +562,6 @@ def test_fused_reduce_scatter_two_processes_ipc(torch):
     assert np.abs(got - ref).max() <= 1e-6
 
 
-@pytest.mark.parametrize("name,path_range", [("c5", None), ("c5", (4, 12)), ("c3", None), ("c1", None)])
-def test_transposed_store_variant(torch, name, path_range, monkeypatch):
-    # opt-in: each half's last pass writes the transposed (c_p-folded for A)
-    # gather operand itself instead of the leaves + transpose_fold_kernel
-    monkeypatch.setenv("HSF_TRANSPOSED_STORE", "1")
-    inst = make_config(name, twin=True)
-    if inst.bitstrings is None:
-        inst.bitstrings = np.random.default_rng(7).integers(0, 1 << inst.n, 4096, dtype=np.uint64)
-    n, g = O.parse_circuit(inst.text)
-    P = O.plan(n, g, inst.n_low, inst.blocks)
-    p0, p1 = path_range or (0, P.n_paths)
-    A, B, c = O.half_states(P, p0, p1)
-    ref = O.recombine_bits(A, B, c, inst.bitstrings, inst.n_low)
-    got, _ = gpu_bits(torch, inst, inst.bitstrings, path_range=path_range)
-    check(got, ref, inst.dtype)
-
-
 @pytest.mark.parametrize("name,path_range", [("c3", None), ("c3", (16, 48)), ("c5", None), ("c5", (3, 9))])
 @pytest.mark.parametrize("grouped", ["0", "1"])
 def test_grouped_gather(torch, name, path_range, grouped, monkeypatch):
@@ -595,59 +578,6 @@ def test_grouped_gather(torch, name, path_range, grouped, monkeypatch):
     ref = O.recombine_bits(A, B, c, bits, inst.n_low)
     got, _ = gpu_bits(torch, inst, bits, path_range=path_range)
     check(got, ref, inst.dtype)
-
-
-@pytest.mark.parametrize("name", ["c2", "c4", "c5", "toy_head"])
-@pytest.mark.parametrize("mode", ["1", "0"])
-def test_gauss_3m_gemm(torch, name, mode, monkeypatch):
-    # tc_gemm3m_kernel (three real products, Re = T1 - T2, Im = T3 - T1 - T2)
-    # vs the 4-real-GEMM kernel, against the oracle: full, ragged path and row
-    # ranges, host output in chunks
-    monkeypatch.setenv("HSF_TC_3M", mode)
-    if name == "toy_head":
-        from types import SimpleNamespace
-        inst = SimpleNamespace(text="qubits 4\nx 1\nx 3\ncz 1 2\ncp 0x1.8p-1 0 3\nh 1\nh 2\ncz 1 3\nh 0\nh 3\n"
-                                    "cz 0 2\nrx 0x1.4p-2 1\nrx 0x1.8p-2 2\n", n_low=2, blocks=[], dtype="c64")
-    else:
-        inst = make_config(name, twin=True, n_bits=0) if name == "c5" else make_config(name, twin=True)
-    n, g = O.parse_circuit(inst.text)
-    P = O.plan(n, g, inst.n_low, inst.blocks)
-    rows = 1 << (n - inst.n_low)
-    for pr, rr in [(None, None), ((1, P.n_paths - 1), (1, rows - 1))]:
-        p0, p1 = pr or (0, P.n_paths)
-        A, B, c = O.half_states(P, p0, p1)
-        ref = O.recombine_full(A, B, c)
-        if rr:
-            ref = ref[rr[0] << inst.n_low:rr[1] << inst.n_low]
-        got, _ = gpu_full(torch, inst, precision="bf16x3", path_range=pr, row_range=rr)
-        check(got, ref, "c64")
-
-
-def test_gauss_3m_c2_full_size(torch, monkeypatch):
-    monkeypatch.setenv("HSF_TC_3M", "1")
-    inst = make_config("c2")
-    got, P = gpu_full(torch, inst, precision="bf16x3")
-    n, x = inst.n, inst.meta["x"]
-    i = np.arange(1 << n, dtype=np.int64)
-    rev = np.zeros_like(i)
-    for b in range(n):
-        rev |= ((i >> b) & 1) << (n - 1 - b)
-    ref = np.exp(2j * np.pi * ((x * rev) % (1 << n)) / (1 << n)) / 2 ** (n / 2)
-    md, rel = check(got, ref, "c64")
-    print(f"c2 3M max|d|={md:.3e} relL2={rel:.3e}")
-
-
-@pytest.mark.parametrize("name", ["c3", "c5"])
-def test_narrow_level_tiles(torch, name, monkeypatch):
-    # opt-in small tiles on narrow levels (t = 10 / 11 roots), tiled tier
-    monkeypatch.setenv("HSF_NARROW_TILES", "1")
-    inst = make_config(name, twin=True, n=28, n_low=14, n_bits=4096)
-    n, g = O.parse_circuit(inst.text)
-    P = O.plan(n, g, inst.n_low, inst.blocks)
-    A, B, c = O.half_states(P, 0, 8)
-    ref = O.recombine_bits(A, B, c, inst.bitstrings, inst.n_low)
-    got, _ = gpu_bits(torch, inst, inst.bitstrings, path_range=(0, 8))
-    check(got, ref, "c64")
 
 
 @pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
