@@ -72,6 +72,8 @@ struct DeviceState {
   cudaStream_t aux = nullptr;   // bitstring prep (H2D, relabel, bucket sort), overlapping the trees
   cudaEvent_t ev_aux = nullptr;
   bool sticky = false;
+  unsigned int* bad_bits = nullptr;      // mapped host word: a sample had bits >= 2^n
+  unsigned int* bad_bits_dev = nullptr;  //   its device alias
 };
 
 void destroy_device(Plan* p) {
@@ -105,6 +107,7 @@ void destroy_device(Plan* p) {
   }
   if (d->side) cudaStreamDestroy(d->side);
   if (d->aux) cudaStreamDestroy(d->aux);
+  if (d->bad_bits) cudaFreeHost(d->bad_bits);
   if (d->ev_aux) cudaEventDestroy(d->ev_aux);
   if (cur >= 0) cudaSetDevice(cur);
   delete d;
@@ -257,6 +260,9 @@ static DeviceState* ensure_device(Plan* P, int device) {
   CK(cudaStreamCreateWithFlags(&d->side, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&d->aux, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&d->ev_aux, cudaEventDisableTiming));
+  CK(cudaHostAlloc((void**)&d->bad_bits, sizeof(unsigned int), cudaHostAllocMapped));
+  *d->bad_bits = 0;
+  CK(cudaHostGetDevicePointer((void**)&d->bad_bits_dev, d->bad_bits, 0));
   return d;
 }
 
@@ -286,14 +292,24 @@ struct Layout {
   size_t off_T[2] = {0, 0};    // transposed operands (bitstring mode)
   size_t off_bits = 0, off_out = 0, off_tc = 0;
   size_t off_pbits = 0, off_pout = 0;  // relabelled bitstrings / internal-order output (partitions)
-  bool grouped = false;        // bitstring gather bucketed by A row (gather_grouped_c64_kernel)
-  size_t off_grp = 0;          // counts[2^nA] | offs[2^nA + 1] | cursor[2^nA] | perm[n] (int32)
+  int direct = -1;             // block gather (gather_block_c64_kernel): half read from its leaves, -1 => none
+  long long Kp = 0;            // its transposed other half's padded row length
+  long long n_blocks = 0;      // blocks of block_rows rows of the direct half
+  int block_rows = 16;
+  size_t off_grp = 0;          // counts[n_blocks] | offs[n_blocks + 1] | cursor[n_blocks] | sidx[n] (int32)
+  size_t off_sbits = 0;        // sbits[n] (uint64): the samples' bitstrings in block order
   size_t tc_bytes = 0;
   uint64_t chunk_rows = 0;     // full mode, host output: rows per staged D2H chunk
   size_t chunk_bytes = 0;
   size_t total = 0;
 };
 
+// block gather launch shape (tuning: HSF_GATHER_CFG = 100 * (RB == 32 ? 3 : 1)
+// + 10 * min CTAs per SM + U samples in flight per warp)
+static int gather_cfg() {
+  if (const char* e = std::getenv("HSF_GATHER_CFG")) return std::atoi(e);
+  return 344;
+}
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 // split-bf16 operand planes per precision mode
 // (4 = tf32x3: hi + lo planes of fp32-storage tf32 values)
@@ -400,9 +416,28 @@ static Layout make_layout(const Plan& P, const hsf_run_args& a, size_t elem) {
     off = align_up(off + ((size_t)(L.hp1[h] - L.hp0[h]) << L.half[h]->m) * elem);
   }
   if (L.bits_mode) {
+    // block gather: >= 4 samples per block of the direct half (the one whose
+    // tree the planner estimates to finish last: its leaves are read in place,
+    // the other half is transposed beside its tree), complex64, K <= 512
+    // (padded to a power of two >= 64), <= 2^15 blocks (the bucket sort's
+    // shared histograms), samples < 2^31
+    const int mA = L.half[0]->m, mB = L.half[1]->m;
+    int dir = L.half[1]->est_ms >= L.half[0]->est_ms ? 1 : 0;
+    if (const char* e = std::getenv("HSF_GATHER_DIRECT")) dir = std::atoi(e);  // tests: 0 / 1, -1 = per-sample gather
+    const int mD = dir == 1 ? mB : mA;
+    const int rb = gather_cfg() / 100 == 3 ? 32 : 16;
+    if (dir >= 0 && P.opts.dtype == HSF_C64 && L.K <= 512 && mD >= 5 && (1ll << mD) / rb <= 32768 &&
+        a.n_bitstrings < (1ull << 31) && (long long)a.n_bitstrings >= (4ll << mD) / rb) {
+      L.direct = dir;
+      L.Kp = 64;
+      while (L.Kp < (long long)L.K) L.Kp *= 2;
+      L.block_rows = rb;
+      L.n_blocks = (1ll << mD) / rb;
+    }
     for (int h = 0; h < 2; ++h) {
+      if (h == L.direct) continue;
       L.off_T[h] = off;
-      off = align_up(off + ((size_t)L.K << L.half[h]->m) * elem);
+      off = align_up(off + ((size_t)(L.direct >= 0 ? L.Kp : L.K) << L.half[h]->m) * elem);
     }
     if (!a.bits_on_device) {
       L.off_bits = off;
@@ -416,18 +451,11 @@ static Layout make_layout(const Plan& P, const hsf_run_args& a, size_t elem) {
       L.off_pbits = off;
       off = align_up(off + a.n_bitstrings * 8);
     }
-    // grouped gather: >= 4 samples per A row on average, K a multiple of 64 up
-    // to 512 (the row lives in registers), complex64, rows and samples < 2^31
-    // (c5, 4 per row: gather 1.65 -> 1.41 ms, step 3.87 -> 3.74 ms with the
-    // sort beside the trees; c3, 32 per row: 0.35 -> 0.23 ms)
-    const long long nrowsA = 1ll << nA;
-    const char* gg = std::getenv("HSF_GROUPED_GATHER");
-    const bool want = gg ? gg[0] == '1' : (long long)a.n_bitstrings >= 4 * nrowsA;
-    L.grouped = want && P.opts.dtype == HSF_C64 && L.K % 64 == 0 && L.K <= 512 && nA <= 30 &&
-                a.n_bitstrings < (1ull << 31);
-    if (L.grouped) {
+    if (L.direct >= 0) {
       L.off_grp = off;
-      off = align_up(off + (size_t)(3 * nrowsA + 1 + (long long)a.n_bitstrings) * 4);
+      off = align_up(off + (size_t)(3 * L.n_blocks + 1 + (long long)a.n_bitstrings) * 4);
+      L.off_sbits = off;
+      off = align_up(off + (size_t)a.n_bitstrings * 8);
     }
   } else {
     if (P.permuted) {
@@ -715,13 +743,16 @@ static void prep_half(Plan* P, DeviceState* d, const Layout& L, int h, cudaStrea
   const long long K = (long long)L.K;
   const C* leaves = (const C*)(ws + L.off_leaves[h]);
   if (L.bits_mode) {
+    if (h == L.direct) return;  // read in place by the block gather
     C* T = (C*)(ws + L.off_T[h]);
+    const long long ldo = L.direct >= 0 ? L.Kp : K;
     const char* tv = std::getenv("HSF_TRANSPOSE_V1");
     if (sizeof(R) == 4 && m >= 1 && !(tv && tv[0] == '1')) {  // 16 B accesses (c5: 0.43 ms per half before)
-      dim3 g((unsigned)(((1ll << m) + 63) / 64), (unsigned)((K + 31) / 32));
+      dim3 g((unsigned)(((1ll << m) + 63) / 64), (unsigned)((ldo + 31) / 32));
       transpose_fold_c64_kernel<<<g, dim3(32, 8), 0, st>>>((const float2*)leaves, (float2*)T,
-                                                           h == 0 ? (const float2*)d->cp : nullptr, K, 1ll << m);
+                                                           h == 0 ? (const float2*)d->cp : nullptr, K, 1ll << m, ldo);
     } else {
+      if (ldo != K) fail(HSF_ERR_INVALID_ARG, "padded transpose needs the complex64 kernel");
       dim3 g((unsigned)(((1ll << m) + 31) / 32), (unsigned)((K + 31) / 32));
       transpose_fold_kernel<C><<<g, dim3(32, 8), 0, st>>>(leaves, T, h == 0 ? (const C*)d->cp : nullptr, K, 1ll << m);
     }
@@ -759,7 +790,8 @@ static void prep_half(Plan* P, DeviceState* d, const Layout& L, int h, cudaStrea
 
 // Bitstring-run input prep, independent of the path trees (runs on the aux
 // stream beside them): H2D of host bitstrings, the relabelling of
-// non-contiguous partitions, and the bucket sort of the grouped gather.
+// non-contiguous partitions, the bits < 2^n check and the bucket sort of the
+// block gather.
 // Returns the device bitstrings in internal bit order.
 static const unsigned long long* prep_bits(Plan* P, DeviceState* d, const Layout& L, const hsf_run_args& a,
                                            cudaStream_t st) {
@@ -778,17 +810,34 @@ static const unsigned long long* prep_bits(Plan* P, DeviceState* d, const Layout
     CK(cudaGetLastError());
     bits = pb;
   }
-  if (L.grouped) {
-    const long long nrowsA = 1ll << (P->n - nB);
+  // precondition bits < 2^n (hsf.h): flagged in mapped host memory, checked
+  // when the run synchronises
+  check_bits_kernel<<<(unsigned)std::min<long long>((ns + 255) / 256, 148ll * 8), 256, 0, st>>>(bits, ns, P->n,
+                                                                                              d->bad_bits_dev);
+  if (L.direct >= 0) {
+    const long long nblk = L.n_blocks;
     int* counts = (int*)(ws + L.off_grp);
-    int* offs = counts + nrowsA;
-    int* cursor = offs + nrowsA + 1;
-    int* perm = cursor + nrowsA;
-    CK(cudaMemsetAsync(counts, 0, (size_t)nrowsA * 4, st));
-    const unsigned gb = (unsigned)std::min<long long>((ns + 255) / 256, 148ll * 16);
-    bucket_count_kernel<<<gb, 256, 0, st>>>(bits, ns, nB, counts);
-    bucket_scan_kernel<<<1, 1024, 0, st>>>(counts, offs, cursor, nrowsA);
-    bucket_scatter_kernel<<<gb, 256, 0, st>>>(bits, ns, nB, cursor, perm);
+    int* offs = counts + nblk;
+    int* cursor = offs + nblk + 1;
+    int* sidx = cursor + nblk;
+    unsigned long long* sbits = (unsigned long long*)(ws + L.off_sbits);
+    const int rb = L.block_rows == 32 ? 5 : 4;
+    const int shift = L.direct == 1 ? rb : nB + rb;  // blocks of the direct half
+    const unsigned long long kmask = (unsigned long long)nblk - 1ull;
+    CK(cudaMemsetAsync(counts, 0, (size_t)nblk * 4, st));
+    // per-CTA shared histograms of nblk ints (<= 128 KB: nblk <= 2^15, checked in make_layout)
+    const size_t hsm = (size_t)nblk * 4;
+    static bool hattr = false;
+    if (!hattr) {
+      CK(cudaFuncSetAttribute(bucket_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 << 10));
+      CK(cudaFuncSetAttribute(bucket_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 << 10));
+      hattr = true;
+    }
+    const int per_sm = std::max(1, std::min(2, (int)((200u << 10) / std::max<size_t>(hsm, 1))));
+    const unsigned gb = (unsigned)std::max(1ll, std::min<long long>((ns + 4095) / 4096, (long long)per_sm * num_sms()));
+    bucket_count_kernel<<<gb, 1024, hsm, st>>>(bits, ns, shift, kmask, (int)nblk, counts);
+    bucket_scan_kernel<<<1, 1024, 0, st>>>(counts, offs, cursor, nblk);
+    bucket_scatter_kernel<<<gb, 1024, hsm, st>>>(bits, ns, shift, kmask, (int)nblk, cursor, sidx, sbits);
     CK(cudaGetLastError());
   }
   return bits;
@@ -814,34 +863,72 @@ static void run_core_bits(Plan* P, DeviceState* d, const Layout& L, const hsf_ru
       tw.off[u] = P->trail_off[u];
     }
   }
-  if (sizeof(R) == 4 && L.grouped) {  // bucket sort done by prep_bits
-    const long long nrowsA = 1ll << (P->n - nB);
-    const int* offs = (const int*)(ws + L.off_grp) + nrowsA;
-    const int* perm = offs + 2 * nrowsA + 1;
-    const unsigned gw = (unsigned)std::min<long long>((nrowsA + 7) / 8, 148ll * 64);  // 8 warps per CTA
-    const float4* A4 = (const float4*)AT;
-    const float4* B4 = (const float4*)BT;
-    switch (K / 64) {
-      case 1: gather_grouped_c64_kernel<1><<<gw, 256, 0, st>>>(A4, B4, bits, offs, perm, (float2*)out, nrowsA, nB, tw,
-                                                               (const float2*)d->trail, a.accumulate); break;
-      case 2: gather_grouped_c64_kernel<2><<<gw, 256, 0, st>>>(A4, B4, bits, offs, perm, (float2*)out, nrowsA, nB, tw,
-                                                               (const float2*)d->trail, a.accumulate); break;
-      case 4: gather_grouped_c64_kernel<4><<<gw, 256, 0, st>>>(A4, B4, bits, offs, perm, (float2*)out, nrowsA, nB, tw,
-                                                               (const float2*)d->trail, a.accumulate); break;
-      case 8: gather_grouped_c64_kernel<8><<<gw, 256, 0, st>>>(A4, B4, bits, offs, perm, (float2*)out, nrowsA, nB, tw,
-                                                               (const float2*)d->trail, a.accumulate); break;
-      default: {  // K = 192, 320, 384, 448: the plain vectorised gather
-        gather_dot_c64_vec_kernel<<<(unsigned)blocks, 256, 0, st>>>(A4, B4, bits, (float2*)out, ns, K, nB, tw,
-                                                                    (const float2*)d->trail, a.accumulate);
+  const unsigned long long maskA = (P->n - nB >= 64) ? ~0ull : (1ull << (P->n - nB)) - 1ull;
+  if (sizeof(R) == 4 && L.direct >= 0) {  // bucket sort done by prep_bits
+    const long long nblk = L.n_blocks;
+    BlockGatherParams bp{};
+    bp.D = (const float2*)(ws + L.off_leaves[L.direct]);
+    bp.ldD = 1ll << L.half[L.direct]->m;
+    bp.K = K;
+    bp.cpD = L.direct == 0 ? (const float2*)d->cp : nullptr;
+    bp.T = (const float4*)(ws + L.off_T[1 - L.direct]);
+    bp.offs = (const int*)(ws + L.off_grp) + nblk;
+    bp.sidx = bp.offs + 2 * nblk + 1;
+    bp.sbits = (const unsigned long long*)(ws + L.off_sbits);
+    bp.out = (float2*)out;
+    bp.n_blocks = nblk;
+    bp.n_low = nB;
+    bp.direct_b = L.direct;
+    bp.maskA = maskA;
+    bp.maskB = (1ull << nB) - 1ull;
+    bp.accumulate = a.accumulate;
+    if (const char* e = std::getenv("HSF_GATHER_DEBUG")) bp.debug = std::atoi(e);
+    const size_t smem = (size_t)L.block_rows * L.Kp * sizeof(float2);
+    auto launch = [&](auto kern, int nt) {
+      static bool attr = false;  // per instantiation
+      if (!attr) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 32 * 512 * 8));
+        attr = true;
       }
+      int per_sm = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nt, smem));
+      const long long grid = std::min<long long>(nblk, (long long)std::max(1, per_sm) * num_sms());
+      kern<<<(unsigned)grid, nt, smem, st>>>(bp, tw, (const float2*)d->trail);
+    };
+    // tuning (HSF_GATHER_CFG = 100 * (RB == 32 ? 3 : 1) + 10 * MINB + U)
+    // default U by row length (c5, Kp = 128: U = 4 -> gather 1.09 ms, U = 2 1.38;
+    // c3, Kp = 256: U = 2 -> 0.25 ms, U = 4 0.45 -- 64 float4 of rows per
+    // thread spill at 4 CTAs per SM)
+    const int cfg = gather_cfg(), MB = (cfg / 10) % 10;
+    const int U = std::getenv("HSF_GATHER_CFG") ? cfg % 10 : L.Kp <= 64 ? 8 : L.Kp == 128 ? 4 : L.Kp == 256 ? 2 : 1;
+#define HSF_GB(NF, U_, RB, MB_) launch(gather_block_c64_kernel<NF, U_, RB, 256, MB_>, 256)
+#define HSF_GB_MB(NF, U_, RB)     \
+  if (MB == 2) HSF_GB(NF, U_, RB, 2); \
+  else if (MB == 3) HSF_GB(NF, U_, RB, 3); \
+  else HSF_GB(NF, U_, RB, 4);
+#define HSF_GB_RB(NF, U_)            \
+  if (L.block_rows == 16) {          \
+    HSF_GB_MB(NF, U_, 16)            \
+  } else {                           \
+    HSF_GB_MB(NF, U_, 32)            \
+  }
+    switch (L.Kp) {
+      case 64: if (U == 8) { HSF_GB_RB(1, 8) } else { HSF_GB_RB(1, 4) } break;
+      case 128: if (U == 8) { HSF_GB_RB(2, 8) } else if (U == 4) { HSF_GB_RB(2, 4) } else { HSF_GB_RB(2, 2) } break;
+      case 256: if (U == 4) { HSF_GB_RB(4, 4) } else { HSF_GB_RB(4, 2) } break;
+      case 512: if (U == 2) { HSF_GB_RB(8, 2) } else { HSF_GB_RB(8, 1) } break;
+#undef HSF_GB_RB
+#undef HSF_GB_MB
+#undef HSF_GB
+      default: fail(HSF_ERR_INVALID_ARG, "block gather row length");
     }
   } else if (sizeof(R) == 4 && K % 64 == 0) {
     gather_dot_c64_vec_kernel<<<(unsigned)blocks, 256, 0, st>>>((const float4*)AT, (const float4*)BT, bits,
                                                                 (float2*)out, ns, K, nB, tw, (const float2*)d->trail,
-                                                                a.accumulate);
+                                                                a.accumulate, maskA);
   } else {
     gather_dot_kernel<C><<<(unsigned)blocks, 256, 0, st>>>(AT, BT, bits, out, ns, K, nB, tw, (const C*)d->trail,
-                                                           a.accumulate);
+                                                           a.accumulate, maskA);
   }
   CK(cudaGetLastError());
 }
@@ -1036,7 +1123,13 @@ static void run(Plan* P, const hsf_run_args& a) {
     } else {
       run_all<double>(P, d, L, a, st, timed);
     }
-    if (timed || !a.out_on_device) CK(cudaStreamSynchronize(st));
+    if (timed || !a.out_on_device) {
+      CK(cudaStreamSynchronize(st));
+      if (L.bits_mode && *(volatile unsigned int*)d->bad_bits) {
+        *d->bad_bits = 0;
+        fail(HSF_ERR_INVALID_ARG, "bitstrings must be < 2^n (a sample has a bit set at or above qubit n)");
+      }
+    }
     if (timed) {
       float tA, tB, tprep, tcore, ttot;
       CK(cudaEventElapsedTime(&tA, d->ev_t0, d->ev[1]));

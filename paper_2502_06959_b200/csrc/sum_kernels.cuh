@@ -46,8 +46,11 @@ __global__ void transpose_fold_kernel(const C* __restrict__ in, C* __restrict__ 
 // the (k, k+1) pair of row m sits in slot (k / 2) ^ ((m / 2) & 15), so both
 // the load-side 8 B writes and the store-side 16 B reads run at the minimum
 // wavefront count.
+// ldo: output row stride (>= K); columns [K, ldo) of rows < M are written as
+// zeros when the grid spans them (gridDim.y = ldo / 32, the block gather's
+// power-of-two padded rows).
 __global__ void transpose_fold_c64_kernel(const float2* __restrict__ in, float2* __restrict__ out,
-                                          const float2* __restrict__ cp, long long K, long long M) {
+                                          const float2* __restrict__ cp, long long K, long long M, long long ldo) {
   __shared__ __align__(16) float2 S[64][32];
   const long long m0 = (long long)blockIdx.x * 64, k0 = (long long)blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
@@ -81,11 +84,11 @@ __global__ void transpose_fold_c64_kernel(const float2* __restrict__ in, float2*
     const long long m = m0 + mr, k = k0 + 2 * kp;
     const float4 v = *reinterpret_cast<const float4*>(&S[mr][2 * (kp ^ ((mr >> 1) & 15))]);
     if (m < M) {
-      if (k + 1 < K && (K & 1) == 0)
-        *reinterpret_cast<float4*>(out + m * K + k) = v;
+      if (k + 1 < ldo && (ldo & 1) == 0)
+        *reinterpret_cast<float4*>(out + m * ldo + k) = v;
       else {
-        if (k < K) out[m * K + k] = make_float2(v.x, v.y);
-        if (k + 1 < K) out[m * K + k + 1] = make_float2(v.z, v.w);
+        if (k < ldo) out[m * ldo + k] = make_float2(v.x, v.y);
+        if (k + 1 < ldo) out[m * ldo + k + 1] = make_float2(v.z, v.w);
       }
     }
   }
@@ -149,14 +152,14 @@ template <typename C>
 __global__ void gather_dot_kernel(const C* __restrict__ AT, const C* __restrict__ BT,
                                   const unsigned long long* __restrict__ bits, C* __restrict__ out,
                                   long long n_samples, long long K, int n_low, const TrailParams tw,
-                                  const C* __restrict__ trail, int accumulate) {
+                                  const C* __restrict__ trail, int accumulate, unsigned long long maskA) {
   const int lane = threadIdx.x & 31;
   const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
   const unsigned long long maskB = (1ull << n_low) - 1ull;
   for (long long s = warp; s < n_samples; s += nwarps) {
     unsigned long long b = bits[s];
-    const C* a = AT + (long long)(b >> n_low) * K;
+    const C* a = AT + (long long)((b >> n_low) & maskA) * K;
     const C* bb = BT + (long long)(b & maskB) * K;
     C acc;
     acc.x = 0;
@@ -183,7 +186,8 @@ __global__ void gather_dot_kernel(const C* __restrict__ AT, const C* __restrict_
 __global__ void gather_dot_c64_vec_kernel(const float4* __restrict__ AT, const float4* __restrict__ BT,
                                           const unsigned long long* __restrict__ bits, float2* __restrict__ out,
                                           long long n_samples, long long K, int n_low, const TrailParams tw,
-                                          const float2* __restrict__ trail, int accumulate) {
+                                          const float2* __restrict__ trail, int accumulate,
+                                          unsigned long long maskA) {
   const int lane = threadIdx.x & 31;
   const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -191,7 +195,7 @@ __global__ void gather_dot_c64_vec_kernel(const float4* __restrict__ AT, const f
   const long long K2 = K >> 1;  // float4 per row
   for (long long s = warp; s < n_samples; s += nwarps) {
     unsigned long long b = bits[s];
-    const float4* a = AT + (long long)(b >> n_low) * K2;
+    const float4* a = AT + (long long)((b >> n_low) & maskA) * K2;
     const float4* bb = BT + (long long)(b & maskB) * K2;
     float re = 0.f, im = 0.f;
     for (long long p = lane; p < K2; p += 32) {
@@ -219,17 +223,45 @@ __global__ void gather_dot_c64_vec_kernel(const float4* __restrict__ AT, const f
   }
 }
 
-// ------------------------------------------------------ K6, grouped by A row
-// When many samples share an A row (c3: 2^20 samples over 2^15 rows, ~32 per
-// row; both operands L2-resident, so the plain gather is bound by L2->SM
-// traffic), the samples are bucketed by A row (counting sort: count, one-CTA
-// scan, scatter of sample indices) and one warp per row keeps the row in
-// registers while it streams its samples' B rows: A traffic drops from one
-// row per sample to one row per distinct row.
-__global__ void bucket_count_kernel(const unsigned long long* __restrict__ bits, long long n, int n_low,
-                                    int* __restrict__ counts) {
+// Samples with bits at or above n violate hsf_run's precondition: flag them
+// (word in mapped host memory, read when the run synchronises).  Every gather
+// masks its row indices, so such a sample never reads out of bounds.
+__global__ void check_bits_kernel(const unsigned long long* __restrict__ bits, long long n, int n_qubits,
+                                  unsigned int* __restrict__ flag) {
+  unsigned long long acc = 0;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    atomicAdd(&counts[bits[i] >> n_low], 1);
+    acc |= bits[i];
+  if (n_qubits < 64 && __any_sync(0xffffffffu, (acc >> n_qubits) != 0ull) && (threadIdx.x & 31) == 0)
+    atomicOr(flag, 1u);
+}
+
+// ------------------------------------------------------- K6b, block gather
+// The bitstring path-sum amp[s] = sum_p A'[iA(s)][p] B[iB(s)][p] (a3
+// folded into A') reads one side -- the "direct" half D, whose path tree
+// finishes last -- straight from its node-major leaves [K][2^mD]: the samples
+// are bucketed by the 32-row block of their D row (counting sort: count, one
+// CTA scan, scatter of sample indices), one CTA per block stages the block's
+// 32 x K amplitudes in shared memory (K-row segments of 256 B, coalesced),
+// and each sample then reads only its row of the other half, transposed to
+// [2^mT][Kp] (Kp = K padded to 2*G*NF with zeros).  D needs no transpose, so
+// the kernel follows D's last simulator pass directly; traffic = D's leaves
+// once + one Kp row of T per sample.
+// Counting sort of the samples by block, aggregated per CTA: each CTA takes a
+// contiguous chunk of the samples and histograms it in shared memory (shared
+// atomics), then adds its non-zero bucket counts to the global counts -- one
+// global atomic per (CTA, bucket) instead of one per sample (c3's 1024
+// buckets hold ~1000 samples each: per-sample atomics serialised at L2).
+__global__ void __launch_bounds__(1024) bucket_count_kernel(const unsigned long long* __restrict__ bits, long long n,
+                                                            int shift, unsigned long long kmask, int nbk,
+                                                            int* __restrict__ counts) {
+  extern __shared__ int h[];
+  for (int i = threadIdx.x; i < nbk; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const long long c0 = n * blockIdx.x / gridDim.x, c1 = n * (blockIdx.x + 1) / gridDim.x;
+  for (long long i = c0 + threadIdx.x; i < c1; i += blockDim.x) atomicAdd(&h[(bits[i] >> shift) & kmask], 1);
+  __syncthreads();
+  for (int i = threadIdx.x; i < nbk; i += blockDim.x)
+    if (h[i]) atomicAdd(&counts[i], h[i]);
 }
 
 // exclusive scan of counts[0..n) into offs[0..n] (offs[n] = total) and
@@ -291,97 +323,160 @@ __global__ void __launch_bounds__(1024) bucket_scan_kernel(const int* __restrict
   }
 }
 
-__global__ void bucket_scatter_kernel(const unsigned long long* __restrict__ bits, long long n, int n_low,
-                                      int* __restrict__ cursor, int* __restrict__ perm) {
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    perm[atomicAdd(&cursor[bits[i] >> n_low], 1)] = (int)i;
+// scatter of the samples into block order (same chunks as the count): each
+// CTA reserves its range in every bucket it touches (one global atomic per
+// (CTA, bucket)), then places its samples with shared atomics; sidx[pos] =
+// sample index, sbits[pos] = its bitstring (the gather reads both coalesced,
+// no dependent lookup).  Order within a bucket is unspecified.
+__global__ void __launch_bounds__(1024) bucket_scatter_kernel(const unsigned long long* __restrict__ bits, long long n,
+                                                              int shift, unsigned long long kmask, int nbk,
+                                                              int* __restrict__ cursor, int* __restrict__ sidx,
+                                                              unsigned long long* __restrict__ sbits) {
+  extern __shared__ int h[];
+  for (int i = threadIdx.x; i < nbk; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const long long c0 = n * blockIdx.x / gridDim.x, c1 = n * (blockIdx.x + 1) / gridDim.x;
+  for (long long i = c0 + threadIdx.x; i < c1; i += blockDim.x) atomicAdd(&h[(bits[i] >> shift) & kmask], 1);
+  __syncthreads();
+  for (int i = threadIdx.x; i < nbk; i += blockDim.x)
+    if (h[i]) h[i] = atomicAdd(&cursor[i], h[i]);
+  __syncthreads();
+  for (long long i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+    const unsigned long long b = bits[i];
+    const int pos = atomicAdd(&h[(b >> shift) & kmask], 1);
+    sidx[pos] = (int)i;
+    sbits[pos] = b;
+  }
 }
 
-// one warp per A row r: the row (T float4 per lane, K = 64*T complex) stays in
-// registers; the row's samples are taken two at a time (both B rows in flight)
-template <int T>
-__global__ void gather_grouped_c64_kernel(const float4* __restrict__ AT, const float4* __restrict__ BT,
-                                          const unsigned long long* __restrict__ bits, const int* __restrict__ offs,
-                                          const int* __restrict__ perm, float2* __restrict__ out, long long n_rows,
-                                          int n_low, const TrailParams tw, const float2* __restrict__ trail,
-                                          int accumulate) {
-  constexpr int K2 = 32 * T;  // float4 per operand row
-  const int lane = threadIdx.x & 31;
-  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
-  const unsigned long long maskB = (1ull << n_low) - 1ull;
-  for (long long r = warp; r < n_rows; r += nwarps) {
-    const int beg = offs[r], end = offs[r + 1];
+
+struct BlockGatherParams {
+  const float2* D;       // direct half's leaves [K][ldD]
+  long long ldD;         // 2^mD
+  long long K;           // paths (rows of D; columns of T below Kp are these)
+  const float2* cpD;     // c_p of the direct half when it is A (else nullptr)
+  const float4* T;       // other half, [2^mT][Kp] complex64 (Kp / 2 float4 per row)
+  const int* offs;       // [n_blocks + 1] sample offsets per block
+  const int* sidx;       // sample indices in block order
+  const unsigned long long* sbits;  // their bitstrings
+  float2* out;
+  long long n_blocks;
+  int n_low;             // n_B
+  int direct_b;          // 1: D = half B (index bits & maskB), 0: D = half A (index bits >> n_B)
+  unsigned long long maskA, maskB;
+  int accumulate;
+  int debug;             // tuning only: 1 skips the staging, 2 skips the samples
+};
+
+// One warp per sample, NF float4 of the K-row per lane (Kp = 64 * NF), U
+// samples in flight per warp, RB rows of the direct half per block, NT
+// threads, MINB CTAs per SM.  Warp w takes the w-th contiguous share of the
+// block's samples, 32 at a time: lane i loads sample i's metadata (the
+// block-ordered arrays, coalesced), then the warp walks them U at a time,
+// each round one dependent load of U rows of T (addresses by shuffle).
+// Shared memory S[RB][F] float4 (F = Kp / 2), slot f of row r at
+// f ^ (r & (F - 1)): the per-sample reads (one row, consecutive slots) run at
+// the minimum wavefront count.
+template <int NF, int U, int RB, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) gather_block_c64_kernel(const BlockGatherParams p, const TrailParams tw,
+                                                                    const float2* __restrict__ trail) {
+  constexpr int F = 32 * NF;  // float4 per row (Kp / 2)
+  constexpr int NW = NT / 32;
+  static_assert(RB == 16 || RB == 32, "block rows");
+  extern __shared__ float4 S[];  // [RB][F]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (long long blk = blockIdx.x; blk < p.n_blocks; blk += gridDim.x) {
+    const int beg = p.offs[blk], end = p.offs[blk + 1];
     if (beg == end) continue;
-    float4 a[T];
+    __syncthreads();  // the previous block's readers are done with S
+    // ---- fill: rows r0 .. r0+RB-1 of D; a warp load covers 32 / RB k rows
+    const long long r0 = blk * RB;
+    constexpr int KPW = 32 / RB;
+    const int r = lane % RB, kq = lane / RB;
+    for (int k0 = KPW * warp; k0 < 2 * F && !(p.debug & 1); k0 += KPW * NW * 4) {
+      float2 v[4];
 #pragma unroll
-    for (int t = 0; t < T; ++t) a[t] = __ldg(&AT[r * K2 + lane + 32 * t]);
-    // the row's sample indices and bitstrings, up to 32 at a time, loaded by
-    // the lanes in parallel and broadcast (no dependent perm -> bits -> B
-    // chain per sample pair)
-    for (int jb = beg; jb < end; jb += 32) {
-    const int nb = end - jb < 32 ? end - jb : 32;
-    int pl = 0;
-    unsigned long long bl = 0;
-    if (lane < nb) {
-      pl = perm[jb + lane];
-      bl = bits[pl];
+      for (int q = 0; q < 4; ++q) {
+        const long long k = k0 + KPW * NW * q + kq;
+        v[q] = (k < p.K) ? __ldg(&p.D[k * p.ldD + r0 + r]) : make_float2(0.f, 0.f);
+        if (p.cpD && k < p.K) v[q] = cmul(v[q], __ldg(&p.cpD[k]));
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int k = k0 + KPW * NW * q + kq;
+        if (RB == 16) {  // lanes r and r + 16 hold k and k + 1 (k even)
+          const float ox = __shfl_down_sync(0xffffffffu, v[q].x, 16), oy = __shfl_down_sync(0xffffffffu, v[q].y, 16);
+          if (kq == 0 && k < 2 * F) S[r * F + ((k >> 1) ^ (r & (F - 1)))] = make_float4(v[q].x, v[q].y, ox, oy);
+        } else {  // RB == 32: one k per warp load; pairs are written as halves
+          if (k < 2 * F) reinterpret_cast<float2*>(S)[2 * (r * F + ((k >> 1) ^ (r & (F - 1)))) + (k & 1)] = v[q];
+        }
+      }
     }
-    // 4 samples per step: 4 B rows in flight per warp
-    for (int jj = 0; jj < nb; jj += 4) {
-      int ii[4];
-      unsigned long long bb[4];
-      float4 y[4][T];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int src = jj + u < nb ? jj + u : jj;  // warp-uniform
-        ii[u] = __shfl_sync(0xffffffffu, pl, src);
-        bb[u] = __shfl_sync(0xffffffffu, bl, src);
-        const float4* q = BT + (long long)(bb[u] & maskB) * K2;
-#pragma unroll
-        for (int t = 0; t < T; ++t) y[u][t] = __ldg(&q[lane + 32 * t]);
+    __syncthreads();
+    if (p.debug & 2) continue;
+    // ---- samples: warp w's share [s0, s1)
+    const int cnt = end - beg;
+    const int s0 = beg + (int)((long long)cnt * warp / NW), s1 = beg + (int)((long long)cnt * (warp + 1) / NW);
+    for (int jb = s0; jb < s1; jb += 32) {
+      const int nb = min(32, s1 - jb);
+      int sid = 0;
+      unsigned long long sbv = 0;
+      if (lane < nb) {
+        sid = p.sidx[jb + lane];
+        sbv = p.sbits[jb + lane];
       }
-      float re[4], im[4];
+      for (int jj = 0; jj < nb; jj += U) {
+        float4 x[U][NF];
+        unsigned long long bw[U];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        re[u] = 0.f;
-        im[u] = 0.f;
+        for (int u = 0; u < U; ++u) {
+          bw[u] = __shfl_sync(0xffffffffu, sbv, min(jj + u, nb - 1));
+          const unsigned long long iT = p.direct_b ? (bw[u] >> p.n_low) & p.maskA : bw[u] & p.maskB;
+          const float4* q = p.T + (long long)iT * F;
 #pragma unroll
-        for (int t = 0; t < T; ++t) {
-          const float4 x = a[t];
-          re[u] = fmaf(x.x, y[u][t].x, fmaf(-x.y, y[u][t].y, re[u]));
-          im[u] = fmaf(x.x, y[u][t].y, fmaf(x.y, y[u][t].x, im[u]));
-          re[u] = fmaf(x.z, y[u][t].z, fmaf(-x.w, y[u][t].w, re[u]));
-          im[u] = fmaf(x.z, y[u][t].w, fmaf(x.w, y[u][t].z, im[u]));
+          for (int t = 0; t < NF; ++t) x[u][t] = __ldg(&q[lane + 32 * t]);
         }
-      }
+        float re[U], im[U];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
+        for (int u = 0; u < U; ++u) {
+          re[u] = 0.f;
+          im[u] = 0.f;
+          const int rd = (int)((p.direct_b ? bw[u] & p.maskB : (bw[u] >> p.n_low) & p.maskA) & (RB - 1));
+          const float4* srow = S + rd * F;
+          const int sw = rd & (F - 1);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          re[u] += __shfl_xor_sync(0xffffffffu, re[u], o);
-          im[u] += __shfl_xor_sync(0xffffffffu, im[u], o);
+          for (int t = 0; t < NF; ++t) {
+            const float4 y = srow[(lane + 32 * t) ^ sw];
+            const float4 a = p.direct_b ? x[u][t] : y;  // a = A' (c_p folded), c = B
+            const float4 c = p.direct_b ? y : x[u][t];
+            re[u] = fmaf(a.x, c.x, fmaf(-a.y, c.y, re[u]));
+            im[u] = fmaf(a.x, c.y, fmaf(a.y, c.x, im[u]));
+            re[u] = fmaf(a.z, c.z, fmaf(-a.w, c.w, re[u]));
+            im[u] = fmaf(a.z, c.w, fmaf(a.w, c.z, im[u]));
+          }
         }
-      const int nv = nb - jj < 4 ? nb - jj : 4;
-      if (lane < nv) {  // lane u writes sample jj + u
-        int idx = ii[0];
-        unsigned long long bs = bb[0];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            re[u] += __shfl_xor_sync(0xffffffffu, re[u], o);
+            im[u] += __shfl_xor_sync(0xffffffffu, im[u], o);
+          }
+        // lane jj + u (the holder of sample jj + u's metadata) writes it
         float2 v = make_float2(re[0], im[0]);
 #pragma unroll
-        for (int u = 1; u < 4; ++u)
-          if (lane == u) {
-            idx = ii[u];
-            bs = bb[u];
-            v = make_float2(re[u], im[u]);
+        for (int u = 1; u < U; ++u)
+          if (lane == jj + u) v = make_float2(re[u], im[u]);
+        if (lane >= jj && lane < jj + U && lane < nb) {
+          if (tw.n) v = cmul(v, trail_weight(tw, trail, sbv));
+          if (p.accumulate) {
+            const float2 w = p.out[sid];
+            v.x += w.x;
+            v.y += w.y;
           }
-        float2 res = tw.n ? cmul(v, trail_weight(tw, trail, bs)) : v;
-        if (accumulate) {
-          res.x += out[idx].x;
-          res.y += out[idx].y;
+          p.out[sid] = v;
         }
-        out[idx] = res;
       }
-    }
     }
   }
 }

@@ -253,6 +253,31 @@ def test_c5_full_run_norm_sampled(torch):
     assert 0.8 < m < 1.2
 
 
+def test_c5_as_benched_elementwise(torch):
+    # c5 exactly as bench.py times it (all 256 paths: folded tree, the block
+    # gather over all 2^22 samples) against the oracle's recombine_bits over
+    # all paths on >= 2^14 outputs: 2^13 random samples plus every sample of
+    # 64 random 32-row blocks of half B (~128 samples per block, rows with
+    # several samples each).  Oracle: every path from scratch in forked workers
+    # (oracle/parallel.py), only the sampled rows kept.
+    from oracle import parallel as OP
+    inst = make_config("c5")
+    got, P = gpu_bits(torch, inst, inst.bitstrings)
+    bits = inst.bitstrings
+    rng = np.random.default_rng(11)
+    blk = (bits & np.uint64((1 << inst.n_low) - 1)) >> np.uint64(5)
+    pick_blk = rng.choice(1 << (inst.n_low - 5), 64, replace=False).astype(np.uint64)
+    sel = np.union1d(rng.choice(len(bits), 9000, replace=False), np.nonzero(np.isin(blk, pick_blk))[0])
+    assert len(sel) >= 1 << 14
+    rows = bits[sel] & np.uint64((1 << inst.n_low) - 1)
+    assert np.max(np.unique(rows, return_counts=True)[1]) >= 2
+    n, g = O.parse_circuit(inst.text)
+    Po = O.plan(n, g, inst.n_low, inst.blocks)
+    ref = OP.bits_amplitudes(Po, bits[sel], inst.n_low)
+    md, rel = check(got[sel], ref, "c64")
+    print(f"c5 as benched: {len(sel)} samples, max|d|={md:.3e} relL2={rel:.3e}, procs={OP.n_procs()}")
+
+
 # --------------------------------------------------- tensor-core path-sum
 @pytest.mark.parametrize("name", ["c1", "c2", "c4", "c5"])
 def test_twins_full_output_bf16x3(torch, name):
@@ -563,12 +588,13 @@ def test_fused_reduce_scatter_two_processes_ipc(torch):
 
 
 @pytest.mark.parametrize("name,path_range", [("c3", None), ("c3", (16, 48)), ("c5", None), ("c5", (3, 9))])
-@pytest.mark.parametrize("grouped", ["0", "1"])
-def test_grouped_gather(torch, name, path_range, grouped, monkeypatch):
-    # bitstring path-sum bucketed by A row (counting sort + one warp per row)
-    # vs the per-sample gather: both against the oracle's partial sums, with
-    # duplicates and unaligned (unfolded) ranges
-    monkeypatch.setenv("HSF_GROUPED_GATHER", grouped)
+@pytest.mark.parametrize("direct", ["-1", "0", "1"])
+def test_block_gather(torch, name, path_range, direct, monkeypatch):
+    # bitstring path-sum: the block gather reading half B (direct=1) or half A
+    # (direct=0, c_p applied while staging) from its leaves, or the per-sample
+    # gather (-1), against the oracle's partial sums, with duplicates and
+    # unaligned (unfolded, K not a power of two) ranges
+    monkeypatch.setenv("HSF_GATHER_DIRECT", direct)
     inst = make_config(name, twin=True)
     bits = np.concatenate([inst.bitstrings, inst.bitstrings[:300]])  # duplicates
     n, g = O.parse_circuit(inst.text)
@@ -578,6 +604,24 @@ def test_grouped_gather(torch, name, path_range, grouped, monkeypatch):
     ref = O.recombine_bits(A, B, c, bits, inst.n_low)
     got, _ = gpu_bits(torch, inst, bits, path_range=path_range)
     check(got, ref, inst.dtype)
+
+
+def test_bitstrings_out_of_range(torch):
+    # precondition bits < 2^n: host samples are rejected by the binding; device
+    # samples are flagged by the library when the run synchronises (no
+    # out-of-bounds access either way)
+    from paper_2502_06959_b200 import Plan
+    from paper_2502_06959_b200.hsf import HsfError
+    inst = make_config("c5", twin=True)
+    P = Plan(inst.text, inst.n_low, inst.blocks)
+    bad = inst.bitstrings.copy()
+    bad[7] |= np.uint64(1) << np.uint64(inst.n)
+    with pytest.raises(ValueError):
+        P.run(np.empty(len(bad), np.complex64), bitstrings=bad)
+    out = torch.empty(len(bad), dtype=torch.complex64, device="cuda")
+    with pytest.raises(HsfError):
+        P.run(out, bitstrings=torch.from_numpy(bad.view(np.int64)).cuda(), timings=True)
+    P.run(out, bitstrings=torch.from_numpy(inst.bitstrings.view(np.int64)).cuda(), timings=True)  # plan still usable
 
 
 @pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])

@@ -420,3 +420,20 @@ def test_table2_counts_from_block_finder(row):
     found, ncasc = O.find_cascades(g, nb)
     assert ncasc == lj
     assert len(found) == blocks
+
+
+@pytest.mark.parametrize("procs", [1, 3])
+def test_parallel_driver_matches_direct(procs):
+    # oracle/parallel.py: forked workers running simulate_path on path chunks,
+    # sampled rows only -> recombine_bits; must equal the direct naive HSF
+    from oracle import parallel as OP
+    inst = make_config("c5", twin=True)
+    n, g = O.parse_circuit(inst.text)
+    P = O.plan(n, g, inst.n_low, inst.blocks)
+    bits = np.concatenate([inst.bitstrings[:500], inst.bitstrings[:50]])
+    ref = O.hsf(n, g, inst.n_low, inst.blocks, bits=bits)
+    got = OP.bits_amplitudes(P, bits, inst.n_low, procs=procs)
+    assert np.abs(got - ref).max() <= 1e-14
+    A, B, c = OP.half_state_rows(P, [0, 3], [1], 2, 7, procs=procs)
+    A2, B2, c2 = O.half_states(P, 2, 7)
+    assert np.array_equal(A, A2[[0, 3]]) and np.array_equal(B, B2[[1]]) and np.array_equal(c, c2)
