@@ -175,6 +175,12 @@ typedef struct {
   int32_t head_units_a, head_units_b;          /* leading units whose factors on that half act on
                                                   computational-basis qubits: scalars folded into
                                                   c_p in full-output tensor-core runs (head fold) */
+  double tree_flops_a, tree_flops_b;           /* floating-point operations of the simulator passes
+                                                  for all paths (FMA = 2; dense k-qubit op 8*2^k,
+                                                  register-pass 1-qubit gate 16, diagonal 6 per
+                                                  amplitude): the compute-roofline numerator */
+  double fold_tree_flops_a, fold_tree_flops_b; /* same for the bitstring folded tree (0 if none) */
+  double tail_tree_flops_a, tail_tree_flops_b; /* same for the half-sided fold trees (0 if none) */
 } hsf_plan_info;
 
 /* Pointers in *info stay valid until hsf_plan_free. */
@@ -233,6 +239,37 @@ typedef struct {
  * been enqueued if out_on_device, after completion otherwise.  The plan owns
  * its device tables and workspace (grown on demand, freed by hsf_plan_free). */
 hsf_status hsf_run(hsf_plan_t* plan, const hsf_run_args* args);
+
+/* What hsf_run does for these args (the launch sequence make_layout picks)
+ * and the method's algorithmic work of each phase -- the numerators of the
+ * rooflines bench.py reports.  Bytes count each operand / result element
+ * once at its storage width; flops count FMA = 2. */
+typedef enum {
+  HSF_CORE_SIMT = 0,          /* K5s: CUDA-core complex GEMM (fp32 / fp64) */
+  HSF_CORE_TC_PAIR = 1,       /* K5: tcgen05 CTA-pair GEMM (cta_group::2) */
+  HSF_CORE_TC_SINGLE = 2,     /* K5: tcgen05 single-CTA GEMM (<= 128 rows) */
+  HSF_CORE_TC_SWAPPED = 3,    /* K5w: narrow-N swapped GEMM + transpose (prefix outputs) */
+  HSF_CORE_GATHER = 4,        /* K6: per-sample gather (both halves transposed) */
+  HSF_CORE_BLOCK_GATHER = 5   /* K6b: block gather (one half read from its leaves) */
+} hsf_core_kind;
+
+typedef struct {
+  int32_t core;               /* hsf_core_kind */
+  int32_t direct_half;        /* block gather: half read from its leaves (0 A, 1 B); else -1 */
+  int32_t tree_variant_a, tree_variant_b; /* 0 full tree, 1 bitstring fold, 2 half-sided fold */
+  uint64_t K;                 /* columns of the path-sum (tree paths of the range) */
+  uint64_t rows;              /* full output: rows of half A evaluated; bitstrings: samples */
+  int32_t tc_products;        /* split-bf16 / tf32 products per real MMA (0 = SIMT / gather) */
+  int32_t kernel_launches;    /* kernels of the run's captured CUDA graph (-1: the run is not
+                                 graph-captured yet, or launches directly) */
+  double sim_bytes[2], sim_flops[2];    /* per half: simulator passes over this range */
+  double prep_bytes;          /* operand preparation (transposes / split-bf16 planes) */
+  double core_bytes;          /* path-sum kernel: operands read once + result written */
+  double core_flops_useful;   /* 8 K per output amplitude (complex multiply-add) */
+  double core_flops_executed; /* tensor-core flops actually issued (split products, padding) */
+} hsf_run_desc;
+
+hsf_status hsf_run_describe(const hsf_plan_t* plan, const hsf_run_args* args, hsf_run_desc* out);
 
 /* Bytes of device workspace hsf_run would need for these args (0 on error). */
 size_t hsf_workspace_bytes(const hsf_plan_t* plan, const hsf_run_args* args);

@@ -115,6 +115,7 @@ struct Half {
   double est_ms = 0;                 // planner's cost-model estimate of the tree (all paths)
   int last_gate_level = 0;           // deepest level holding a local gate
   double tree_bytes = 0;             // state bytes the tile passes read + write (all paths)
+  double tree_flops = 0;             // their floating-point operations (all paths; FMA = 2)
 };
 
 struct Plan {

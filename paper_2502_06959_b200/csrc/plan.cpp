@@ -1040,11 +1040,22 @@ static void build_half(Plan& P, int h, const std::vector<SchedItem>& order, int 
   // algorithmic traffic of the tree: every pass reads and writes each output
   // node's state once (the first pass from |0...0> reads nothing)
   H.tree_bytes = 0;
+  H.tree_flops = 0;
   {
     const double S = std::ldexp(1.0, H.m) * (P.opts.dtype == HSF_C64 ? 8.0 : 16.0);
     for (const auto& tr : H.trans) {
       const double N = (double)range_prod(R, 0, tr.level_out);
       H.tree_bytes += N * S * (2.0 * (double)tr.passes.size() - (tr.level_in < 0 ? 1.0 : 0.0));
+      // FP32/FP64 flops per amplitude (FMA = 2): a dense k-qubit op 8 * 2^k
+      // (2^k complex multiply-adds per output amplitude), a 1-qubit gate of a
+      // register pass 16, a diagonal 6 (one complex multiply)
+      double fl = 0;
+      for (const auto& ps : tr.passes)
+        for (int64_t i = ps.op_begin; i < ps.op_end; ++i) {
+          const DevOp& d = H.dev_ops[i];
+          fl += d.kind == OP_DENSE ? 8.0 * std::ldexp(1.0, d.k) : d.kind == OP_R1 ? 16.0 : d.kind == OP_DIAG ? 6.0 : 0.0;
+        }
+      H.tree_flops += N * std::ldexp(1.0, H.m) * fl;
     }
   }
   if (std::getenv("HSF_DEBUG_PLAN")) {

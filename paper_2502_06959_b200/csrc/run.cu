@@ -66,6 +66,7 @@ struct DeviceState {
   cudaStream_t cap = nullptr;
   cudaGraphExec_t gexec = nullptr;
   std::vector<uint64_t> gkey;
+  int gkernels = -1;                        // kernel nodes of the captured graph
   bool capturing = false;
   cudaEvent_t evg[2] = {}, evc[2] = {};  // host-output chunks: GEMM done / D2H done
   cudaStream_t side = nullptr;  // half-B stream; D2H stream of host-output chunks
@@ -1112,6 +1113,19 @@ static void run(Plan* P, const hsf_run_args& a) {
         }
         d->capturing = false;
         CK(cudaStreamEndCapture(d->cap, &g));
+        {
+          size_t nn = 0;
+          CK(cudaGraphGetNodes(g, nullptr, &nn));
+          std::vector<cudaGraphNode_t> nodes(nn);
+          if (nn) CK(cudaGraphGetNodes(g, nodes.data(), &nn));
+          int nk = 0;
+          for (auto nd : nodes) {
+            cudaGraphNodeType ty;
+            CK(cudaGraphNodeGetType(nd, &ty));
+            nk += ty == cudaGraphNodeTypeKernel ? 1 : 0;
+          }
+          d->gkernels = nk;
+        }
         cudaError_t e = cudaGraphInstantiate(&d->gexec, g, 0);
         cudaGraphDestroy(g);
         if (e != cudaSuccess) fail(HSF_ERR_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
@@ -1153,9 +1167,9 @@ static void run(Plan* P, const hsf_run_args& a) {
 
 using namespace hsf;
 
-#define ABI_GUARD(body)                        \
+#define ABI_GUARD(...)                         \
   try {                                        \
-    body;                                      \
+    __VA_ARGS__;                               \
     return HSF_OK;                             \
   } catch (const Error& e) {                   \
     set_last_error(e.msg);                     \
@@ -1246,6 +1260,12 @@ hsf_status hsf_plan_info_get(const hsf_plan_t* plan, hsf_plan_info* info) {
       (h ? info->tail_passes_b : info->tail_passes_a) = on ? T.half.n_passes : 0;
       (h ? info->tail_tree_bytes_b : info->tail_tree_bytes_a) = on ? T.half.tree_bytes : 0.0;
     }
+    info->tree_flops_a = P->half[0].tree_flops;
+    info->tree_flops_b = P->half[1].tree_flops;
+    info->fold_tree_flops_a = P->fold_u0 >= 0 ? P->half_fold[0].tree_flops : 0.0;
+    info->fold_tree_flops_b = P->fold_u0 >= 0 ? P->half_fold[1].tree_flops : 0.0;
+    info->tail_tree_flops_a = P->tail[0].u0 >= 0 ? P->tail[0].half.tree_flops : 0.0;
+    info->tail_tree_flops_b = P->tail[1].u0 >= 0 ? P->tail[1].half.tree_flops : 0.0;
     info->n_joint_blocks = 0;
     for (const auto& un : P->units) info->n_joint_blocks += un.gids.size() > 1 ? 1 : 0;
   })
@@ -1299,6 +1319,81 @@ hsf_status hsf_ipc_release(void* dev_ptr, uint64_t offset) {
   ABI_GUARD({
     if (!dev_ptr) fail(HSF_ERR_INVALID_ARG, "NULL argument");
     CK(cudaIpcCloseMemHandle((char*)dev_ptr - offset));
+  })
+}
+
+hsf_status hsf_run_describe(const hsf_plan_t* plan, const hsf_run_args* args, hsf_run_desc* out) {
+  ABI_GUARD({
+    if (!plan || !args || !out) fail(HSF_ERR_INVALID_ARG, "NULL argument");
+    const Plan* P = reinterpret_cast<const Plan*>(plan);
+    const size_t elem = P->opts.dtype == HSF_C64 ? 8 : 16;
+    const Layout L = make_layout(*P, *args, elem);
+    hsf_run_desc& o = *out;
+    std::memset(&o, 0, sizeof(o));
+    const int nA = P->n - P->n_low, nB = P->n_low;
+    const double K = (double)L.K, MB = std::ldexp(1.0, nB);
+    o.K = L.K;
+    o.direct_half = L.direct;
+    o.tree_variant_a = L.var[0];
+    o.tree_variant_b = L.var[1];
+    for (int h = 0; h < 2; ++h) {  // this range's share of the evaluated tree
+      const Half& H = *L.half[h];
+      const double tot = (double)range_prod(L.hranks[h], 0, (int)L.hranks[h].size());
+      const double frac = (double)(L.hp1[h] - L.hp0[h]) / std::max(1.0, tot);
+      o.sim_bytes[h] = H.tree_bytes * frac;
+      o.sim_flops[h] = H.tree_flops * frac;
+    }
+    if (L.bits_mode) {
+      const double ns = (double)args->n_bitstrings;
+      o.rows = args->n_bitstrings;
+      o.core_flops_useful = o.core_flops_executed = 8.0 * K * ns;
+      if (L.direct >= 0) {
+        o.core = HSF_CORE_BLOCK_GATHER;
+        const double mD = L.half[L.direct]->m, mT = L.half[1 - L.direct]->m;
+        // D's leaves once, one padded T row + sample index, bits and result per sample
+        o.core_bytes = K * std::ldexp(1.0, (int)mD) * elem + ns * ((double)L.Kp * elem + 4 + 8 + elem);
+        o.prep_bytes = 2.0 * K * std::ldexp(1.0, (int)mT) * elem;
+      } else {
+        o.core = HSF_CORE_GATHER;
+        o.core_bytes = ns * (2.0 * K * elem + 8 + elem);
+        o.prep_bytes = 2.0 * K * (std::ldexp(1.0, L.half[0]->m) + std::ldexp(1.0, L.half[1]->m)) * elem;
+      }
+    } else {
+      const double rows = (double)(L.r1 - L.r0);
+      o.rows = L.r1 - L.r0;
+      o.core_flops_useful = 8.0 * K * rows * MB;
+      if (L.prec == HSF_PREC_SIMT) {
+        o.core = HSF_CORE_SIMT;
+        o.core_flops_executed = o.core_flops_useful;
+        o.core_bytes = K * (rows + MB) * elem + rows * MB * elem;
+      } else {
+        const int planes = tc_planes(L.prec);
+        const int prods = L.prec == HSF_PREC_BF16X6 ? 6 : L.prec == HSF_PREC_BF16X1 ? 1 : 3;
+        const double esz = L.prec == HSF_PREC_TF32X3 ? 4.0 : 2.0;
+        const double pl = L.prec == HSF_PREC_TF32X3 ? 2.0 : (double)planes;
+        o.tc_products = prods;
+        const double Kp = (double)((L.K + 31) / 32 * 32);
+        if (L.swap) {
+          o.core = HSF_CORE_TC_SWAPPED;
+          const double R = (double)swap_cols(L);
+          const double bn = std::ceil(2.0 * R / 32.0) * 32.0;
+          o.core_flops_executed = prods * 2.0 * MB * bn * 2.0 * Kp;
+          // M operand (half B's planes, 2K rows) read once, the narrow N operand,
+          // the fp32 [2^nB][2R] GEMM output written and read by the transpose, the result
+          o.core_bytes = pl * esz * 2.0 * Kp * (MB + bn) + 2.0 * MB * 2.0 * R * 4.0 + rows * MB * elem;
+        } else {
+          o.core = rows > 128 ? HSF_CORE_TC_PAIR : HSF_CORE_TC_SINGLE;
+          const double rp = std::ceil(rows / 128.0) * 128.0;
+          o.core_flops_executed = prods * 2.0 * rp * (2.0 * MB) * (2.0 * Kp);
+          // operand planes read once (A'' rows x 2K, B'' 2 MB rows x 2K) + the output written
+          o.core_bytes = pl * esz * 2.0 * Kp * (rp + 2.0 * MB) + rows * MB * elem;
+        }
+        o.prep_bytes = K * (rows + MB) * elem + pl * esz * 2.0 * Kp * (rows + 2.0 * MB);
+      }
+    }
+    o.kernel_launches = -1;
+    const auto* d = (const DeviceState*)P->dev;
+    if (d && d->gexec) o.kernel_launches = d->gkernels;
   })
 }
 

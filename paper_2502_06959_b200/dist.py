@@ -157,12 +157,31 @@ def sharded_step(shard: Shard, partial, out, shard_out=None, group=None):
     return shard_out
 
 
-def run_sharded(plan, out, shard: Shard, shard_out=None, bitstrings=None, precision="auto", group=None):
+def check_plan_hash(plan_hash: int, group=None) -> None:
+    """Every rank must evaluate the same plan (the same device programs and
+    tables): compare the plans' hashes (hsf_plan_info.plan_hash) across ranks."""
+    import torch
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    h = torch.tensor([plan_hash & 0x7FFFFFFFFFFFFFFF], dtype=torch.int64, device=dev)
+    lo, hi = h.clone(), h.clone()
+    dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=group)
+    dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=group)
+    if int(lo.item()) != int(hi.item()):
+        raise RuntimeError("plan hash mismatch across ranks (HSF_ERR_PLAN_MISMATCH)")
+
+
+def run_sharded(plan, out, shard: Shard, shard_out=None, bitstrings=None, precision="auto", group=None,
+                row_range=None):
     """GPU entry: `plan.run` (libhsf.so, C ABI) on this rank's range, then the
-    collective over NCCL."""
-    def partial(path_range, row_range, o):
+    collective over NCCL.  `row_range` overrides the shard's rows (prefix
+    outputs: every rank evaluates the same first rows)."""
+    def partial(path_range, rows, o):
         if isinstance(o, PeerShards):
-            plan.run(None, path_range=path_range, precision=precision, out_shards=o.ptrs)
+            plan.run(None, bitstrings=bitstrings, path_range=path_range, precision=precision, out_shards=o.ptrs)
         else:
-            plan.run(o, bitstrings=bitstrings, path_range=path_range, row_range=row_range, precision=precision)
+            plan.run(o, bitstrings=bitstrings, path_range=path_range, row_range=row_range or rows,
+                     precision=precision)
     return sharded_step(shard, partial, out, shard_out, group)

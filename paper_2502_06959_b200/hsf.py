@@ -49,7 +49,10 @@ class _Info(C.Structure):
                 ("tail_units_a", C.c_int32), ("tail_units_b", C.c_int32),
                 ("tail_passes_a", C.c_int32), ("tail_passes_b", C.c_int32),
                 ("tail_tree_bytes_a", C.c_double), ("tail_tree_bytes_b", C.c_double),
-                ("head_units_a", C.c_int32), ("head_units_b", C.c_int32)]
+                ("head_units_a", C.c_int32), ("head_units_b", C.c_int32),
+                ("tree_flops_a", C.c_double), ("tree_flops_b", C.c_double),
+                ("fold_tree_flops_a", C.c_double), ("fold_tree_flops_b", C.c_double),
+                ("tail_tree_flops_a", C.c_double), ("tail_tree_flops_b", C.c_double)]
 
 
 class _RunArgs(C.Structure):
@@ -61,11 +64,21 @@ class _RunArgs(C.Structure):
                 ("out_shards", C.POINTER(C.c_void_p)), ("n_out_shards", C.c_int32), ("shard_rows", C.c_uint64)]
 
 
+class _RunDesc(C.Structure):
+    _fields_ = [("core", C.c_int32), ("direct_half", C.c_int32), ("tree_variant_a", C.c_int32),
+                ("tree_variant_b", C.c_int32), ("K", C.c_uint64), ("rows", C.c_uint64), ("tc_products", C.c_int32),
+                ("kernel_launches", C.c_int32), ("sim_bytes", C.c_double * 2), ("sim_flops", C.c_double * 2),
+                ("prep_bytes", C.c_double), ("core_bytes", C.c_double), ("core_flops_useful", C.c_double),
+                ("core_flops_executed", C.c_double)]
+
+
+CORE_KINDS = ["simt", "tc_pair", "tc_single", "tc_swapped", "gather", "block_gather"]
+
 _lib = None
 
 EXPORTS = ["hsf_plan_opts_default", "hsf_plan", "hsf_plan_info_get", "hsf_run", "hsf_workspace_bytes",
            "hsf_plan_free", "hsf_status_str", "hsf_last_error", "hsf_version", "hsf_debug_pass_source",
-           "hsf_ipc_export", "hsf_ipc_import", "hsf_ipc_release"]
+           "hsf_ipc_export", "hsf_ipc_import", "hsf_ipc_release", "hsf_run_describe"]
 
 
 def lib():
@@ -82,6 +95,7 @@ def lib():
     L.hsf_plan_info_get.argtypes = [C.c_void_p, C.POINTER(_Info)]
     L.hsf_run.argtypes = [C.c_void_p, C.POINTER(_RunArgs)]
     L.hsf_workspace_bytes.argtypes = [C.c_void_p, C.POINTER(_RunArgs)]
+    L.hsf_run_describe.argtypes = [C.c_void_p, C.POINTER(_RunArgs), C.POINTER(_RunDesc)]
     L.hsf_workspace_bytes.restype = C.c_size_t
     L.hsf_plan_free.argtypes = [C.c_void_p]
     L.hsf_plan_free.restype = None
@@ -96,7 +110,7 @@ def lib():
     L.hsf_ipc_import.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_void_p)]
     L.hsf_ipc_release.argtypes = [C.c_void_p, C.c_uint64]
     for f in ("hsf_plan_opts_default", "hsf_plan", "hsf_plan_info_get", "hsf_run", "hsf_ipc_export", "hsf_ipc_import",
-              "hsf_ipc_release"):
+              "hsf_ipc_release", "hsf_run_describe"):
         getattr(L, f).restype = C.c_int
     _lib = L
     return L
@@ -201,6 +215,9 @@ class Plan:
         self.tail_passes = (int(i.tail_passes_a), int(i.tail_passes_b))
         self.tail_tree_bytes = (float(i.tail_tree_bytes_a), float(i.tail_tree_bytes_b))
         self.head_units = (int(i.head_units_a), int(i.head_units_b))
+        self.tree_flops = (float(i.tree_flops_a), float(i.tree_flops_b))
+        self.fold_tree_flops = (float(i.fold_tree_flops_a), float(i.fold_tree_flops_b))
+        self.tail_tree_flops = (float(i.tail_tree_flops_a), float(i.tail_tree_flops_b))
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -283,10 +300,6 @@ class Plan:
                 raise ValueError("out is None")
             op, odev, n_out = ptr(out, "out")
         bp, bdev, nb = (None, False, 0) if bitstrings is None else ptr(bitstrings, "bitstrings")
-        if bitstrings is not None and not bdev:  # host samples: checked here (device ones in the library)
-            hb = bitstrings.numpy() if isinstance(bitstrings, torch.Tensor) else bitstrings
-            if nb and self.n < 64 and int(np.bitwise_or.reduce(hb.view(np.uint64).ravel())) >> self.n:
-                raise ValueError(f"bitstrings must be < 2^{self.n}")
         if not out_shards:
             if bitstrings is not None:
                 need = nb
@@ -315,6 +328,21 @@ class Plan:
         buf = C.create_string_buffer(n + 1)
         L.hsf_debug_pass_source(self._h, variant, half, pass_index, buf, n + 1)
         return buf.value.decode()
+
+    def describe(self, bitstrings_count: int = 0, path_range=None, row_range=None, precision="auto") -> dict:
+        """hsf_run_describe(): the launch sequence and algorithmic work of a run
+        with these arguments (after a run with the same arguments,
+        `kernel_launches` counts the kernels of its captured graph)."""
+        a = self._args(1, True, 1 if bitstrings_count else None, bitstrings_count, True, path_range, row_range,
+                       precision, None, -1, None)
+        d = _RunDesc()
+        _check(lib().hsf_run_describe(self._h, C.byref(a), C.byref(d)))
+        return {"core": CORE_KINDS[d.core], "direct_half": d.direct_half,
+                "tree_variant": (d.tree_variant_a, d.tree_variant_b), "K": int(d.K), "rows": int(d.rows),
+                "tc_products": d.tc_products, "kernel_launches": d.kernel_launches,
+                "sim_bytes": tuple(d.sim_bytes), "sim_flops": tuple(d.sim_flops), "prep_bytes": d.prep_bytes,
+                "core_bytes": d.core_bytes, "core_flops_useful": d.core_flops_useful,
+                "core_flops_executed": d.core_flops_executed}
 
     def workspace_bytes(self, bitstrings_count: int = 0, path_range=None, row_range=None, precision="auto") -> int:
         a = self._args(1, True, 1 if bitstrings_count else None, bitstrings_count, True, path_range, row_range,

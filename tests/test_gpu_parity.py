@@ -607,16 +607,16 @@ def test_block_gather(torch, name, path_range, direct, monkeypatch):
 
 
 def test_bitstrings_out_of_range(torch):
-    # precondition bits < 2^n: host samples are rejected by the binding; device
-    # samples are flagged by the library when the run synchronises (no
-    # out-of-bounds access either way)
+    # precondition bits < 2^n: the library flags such samples on the device and
+    # fails the run when it synchronises (host output / timings); no
+    # out-of-bounds access either way
     from paper_2502_06959_b200 import Plan
     from paper_2502_06959_b200.hsf import HsfError
     inst = make_config("c5", twin=True)
     P = Plan(inst.text, inst.n_low, inst.blocks)
     bad = inst.bitstrings.copy()
     bad[7] |= np.uint64(1) << np.uint64(inst.n)
-    with pytest.raises(ValueError):
+    with pytest.raises(HsfError):
         P.run(np.empty(len(bad), np.complex64), bitstrings=bad)
     out = torch.empty(len(bad), dtype=torch.complex64, device="cuda")
     with pytest.raises(HsfError):
