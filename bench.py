@@ -405,20 +405,13 @@ def main():
             out = D.PeerShards(torch.zeros(D.bits_shard_len(N_out, world), dtype=cdt, device="cuda"))
     rr_run = (0, prefix_rows) if prefix else sh.row_range
     phases = []
+    # N > 1: the exchange step runs inside the library (its own NCCL
+    # communicator, hsf_run_args.coll), captured in the run's graph
+    lcomm = D.library_comm() if world > 1 else None
 
     def step(timed=False):
-        def partial(path_range, row_range, o):
-            if prefix:
-                row_range = (0, prefix_rows)
-            if isinstance(o, D.PeerShards):
-                ph = P.run(None, bitstrings=bits_d, path_range=path_range, precision=a.precision, timings=timed,
-                           out_shards=o.ptrs)
-            else:
-                ph = P.run(o, bitstrings=bits_d, path_range=path_range, row_range=row_range, precision=a.precision,
-                           timings=timed)
-            if timed:
-                phases.append(ph)
-        D.sharded_step(sh, partial, out, shard)
+        D.run_sharded(P, out, sh, shard_out=shard, bitstrings=bits_d, precision=a.precision, row_range=rr_run,
+                      comm=lcomm, phases=phases if timed else None)
 
     # L2 flush buffer (> 126 MB L2) written between timed steps, outside the events
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -573,11 +566,13 @@ def end_to_end(a, inst, P, D, sh, mode, world, rank, full, prefix_rows, rows, N_
             return {"value": None, "unit": "paths/s", "skipped": "fused modes are measured by the device-timed "
                     "value only"}
 
+        lcomm = D.library_comm()
+
         def e2e_step():
             if bits_dev is not None:
                 bits_dev.copy_(host_bits, non_blocking=True)
             D.run_sharded(P2, dev_out, sh, shard_out=shard, bitstrings=bits_dev, precision=a.precision,
-                          row_range=rr2)
+                          row_range=rr2, comm=lcomm)
             hout.copy_(res_dev, non_blocking=True)
             torch.cuda.synchronize()
         how = ("per rank: pinned H2D of the bitstrings, this rank's hsf_run (C ABI), the %s collective, D2H of "

@@ -56,7 +56,9 @@ typedef enum {
   HSF_ERR_PATH_BUDGET = 8,       /* n_p exceeds 2^log2_path_budget */
   HSF_ERR_OUT_OF_MEMORY = 9,     /* host or device allocation failed */
   HSF_ERR_CUDA = 10,             /* CUDA runtime error (sticky for the plan) */
-  HSF_ERR_UNSUPPORTED = 11       /* valid request this build does not handle */
+  HSF_ERR_UNSUPPORTED = 11,      /* valid request this build does not handle */
+  HSF_ERR_NCCL = 12,             /* NCCL missing or an NCCL call failed (communicator) */
+  HSF_ERR_PLAN_MISMATCH = 13     /* the ranks of a communicator hold different plans */
 } hsf_status;
 
 typedef enum { HSF_C64 = 0, HSF_C128 = 1 } hsf_dtype;
@@ -113,9 +115,26 @@ typedef struct {
   int32_t graphs;                /* 1 (default) => runs with device buffers are captured once
                                     into a CUDA graph (both streams, all launches) and replayed
                                     while pointers, ranges and precision stay the same */
+  int32_t analytic_cascades;     /* 1 (default) => a block that is a cascade of two-qubit gates
+                                    on one common qubit, each block-diagonal in that qubit's
+                                    computational basis (CNOT, CZ, CP, RZZ; Eq. 11),
+                                    gets its rank-<=2 Schmidt factors in closed form (no block
+                                    assembly or SVD; sigma equal to the SVD's); 0 => numeric
+                                    route for every block */
 } hsf_plan_opts;
 
 typedef struct hsf_plan_s hsf_plan_t; /* opaque */
+typedef struct hsf_comm_s hsf_comm_t; /* opaque: NCCL communicator of the exchange step */
+
+/* The exchange step after the path-sum (every path's contribution is
+ * added up; paths split across ranks need one sum over ranks). */
+typedef enum {
+  HSF_COLL_NONE = 0,           /* the run's partial result stays in `out` */
+  HSF_COLL_ALLREDUCE = 1,      /* out <- sum over ranks of out (in place); bitstrings and
+                                  small full outputs */
+  HSF_COLL_REDUCE_SCATTER = 2  /* coll_out <- rank r's row shard [r R / G, (r+1) R / G) of the
+                                  sum over ranks of out (R = the run's rows) */
+} hsf_collective;
 
 /* Fill *opts with the defaults listed above. */
 hsf_status hsf_plan_opts_default(hsf_plan_opts* opts);
@@ -181,6 +200,8 @@ typedef struct {
                                                   amplitude): the compute-roofline numerator */
   double fold_tree_flops_a, fold_tree_flops_b; /* same for the bitstring folded tree (0 if none) */
   double tail_tree_flops_a, tail_tree_flops_b; /* same for the half-sided fold trees (0 if none) */
+  int32_t n_analytic_units;     /* units decomposed by the analytic cascade route */
+  const int32_t* unit_analytic; /* [n_units] 1 if that unit's factors are closed-form */
 } hsf_plan_info;
 
 /* Pointers in *info stay valid until hsf_plan_free. */
@@ -230,6 +251,17 @@ typedef struct {
   void* const* out_shards;
   int32_t n_out_shards;
   uint64_t shard_rows;
+  /* Exchange step (device output only): with comm != NULL and coll !=
+   * HSF_COLL_NONE, the sum over the communicator's ranks is enqueued on
+   * cuda_stream right after the path-sum (captured into the run's CUDA graph
+   * with it).  Every rank calls hsf_run with the same plan, collective,
+   * output size and row range and its own path range.  The first run of a plan
+   * on a communicator compares the ranks' plan hashes (HSF_ERR_PLAN_MISMATCH).
+   * coll_out: REDUCE_SCATTER destination, device, (rows / nranks) * 2^nB
+   * complex values (rows divisible by nranks); ignored otherwise. */
+  hsf_comm_t* comm;
+  hsf_collective coll;
+  void* coll_out;
 } hsf_run_args;
 
 /* hsf_run — evaluate the paths [path_begin, path_end) on the GPU: path-tree
@@ -301,6 +333,16 @@ size_t hsf_debug_pass_source(const hsf_plan_t* plan, int32_t variant, int32_t ha
 hsf_status hsf_ipc_export(const void* dev_ptr, void* handle_out, uint64_t* offset_out);
 hsf_status hsf_ipc_import(const void* handle, uint64_t offset, void** dev_ptr_out);
 hsf_status hsf_ipc_release(void* dev_ptr, uint64_t offset);
+
+/* NCCL communicator of the exchange step (one per rank and GPU).  Rank 0
+ * calls hsf_comm_unique_id and sends the 128 bytes to every rank out of band
+ * (e.g. torch.distributed); every rank then calls hsf_comm_create with its
+ * rank (collective: blocks until all ranks joined).  device: CUDA ordinal, -1
+ * = current.  NCCL is loaded at run time (libnccl.so.2; HSF_ERR_NCCL if
+ * absent).  Free after the last run that uses it. */
+hsf_status hsf_comm_unique_id(void* id_out128);
+hsf_status hsf_comm_create(const void* id128, int32_t nranks, int32_t rank, int32_t device, hsf_comm_t** out);
+void hsf_comm_free(hsf_comm_t* comm);
 
 /* Library build identification string (compile flags, arch). */
 const char* hsf_version(void);

@@ -34,6 +34,7 @@ struct Unit {
   std::vector<int> gids;           // member gates (file order)
   std::vector<int> support, Sa, Sb;// ascending global qubit ids
   bool diag_route = false;         // all members diagonal => diagonal factors
+  bool analytic = false;           // factors from the closed-form cascade route (Eq. 11)
   int rank = 0;
   std::vector<double> sigma;       // kept singular values (descending)
   std::vector<cd> c;               // sigma_m / sqrt(2^|S|)
@@ -127,6 +128,7 @@ struct Plan {
   std::vector<Gate> gates;
   std::vector<Unit> units;          // schedule order
   std::vector<int32_t> ranks, sa, sb;
+  std::vector<int32_t> unit_analytic;  // per unit: closed-form cascade factors
   std::vector<int64_t> sigma_off;
   std::vector<double> sigmas;
   uint64_t n_paths = 1;

@@ -17,6 +17,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <array>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
@@ -273,6 +274,150 @@ static Svd jacobi_svd(const std::vector<cd>& M, int R, int C) {
 }
 
 // ----------------------------------------------------- H3-H6 one cut unit
+// Analytic cascade route (Eq. 11; "analytical expressions
+// can be found for cascade structures"): every member is a two-qubit gate on
+// one common qubit c and block-diagonal in c's computational basis,
+// G = P0_c (x) G_0 + P1_c (x) G_1 (CNOT: G_0 = I, G_1 = X; CZ, CP, RZZ: diagonal
+// G_v).  Members on distinct targets commute inside each c-sector, so
+//   U_S = sum_{v=0,1} P_v,c (x) prod_t G_{t,v}
+//       = O_0 (x) N_0 + O_1 (x) N_1,
+// O_v on c's side (P_v (x) that side's targets' products, Frobenius-orthogonal
+// with equal norms alpha), N_v on the other side (unitary, norm beta).  The
+// reshaped matrix (Eq. 6) then has rank <= 2 and its SVD is closed-form: the
+// 2 x 2 Gram matrix of the N_v, [[beta, g], [conj g, beta]] with
+// g = <N_0, N_1>_F, has eigenvalues beta +- |g| and eigenvectors
+// (1, +-conj(g)/|g|) / sqrt 2, so sigma_+- = sqrt(alpha (beta +- |g|)) and the
+// Schmidt pairs are the Gram-rotated combinations (Eq. 7-9) -- no block
+// assembly, no iterative SVD.  Returns false (numeric route) when the block
+// is not such a cascade.
+static bool analytic_cascade(const std::vector<Gate>& gates, Unit& u, int n_low, const hsf_plan_opts& o) {
+  if (u.gids.empty()) return false;
+  std::set<int> common;
+  for (size_t i = 0; i < u.gids.size(); ++i) {
+    const Gate& g = gates[u.gids[i]];
+    if (g.k != 2) return false;
+    std::set<int> qs(g.q.begin(), g.q.end());
+    if (i == 0) {
+      common = qs;
+    } else {
+      std::set<int> inter;
+      for (int q : qs)
+        if (common.count(q)) inter.insert(q);
+      common.swap(inter);
+    }
+  }
+  for (int c : common) {
+    // G_v of every member as a 2 x 2 matrix on its target, block-diagonality checked
+    std::vector<std::array<std::array<cd, 4>, 2>> Gv(u.gids.size());
+    std::vector<int> tgt(u.gids.size());
+    bool ok = true;
+    for (size_t i = 0; i < u.gids.size() && ok; ++i) {
+      const Gate& g = gates[u.gids[i]];
+      const bool cmsb = g.q[0] == c;  // first-listed qubit = MSB of the gate-local index
+      tgt[i] = cmsb ? g.q[1] : g.q[0];
+      auto idx = [&](int v, int t) { return cmsb ? (v << 1) | t : (t << 1) | v; };
+      for (int vi = 0; vi < 2 && ok; ++vi)
+        for (int ti = 0; ti < 2; ++ti)
+          for (int vj = 0; vj < 2; ++vj)
+            for (int tj = 0; tj < 2; ++tj) {
+              const cd x = g.U[(size_t)idx(vi, ti) * 4 + idx(vj, tj)];
+              if (vi != vj) {
+                if (x != cd(0.0)) ok = false;
+              } else {
+                Gv[i][vi][ti * 2 + tj] = x;
+              }
+            }
+    }
+    if (!ok) continue;
+    const bool diag = u.diag_route;
+    const bool c_low = c < n_low;
+    const std::vector<int>& So = c_low ? u.Sb : u.Sa;  // c's side
+    const std::vector<int>& Sn = c_low ? u.Sa : u.Sb;  // the other side
+    const int ko = (int)So.size(), kn = (int)Sn.size();
+    if (!diag && (ko > 5 || kn > 5)) return false;  // dense factors of <= 5 qubits per half (device limit)
+    // per-qubit 2 x 2 products (later gates on the left), per sector v
+    auto side_op = [&](const std::vector<int>& S, int v, bool with_proj) {
+      const size_t d = (size_t)1 << S.size();
+      std::vector<std::array<cd, 4>> per(S.size());
+      for (size_t j = 0; j < S.size(); ++j) per[j] = {1.0, 0.0, 0.0, 1.0};
+      for (size_t i = 0; i < u.gids.size(); ++i) {
+        const size_t j = (size_t)(std::find(S.begin(), S.end(), tgt[i]) - S.begin());
+        if (j == S.size()) continue;
+        const auto& G = Gv[i][v];
+        const auto P = per[j];
+        per[j] = {G[0] * P[0] + G[1] * P[2], G[0] * P[1] + G[1] * P[3], G[2] * P[0] + G[3] * P[2],
+                  G[2] * P[1] + G[3] * P[3]};
+      }
+      if (with_proj) {
+        const size_t jc = (size_t)(std::find(S.begin(), S.end(), c) - S.begin());
+        per[jc] = v == 0 ? std::array<cd, 4>{1.0, 0.0, 0.0, 0.0} : std::array<cd, 4>{0.0, 0.0, 0.0, 1.0};
+      }
+      // tensor product, local index LSB = smallest support qubit (S ascending)
+      std::vector<cd> M(diag ? d : d * d);
+      for (size_t r = 0; r < d; ++r)
+        for (size_t col = 0; col < (diag ? 1 : d); ++col) {
+          const size_t cc = diag ? r : col;
+          cd x = 1.0;
+          for (size_t j = 0; j < S.size(); ++j) x *= per[j][((r >> j) & 1) * 2 + ((cc >> j) & 1)];
+          M[diag ? r : r * d + col] = x;
+        }
+      return M;
+    };
+    std::vector<cd> O0 = side_op(So, 0, true), O1 = side_op(So, 1, true);
+    std::vector<cd> N0 = side_op(Sn, 0, false), N1 = side_op(Sn, 1, false);
+    auto inner = [](const std::vector<cd>& A, const std::vector<cd>& B) {
+      cd s = 0.0;
+      for (size_t e = 0; e < A.size(); ++e) s += std::conj(A[e]) * B[e];
+      return s;
+    };
+    const double alpha = std::real(inner(O0, O0)), beta = std::real(inner(N0, N0));
+    const cd g = inner(N0, N1);
+    const double ag = std::abs(g);
+    const cd ph = ag > 0 ? std::conj(g) / ag : cd(1.0);
+    // M = [u_+, u_-] (columns), u_+- = (1, +-ph) / sqrt 2; |g| = 0: identity
+    cd M[2][2];
+    if (ag > 0) {
+      const double r2 = 1.0 / std::sqrt(2.0);
+      M[0][0] = r2, M[1][0] = ph * r2, M[0][1] = r2, M[1][1] = -ph * r2;
+    } else {
+      M[0][0] = 1.0, M[1][0] = 0.0, M[0][1] = 0.0, M[1][1] = 1.0;
+    }
+    // lambda_k = || sum_v M_vk N_v ||^2 (= beta +- |g|), from the combined vectors:
+    // the difference form keeps the small sigma accurate (no beta - |g| cancellation)
+    std::vector<cd> Nc[2];
+    double lam[2];
+    for (int k = 0; k < 2; ++k) {
+      Nc[k].resize(N0.size());
+      for (size_t e = 0; e < N0.size(); ++e) Nc[k][e] = M[0][k] * N0[e] + M[1][k] * N1[e];
+      lam[k] = std::real(inner(Nc[k], Nc[k]));
+    }
+    const double s0 = std::sqrt(alpha * lam[0]);
+    const int na = (int)u.Sa.size(), nb = (int)u.Sb.size();
+    const double sa = std::sqrt((double)(1 << na)), sb = std::sqrt((double)(1 << nb));
+    for (int k = 0; k < 2; ++k) {
+      const double sig = std::sqrt(std::max(0.0, alpha * lam[k]));
+      if (!(sig > o.svd_rel_tol * s0)) break;
+      // N^_k = sum_v M_vk N_v (unit norm / sqrt(lam)), O^_k = sum_w conj(M_wk) O_w (/ sqrt(alpha))
+      std::vector<cd> Nk(N0.size()), Ok(O0.size());
+      for (size_t e = 0; e < Nk.size(); ++e) Nk[e] = Nc[k][e] / std::sqrt(lam[k]);
+      for (size_t e = 0; e < Ok.size(); ++e)
+        Ok[e] = (std::conj(M[0][k]) * O0[e] + std::conj(M[1][k]) * O1[e]) / std::sqrt(alpha);
+      std::vector<cd>& xa = c_low ? Nk : Ok;  // side a (high)
+      std::vector<cd>& yb = c_low ? Ok : Nk;  // side b (low)
+      for (auto& x : xa) x *= sa;  // unitary-scale factors, c = sigma / sqrt(2^|S|) (reading 4)
+      for (auto& y : yb) y *= sb;
+      u.sigma.push_back(sig);
+      u.c.push_back(cd(sig / (sa * sb), 0.0));
+      u.X.push_back(std::move(xa));
+      u.Y.push_back(std::move(yb));
+    }
+    u.rank = (int)u.sigma.size();
+    u.analytic = true;
+    return true;
+  }
+  return false;
+}
+
 static void decompose_unit(const std::vector<Gate>& gates, Unit& u, int n_low, const hsf_plan_opts& o) {
   std::set<int> sup;
   for (int gi : u.gids)
@@ -282,6 +427,7 @@ static void decompose_unit(const std::vector<Gate>& gates, Unit& u, int n_low, c
   const int nb = (int)u.Sb.size(), na = (int)u.Sa.size(), ks = nb + na;
   u.diag_route = true;
   for (int gi : u.gids) u.diag_route = u.diag_route && gates[gi].diag;
+  if (o.analytic_cascades && analytic_cascade(gates, u, n_low, o)) return;
   Svd sv;
   if (u.diag_route) {
     if (ks > 24) fail(HSF_ERR_BLOCK_TOO_LARGE, "diagonal block on more than 24 qubits");
@@ -1290,6 +1436,7 @@ Plan* build_plan(const char* text, size_t len, int n_low, int64_t n_blocks, cons
   for (auto& u : P->units) {
     P->n_paths *= (uint64_t)u.rank;
     P->ranks.push_back(u.rank);
+    P->unit_analytic.push_back(u.analytic ? 1 : 0);
     P->sa.push_back((int32_t)u.Sa.size());
     P->sb.push_back((int32_t)u.Sb.size());
     P->sigmas.insert(P->sigmas.end(), u.sigma.begin(), u.sigma.end());

@@ -16,6 +16,7 @@
 #include "sum_kernels.cuh"
 #include "gemm_tc.cuh"
 #include "jit.h"
+#include "comm.h"
 
 namespace hsf {
 
@@ -67,6 +68,7 @@ struct DeviceState {
   cudaGraphExec_t gexec = nullptr;
   std::vector<uint64_t> gkey;
   int gkernels = -1;                        // kernel nodes of the captured graph
+  std::vector<uint64_t> comm_ok;            // communicators whose ranks' plan hashes were compared
   bool capturing = false;
   cudaEvent_t evg[2] = {}, evc[2] = {};  // host-output chunks: GEMM done / D2H done
   cudaStream_t side = nullptr;  // half-B stream; D2H stream of host-output chunks
@@ -886,10 +888,10 @@ static void run_core_bits(Plan* P, DeviceState* d, const Layout& L, const hsf_ru
     if (const char* e = std::getenv("HSF_GATHER_DEBUG")) bp.debug = std::atoi(e);
     const size_t smem = (size_t)L.block_rows * L.Kp * sizeof(float2);
     auto launch = [&](auto kern, int nt) {
-      static bool attr = false;  // per instantiation
-      if (!attr) {
+      static std::vector<const void*> attr;  // kernels whose SMEM limit is raised (all share one type)
+      if (std::find(attr.begin(), attr.end(), (const void*)kern) == attr.end()) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 32 * 512 * 8));
-        attr = true;
+        attr.push_back((const void*)kern);
       }
       int per_sm = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nt, smem));
@@ -1036,6 +1038,15 @@ static void run_all(Plan* P, DeviceState* d, const Layout& L, const hsf_run_args
     }
     for (int i = 0; i < std::min(c, 2); ++i) CK(cudaStreamWaitEvent(st, d->evc[i], 0));
   }
+  if (a.comm && a.coll != HSF_COLL_NONE) {  // the exchange step (contributions added up)
+    Comm* cm = reinterpret_cast<Comm*>(a.comm);
+    const bool f64 = sizeof(R) == 8;
+    const size_t n = L.bits_mode ? (size_t)a.n_bitstrings : ((size_t)(L.r1 - L.r0) << P->n_low);
+    if (a.coll == HSF_COLL_ALLREDUCE)
+      comm_allreduce(cm, a.out, 2 * n, f64, st);
+    else
+      comm_reduce_scatter(cm, a.out, a.coll_out, 2 * n / comm_nranks(cm), f64, st);
+  }
   if (timed) rec(d->ev[4], st);
 }
 
@@ -1058,6 +1069,26 @@ static void run(Plan* P, const hsf_run_args& a) {
   }
   if (a.accumulate && !a.out_on_device && a.n_out_shards == 0)
     fail(HSF_ERR_INVALID_ARG, "accumulate needs a device output buffer");
+  if ((int)a.coll < (int)HSF_COLL_NONE || (int)a.coll > (int)HSF_COLL_REDUCE_SCATTER)
+    fail(HSF_ERR_INVALID_ARG, "unknown collective");
+  if (a.coll != HSF_COLL_NONE) {
+    if (!a.comm) fail(HSF_ERR_INVALID_ARG, "collective without a communicator");
+    Comm* cm = reinterpret_cast<Comm*>(a.comm);
+    if (!a.out_on_device || a.n_out_shards > 0 || P->permuted)
+      fail(HSF_ERR_UNSUPPORTED, "the exchange step needs a device output (no out_shards, contiguous cut)");
+    if (comm_device(cm) != d->device) fail(HSF_ERR_INVALID_ARG, "communicator bound to another device");
+    if (a.coll == HSF_COLL_REDUCE_SCATTER) {
+      if (L.bits_mode) fail(HSF_ERR_INVALID_ARG, "reduce-scatter is for full outputs");
+      if ((L.r1 - L.r0) % (uint64_t)comm_nranks(cm)) fail(HSF_ERR_INVALID_ARG, "rows not divisible by nranks");
+      if (!a.coll_out) fail(HSF_ERR_INVALID_ARG, "reduce-scatter needs coll_out");
+    }
+    const uint64_t key = comm_serial(cm);
+    if (std::find(d->comm_ok.begin(), d->comm_ok.end(), key) == d->comm_ok.end()) {
+      if (!comm_same_hash(cm, P->hash, (cudaStream_t)a.cuda_stream))
+        fail(HSF_ERR_PLAN_MISMATCH, "ranks of the communicator hold different plans (plan_hash differs)");
+      d->comm_ok.push_back(key);
+    }
+  }
   ensure_ws(d, L.total);
   cudaStream_t st = (cudaStream_t)a.cuda_stream;
   int heads = 0;
@@ -1091,7 +1122,8 @@ static void run(Plan* P, const hsf_run_args& a) {
                                    (uint64_t)timed, (uint64_t)L.fold, (uint64_t)(uintptr_t)d->ws,
                                    (uint64_t)(uintptr_t)d->cp, (uint64_t)L.total, (uint64_t)a.n_out_shards,
                                    a.shard_rows, (uint64_t)L.swap, (uint64_t)L.bop,
-                                   (uint64_t)a.out_on_device, (uint64_t)a.bits_on_device};
+                                   (uint64_t)a.out_on_device, (uint64_t)a.bits_on_device,
+                                   (uint64_t)(uintptr_t)a.comm, (uint64_t)a.coll, (uint64_t)(uintptr_t)a.coll_out};
       for (int o = 0; o < a.n_out_shards; ++o) key.push_back((uint64_t)(uintptr_t)a.out_shards[o]);
       if (!d->gexec || key != d->gkey) {
         if (d->gexec) CK(cudaGraphExecDestroy(d->gexec));
@@ -1200,6 +1232,7 @@ hsf_status hsf_plan_opts_default(hsf_plan_opts* o) {
   o->fold_trailing_diag = 1;
   o->jit = 1;
   o->graphs = 1;
+  o->analytic_cascades = 1;
   o->partition_b = 0;
   return HSF_OK;
 }
@@ -1266,6 +1299,9 @@ hsf_status hsf_plan_info_get(const hsf_plan_t* plan, hsf_plan_info* info) {
     info->fold_tree_flops_b = P->fold_u0 >= 0 ? P->half_fold[1].tree_flops : 0.0;
     info->tail_tree_flops_a = P->tail[0].u0 >= 0 ? P->tail[0].half.tree_flops : 0.0;
     info->tail_tree_flops_b = P->tail[1].u0 >= 0 ? P->tail[1].half.tree_flops : 0.0;
+    info->n_analytic_units = 0;
+    for (int32_t x : P->unit_analytic) info->n_analytic_units += x;
+    info->unit_analytic = P->unit_analytic.data();
     info->n_joint_blocks = 0;
     for (const auto& un : P->units) info->n_joint_blocks += un.gids.size() > 1 ? 1 : 0;
   })
@@ -1432,6 +1468,8 @@ const char* hsf_status_str(hsf_status s) {
     case HSF_ERR_OUT_OF_MEMORY: return "HSF_ERR_OUT_OF_MEMORY";
     case HSF_ERR_CUDA: return "HSF_ERR_CUDA";
     case HSF_ERR_UNSUPPORTED: return "HSF_ERR_UNSUPPORTED";
+    case HSF_ERR_NCCL: return "HSF_ERR_NCCL";
+    case HSF_ERR_PLAN_MISMATCH: return "HSF_ERR_PLAN_MISMATCH";
   }
   return "HSF_ERR_UNKNOWN";
 }

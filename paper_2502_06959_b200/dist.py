@@ -173,15 +173,52 @@ def check_plan_hash(plan_hash: int, group=None) -> None:
         raise RuntimeError("plan hash mismatch across ranks (HSF_ERR_PLAN_MISMATCH)")
 
 
+_LIB_COMMS = {}
+
+
+def library_comm(group=None):
+    """The library's own NCCL communicator for this process group
+    (hsf_comm_create), built once: rank 0's unique id travels through
+    torch.distributed, then every rank joins."""
+    import torch
+    import torch.distributed as dist
+    from .hsf import Comm
+    key = id(group)
+    if key not in _LIB_COMMS:
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [Comm.unique_id() if rank == 0 else None]
+        src = dist.get_global_rank(group, 0) if group is not None else 0
+        dist.broadcast_object_list(obj, src=src, group=group)
+        _LIB_COMMS[key] = Comm(obj[0], world, rank, torch.cuda.current_device())
+    return _LIB_COMMS[key]
+
+
 def run_sharded(plan, out, shard: Shard, shard_out=None, bitstrings=None, precision="auto", group=None,
-                row_range=None):
-    """GPU entry: `plan.run` (libhsf.so, C ABI) on this rank's range, then the
-    collective over NCCL.  `row_range` overrides the shard's rows (prefix
-    outputs: every rank evaluates the same first rows)."""
+                row_range=None, comm=None, phases=None):
+    """GPU entry: `plan.run` (libhsf.so, C ABI) on this rank's range and the
+    mode's exchange step.  With `comm` (library_comm()) the all-reduce /
+    reduce-scatter runs inside the library, enqueued right after the path-sum
+    in the run's CUDA graph; otherwise through torch.distributed.  `row_range`
+    overrides the shard's rows (prefix outputs: every rank evaluates the same
+    first rows).  Returns the tensor holding this rank's result; with a list
+    `phases`, appends the run's per-phase ms (hsf_run_args.phase_ms)."""
+    timings = phases is not None
+    if comm is not None and shard.mode in ("allreduce", "reduce_scatter") and comm.nranks > 1:
+        if shard.path_range[0] >= shard.path_range[1]:
+            raise ValueError("the library collective needs a non-empty path range on every rank")
+        r = plan.run(out, bitstrings=bitstrings, path_range=shard.path_range, row_range=row_range or shard.row_range,
+                     precision=precision, comm=comm, coll=shard.mode, coll_out=shard_out, timings=timings)
+        if timings:
+            phases.append(r)
+        return shard_out if shard.mode == "reduce_scatter" else out
+
     def partial(path_range, rows, o):
         if isinstance(o, PeerShards):
-            plan.run(None, bitstrings=bitstrings, path_range=path_range, precision=precision, out_shards=o.ptrs)
+            r = plan.run(None, bitstrings=bitstrings, path_range=path_range, precision=precision, out_shards=o.ptrs,
+                         timings=timings)
         else:
-            plan.run(o, bitstrings=bitstrings, path_range=path_range, row_range=row_range or rows,
-                     precision=precision)
+            r = plan.run(o, bitstrings=bitstrings, path_range=path_range, row_range=row_range or rows,
+                         precision=precision, timings=timings)
+        if timings:
+            phases.append(r)
     return sharded_step(shard, partial, out, shard_out, group)

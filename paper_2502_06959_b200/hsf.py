@@ -32,7 +32,7 @@ class _Opts(C.Structure):
                 ("log2_path_budget", C.c_double), ("individual", C.c_int32), ("tile_qubits", C.c_int32),
                 ("fuse_gates", C.c_int32), ("hoist_gates", C.c_int32), ("fold_trailing_diag", C.c_int32),
                 ("jit", C.c_int32), ("partition_b", C.c_uint64),
-                ("graphs", C.c_int32)]
+                ("graphs", C.c_int32), ("analytic_cascades", C.c_int32)]
 
 
 class _Info(C.Structure):
@@ -52,7 +52,8 @@ class _Info(C.Structure):
                 ("head_units_a", C.c_int32), ("head_units_b", C.c_int32),
                 ("tree_flops_a", C.c_double), ("tree_flops_b", C.c_double),
                 ("fold_tree_flops_a", C.c_double), ("fold_tree_flops_b", C.c_double),
-                ("tail_tree_flops_a", C.c_double), ("tail_tree_flops_b", C.c_double)]
+                ("tail_tree_flops_a", C.c_double), ("tail_tree_flops_b", C.c_double),
+                ("n_analytic_units", C.c_int32), ("unit_analytic", C.POINTER(C.c_int32))]
 
 
 class _RunArgs(C.Structure):
@@ -61,7 +62,10 @@ class _RunArgs(C.Structure):
                 ("path_end", C.c_uint64), ("row_begin", C.c_uint64), ("row_end", C.c_uint64),
                 ("cuda_stream", C.c_void_p), ("precision", C.c_int), ("device", C.c_int32),
                 ("phase_ms", C.POINTER(C.c_double)), ("accumulate", C.c_int32),
-                ("out_shards", C.POINTER(C.c_void_p)), ("n_out_shards", C.c_int32), ("shard_rows", C.c_uint64)]
+                ("out_shards", C.POINTER(C.c_void_p)), ("n_out_shards", C.c_int32), ("shard_rows", C.c_uint64),
+                ("comm", C.c_void_p), ("coll", C.c_int), ("coll_out", C.c_void_p)]
+
+COLL = {None: 0, "none": 0, "allreduce": 1, "reduce_scatter": 2}
 
 
 class _RunDesc(C.Structure):
@@ -78,7 +82,8 @@ _lib = None
 
 EXPORTS = ["hsf_plan_opts_default", "hsf_plan", "hsf_plan_info_get", "hsf_run", "hsf_workspace_bytes",
            "hsf_plan_free", "hsf_status_str", "hsf_last_error", "hsf_version", "hsf_debug_pass_source",
-           "hsf_ipc_export", "hsf_ipc_import", "hsf_ipc_release", "hsf_run_describe"]
+           "hsf_ipc_export", "hsf_ipc_import", "hsf_ipc_release", "hsf_run_describe", "hsf_comm_unique_id",
+           "hsf_comm_create", "hsf_comm_free"]
 
 
 def lib():
@@ -96,6 +101,10 @@ def lib():
     L.hsf_run.argtypes = [C.c_void_p, C.POINTER(_RunArgs)]
     L.hsf_workspace_bytes.argtypes = [C.c_void_p, C.POINTER(_RunArgs)]
     L.hsf_run_describe.argtypes = [C.c_void_p, C.POINTER(_RunArgs), C.POINTER(_RunDesc)]
+    L.hsf_comm_unique_id.argtypes = [C.c_void_p]
+    L.hsf_comm_create.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]
+    L.hsf_comm_free.argtypes = [C.c_void_p]
+    L.hsf_comm_free.restype = None
     L.hsf_workspace_bytes.restype = C.c_size_t
     L.hsf_plan_free.argtypes = [C.c_void_p]
     L.hsf_plan_free.restype = None
@@ -110,7 +119,7 @@ def lib():
     L.hsf_ipc_import.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_void_p)]
     L.hsf_ipc_release.argtypes = [C.c_void_p, C.c_uint64]
     for f in ("hsf_plan_opts_default", "hsf_plan", "hsf_plan_info_get", "hsf_run", "hsf_ipc_export", "hsf_ipc_import",
-              "hsf_ipc_release", "hsf_run_describe"):
+              "hsf_ipc_release", "hsf_run_describe", "hsf_comm_unique_id", "hsf_comm_create"):
         getattr(L, f).restype = C.c_int
     _lib = L
     return L
@@ -144,6 +153,37 @@ def ipc_release(ptr: int, offset: int) -> None:
     _check(lib().hsf_ipc_release(C.c_void_p(ptr), C.c_uint64(offset)))
 
 
+class Comm:
+    """hsf_comm_create(): the library's NCCL communicator for the exchange step
+    (one per rank).  `unique_id()` on rank 0, broadcast the 128 bytes, then
+    every rank constructs Comm(uid, nranks, rank)."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        b = (C.c_char * 128)()
+        _check(lib().hsf_comm_unique_id(b))
+        return bytes(b)
+
+    def __init__(self, uid: bytes, nranks: int, rank: int, device: int = -1):
+        h = C.c_void_p()
+        ub = C.create_string_buffer(bytes(uid), 128)
+        _check(lib().hsf_comm_create(ub, nranks, rank, device, C.byref(h)))
+        self._h = h
+        self.nranks, self.rank = nranks, rank
+
+    @property
+    def handle(self):
+        return self._h.value
+
+    def close(self):
+        if self._h is not None and self._h.value and _lib is not None:
+            _lib.hsf_comm_free(self._h)
+        self._h = None
+
+    def __del__(self):
+        self.close()
+
+
 def version() -> str:
     return lib().hsf_version().decode()
 
@@ -158,7 +198,8 @@ class Plan:
     def __init__(self, circuit_text: str, n_low: int, blocks=None, dtype: str = "c64", individual: bool = False,
                  svd_rel_tol: float = 1e-12, tile_qubits: int = 0, fuse_gates: bool = True,
                  log2_path_budget: float = 26.0, max_dense_block_qubits: int = 10, hoist_gates: bool = True,
-                 fold_trailing_diag: bool = True, jit: bool = True, graphs: bool = True):
+                 fold_trailing_diag: bool = True, jit: bool = True, graphs: bool = True,
+                 analytic_cascades: bool = True):
         L = lib()
         o = _Opts()
         _check(L.hsf_plan_opts_default(C.byref(o)))
@@ -175,6 +216,7 @@ class Plan:
         o.fold_trailing_diag = int(fold_trailing_diag)
         o.jit = int(jit)
         o.graphs = int(graphs)
+        o.analytic_cascades = int(analytic_cascades)
         o.log2_path_budget = log2_path_budget
         o.max_dense_block_qubits = max_dense_block_qubits
         auto = isinstance(blocks, str)
@@ -218,6 +260,8 @@ class Plan:
         self.tree_flops = (float(i.tree_flops_a), float(i.tree_flops_b))
         self.fold_tree_flops = (float(i.fold_tree_flops_a), float(i.fold_tree_flops_b))
         self.tail_tree_flops = (float(i.tail_tree_flops_a), float(i.tail_tree_flops_b))
+        self.n_analytic_units = int(i.n_analytic_units)
+        self.unit_analytic = [bool(i.unit_analytic[u]) for u in range(i.n_units)]
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -244,7 +288,8 @@ class Plan:
         return a
 
     def run(self, out, bitstrings=None, path_range=None, row_range=None, precision: str = "auto", stream=None,
-            timings: bool = False, accumulate: bool = False, out_shards=None):
+            timings: bool = False, accumulate: bool = False, out_shards=None, comm=None, coll=None,
+            coll_out=None):
         """hsf_run(): evaluate paths [path_range) into `out`.
 
         `out` / `bitstrings` are torch tensors (device or host) or numpy arrays
@@ -254,7 +299,11 @@ class Plan:
         each a device tensor or an int device pointer (e.g. another GPU's
         buffer opened via CUDA IPC) of 2^nA / len(out_shards) rows; the
         GEMM epilogue reduce-adds each row shard into its owner; `out` may
-        be None."""
+        be None.
+
+        comm / coll / coll_out: the exchange step inside the run (hsf.h):
+        coll = "allreduce" (out summed over the communicator's ranks in place)
+        or "reduce_scatter" (this rank's row shard of the sum into coll_out)."""
         import torch
 
         keep = []  # host arrays converted here stay alive until hsf_run returns
@@ -286,10 +335,9 @@ class Plan:
             return x.ctypes.data, False, x.size
 
         dev = torch.cuda.current_device() if torch.cuda.is_available() else -1
-        if path_range is not None:
-            p0, p1 = int(path_range[0]), int(path_range[1])
-            if not 0 <= p0 < p1 <= self.n_paths:
-                raise ValueError(f"path_range {path_range} must be non-empty within [0, {self.n_paths})")
+        if path_range is not None and int(path_range[0]) == int(path_range[1]):
+            # hsf_run reads (0, 0) as "all paths": an empty range must not reach it
+            raise ValueError(f"empty path_range {path_range}")
         shards_arr = None
         if out_shards:
             ps = [s if isinstance(s, int) else s.data_ptr() for s in out_shards]
@@ -316,6 +364,20 @@ class Plan:
             a.out_shards = C.cast(shards_arr, C.POINTER(C.c_void_p))
             a.n_out_shards = len(out_shards)
             a.shard_rows = (1 << self.n_a) // len(out_shards)
+        if coll not in COLL:
+            raise ValueError(f"unknown collective {coll!r}")
+        if COLL[coll]:
+            if comm is None:
+                raise ValueError("a collective needs comm=")
+            a.comm = comm.handle
+            a.coll = COLL[coll]
+            if coll == "reduce_scatter":
+                if coll_out is None:
+                    raise ValueError("reduce_scatter needs coll_out")
+                cp_, cdev, cn = ptr(coll_out, "out")
+                if not cdev or cn * comm.nranks != n_out:
+                    raise ValueError("coll_out must be a device tensor of out.numel() / nranks values")
+                a.coll_out = cp_
         _check(lib().hsf_run(self._h, C.byref(a)))
         return list(phase) if timings else None
 

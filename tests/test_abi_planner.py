@@ -145,11 +145,38 @@ def test_workspace_bytes_no_gpu(hsf):
     inst = make_config("c5", n_bits=0)
     P = Plan(inst.text, inst.n_low, inst.blocks)
     b = P.workspace_bytes(bitstrings_count=1 << 22)
-    # leaves + transposed copies of both halves dominate: 128 x 2^20 complex64
-    # each with the last (diagonal) unit folded, 256 x 2^20 without
-    assert 4 * 128 * (1 << 20) * 8 <= b < 4 * 256 * (1 << 20) * 8
+    # both halves' leaves + the transposed copy of the half the block gather
+    # does not read in place dominate: 128 x 2^20 complex64 each with the last
+    # (diagonal) unit folded, 256 x 2^20 without
+    assert 3 * 128 * (1 << 20) * 8 <= b < 3 * 256 * (1 << 20) * 8
     P2 = Plan(inst.text, inst.n_low, inst.blocks, fold_trailing_diag=False)
-    assert P2.workspace_bytes(bitstrings_count=1 << 22) >= 4 * 256 * (1 << 20) * 8
+    assert P2.workspace_bytes(bitstrings_count=1 << 22) >= 3 * 256 * (1 << 20) * 8
+
+
+def test_run_describe_no_gpu(hsf):
+    # hsf_run_describe: the launch sequence and algorithmic work, host only
+    from paper_2502_06959_b200 import Plan
+    inst = make_config("c5", n_bits=0)
+    P = Plan(inst.text, inst.n_low, inst.blocks)
+    d = P.describe(1 << 22)
+    assert d["core"] == "block_gather" and d["direct_half"] in (0, 1) and d["K"] == 128
+    assert d["core_bytes"] == 128 * (1 << 20) * 8 + (1 << 22) * (128 * 8 + 4 + 8 + 8)
+    assert d["core_flops_useful"] == 8 * 128 * (1 << 22)
+    assert d["sim_bytes"] == P.fold_tree_bytes and d["sim_flops"] == P.fold_tree_flops
+    assert d["kernel_launches"] == -1  # never run
+    d2 = P.describe(1 << 22, path_range=(3, 9))  # unaligned: the full tree, K = 6 padded to 64
+    assert d2["tree_variant"] == (0, 0) and d2["K"] == 6
+    assert d2["sim_bytes"][0] == pytest.approx(P.tree_bytes[0] * 6 / 256)
+    d3 = P.describe(1 << 10)  # too few samples per block: the per-sample gather
+    assert d3["core"] == "gather"
+    c2 = make_config("c2")
+    Q = Plan(c2.text, c2.n_low, c2.blocks)
+    e = Q.describe()
+    assert e["core"] == "tc_pair" and e["tc_products"] == 3
+    assert e["core_flops_useful"] == 8 * 4096 * 4096 * 4096
+    assert e["core_flops_executed"] == 3 * 2 * 4096 * 8192 * 8192
+    assert Q.describe(precision="simt")["core"] == "simt"
+    assert Q.describe(row_range=(0, 16))["core"] == "tc_swapped"
 
 
 def test_trailing_fold_detection(hsf):
@@ -255,3 +282,54 @@ def test_partition_mask_validation_and_counts(hsf):
     assert Plan(txt, [0, 1], []).plan_hash == Plan(txt, 2, []).plan_hash
     with pytest.raises(HsfError):
         Plan(txt, [0, 9], [])  # qubit beyond the circuit
+
+
+def test_comm_unique_id_no_gpu(hsf):
+    # hsf_comm_unique_id: 128 bytes from NCCL (loaded at run time); no GPU needed
+    try:
+        uid = hsf.Comm.unique_id()
+    except hsf.HsfError as e:  # NCCL not loadable: the library says so, with its own status
+        assert e.name == "HSF_ERR_NCCL"
+        return
+    assert isinstance(uid, bytes) and len(uid) == 128 and uid != bytes(128)
+    assert hsf.lib().hsf_status_str(12) == b"HSF_ERR_NCCL" and hsf.lib().hsf_status_str(13) == b"HSF_ERR_PLAN_MISMATCH"
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c5", "q30-1", "q33-3"])
+def test_analytic_cascade_sigmas_match_svd(hsf, name):
+    # Eq. 11 route: closed-form rank-2 factors of CP / RZZ cascades; the
+    # singular values equal the numeric route's (assembly + Jacobi SVD) and
+    # LAPACK's on the oracle's block matrices
+    from paper_2502_06959_b200 import Plan
+    inst = make_config(name)
+    blocks = inst.blocks
+    if blocks == "auto":
+        blocks = O.find_cascades(O.parse_circuit(inst.text)[1], inst.n_low)[0]
+    P = Plan(inst.text, inst.n_low, blocks, dtype=inst.dtype)
+    Q = Plan(inst.text, inst.n_low, blocks, dtype=inst.dtype, analytic_cascades=False)
+    assert P.n_analytic_units == P.n_units and Q.n_analytic_units == 0
+    assert P.ranks == Q.ranks and P.n_paths == Q.n_paths
+    for a, b in zip(P.sigmas, Q.sigmas):
+        assert np.allclose(a, b, rtol=1e-11, atol=0)
+    n, g = O.parse_circuit(inst.text)
+    OP = O.plan(n, g, inst.n_low, blocks)
+    for a, u in zip(P.sigmas, OP.units):
+        assert np.allclose(sorted(a), sorted(u.sigmas[:len(a)]), rtol=1e-10)
+
+
+def test_analytic_cascade_cnot_and_mixed_sides(hsf):
+    # CNOT cascade (Eq. 11: P0 (x) I..I + P1 (x) X..X, degenerate sigma), targets
+    # on both sides of the cut, control on the low side, and a non-cascade
+    # block (falls back to the numeric route)
+    from paper_2502_06959_b200 import Plan
+    text = ("qubits 6\nh 3\ncx 3 0\ncx 3 1\ncx 3 4\ncx 3 2\ncp 0x1.8p-1 1 5\nrzz 0x1.4p+0 5 1\nrzz 0x1.2p-1 2 1\n"
+            "cz 1 4\nh 4\ncx 2 5\n")
+    blocks = [[1, 2, 3, 4], [5, 6, 7, 8], [10]]
+    P = Plan(text, 3, blocks)
+    Q = Plan(text, 3, blocks, analytic_cascades=False)
+    assert P.unit_analytic == [True, True, True]
+    assert P.ranks == Q.ranks == [2, 2, 2]
+    for a, b in zip(P.sigmas, Q.sigmas):
+        assert np.allclose(a, b, rtol=1e-12, atol=1e-12)
+    R = Plan("qubits 4\ncx 2 1\nh 2\ncx 2 0\n", 2, [[0, 1, 2]])  # H on the shared qubit: not a cascade
+    assert R.unit_analytic == [False]

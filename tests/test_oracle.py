@@ -56,6 +56,58 @@ def test_rx_is_exponential_of_x():
     assert np.allclose(O.gate_matrix("rx", (t,), 1), E, atol=1e-14)
 
 
+def test_z_h_relations():
+    # Z written out by hand; Z = H X H and X = H Z H (the Hadamard conjugation)
+    Z = np.array([[1, 0], [0, -1]], dtype=complex)
+    H, X = O.gate_matrix("h", (), 1), O.gate_matrix("x", (), 1)
+    assert np.allclose(O.gate_matrix("z", (), 1), Z, atol=0)
+    assert np.allclose(H @ X @ H, Z, atol=1e-15) and np.allclose(H @ Z @ H, X, atol=1e-15)
+
+
+def test_rz_is_exponential_of_z():
+    # RZ(t) = exp(-i t/2 Z) (the RZZ / RX convention), Taylor series of the generator
+    t = -2.71
+    G = -0.5j * t * np.diag([1, -1]).astype(complex)
+    E, term = np.eye(2, dtype=complex), np.eye(2, dtype=complex)
+    for j in range(1, 40):
+        term = term @ G / j
+        E = E + term
+    assert np.allclose(O.gate_matrix("rz", (t,), 1), E, atol=1e-14)
+
+
+def test_cz_cp_phase_on_11():
+    # CZ |11> = -|11>, identity on the other basis states; CZ = (I (x) H) CNOT (I (x) H);
+    # CP(t) multiplies |11> by e^{it} (control and target symmetric), CP(pi) = CZ
+    CZ = O.gate_matrix("cz", (), 2)
+    for j in range(4):
+        e = np.zeros(4, dtype=complex)
+        e[j] = 1
+        assert np.array_equal(CZ @ e, -e if j == 3 else e)
+    IH = np.kron(np.eye(2), O.gate_matrix("h", (), 1))
+    assert np.allclose(IH @ O.gate_matrix("cx", (), 2) @ IH, CZ, atol=1e-15)
+    t = 0.4321
+    CP = O.gate_matrix("cp", (t,), 2)
+    assert np.allclose(CP @ np.array([0, 0, 0, 1]), [0, 0, 0, np.exp(1j * t)], atol=1e-15)
+    assert np.allclose(CP[:3, :3], np.eye(3), atol=0)
+    assert np.allclose(O.gate_matrix("cp", (math.pi,), 2), CZ, atol=1e-15)
+    n, g = _circ("qubits 2\ncp %s 0 1\n" % float(t).hex())
+    n2, g2 = _circ("qubits 2\ncp %s 1 0\n" % float(t).hex())
+    psi0 = np.full(4, 0.5, dtype=complex)
+    assert np.allclose(O.apply_gate(psi0, 2, g[0].U, g[0].qubits), O.apply_gate(psi0, 2, g2[0].U, g2[0].qubits))
+
+
+def test_swap_exchanges_qubits():
+    # SWAP (a (x) b) = b (x) a; SWAP = CNOT(0,1) CNOT(1,0) CNOT(0,1)
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal(2) + 1j * rng.standard_normal(2)
+    b = rng.standard_normal(2) + 1j * rng.standard_normal(2)
+    S = O.gate_matrix("swap", (), 2)
+    assert np.allclose(S @ np.kron(a, b), np.kron(b, a), atol=1e-15)
+    CX = O.gate_matrix("cx", (), 2)
+    P = np.array([[1, 0, 0, 0], [0, 0, 1, 0], [0, 1, 0, 0], [0, 0, 0, 1]], dtype=complex)  # relabel qubits
+    assert np.allclose(CX @ (P @ CX @ P) @ CX, S, atol=1e-15)
+
+
 # ------------------------------------------------------------ Schroedinger
 def test_bell_state_paper_example1():
     text = open(os.path.join(GOLD, "bell.txt")).read()
