@@ -289,9 +289,14 @@ static Svd jacobi_svd(const std::vector<cd>& M, int R, int C) {
 // (1, +-conj(g)/|g|) / sqrt 2, so sigma_+- = sqrt(alpha (beta +- |g|)) and the
 // Schmidt pairs are the Gram-rotated combinations (Eq. 7-9) -- no block
 // assembly, no iterative SVD.  Returns false (numeric route) when the block
-// is not such a cascade.
+// is not such a cascade.  (For degenerate sigma -- g = 0, e.g. CNOT cascades --
+// the factors are one valid basis of the degenerate pair; the path sum over
+// all terms is the same for every basis, partial sums of a degenerate pair's
+// terms are not unique, SURVEY §8(c) reading 6.)
 static bool analytic_cascade(const std::vector<Gate>& gates, Unit& u, int n_low, const hsf_plan_opts& o) {
-  if (u.gids.empty()) return false;
+  // cascades of >= 2 gates; a single crossing gate keeps the numeric route
+  // (its SVD is tiny, and it then shares LAPACK's basis for degenerate sigma)
+  if (u.gids.size() < 2) return false;
   std::set<int> common;
   for (size_t i = 0; i < u.gids.size(); ++i) {
     const Gate& g = gates[u.gids[i]];

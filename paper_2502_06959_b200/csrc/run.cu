@@ -886,6 +886,9 @@ static void run_core_bits(Plan* P, DeviceState* d, const Layout& L, const hsf_ru
     bp.maskB = (1ull << nB) - 1ull;
     bp.accumulate = a.accumulate;
     if (const char* e = std::getenv("HSF_GATHER_DEBUG")) bp.debug = std::atoi(e);
+    bp.n_shards = a.n_out_shards;
+    bp.shard_len = (long long)a.shard_rows;
+    for (int o = 0; o < a.n_out_shards; ++o) bp.shard[o] = (float2*)a.out_shards[o];
     const size_t smem = (size_t)L.block_rows * L.Kp * sizeof(float2);
     auto launch = [&](auto kern, int nt) {
       static std::vector<const void*> attr;  // kernels whose SMEM limit is raised (all share one type)
@@ -1004,10 +1007,10 @@ static void run_all(Plan* P, DeviceState* d, const Layout& L, const hsf_run_args
   if (timed) rec(d->ev[3], st);
   char* ws = (char*)d->ws;
   if (L.bits_mode) {
-    C* out = a.out_on_device ? (C*)a.out : (C*)(ws + L.off_out);
+    C* out = a.n_out_shards > 0 ? nullptr : a.out_on_device ? (C*)a.out : (C*)(ws + L.off_out);
     CK(cudaStreamWaitEvent(st, d->ev_aux, 0));
     run_core_bits<R>(P, d, L, a, st, out, bits_d);
-    if (!a.out_on_device)
+    if (!a.out_on_device && a.n_out_shards == 0)
       CK(cudaMemcpyAsync(a.out, out, (size_t)a.n_bitstrings * sizeof(C), cudaMemcpyDeviceToHost, st));
   } else if (a.out_on_device && P->permuted) {
     // internal-order result into the workspace, then back to the caller's qubit order
@@ -1054,8 +1057,18 @@ static void run(Plan* P, const hsf_run_args& a) {
   DeviceState* d = ensure_device(P, a.device);
   Layout L = make_layout(*P, a, d->elem);
   if (a.n_out_shards < 0 || a.n_out_shards > 8) fail(HSF_ERR_INVALID_ARG, "n_out_shards must be in 0..8");
-  if (a.n_out_shards > 0) {
-    if (L.bits_mode || L.prec == HSF_PREC_SIMT || P->permuted || L.r0 != 0 || L.r1 != (1ull << (P->n - P->n_low)))
+  if (a.n_out_shards > 0 && L.bits_mode) {
+    // fused exchange of bitstring runs: the block gather reduce-adds each
+    // sample into its owner's shard (samples [o * shard_rows, (o+1) * shard_rows))
+    if (L.direct < 0 || P->opts.dtype != HSF_C64)
+      fail(HSF_ERR_UNSUPPORTED, "owner-sharded bitstring output needs the complex64 block gather");
+    if (!a.out_shards || a.shard_rows == 0 || a.shard_rows * (uint64_t)a.n_out_shards < a.n_bitstrings ||
+        a.shard_rows * (uint64_t)(a.n_out_shards - 1) >= a.n_bitstrings)
+      fail(HSF_ERR_INVALID_ARG, "out_shards: n_out_shards pointers of shard_rows samples covering all samples");
+    for (int o = 0; o < a.n_out_shards; ++o)
+      if (!a.out_shards[o]) fail(HSF_ERR_INVALID_ARG, "out_shards[o] is NULL");
+  } else if (a.n_out_shards > 0) {
+    if (L.prec == HSF_PREC_SIMT || P->permuted || L.r0 != 0 || L.r1 != (1ull << (P->n - P->n_low)))
       fail(HSF_ERR_UNSUPPORTED, "fused reduce-scatter needs a full-output tensor-core run over all rows of a "
                                 "contiguous cut");
     if (!a.out_shards || a.shard_rows == 0 || a.shard_rows % 256 ||

@@ -366,7 +366,29 @@ struct BlockGatherParams {
   unsigned long long maskA, maskB;
   int accumulate;
   int debug;             // tuning only: 1 skips the staging, 2 skips the samples
+  // owner-sharded output (fused exchange, hsf_run_args.out_shards): sample s
+  // is reduce-added (vector red.add) into shard[s / shard_len][s % shard_len]
+  // -- device or peer (NVLink / CUDA IPC) memory; n_shards == 0: plain out
+  float2* shard[8];
+  long long shard_len;
+  int n_shards;
 };
+
+// the result of sample `sid`: stored (+= with accumulate) into out, or
+// reduce-added into its owner's shard
+__device__ __forceinline__ void put_amp(const BlockGatherParams& p, int sid, float2 v) {
+  if (p.n_shards) {
+    const int o = (int)(sid / p.shard_len);
+    atomicAdd(p.shard[o] + (sid - (long long)o * p.shard_len), v);
+    return;
+  }
+  if (p.accumulate) {
+    const float2 w = p.out[sid];
+    v.x += w.x;
+    v.y += w.y;
+  }
+  p.out[sid] = v;
+}
 
 // One warp per sample, NF float4 of the K-row per lane (Kp = 64 * NF), U
 // samples in flight per warp, RB rows of the direct half per block, NT
@@ -469,12 +491,7 @@ __global__ void __launch_bounds__(NT, MINB) gather_block_c64_kernel(const BlockG
           if (lane == jj + u) v = make_float2(re[u], im[u]);
         if (lane >= jj && lane < jj + U && lane < nb) {
           if (tw.n) v = cmul(v, trail_weight(tw, trail, sbv));
-          if (p.accumulate) {
-            const float2 w = p.out[sid];
-            v.x += w.x;
-            v.y += w.y;
-          }
-          p.out[sid] = v;
+          put_amp(p, sid, v);
         }
       }
     }

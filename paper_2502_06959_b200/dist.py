@@ -17,6 +17,11 @@ Modes (`mode`):
   "rows"            every rank evaluates ALL paths but writes only its row
                     shard (rows as above) -- no collective on the data path.
                     The recommended c4 mode.
+  "fused_bits"      bitstring runs: paths split as in allreduce, no partial
+                    vector and no collective call: the block gather reduce-adds
+                    (vector red.add) each sample's partial amplitude straight
+                    into its owner's shard over peer memory; rank r holds
+                    samples [r L, (r+1) L), L = ceil(n / G).
   "fused_rs"        paths split as in reduce_scatter, but there is no partial
                     output and no collective call: every rank's GEMM epilogue
                     reduce-adds (TMA .add) each output tile straight into the
@@ -33,7 +38,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
-MODES = ("allreduce", "reduce_scatter", "rows", "fused_rs")
+MODES = ("allreduce", "reduce_scatter", "rows", "fused_rs", "fused_bits")
 
 
 @dataclass(frozen=True)
@@ -50,6 +55,11 @@ def path_range_for_rank(n_paths: int, rank: int, world: int):
     radices (true for c1..c5 at 1/2/4/8).  Empty (p0 == p1) for some ranks
     when world > n_paths; `sharded_step` then skips the evaluation."""
     return (n_paths * rank // world, n_paths * (rank + 1) // world)
+
+
+def bits_shard_len(n_samples: int, world: int) -> int:
+    """Samples per owner shard of the fused bitstring exchange."""
+    return -(-n_samples // world)
 
 
 def row_range_for_rank(n_a: int, rank: int, world: int):
@@ -75,12 +85,14 @@ def default_mode(full_output: bool, n_paths: int, n_a: int, n_b: int, world: int
 def make_shard(mode: str, n_paths: int, n_a: int, rank: int, world: int, full_output: bool) -> Shard:
     if mode not in MODES:
         raise ValueError(f"unknown mode {mode!r}")
-    if not full_output and mode != "allreduce":
-        raise ValueError("bitstring runs use mode='allreduce'")
+    if not full_output and mode not in ("allreduce", "fused_bits"):
+        raise ValueError("bitstring runs use mode='allreduce' or 'fused_bits'")
+    if full_output and mode == "fused_bits":
+        raise ValueError("fused_bits is for bitstring runs")
     if mode in ("reduce_scatter", "rows", "fused_rs") and (1 << n_a) % world:
         raise ValueError("row sharding needs world to divide 2^n_A")
     pr = path_range_for_rank(n_paths, rank, world)
-    if mode == "allreduce":
+    if mode in ("allreduce", "fused_bits"):  # fused_bits: out_rows filled in by the caller's sample count
         return Shard(mode, pr, None, None)
     rr = row_range_for_rank(n_a, rank, world)
     if mode in ("reduce_scatter", "fused_rs"):
@@ -129,7 +141,7 @@ def sharded_step(shard: Shard, partial, out, shard_out=None, group=None):
     import torch
     import torch.distributed as dist
 
-    if shard.mode == "fused_rs":
+    if shard.mode in ("fused_rs", "fused_bits"):
         # zero the own shard, all ranks' adds land in it, then everyone waits
         sync = torch.cuda.synchronize if out.local.is_cuda else (lambda: None)
         out.local.zero_()

@@ -295,11 +295,12 @@ class Plan:
         `out` / `bitstrings` are torch tensors (device or host) or numpy arrays
         (host).  Returns per-phase ms [simA, simB, prep, core, total] if `timings`.
 
-        out_shards: fused reduce-scatter (hsf.h) -- a list of 1..8 destinations,
+        out_shards: fused exchange (hsf.h) -- a list of 1..8 destinations,
         each a device tensor or an int device pointer (e.g. another GPU's
-        buffer opened via CUDA IPC) of 2^nA / len(out_shards) rows; the
-        GEMM epilogue reduce-adds each row shard into its owner; `out` may
-        be None.
+        buffer opened via CUDA IPC).  Full output: 2^nA / len(out_shards)
+        rows each, the GEMM epilogue reduce-adds each row shard into its
+        owner.  Bitstrings: ceil(n / len(out_shards)) samples each, the block
+        gather reduce-adds each sample into its owner.  `out` may be None.
 
         comm / coll / coll_out: the exchange step inside the run (hsf.h):
         coll = "allreduce" (out summed over the communicator's ranks in place)
@@ -363,7 +364,9 @@ class Plan:
         if shards_arr is not None:
             a.out_shards = C.cast(shards_arr, C.POINTER(C.c_void_p))
             a.n_out_shards = len(out_shards)
-            a.shard_rows = (1 << self.n_a) // len(out_shards)
+            # full output: rows of half A per shard; bitstrings: samples per shard
+            a.shard_rows = (-(-nb // len(out_shards)) if bitstrings is not None
+                            else (1 << self.n_a) // len(out_shards))
         if coll not in COLL:
             raise ValueError(f"unknown collective {coll!r}")
         if COLL[coll]:

@@ -70,6 +70,22 @@ def _inst(name):
     return make_config(name, twin=True)
 
 
+def _fused_bits_partial(inst, P):
+    import torch
+    import torch.distributed as dist
+
+    def partial(path_range, row_range, peers):
+        # CPU stand-in for the block gather's reduce-adds into the owners' samples
+        A, B, c = O.half_states(P, *path_range)
+        v = O.recombine_bits(A, B, c, inst.bitstrings, inst.n_low)
+        L = D.bits_shard_len(len(v), dist.get_world_size())
+        pad = np.zeros(L * dist.get_world_size(), dtype=complex)
+        pad[:len(v)] = v
+        dist.reduce_scatter_tensor(torch.view_as_real(peers.local), torch.view_as_real(torch.from_numpy(pad)),
+                                   op=dist.ReduceOp.SUM)
+    return partial
+
+
 def _worker(rank, world, port, name, mode, q):
     import torch
     import torch.distributed as dist
@@ -92,6 +108,11 @@ def _worker(rank, world, port, name, mode, q):
         if mode == "fused_rs":
             peers = _HostPeers(torch.zeros((1 << n) // world, dtype=torch.complex128))
             res = D.sharded_step(sh, _fused_partial(inst, P), peers)
+        elif mode == "fused_bits":
+            L = D.bits_shard_len(len(inst.bitstrings), world)
+            peers = _HostPeers(torch.zeros(L, dtype=torch.complex128))
+            res = D.sharded_step(sh, _fused_bits_partial(inst, P), peers)
+            sh = D.Shard(sh.mode, sh.path_range, None, (rank * L, min(len(inst.bitstrings), (rank + 1) * L)))
         else:
             res = D.sharded_step(sh, _oracle_partial(inst, P, inst.bitstrings), out, shard_out)
         # gather every rank's piece on rank 0 in rank order
@@ -128,13 +149,16 @@ def _reference(name):
 @pytest.mark.parametrize("name,mode", [("c4", "reduce_scatter"), ("c4", "rows"), ("c4", "allreduce"),
                                        ("c4", "fused_rs"), ("c2", "fused_rs"),
                                        ("c1", "allreduce"), ("c5", "allreduce"), ("c3", "allreduce"),
-                                       ("single_path", "allreduce")])
+                                       ("single_path", "allreduce"), ("c5", "fused_bits")])
 def test_two_rank_shards_reassemble(name, mode):
     inst, ref = _reference(name)
     pieces = _run(name, mode)
     if mode == "allreduce":
         for _, v in pieces:  # every rank holds the whole reduced result
             assert np.abs(v - ref).max() <= 1e-12
+    elif mode == "fused_bits":  # rank r owns samples [r L, (r+1) L)
+        got = np.concatenate([v for _, v in sorted(pieces, key=lambda x: x[0][0])])[:len(ref)]
+        assert np.abs(got - ref).max() <= 1e-12
     else:
         got = np.concatenate([v for _, v in sorted(pieces, key=lambda x: x[0][0])])
         assert [r for r, _ in pieces] == [D.row_range_for_rank(inst.n - inst.n_low, r, 2) for r in range(2)]

@@ -42,7 +42,8 @@ def _check(got, ref, tol=1e-5, rel=1e-5):
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("name,mode", [("c5", "allreduce"), ("c3", "allreduce"), ("c2", "reduce_scatter"),
                                        ("c2", "rows"), ("c4", "rows"), ("c4", "reduce_scatter"),
-                                       ("c4", "allreduce"), ("c2", "fused_rs")])
+                                       ("c4", "allreduce"), ("c2", "fused_rs"), ("c5", "fused_bits"),
+                                       ("c3", "fused_bits")])
 def test_emulated_ranks_every_mode(torch, world, name, mode):
     from paper_2502_06959_b200 import Plan
     from paper_2502_06959_b200 import dist as D
@@ -61,10 +62,16 @@ def test_emulated_ranks_every_mode(torch, world, name, mode):
     if mode == "fused_rs":
         shards = [torch.zeros(((1 << n_a) // world) << inst.n_low, dtype=torch.complex64, device="cuda")
                   for _ in range(world)]
+    if mode == "fused_bits":
+        L = D.bits_shard_len(len(inst.bitstrings), world)
+        shards = [torch.zeros(L, dtype=torch.complex64, device="cuda") for _ in range(world)]
     for r in range(world):
         sh = D.make_shard(mode, P.n_paths, n_a, r, world, full)
         if mode == "fused_rs":  # every rank's epilogue adds into every owner's shard
             P.run(None, path_range=sh.path_range, out_shards=shards)
+            continue
+        if mode == "fused_bits":  # every rank's block gather adds into every owner's samples
+            P.run(None, bitstrings=bits, path_range=sh.path_range, out_shards=shards)
             continue
         rows = (sh.row_range[1] - sh.row_range[0]) if sh.row_range else (1 << n_a)
         o = torch.empty((rows << inst.n_low) if full else len(inst.bitstrings), dtype=torch.complex64, device="cuda")
@@ -80,8 +87,30 @@ def test_emulated_ranks_every_mode(torch, world, name, mode):
     elif mode == "rows":
         got = torch.cat([o for _, o in parts])
     else:
-        got = torch.cat(shards)
+        got = torch.cat(shards)[:len(ref)]
     _check(got.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("n_shards", [1, 2, 3, 4])
+def test_fused_bits_shards_rejects_and_reduces(torch, n_shards):
+    # owner-sharded bitstring output (hsf_run_args.out_shards in bitstring
+    # mode): two path halves reduce-added into the same zeroed shards == the
+    # oracle's amplitudes, ragged last shard (n not divisible by 3)
+    from paper_2502_06959_b200 import Plan
+    from paper_2502_06959_b200.hsf import HsfError
+    inst = make_config("c5", twin=True)
+    P = Plan(inst.text, inst.n_low, inst.blocks)
+    ref = _oracle(inst, inst.bitstrings)
+    bits = torch.from_numpy(inst.bitstrings.view(np.int64)).cuda()
+    L = -(-len(ref) // n_shards)
+    shards = [torch.zeros(L, dtype=torch.complex64, device="cuda") for _ in range(n_shards)]
+    h = P.n_paths // 2
+    for pr in ((0, h), (h, P.n_paths)):
+        P.run(None, bitstrings=bits, path_range=pr, out_shards=shards)
+    torch.cuda.synchronize()
+    _check(torch.cat(shards)[:len(ref)].cpu().numpy(), ref)
+    with pytest.raises(HsfError):  # the per-sample gather (too few samples per block) has no sharded epilogue
+        P.run(None, bitstrings=bits[:8], out_shards=shards)
 
 
 @pytest.mark.parametrize("name,coll", [("c5", "allreduce"), ("c3", "allreduce"), ("c2", "allreduce"),

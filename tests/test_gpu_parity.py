@@ -861,9 +861,10 @@ def test_empty_and_invalid_requests(torch):
     out = torch.empty(1 << 12, dtype=torch.complex64, device="cuda")
     with pytest.raises(ValueError):  # empty: the binding stops it ((0, 0) would mean "all" in the ABI)
         P.run(out, path_range=(0, 0))
+    big = torch.empty(65 << 6, dtype=torch.complex64, device="cuda")  # the library's row check, not the binding's size check
     for kw in (dict(path_range=(0, 17)), dict(row_range=(0, 65)), dict(row_range=(4, 4))):
         with pytest.raises(HsfError):
-            P.run(out, **kw)
+            P.run(big, **kw)
     with pytest.raises(HsfError):  # accumulate needs a device buffer
         P.run(np.zeros(1 << 12, dtype=np.complex64), accumulate=True)
     # the plan stays usable after argument errors
