@@ -50,7 +50,7 @@ def _args():
     ap.add_argument("--standard", action="store_true",
                     help="also time standard HSF (every crossing gate cut alone) on the same output: T/J")
     ap.add_argument("--collective", default="auto",
-                    choices=["auto", "reduce_scatter", "allreduce", "rows", "fused_rs", "fused_bits"],
+                    choices=["auto", "reduce_scatter", "allreduce", "rows", "fused_rs", "fused_bits", "nvls_bits"],
                     help="N>1 exchange (paper_2502_06959_b200/dist.py); auto = cheapest for the output mode")
     return ap.parse_args()
 
@@ -403,6 +403,8 @@ def main():
         shard = None
         if mode == "fused_bits":
             out = D.PeerShards(torch.zeros(D.bits_shard_len(N_out, world), dtype=cdt, device="cuda"))
+        if mode == "nvls_bits":  # every rank's copy of the multicast buffer receives the sum
+            out = D.MulticastBuffer(N_out)
     rr_run = (0, prefix_rows) if prefix else sh.row_range
     phases = []
     # N > 1: the exchange step runs inside the library (its own NCCL
@@ -562,7 +564,7 @@ def end_to_end(a, inst, P, D, sh, mode, world, rank, full, prefix_rows, rows, N_
         res_dev = shard if shard is not None else dev_out
         hout = torch.empty(res_dev.numel(), dtype=cdt, pin_memory=True)
         d2h = res_dev.numel() * esz
-        if mode in ("fused_rs", "fused_bits"):
+        if mode in ("fused_rs", "fused_bits", "nvls_bits"):
             return {"value": None, "unit": "paths/s", "skipped": "fused modes are measured by the device-timed "
                     "value only"}
 

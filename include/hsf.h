@@ -262,6 +262,12 @@ typedef struct {
   hsf_comm_t* comm;
   hsf_collective coll;
   void* coll_out;
+  /* 1 => out_shards[0] is the multicast address of an NVLS buffer
+   * (hsf_mcast_bind) and n_out_shards == 1: a bitstring run's block gather
+   * reduce-adds every sample with multimem.red into all ranks' copies (each
+   * rank then holds the whole sum: a fused all-reduce).  Zero the buffers and
+   * barrier before, barrier after, as for out_shards. */
+  int32_t shards_multicast;
 } hsf_run_args;
 
 /* hsf_run — evaluate the paths [path_begin, path_end) on the GPU: path-tree
@@ -343,6 +349,21 @@ hsf_status hsf_ipc_release(void* dev_ptr, uint64_t offset);
 hsf_status hsf_comm_unique_id(void* id_out128);
 hsf_status hsf_comm_create(const void* id128, int32_t nranks, int32_t rank, int32_t device, hsf_comm_t** out);
 void hsf_comm_free(hsf_comm_t* comm);
+
+/* NVLink SHARP multicast buffers (the fused all-reduce of bitstring runs,
+ * hsf_run_args.shards_multicast).  Collective set-up, every rank in order:
+ * rank 0 hsf_mcast_create (returns a 64-byte fabric handle, sent to the other
+ * ranks out of band), the others hsf_mcast_import(handle); every rank
+ * hsf_mcast_add_device; barrier; every rank hsf_mcast_bind (allocates `bytes`
+ * on its device, binds it, maps the local and the multicast address, zeroes
+ * it); barrier.  HSF_ERR_UNSUPPORTED without multicast support (no NVSwitch /
+ * fabric).  hsf_mcast_free unmaps and releases (after every rank's last use). */
+typedef struct hsf_mcast_s hsf_mcast_t;
+hsf_status hsf_mcast_create(size_t bytes, int32_t nranks, int32_t device, void* handle_out64, hsf_mcast_t** out);
+hsf_status hsf_mcast_import(const void* handle64, size_t bytes, int32_t nranks, int32_t device, hsf_mcast_t** out);
+hsf_status hsf_mcast_add_device(hsf_mcast_t* m);
+hsf_status hsf_mcast_bind(hsf_mcast_t* m, void** local_out, void** multicast_out);
+void hsf_mcast_free(hsf_mcast_t* m);
 
 /* Library build identification string (compile flags, arch). */
 const char* hsf_version(void);

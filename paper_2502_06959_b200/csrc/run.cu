@@ -889,6 +889,7 @@ static void run_core_bits(Plan* P, DeviceState* d, const Layout& L, const hsf_ru
     bp.n_shards = a.n_out_shards;
     bp.shard_len = (long long)a.shard_rows;
     for (int o = 0; o < a.n_out_shards; ++o) bp.shard[o] = (float2*)a.out_shards[o];
+    bp.multicast = a.shards_multicast;
     const size_t smem = (size_t)L.block_rows * L.Kp * sizeof(float2);
     auto launch = [&](auto kern, int nt) {
       static std::vector<const void*> attr;  // kernels whose SMEM limit is raised (all share one type)
@@ -1067,7 +1068,10 @@ static void run(Plan* P, const hsf_run_args& a) {
       fail(HSF_ERR_INVALID_ARG, "out_shards: n_out_shards pointers of shard_rows samples covering all samples");
     for (int o = 0; o < a.n_out_shards; ++o)
       if (!a.out_shards[o]) fail(HSF_ERR_INVALID_ARG, "out_shards[o] is NULL");
+    if (a.shards_multicast && a.n_out_shards != 1)
+      fail(HSF_ERR_INVALID_ARG, "a multicast output is one shard holding every sample");
   } else if (a.n_out_shards > 0) {
+    if (a.shards_multicast) fail(HSF_ERR_UNSUPPORTED, "multicast output is for bitstring runs");
     if (L.prec == HSF_PREC_SIMT || P->permuted || L.r0 != 0 || L.r1 != (1ull << (P->n - P->n_low)))
       fail(HSF_ERR_UNSUPPORTED, "fused reduce-scatter needs a full-output tensor-core run over all rows of a "
                                 "contiguous cut");
@@ -1136,7 +1140,8 @@ static void run(Plan* P, const hsf_run_args& a) {
                                    (uint64_t)(uintptr_t)d->cp, (uint64_t)L.total, (uint64_t)a.n_out_shards,
                                    a.shard_rows, (uint64_t)L.swap, (uint64_t)L.bop,
                                    (uint64_t)a.out_on_device, (uint64_t)a.bits_on_device,
-                                   (uint64_t)(uintptr_t)a.comm, (uint64_t)a.coll, (uint64_t)(uintptr_t)a.coll_out};
+                                   (uint64_t)(uintptr_t)a.comm, (uint64_t)a.coll, (uint64_t)(uintptr_t)a.coll_out,
+                                   (uint64_t)a.shards_multicast};
       for (int o = 0; o < a.n_out_shards; ++o) key.push_back((uint64_t)(uintptr_t)a.out_shards[o]);
       if (!d->gexec || key != d->gkey) {
         if (d->gexec) CK(cudaGraphExecDestroy(d->gexec));

@@ -372,11 +372,18 @@ struct BlockGatherParams {
   float2* shard[8];
   long long shard_len;
   int n_shards;
+  int multicast;  // shard[0] is an NVLS multicast address: multimem.red into every rank's copy
 };
 
 // the result of sample `sid`: stored (+= with accumulate) into out, or
 // reduce-added into its owner's shard
 __device__ __forceinline__ void put_amp(const BlockGatherParams& p, int sid, float2 v) {
+  if (p.multicast) {  // in-switch reduction into all ranks' buffers (sm_90+ multimem)
+    float2* a = p.shard[0] + sid;
+    asm volatile("multimem.red.relaxed.sys.global.add.v2.f32 [%0], {%1, %2};" ::"l"(a), "f"(v.x), "f"(v.y)
+                 : "memory");
+    return;
+  }
   if (p.n_shards) {
     const int o = (int)(sid / p.shard_len);
     atomicAdd(p.shard[o] + (sid - (long long)o * p.shard_len), v);

@@ -22,6 +22,11 @@ Modes (`mode`):
                     (vector red.add) each sample's partial amplitude straight
                     into its owner's shard over peer memory; rank r holds
                     samples [r L, (r+1) L), L = ceil(n / G).
+  "nvls_bits"       bitstring runs: paths split as in allreduce; the block
+                    gather reduce-adds each sample with multimem.red through an
+                    NVLS multicast buffer (MulticastBuffer), so the NVSwitch
+                    sums the ranks' contributions into every rank's copy: a
+                    fused all-reduce, no collective call.
   "fused_rs"        paths split as in reduce_scatter, but there is no partial
                     output and no collective call: every rank's GEMM epilogue
                     reduce-adds (TMA .add) each output tile straight into the
@@ -38,7 +43,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
-MODES = ("allreduce", "reduce_scatter", "rows", "fused_rs", "fused_bits")
+MODES = ("allreduce", "reduce_scatter", "rows", "fused_rs", "fused_bits", "nvls_bits")
 
 
 @dataclass(frozen=True)
@@ -85,14 +90,14 @@ def default_mode(full_output: bool, n_paths: int, n_a: int, n_b: int, world: int
 def make_shard(mode: str, n_paths: int, n_a: int, rank: int, world: int, full_output: bool) -> Shard:
     if mode not in MODES:
         raise ValueError(f"unknown mode {mode!r}")
-    if not full_output and mode not in ("allreduce", "fused_bits"):
-        raise ValueError("bitstring runs use mode='allreduce' or 'fused_bits'")
-    if full_output and mode == "fused_bits":
-        raise ValueError("fused_bits is for bitstring runs")
+    if not full_output and mode not in ("allreduce", "fused_bits", "nvls_bits"):
+        raise ValueError("bitstring runs use mode='allreduce', 'fused_bits' or 'nvls_bits'")
+    if full_output and mode in ("fused_bits", "nvls_bits"):
+        raise ValueError(f"{mode} is for bitstring runs")
     if mode in ("reduce_scatter", "rows", "fused_rs") and (1 << n_a) % world:
         raise ValueError("row sharding needs world to divide 2^n_A")
     pr = path_range_for_rank(n_paths, rank, world)
-    if mode in ("allreduce", "fused_bits"):  # fused_bits: out_rows filled in by the caller's sample count
+    if mode in ("allreduce", "fused_bits", "nvls_bits"):  # fused_bits: out_rows = the caller's sample slice
         return Shard(mode, pr, None, None)
     rr = row_range_for_rank(n_a, rank, world)
     if mode in ("reduce_scatter", "fused_rs"):
@@ -131,6 +136,53 @@ class PeerShards:
         self._opened = []
 
 
+class MulticastBuffer:
+    """An NVLS multicast buffer of `n` complex64 values on every rank of the
+    group (hsf_mcast_*), set up collectively over torch.distributed: rank 0
+    creates the multicast object and broadcasts its fabric handle, every rank
+    adds its device, binds its memory.  `local` is this rank's copy (a torch
+    view of it), `ptrs = [multicast address]` goes to Plan.run(multicast=...)."""
+
+    def __init__(self, n: int, group=None):
+        import torch
+        import torch.distributed as dist
+        from . import hsf as H
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        dev = torch.cuda.current_device()
+        nbytes = 8 * n
+        if rank == 0:
+            self.m = H.Multicast(nbytes, world, dev)
+            obj = [self.m.handle]
+        else:
+            obj = [None]
+        if world > 1:
+            dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+            if rank != 0:
+                self.m = H.Multicast(nbytes, world, dev, handle=obj[0])
+        self.m.add_device()
+        if world > 1:
+            dist.barrier(group=group)
+        lo, mc = self.m.bind()
+        if world > 1:
+            dist.barrier(group=group)
+        self.n = n
+        self.mc = mc
+        self.local = _tensor_at(lo, n, dev)
+
+    def close(self):
+        self.m.close()
+
+
+def _tensor_at(ptr: int, n: int, dev: int):
+    """A complex64 torch tensor over n values at device pointer `ptr` (not owned)."""
+    import torch
+
+    class _Arr:
+        __cuda_array_interface__ = {"shape": (2 * n,), "typestr": "<f4", "data": (ptr, False), "version": 3}
+    return torch.as_tensor(_Arr(), device=f"cuda:{dev}").view(torch.complex64)
+
+
 def sharded_step(shard: Shard, partial, out, shard_out=None, group=None):
     """One rank's step: evaluate, then the mode's collective.
 
@@ -141,7 +193,7 @@ def sharded_step(shard: Shard, partial, out, shard_out=None, group=None):
     import torch
     import torch.distributed as dist
 
-    if shard.mode in ("fused_rs", "fused_bits"):
+    if shard.mode in ("fused_rs", "fused_bits", "nvls_bits"):
         # zero the own shard, all ranks' adds land in it, then everyone waits
         sync = torch.cuda.synchronize if out.local.is_cuda else (lambda: None)
         out.local.zero_()
@@ -225,7 +277,10 @@ def run_sharded(plan, out, shard: Shard, shard_out=None, bitstrings=None, precis
         return shard_out if shard.mode == "reduce_scatter" else out
 
     def partial(path_range, rows, o):
-        if isinstance(o, PeerShards):
+        if isinstance(o, MulticastBuffer):
+            r = plan.run(None, bitstrings=bitstrings, path_range=path_range, precision=precision, multicast=o.mc,
+                         timings=timings)
+        elif isinstance(o, PeerShards):
             r = plan.run(None, bitstrings=bitstrings, path_range=path_range, precision=precision, out_shards=o.ptrs,
                          timings=timings)
         else:

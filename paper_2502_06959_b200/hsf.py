@@ -63,7 +63,7 @@ class _RunArgs(C.Structure):
                 ("cuda_stream", C.c_void_p), ("precision", C.c_int), ("device", C.c_int32),
                 ("phase_ms", C.POINTER(C.c_double)), ("accumulate", C.c_int32),
                 ("out_shards", C.POINTER(C.c_void_p)), ("n_out_shards", C.c_int32), ("shard_rows", C.c_uint64),
-                ("comm", C.c_void_p), ("coll", C.c_int), ("coll_out", C.c_void_p)]
+                ("comm", C.c_void_p), ("coll", C.c_int), ("coll_out", C.c_void_p), ("shards_multicast", C.c_int32)]
 
 COLL = {None: 0, "none": 0, "allreduce": 1, "reduce_scatter": 2}
 
@@ -83,7 +83,8 @@ _lib = None
 EXPORTS = ["hsf_plan_opts_default", "hsf_plan", "hsf_plan_info_get", "hsf_run", "hsf_workspace_bytes",
            "hsf_plan_free", "hsf_status_str", "hsf_last_error", "hsf_version", "hsf_debug_pass_source",
            "hsf_ipc_export", "hsf_ipc_import", "hsf_ipc_release", "hsf_run_describe", "hsf_comm_unique_id",
-           "hsf_comm_create", "hsf_comm_free"]
+           "hsf_comm_create", "hsf_comm_free", "hsf_mcast_create", "hsf_mcast_import", "hsf_mcast_add_device",
+           "hsf_mcast_bind", "hsf_mcast_free"]
 
 
 def lib():
@@ -105,6 +106,12 @@ def lib():
     L.hsf_comm_create.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]
     L.hsf_comm_free.argtypes = [C.c_void_p]
     L.hsf_comm_free.restype = None
+    L.hsf_mcast_create.argtypes = [C.c_size_t, C.c_int32, C.c_int32, C.c_void_p, C.POINTER(C.c_void_p)]
+    L.hsf_mcast_import.argtypes = [C.c_void_p, C.c_size_t, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]
+    L.hsf_mcast_add_device.argtypes = [C.c_void_p]
+    L.hsf_mcast_bind.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]
+    L.hsf_mcast_free.argtypes = [C.c_void_p]
+    L.hsf_mcast_free.restype = None
     L.hsf_workspace_bytes.restype = C.c_size_t
     L.hsf_plan_free.argtypes = [C.c_void_p]
     L.hsf_plan_free.restype = None
@@ -119,7 +126,8 @@ def lib():
     L.hsf_ipc_import.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_void_p)]
     L.hsf_ipc_release.argtypes = [C.c_void_p, C.c_uint64]
     for f in ("hsf_plan_opts_default", "hsf_plan", "hsf_plan_info_get", "hsf_run", "hsf_ipc_export", "hsf_ipc_import",
-              "hsf_ipc_release", "hsf_run_describe", "hsf_comm_unique_id", "hsf_comm_create"):
+              "hsf_ipc_release", "hsf_run_describe", "hsf_comm_unique_id", "hsf_comm_create", "hsf_mcast_create",
+              "hsf_mcast_import", "hsf_mcast_add_device", "hsf_mcast_bind"):
         getattr(L, f).restype = C.c_int
     _lib = L
     return L
@@ -178,6 +186,44 @@ class Comm:
     def close(self):
         if self._h is not None and self._h.value and _lib is not None:
             _lib.hsf_comm_free(self._h)
+        self._h = None
+
+    def __del__(self):
+        self.close()
+
+
+class Multicast:
+    """NVLS multicast buffer (hsf_mcast_*): `create` on rank 0 returns the
+    64-byte fabric handle, `import_` on the other ranks; then every rank
+    add_device(), a barrier, bind() (-> local and multicast addresses), a
+    barrier.  dist.MulticastBuffer drives the sequence over torch.distributed."""
+
+    def __init__(self, nbytes: int, nranks: int, device: int = -1, handle: bytes | None = None):
+        h = C.c_void_p()
+        self.nbytes = nbytes
+        if handle is None:
+            hb = (C.c_char * 64)()
+            _check(lib().hsf_mcast_create(nbytes, nranks, device, hb, C.byref(h)))
+            self.handle = bytes(hb)
+        else:
+            _check(lib().hsf_mcast_import(C.create_string_buffer(bytes(handle), 64), nbytes, nranks, device,
+                                          C.byref(h)))
+            self.handle = bytes(handle)
+        self._h = h
+        self.local = self.multicast = None
+
+    def add_device(self):
+        _check(lib().hsf_mcast_add_device(self._h))
+
+    def bind(self):
+        lo, mc = C.c_void_p(), C.c_void_p()
+        _check(lib().hsf_mcast_bind(self._h, C.byref(lo), C.byref(mc)))
+        self.local, self.multicast = int(lo.value), int(mc.value)
+        return self.local, self.multicast
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value and _lib is not None:
+            _lib.hsf_mcast_free(self._h)
         self._h = None
 
     def __del__(self):
@@ -289,7 +335,7 @@ class Plan:
 
     def run(self, out, bitstrings=None, path_range=None, row_range=None, precision: str = "auto", stream=None,
             timings: bool = False, accumulate: bool = False, out_shards=None, comm=None, coll=None,
-            coll_out=None):
+            coll_out=None, multicast=None):
         """hsf_run(): evaluate paths [path_range) into `out`.
 
         `out` / `bitstrings` are torch tensors (device or host) or numpy arrays
@@ -301,6 +347,10 @@ class Plan:
         rows each, the GEMM epilogue reduce-adds each row shard into its
         owner.  Bitstrings: ceil(n / len(out_shards)) samples each, the block
         gather reduce-adds each sample into its owner.  `out` may be None.
+
+        multicast: an NVLS multicast address (Multicast.bind()): a bitstring
+        run's block gather reduce-adds every sample into all ranks' copies
+        (multimem.red; the fused all-reduce).  `out` may be None.
 
         comm / coll / coll_out: the exchange step inside the run (hsf.h):
         coll = "allreduce" (out summed over the communicator's ranks in place)
@@ -340,6 +390,8 @@ class Plan:
             # hsf_run reads (0, 0) as "all paths": an empty range must not reach it
             raise ValueError(f"empty path_range {path_range}")
         shards_arr = None
+        if multicast is not None:
+            out_shards = [int(multicast)]
         if out_shards:
             ps = [s if isinstance(s, int) else s.data_ptr() for s in out_shards]
             shards_arr = (C.c_void_p * len(ps))(*ps)
@@ -367,6 +419,7 @@ class Plan:
             # full output: rows of half A per shard; bitstrings: samples per shard
             a.shard_rows = (-(-nb // len(out_shards)) if bitstrings is not None
                             else (1 << self.n_a) // len(out_shards))
+            a.shards_multicast = int(multicast is not None)
         if coll not in COLL:
             raise ValueError(f"unknown collective {coll!r}")
         if COLL[coll]:

@@ -110,7 +110,7 @@ def test_fused_bits_shards_rejects_and_reduces(torch, n_shards):
     torch.cuda.synchronize()
     _check(torch.cat(shards)[:len(ref)].cpu().numpy(), ref)
     with pytest.raises(HsfError):  # the per-sample gather (too few samples per block) has no sharded epilogue
-        P.run(None, bitstrings=bits[:8], out_shards=shards)
+        P.run(None, bitstrings=bits[:4], out_shards=shards)
 
 
 @pytest.mark.parametrize("name,coll", [("c5", "allreduce"), ("c3", "allreduce"), ("c2", "allreduce"),
@@ -175,3 +175,34 @@ def test_run_sharded_with_library_comm(torch):
     _check(out.cpu().numpy(), ref)
     assert not dist.is_initialized()
     comm.close()
+
+
+@pytest.mark.parametrize("name", ["c5", "c3"])
+def test_nvls_multicast_bits_single_rank(torch, name):
+    # NVLS multicast buffer (hsf_mcast_*, a team of one GPU here): the block
+    # gather's multimem.red.add through the multicast address lands in the
+    # rank's copy; two path halves accumulate to the oracle's amplitudes, also
+    # through dist.run_sharded (mode nvls_bits: zero, evaluate, result = local)
+    from paper_2502_06959_b200 import Plan
+    from paper_2502_06959_b200 import dist as D
+    from paper_2502_06959_b200.hsf import HsfError
+    inst = make_config(name, twin=True)
+    P = Plan(inst.text, inst.n_low, inst.blocks)
+    ref = _oracle(inst, inst.bitstrings)
+    bits = torch.from_numpy(inst.bitstrings.view(np.int64)).cuda()
+    try:
+        mb = D.MulticastBuffer(len(ref))
+    except HsfError as e:  # this pool's single-GPU partitions reject every multicast object
+        assert e.name == "HSF_ERR_UNSUPPORTED", e
+        pytest.skip(str(e))
+    h = P.n_paths // 2
+    for pr in ((0, h), (h, P.n_paths)):
+        P.run(None, bitstrings=bits, path_range=pr, multicast=mb.mc)
+    torch.cuda.synchronize()
+    _check(mb.local.cpu().numpy(), ref)
+    sh = D.make_shard("nvls_bits", P.n_paths, inst.n - inst.n_low, 0, 1, False)
+    for _ in range(2):  # graph capture, then replay (zeroed in between by sharded_step)
+        res = D.run_sharded(P, mb, sh, bitstrings=bits)
+    torch.cuda.synchronize()
+    _check(res.cpu().numpy(), ref)
+    mb.close()
