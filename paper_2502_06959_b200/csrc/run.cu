@@ -890,6 +890,7 @@ static void run_core_bits(Plan* P, DeviceState* d, const Layout& L, const hsf_ru
     bp.shard_len = (long long)a.shard_rows;
     for (int o = 0; o < a.n_out_shards; ++o) bp.shard[o] = (float2*)a.out_shards[o];
     bp.multicast = a.shards_multicast;
+    if (const char* e = std::getenv("HSF_GATHER_LD")) bp.ldmode = std::atoi(e);
     const size_t smem = (size_t)L.block_rows * L.Kp * sizeof(float2);
     auto launch = [&](auto kern, int nt) {
       static std::vector<const void*> attr;  // kernels whose SMEM limit is raised (all share one type)

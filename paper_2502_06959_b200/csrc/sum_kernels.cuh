@@ -373,7 +373,59 @@ struct BlockGatherParams {
   long long shard_len;
   int n_shards;
   int multicast;  // shard[0] is an NVLS multicast address: multimem.red into every rank's copy
+  int ldmode;     // T-row load flavour (ld_row)
 };
+
+// a T-row chunk: 0 = ld.global.nc (L1 allocate), 1 = ld.global.cg (L2 only),
+// 2 = ld.global.nc.L1::no_allocate.L2::256B
+__device__ __forceinline__ float4 ld_row(const float4* a, int mode) {
+  float4 v;
+  if (mode == 1) {
+    v = __ldcg(a);
+  } else if (mode == 2) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(a));
+  } else {
+    v = __ldg(a);
+  }
+  return v;
+}
+
+// Warp sums of U (re, im) pairs by recursive halving: each xor step sends half
+// of the lane's remaining values and keeps the other half (2U - 1 shuffles
+// instead of 10 U for U separate butterflies); lane L then holds the sum of
+// value (L >> (5 - log2 2U)), values 0..U-1 = re, U..2U-1 = im.  Returns
+// sample u_sel's (re, im) to every lane (two indexed shuffles).
+template <int U>
+__device__ __forceinline__ float2 warp_sum_pairs(const float (&re)[U], const float (&im)[U], int lane, int u_sel) {
+  constexpr int V = 2 * U;
+  constexpr int LV = V == 2 ? 1 : V == 4 ? 2 : V == 8 ? 3 : V == 16 ? 4 : 5;
+  static_assert((1 << LV) == V, "U a power of two <= 16");
+  float v[V];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    v[u] = re[u];
+    v[U + u] = im[u];
+  }
+#pragma unroll
+  for (int step = 0; step < LV; ++step) {
+    const int o = 16 >> step, half = V >> (step + 1);
+    const bool hi = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const float send = hi ? v[i] : v[i + half];
+      const float keep = hi ? v[i + half] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+#pragma unroll
+  for (int o = 16 >> LV; o > 0; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+  constexpr int sh = 5 - LV;
+  const float r = __shfl_sync(0xffffffffu, v[0], u_sel << sh);
+  const float i = __shfl_sync(0xffffffffu, v[0], 16 + (u_sel << sh));
+  return make_float2(r, i);
+}
 
 // the result of sample `sid`: stored (+= with accumulate) into out, or
 // reduce-added into its owner's shard
@@ -463,7 +515,7 @@ __global__ void __launch_bounds__(NT, MINB) gather_block_c64_kernel(const BlockG
           const unsigned long long iT = p.direct_b ? (bw[u] >> p.n_low) & p.maskA : bw[u] & p.maskB;
           const float4* q = p.T + (long long)iT * F;
 #pragma unroll
-          for (int t = 0; t < NF; ++t) x[u][t] = __ldg(&q[lane + 32 * t]);
+          for (int t = 0; t < NF; ++t) x[u][t] = ld_row(q + lane + 32 * t, p.ldmode);
         }
         float re[U], im[U];
 #pragma unroll
@@ -484,18 +536,9 @@ __global__ void __launch_bounds__(NT, MINB) gather_block_c64_kernel(const BlockG
             im[u] = fmaf(a.z, c.w, fmaf(a.w, c.z, im[u]));
           }
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            re[u] += __shfl_xor_sync(0xffffffffu, re[u], o);
-            im[u] += __shfl_xor_sync(0xffffffffu, im[u], o);
-          }
         // lane jj + u (the holder of sample jj + u's metadata) writes it
-        float2 v = make_float2(re[0], im[0]);
-#pragma unroll
-        for (int u = 1; u < U; ++u)
-          if (lane == jj + u) v = make_float2(re[u], im[u]);
+        const int us = lane - jj;
+        float2 v = warp_sum_pairs<U>(re, im, lane, (us >= 0 && us < U) ? us : 0);
         if (lane >= jj && lane < jj + U && lane < nb) {
           if (tw.n) v = cmul(v, trail_weight(tw, trail, sbv));
           put_amp(p, sid, v);
