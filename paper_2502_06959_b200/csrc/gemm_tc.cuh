@@ -81,6 +81,7 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifndef HSF_DEBUG_SYNC
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
   asm volatile(
@@ -93,6 +94,38 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+#else
+// Debug build (libhsf_debug.so, -DHSF_DEBUG_SYNC; the substitute for
+// compute-sanitizer, which this pool does not run): every mbarrier wait is
+// bounded -- after ~2 s of SM clock without the phase flipping (a lost TMA
+// transaction, a wrong expect_tx byte count, a missing arrive) the thread
+// reports the barrier and traps, so a protocol bug ends the kernel with an
+// error instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  const long long t0 = clock64();
+  for (;;) {
+    uint32_t ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (clock64() - t0 > 4000000000ll) {
+      uint64_t st;
+      asm volatile("ld.shared.b64 %0, [%1];" : "=l"(st) : "r"(addr));
+      printf("hsf debug: mbarrier wait timed out: block (%d,%d) thread %d barrier smem 0x%x parity %u state 0x%llx\n",
+             blockIdx.x, blockIdx.y, threadIdx.x, addr, parity, (unsigned long long)st);
+      __trap();
+    }
+  }
+}
+#endif
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(

@@ -13,7 +13,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libhsf.so")
+# HSF_DEBUG_LIB=1 loads the debug build (bounded mbarrier waits that trap;
+# build.build(debug=True))
+LIB_PATH = os.path.join(_HERE, "lib", "libhsf_debug.so" if os.environ.get("HSF_DEBUG_LIB") == "1" else "libhsf.so")
 
 HSF_C64, HSF_C128 = 0, 1
 PREC = {"auto": 0, "simt": 1, "bf16x3": 2, "bf16x1": 3, "bf16x6": 4, "tf32x3": 5}

@@ -206,3 +206,40 @@ def test_nvls_multicast_bits_single_rank(torch, name):
     torch.cuda.synchronize()
     _check(res.cpu().numpy(), ref)
     mb.close()
+
+
+def test_debug_build_parity(torch):
+    # libhsf_debug.so (bounded mbarrier waits that report and trap, the
+    # sanitizer substitute) gives the same results: a tcgen05 GEMM run and a
+    # bitstring run against the oracle, in a fresh process
+    import os
+    import subprocess
+    import sys
+    from paper_2502_06959_b200 import build
+    build.build(debug=True)
+    code = r"""
+import numpy as np, torch
+from hsf_inputs import make_config
+from oracle import hsf_oracle as O
+from paper_2502_06959_b200 import Plan, hsf
+assert hsf.LIB_PATH.endswith("libhsf_debug.so")
+for name in ("c2", "c5"):
+    inst = make_config(name, twin=True)
+    n, g = O.parse_circuit(inst.text)
+    ref = O.schrodinger(n, g)
+    P = Plan(inst.text, inst.n_low, inst.blocks)
+    if inst.bitstrings is None:
+        out = torch.empty(1 << n, dtype=torch.complex64, device="cuda")
+        P.run(out)
+    else:
+        ref = ref[inst.bitstrings.astype(np.int64)]
+        out = torch.empty(len(ref), dtype=torch.complex64, device="cuda")
+        P.run(out, bitstrings=torch.from_numpy(inst.bitstrings.view(np.int64)).cuda())
+    torch.cuda.synchronize()
+    assert np.abs(out.cpu().numpy() - ref).max() <= 1e-5, name
+print("debug build ok")
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, HSF_DEBUG_LIB="1"), cwd=root,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "debug build ok" in r.stdout, r.stdout + r.stderr
