@@ -262,13 +262,22 @@ struct Gen {
     o << "    u32 b = gi;";
     for (int p : sorted) o << " b = ins0<" << p << ">(b);";
     o << "\n    const u32 gb = G(" << (x ? "b" : "(RANK << LB) | b") << "); (void)gb;\n    C v[16];\n";
+    // the swizzle is GF(2)-linear and b, e have disjoint bits: sw(b | e) =
+    // sw(b) ^ sw(e), one XOR with a constant per access (c5 leaf pass: ~2 ALU
+    // instructions fewer per shared-memory access)
+    if (!x) o << "    const u32 sb = (u32)sw((int)b);\n";
+    auto elk = [&](uint32_t e) {
+      if (x) return el(x, "(b | " + std::to_string(e) + "u)");
+      const uint32_t swe = e ^ ((e >> 4) & 15u);
+      return std::string("s[sb ^ ") + std::to_string(swe) + "u]";
+    };
     uint32_t ek[16];
     for (int k = 0; k < 16; ++k) {
       uint32_t e = 0;
       for (int j = 0; j < 4; ++j)
         if ((k >> j) & 1) e |= 1u << pos[j];
       ek[k] = e;
-      o << "    v[" << k << "] = " << el(x, "(b | " + std::to_string(e) + "u)") << ";\n";
+      o << "    v[" << k << "] = " << elk(e) << ";\n";
     }
     for (size_t r = i + 1; r <= i + (size_t)n; ++r) {
       const DevOp& d = ops[r];
@@ -292,7 +301,7 @@ struct Gen {
         o << "    }\n";
       }
     }
-    for (int k = 0; k < 16; ++k) o << "    " << el(x, "(b | " + std::to_string(ek[k]) + "u)") << " = v[" << k << "];\n";
+    for (int k = 0; k < 16; ++k) o << "    " << elk(ek[k]) << " = v[" << k << "];\n";
     o << "  }\n";
     sync_pre(x);
   }
