@@ -21,7 +21,7 @@ SC = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 def short(name: str) -> str:
     n = name.split("(")[0]
     n = re.sub(r"<.*>", "", n)
-    return n.replace("void ", "").replace("hsf::tc::", "").replace("hsf::", "").strip()
+    return n.replace("void ", "").strip().split("::")[-1]
 
 
 def main():
