@@ -325,7 +325,8 @@ size_t hsf_last_error(char* buf, size_t len);
  * `variant` (0 = full tree, 1 = bitstring trailing-diagonal fold, 2 = the
  * half-sided trailing fold of full-output runs; + 4·cb for the cluster tier
  * with 2^cb CTAs per tile; + 16·s for the store variant s: 1 = split-bf16 B
- * operand, 3 = the swapped path-sum's M operand).  Copies at most
+ * operand, 3 = the swapped path-sum's M operand; + 64: the T-leaf variant of
+ * that tree's last transition, `pass` ignored).  Copies at most
  * len-1 bytes + NUL into buf (may be NULL) and returns the full length; 0 if
  * the pass does not exist.  Host only. */
 size_t hsf_debug_pass_source(const hsf_plan_t* plan, int32_t variant, int32_t half, int32_t pass, char* buf,

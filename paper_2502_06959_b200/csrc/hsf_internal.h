@@ -3,6 +3,7 @@
 #pragma once
 
 #include <complex>
+#include <memory>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -117,6 +118,12 @@ struct Half {
   int last_gate_level = 0;           // deepest level holding a local gate
   double tree_bytes = 0;             // state bytes the tile passes read + write (all paths)
   double tree_flops = 0;             // their floating-point operations (all paths; FMA = 2)
+  // T-leaf variant of the last transition (bitstring runs, the half the block
+  // gather reads transposed): one pass over 2^10-amplitude tiles evaluating all
+  // tleaf_R leaves of a parent per CTA and writing them transposed ([2^m][Kp]
+  // rows, c_p folded for half A) -- no leaf buffer, no transpose kernel
+  std::shared_ptr<struct Half> tleaf;
+  int tleaf_R = 0;
 };
 
 struct Plan {

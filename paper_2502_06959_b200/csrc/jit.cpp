@@ -87,6 +87,12 @@ struct Gen {
   }
 
   std::string table(int i) const { return "M" + std::to_string(i); }
+  // T-leaf: one group's shared memory (its tile + staged tables; 16 B more so
+  // consecutive groups' tiles start on different banks)
+  size_t group_bytes() const {
+    const size_t elem = c64 ? 8 : 16;
+    return ((((elem << t) + (size_t)ps.tbl_elems * elem) + 15) & ~(size_t)15) + 16;
+  }
   // fixed (non-factor) gate entries become literals in the generated code: no
   // dependent table loads on the gate chain (exact: %a of the run-dtype value)
   bool literal(const DevOp& d) const { return coef && d.radix <= 1 && (d.kind == OP_R1 || d.kind == OP_DENSE); }
@@ -113,37 +119,13 @@ struct Gen {
     return staged(d) ? table(i) + "[" + idx + "]" : "__ldg(&" + table(i) + "[" + idx + "])";
   }
 
-  void header(const std::string& name, int minb) {
-    o << "extern \"C\" __global__ void __launch_bounds__(" << nt << ", " << minb << ") " << name
-      << "(const JitArgs a) {\n";
-    o << "  typedef " << (c64 ? "float2" : "double2") << " C;\n";
-    o << "  constexpr u32 NT = " << nt << "u, NEL = 1u << " << t << ";\n";
-    // cluster tier (cb > 0): the tile is split over 2^cb CTAs of a cluster by
-    // its top cb tile positions; CTA `RANK` holds elements [RANK << LB, +LNEL)
-    o << "  constexpr u32 CB = " << cb << "u, LB = " << (t - cb) << "u, LNEL = 1u << LB;\n";
-    o << "  (void)CB;\n";
-    o << "  extern __shared__ __align__(128) unsigned char smem_raw[];\n";
-    o << "  C* s = reinterpret_cast<C*>(smem_raw);\n";
-    o << "  C* stab = reinterpret_cast<C*>(smem_raw + (sizeof(C) << " << (t - cb) << "));\n";
-    if (cb) {
-      o << "  const u32 RANK = cluster_rank();\n";
-      o << "  C* sr[" << (1 << cb) << "];\n";
-      o << "#pragma unroll\n  for (u32 r = 0; r < " << (1 << cb) << "u; ++r) sr[r] = map_rank(s, r);\n";
-      o << "  auto P = [&](u32 e) -> C& { return sr[e >> LB][sw(e & (LNEL - 1u))]; };\n";
-    } else {
-      o << "  constexpr u32 RANK = 0u;\n";
-    }
-    o << "  (void)stab;\n";
-    // grid: x = tile, y = node
-    o << "  const u32 NODE_ID = blockIdx.y;\n";
-    o << "  const u32 TILE_ID = blockIdx.x;\n";
-    o << "  (void)TILE_ID;\n";
-    o << "  const long long node_g = a.node_first + NODE_ID;\n";
-    o << "  const C* coef = reinterpret_cast<const C*>(a.coef);\n";
-    o << "  C* dst = reinterpret_cast<C*>(a.dst) + (a.node_local0 + NODE_ID) * " << (1ll << m) << "ll;\n";
-    o << "  (void)dst;\n";
-    o << "  const C* src = a.src ? reinterpret_cast<const C*>(a.src) + (node_g / a.src_div - a.src_first) * "
-      << (1ll << m) << "ll : nullptr;\n";
+  int multi = 0;  // T-leaf variant: leaves per CTA (0 = one node per CTA)
+  // T-leaf: one 64-thread group per leaf (its own tile and tables, named
+  // barrier 1 + group); elsewhere the whole CTA
+  std::string TIDs = "threadIdx.x", SYNCs = "__syncthreads()";
+
+  // tile -> state index map G(e) (uses TILE_ID)
+  void emit_G() {
     // tile -> state index map
     if (whole) {
       o << "  auto G = [&](u32 e) -> u32 { return e; };\n";
@@ -162,6 +144,53 @@ struct Gen {
       }
       o << "  auto G = [&](u32 e) -> u32 { return base | " << gather_expr("e", pf, pt) << "; };\n";
     }
+  }
+
+
+  void header(const std::string& name, int minb) {
+    o << "extern \"C\" __global__ void __launch_bounds__(" << nt << ", " << minb << ") " << name
+      << "(const JitArgs a) {\n";
+    o << "  typedef " << (c64 ? "float2" : "double2") << " C;\n";
+    o << "  constexpr u32 NT = " << (multi ? 64 : nt) << "u, NEL = 1u << " << t << ";\n";
+    // cluster tier (cb > 0): the tile is split over 2^cb CTAs of a cluster by
+    // its top cb tile positions; CTA `RANK` holds elements [RANK << LB, +LNEL)
+    o << "  constexpr u32 CB = " << cb << "u, LB = " << (t - cb) << "u, LNEL = 1u << LB;\n";
+    o << "  (void)CB;\n";
+    o << "  extern __shared__ __align__(128) unsigned char smem_raw[];\n";
+    if (multi) {
+      o << "  const u32 GRP = threadIdx.x >> 6, TID = threadIdx.x & 63u;\n";
+      o << "  unsigned char* gbase = smem_raw + GRP * " << group_bytes() << "u;\n";
+      o << "  C* s = reinterpret_cast<C*>(gbase);\n";
+      o << "  C* stab = reinterpret_cast<C*>(gbase + (sizeof(C) << " << t << "));\n";
+    } else {
+      o << "  C* s = reinterpret_cast<C*>(smem_raw);\n";
+      o << "  C* stab = reinterpret_cast<C*>(smem_raw + (sizeof(C) << " << (t - cb) << "));\n";
+    }
+    if (cb) {
+      o << "  const u32 RANK = cluster_rank();\n";
+      o << "  C* sr[" << (1 << cb) << "];\n";
+      o << "#pragma unroll\n  for (u32 r = 0; r < " << (1 << cb) << "u; ++r) sr[r] = map_rank(s, r);\n";
+      o << "  auto P = [&](u32 e) -> C& { return sr[e >> LB][sw(e & (LNEL - 1u))]; };\n";
+    } else {
+      o << "  constexpr u32 RANK = 0u;\n";
+    }
+    o << "  (void)stab;\n";
+    // grid: x = tile, y = node (T-leaf: y = parent, its `multi` leaves looped over)
+    o << "  const u32 TILE_ID = blockIdx.x;\n";
+    o << "  (void)TILE_ID;\n";
+    o << "  const C* coef = reinterpret_cast<const C*>(a.coef);\n";
+    if (multi) {
+      emit_G();
+      o << "  {\n  const u32 NODE_ID = blockIdx.y * " << multi << "u + GRP;\n";
+    } else {
+      o << "  const u32 NODE_ID = blockIdx.y;\n";
+    }
+    o << "  const long long node_g = a.node_first + NODE_ID;\n";
+    o << "  C* dst = reinterpret_cast<C*>(a.dst) + (a.node_local0 + NODE_ID) * " << (1ll << m) << "ll;\n";
+    o << "  (void)dst;\n";
+    o << "  const C* src = a.src ? reinterpret_cast<const C*>(a.src) + (node_g / a.src_div - a.src_first) * "
+      << (1ll << m) << "ll : nullptr;\n";
+    if (!multi) emit_G();
     // per-op table pointers (digit-resolved for Schmidt factors)
     for (size_t i = 0; i < ops.size(); ++i) {
       const DevOp& d = ops[i];
@@ -172,7 +201,7 @@ struct Gen {
                std::to_string(d.stride) + "ll";
       if (staged(d)) {
         o << "  C* " << table(i) << " = stab + " << d.soff << ";\n";
-        o << "  { const C* g_ = " << ptr << "; for (u32 e = threadIdx.x; e < " << (1u << d.k)
+        o << "  { const C* g_ = " << ptr << "; for (u32 e = " << TIDs << "; e < " << (1u << d.k)
           << "u; e += NT) " << table(i) << "[e] = __ldg(&g_[e]); }\n";
       } else {
         o << "  const C* __restrict__ " << table(i) << " = " << ptr << ";\n";
@@ -181,13 +210,13 @@ struct Gen {
     // load (or |0...0>)
     o << "  if (src) {\n";
     o << "#pragma unroll 4\n";
-    o << "    for (u32 e = 2u * threadIdx.x; e < LNEL; e += 2u * NT) { C x_, y_; ld2(src + G((RANK << LB) | e), x_, y_); "
+    o << "    for (u32 e = 2u * " << TIDs << "; e < LNEL; e += 2u * NT) { C x_, y_; ld2(src + G((RANK << LB) | e), x_, y_); "
          "s[sw(e)] = x_; s[sw(e + 1)] = y_; }\n";
     o << "  } else {\n";
-    o << "    for (u32 e = threadIdx.x; e < LNEL; e += NT) { C v_ = czero<C>(); if (G((RANK << LB) | e) == 0u) v_.x = 1; "
+    o << "    for (u32 e = " << TIDs << "; e < LNEL; e += NT) { C v_ = czero<C>(); if (G((RANK << LB) | e) == 0u) v_.x = 1; "
          "s[sw(e)] = v_; }\n";
     o << "  }\n";
-    o << (cb ? "  cluster_sync();\n" : "  __syncthreads();\n");
+    o << (cb ? "  cluster_sync();\n" : "  " + SYNCs + ";\n");
   }
 
   bool cross(const int* pos, int k) const {
@@ -197,14 +226,14 @@ struct Gen {
   }
   // element access: local op -> this CTA's SMEM, cross op -> any CTA's (DSMEM)
   std::string el(bool x, const std::string& e) const { return x ? "P(" + e + ")" : "s[sw(" + e + ")]"; }
-  void sync_pre(bool x) { o << (x ? "  cluster_sync();\n" : "  __syncthreads();\n"); }
+  void sync_pre(bool x) { o << (x ? std::string("  cluster_sync();\n") : "  " + SYNCs + ";\n"); }
   // loop over groups: local ops walk this CTA's groups, cross ops the whole tile's
   void group_loop(bool x, const std::string& var, int shift) {
     if (x)
       o << "  for (u32 " << var << " = RANK * NT + threadIdx.x; " << var << " < (NEL >> " << shift << "); " << var
         << " += (NT << CB)) {\n";
     else
-      o << "  for (u32 " << var << " = threadIdx.x; " << var << " < (LNEL >> " << shift << "); " << var
+      o << "  for (u32 " << var << " = " << TIDs << "; " << var << " < (LNEL >> " << shift << "); " << var
         << " += NT) {\n";
   }
 
@@ -308,7 +337,7 @@ struct Gen {
 
   // run of standalone diagonal ops [i, j): element-owner mapping, 4 per thread
   void diag_run(size_t i, size_t j) {
-    o << "  for (u32 e0 = threadIdx.x; e0 < LNEL; e0 += 4u * NT) {\n";
+    o << "  for (u32 e0 = " << TIDs << "; e0 < LNEL; e0 += 4u * NT) {\n";
     o << "#pragma unroll\n    for (u32 w = 0; w < 4u; ++w) { const u32 e = e0 + w * NT;";
     o << " if (e < LNEL) { const u32 g = G((RANK << LB) | e); C v = s[sw(e)];\n";
     for (size_t r = i; r < j; ++r)
@@ -335,7 +364,7 @@ struct Gen {
     int heavy_minb = 4, light_minb = 3;
     if (const char* e = std::getenv("HSF_JIT_HEAVY_MINB")) heavy_minb = std::atoi(e);
     if (const char* e = std::getenv("HSF_JIT_LIGHT_MINB")) light_minb = std::atoi(e);
-    header(name, nt > 256 ? 1 : (heavy ? heavy_minb : light_minb));
+    header(name, multi ? 2 : nt > 256 ? 1 : (heavy ? heavy_minb : light_minb));
     size_t i = 0;
     while (i < ops.size()) {
       const DevOp& d = ops[i];
@@ -349,12 +378,30 @@ struct Gen {
         size_t j = i;
         while (j < ops.size() && ops[j].kind == OP_DIAG) ++j;
         diag_run(i, j);
-        o << "  __syncthreads();\n";  // element-owner mapping differs from the store mapping
+        o << "  " << SYNCs << ";\n";  // element-owner mapping differs from the store mapping
         i = j;
       }
     }
-    o << "  __syncthreads();\n";
-    if (operand_store) {
+    o << "  " << SYNCs << ";\n";
+    if (multi) {
+      o << "  }\n  __syncthreads();\n";
+      // transposed store of the CTA's `multi` leaves (group g's tile = leaf g):
+      // row G(e) of the gather operand gets columns k0 .. k0 + multi - 1
+      // (x c_p for half A), two columns (16 B) per thread, a row's multi / 2
+      // threads adjacent
+      const int hp = multi / 2;
+      o << "  { C* T = reinterpret_cast<C*>(a.dst); const C* cp = reinterpret_cast<const C*>(a.dst_lo);\n";
+      o << "    const long long k0 = a.node_local0 + (long long)blockIdx.y * " << multi << "ll;\n";
+      o << "#pragma unroll 4\n";
+      o << "    for (u32 i = threadIdx.x; i < LNEL * " << hp << "u; i += " << multi * 64 << "u) {\n";
+      o << "      const u32 e = i / " << hp << "u, c2 = 2u * (i % " << hp << "u);\n";
+      o << "      const C* t0 = reinterpret_cast<const C*>(smem_raw + c2 * " << group_bytes() << "u);\n";
+      o << "      const C* t1 = reinterpret_cast<const C*>(smem_raw + (c2 + 1u) * " << group_bytes() << "u);\n";
+      o << "      C v0 = t0[sw(e)], v1 = t1[sw(e)];\n";
+      o << "      if (cp) { v0 = cmul(v0, cp[k0 + c2]); v1 = cmul(v1, cp[k0 + c2 + 1u]); }\n";
+      o << "      st2(T + (long long)G(e) * a.ldw + k0 + c2, v0, v1);\n";
+      o << "    }\n  }\n";
+    } else if (operand_store) {
       o << "#pragma unroll 4\n";
       o << "  for (u32 e = 2u * threadIdx.x; e < LNEL; e += 2u * NT) " << (store_mode == 3 ? "st_aop" : "st_bop")
         << "(a, a.node_local0 + NODE_ID, G((RANK << LB) | e), s[sw(e)], s[sw(e + 1)]);\n";
@@ -440,6 +487,21 @@ std::string jit_pass_source(const Half& H, const Pass& ps, bool c64, int threads
                             const std::vector<cd>* coef, int store_mode) {
   Gen g(H, ps, c64, coef);
   return std::string(kPrelude) + "\n" + g.build("hsf_jit_pass", threads, cluster_bits, store_mode);
+}
+
+std::string jit_tleaf_source(const Half& TL, int leaves, bool c64, const std::vector<cd>* coef) {
+  const Pass& ps = TL.trans[0].passes[0];
+  Gen g(TL, ps, c64, coef);
+  g.multi = leaves;
+  g.TIDs = "TID";
+  g.SYNCs = "asm volatile(\"bar.sync %0, 64;\" :: \"r\"(1u + GRP) : \"memory\")";
+  return std::string(kPrelude) + "\n" + g.build("hsf_jit_pass", 64 * leaves, 0, 0);
+}
+
+size_t jit_tleaf_smem_bytes(const Half& TL, int leaves, bool c64) {
+  const Pass& ps = TL.trans[0].passes[0];
+  const size_t elem = c64 ? 8 : 16;
+  return (size_t)leaves * (((((elem << ps.t) + (size_t)ps.tbl_elems * elem) + 15) & ~(size_t)15) + 16);
 }
 
 size_t jit_smem_bytes(const Pass& ps, bool c64, int cluster_bits) {

@@ -28,6 +28,12 @@ struct JitLaunchArgs {
 // store_mode 3: the swapped path-sum's MN-major M operand (st_aop)
 std::string jit_pass_source(const Half& H, const Pass& ps, bool c64, int threads = 256, int cluster_bits = 0,
                             const std::vector<cd>* coef = nullptr, int store_mode = 0);
+// T-leaf variant (Half::tleaf): one CTA per (tile, parent) evaluates the
+// parent's `leaves` leaves and writes them transposed into the gather operand
+// (JitArgs dst = operand [2^m][ldw], dst_lo = c_p of half A or nullptr)
+// (64 threads per leaf: launch with 64 * leaves threads)
+std::string jit_tleaf_source(const Half& TL, int leaves, bool c64, const std::vector<cd>* coef);
+size_t jit_tleaf_smem_bytes(const Half& TL, int leaves, bool c64);
 // dynamic shared memory of that kernel (tile + staged diagonal tables)
 size_t jit_smem_bytes(const Pass& ps, bool c64, int cluster_bits = 0);
 // NVRTC-compile (cached per device and source, parallel) and load; returns CUfunctions

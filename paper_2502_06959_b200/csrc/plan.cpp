@@ -980,6 +980,39 @@ static int head_units(const Plan& P, int h, const std::vector<SchedItem>& order,
 // Builds half h's path-tree program over the first U_tree units (U_tree <
 // n_units only for the trailing-diagonal fold, whose dropped units carry no
 // gate after them).
+// Factor ops of a pass evaluated at output level L: the digit of unit u is
+// (node / prod_{u < v < L} r_v) % r_u; diagonal qubit lists as <= 3 runs.
+static void resolve_digits(Half& H, Pass& p, const std::vector<int32_t>& R, int L) {
+  for (int64_t i = p.op_begin; i < p.op_end; ++i) {
+    DevOp& d = H.dev_ops[i];
+    int unit = (int)d.div;
+    if (unit >= 0) {
+      d.radix = R[unit];
+      d.div = (int64_t)range_prod(R, unit + 1, L);
+    } else {
+      d.radix = 1;
+      d.div = 1;
+    }
+    // contiguous runs of the diagonal's qubit list (index bit j <- q[j])
+    d.nruns = 0;
+    if (d.kind == OP_DIAG) {
+      int r = 0;
+      for (int j = 0; j < d.k;) {
+        int e = j + 1;
+        while (e < d.k && d.q[e] == d.q[e - 1] + 1) ++e;
+        if (r < 3) {
+          d.rshift[r] = (uint8_t)d.q[j];
+          d.rlen[r] = (uint8_t)(e - j);
+          d.roff[r] = (uint8_t)j;
+        }
+        ++r;
+        j = e;
+      }
+      d.nruns = (r <= 3) ? r : 0;
+    }
+  }
+}
+
 static void build_half(Plan& P, int h, const std::vector<SchedItem>& order, int U_tree, Half& H, int v0 = 0) {
   const int n_low = P.n_low;
   // units [0, v0) are scalars on this half (head fold, see head_units): no
@@ -1155,35 +1188,7 @@ static void build_half(Plan& P, int h, const std::vector<SchedItem>& order, int 
       plan_passes(H, tr, ob, oe, t, t_max);
     }
     // resolve factor digits for this transition's output level
-    for (auto& p : tr.passes)
-      for (int64_t i = p.op_begin; i < p.op_end; ++i) {
-        DevOp& d = H.dev_ops[i];
-        int unit = (int)d.div;
-        if (unit >= 0) {
-          d.radix = R[unit];
-          d.div = (int64_t)range_prod(R, unit + 1, L);
-        } else {
-          d.radix = 1;
-          d.div = 1;
-        }
-        // contiguous runs of the diagonal's qubit list (index bit j <- q[j])
-        d.nruns = 0;
-        if (d.kind == OP_DIAG) {
-          int r = 0;
-          for (int j = 0; j < d.k;) {
-            int e = j + 1;
-            while (e < d.k && d.q[e] == d.q[e - 1] + 1) ++e;
-            if (r < 3) {
-              d.rshift[r] = (uint8_t)d.q[j];
-              d.rlen[r] = (uint8_t)(e - j);
-              d.roff[r] = (uint8_t)j;
-            }
-            ++r;
-            j = e;
-          }
-          d.nruns = (r <= 3) ? r : 0;
-        }
-      }
+    for (auto& p : tr.passes) resolve_digits(H, p, R, L);
     H.trans.push_back(std::move(tr));
     prev = L;
   }
@@ -1207,6 +1212,41 @@ static void build_half(Plan& P, int h, const std::vector<SchedItem>& order, int 
           fl += d.kind == OP_DENSE ? 8.0 * std::ldexp(1.0, d.k) : d.kind == OP_R1 ? 16.0 : d.kind == OP_DIAG ? 6.0 : 0.0;
         }
       H.tree_flops += N * std::ldexp(1.0, H.m) * fl;
+    }
+  }
+  // T-leaf variant (see Half::tleaf): the last transition's ops over tiles of
+  // 2^10 amplitudes in ONE pass, its R = 2 / 4 / 8 leaves per parent
+  // evaluated by one CTA (R x 8 KiB of staging)
+  H.tleaf.reset();
+  H.tleaf_R = 0;
+  if (!whole && H.m >= 10 && !H.trans.empty() && H.trans.back().level_in >= 0) {
+    const int lin = H.trans.back().level_in;
+    const uint64_t Rc = range_prod(R, lin, U);
+    const int64_t ob = H.seg_end[lin], oe = H.seg_end[U];
+    if (Rc == 2 || Rc == 4 || Rc == 8) {
+      std::vector<PassChoice> pcs = greedy_passes(H, ob, oe, 10);
+      if (pcs.size() == 1) {
+        auto TL = std::make_shared<Half>();
+        TL->m = H.m;
+        TL->first_qubit = H.first_qubit;
+        Pass p;
+        p.t = 10;
+        p.T = pcs[0].T;
+        p.op_begin = 0;
+        for (int64_t oi : pcs[0].take) TL->dev_ops.push_back(to_dev(H.ops[oi], &p.T));
+        p.op_end = (int64_t)TL->dev_ops.size();
+        resolve_digits(*TL, p, R, U);
+        Transition tr;
+        tr.level_in = lin;
+        tr.level_out = U;
+        tr.passes.push_back(p);
+        TL->trans.push_back(tr);
+        finalize_half(*TL, P.opts.dtype == HSF_C64 ? 8 : 16);
+        if (TL->trans[0].passes.size() == 1) {
+          H.tleaf = TL;
+          H.tleaf_R = (int)Rc;
+        }
+      }
     }
   }
   if (std::getenv("HSF_DEBUG_PLAN")) {

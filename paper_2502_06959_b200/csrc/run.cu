@@ -45,6 +45,8 @@ struct DeviceState {
   void* jit_bop = nullptr;
   int jit_bop_nt = 256;
   void* jit_aop = nullptr;  // the same pass writing the swapped path-sum's M operand
+  // T-leaf variants (Half::tleaf) of each half's last transition: [variant 0 full / 1 fold][half]
+  void* jit_tl[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
 
   bool jit = false;                         // specialised pass kernels loaded
   unsigned long long* perm_tab = nullptr;   // caller -> internal index bits (partitions)
@@ -244,10 +246,22 @@ static DeviceState* ensure_device(Plan* P, int device) {
         owner.push_back({-1, 3});
       }
     }
+    // T-leaf variants (bitstring runs: the half the block gather reads transposed)
+    for (int v = 0; v < 2 && c64; ++v) {
+      if (v == 1 && P->fold_u0 < 0) continue;
+      for (int h = 0; h < 2; ++h) {
+        const Half& H = v ? P->half_fold[h] : P->half[h];
+        if (!H.tleaf) continue;
+        src.push_back(jit_tleaf_source(*H.tleaf, H.tleaf_R, c64, &P->coef));
+        owner.push_back({-2 - (2 * v + h), 0});
+      }
+    }
     std::vector<void*> fns = jit_compile_all(device, src);
     for (size_t i = 0; i < fns.size(); ++i) {
       if (owner[i].first == -1)
         (owner[i].second == 3 ? d->jit_aop : d->jit_bop) = fns[i];
+      else if (owner[i].first <= -2)
+        d->jit_tl[(-2 - owner[i].first) / 2][(-2 - owner[i].first) % 2] = fns[i];
       else
         d->jit_fn[owner[i].first][owner[i].second].push_back(fns[i]);
     }
@@ -299,6 +313,7 @@ struct Layout {
   long long Kp = 0;            // its transposed other half's padded row length
   long long n_blocks = 0;      // blocks of block_rows rows of the direct half
   int block_rows = 16;
+  bool tleaf[2] = {false, false};  // that half's last transition = its T-leaf pass (no leaves, no transpose)
   size_t off_grp = 0;          // counts[n_blocks] | offs[n_blocks + 1] | cursor[n_blocks] | sidx[n] (int32)
   size_t off_sbits = 0;        // sbits[n] (uint64): the samples' bitstrings in block order
   size_t tc_bytes = 0;
@@ -436,6 +451,13 @@ static Layout make_layout(const Plan& P, const hsf_run_args& a, size_t elem) {
       while (L.Kp < (long long)L.K) L.Kp *= 2;
       L.block_rows = rb;
       L.n_blocks = (1ll << mD) / rb;
+      const int th = 1 - dir;
+      const Half& HT = *L.half[th];
+      const char* te = std::getenv("HSF_TLEAF");
+      // (only without K padding: the T-leaf pass writes the K real columns)
+      L.tleaf[th] = HT.tleaf && P.opts.jit && L.var[th] <= 1 && (long long)L.K == L.Kp &&
+                    L.hp0[th] % (uint64_t)HT.tleaf_R == 0 &&
+                    L.hp1[th] % (uint64_t)HT.tleaf_R == 0 && !(te && te[0] == '0');
     }
     for (int h = 0; h < 2; ++h) {
       if (h == L.direct) continue;
@@ -614,6 +636,25 @@ static void run_half(const Plan& P, DeviceState* d, int h, const Layout& L, cuda
   for (size_t ti = 0; ti < H.trans.size(); ++ti) {
     const Transition& tr = H.trans[ti];
     const bool last = (ti + 1 == H.trans.size());
+    if (last && L.tleaf[h] && d->jit_tl[var][h]) {
+      // T-leaf: one CTA per (2^10-amplitude tile, parent) evaluates the
+      // parent's R leaves and writes them transposed into the gather operand
+      const Half& TL = *H.tleaf;
+      const int Rl = H.tleaf_R;
+      const uint64_t S_in = suffix_prod(ranks, tr.level_in);
+      JitLaunchArgs ja{prev_buf, ws + L.off_T[h], d->coef, (long long)hp0, 0, (long long)(hp0 / S_in),
+                       (long long)range_prod(ranks, tr.level_in, tr.level_out), 0u,
+                       h == 0 ? d->cp : nullptr, L.Kp};
+      const uint64_t parents = (hp1 - hp0) / (uint64_t)Rl;
+      for (uint64_t y0 = 0; y0 < parents; y0 += 65535) {
+        const uint64_t ny = std::min<uint64_t>(65535, parents - y0);
+        ja.node_first = (long long)(hp0 + y0 * Rl);
+        ja.node_local0 = (long long)(y0 * Rl);
+        jit_launch(d->jit_tl[var][h], (unsigned)(1u << (H.m - 10)), (unsigned)ny, (unsigned)(64 * Rl),
+                   jit_tleaf_smem_bytes(TL, Rl, true), st, ja, 0);
+      }
+      break;
+    }
     void* out = ws + (last ? L.off_leaves[h] : L.off_scratch[h][ti & 1]);
     const uint64_t S_out = suffix_prod(ranks, tr.level_out);
     const uint64_t first_out = hp0 / S_out;
@@ -747,6 +788,7 @@ static void prep_half(Plan* P, DeviceState* d, const Layout& L, int h, cudaStrea
   const C* leaves = (const C*)(ws + L.off_leaves[h]);
   if (L.bits_mode) {
     if (h == L.direct) return;  // read in place by the block gather
+    if (L.tleaf[h] && d->jit_tl[L.var[h]][h]) return;  // written transposed by the half's T-leaf pass
     C* T = (C*)(ws + L.off_T[h]);
     const long long ldo = L.direct >= 0 ? L.Kp : K;
     const char* tv = std::getenv("HSF_TRANSPOSE_V1");
@@ -1507,6 +1549,19 @@ size_t hsf_debug_pass_source(const hsf_plan_t* plan, int32_t variant, int32_t ha
                              size_t len) {
   try {
     const Plan* P = reinterpret_cast<const Plan*>(plan);
+    if (variant & 64) {  // bit 6: the T-leaf variant of that tree's last transition
+      const int v = variant & 3;
+      if (!P || half < 0 || half > 1 || v > 1 || (v == 1 && P->fold_u0 < 0)) return 0;
+      const Half& H = v ? P->half_fold[half] : P->half[half];
+      if (!H.tleaf) return 0;
+      const std::string s = jit_tleaf_source(*H.tleaf, H.tleaf_R, P->opts.dtype == HSF_C64, &P->coef);
+      if (buf && len) {
+        const size_t n = std::min(len - 1, s.size());
+        std::memcpy(buf, s.data(), n);
+        buf[n] = 0;
+      }
+      return s.size();
+    }
     const int cbq = (variant >> 2) & 3;  // bits 2-3: cluster-tier variant with 2^cb CTAs per tile
     const int store = (variant >> 4) & 3;  // bits 4-5: store mode (1 B operand, 2 transposed leaf)
     variant &= 3;                        // 0 full tree, 1 bitstring fold, 2 half-sided tail

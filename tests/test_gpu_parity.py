@@ -604,12 +604,14 @@ def test_fused_reduce_scatter_two_processes_ipc(torch):
 
 @pytest.mark.parametrize("name,path_range", [("c3", None), ("c3", (16, 48)), ("c5", None), ("c5", (3, 9))])
 @pytest.mark.parametrize("direct", ["-1", "0", "1"])
-def test_block_gather(torch, name, path_range, direct, monkeypatch):
+@pytest.mark.parametrize("tleaf", ["1", "0"])
+def test_block_gather(torch, name, path_range, direct, tleaf, monkeypatch):
     # bitstring path-sum: the block gather reading half B (direct=1) or half A
     # (direct=0, c_p applied while staging) from its leaves, or the per-sample
     # gather (-1), against the oracle's partial sums, with duplicates and
     # unaligned (unfolded, K not a power of two) ranges
     monkeypatch.setenv("HSF_GATHER_DIRECT", direct)
+    monkeypatch.setenv("HSF_TLEAF", tleaf)  # the transposed half's leaves written by its T-leaf pass
     inst = make_config(name, twin=True)
     bits = np.concatenate([inst.bitstrings, inst.bitstrings[:300]])  # duplicates
     n, g = O.parse_circuit(inst.text)
