@@ -147,7 +147,87 @@ struct Gen {
   }
 
 
+  // T-leaf kernel head: persistent CTAs over (tile, parent) items; the next
+  // item's parent tile is prefetched by cp.async into a double buffer while the
+  // groups (one 64-thread group per leaf) evaluate the current one
+  void header_multi(const std::string& name, int minb) {
+    const size_t elem = c64 ? 8 : 16;
+    o << "extern \"C\" __global__ void __launch_bounds__(" << nt << ", " << minb << ") " << name
+      << "(const JitArgs a) {\n";
+    o << "  typedef " << (c64 ? "float2" : "double2") << " C;\n";
+    o << "  constexpr u32 NT = 64u, NEL = 1u << " << t << ";\n";
+    o << "  constexpr u32 CB = 0u, LB = " << t << "u, LNEL = 1u << LB;\n  (void)CB; (void)NEL;\n";
+    o << "  constexpr u32 RANK = 0u;\n";
+    o << "  extern __shared__ __align__(128) unsigned char smem_raw[];\n";
+    o << "  const u32 GRP = threadIdx.x >> 6, TID = threadIdx.x & 63u;\n";
+    o << "  unsigned char* gbase = smem_raw + GRP * " << group_bytes() << "u;\n";
+    o << "  C* s = reinterpret_cast<C*>(gbase);\n";
+    o << "  C* stab = reinterpret_cast<C*>(gbase + (sizeof(C) << " << t << "));\n  (void)stab;\n";
+    o << "  C* pbuf = reinterpret_cast<C*>(smem_raw + " << (size_t)multi * group_bytes() << "u);\n";
+    o << "  const C* coef = reinterpret_cast<const C*>(a.coef);\n";
+    o << "  const C* srcb = reinterpret_cast<const C*>(a.src);\n";
+    o << "  constexpr long long NTILES = " << (1ll << (m - t)) << "ll;\n";
+    o << "  const long long n_items = NTILES * (long long)a.tile_free;  // tile_free = parents\n";
+    // tile map of an item's tile
+    std::vector<int> nonT;
+    for (int q = 0; q < m; ++q)
+      if (std::find(ps.T.begin(), ps.T.end(), q) == ps.T.end()) nonT.push_back(q);
+    std::vector<int> from(nonT.size()), to = nonT;
+    for (size_t j = 0; j < nonT.size(); ++j) from[j] = (int)j;
+    std::vector<int> pf, pt;
+    for (int i = 0; i < t; ++i) {
+      pf.push_back(i);
+      pt.push_back(pos2q[i]);
+    }
+    o << "  auto base_of = [&](u32 tile) -> u32 { return " << gather_expr("tile", from, to) << "; };\n";
+    o << "  auto GE = [&](u32 e) -> u32 { return " << gather_expr("e", pf, pt) << "; };\n";
+    o << "  auto prefetch = [&](long long it, u32 buf) {\n";
+    o << "    const long long parent = it / NTILES; const u32 pb = base_of((u32)(it % NTILES));\n";
+    o << "    const C* p_ = srcb + ((a.node_first + parent * " << multi << "ll) / a.src_div - a.src_first) * "
+      << (1ll << m) << "ll;\n";
+    o << "    C* d_ = pbuf + buf * LNEL;\n";
+    o << "    for (u32 e = 2u * threadIdx.x; e < LNEL; e += " << 2 * nt << "u) {\n";
+    o << "      const unsigned sa = (unsigned)__cvta_generic_to_shared(d_ + e);\n";
+    o << "      asm volatile(\"cp.async.cg.shared.global [%0], [%1], 16;\" :: \"r\"(sa), \"l\"(p_ + (pb | GE(e))) : \"memory\");\n";
+    o << "    }\n";
+    o << "    asm volatile(\"cp.async.commit_group;\" ::: \"memory\");\n  };\n";
+    o << "  long long it = blockIdx.x;\n  u32 buf = 0u;\n";
+    o << "  if (it < n_items) prefetch(it, 0u); else asm volatile(\"cp.async.commit_group;\" ::: \"memory\");\n";
+    o << "  for (; it < n_items; it += gridDim.x, buf ^= 1u) {\n";
+    o << "  if (it + gridDim.x < n_items) prefetch(it + gridDim.x, buf ^ 1u);\n";
+    o << "  else asm volatile(\"cp.async.commit_group;\" ::: \"memory\");\n";
+    o << "  asm volatile(\"cp.async.wait_group 1;\" ::: \"memory\");\n";
+    o << "  __syncthreads();\n";
+    o << "  const long long parent = it / NTILES;\n";
+    o << "  const u32 base = base_of((u32)(it % NTILES));\n";
+    o << "  auto G = [&](u32 e) -> u32 { return base | GE(e); };\n";
+    o << "  {\n  const long long node_g = a.node_first + parent * " << multi << "ll + GRP;\n";
+    // per-op table pointers (digit-resolved)
+    for (size_t i = 0; i < ops.size(); ++i) {
+      const DevOp& d = ops[i];
+      if (d.kind == OP_RPASS) continue;
+      std::string ptr = "coef + " + std::to_string(d.table) + "ll";
+      if (d.radix > 1)
+        ptr += " + ((node_g / " + std::to_string(d.div) + "ll) % " + std::to_string(d.radix) + "ll) * " +
+               std::to_string(d.stride) + "ll";
+      if (staged(d)) {
+        o << "  C* " << table(i) << " = stab + " << d.soff << ";\n";
+        o << "  { const C* g_ = " << ptr << "; for (u32 e = TID; e < " << (1u << d.k) << "u; e += NT) " << table(i)
+          << "[e] = __ldg(&g_[e]); }\n";
+      } else {
+        o << "  const C* __restrict__ " << table(i) << " = " << ptr << ";\n";
+      }
+    }
+    o << "  { const C* pp = pbuf + buf * LNEL; for (u32 e = TID; e < LNEL; e += NT) s[sw(e)] = pp[e]; }\n";
+    o << "  " << SYNCs << ";\n";
+    (void)elem;
+  }
+
   void header(const std::string& name, int minb) {
+    if (multi) {
+      header_multi(name, minb);
+      return;
+    }
     o << "extern \"C\" __global__ void __launch_bounds__(" << nt << ", " << minb << ") " << name
       << "(const JitArgs a) {\n";
     o << "  typedef " << (c64 ? "float2" : "double2") << " C;\n";
@@ -385,13 +465,13 @@ struct Gen {
     o << "  " << SYNCs << ";\n";
     if (multi) {
       o << "  }\n  __syncthreads();\n";
-      // transposed store of the CTA's `multi` leaves (group g's tile = leaf g):
+      // transposed store of the item's `multi` leaves (group g's tile = leaf g):
       // row G(e) of the gather operand gets columns k0 .. k0 + multi - 1
       // (x c_p for half A), two columns (16 B) per thread, a row's multi / 2
       // threads adjacent
       const int hp = multi / 2;
       o << "  { C* T = reinterpret_cast<C*>(a.dst); const C* cp = reinterpret_cast<const C*>(a.dst_lo);\n";
-      o << "    const long long k0 = a.node_local0 + (long long)blockIdx.y * " << multi << "ll;\n";
+      o << "    const long long k0 = a.node_local0 + parent * " << multi << "ll;\n";
       o << "#pragma unroll 4\n";
       o << "    for (u32 i = threadIdx.x; i < LNEL * " << hp << "u; i += " << multi * 64 << "u) {\n";
       o << "      const u32 e = i / " << hp << "u, c2 = 2u * (i % " << hp << "u);\n";
@@ -401,6 +481,8 @@ struct Gen {
       o << "      if (cp) { v0 = cmul(v0, cp[k0 + c2]); v1 = cmul(v1, cp[k0 + c2 + 1u]); }\n";
       o << "      st2(T + (long long)G(e) * a.ldw + k0 + c2, v0, v1);\n";
       o << "    }\n  }\n";
+      o << "  __syncthreads();\n  }\n";
+      o << "  asm volatile(\"cp.async.wait_group 0;\" ::: \"memory\");\n";
     } else if (operand_store) {
       o << "#pragma unroll 4\n";
       o << "  for (u32 e = 2u * threadIdx.x; e < LNEL; e += 2u * NT) " << (store_mode == 3 ? "st_aop" : "st_bop")
@@ -501,7 +583,9 @@ std::string jit_tleaf_source(const Half& TL, int leaves, bool c64, const std::ve
 size_t jit_tleaf_smem_bytes(const Half& TL, int leaves, bool c64) {
   const Pass& ps = TL.trans[0].passes[0];
   const size_t elem = c64 ? 8 : 16;
-  return (size_t)leaves * (((((elem << ps.t) + (size_t)ps.tbl_elems * elem) + 15) & ~(size_t)15) + 16);
+  // the groups' tiles + tables, then the double-buffered parent tile
+  return (size_t)leaves * (((((elem << ps.t) + (size_t)ps.tbl_elems * elem) + 15) & ~(size_t)15) + 16) +
+         2 * (elem << ps.t);
 }
 
 size_t jit_smem_bytes(const Pass& ps, bool c64, int cluster_bits) {

@@ -645,14 +645,14 @@ static void run_half(const Plan& P, DeviceState* d, int h, const Layout& L, cuda
       JitLaunchArgs ja{prev_buf, ws + L.off_T[h], d->coef, (long long)hp0, 0, (long long)(hp0 / S_in),
                        (long long)range_prod(ranks, tr.level_in, tr.level_out), 0u,
                        h == 0 ? d->cp : nullptr, L.Kp};
+      // persistent CTAs over (tile, parent) items (tile_free carries the parent count)
       const uint64_t parents = (hp1 - hp0) / (uint64_t)Rl;
-      for (uint64_t y0 = 0; y0 < parents; y0 += 65535) {
-        const uint64_t ny = std::min<uint64_t>(65535, parents - y0);
-        ja.node_first = (long long)(hp0 + y0 * Rl);
-        ja.node_local0 = (long long)(y0 * Rl);
-        jit_launch(d->jit_tl[var][h], (unsigned)(1u << (H.m - 10)), (unsigned)ny, (unsigned)(64 * Rl),
-                   jit_tleaf_smem_bytes(TL, Rl, true), st, ja, 0);
-      }
+      ja.tile_free = (unsigned)parents;
+      const size_t smem = jit_tleaf_smem_bytes(TL, Rl, true);
+      const int per_sm = std::max(1, std::min(2, (int)((227u << 10) / smem)));
+      const uint64_t items = parents << (H.m - 10);
+      jit_launch(d->jit_tl[var][h], (unsigned)std::min<uint64_t>(items, (uint64_t)per_sm * num_sms()), 1u,
+                 (unsigned)(64 * Rl), smem, st, ja, 0);
       break;
     }
     void* out = ws + (last ? L.off_leaves[h] : L.off_scratch[h][ti & 1]);
