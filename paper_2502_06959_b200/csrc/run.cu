@@ -1449,7 +1449,9 @@ hsf_status hsf_run_describe(const hsf_plan_t* plan, const hsf_run_args* args, hs
         const double mD = L.half[L.direct]->m, mT = L.half[1 - L.direct]->m;
         // D's leaves once, one padded T row + sample index, bits and result per sample
         o.core_bytes = K * std::ldexp(1.0, (int)mD) * elem + ns * ((double)L.Kp * elem + 4 + 8 + elem);
-        o.prep_bytes = 2.0 * K * std::ldexp(1.0, (int)mT) * elem;
+        // the T half's transpose (none when its T-leaf pass writes the rows: the
+        // leaf level's bytes, counted in sim_bytes, are then the operand's)
+        o.prep_bytes = L.tleaf[1 - L.direct] ? 0.0 : 2.0 * K * std::ldexp(1.0, (int)mT) * elem;
       } else {
         o.core = HSF_CORE_GATHER;
         o.core_bytes = ns * (2.0 * K * elem + 8 + elem);

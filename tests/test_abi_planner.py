@@ -333,3 +333,15 @@ def test_analytic_cascade_cnot_and_mixed_sides(hsf):
         assert np.allclose(a, b, rtol=1e-12, atol=1e-12)
     R = Plan("qubits 4\ncx 2 1\nh 2\ncx 2 0\n", 2, [[0, 1, 2]])  # H on the shared qubit: not a cascade
     assert R.unit_analytic == [False]
+
+
+def test_tleaf_variant_planned(hsf):
+    # bitstring runs: the transposed half's last transition gets a T-leaf pass
+    # (2^10-amplitude tiles, R leaves per parent, one 64-thread group per leaf);
+    # its generated source is inspectable and self-contained
+    from paper_2502_06959_b200 import Plan
+    inst = make_config("c5", n_bits=0)
+    P = Plan(inst.text, inst.n_low, inst.blocks)
+    src = P.pass_source(0, 0, variant=64 + 1)  # folded tree, half A
+    assert src and "bar.sync" in src and "cp.async.cg.shared.global" in src and "NTILES" in src
+    assert P.pass_source(0, 0, variant=64 + 3) is None  # no such tree variant
