@@ -644,7 +644,7 @@ static void run_half(const Plan& P, DeviceState* d, int h, const Layout& L, cuda
       const uint64_t S_in = suffix_prod(ranks, tr.level_in);
       JitLaunchArgs ja{prev_buf, ws + L.off_T[h], d->coef, (long long)hp0, 0, (long long)(hp0 / S_in),
                        (long long)range_prod(ranks, tr.level_in, tr.level_out), 0u,
-                       h == 0 ? d->cp : nullptr, L.Kp};
+                       h != L.direct ? d->cp : nullptr, L.Kp};  // c_p rides on the transposed half
       // persistent CTAs over (tile, parent) items (tile_free carries the parent count)
       const uint64_t parents = (hp1 - hp0) / (uint64_t)Rl;
       ja.tile_free = (unsigned)parents;
@@ -788,6 +788,10 @@ static void prep_half(Plan* P, DeviceState* d, const Layout& L, int h, cudaStrea
   const C* leaves = (const C*)(ws + L.off_leaves[h]);
   if (L.bits_mode) {
     if (h == L.direct) return;  // read in place by the block gather
+    // c_p (a3) is folded into the transposed half: half A in the per-sample
+    // gather, the non-direct half in the block gather (whose staging then is
+    // a plain copy)
+    const bool with_cp = L.direct >= 0 ? h != L.direct : h == 0;
     if (L.tleaf[h] && d->jit_tl[L.var[h]][h]) return;  // written transposed by the half's T-leaf pass
     C* T = (C*)(ws + L.off_T[h]);
     const long long ldo = L.direct >= 0 ? L.Kp : K;
@@ -795,11 +799,11 @@ static void prep_half(Plan* P, DeviceState* d, const Layout& L, int h, cudaStrea
     if (sizeof(R) == 4 && m >= 1 && !(tv && tv[0] == '1')) {  // 16 B accesses (c5: 0.43 ms per half before)
       dim3 g((unsigned)(((1ll << m) + 63) / 64), (unsigned)((ldo + 31) / 32));
       transpose_fold_c64_kernel<<<g, dim3(32, 8), 0, st>>>((const float2*)leaves, (float2*)T,
-                                                           h == 0 ? (const float2*)d->cp : nullptr, K, 1ll << m, ldo);
+                                                           with_cp ? (const float2*)d->cp : nullptr, K, 1ll << m, ldo);
     } else {
       if (ldo != K) fail(HSF_ERR_INVALID_ARG, "padded transpose needs the complex64 kernel");
       dim3 g((unsigned)(((1ll << m) + 31) / 32), (unsigned)((K + 31) / 32));
-      transpose_fold_kernel<C><<<g, dim3(32, 8), 0, st>>>(leaves, T, h == 0 ? (const C*)d->cp : nullptr, K, 1ll << m);
+      transpose_fold_kernel<C><<<g, dim3(32, 8), 0, st>>>(leaves, T, with_cp ? (const C*)d->cp : nullptr, K, 1ll << m);
     }
     CK(cudaGetLastError());
   } else if (L.prec != HSF_PREC_SIMT) {
@@ -915,7 +919,7 @@ static void run_core_bits(Plan* P, DeviceState* d, const Layout& L, const hsf_ru
     bp.D = (const float2*)(ws + L.off_leaves[L.direct]);
     bp.ldD = 1ll << L.half[L.direct]->m;
     bp.K = K;
-    bp.cpD = L.direct == 0 ? (const float2*)d->cp : nullptr;
+    bp.cpD = nullptr;  // c_p is in the transposed half
     bp.T = (const float4*)(ws + L.off_T[1 - L.direct]);
     bp.offs = (const int*)(ws + L.off_grp) + nblk;
     bp.sidx = bp.offs + 2 * nblk + 1;
@@ -937,7 +941,7 @@ static void run_core_bits(Plan* P, DeviceState* d, const Layout& L, const hsf_ru
     auto launch = [&](auto kern, int nt) {
       static std::vector<const void*> attr;  // kernels whose SMEM limit is raised (all share one type)
       if (std::find(attr.begin(), attr.end(), (const void*)kern) == attr.end()) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 32 * 512 * 8));
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         attr.push_back((const void*)kern);
       }
       int per_sm = 0;
