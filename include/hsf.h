@@ -305,6 +305,9 @@ typedef struct {
   double core_bytes;          /* path-sum kernel: operands read once + result written */
   double core_flops_useful;   /* 8 K per output amplitude (complex multiply-add) */
   double core_flops_executed; /* tensor-core flops actually issued (split products, padding) */
+  int32_t tleaf_half;         /* bitstring runs: the half whose last transition is a T-leaf pass
+                                 (writes the gather operand rows directly), -1 none */
+  int32_t tleaf_leaves;       /* its leaves per parent (2, 4 or 8) */
 } hsf_run_desc;
 
 hsf_status hsf_run_describe(const hsf_plan_t* plan, const hsf_run_args* args, hsf_run_desc* out);

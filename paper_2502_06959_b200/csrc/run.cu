@@ -1435,6 +1435,8 @@ hsf_status hsf_run_describe(const hsf_plan_t* plan, const hsf_run_args* args, hs
     const double K = (double)L.K, MB = std::ldexp(1.0, nB);
     o.K = L.K;
     o.direct_half = L.direct;
+    o.tleaf_half = L.tleaf[0] ? 0 : L.tleaf[1] ? 1 : -1;
+    o.tleaf_leaves = o.tleaf_half >= 0 ? L.half[o.tleaf_half]->tleaf_R : 0;
     o.tree_variant_a = L.var[0];
     o.tree_variant_b = L.var[1];
     for (int h = 0; h < 2; ++h) {  // this range's share of the evaluated tree

@@ -75,7 +75,7 @@ class _RunDesc(C.Structure):
                 ("tree_variant_b", C.c_int32), ("K", C.c_uint64), ("rows", C.c_uint64), ("tc_products", C.c_int32),
                 ("kernel_launches", C.c_int32), ("sim_bytes", C.c_double * 2), ("sim_flops", C.c_double * 2),
                 ("prep_bytes", C.c_double), ("core_bytes", C.c_double), ("core_flops_useful", C.c_double),
-                ("core_flops_executed", C.c_double)]
+                ("core_flops_executed", C.c_double), ("tleaf_half", C.c_int32), ("tleaf_leaves", C.c_int32)]
 
 
 CORE_KINDS = ["simt", "tc_pair", "tc_single", "tc_swapped", "gather", "block_gather"]
@@ -462,7 +462,8 @@ class Plan:
                 "tc_products": d.tc_products, "kernel_launches": d.kernel_launches,
                 "sim_bytes": tuple(d.sim_bytes), "sim_flops": tuple(d.sim_flops), "prep_bytes": d.prep_bytes,
                 "core_bytes": d.core_bytes, "core_flops_useful": d.core_flops_useful,
-                "core_flops_executed": d.core_flops_executed}
+                "core_flops_executed": d.core_flops_executed, "tleaf_half": d.tleaf_half,
+                "tleaf_leaves": d.tleaf_leaves}
 
     def workspace_bytes(self, bitstrings_count: int = 0, path_range=None, row_range=None, precision="auto") -> int:
         a = self._args(1, True, 1 if bitstrings_count else None, bitstrings_count, True, path_range, row_range,

@@ -345,3 +345,10 @@ def test_tleaf_variant_planned(hsf):
     src = P.pass_source(0, 0, variant=64 + 1)  # folded tree, half A
     assert src and "bar.sync" in src and "cp.async.cg.shared.global" in src and "NTILES" in src
     assert P.pass_source(0, 0, variant=64 + 3) is None  # no such tree variant
+    d = P.describe(1 << 22)  # c5 as benched: half B read in place, half A through its T-leaf pass
+    assert (d["direct_half"], d["tleaf_half"], d["tleaf_leaves"]) == (1, 0, 8) and d["prep_bytes"] == 0
+    assert P.describe(1 << 22, path_range=(2, 10))["tleaf_half"] == -1  # K = 4 padded: no T-leaf
+    c3 = make_config("c3", n_bits=0)
+    Q = Plan(c3.text, c3.n_low, c3.blocks)
+    e = Q.describe(1 << 20)
+    assert (e["direct_half"], e["tleaf_half"], e["tleaf_leaves"]) == (0, 1, 4)
