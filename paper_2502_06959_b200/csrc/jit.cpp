@@ -105,6 +105,60 @@ struct Gen {
       std::snprintf(b, sizeof b, "make_double2(%a, %a)", v.real(), v.imag());
     return b;
   }
+  // one real literal of the run dtype
+  std::string rl(double x) const {
+    char b[64];
+    if (c64)
+      std::snprintf(b, sizeof b, "%af", (double)(float)x);
+    else
+      std::snprintf(b, sizeof b, "%a", x);
+    return b;
+  }
+  // 1-qubit literal gate on register slot J of the 16 register amplitudes,
+  // written out per pair with the terms of exactly-zero matrix parts dropped:
+  // RX (real diagonal, imaginary off-diagonal) and H (real) cost 4 real
+  // multiply-adds per amplitude instead of 8 (the QAOA mixers of c4 / q*)
+  void r1_literal(int J, const DevOp& d) {
+    cd m[4];
+    for (int e = 0; e < 4; ++e) {
+      const cd v = (*coef)[(size_t)(d.table + e)];
+      m[e] = c64 ? cd((float)v.real(), (float)v.imag()) : v;
+    }
+    // out.re = sum_j (m_j.re x_j.re - m_j.im x_j.im); out.im = sum_j (m_j.re x_j.im + m_j.im x_j.re)
+    auto expr = [&](const cd& m0, const cd& m1, bool im) {
+      struct T {
+        double c;
+        std::string x;
+      };
+      std::vector<T> ts;
+      auto add = [&](double c, const std::string& x) {
+        if (c != 0.0) ts.push_back({c, x});
+      };
+      if (!im) {
+        add(m0.real(), "a.x");
+        add(-m0.imag(), "a.y");
+        add(m1.real(), "b.x");
+        add(-m1.imag(), "b.y");
+      } else {
+        add(m0.real(), "a.y");
+        add(m0.imag(), "a.x");
+        add(m1.real(), "b.y");
+        add(m1.imag(), "b.x");
+      }
+      if (ts.empty()) return rl(0.0);
+      std::string e = ts[0].x + " * " + rl(ts[0].c);
+      for (size_t k = 1; k < ts.size(); ++k) e = std::string(c64 ? "fmaf(" : "fma(") + ts[k].x + ", " + rl(ts[k].c) + ", " + e + ")";
+      return e;
+    };
+    const char* mk = c64 ? "make_float2" : "make_double2";
+    for (int i = 0; i < 16; ++i) {
+      if (i & (1 << J)) continue;
+      const int j = i | (1 << J);
+      o << "    { const C a = v[" << i << "], b = v[" << j << "]; v[" << i << "] = " << mk << "(" << expr(m[0], m[1], false)
+        << ", " << expr(m[0], m[1], true) << "); v[" << j << "] = " << mk << "(" << expr(m[2], m[3], false) << ", "
+        << expr(m[2], m[3], true) << "); }\n";
+    }
+  }
   std::string mat(const DevOp& d, int i, int e) const {
     return literal(d) ? lit(d.table + e) : "__ldg(&" + table(i) + "[" + std::to_string(e) + "])";
   }
@@ -392,8 +446,7 @@ struct Gen {
       const DevOp& d = ops[r];
       if (d.kind == OP_R1) {
         if (literal(d))
-          o << "    r1c<" << d.q[0] << ">(v, " << lit(d.table) << ", " << lit(d.table + 1) << ", " << lit(d.table + 2)
-            << ", " << lit(d.table + 3) << ");\n";
+          r1_literal(d.q[0], d);
         else
           o << "    r1<" << d.q[0] << ">(v, " << table((int)r) << ");\n";
       } else {  // diagonal: index of element k = i0 | IK[k]
