@@ -953,7 +953,9 @@ static void run_core_bits(Plan* P, DeviceState* d, const Layout& L, const hsf_ru
     // default U by row length (c5, Kp = 128: U = 4 -> gather 1.09 ms, U = 2 1.38;
     // c3, Kp = 256: U = 2 -> 0.25 ms, U = 4 0.45 -- 64 float4 of rows per
     // thread spill at 4 CTAs per SM)
-    const int cfg = gather_cfg(), MB = (cfg / 10) % 10;
+    // min CTAs/SM: 4 (64 registers) for Kp <= 128; 3 for Kp = 256 (c3: 0.254 vs 0.273 ms)
+    const int cfg = gather_cfg(),
+              MB = std::getenv("HSF_GATHER_CFG") ? (cfg / 10) % 10 : (L.Kp >= 256 ? 3 : 4);
     const int U = std::getenv("HSF_GATHER_CFG") ? cfg % 10 : L.Kp <= 64 ? 8 : L.Kp == 128 ? 4 : L.Kp == 256 ? 2 : 1;
 #define HSF_GB(NF, U_, RB, MB_) launch(gather_block_c64_kernel<NF, U_, RB, 256, MB_>, 256)
 #define HSF_GB_MB(NF, U_, RB)     \
