@@ -65,6 +65,13 @@ std::string gather_expr(const std::string& x, const std::vector<int>& from, cons
   return "(" + s + ")";
 }
 
+// T-leaf group stride: tile + tables, then padded to 32 mod 64 bytes so that
+// the transposed store's reads of groups c2 = 0, 2, 4, 6 (same element, four
+// lanes) fall on two 64 B bank halves instead of one (8-way -> 2 wavefronts)
+static size_t tleaf_group_bytes(int t, long long tbl_elems, size_t elem) {
+  return ((((elem << t) + (size_t)tbl_elems * elem) + 63) & ~(size_t)63) + 32;
+}
+
 struct Gen {
   std::ostringstream o;
   const Half& H;
@@ -89,10 +96,7 @@ struct Gen {
   std::string table(int i) const { return "M" + std::to_string(i); }
   // T-leaf: one group's shared memory (its tile + staged tables; 16 B more so
   // consecutive groups' tiles start on different banks)
-  size_t group_bytes() const {
-    const size_t elem = c64 ? 8 : 16;
-    return ((((elem << t) + (size_t)ps.tbl_elems * elem) + 15) & ~(size_t)15) + 16;
-  }
+  size_t group_bytes() const { return tleaf_group_bytes(t, ps.tbl_elems, c64 ? 8 : 16); }
   // fixed (non-factor) gate entries become literals in the generated code: no
   // dependent table loads on the gate chain (exact: %a of the run-dtype value)
   bool literal(const DevOp& d) const { return coef && d.radix <= 1 && (d.kind == OP_R1 || d.kind == OP_DENSE); }
@@ -174,6 +178,9 @@ struct Gen {
   }
 
   int multi = 0;  // T-leaf variant: leaves per CTA (0 = one node per CTA)
+  // T-leaf: the first op is a register pass, which loads straight from the
+  // (swizzled) parent tile instead of a per-group copy of it
+  bool pb_first = false;
   // T-leaf: one 64-thread group per leaf (its own tile and tables, named
   // barrier 1 + group); elsewhere the whole CTA
   std::string TIDs = "threadIdx.x", SYNCs = "__syncthreads()";
@@ -240,10 +247,19 @@ struct Gen {
     o << "    const C* p_ = srcb + ((a.node_first + parent * " << multi << "ll) / a.src_div - a.src_first) * "
       << (1ll << m) << "ll;\n";
     o << "    C* d_ = pbuf + buf * LNEL;\n";
-    o << "    for (u32 e = 2u * threadIdx.x; e < LNEL; e += " << 2 * nt << "u) {\n";
-    o << "      const unsigned sa = (unsigned)__cvta_generic_to_shared(d_ + e);\n";
-    o << "      asm volatile(\"cp.async.cg.shared.global [%0], [%1], 16;\" :: \"r\"(sa), \"l\"(p_ + (pb | GE(e))) : \"memory\");\n";
-    o << "    }\n";
+    if (pb_first) {
+      // swizzled like the group tiles (8 B copies: the swizzle may swap a
+      // pair's halves), so the first register pass reads it in place
+      o << "    for (u32 e = threadIdx.x; e < LNEL; e += " << nt << "u) {\n";
+      o << "      const unsigned sa = (unsigned)__cvta_generic_to_shared(d_ + sw((int)e));\n";
+      o << "      asm volatile(\"cp.async.ca.shared.global [%0], [%1], 8;\" :: \"r\"(sa), \"l\"(p_ + (pb | GE(e))) : \"memory\");\n";
+      o << "    }\n";
+    } else {
+      o << "    for (u32 e = 2u * threadIdx.x; e < LNEL; e += " << 2 * nt << "u) {\n";
+      o << "      const unsigned sa = (unsigned)__cvta_generic_to_shared(d_ + e);\n";
+      o << "      asm volatile(\"cp.async.cg.shared.global [%0], [%1], 16;\" :: \"r\"(sa), \"l\"(p_ + (pb | GE(e))) : \"memory\");\n";
+      o << "    }\n";
+    }
     o << "    asm volatile(\"cp.async.commit_group;\" ::: \"memory\");\n  };\n";
     o << "  long long it = blockIdx.x;\n  u32 buf = 0u;\n";
     o << "  if (it < n_items) prefetch(it, 0u); else asm volatile(\"cp.async.commit_group;\" ::: \"memory\");\n";
@@ -272,8 +288,12 @@ struct Gen {
         o << "  const C* __restrict__ " << table(i) << " = " << ptr << ";\n";
       }
     }
-    o << "  { const C* pp = pbuf + buf * LNEL; for (u32 e = TID; e < LNEL; e += NT) s[sw(e)] = pp[e]; }\n";
-    o << "  " << SYNCs << ";\n";
+    if (pb_first) {
+      o << "  const C* pb_ = pbuf + buf * LNEL;\n";
+    } else {
+      o << "  { const C* pp = pbuf + buf * LNEL; for (u32 e = TID; e < LNEL; e += NT) s[sw(e)] = pp[e]; }\n";
+      o << "  " << SYNCs << ";\n";
+    }
     (void)elem;
   }
 
@@ -434,13 +454,19 @@ struct Gen {
       const uint32_t swe = e ^ ((e >> 4) & 15u);
       return std::string("s[sb ^ ") + std::to_string(swe) + "u]";
     };
+    const bool from_pb = pb_first && i == 0;
+    auto elk_ld = [&](uint32_t e) {
+      if (!from_pb) return elk(e);
+      const uint32_t swe = e ^ ((e >> 4) & 15u);
+      return std::string("pb_[sb ^ ") + std::to_string(swe) + "u]";
+    };
     uint32_t ek[16];
     for (int k = 0; k < 16; ++k) {
       uint32_t e = 0;
       for (int j = 0; j < 4; ++j)
         if ((k >> j) & 1) e |= 1u << pos[j];
       ek[k] = e;
-      o << "    v[" << k << "] = " << elk(e) << ";\n";
+      o << "    v[" << k << "] = " << elk_ld(e) << ";\n";
     }
     for (size_t r = i + 1; r <= i + (size_t)n; ++r) {
       const DevOp& d = ops[r];
@@ -523,15 +549,19 @@ struct Gen {
       // (x c_p for half A), two columns (16 B) per thread, a row's multi / 2
       // threads adjacent
       const int hp = multi / 2;
+      // (a thread's two columns are loop-invariant: their c_p loaded once)
       o << "  { C* T = reinterpret_cast<C*>(a.dst); const C* cp = reinterpret_cast<const C*>(a.dst_lo);\n";
       o << "    const long long k0 = a.node_local0 + parent * " << multi << "ll;\n";
+      o << "    const u32 c2 = 2u * (threadIdx.x % " << hp << "u);\n";
+      o << "    const C* t0 = reinterpret_cast<const C*>(smem_raw + c2 * " << group_bytes() << "u);\n";
+      o << "    const C* t1 = reinterpret_cast<const C*>(smem_raw + (c2 + 1u) * " << group_bytes() << "u);\n";
+      o << "    const bool hc = cp != nullptr; C w0 = czero<C>(), w1 = czero<C>();\n";
+      o << "    if (hc) { w0 = cp[k0 + c2]; w1 = cp[k0 + c2 + 1u]; }\n";
       o << "#pragma unroll 4\n";
       o << "    for (u32 i = threadIdx.x; i < LNEL * " << hp << "u; i += " << multi * 64 << "u) {\n";
-      o << "      const u32 e = i / " << hp << "u, c2 = 2u * (i % " << hp << "u);\n";
-      o << "      const C* t0 = reinterpret_cast<const C*>(smem_raw + c2 * " << group_bytes() << "u);\n";
-      o << "      const C* t1 = reinterpret_cast<const C*>(smem_raw + (c2 + 1u) * " << group_bytes() << "u);\n";
+      o << "      const u32 e = i / " << hp << "u;\n";
       o << "      C v0 = t0[sw(e)], v1 = t1[sw(e)];\n";
-      o << "      if (cp) { v0 = cmul(v0, cp[k0 + c2]); v1 = cmul(v1, cp[k0 + c2 + 1u]); }\n";
+      o << "      if (hc) { v0 = cmul(v0, w0); v1 = cmul(v1, w1); }\n";
       o << "      st2(T + (long long)G(e) * a.ldw + k0 + c2, v0, v1);\n";
       o << "    }\n  }\n";
       o << "  __syncthreads();\n  }\n";
@@ -628,6 +658,7 @@ std::string jit_tleaf_source(const Half& TL, int leaves, bool c64, const std::ve
   const Pass& ps = TL.trans[0].passes[0];
   Gen g(TL, ps, c64, coef);
   g.multi = leaves;
+  g.pb_first = !g.ops.empty() && g.ops[0].kind == OP_RPASS && !std::getenv("HSF_TLEAF_COPY");
   g.TIDs = "TID";
   g.SYNCs = "asm volatile(\"bar.sync %0, 64;\" :: \"r\"(1u + GRP) : \"memory\")";
   return std::string(kPrelude) + "\n" + g.build("hsf_jit_pass", 64 * leaves, 0, 0);
@@ -637,8 +668,7 @@ size_t jit_tleaf_smem_bytes(const Half& TL, int leaves, bool c64) {
   const Pass& ps = TL.trans[0].passes[0];
   const size_t elem = c64 ? 8 : 16;
   // the groups' tiles + tables, then the double-buffered parent tile
-  return (size_t)leaves * (((((elem << ps.t) + (size_t)ps.tbl_elems * elem) + 15) & ~(size_t)15) + 16) +
-         2 * (elem << ps.t);
+  return (size_t)leaves * tleaf_group_bytes(ps.t, ps.tbl_elems, elem) + 2 * (elem << ps.t);
 }
 
 size_t jit_smem_bytes(const Pass& ps, bool c64, int cluster_bits) {
