@@ -85,9 +85,11 @@ typedef struct {
   double log2_path_budget;       /* default 26 */
   int32_t individual;            /* 1 => ignore blocks, cut every crossing gate alone */
   int32_t tile_qubits;           /* in [10,13]: amplitudes per SMEM tile = 2^tile_qubits for
-                                    halves larger than the SMEM-resident limit;
-                                    0 => auto (default): 12, widened to 13 for
-                                    complex64 where that saves an HBM pass */
+                                    halves larger than the SMEM-resident limit (2^14
+                                    complex64 / 2^13 complex128 amplitudes: whole state in
+                                    one CTA) and for any half with m > tile_qubits (forces
+                                    the tiled tier); 0 => auto (default): 12, widened to 13
+                                    for complex64 where that saves an HBM pass */
   int32_t fuse_gates;            /* 1 (default) => host gate fusion */
   int32_t hoist_gates;           /* 1 (default) => commutation-aware path tree: a local gate
                                     is hoisted above every cut unit whose factors it commutes
@@ -121,6 +123,11 @@ typedef struct {
                                     gets its rank-<=2 Schmidt factors in closed form (no block
                                     assembly or SVD; sigma equal to the SVD's); 0 => numeric
                                     route for every block */
+  int32_t smem_tier;             /* K1 tier (whole half state in one CTA's shared memory,
+                                    north_star part (1)): 0 (default) => halves up to 2^13
+                                    complex64 / 2^12 complex128 always, 2^14 / 2^13 (128 KiB,
+                                    one CTA per SM) where the planner's cost model prefers it
+                                    to 2^12-2^13 tiles; 1 => every half that fits */
 } hsf_plan_opts;
 
 typedef struct hsf_plan_s hsf_plan_t; /* opaque */
@@ -202,6 +209,9 @@ typedef struct {
   double tail_tree_flops_a, tail_tree_flops_b; /* same for the half-sided fold trees (0 if none) */
   int32_t n_analytic_units;     /* units decomposed by the analytic cascade route */
   const int32_t* unit_analytic; /* [n_units] 1 if that unit's factors are closed-form */
+  int32_t whole_state_a, whole_state_b; /* 1: K1 tier -- each pass holds the whole half state in one
+                                           CTA's shared memory (2^m <= 2^14 complex64 / 2^13
+                                           complex128); 0: K2 tiles streamed through HBM/L2 */
 } hsf_plan_info;
 
 /* Pointers in *info stay valid until hsf_plan_free. */

@@ -1113,11 +1113,19 @@ static void build_half(Plan& P, int h, const std::vector<SchedItem>& order, int 
   // where a transition a -> b writes every level-b node once per pass, reads
   // its level-a parent (siblings mostly hit L2) and re-applies all ops of the
   // skipped levels per child.  The leaves (level U) are always materialised.
-  const int smem_limit = (P.opts.dtype == HSF_C64) ? 13 : 12;
+  // K1 tier: the whole half state in one CTA's shared memory (2^14 complex64
+  // = 128 KiB of the 227 KiB; 2^13 complex128)
+  int smem_limit = (P.opts.dtype == HSF_C64) ? 14 : 13;
+  if (const char* e = std::getenv("HSF_SMEM_LIMIT")) smem_limit = std::atoi(e) - (P.opts.dtype == HSF_C64 ? 0 : 1);
   const int t = std::min(H.m, P.opts.tile_qubits > 0 ? P.opts.tile_qubits : 12);
   const int t_max = (P.opts.tile_qubits == 0 && P.opts.dtype == HSF_C64) ? 13 : t;
-  const bool whole = H.m <= smem_limit;
-  {
+  // (tile_qubits > 0 below m forces the tiled tier: tests, tile sweeps)
+  const bool whole_fits = H.m <= smem_limit && !(P.opts.tile_qubits > 0 && P.opts.tile_qubits < H.m);
+  // 2^14 complex64 (128 KiB: one CTA per SM) is K1 only where the cost model
+  // prefers it to tiles; smaller halves always are (3+ CTAs per SM)
+  const int k1_always = (P.opts.dtype == HSF_C64) ? 13 : 12;
+  bool whole = whole_fits;
+  auto run_dp = [&](bool whole) {
     const double elem = (P.opts.dtype == HSF_C64) ? 8.0 : 16.0;
     const double amps = std::ldexp(1.0, H.m), S = amps * elem;
     auto nodes = [&](int l) { return (double)range_prod(R, 0, l); };
@@ -1143,8 +1151,11 @@ static void build_half(Plan& P, int h, const std::vector<SchedItem>& order, int 
           fma += 4.0 * std::ldexp(1.0, op.k);
         }
       }
-      // narrow levels run on few SMs: the op chain's throughput scales with CTAs
-      const double par = std::min(1.0, Nb * tiles / (2.0 * 148));
+      // narrow levels run on few SMs: the op chain's throughput scales with
+      // CTAs; a 128 KiB whole state is one 8-warp CTA per SM (about half the
+      // issue rate of the tiled passes' 3-4 CTAs)
+      const bool big = whole && H.m > k1_always;
+      const double par = std::min(1.0, Nb * tiles / ((big ? 1.0 : 2.0) * 148)) * (big ? 0.5 : 1.0);
       return 3e-6 * (double)np + bytes / 5e12 + table / 15e12 + fma * amps * Nb / (2.5e13 * par);
     };
     std::vector<double> best(U + 1, 1e300);
@@ -1160,10 +1171,24 @@ static void build_half(Plan& P, int h, const std::vector<SchedItem>& order, int 
         }
       }
     }
-    H.materialized.clear();
-    for (int l = U; l >= 0; l = from[l]) H.materialized.push_back(l);
-    std::reverse(H.materialized.begin(), H.materialized.end());
-    H.est_ms = best[U] * 1e3;
+    std::vector<int> mat;
+    for (int l = U; l >= 0; l = from[l]) mat.push_back(l);
+    std::reverse(mat.begin(), mat.end());
+    return std::make_pair(best[U], mat);
+  };
+  {
+    auto r = run_dp(whole);
+    if (whole && H.m > k1_always && P.opts.smem_tier != 1) {
+      auto rt = run_dp(false);
+      if (std::getenv("HSF_DEBUG_PLAN"))
+        std::fprintf(stderr, "K1 tier 2^%d: whole %.3f ms vs tiled %.3f ms\n", H.m, r.first * 1e3, rt.first * 1e3);
+      if (rt.first < r.first) {
+        whole = false;
+        r = rt;
+      }
+    }
+    H.materialized = r.second;
+    H.est_ms = r.first * 1e3;
   }
   // transitions + passes
   H.trans.clear();

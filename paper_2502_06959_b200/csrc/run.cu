@@ -1300,6 +1300,7 @@ hsf_status hsf_plan_opts_default(hsf_plan_opts* o) {
   o->jit = 1;
   o->graphs = 1;
   o->analytic_cascades = 1;
+  o->smem_tier = 0;
   o->partition_b = 0;
   return HSF_OK;
 }
@@ -1369,6 +1370,11 @@ hsf_status hsf_plan_info_get(const hsf_plan_t* plan, hsf_plan_info* info) {
     info->n_analytic_units = 0;
     for (int32_t x : P->unit_analytic) info->n_analytic_units += x;
     info->unit_analytic = P->unit_analytic.data();
+    for (int h = 0; h < 2; ++h) {
+      const Half& H = P->half[h];
+      (h ? info->whole_state_b : info->whole_state_a) =
+          !H.trans.empty() && !H.trans[0].passes.empty() && H.trans[0].passes[0].t == H.m ? 1 : 0;
+    }
     info->n_joint_blocks = 0;
     for (const auto& un : P->units) info->n_joint_blocks += un.gids.size() > 1 ? 1 : 0;
   })

@@ -343,7 +343,7 @@ def test_tleaf_variant_planned(hsf):
     inst = make_config("c5", n_bits=0)
     P = Plan(inst.text, inst.n_low, inst.blocks)
     src = P.pass_source(0, 0, variant=64 + 1)  # folded tree, half A
-    assert src and "bar.sync" in src and "cp.async.cg.shared.global" in src and "NTILES" in src
+    assert src and "bar.sync" in src and "cp.async.ca.shared.global" in src and "pb_[sb ^" in src and "NTILES" in src
     assert P.pass_source(0, 0, variant=64 + 3) is None  # no such tree variant
     d = P.describe(1 << 22)  # c5 as benched: half B read in place, half A through its T-leaf pass
     assert (d["direct_half"], d["tleaf_half"], d["tleaf_leaves"]) == (1, 0, 8) and d["prep_bytes"] == 0
@@ -352,3 +352,17 @@ def test_tleaf_variant_planned(hsf):
     Q = Plan(c3.text, c3.n_low, c3.blocks)
     e = Q.describe(1 << 20)
     assert (e["direct_half"], e["tleaf_half"], e["tleaf_leaves"]) == (0, 1, 4)
+
+
+def test_smem_tier_choice(hsf):
+    # K1 tier limits: 2^13 complex64 always whole-state; 2^14 complex64 whole
+    # with smem_tier = 1 (128 KiB per CTA), by the cost model otherwise; 2^15
+    # never (256 KiB does not fit in 227 KiB of shared memory)
+    from paper_2502_06959_b200 import Plan
+    for m, tier, want in [(13, 0, True), (14, 1, True), (15, 1, False)]:
+        inst = make_config("c5", n=2 * m, n_low=m, layers=4, fanout=4, n_bits=0)
+        P = Plan(inst.text, inst.n_low, inst.blocks, smem_tier=tier)
+        assert P.whole_state == (want, want), (m, tier, P.whole_state)
+    inst = make_config("c5", n=26, n_low=13, layers=4, fanout=4, n_bits=0)
+    assert Plan(inst.text, inst.n_low, inst.blocks, dtype="c128", smem_tier=1).whole_state == (True, True)
+    assert Plan(inst.text, inst.n_low, inst.blocks, tile_qubits=11).whole_state == (False, False)

@@ -262,6 +262,30 @@ def test_c5_full_size_partial_paths(torch):
     check(got, ref, "c64")
 
 
+@pytest.mark.parametrize("name,dtype,m", [("c3", "c64", 14), ("c5", "c64", 14), ("c5", "c128", 13),
+                                          ("c3", "c64", 15), ("c5", "c64", 13)])
+def test_smem_resident_tier_boundary(torch, name, dtype, m):
+    # K1 tier (north_star: one CTA owns a path's half state when 2^m fits in
+    # shared memory): with smem_tier = 1, 2^14 complex64 = 128 KiB and 2^13
+    # complex128 run as whole-state passes; 2^15 complex64 (256 KiB) does not
+    # fit and is tiled.  By default the 128 KiB states go K1 only where the
+    # cost model prefers it (here: tiles -- measured 0.51 vs 1.10 ms on a
+    # 14|14 brickwork, scripts/k1_tier.py); 2^13 complex64 always is K1.
+    kw = dict(n=2 * m, n_low=m, n_bits=1 << 14)
+    kw.update(dict(depth=8) if name == "c3" else dict(layers=4, fanout=4))
+    inst = make_config(name, **kw)
+    n, g = O.parse_circuit(inst.text)
+    Po = O.plan(n, g, inst.n_low, inst.blocks)
+    A, B, c = O.half_states(Po, 0, 8)
+    ref = O.recombine_bits(A, B, c, inst.bitstrings, inst.n_low)
+    fits = (m <= 14) if dtype == "c64" else (m <= 13)
+    for tier in (1, 0):
+        got, P = gpu_bits(torch, inst, inst.bitstrings, dtype=dtype, path_range=(0, 8), smem_tier=tier)
+        whole = fits and (tier == 1 or m <= (13 if dtype == "c64" else 12))
+        assert P.whole_state == (whole, whole), (tier, P.whole_state)
+        check(got, ref, dtype)
+
+
 def test_c5_full_run_norm_sampled(torch):
     # all 256 paths, all 2^22 bitstrings: |amp|^2 averages to 2^-40 per sample
     inst = make_config("c5")
