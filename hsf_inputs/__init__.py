@@ -14,6 +14,7 @@ from .circuits import (  # noqa: F401
     make_c3,
     make_c4,
     make_c5,
+    make_brick_block,
     make_sbm_qaoa,
     make_table2,
     TABLE2,

@@ -304,6 +304,30 @@ def make_table2(name: str, seed: int | None = None, prefix: int = 10 ** 6) -> In
     return inst
 
 
+# ------------------------------------------------------- one large dense block
+def make_brick_block(na: int, nb: int, depth: int, seed: int = 0, n: int = 16, n_low: int = 8,
+                     n_bits: int = 0) -> Instance:
+    """One joint block of `depth` brickwork layers (Haar SU(2) on every block
+    qubit, then CZ on alternating neighbour pairs) on the nb + na qubits around
+    the cut [n_low - nb, n_low + na), after a Haar layer on all n qubits and
+    before another: the large dense blocks the paper's cost remark is about
+    (P:192-194), for the sequential factor route."""
+    rng = np.random.default_rng([seed, 11])
+    qs = list(range(n_low - nb, n_low + na))
+    g = [_u1(q, rng) for q in range(n)]
+    blk = []
+    for L in range(depth):
+        for q in qs:
+            blk.append(len(g))
+            g.append(_u1(q, rng))
+        for a in range(L % 2, len(qs) - 1, 2):
+            blk.append(len(g))
+            g.append(("cz", (), (qs[a], qs[a + 1]), None))
+    g += [_u1(q, rng) for q in range(n)]
+    bits = _bitstrings(seed, n, n_bits) if n_bits else None
+    return Instance("brick%d+%d" % (nb, na), n, n_low, g, [blk], bits, "c64", {"seed": seed, "depth": depth})
+
+
 # ---------------------------------------------------------- random small sweeps
 _NAMED_1Q = ("h", "x", "z", "rx", "rz")
 _NAMED_2Q = ("cz", "cx", "swap", "cp", "rzz")

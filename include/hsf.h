@@ -128,6 +128,14 @@ typedef struct {
                                     complex64 / 2^12 complex128 always, 2^14 / 2^13 (128 KiB,
                                     one CTA per SM) where the planner's cost model prefers it
                                     to 2^12-2^13 tiles; 1 => every half that fits */
+  int32_t block_route;           /* dense (non-diagonal, non-cascade) blocks: 0 (default) =>
+                                    sequential route from 8 support qubits on, assembly below;
+                                    1 => assembly of the 2^s x 2^s block + SVD of the reshaped
+                                    matrix (Eq. 6-9; s <= max_dense_block_qubits); 2 =>
+                                    sequential (MPO-style) route: factors built gate by gate
+                                    across the cut and recompressed to the operator-Schmidt
+                                    form after each crossing gate (no block assembly).
+                                    Either way dense factors are <= 5 qubits per side. */
 } hsf_plan_opts;
 
 typedef struct hsf_plan_s hsf_plan_t; /* opaque */
@@ -209,6 +217,8 @@ typedef struct {
   double tail_tree_flops_a, tail_tree_flops_b; /* same for the half-sided fold trees (0 if none) */
   int32_t n_analytic_units;     /* units decomposed by the analytic cascade route */
   const int32_t* unit_analytic; /* [n_units] 1 if that unit's factors are closed-form */
+  const int32_t* unit_sequential; /* [n_units] 1 if that unit's factors came from the sequential
+                                     (MPO-style) route */
   int32_t whole_state_a, whole_state_b; /* 1: K1 tier -- each pass holds the whole half state in one
                                            CTA's shared memory (2^m <= 2^14 complex64 / 2^13
                                            complex128); 0: K2 tiles streamed through HBM/L2 */

@@ -36,6 +36,7 @@ struct Unit {
   std::vector<int> support, Sa, Sb;// ascending global qubit ids
   bool diag_route = false;         // all members diagonal => diagonal factors
   bool analytic = false;           // factors from the closed-form cascade route (Eq. 11)
+  bool sequential = false;         // factors from the sequential (MPO-style) route
   int rank = 0;
   std::vector<double> sigma;       // kept singular values (descending)
   std::vector<cd> c;               // sigma_m / sqrt(2^|S|)
@@ -136,6 +137,7 @@ struct Plan {
   std::vector<Unit> units;          // schedule order
   std::vector<int32_t> ranks, sa, sb;
   std::vector<int32_t> unit_analytic;  // per unit: closed-form cascade factors
+  std::vector<int32_t> unit_sequential;  // per unit: sequential (MPO-style) route
   std::vector<int64_t> sigma_off;
   std::vector<double> sigmas;
   uint64_t n_paths = 1;

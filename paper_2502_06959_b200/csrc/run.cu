@@ -1301,6 +1301,7 @@ hsf_status hsf_plan_opts_default(hsf_plan_opts* o) {
   o->graphs = 1;
   o->analytic_cascades = 1;
   o->smem_tier = 0;
+  o->block_route = 0;
   o->partition_b = 0;
   return HSF_OK;
 }
@@ -1314,6 +1315,7 @@ hsf_status hsf_plan(const char* text, size_t len, int32_t n_low, int64_t n_block
     hsf_plan_opts o;
     hsf_plan_opts_default(&o);
     if (opts) o = *opts;
+    if (o.block_route < 0 || o.block_route > 2) fail(HSF_ERR_INVALID_ARG, "block_route must be 0, 1 or 2");
     if (o.tile_qubits != 0 && (o.tile_qubits < 10 || o.tile_qubits > 13))
       fail(HSF_ERR_INVALID_ARG, "tile_qubits must be 0 (auto) or in [10,13]");
     if (o.dtype != HSF_C64 && o.dtype != HSF_C128) fail(HSF_ERR_INVALID_ARG, "bad dtype");
@@ -1370,6 +1372,7 @@ hsf_status hsf_plan_info_get(const hsf_plan_t* plan, hsf_plan_info* info) {
     info->n_analytic_units = 0;
     for (int32_t x : P->unit_analytic) info->n_analytic_units += x;
     info->unit_analytic = P->unit_analytic.data();
+    info->unit_sequential = P->unit_sequential.data();
     for (int h = 0; h < 2; ++h) {
       const Half& H = P->half[h];
       (h ? info->whole_state_b : info->whole_state_a) =

@@ -34,7 +34,8 @@ class _Opts(C.Structure):
                 ("log2_path_budget", C.c_double), ("individual", C.c_int32), ("tile_qubits", C.c_int32),
                 ("fuse_gates", C.c_int32), ("hoist_gates", C.c_int32), ("fold_trailing_diag", C.c_int32),
                 ("jit", C.c_int32), ("partition_b", C.c_uint64),
-                ("graphs", C.c_int32), ("analytic_cascades", C.c_int32), ("smem_tier", C.c_int32)]
+                ("graphs", C.c_int32), ("analytic_cascades", C.c_int32), ("smem_tier", C.c_int32),
+                ("block_route", C.c_int32)]
 
 
 class _Info(C.Structure):
@@ -56,6 +57,7 @@ class _Info(C.Structure):
                 ("fold_tree_flops_a", C.c_double), ("fold_tree_flops_b", C.c_double),
                 ("tail_tree_flops_a", C.c_double), ("tail_tree_flops_b", C.c_double),
                 ("n_analytic_units", C.c_int32), ("unit_analytic", C.POINTER(C.c_int32)),
+                ("unit_sequential", C.POINTER(C.c_int32)),
                 ("whole_state_a", C.c_int32), ("whole_state_b", C.c_int32)]
 
 
@@ -248,7 +250,7 @@ class Plan:
                  svd_rel_tol: float = 1e-12, tile_qubits: int = 0, fuse_gates: bool = True,
                  log2_path_budget: float = 26.0, max_dense_block_qubits: int = 10, hoist_gates: bool = True,
                  fold_trailing_diag: bool = True, jit: bool = True, graphs: bool = True,
-                 analytic_cascades: bool = True, smem_tier: int = 0):
+                 analytic_cascades: bool = True, smem_tier: int = 0, block_route: int = 0):
         L = lib()
         o = _Opts()
         _check(L.hsf_plan_opts_default(C.byref(o)))
@@ -267,6 +269,7 @@ class Plan:
         o.graphs = int(graphs)
         o.analytic_cascades = int(analytic_cascades)
         o.smem_tier = int(smem_tier)
+        o.block_route = int(block_route)
         o.log2_path_budget = log2_path_budget
         o.max_dense_block_qubits = max_dense_block_qubits
         auto = isinstance(blocks, str)
@@ -312,6 +315,7 @@ class Plan:
         self.tail_tree_flops = (float(i.tail_tree_flops_a), float(i.tail_tree_flops_b))
         self.n_analytic_units = int(i.n_analytic_units)
         self.unit_analytic = [bool(i.unit_analytic[u]) for u in range(i.n_units)]
+        self.unit_sequential = [bool(i.unit_sequential[u]) for u in range(i.n_units)]
         self.whole_state = (bool(i.whole_state_a), bool(i.whole_state_b))
 
     def __del__(self):

@@ -366,3 +366,53 @@ def test_smem_tier_choice(hsf):
     inst = make_config("c5", n=26, n_low=13, layers=4, fanout=4, n_bits=0)
     assert Plan(inst.text, inst.n_low, inst.blocks, dtype="c128", smem_tier=1).whole_state == (True, True)
     assert Plan(inst.text, inst.n_low, inst.blocks, tile_qubits=11).whole_state == (False, False)
+
+
+@pytest.mark.parametrize("na,nb,depth", [(2, 2, 4), (3, 3, 8), (4, 4, 8), (5, 5, 6), (5, 3, 7)])
+def test_sequential_route_sigmas(hsf, na, nb, depth):
+    # sequential (MPO-style) factors of a dense block: same rank and singular
+    # values as the assembly + SVD route and as LAPACK on the oracle's block
+    # matrix, without assembling the block
+    import time
+    from hsf_inputs import make_brick_block
+    from paper_2502_06959_b200 import Plan
+    inst = make_brick_block(na, nb, depth)
+    t0 = time.perf_counter()
+    P = Plan(inst.text, inst.n_low, inst.blocks, block_route=2)
+    t_seq = time.perf_counter() - t0
+    assert P.unit_sequential == [True] and P.unit_analytic == [False]
+    n, g = O.parse_circuit(inst.text)
+    OP = O.plan(n, g, inst.n_low, inst.blocks)
+    assert P.ranks == [OP.units[0].rank]
+    assert np.allclose(P.sigmas[0], OP.units[0].sigmas[:len(P.sigmas[0])], rtol=1e-10, atol=1e-12)
+    if na + nb <= 8:  # the assembly route is fast enough to compare beside it
+        Q = Plan(inst.text, inst.n_low, inst.blocks, block_route=1)
+        assert Q.unit_sequential == [False] and P.ranks == Q.ranks
+        assert np.allclose(P.sigmas[0], Q.sigmas[0], rtol=1e-11, atol=1e-12)
+    assert t_seq < 2.0, t_seq  # (assembly + Jacobi SVD of the 5 + 5 block: ~12 s)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_sequential_route_random_blocks(hsf, seed):
+    # random blocks with dense 1..3-qubit gates (crossing 3-qubit gates have
+    # 1 + 2 or 2 + 1 sides): both routes give the same ranks and sigma
+    from paper_2502_06959_b200 import Plan
+    inst = random_small_circuit(seed)
+    P = Plan(inst.text, inst.n_low, inst.blocks, block_route=2, analytic_cascades=False)
+    Q = Plan(inst.text, inst.n_low, inst.blocks, block_route=1, analytic_cascades=False)
+    assert P.ranks == Q.ranks
+    for a, b in zip(P.sigmas, Q.sigmas):
+        assert np.allclose(a, b, rtol=1e-11, atol=1e-12)
+    n, g = O.parse_circuit(inst.text)
+    OP = O.plan(n, g, inst.n_low, inst.blocks)
+    for a, u in zip(P.sigmas, OP.units):
+        assert np.allclose(a, u.sigmas[:len(a)], rtol=1e-10, atol=1e-12)
+
+
+def test_block_route_option_checked(hsf):
+    from paper_2502_06959_b200 import Plan
+    inst = make_config("c3", twin=True)
+    with pytest.raises(hsf.HsfError):
+        Plan(inst.text, inst.n_low, inst.blocks, block_route=3)
+    # auto: the c3 windows (2 + 2) keep the assembly route
+    assert Plan(inst.text, inst.n_low, inst.blocks).unit_sequential == [False] * len(inst.blocks)

@@ -170,6 +170,36 @@ def test_tile_passes_forced(torch, tile):
     check(got, ref, "c64")
 
 
+@pytest.mark.parametrize("na,nb,depth", [(5, 5, 6), (4, 4, 8), (5, 3, 7)])
+@pytest.mark.parametrize("route", [2, 0])
+def test_sequential_route_blocks(torch, na, nb, depth, route):
+    # large dense blocks factored by the sequential (MPO-style) route, full
+    # output against the Schroedinger state (n = 16) in complex64 and
+    # complex128 (SIMT), bitstrings through the gather
+    from hsf_inputs import make_brick_block
+    inst = make_brick_block(na, nb, depth, n_bits=4096)
+    n, g = O.parse_circuit(inst.text)
+    ref = O.schrodinger(n, g)
+    for dtype, prec in (("c64", "auto"), ("c128", "simt")):
+        got, P = gpu_full(torch, inst, dtype=dtype, precision=prec, block_route=route)
+        assert P.unit_sequential == [True]
+        check(got, ref, dtype)
+    got, _ = gpu_bits(torch, inst, inst.bitstrings, block_route=route)
+    check(got, ref[inst.bitstrings.astype(np.int64)], "c64")
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_sequential_route_random_circuits(torch, seed):
+    inst = random_small_circuit(seed, n_gates=8 + seed % 17)
+    n, g = O.parse_circuit(inst.text)
+    if O.plan(n, g, inst.n_low, inst.blocks).n_paths > 4096:
+        inst = random_small_circuit(seed, n_gates=8)
+        n, g = O.parse_circuit(inst.text)
+    ref = O.schrodinger(n, g)
+    got, _ = gpu_full(torch, inst, dtype="c128", precision="simt", block_route=2, analytic_cascades=False)
+    check(got, ref, "c128")
+
+
 def test_no_crossing_gates(torch):
     inst = random_small_circuit(3, n=8, n_gates=20)
     # keep only local gates
