@@ -91,6 +91,7 @@ struct Gen {
     ops.assign(h.dev_ops.begin() + p.op_begin, h.dev_ops.begin() + p.op_end);
     pos2q.resize(t);
     for (int i = 0; i < t; ++i) pos2q[i] = whole ? i : p.T[i];
+    if (const char* e = std::getenv("HSF_JIT_GIVENS")) givens = std::atoi(e) != 0;
   }
 
   std::string table(int i) const { return "M" + std::to_string(i); }
@@ -428,6 +429,218 @@ struct Gen {
     sync_pre(x);
   }
 
+  // ---- Euler / fast-Givens form of a register pass's literal 1-qubit gates.
+  // A (scaled) unitary 2x2 literal is M = diag(p0, p1) . [[c, -s], [s, c]] .
+  // diag(1, q1) (ZYZ Euler form with the phases as diagonals).  Diagonals
+  // commute with each other and with gates on other register slots, so the
+  // pass's right / left diagonals are carried at code-generation time as
+  // separable per-slot factors and applied together, once per round of
+  // rotations (a 16-entry product table: <= 15 complex multiplies per 16
+  // amplitudes), and each rotation is applied in the scaled form
+  // c . [[1, -t], [t, 1]] (t = s / c <= 1; else s . [[u, -1], [1, u]]), one
+  // real FMA per component, with the scale folded into the carried constant.
+  // A Haar SU(2) then costs 2 FP32 ops per amplitude plus its share of the
+  // diagonal flushes instead of 8 (the B leaf / T-leaf passes of c5 are
+  // FP32-issue bound).  Table-driven ops (Schmidt factors indexed
+  // per node) are emitted as before, scheduled by the same commutation rules.
+  bool givens = true;
+  struct SOp {
+    int kind;        // 0 const diag (slot J), 1 rotation, 2 table diag, 3 table R1, 4 general literal R1
+    int J = 0;       // slot (kinds 0, 1, 3, 4)
+    unsigned mask;   // slots touched
+    cd d0, d1;       // kind 0
+    int mode = 0;    // kind 1: 0 t-form, 1 u-form, 2 swap
+    double x = 0;    // kind 1: t or u
+    double scale = 1;
+    size_t r = 0;    // op index (kinds 2, 3, 4)
+  };
+  static bool is_diag_kind(int k) { return k == 0 || k == 2; }
+  std::string cl(const cd& v) const {
+    char b[160];
+    if (c64)
+      std::snprintf(b, sizeof b, "make_float2(%af, %af)", (double)(float)v.real(), (double)(float)v.imag());
+    else
+      std::snprintf(b, sizeof b, "make_double2(%a, %a)", v.real(), v.imag());
+    return b;
+  }
+  // decompose a literal 1-qubit op on slot J; false => not a scaled unitary
+  bool euler(const DevOp& d, std::vector<SOp>& out) {
+    const int J = d.q[0];
+    cd m[4];
+    for (int e = 0; e < 4; ++e) m[e] = (*coef)[(size_t)(d.table + e)];
+    const double n0 = std::norm(m[0]) + std::norm(m[1]), n1 = std::norm(m[2]) + std::norm(m[3]);
+    if (!(n0 > 0) || !(n1 > 0)) return false;
+    const double tol = 1e-12 * (n0 + n1);
+    if (std::abs(n0 - n1) > tol || std::abs(m[0] * std::conj(m[2]) + m[1] * std::conj(m[3])) > tol ||
+        std::abs(std::norm(m[0]) - std::norm(m[3])) > tol)
+      return false;
+    SOp a{};
+    a.J = J;
+    a.mask = 1u << J;
+    if (m[1] == cd(0) && m[2] == cd(0)) {  // diagonal
+      a.kind = 0;
+      a.d0 = m[0];
+      a.d1 = m[3];
+      out.push_back(a);
+      return true;
+    }
+    if (m[0] == cd(0) && m[3] == cd(0)) {  // anti-diagonal: swap, then diag(m01, m10)
+      a.kind = 1;
+      a.mode = 2;
+      out.push_back(a);
+      a.kind = 0;
+      a.d0 = m[1];
+      a.d1 = m[2];
+      out.push_back(a);
+      return true;
+    }
+    const double lam = std::sqrt(n0);
+    const double c = std::abs(m[0]) / lam, s = std::abs(m[1]) / lam;
+    const cd p0 = m[0] / c, p1 = m[2] / s, q1 = -m[1] / (s * p0);
+    a.kind = 0;
+    a.d0 = 1.0;
+    a.d1 = q1;
+    out.push_back(a);
+    SOp rt{};
+    rt.kind = 1;
+    rt.J = J;
+    rt.mask = 1u << J;
+    if (c >= s) {
+      rt.mode = 0;
+      rt.x = s / c;
+      rt.scale = c;
+    } else {
+      rt.mode = 1;
+      rt.x = c / s;
+      rt.scale = s;
+    }
+    out.push_back(rt);
+    a.d0 = p0;
+    a.d1 = p1;
+    out.push_back(a);
+    return true;
+  }
+  template <typename TD>
+  void givens_schedule(size_t i, int n, const int* qreg, TD&& emit_tdiag) {
+    std::vector<SOp> sl;
+    for (size_t r = i + 1; r <= i + (size_t)n; ++r) {
+      const DevOp& d = ops[r];
+      if (d.kind == OP_R1) {
+        if (literal(d) && euler(d, sl)) continue;
+        SOp g{};
+        g.kind = literal(d) ? 4 : 3;
+        g.J = d.q[0];
+        g.mask = 1u << d.q[0];
+        g.r = r;
+        sl.push_back(g);
+      } else {
+        SOp g{};
+        g.kind = 2;
+        g.r = r;
+        g.mask = 0;
+        for (int j = 0; j < 4; ++j)
+          for (int jj = 0; jj < d.k; ++jj)
+            if (d.q[jj] == qreg[j]) g.mask |= 1u << j;
+        sl.push_back(g);
+      }
+    }
+    // carried constants: per-slot diag(1, pd[J]) and a global scalar gs
+    cd pd[4] = {1.0, 1.0, 1.0, 1.0};
+    cd gs = 1.0;
+    const char* fm = c64 ? "fmaf" : "fma";
+    const char* mk = c64 ? "make_float2" : "make_double2";
+    auto flush = [&](unsigned S, bool with_scalar) {
+      for (int k = 0; k < 16; ++k) {
+        cd f = with_scalar ? gs : cd(1.0);
+        for (int j = 0; j < 4; ++j)
+          if (((S >> j) & 1) && ((k >> j) & 1)) f *= pd[j];
+        if (f == cd(1.0)) continue;
+        const std::string v = "v[" + std::to_string(k) + "]";
+        const double fr = c64 ? (double)(float)f.real() : f.real(), fi = c64 ? (double)(float)f.imag() : f.imag();
+        if (fi == 0.0)
+          o << "    " << v << " = " << mk << "(" << v << ".x * " << rl(fr) << ", " << v << ".y * " << rl(fr) << ");\n";
+        else if (fr == 0.0)
+          o << "    " << v << " = " << mk << "(" << v << ".y * " << rl(-fi) << ", " << v << ".x * " << rl(fi) << ");\n";
+        else
+          o << "    " << v << " = cmul(" << v << ", " << cl(f) << ");\n";
+      }
+      for (int j = 0; j < 4; ++j)
+        if ((S >> j) & 1) pd[j] = 1.0;
+      if (with_scalar) gs = 1.0;
+    };
+    auto emit_rot = [&](const SOp& s) {
+      for (int a = 0; a < 16; ++a) {
+        if (a & (1 << s.J)) continue;
+        const int b = a | (1 << s.J);
+        const std::string va = "v[" + std::to_string(a) + "]", vb = "v[" + std::to_string(b) + "]";
+        if (s.mode == 2) {
+          o << "    { const C t_ = " << va << "; " << va << " = " << vb << "; " << vb << " = t_; }\n";
+        } else if (s.mode == 0) {  // a' = a - t b, b' = b + t a
+          const std::string mt = rl(-s.x), pt = rl(s.x);
+          o << "    { const C a = " << va << ", b = " << vb << "; " << va << " = " << mk << "(" << fm << "(b.x, " << mt
+            << ", a.x), " << fm << "(b.y, " << mt << ", a.y)); " << vb << " = " << mk << "(" << fm << "(a.x, " << pt
+            << ", b.x), " << fm << "(a.y, " << pt << ", b.y)); }\n";
+        } else {  // a' = u a - b, b' = u b + a
+          const std::string u = rl(s.x);
+          o << "    { const C a = " << va << ", b = " << vb << "; " << va << " = " << mk << "(" << fm << "(a.x, " << u
+            << ", -b.x), " << fm << "(a.y, " << u << ", -b.y)); " << vb << " = " << mk << "(" << fm << "(b.x, " << u
+            << ", a.x), " << fm << "(b.y, " << u << ", a.y)); }\n";
+        }
+      }
+    };
+    std::vector<char> done(sl.size(), 0);
+    auto ready = [&](size_t x) {
+      for (size_t y = 0; y < x; ++y)
+        if (!done[y] && (sl[y].mask & sl[x].mask) && !(is_diag_kind(sl[x].kind) && is_diag_kind(sl[y].kind)))
+          return false;
+      return true;
+    };
+    for (;;) {
+      bool any = false;
+      for (bool ch = true; ch;) {  // every ready diagonal: carried (constants) or applied now (tables)
+        ch = false;
+        for (size_t x = 0; x < sl.size(); ++x) {
+          if (done[x] || !is_diag_kind(sl[x].kind) || !ready(x)) continue;
+          if (sl[x].kind == 0) {
+            const SOp& s = sl[x];
+            gs *= s.d0;
+            pd[s.J] *= s.d1 / s.d0;
+          } else {
+            emit_tdiag(sl[x].r);
+          }
+          done[x] = 1;
+          ch = any = true;
+        }
+      }
+      std::vector<size_t> round;
+      unsigned S = 0;
+      for (size_t x = 0; x < sl.size(); ++x)
+        if (!done[x] && !is_diag_kind(sl[x].kind) && ready(x)) {
+          round.push_back(x);
+          if (pd[sl[x].J] != cd(1.0)) S |= 1u << sl[x].J;
+        }
+      if (round.empty()) {
+        if (!any) break;
+        continue;
+      }
+      // (every op is linear, so the global scalar rides to the pass's end)
+      if (S) flush(S, false);
+      for (size_t x : round) {
+        const SOp& s = sl[x];
+        if (s.kind == 1) {
+          emit_rot(s);
+          gs *= s.scale;
+        } else if (s.kind == 3) {
+          o << "    r1<" << s.J << ">(v, " << table((int)s.r) << ");\n";
+        } else {
+          r1_literal(s.J, ops[s.r]);
+        }
+        done[x] = 1;
+      }
+    }
+    flush(0xFu, true);
+  }
+
   // register pass: header at ops[i], then ops[i+1 .. i+n]
   void rpass(size_t i) {
     const DevOp& h = ops[i];
@@ -468,25 +681,33 @@ struct Gen {
       ek[k] = e;
       o << "    v[" << k << "] = " << elk_ld(e) << ";\n";
     }
-    for (size_t r = i + 1; r <= i + (size_t)n; ++r) {
+    auto emit_tdiag = [&](size_t r) {  // diagonal: index of element k = i0 | IK[k]
       const DevOp& d = ops[r];
-      if (d.kind == OP_R1) {
-        if (literal(d))
-          r1_literal(d.q[0], d);
-        else
-          o << "    r1<" << d.q[0] << ">(v, " << table((int)r) << ");\n";
-      } else {  // diagonal: index of element k = i0 | IK[k]
-        o << "    { const u32 i0 = " << didx(d, "gb") << ";\n";
-        for (int k = 0; k < 16; ++k) {
-          uint32_t ik = 0;
-          for (int j = 0; j < 4; ++j)
-            if ((k >> j) & 1)
-              for (int jj = 0; jj < d.k; ++jj)
-                if (d.q[jj] == qreg[j]) ik |= 1u << jj;
-          o << "      v[" << k << "] = cmul(v[" << k << "], " << tload(d, (int)r, "i0 | " + std::to_string(ik) + "u")
-            << ");\n";
+      o << "    { const u32 i0 = " << didx(d, "gb") << ";\n";
+      for (int k = 0; k < 16; ++k) {
+        uint32_t ik = 0;
+        for (int j = 0; j < 4; ++j)
+          if ((k >> j) & 1)
+            for (int jj = 0; jj < d.k; ++jj)
+              if (d.q[jj] == qreg[j]) ik |= 1u << jj;
+        o << "      v[" << k << "] = cmul(v[" << k << "], " << tload(d, (int)r, "i0 | " + std::to_string(ik) + "u")
+          << ");\n";
+      }
+      o << "    }\n";
+    };
+    if (givens && coef) {
+      givens_schedule(i, n, qreg, emit_tdiag);
+    } else {
+      for (size_t r = i + 1; r <= i + (size_t)n; ++r) {
+        const DevOp& d = ops[r];
+        if (d.kind == OP_R1) {
+          if (literal(d))
+            r1_literal(d.q[0], d);
+          else
+            o << "    r1<" << d.q[0] << ">(v, " << table((int)r) << ");\n";
+        } else {
+          emit_tdiag(r);
         }
-        o << "    }\n";
       }
     }
     for (int k = 0; k < 16; ++k) o << "    " << elk(ek[k]) << " = v[" << k << "];\n";
