@@ -65,6 +65,12 @@ std::string gather_expr(const std::string& x, const std::vector<int>& from, cons
   return "(" + s + ")";
 }
 
+// shared-memory tile swizzle (8 B / 16 B elements), same as the prelude's
+// sw(): every group of 4 index bits is folded onto the bank bits, so any 4
+// register positions leave lane positions of every residue mod 4 (full-rank
+// bank indices per half-warp, see rpass)
+static uint32_t swz(uint32_t e) { return e ^ ((e >> 4) & 15u) ^ ((e >> 8) & 15u) ^ ((e >> 12) & 15u); }
+
 // T-leaf group stride: tile + tables, then padded to 32 mod 64 bytes so that
 // the transposed store's reads of groups c2 = 0, 2, 4, 6 (same element, four
 // lanes) fall on two 64 B bank halves instead of one (8-way -> 2 wavefronts)
@@ -655,8 +661,44 @@ struct Gen {
     const bool x = cross(pos, 4);
     sync_pre(x);
     group_loop(x, "gi", 4);
-    o << "    u32 b = gi;";
-    for (int p : sorted) o << " b = ins0<" << p << ">(b);";
+    if (!x && cb == 0 && t > 4) {
+      // lane bits -> non-register tile positions, ordered so that the first
+      // lanes' swizzled bank indices are linearly independent: sw(e) puts
+      // e[0..3] ^ e[4..7] ^ e[8..11] ^ e[12..15] on the bank bits, so each position contributes a
+      // GF(2) vector; a half-warp (c64, 8 B) / quarter-warp (c128, 16 B) then
+      // touches distinct banks (c5's leaf pass: 2-way conflicts on the
+      // register passes with low register positions, ncu profiles/r02c)
+      const int bank_bits = c64 ? 4 : 3;
+      std::vector<int> ns, order;
+      for (int p = 0; p < t; ++p)
+        if (std::find(pos, pos + 4, p) == pos + 4) ns.push_back(p);
+      auto vec = [&](int p) -> unsigned { return (p < 16 ? 1u << (p & 3) : 0u) & ((1u << bank_bits) - 1); };
+      std::vector<unsigned> basis;  // reduced row echelon by leading bit
+      auto add_if_indep = [&](unsigned v) {
+        for (unsigned bv : basis)
+          if ((v ^ bv) < v) v ^= bv;
+        if (!v) return false;
+        basis.push_back(v);
+        std::sort(basis.begin(), basis.end(), [](unsigned a, unsigned b) { return a > b; });
+        return true;
+      };
+      std::vector<char> used(ns.size(), 0);
+      for (size_t j = 0; j < ns.size() && (int)order.size() < bank_bits; ++j)
+        if (add_if_indep(vec(ns[j]))) {
+          order.push_back(ns[j]);
+          used[j] = 1;
+        }
+      for (size_t j = 0; j < ns.size(); ++j)
+        if (!used[j]) order.push_back(ns[j]);
+      std::vector<int> from(order.size());
+      for (size_t j = 0; j < order.size(); ++j) from[j] = (int)j;
+      // gather_expr merges runs only when both sides advance by one, so pass
+      // the pairs sorted by source bit (they already are)
+      o << "    const u32 b = " << gather_expr("gi", from, order) << ";";
+    } else {
+      o << "    u32 b = gi;";
+      for (int p : sorted) o << " b = ins0<" << p << ">(b);";
+    }
     o << "\n    const u32 gb = G(" << (x ? "b" : "(RANK << LB) | b") << "); (void)gb;\n    C v[16];\n";
     // the swizzle is GF(2)-linear and b, e have disjoint bits: sw(b | e) =
     // sw(b) ^ sw(e), one XOR with a constant per access (c5 leaf pass: ~2 ALU
@@ -664,13 +706,13 @@ struct Gen {
     if (!x) o << "    const u32 sb = (u32)sw((int)b);\n";
     auto elk = [&](uint32_t e) {
       if (x) return el(x, "(b | " + std::to_string(e) + "u)");
-      const uint32_t swe = e ^ ((e >> 4) & 15u);
+      const uint32_t swe = swz(e);
       return std::string("s[sb ^ ") + std::to_string(swe) + "u]";
     };
     const bool from_pb = pb_first && i == 0;
     auto elk_ld = [&](uint32_t e) {
       if (!from_pb) return elk(e);
-      const uint32_t swe = e ^ ((e >> 4) & 15u);
+      const uint32_t swe = swz(e);
       return std::string("pb_[sb ^ ") + std::to_string(swe) + "u]";
     };
     uint32_t ek[16];
