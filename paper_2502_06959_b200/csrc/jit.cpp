@@ -235,7 +235,11 @@ struct Gen {
     o << "  const C* coef = reinterpret_cast<const C*>(a.coef);\n";
     o << "  const C* srcb = reinterpret_cast<const C*>(a.src);\n";
     o << "  constexpr long long NTILES = " << (1ll << (m - t)) << "ll;\n";
-    o << "  const long long n_items = NTILES * (long long)a.tile_free;  // tile_free = parents\n";
+    // items = (tile, parent) with the parent fastest: the CTAs in flight
+    // write all K columns of the same rows close together in time, so L2
+    // merges whole 1 KiB operand rows before they reach DRAM
+    o << "  const long long NPAR = (long long)a.tile_free;  // tile_free = parents\n";
+    o << "  const long long n_items = NTILES * NPAR;\n";
     // tile map of an item's tile
     std::vector<int> nonT;
     for (int q = 0; q < m; ++q)
@@ -250,7 +254,7 @@ struct Gen {
     o << "  auto base_of = [&](u32 tile) -> u32 { return " << gather_expr("tile", from, to) << "; };\n";
     o << "  auto GE = [&](u32 e) -> u32 { return " << gather_expr("e", pf, pt) << "; };\n";
     o << "  auto prefetch = [&](long long it, u32 buf) {\n";
-    o << "    const long long parent = it / NTILES; const u32 pb = base_of((u32)(it % NTILES));\n";
+    o << "    const long long parent = it % NPAR; const u32 pb = base_of((u32)(it / NPAR));\n";
     o << "    const C* p_ = srcb + ((a.node_first + parent * " << multi << "ll) / a.src_div - a.src_first) * "
       << (1ll << m) << "ll;\n";
     o << "    C* d_ = pbuf + buf * LNEL;\n";
@@ -269,14 +273,22 @@ struct Gen {
     }
     o << "    asm volatile(\"cp.async.commit_group;\" ::: \"memory\");\n  };\n";
     o << "  long long it = blockIdx.x;\n  u32 buf = 0u;\n";
+    // one CTA barrier at the end of an item covers both the group tiles'
+    // reuse and the next parent tile's arrival (its copies were issued at the
+    // item's start into the buffer the previous item had finished reading)
     o << "  if (it < n_items) prefetch(it, 0u); else asm volatile(\"cp.async.commit_group;\" ::: \"memory\");\n";
+    o << "  asm volatile(\"cp.async.wait_group 0;\" ::: \"memory\");\n  __syncthreads();\n";
+    o << "  const C* cpt = reinterpret_cast<const C*>(a.dst_lo);\n";
+    o << "  const u32 c2 = 2u * (threadIdx.x % " << multi / 2 << "u);\n";
     o << "  for (; it < n_items; it += gridDim.x, buf ^= 1u) {\n";
     o << "  if (it + gridDim.x < n_items) prefetch(it + gridDim.x, buf ^ 1u);\n";
     o << "  else asm volatile(\"cp.async.commit_group;\" ::: \"memory\");\n";
-    o << "  asm volatile(\"cp.async.wait_group 1;\" ::: \"memory\");\n";
-    o << "  __syncthreads();\n";
-    o << "  const long long parent = it / NTILES;\n";
-    o << "  const u32 base = base_of((u32)(it % NTILES));\n";
+    o << "  const long long parent = it % NPAR;\n";
+    o << "  const u32 base = base_of((u32)(it / NPAR));\n";
+    // the store's two c_p columns, requested before the leaf evaluation
+    o << "  const long long k0 = a.node_local0 + parent * " << multi << "ll;\n";
+    o << "  C w0 = czero<C>(), w1 = czero<C>();\n";
+    o << "  if (cpt) { w0 = cpt[k0 + c2]; w1 = cpt[k0 + c2 + 1u]; }\n";
     o << "  auto G = [&](u32 e) -> u32 { return base | GE(e); };\n";
     o << "  {\n  const long long node_g = a.node_first + parent * " << multi << "ll + GRP;\n";
     // per-op table pointers (digit-resolved)
@@ -804,7 +816,7 @@ struct Gen {
         i = j;
       }
     }
-    o << "  " << SYNCs << ";\n";
+    if (!multi) o << "  " << SYNCs << ";\n";  // (T-leaf: the CTA barrier before the store covers it)
     if (multi) {
       o << "  }\n  __syncthreads();\n";
       // transposed store of the item's `multi` leaves (group g's tile = leaf g):
@@ -813,13 +825,10 @@ struct Gen {
       // threads adjacent
       const int hp = multi / 2;
       // (a thread's two columns are loop-invariant: their c_p loaded once)
-      o << "  { C* T = reinterpret_cast<C*>(a.dst); const C* cp = reinterpret_cast<const C*>(a.dst_lo);\n";
-      o << "    const long long k0 = a.node_local0 + parent * " << multi << "ll;\n";
-      o << "    const u32 c2 = 2u * (threadIdx.x % " << hp << "u);\n";
+      o << "  { C* T = reinterpret_cast<C*>(a.dst);\n";
       o << "    const C* t0 = reinterpret_cast<const C*>(smem_raw + c2 * " << group_bytes() << "u);\n";
       o << "    const C* t1 = reinterpret_cast<const C*>(smem_raw + (c2 + 1u) * " << group_bytes() << "u);\n";
-      o << "    const bool hc = cp != nullptr; C w0 = czero<C>(), w1 = czero<C>();\n";
-      o << "    if (hc) { w0 = cp[k0 + c2]; w1 = cp[k0 + c2 + 1u]; }\n";
+      o << "    const bool hc = cpt != nullptr;\n";
       o << "#pragma unroll 4\n";
       o << "    for (u32 i = threadIdx.x; i < LNEL * " << hp << "u; i += " << multi * 64 << "u) {\n";
       o << "      const u32 e = i / " << hp << "u;\n";
@@ -827,8 +836,8 @@ struct Gen {
       o << "      if (hc) { v0 = cmul(v0, w0); v1 = cmul(v1, w1); }\n";
       o << "      st2(T + (long long)G(e) * a.ldw + k0 + c2, v0, v1);\n";
       o << "    }\n  }\n";
-      o << "  __syncthreads();\n  }\n";
       o << "  asm volatile(\"cp.async.wait_group 0;\" ::: \"memory\");\n";
+      o << "  __syncthreads();\n  }\n";
     } else if (operand_store) {
       o << "#pragma unroll 4\n";
       o << "  for (u32 e = 2u * threadIdx.x; e < LNEL; e += 2u * NT) " << (store_mode == 3 ? "st_aop" : "st_bop")
