@@ -98,6 +98,8 @@ struct Gen {
     pos2q.resize(t);
     for (int i = 0; i < t; ++i) pos2q[i] = whole ? i : p.T[i];
     if (const char* e = std::getenv("HSF_JIT_GIVENS")) givens = std::atoi(e) != 0;
+    packed = c64;
+    if (const char* e = std::getenv("HSF_JIT_PACKED")) packed = c64 && std::atoi(e) != 0;
   }
 
   std::string table(int i) const { return "M" + std::to_string(i); }
@@ -462,6 +464,10 @@ struct Gen {
   // FP32-issue bound).  Table-driven ops (Schmidt factors indexed
   // per node) are emitted as before, scheduled by the same commutation rules.
   bool givens = true;
+  // c64 rotations as packed FFMA2 with a broadcast immediate (SASS count of
+  // c5's B leaf pass 1584 -> 1400; literal complex products stay scalar: their
+  // FMUL2 / FFMA2 form needs the constant pairs in registers, 1400 -> 1672)
+  bool packed = false;
   struct SOp {
     int kind;        // 0 const diag (slot J), 1 rotation, 2 table diag, 3 table R1, 4 general literal R1
     int J = 0;       // slot (kinds 0, 1, 3, 4)
@@ -593,6 +599,12 @@ struct Gen {
         const std::string va = "v[" + std::to_string(a) + "]", vb = "v[" + std::to_string(b) + "]";
         if (s.mode == 2) {
           o << "    { const C t_ = " << va << "; " << va << " = " << vb << "; " << vb << " = t_; }\n";
+        } else if (packed && s.mode == 0) {  // FFMA2 with the broadcast literal
+          o << "    { const C a = " << va << ", b = " << vb << "; " << va << " = axpy2(" << rl(-s.x) << ", b, a); " << vb
+            << " = axpy2(" << rl(s.x) << ", a, b); }\n";
+        } else if (packed) {
+          o << "    { const C a = " << va << ", b = " << vb << "; " << va << " = fma2(a, make_float2(" << rl(s.x) << ", "
+            << rl(s.x) << "), make_float2(-b.x, -b.y)); " << vb << " = axpy2(" << rl(s.x) << ", b, a); }\n";
         } else if (s.mode == 0) {  // a' = a - t b, b' = b + t a
           const std::string mt = rl(-s.x), pt = rl(s.x);
           o << "    { const C a = " << va << ", b = " << vb << "; " << va << " = " << mk << "(" << fm << "(b.x, " << mt

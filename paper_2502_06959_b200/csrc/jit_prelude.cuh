@@ -49,6 +49,17 @@ __device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 acc) {
   acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
   return acc;
 }
+// packed FP32 (sm_100 FFMA2 / FMUL2): both components of a complex64 in one
+// instruction; a scalar factor broadcast to both lanes is an immediate
+__device__ __forceinline__ unsigned long long pk2(float2 a) { return *reinterpret_cast<unsigned long long*>(&a); }
+__device__ __forceinline__ float2 up2(unsigned long long a) { return *reinterpret_cast<float2*>(&a); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(pk2(a)), "l"(pk2(b)), "l"(pk2(c)));
+  return up2(d);
+}
+// a + s b (s a literal): the scaled rotation's update, one FFMA2 with a broadcast immediate
+__device__ __forceinline__ float2 axpy2(float s, float2 b, float2 a) { return fma2(b, make_float2(s, s), a); }
 template <typename C>
 __device__ __forceinline__ C czero();
 template <>
