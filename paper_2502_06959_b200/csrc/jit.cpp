@@ -71,11 +71,14 @@ std::string gather_expr(const std::string& x, const std::vector<int>& from, cons
 // bank indices per half-warp, see rpass)
 static uint32_t swz(uint32_t e) { return e ^ ((e >> 4) & 15u) ^ ((e >> 8) & 15u) ^ ((e >> 12) & 15u); }
 
-// T-leaf group stride: tile + tables, then padded to 32 mod 64 bytes so that
-// the transposed store's reads of groups c2 = 0, 2, 4, 6 (same element, four
-// lanes) fall on two 64 B bank halves instead of one (8-way -> 2 wavefronts)
+// T-leaf group stride: tile + tables, then padded to 16 mod 64 bytes.  In the
+// transposed store a half-warp reads 4 consecutive rows e (8 contiguous
+// words after the swizzle) of the column groups c2 = 0, 2, 4, 6: strides of
+// 4 mod 16 words put them at word offsets 0, 8, 16, 24 (t1: 4, 12, 20, 28), so
+// each half-warp covers the 32 banks once (ncu: the 32 mod 64 B stride
+// left 2-way conflicts, 4 wavefronts per load instead of 2)
 static size_t tleaf_group_bytes(int t, long long tbl_elems, size_t elem) {
-  return ((((elem << t) + (size_t)tbl_elems * elem) + 63) & ~(size_t)63) + 32;
+  return ((((elem << t) + (size_t)tbl_elems * elem) + 63) & ~(size_t)63) + 16;
 }
 
 struct Gen {
