@@ -60,7 +60,8 @@ constexpr int kSmemTableQ = 8;     // diag tables with <= 2^8 entries are staged
 constexpr int kSmemTableBytes = 48 * 1024;  // per-pass cap on staged tables
 constexpr int kMaxOpQ = 13;      // widest diagonal op (2^13 entries)
 constexpr int kMaxDenseQ = 5;    // widest dense op in the SMEM kernels
-constexpr int kMaxTrail = 8;     // folded trailing diagonal units (bitstring runs)
+constexpr int kMaxFoldUnits = 8;  // folded trailing diagonal units (bitstring runs)
+constexpr int kMaxTrail = 16;    // folded trailing diagonal units + deferred-diagonal tables (bitstring runs)
 constexpr int kMaxTail = 16;     // half-sided trailing diagonal factors (full-output operand prep)
 constexpr double kTailPrefixBytes = 16.0 * (1 << 20);  // prefix-leaf budget (HSF_TAIL_PREFIX_BYTES mode)
 constexpr double kTailTableEntries = 1 << 20;           // default: tail weight table W[T][2^m] cap

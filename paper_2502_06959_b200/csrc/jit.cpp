@@ -467,6 +467,12 @@ struct Gen {
   // FP32-issue bound).  Table-driven ops (Schmidt factors indexed
   // per node) are emitted as before, scheduled by the same commutation rules.
   bool givens = true;
+  // deferral of the pass's final diagonals (see DeferOut): the pending
+  // per-qubit phases carried from one register pass to the next and left
+  // unapplied at the end
+  bool defer = false;
+  std::map<int, cd> carry;  // half-local qubit -> phase of |1> (|0> normalised to 1)
+  cd carry_scalar = 1.0;
   // c64 rotations as packed FFMA2 with a broadcast immediate (SASS count of
   // c5's B leaf pass 1584 -> 1400; literal complex products stay scalar: their
   // FMUL2 / FFMA2 form needs the constant pairs in registers, 1400 -> 1672)
@@ -572,8 +578,20 @@ struct Gen {
       }
     }
     // carried constants: per-slot diag(1, pd[J]) and a global scalar gs
+    // (deferral: seeded from what earlier register passes left pending)
     cd pd[4] = {1.0, 1.0, 1.0, 1.0};
     cd gs = 1.0;
+    if (defer) {
+      gs = carry_scalar;
+      carry_scalar = 1.0;
+      for (int j = 0; j < 4; ++j) {
+        auto it = carry.find(qreg[j]);
+        if (it != carry.end()) {
+          pd[j] = it->second;
+          carry.erase(it);
+        }
+      }
+    }
     const char* fm = c64 ? "fmaf" : "fma";
     const char* mk = c64 ? "make_float2" : "make_double2";
     auto flush = [&](unsigned S, bool with_scalar) {
@@ -671,7 +689,13 @@ struct Gen {
         done[x] = 1;
       }
     }
-    flush(0xFu, true);
+    if (defer) {  // left pending: later register passes or the gather apply them
+      carry_scalar = gs;
+      for (int j = 0; j < 4; ++j)
+        if (pd[j] != cd(1.0)) carry[qreg[j]] = pd[j];
+    } else {
+      flush(0xFu, true);
+    }
   }
 
   // register pass: header at ops[i], then ops[i+1 .. i+n]
@@ -810,6 +834,8 @@ struct Gen {
     // / 5: q33-3 6.19 / 5.67 / 5.32 / 5.43 ms, q32-1 1.85 / 1.69 / 1.54 / 1.58,
     // c5 4.10 / 3.95 / 3.88 / 4.02 (latency-bound at 25 % occupancy with 86
     // registers); light passes insensitive 3 .. 5
+    for (auto& d : ops) defer = defer && d.kind != OP_DENSE;  // a dense sweep would need the pending applied
+    if (cb || !givens || !coef) defer = false;
     int heavy_minb = 4, light_minb = 3;
     if (const char* e = std::getenv("HSF_JIT_HEAVY_MINB")) heavy_minb = std::atoi(e);
     if (const char* e = std::getenv("HSF_JIT_LIGHT_MINB")) light_minb = std::atoi(e);
@@ -935,20 +961,36 @@ std::vector<char> nvrtc_compile(const std::string& src, std::string& log) {
 
 }  // namespace
 
-std::string jit_pass_source(const Half& H, const Pass& ps, bool c64, int threads, int cluster_bits,
-                            const std::vector<cd>* coef, int store_mode) {
-  Gen g(H, ps, c64, coef);
-  return std::string(kPrelude) + "\n" + g.build("hsf_jit_pass", threads, cluster_bits, store_mode);
+static void defer_result(const Gen& g, DeferOut* d) {
+  if (!d) return;
+  d->active = g.defer;
+  d->phase.clear();
+  d->scalar = 1.0;
+  if (!g.defer) return;
+  for (auto& kv : g.carry) d->phase.push_back({kv.first, kv.second});
+  d->scalar = g.carry_scalar;
 }
 
-std::string jit_tleaf_source(const Half& TL, int leaves, bool c64, const std::vector<cd>* coef) {
+std::string jit_pass_source(const Half& H, const Pass& ps, bool c64, int threads, int cluster_bits,
+                            const std::vector<cd>* coef, int store_mode, DeferOut* defer) {
+  Gen g(H, ps, c64, coef);
+  g.defer = defer != nullptr && store_mode == 0;
+  std::string src = std::string(kPrelude) + "\n" + g.build("hsf_jit_pass", threads, cluster_bits, store_mode);
+  defer_result(g, defer);
+  return src;
+}
+
+std::string jit_tleaf_source(const Half& TL, int leaves, bool c64, const std::vector<cd>* coef, DeferOut* defer) {
   const Pass& ps = TL.trans[0].passes[0];
   Gen g(TL, ps, c64, coef);
+  g.defer = defer != nullptr;
   g.multi = leaves;
   g.pb_first = !g.ops.empty() && g.ops[0].kind == OP_RPASS && !std::getenv("HSF_TLEAF_COPY");
   g.TIDs = "TID";
   g.SYNCs = "asm volatile(\"bar.sync %0, 64;\" :: \"r\"(1u + GRP) : \"memory\")";
-  return std::string(kPrelude) + "\n" + g.build("hsf_jit_pass", 64 * leaves, 0, 0);
+  std::string src = std::string(kPrelude) + "\n" + g.build("hsf_jit_pass", 64 * leaves, 0, 0);
+  defer_result(g, defer);
+  return src;
 }
 
 size_t jit_tleaf_smem_bytes(const Half& TL, int leaves, bool c64) {

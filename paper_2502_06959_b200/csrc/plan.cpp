@@ -1684,7 +1684,7 @@ Plan* build_plan(const char* text, size_t len, int n_low, int64_t n_blocks, cons
   // (P:104-109 regrouped).  The path tree then stops at level u0.
   P->fold_u0 = -1;
   if (opts.fold_trailing_diag && U > 0 && P->n <= 63) {
-    int u0 = std::max({P->half[0].last_gate_level, P->half[1].last_gate_level, U - kMaxTrail});
+    int u0 = std::max({P->half[0].last_gate_level, P->half[1].last_gate_level, U - kMaxFoldUnits});
     for (int u = U - 1; u >= u0; --u)
       if (!P->units[u].diag_route || P->units[u].support.size() > 16) {
         u0 = u + 1;

@@ -38,6 +38,11 @@ struct DeviceState {
   DevOp* ops_fold[2] = {nullptr, nullptr};  // trailing-diagonal fold variant
   DevOp* ops_tail[2] = {nullptr, nullptr};  // half-sided trailing fold variant (full output)
   void* trail = nullptr;                    // folded units' block diagonals (run dtype)
+  // deferred final diagonals of the bitstring-fold variant's last kernel per
+  // half ([0] its last tile pass, [1] its T-leaf pass): extra per-sample
+  // weight tables appended to `trail` (mask of global bits, table offset)
+  DeferOut dfin[2][2];
+  std::vector<std::pair<unsigned long long, long long>> dfin_units[2][2];
   void* tail = nullptr;                     // half-sided folded diagonal factors (run dtype)
   float2* tailw[2] = {nullptr, nullptr};    // [T][2^m] tail weights per half (tensor-core runs)
   // half B's last pass (full tree) writing the MN-major split-bf16 GEMM
@@ -226,7 +231,9 @@ static DeviceState* ensure_device(Plan* P, int device) {
             else if (tiled && n_cta * 2 <= num_sms()) cb = 1;
             int nt = cb ? std::max(128, 1 << (ps.t - cb - 4)) : (n_cta < 2.0 * num_sms() ? 512 : 256);
             if (!cb) nt = std::min(nt, std::max(128, 1 << (ps.t - 2)));  // small narrow-level tiles (t = 10, 11)
-            src.push_back(jit_pass_source(H, ps, c64, nt, cb, &P->coef));
+            // the fold variant's last pass leaves its final diagonals to the gather
+            const bool lastp = v == 1 && &tr == &H.trans.back() && &ps == &tr.passes.back();
+            src.push_back(jit_pass_source(H, ps, c64, nt, cb, &P->coef, 0, lastp ? &d->dfin[0][h] : nullptr));
             owner.push_back({v, h});
             d->jit_nt[v][h].push_back(nt);
             d->jit_cb[v][h].push_back(cb);
@@ -252,7 +259,7 @@ static DeviceState* ensure_device(Plan* P, int device) {
       for (int h = 0; h < 2; ++h) {
         const Half& H = v ? P->half_fold[h] : P->half[h];
         if (!H.tleaf) continue;
-        src.push_back(jit_tleaf_source(*H.tleaf, H.tleaf_R, c64, &P->coef));
+        src.push_back(jit_tleaf_source(*H.tleaf, H.tleaf_R, c64, &P->coef, v == 1 ? &d->dfin[1][h] : nullptr));
         owner.push_back({-2 - (2 * v + h), 0});
       }
     }
@@ -266,6 +273,42 @@ static DeviceState* ensure_device(Plan* P, int device) {
         d->jit_fn[owner[i].first][owner[i].second].push_back(fns[i]);
     }
     d->jit = true;
+    // D_fin tables over contiguous ranges of <= 10 of the half's qubits
+    // (index = one shift and mask in the gather), entry = product of the
+    // pending phases of the range's set bits (the scalar in the first range
+    // used), appended after the folded units' tables
+    std::vector<cd> tab = P->trail_tab;
+    bool any = false;
+    for (int kind = 0; kind < 2; ++kind)
+      for (int h = 0; h < 2; ++h) {
+        const DeferOut& df = d->dfin[kind][h];
+        if (!df.active || (df.phase.empty() && df.scalar == cd(1.0))) continue;
+        any = true;
+        const int first = P->half[h].first_qubit, mq = P->half[h].m;
+        std::vector<cd> ph(mq, cd(1.0));
+        for (const auto& q : df.phase) ph[q.first] = q.second;
+        bool scalar_done = false;
+        for (int lo = 0; lo < mq; lo += 10) {
+          const int hi = std::min(mq, lo + 10);
+          bool used = !scalar_done && df.scalar != cd(1.0);
+          for (int q = lo; q < hi; ++q) used = used || ph[q] != cd(1.0);
+          if (!used) continue;
+          const unsigned long long mask = ((1ull << (hi - lo)) - 1ull) << (first + lo);
+          d->dfin_units[kind][h].push_back({mask, (long long)tab.size()});
+          for (size_t idx = 0; idx < (1ull << (hi - lo)); ++idx) {
+            cd w = scalar_done ? cd(1.0) : df.scalar;
+            for (int j = 0; j < hi - lo; ++j)
+              if ((idx >> j) & 1) w *= ph[lo + j];
+            tab.push_back(w);
+          }
+          scalar_done = true;
+        }
+      }
+    if (any) {
+      cudaFree(d->trail);
+      d->trail = nullptr;
+      upload_tab(tab, &d->trail);
+    }
   }
   for (auto& e : d->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDefault));
   CK(cudaEventCreateWithFlags(&d->ev_t0, cudaEventDefault));
@@ -910,6 +953,16 @@ static void run_core_bits(Plan* P, DeviceState* d, const Layout& L, const hsf_ru
     for (int u = 0; u < tw.n; ++u) {
       tw.mask[u] = P->trail_mask[u];
       tw.off[u] = P->trail_off[u];
+    }
+    // the deferred final diagonals of the kernels that produced the leaves
+    for (int h = 0; h < 2 && d->jit; ++h) {
+      const int kind = (L.tleaf[h] && d->jit_tl[1][h]) ? 1 : 0;
+      for (const auto& un : d->dfin_units[kind][h]) {
+        if (tw.n >= kMaxTrail) fail(HSF_ERR_UNSUPPORTED, "too many per-sample weight tables");
+        tw.mask[tw.n] = un.first;
+        tw.off[tw.n] = un.second;
+        ++tw.n;
+      }
     }
   }
   const unsigned long long maskA = (P->n - nB >= 64) ? ~0ull : (1ull << (P->n - nB)) - 1ull;
@@ -1573,7 +1626,8 @@ size_t hsf_debug_pass_source(const hsf_plan_t* plan, int32_t variant, int32_t ha
       if (!P || half < 0 || half > 1 || v > 1 || (v == 1 && P->fold_u0 < 0)) return 0;
       const Half& H = v ? P->half_fold[half] : P->half[half];
       if (!H.tleaf) return 0;
-      const std::string s = jit_tleaf_source(*H.tleaf, H.tleaf_R, P->opts.dtype == HSF_C64, &P->coef);
+      DeferOut df;  // as compiled for runs (the fold variant defers its final diagonals)
+      const std::string s = jit_tleaf_source(*H.tleaf, H.tleaf_R, P->opts.dtype == HSF_C64, &P->coef, v == 1 ? &df : nullptr);
       if (buf && len) {
         const size_t n = std::min(len - 1, s.size());
         std::memcpy(buf, s.data(), n);
@@ -1593,8 +1647,10 @@ size_t hsf_debug_pass_source(const hsf_plan_t* plan, int32_t variant, int32_t ha
       for (const auto& ps : tr.passes)
         if (k++ == pass) {
           const int nt = cbq ? std::max(128, 1 << (ps.t - cbq - 4)) : 256;
-          const std::string s =
-              jit_pass_source(H, ps, P->opts.dtype == HSF_C64, nt, ps.t < H.m ? cbq : 0, &P->coef, store);
+          DeferOut df;
+          const bool lastp = variant == 1 && &tr == &H.trans.back() && &ps == &tr.passes.back();
+          const std::string s = jit_pass_source(H, ps, P->opts.dtype == HSF_C64, nt, ps.t < H.m ? cbq : 0, &P->coef,
+                                                store, lastp ? &df : nullptr);
           if (buf && len) {
             const size_t n = std::min(len - 1, s.size());
             std::memcpy(buf, s.data(), n);

@@ -141,7 +141,12 @@ __device__ __forceinline__ C trail_weight(const TrailParams& tw, const C* __rest
   for (int u = 0; u < tw.n; ++u) {
     unsigned long long m = tw.mask[u];
     uint32_t idx = 0;
-    for (int j = 0; m; ++j, m &= m - 1) idx |= (uint32_t)((s >> (__ffsll((long long)m) - 1)) & 1ull) << j;
+    const int lo = __ffsll((long long)m) - 1;
+    if ((((m >> lo) + 1ull) & (m >> lo)) == 0ull) {  // contiguous bits: one shift and mask
+      idx = (uint32_t)((s >> lo) & (m >> lo));
+    } else {
+      for (int j = 0; m; ++j, m &= m - 1) idx |= (uint32_t)((s >> (__ffsll((long long)m) - 1)) & 1ull) << j;
+    }
     w = cmul(w, __ldg(&tab[tw.off[u] + idx]));
   }
   return w;
@@ -506,6 +511,10 @@ __global__ void __launch_bounds__(NT, MINB) gather_block_c64_kernel(const BlockG
         sid = p.sidx[jb + lane];
         sbv = p.sbits[jb + lane];
       }
+      // the batch's per-sample weights (folded units, deferred diagonals),
+      // all lanes at once: their table loads overlap the first round's rows
+      float2 wgt = make_float2(1.f, 0.f);
+      if (tw.n && lane < nb) wgt = trail_weight(tw, trail, sbv);
       for (int jj = 0; jj < nb; jj += U) {
         float4 x[U][NF];
         unsigned long long bw[U];
@@ -540,7 +549,7 @@ __global__ void __launch_bounds__(NT, MINB) gather_block_c64_kernel(const BlockG
         const int us = lane - jj;
         float2 v = warp_sum_pairs<U>(re, im, lane, (us >= 0 && us < U) ? us : 0);
         if (lane >= jj && lane < jj + U && lane < nb) {
-          if (tw.n) v = cmul(v, trail_weight(tw, trail, sbv));
+          if (tw.n) v = cmul(v, wgt);
           put_amp(p, sid, v);
         }
       }
