@@ -259,7 +259,9 @@ static DeviceState* ensure_device(Plan* P, int device) {
       for (int h = 0; h < 2; ++h) {
         const Half& H = v ? P->half_fold[h] : P->half[h];
         if (!H.tleaf) continue;
-        src.push_back(jit_tleaf_source(*H.tleaf, H.tleaf_R, c64, &P->coef, v == 1 ? &d->dfin[1][h] : nullptr));
+        // (no deferral here: the T side's D_fin would be per-sample table
+        // lookups in the gather, and this pass is write-bound, not issue-bound)
+        src.push_back(jit_tleaf_source(*H.tleaf, H.tleaf_R, c64, &P->coef));
         owner.push_back({-2 - (2 * v + h), 0});
       }
     }
@@ -955,8 +957,10 @@ static void run_core_bits(Plan* P, DeviceState* d, const Layout& L, const hsf_ru
       tw.off[u] = P->trail_off[u];
     }
     // the deferred final diagonals of the kernels that produced the leaves
+    // (the direct half's are applied to its staged rows by the block gather)
     for (int h = 0; h < 2 && d->jit; ++h) {
       const int kind = (L.tleaf[h] && d->jit_tl[1][h]) ? 1 : 0;
+      if (h == L.direct && sizeof(R) == 4) continue;
       for (const auto& un : d->dfin_units[kind][h]) {
         if (tw.n >= kMaxTrail) fail(HSF_ERR_UNSUPPORTED, "too many per-sample weight tables");
         tw.mask[tw.n] = un.first;
@@ -990,6 +994,19 @@ static void run_core_bits(Plan* P, DeviceState* d, const Layout& L, const hsf_ru
     for (int o = 0; o < a.n_out_shards; ++o) bp.shard[o] = (float2*)a.out_shards[o];
     bp.multicast = a.shards_multicast;
     if (const char* e = std::getenv("HSF_GATHER_LD")) bp.ldmode = std::atoi(e);
+    if (L.fold && d->jit) {  // the direct half's deferred final diagonal, per staged row
+      const int hd = L.direct, kind = (L.tleaf[hd] && d->jit_tl[1][hd]) ? 1 : 0;
+      const int first = P->half[hd].first_qubit;
+      bp.dtab = (const float2*)d->trail;
+      for (const auto& un : d->dfin_units[kind][hd]) {
+        if (bp.dnr >= 4) fail(HSF_ERR_UNSUPPORTED, "too many deferred-diagonal tables");
+        const int lo = __builtin_ctzll(un.first);
+        bp.dlo[bp.dnr] = lo - first;
+        bp.dmask[bp.dnr] = (unsigned)(un.first >> lo);
+        bp.doff[bp.dnr] = un.second;
+        ++bp.dnr;
+      }
+    }
     const size_t smem = (size_t)L.block_rows * L.Kp * sizeof(float2);
     auto launch = [&](auto kern, int nt) {
       static std::vector<const void*> attr;  // kernels whose SMEM limit is raised (all share one type)
@@ -1626,8 +1643,7 @@ size_t hsf_debug_pass_source(const hsf_plan_t* plan, int32_t variant, int32_t ha
       if (!P || half < 0 || half > 1 || v > 1 || (v == 1 && P->fold_u0 < 0)) return 0;
       const Half& H = v ? P->half_fold[half] : P->half[half];
       if (!H.tleaf) return 0;
-      DeferOut df;  // as compiled for runs (the fold variant defers its final diagonals)
-      const std::string s = jit_tleaf_source(*H.tleaf, H.tleaf_R, P->opts.dtype == HSF_C64, &P->coef, v == 1 ? &df : nullptr);
+      const std::string s = jit_tleaf_source(*H.tleaf, H.tleaf_R, P->opts.dtype == HSF_C64, &P->coef);
       if (buf && len) {
         const size_t n = std::min(len - 1, s.size());
         std::memcpy(buf, s.data(), n);

@@ -379,6 +379,13 @@ struct BlockGatherParams {
   int n_shards;
   int multicast;  // shard[0] is an NVLS multicast address: multimem.red into every rank's copy
   int ldmode;     // T-row load flavour (ld_row)
+  // the direct half's deferred final diagonal (DeferOut), applied per staged
+  // row: factor(row) = prod_r dtab[doff[r] + ((row >> dlo[r]) & dmask[r])]
+  const float2* dtab;
+  int dnr;
+  int dlo[4];
+  unsigned dmask[4];
+  long long doff[4];
 };
 
 // a T-row chunk: 0 = ld.global.nc (L1 allocate), 1 = ld.global.cg (L2 only),
@@ -479,6 +486,9 @@ __global__ void __launch_bounds__(NT, MINB) gather_block_c64_kernel(const BlockG
     const long long r0 = blk * RB;
     constexpr int KPW = 32 / RB;
     const int r = lane % RB, kq = lane / RB;
+    float2 fr = make_float2(1.f, 0.f);  // this thread's staged row's deferred diagonal
+    for (int u = 0; u < p.dnr; ++u)
+      fr = cmul(fr, __ldg(&p.dtab[p.doff[u] + (long long)(((unsigned long long)(r0 + r) >> p.dlo[u]) & p.dmask[u])]));
     for (int k0 = KPW * warp; k0 < 2 * F && !(p.debug & 1); k0 += KPW * NW * 4) {
       float2 v[4];
 #pragma unroll
@@ -486,6 +496,7 @@ __global__ void __launch_bounds__(NT, MINB) gather_block_c64_kernel(const BlockG
         const long long k = k0 + KPW * NW * q + kq;
         v[q] = (k < p.K) ? __ldg(&p.D[k * p.ldD + r0 + r]) : make_float2(0.f, 0.f);
         if (p.cpD && k < p.K) v[q] = cmul(v[q], __ldg(&p.cpD[k]));
+        if (p.dnr) v[q] = cmul(v[q], fr);
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
