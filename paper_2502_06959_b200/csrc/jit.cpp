@@ -220,6 +220,14 @@ struct Gen {
   }
 
 
+  // T-leaf: index of the first staged table op (-1: none)
+  int first_staged() const {
+    for (size_t i = 0; i < ops.size(); ++i)
+      if (ops[i].kind != OP_RPASS && staged(ops[i])) return (int)i;
+    return -1;
+  }
+  bool cp_in_table() const { return multi && first_staged() >= 0; }
+
   // T-leaf kernel head: persistent CTAs over (tile, parent) items; the next
   // item's parent tile is prefetched by cp.async into a double buffer while the
   // groups (one 64-thread group per leaf) evaluate the current one
@@ -243,8 +251,16 @@ struct Gen {
     // items = (tile, parent) with the parent fastest: the CTAs in flight
     // write all K columns of the same rows close together in time, so L2
     // merges whole 1 KiB operand rows before they reach DRAM
-    o << "  const long long NPAR = (long long)a.tile_free;  // tile_free = parents\n";
-    o << "  const long long n_items = NTILES * NPAR;\n";
+    o << "  const u32 NPAR = a.tile_free;  // tile_free = parents\n";
+    o << "  const u32 n_items = (u32)NTILES * NPAR;\n";
+    // item -> (tile, parent) in 32-bit arithmetic (shift / mask when the
+    // parent count is a power of two); parent p's tile sits at src index
+    // pb0 + p (node_first is a multiple of src_div == leaves per parent)
+    o << "  const bool npow = (NPAR & (NPAR - 1u)) == 0u;\n";
+    o << "  const u32 nsh = npow ? (u32)(__ffs(NPAR) - 1) : 0u;\n";
+    o << "  auto par_of = [&](u32 it) -> u32 { return npow ? (it & (NPAR - 1u)) : (it % NPAR); };\n";
+    o << "  auto til_of = [&](u32 it) -> u32 { return npow ? (it >> nsh) : (it / NPAR); };\n";
+    o << "  const long long pb0 = a.node_first / a.src_div - a.src_first;\n";
     // tile map of an item's tile
     std::vector<int> nonT;
     for (int q = 0; q < m; ++q)
@@ -258,10 +274,9 @@ struct Gen {
     }
     o << "  auto base_of = [&](u32 tile) -> u32 { return " << gather_expr("tile", from, to) << "; };\n";
     o << "  auto GE = [&](u32 e) -> u32 { return " << gather_expr("e", pf, pt) << "; };\n";
-    o << "  auto prefetch = [&](long long it, u32 buf) {\n";
-    o << "    const long long parent = it % NPAR; const u32 pb = base_of((u32)(it / NPAR));\n";
-    o << "    const C* p_ = srcb + ((a.node_first + parent * " << multi << "ll) / a.src_div - a.src_first) * "
-      << (1ll << m) << "ll;\n";
+    o << "  auto prefetch = [&](u32 it, u32 buf) {\n";
+    o << "    const u32 parent = par_of(it); const u32 pb = base_of(til_of(it));\n";
+    o << "    const C* p_ = srcb + (pb0 + (long long)parent) * " << (1ll << m) << "ll;\n";
     o << "    C* d_ = pbuf + buf * LNEL;\n";
     if (pb_first) {
       // swizzled like the group tiles (8 B copies: the swizzle may swap a
@@ -277,7 +292,7 @@ struct Gen {
       o << "    }\n";
     }
     o << "    asm volatile(\"cp.async.commit_group;\" ::: \"memory\");\n  };\n";
-    o << "  long long it = blockIdx.x;\n  u32 buf = 0u;\n";
+    o << "  u32 it = blockIdx.x;\n  u32 buf = 0u;\n";
     // one CTA barrier at the end of an item covers both the group tiles'
     // reuse and the next parent tile's arrival (its copies were issued at the
     // item's start into the buffer the previous item had finished reading)
@@ -288,12 +303,15 @@ struct Gen {
     o << "  for (; it < n_items; it += gridDim.x, buf ^= 1u) {\n";
     o << "  if (it + gridDim.x < n_items) prefetch(it + gridDim.x, buf ^ 1u);\n";
     o << "  else asm volatile(\"cp.async.commit_group;\" ::: \"memory\");\n";
-    o << "  const long long parent = it % NPAR;\n";
-    o << "  const u32 base = base_of((u32)(it / NPAR));\n";
-    // the store's two c_p columns, requested before the leaf evaluation
+    o << "  const long long parent = par_of(it);\n";
+    o << "  const u32 base = base_of(til_of(it));\n";
     o << "  const long long k0 = a.node_local0 + parent * " << multi << "ll;\n";
+    // c_p of each group's leaf rides on its first staged table (every
+    // amplitude is multiplied by one of its entries); without such a table
+    // the store applies the two c_p columns, requested before the evaluation
     o << "  C w0 = czero<C>(), w1 = czero<C>();\n";
-    o << "  if (cpt) { w0 = cpt[k0 + c2]; w1 = cpt[k0 + c2 + 1u]; }\n";
+    if (!cp_in_table()) o << "  if (cpt) { w0 = cpt[k0 + c2]; w1 = cpt[k0 + c2 + 1u]; }\n";
+    else o << "  (void)w0; (void)w1;\n";
     o << "  auto G = [&](u32 e) -> u32 { return base | GE(e); };\n";
     o << "  {\n  const long long node_g = a.node_first + parent * " << multi << "ll + GRP;\n";
     // per-op table pointers (digit-resolved)
@@ -306,8 +324,13 @@ struct Gen {
                std::to_string(d.stride) + "ll";
       if (staged(d)) {
         o << "  C* " << table(i) << " = stab + " << d.soff << ";\n";
-        o << "  { const C* g_ = " << ptr << "; for (u32 e = TID; e < " << (1u << d.k) << "u; e += NT) " << table(i)
-          << "[e] = __ldg(&g_[e]); }\n";
+        if (cp_in_table() && (int)i == first_staged())
+          o << "  { const C* g_ = " << ptr << "; const C cpl = cpt ? cpt[k0 + GRP] : make_" << (c64 ? "float2" : "double2")
+            << "(1, 0); for (u32 e = TID; e < " << (1u << d.k) << "u; e += NT) " << table(i)
+            << "[e] = cmul(__ldg(&g_[e]), cpl); }\n";
+        else
+          o << "  { const C* g_ = " << ptr << "; for (u32 e = TID; e < " << (1u << d.k) << "u; e += NT) " << table(i)
+            << "[e] = __ldg(&g_[e]); }\n";
       } else {
         o << "  const C* __restrict__ " << table(i) << " = " << ptr << ";\n";
       }
@@ -869,7 +892,7 @@ struct Gen {
       o << "  { C* T = reinterpret_cast<C*>(a.dst);\n";
       o << "    const C* t0 = reinterpret_cast<const C*>(smem_raw + c2 * " << group_bytes() << "u);\n";
       o << "    const C* t1 = reinterpret_cast<const C*>(smem_raw + (c2 + 1u) * " << group_bytes() << "u);\n";
-      o << "    const bool hc = cpt != nullptr;\n";
+      o << "    const bool hc = " << (cp_in_table() ? "false" : "cpt != nullptr") << ";\n";
       o << "#pragma unroll 4\n";
       o << "    for (u32 i = threadIdx.x; i < LNEL * " << hp << "u; i += " << multi * 64 << "u) {\n";
       o << "      const u32 e = i / " << hp << "u;\n";
