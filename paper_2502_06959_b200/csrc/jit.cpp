@@ -281,9 +281,13 @@ struct Gen {
     if (pb_first) {
       // swizzled like the group tiles (8 B copies: the swizzle may swap a
       // pair's halves), so the first register pass reads it in place
-      o << "    for (u32 e = threadIdx.x; e < LNEL; e += " << nt << "u) {\n";
-      o << "      const unsigned sa = (unsigned)__cvta_generic_to_shared(d_ + sw((int)e));\n";
-      o << "      asm volatile(\"cp.async.ca.shared.global [%0], [%1], 8;\" :: \"r\"(sa), \"l\"(p_ + (pb | GE(e))) : \"memory\");\n";
+      o << "    const u32 e0 = threadIdx.x, g0 = pb | GE(e0), s0 = (u32)sw((int)e0);\n";
+      o << "    const unsigned sa0 = (unsigned)__cvta_generic_to_shared(d_);\n";
+      o << "#pragma unroll\n";
+      o << "    for (u32 j = 0; j < LNEL / " << nt << "u; ++j) {\n";
+      o << "      const u32 ej = j * " << nt << "u;\n";
+      o << "      asm volatile(\"cp.async.ca.shared.global [%0], [%1], 8;\" :: \"r\"(sa0 + 8u * (s0 ^ (u32)sw((int)ej))), "
+           "\"l\"(p_ + (g0 | GE(ej))) : \"memory\");\n";
       o << "    }\n";
     } else {
       o << "    for (u32 e = 2u * threadIdx.x; e < LNEL; e += " << 2 * nt << "u) {\n";
@@ -389,7 +393,11 @@ struct Gen {
     o << "  const long long node_g = a.node_first + NODE_ID;\n";
     o << "  C* dst = reinterpret_cast<C*>(a.dst) + (a.node_local0 + NODE_ID) * " << (1ll << m) << "ll;\n";
     o << "  (void)dst;\n";
-    o << "  const C* src = a.src ? reinterpret_cast<const C*>(a.src) + (node_g / a.src_div - a.src_first) * "
+    // (a 32-bit division for the parent index whenever the node index fits,
+    // as it does below the default path budget of 2^26: ~5x fewer
+    // instructions per thread than the 64-bit one)
+    o << "  const long long par_g = ((node_g | a.src_div) >> 32) == 0 ? (long long)((unsigned)node_g / (unsigned)a.src_div) : node_g / a.src_div;\n";
+    o << "  const C* src = a.src ? reinterpret_cast<const C*>(a.src) + (par_g - a.src_first) * "
       << (1ll << m) << "ll : nullptr;\n";
     if (!multi) emit_G();
     // per-op table pointers (digit-resolved for Schmidt factors)
@@ -408,11 +416,22 @@ struct Gen {
         o << "  const C* __restrict__ " << table(i) << " = " << ptr << ";\n";
       }
     }
-    // load (or |0...0>)
+    // load (or |0...0>).  Unrolled with the thread's element split off: the
+    // tile map G and the swizzle are bit-linear over disjoint bits, so
+    // G(e0 | ej) = G(e0) | G(ej) and sw(e0 | ej) = sw(e0) ^ sw(ej) with ej a
+    // constant per unrolled step (the generic loop spent ~20 integer
+    // instructions per pair on them)
     o << "  if (src) {\n";
-    o << "#pragma unroll 4\n";
-    o << "    for (u32 e = 2u * " << TIDs << "; e < LNEL; e += 2u * NT) { C x_, y_; ld2(src + G((RANK << LB) | e), x_, y_); "
-         "s[sw(e)] = x_; s[sw(e + 1)] = y_; }\n";
+    if (!cb && (1 << t) >= 2 * nt) {
+      o << "    const u32 e0 = 2u * " << TIDs << ", g0 = G(e0), s0 = (u32)sw((int)e0);\n";
+      o << "#pragma unroll\n";
+      o << "    for (u32 j = 0; j < LNEL / (2u * NT); ++j) { const u32 ej = j * 2u * NT; C x_, y_; "
+           "ld2(src + (g0 | G(ej)), x_, y_); const u32 sj = s0 ^ (u32)sw((int)ej); s[sj] = x_; s[sj ^ 1u] = y_; }\n";
+    } else {
+      o << "#pragma unroll 4\n";
+      o << "    for (u32 e = 2u * " << TIDs << "; e < LNEL; e += 2u * NT) { C x_, y_; ld2(src + G((RANK << LB) | e), x_, y_); "
+           "s[sw(e)] = x_; s[sw(e + 1)] = y_; }\n";
+    }
     o << "  } else {\n";
     o << "    for (u32 e = " << TIDs << "; e < LNEL; e += NT) { C v_ = czero<C>(); if (G((RANK << LB) | e) == 0u) v_.x = 1; "
          "s[sw(e)] = v_; }\n";
@@ -893,12 +912,14 @@ struct Gen {
       o << "    const C* t0 = reinterpret_cast<const C*>(smem_raw + c2 * " << group_bytes() << "u);\n";
       o << "    const C* t1 = reinterpret_cast<const C*>(smem_raw + (c2 + 1u) * " << group_bytes() << "u);\n";
       o << "    const bool hc = " << (cp_in_table() ? "false" : "cpt != nullptr") << ";\n";
-      o << "#pragma unroll 4\n";
-      o << "    for (u32 i = threadIdx.x; i < LNEL * " << hp << "u; i += " << multi * 64 << "u) {\n";
-      o << "      const u32 e = i / " << hp << "u;\n";
-      o << "      C v0 = t0[sw(e)], v1 = t1[sw(e)];\n";
+      // unrolled: e = e0 + j * (rows per sweep), split off as in the load
+      o << "    const u32 e0 = threadIdx.x / " << hp << "u, g0 = G(e0), s0 = (u32)sw((int)e0);\n";
+      o << "#pragma unroll\n";
+      o << "    for (u32 j = 0; j < LNEL * " << hp << "u / " << multi * 64 << "u; ++j) {\n";
+      o << "      const u32 ej = j * " << multi * 64 / hp << "u, se = s0 ^ (u32)sw((int)ej);\n";
+      o << "      C v0 = t0[se], v1 = t1[se];\n";
       o << "      if (hc) { v0 = cmul(v0, w0); v1 = cmul(v1, w1); }\n";
-      o << "      st2(T + (long long)G(e) * a.ldw + k0 + c2, v0, v1);\n";
+      o << "      st2(T + (long long)(g0 | G(ej)) * a.ldw + k0 + c2, v0, v1);\n";
       o << "    }\n  }\n";
       o << "  asm volatile(\"cp.async.wait_group 0;\" ::: \"memory\");\n";
       o << "  __syncthreads();\n  }\n";
@@ -906,6 +927,11 @@ struct Gen {
       o << "#pragma unroll 4\n";
       o << "  for (u32 e = 2u * threadIdx.x; e < LNEL; e += 2u * NT) " << (store_mode == 3 ? "st_aop" : "st_bop")
         << "(a, a.node_local0 + NODE_ID, G((RANK << LB) | e), s[sw(e)], s[sw(e + 1)]);\n";
+    } else if (!cb && (1 << t) >= 2 * nt) {  // unrolled, thread element split off (see the load)
+      o << "  { const u32 e0 = 2u * threadIdx.x, g0 = G(e0), s0 = (u32)sw((int)e0);\n";
+      o << "#pragma unroll\n";
+      o << "    for (u32 j = 0; j < LNEL / (2u * NT); ++j) { const u32 ej = j * 2u * NT, sj = s0 ^ (u32)sw((int)ej); "
+           "st2(dst + (g0 | G(ej)), s[sj], s[sj ^ 1u]); } }\n";
     } else {
       o << "#pragma unroll 4\n";
       o << "  for (u32 e = 2u * threadIdx.x; e < LNEL; e += 2u * NT) st2(dst + G((RANK << LB) | e), s[sw(e)], s[sw(e + 1)]);\n";
