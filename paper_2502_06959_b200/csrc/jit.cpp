@@ -65,11 +65,16 @@ std::string gather_expr(const std::string& x, const std::vector<int>& from, cons
   return "(" + s + ")";
 }
 
-// shared-memory tile swizzle (8 B / 16 B elements), same as the prelude's
-// sw(): every group of 4 index bits is folded onto the bank bits, so any 4
-// register positions leave lane positions of every residue mod 4 (full-rank
-// bank indices per half-warp, see rpass)
-static uint32_t swz(uint32_t e) { return e ^ ((e >> 4) & 15u) ^ ((e >> 8) & 15u) ^ ((e >> 12) & 15u); }
+// shared-memory tile layout (8 B / 16 B elements), same as the prelude's
+// sw(): a padded index e + e/16 + e/256 + e/4096.  Every 4-bit group of the
+// index adds onto the bank bits, so any 4 register positions leave lane
+// positions of every residue mod 4 (distinct banks per half-warp, see rpass);
+// and the map is additive over disjoint bits (no carry out of a group), so a
+// register access is base + constant: an immediate LDS / STS offset instead
+// of an XOR per access (c5 B leaf pass: ~96 LOP3 per thread)
+static uint32_t swz(uint32_t e) { return e + (e >> 4) + (e >> 8) + (e >> 12); }
+// padded tile size in elements
+static uint32_t padded(int t) { return swz((1u << t) - 1u) + 1u; }
 
 // T-leaf group stride: tile + tables, then padded to 16 mod 64 bytes.  In the
 // transposed store a half-warp reads 4 consecutive rows e (8 contiguous
@@ -78,7 +83,7 @@ static uint32_t swz(uint32_t e) { return e ^ ((e >> 4) & 15u) ^ ((e >> 8) & 15u)
 // each half-warp covers the 32 banks once (ncu: the 32 mod 64 B stride
 // left 2-way conflicts, 4 wavefronts per load instead of 2)
 static size_t tleaf_group_bytes(int t, long long tbl_elems, size_t elem) {
-  return ((((elem << t) + (size_t)tbl_elems * elem) + 63) & ~(size_t)63) + 16;
+  return ((((elem * padded(t)) + (size_t)tbl_elems * elem) + 63) & ~(size_t)63) + 16;
 }
 
 struct Gen {
@@ -243,7 +248,8 @@ struct Gen {
     o << "  const u32 GRP = threadIdx.x >> 6, TID = threadIdx.x & 63u;\n";
     o << "  unsigned char* gbase = smem_raw + GRP * " << group_bytes() << "u;\n";
     o << "  C* s = reinterpret_cast<C*>(gbase);\n";
-    o << "  C* stab = reinterpret_cast<C*>(gbase + (sizeof(C) << " << t << "));\n  (void)stab;\n";
+    o << "  C* stab = reinterpret_cast<C*>(gbase + sizeof(C) * " << padded(t) << "u);\n  (void)stab;\n";
+    o << "  constexpr u32 PADL = " << padded(t) << "u;\n";
     o << "  C* pbuf = reinterpret_cast<C*>(smem_raw + " << (size_t)multi * group_bytes() << "u);\n";
     o << "  const C* coef = reinterpret_cast<const C*>(a.coef);\n";
     o << "  const C* srcb = reinterpret_cast<const C*>(a.src);\n";
@@ -277,7 +283,7 @@ struct Gen {
     o << "  auto prefetch = [&](u32 it, u32 buf) {\n";
     o << "    const u32 parent = par_of(it); const u32 pb = base_of(til_of(it));\n";
     o << "    const C* p_ = srcb + (pb0 + (long long)parent) * " << (1ll << m) << "ll;\n";
-    o << "    C* d_ = pbuf + buf * LNEL;\n";
+    o << "    C* d_ = pbuf + buf * PADL;\n";
     if (pb_first) {
       // swizzled like the group tiles (8 B copies: the swizzle may swap a
       // pair's halves), so the first register pass reads it in place
@@ -286,7 +292,7 @@ struct Gen {
       o << "#pragma unroll\n";
       o << "    for (u32 j = 0; j < LNEL / " << nt << "u; ++j) {\n";
       o << "      const u32 ej = j * " << nt << "u;\n";
-      o << "      asm volatile(\"cp.async.ca.shared.global [%0], [%1], 8;\" :: \"r\"(sa0 + 8u * (s0 ^ (u32)sw((int)ej))), "
+      o << "      asm volatile(\"cp.async.ca.shared.global [%0], [%1], 8;\" :: \"r\"(sa0 + 8u * (s0 + (u32)sw((int)ej))), "
            "\"l\"(p_ + (g0 | GE(ej))) : \"memory\");\n";
       o << "    }\n";
     } else {
@@ -340,9 +346,9 @@ struct Gen {
       }
     }
     if (pb_first) {
-      o << "  const C* pb_ = pbuf + buf * LNEL;\n";
+      o << "  const C* pb_ = pbuf + buf * PADL;\n";
     } else {
-      o << "  { const C* pp = pbuf + buf * LNEL; for (u32 e = TID; e < LNEL; e += NT) s[sw(e)] = pp[e]; }\n";
+      o << "  { const C* pp = pbuf + buf * PADL; for (u32 e = TID; e < LNEL; e += NT) s[sw(e)] = pp[e]; }\n";
       o << "  " << SYNCs << ";\n";
     }
     (void)elem;
@@ -366,10 +372,10 @@ struct Gen {
       o << "  const u32 GRP = threadIdx.x >> 6, TID = threadIdx.x & 63u;\n";
       o << "  unsigned char* gbase = smem_raw + GRP * " << group_bytes() << "u;\n";
       o << "  C* s = reinterpret_cast<C*>(gbase);\n";
-      o << "  C* stab = reinterpret_cast<C*>(gbase + (sizeof(C) << " << t << "));\n";
+      o << "  C* stab = reinterpret_cast<C*>(gbase + sizeof(C) * " << padded(t) << "u);\n";
     } else {
       o << "  C* s = reinterpret_cast<C*>(smem_raw);\n";
-      o << "  C* stab = reinterpret_cast<C*>(smem_raw + (sizeof(C) << " << (t - cb) << "));\n";
+      o << "  C* stab = reinterpret_cast<C*>(smem_raw + sizeof(C) * " << padded(t - cb) << "u);\n";
     }
     if (cb) {
       o << "  const u32 RANK = cluster_rank();\n";
@@ -426,7 +432,7 @@ struct Gen {
       o << "    const u32 e0 = 2u * " << TIDs << ", g0 = G(e0), s0 = (u32)sw((int)e0);\n";
       o << "#pragma unroll\n";
       o << "    for (u32 j = 0; j < LNEL / (2u * NT); ++j) { const u32 ej = j * 2u * NT; C x_, y_; "
-           "ld2(src + (g0 | G(ej)), x_, y_); const u32 sj = s0 ^ (u32)sw((int)ej); s[sj] = x_; s[sj ^ 1u] = y_; }\n";
+           "ld2(src + (g0 | G(ej)), x_, y_); const u32 sj = s0 + (u32)sw((int)ej); s[sj] = x_; s[sj + 1u] = y_; }\n";
     } else {
       o << "#pragma unroll 4\n";
       o << "    for (u32 e = 2u * " << TIDs << "; e < LNEL; e += 2u * NT) { C x_, y_; ld2(src + G((RANK << LB) | e), x_, y_); "
@@ -796,17 +802,17 @@ struct Gen {
     // the swizzle is GF(2)-linear and b, e have disjoint bits: sw(b | e) =
     // sw(b) ^ sw(e), one XOR with a constant per access (c5 leaf pass: ~2 ALU
     // instructions fewer per shared-memory access)
-    if (!x) o << "    const u32 sb = (u32)sw((int)b);\n";
+    if (!x) o << "    const u32 sb = (u32)sw((int)b);\n";  // sw(b | e) = sw(b) + sw(e)
     auto elk = [&](uint32_t e) {
       if (x) return el(x, "(b | " + std::to_string(e) + "u)");
       const uint32_t swe = swz(e);
-      return std::string("s[sb ^ ") + std::to_string(swe) + "u]";
+      return std::string("s[sb + ") + std::to_string(swe) + "u]";
     };
     const bool from_pb = pb_first && i == 0;
     auto elk_ld = [&](uint32_t e) {
       if (!from_pb) return elk(e);
       const uint32_t swe = swz(e);
-      return std::string("pb_[sb ^ ") + std::to_string(swe) + "u]";
+      return std::string("pb_[sb + ") + std::to_string(swe) + "u]";
     };
     uint32_t ek[16];
     for (int k = 0; k < 16; ++k) {
@@ -916,7 +922,7 @@ struct Gen {
       o << "    const u32 e0 = threadIdx.x / " << hp << "u, g0 = G(e0), s0 = (u32)sw((int)e0);\n";
       o << "#pragma unroll\n";
       o << "    for (u32 j = 0; j < LNEL * " << hp << "u / " << multi * 64 << "u; ++j) {\n";
-      o << "      const u32 ej = j * " << multi * 64 / hp << "u, se = s0 ^ (u32)sw((int)ej);\n";
+      o << "      const u32 ej = j * " << multi * 64 / hp << "u, se = s0 + (u32)sw((int)ej);\n";
       o << "      C v0 = t0[se], v1 = t1[se];\n";
       o << "      if (hc) { v0 = cmul(v0, w0); v1 = cmul(v1, w1); }\n";
       o << "      st2(T + (long long)(g0 | G(ej)) * a.ldw + k0 + c2, v0, v1);\n";
@@ -930,8 +936,8 @@ struct Gen {
     } else if (!cb && (1 << t) >= 2 * nt) {  // unrolled, thread element split off (see the load)
       o << "  { const u32 e0 = 2u * threadIdx.x, g0 = G(e0), s0 = (u32)sw((int)e0);\n";
       o << "#pragma unroll\n";
-      o << "    for (u32 j = 0; j < LNEL / (2u * NT); ++j) { const u32 ej = j * 2u * NT, sj = s0 ^ (u32)sw((int)ej); "
-           "st2(dst + (g0 | G(ej)), s[sj], s[sj ^ 1u]); } }\n";
+      o << "    for (u32 j = 0; j < LNEL / (2u * NT); ++j) { const u32 ej = j * 2u * NT, sj = s0 + (u32)sw((int)ej); "
+           "st2(dst + (g0 | G(ej)), s[sj], s[sj + 1u]); } }\n";
     } else {
       o << "#pragma unroll 4\n";
       o << "  for (u32 e = 2u * threadIdx.x; e < LNEL; e += 2u * NT) st2(dst + G((RANK << LB) | e), s[sw(e)], s[sw(e + 1)]);\n";
@@ -1046,12 +1052,12 @@ size_t jit_tleaf_smem_bytes(const Half& TL, int leaves, bool c64) {
   const Pass& ps = TL.trans[0].passes[0];
   const size_t elem = c64 ? 8 : 16;
   // the groups' tiles + tables, then the double-buffered parent tile
-  return (size_t)leaves * tleaf_group_bytes(ps.t, ps.tbl_elems, elem) + 2 * (elem << ps.t);
+  return (size_t)leaves * tleaf_group_bytes(ps.t, ps.tbl_elems, elem) + 2 * elem * padded(ps.t);
 }
 
 size_t jit_smem_bytes(const Pass& ps, bool c64, int cluster_bits) {
   const size_t elem = c64 ? 8 : 16;
-  return (elem << (ps.t - cluster_bits)) + (size_t)ps.tbl_elems * elem;
+  return elem * padded(ps.t - cluster_bits) + (size_t)ps.tbl_elems * elem;
 }
 
 std::vector<void*> jit_compile_all(int device, const std::vector<std::string>& sources) {

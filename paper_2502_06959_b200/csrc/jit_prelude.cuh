@@ -5,7 +5,7 @@
 //
 // Semantics are those of hsf_pass_kernel (sim_kernels.cuh): one CTA owns one
 // (path-tree node, tile) pair, the tile lives in shared memory with the
-// XOR-swizzled layout sw(e) = e ^ (e>>4 & 15) ^ (e>>8 & 15) ^ (e>>12 & 15), and the pass's ops are
+// padded layout sw(e) = e + e/16 + e/256 + e/4096 (additive over disjoint bits), and the pass's ops are
 // applied in order.  In the generated kernels every qubit position, table
 // offset, digit divisor and loop bound is a compile-time constant.
 typedef unsigned int u32;
@@ -31,7 +31,7 @@ __device__ __forceinline__ u32 restricted_tile(u32 id, u32 tile0, u32 free_mask)
   return t;
 }
 
-__device__ __forceinline__ int sw(int e) { return e ^ ((e >> 4) & 15) ^ ((e >> 8) & 15) ^ ((e >> 12) & 15); }
+__device__ __forceinline__ int sw(int e) { return e + (e >> 4) + (e >> 8) + (e >> 12); }
 
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
   return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);

@@ -7,7 +7,7 @@ from collections import Counter
 sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))))
 from hsf_inputs import make_config
 from paper_2502_06959_b200 import Plan
-def sw(e): return e ^ ((e>>4)&15) ^ ((e>>8)&15) ^ ((e>>12)&15)
+def sw(e): return e + (e>>4) + (e>>8) + (e>>12)
 def check(src, c64=True):
     res=[]
     lines=src.split('\n')
@@ -17,7 +17,7 @@ def check(src, c64=True):
         expr=m.group(1).replace('u','')
         offs=[]
         for l2 in lines[i+1:i+25]:
-            mm=re.search(r'v\[\d+\] = (?:s|pb_)\[sb \^ (\d+)u\]', l2)
+            mm=re.search(r'v\[\d+\] = (?:s|pb_)\[sb \+ (\d+)u\]', l2)
             if mm: offs.append(int(mm.group(1)))
         worst=0
         for o in offs[:16]:
@@ -25,7 +25,7 @@ def check(src, c64=True):
             for lane in range(32):
                 gi=lane
                 b=eval(expr)
-                a=sw(b)^o
+                a=sw(b)+o
                 bank=(2*a)%32 if c64 else (4*a)%32
                 (c0 if lane<16 else c1)[bank]+=1
             worst=max(worst,max(c0.values()),max(c1.values()))
