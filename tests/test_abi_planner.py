@@ -343,7 +343,7 @@ def test_tleaf_variant_planned(hsf):
     inst = make_config("c5", n_bits=0)
     P = Plan(inst.text, inst.n_low, inst.blocks)
     src = P.pass_source(0, 0, variant=64 + 1)  # folded tree, half A
-    assert src and "bar.sync" in src and "cp.async.ca.shared.global" in src and "pb_[sb ^" in src and "NTILES" in src
+    assert src and "bar.sync" in src and "cp.async.ca.shared.global" in src and "pb_[sb + " in src and "NTILES" in src
     assert P.pass_source(0, 0, variant=64 + 3) is None  # no such tree variant
     d = P.describe(1 << 22)  # c5 as benched: half B read in place, half A through its T-leaf pass
     assert (d["direct_half"], d["tleaf_half"], d["tleaf_leaves"]) == (1, 0, 8) and d["prep_bytes"] == 0
