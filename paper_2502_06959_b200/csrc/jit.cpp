@@ -11,6 +11,7 @@
 // shared-memory layout, same op order -- without its per-op dispatch and
 // variable-shift index arithmetic (ncu on the interpreter: FFMA was 20 % of
 // the issued instructions, profiles/r01).
+#include <cctype>
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <nvrtc.h>
@@ -111,6 +112,26 @@ struct Gen {
   }
 
   std::string table(int i) const { return "M" + std::to_string(i); }
+
+  // direct register passes: the pass's first register pass loads its 16
+  // amplitudes straight from the parent state and its last one stores them
+  // straight to the node state (no tile copy through shared memory on either
+  // side: two shared-memory round trips and two barriers fewer per tile; the
+  // B leaf pass of c5 is bound by the L1 / shared-memory pipe)
+  bool direct_ld = false, direct_st = false;
+  // G(e) without the tile's base: G is bit-linear, G(b | e) = G(b) | fmap(e)
+  uint32_t fmap(uint32_t e) const {
+    if (whole) return e;
+    uint32_t g = 0;
+    for (int i = 0; i < t; ++i)
+      if ((e >> i) & 1u) g |= 1u << pos2q[i];
+    return g;
+  }
+  bool any_staged() const {
+    for (auto& d : ops)
+      if (staged(d)) return true;
+    return false;
+  }
   // T-leaf: one group's shared memory (its tile + staged tables; 16 B more so
   // consecutive groups' tiles start on different banks)
   size_t group_bytes() const { return tleaf_group_bytes(t, ps.tbl_elems, c64 ? 8 : 16); }
@@ -427,6 +448,9 @@ struct Gen {
     // G(e0 | ej) = G(e0) | G(ej) and sw(e0 | ej) = sw(e0) ^ sw(ej) with ej a
     // constant per unrolled step (the generic loop spent ~20 integer
     // instructions per pair on them)
+    // (direct first register pass: it reads the parent state itself; the tile
+    // load stays for the HSF_NO_DIRECT build, see nvrtc_compile)
+    if (direct_ld) o << "#ifdef HSF_NO_DIRECT\n";
     o << "  if (src) {\n";
     if (!cb && (1 << t) >= 2 * nt) {
       o << "    const u32 e0 = 2u * " << TIDs << ", g0 = G(e0), s0 = (u32)sw((int)e0);\n";
@@ -443,6 +467,7 @@ struct Gen {
          "s[sw(e)] = v_; }\n";
     o << "  }\n";
     o << (cb ? "  cluster_sync();\n" : "  " + SYNCs + ";\n");
+    if (direct_ld) o << "#endif\n";
   }
 
   bool cross(const int* pos, int k) const {
@@ -758,7 +783,11 @@ struct Gen {
     std::vector<int> sorted(pos, pos + 4);
     std::sort(sorted.begin(), sorted.end());
     const bool x = cross(pos, 4);
-    sync_pre(x);
+    const bool dl = direct_ld && i == 0, ds = direct_st && i + (size_t)n + 1 == ops.size();
+    if (!dl || any_staged()) sync_pre(x);  // (direct first pass: only staged tables to wait for; HSF_NO_DIRECT: the load's barrier)
+    // direct passes unrolled over the thread's groups (as a loop, the global
+    // addresses kept live across iterations spill at the 64-register cap: c3)
+    if ((dl || ds) && !x) o << "#pragma unroll\n";
     group_loop(x, "gi", 4);
     if (!x && cb == 0 && t > 4) {
       // lane bits -> non-register tile positions, ordered so that the first
@@ -820,8 +849,41 @@ struct Gen {
       for (int j = 0; j < 4; ++j)
         if ((k >> j) & 1) e |= 1u << pos[j];
       ek[k] = e;
-      o << "    v[" << k << "] = " << elk_ld(e) << ";\n";
     }
+    // direct access: register slot j0 on the tile position that G puts on
+    // state bit 0 pairs slots k, k | 2^j0 into one 16 B (c64) access
+    int j0 = -1;
+    for (int j = 0; j < 4; ++j)
+      if (fmap(1u << pos[j]) == 1u) j0 = j;
+    auto direct = [&](bool load) {
+      for (int k = 0; k < 16; ++k) {
+        const std::string g = u(fmap(ek[k]));  // gb | g = gb + g (disjoint bits): an immediate offset
+        if (j0 >= 0 && ((k >> j0) & 1)) continue;
+        const int k1 = j0 >= 0 ? (k | (1 << j0)) : -1;
+        if (load) {
+          if (k1 >= 0)
+            o << "      ld2(sp + " << g << ", v[" << k << "], v[" << k1 << "]);\n";
+          else
+            o << "      v[" << k << "] = sp[" << g << "];\n";
+        } else {
+          if (k1 >= 0)
+            o << "    st2(dp + " << g << ", v[" << k << "], v[" << k1 << "]);\n";
+          else
+            o << "    dp[" << g << "] = v[" << k << "];\n";
+        }
+      }
+    };
+    if (dl) {
+      o << "#ifndef HSF_NO_DIRECT\n";
+      o << "    if (src) {\n      const C* sp = src + gb;\n";
+      direct(true);
+      o << "    } else {\n";
+      for (int k = 0; k < 16; ++k)
+        o << "      v[" << k << "] = czero<C>(); if ((gb | " << u(fmap(ek[k])) << ") == 0u) v[" << k << "].x = 1;\n";
+      o << "    }\n#else\n";
+    }
+    for (int k = 0; k < 16; ++k) o << "    v[" << k << "] = " << elk_ld(ek[k]) << ";\n";
+    if (dl) o << "#endif\n";
     auto emit_tdiag = [&](size_t r) {  // diagonal: index of element k = i0 | IK[k]
       const DevOp& d = ops[r];
       o << "    { const u32 i0 = " << didx(d, "gb") << ";\n";
@@ -851,9 +913,17 @@ struct Gen {
         }
       }
     }
+    if (ds) {
+      o << "#ifndef HSF_NO_DIRECT\n    C* dp = dst + gb;\n";
+      direct(false);
+      o << "#else\n";
+    }
     for (int k = 0; k < 16; ++k) o << "    " << elk(ek[k]) << " = v[" << k << "];\n";
+    if (ds) o << "#endif\n";
     o << "  }\n";
+    if (ds) o << "#ifdef HSF_NO_DIRECT\n";
     sync_pre(x);
+    if (ds) o << "#endif\n";
   }
 
   // run of standalone diagonal ops [i, j): element-owner mapping, 4 per thread
@@ -887,6 +957,22 @@ struct Gen {
     int heavy_minb = 4, light_minb = 3;
     if (const char* e = std::getenv("HSF_JIT_HEAVY_MINB")) heavy_minb = std::atoi(e);
     if (const char* e = std::getenv("HSF_JIT_LIGHT_MINB")) light_minb = std::atoi(e);
+    {
+      const char* e = std::getenv("HSF_JIT_DIRECT");
+      const int dm = e ? std::atoi(e) : 3;  // bit 0: direct first register pass, bit 1: direct last
+      const bool elig = !multi && !pb_first && cb == 0 && t > 4 && !ops.empty();
+      direct_ld = elig && (dm & 1) && ops[0].kind == OP_RPASS;
+      size_t r = 0, last = (size_t)-1;
+      while (r < ops.size()) {
+        if (ops[r].kind == OP_RPASS) {
+          last = r;
+          r += (size_t)ops[r].k + 1;
+        } else {
+          ++r;
+        }
+      }
+      direct_st = elig && (dm & 2) && store_mode == 0 && last != (size_t)-1 && last + (size_t)ops[last].k + 1 == ops.size();
+    }
     header(name, multi ? 2 : nt > 256 ? 1 : (heavy ? heavy_minb : light_minb));
     size_t i = 0;
     while (i < ops.size()) {
@@ -905,6 +991,9 @@ struct Gen {
         i = j;
       }
     }
+    // (direct last register pass: it stored the node state itself; the tile
+    // store stays for the HSF_NO_DIRECT build)
+    if (direct_st) o << "#ifdef HSF_NO_DIRECT\n";
     if (!multi) o << "  " << SYNCs << ";\n";  // (T-leaf: the CTA barrier before the store covers it)
     if (multi) {
       o << "  }\n  __syncthreads();\n";
@@ -942,8 +1031,13 @@ struct Gen {
       o << "#pragma unroll 4\n";
       o << "  for (u32 e = 2u * threadIdx.x; e < LNEL; e += 2u * NT) st2(dst + G((RANK << LB) | e), s[sw(e)], s[sw(e + 1)]);\n";
     }
+    if (direct_st) o << "#endif\n";
     o << "}\n";
-    return o.str();
+    // back-to-back barriers (one pass's end, the next one's start) -> one
+    std::string src = o.str();
+    const std::string two = "  __syncthreads();\n  __syncthreads();\n", one = "  __syncthreads();\n";
+    for (size_t p = src.find(two); p != std::string::npos; p = src.find(two, p)) src.replace(p, two.size(), one);
+    return src;
   }
 };
 
@@ -991,14 +1085,31 @@ uint64_t fnv64(const std::string& s) {
 std::mutex g_mu;
 std::map<std::pair<int, std::string>, void*> g_cache;  // (device, source) -> CUfunction
 
-std::vector<char> nvrtc_compile(const std::string& src, std::string& log) {
+// ptxas reported local-memory spills (the -v log's "N bytes spill stores")
+static bool log_spills(const std::string& log) {
+  const std::string key = " bytes spill stores";
+  for (size_t p = log.find(key); p != std::string::npos; p = log.find(key, p + 1)) {
+    size_t b = p;
+    while (b > 0 && std::isdigit((unsigned char)log[b - 1])) --b;
+    if (b < p && std::atoi(log.c_str() + b) > 0) return true;
+  }
+  return false;
+}
+
+// A pass with direct register passes whose build spills at the register cap
+// (ptxas -v) is rebuilt with HSF_NO_DIRECT: tile load / store through shared
+// memory, as before (c3's narrow root passes at 64 registers)
+std::vector<char> nvrtc_compile(const std::string& src, std::string& log, bool no_direct = false);
+std::vector<char> nvrtc_compile(const std::string& src, std::string& log, bool no_direct) {
   nvrtcProgram prog;
   if (nvrtcCreateProgram(&prog, src.c_str(), "hsf_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
     log = "nvrtcCreateProgram failed";
     return {};
   }
-  const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo", "--fmad=true"};
-  nvrtcResult r = nvrtcCompileProgram(prog, 4, opts);
+  const bool direct = !no_direct && src.find("HSF_NO_DIRECT") != std::string::npos;
+  const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo", "--fmad=true",
+                        no_direct ? "-DHSF_NO_DIRECT" : "--ptxas-options=-v"};
+  nvrtcResult r = nvrtcCompileProgram(prog, (no_direct || direct) ? 5 : 4, opts);
   size_t n = 0;
   nvrtcGetProgramLogSize(prog, &n);
   log.assign(n, '\0');
@@ -1011,6 +1122,7 @@ std::vector<char> nvrtc_compile(const std::string& src, std::string& log) {
     nvrtcGetCUBIN(prog, cubin.data());
   }
   nvrtcDestroyProgram(&prog);
+  if (direct && r == NVRTC_SUCCESS && log_spills(log)) return nvrtc_compile(src, log, true);
   return cubin;
 }
 

@@ -1059,3 +1059,28 @@ def test_swapped_prefix_path_sum(torch, name, precision, aop, monkeypatch):
     Pg.run(out, row_range=(0, 11), precision=precision, path_range=(P.n_paths // 2, P.n_paths), accumulate=True)
     torch.cuda.synchronize()
     assert np.abs(out.cpu().numpy() - ref).max() <= tol["c64"]
+
+
+@pytest.mark.parametrize("direct", ["0", "1", "2", "3"])
+def test_direct_register_passes(torch, monkeypatch, direct):
+    # HSF_JIT_DIRECT bit 0: a pass's first register pass loads from the parent
+    # state, bit 1: its last one stores the node state (no shared-memory tile
+    # copy); every combination on twins (full output c64 / c128 through the
+    # whole-state tier, bitstrings through 2^11-amplitude tiles) matches the
+    # oracle; c5 as benched runs the default in test_c5_as_benched_elementwise
+    monkeypatch.setenv("HSF_JIT_DIRECT", direct)
+    for name in ("c3", "c5"):
+        inst = make_config(name, twin=True)
+        n, g = O.parse_circuit(inst.text)
+        ref = O.schrodinger(n, g)
+        for dtype in ("c64", "c128"):
+            got, _ = gpu_full(torch, inst, dtype=dtype, precision="simt")  # whole-state tier
+            check(got, ref, dtype)
+        inst = make_config(name, twin=True, n=26, n_low=13)
+        n, g = O.parse_circuit(inst.text)
+        P = O.plan(n, g, inst.n_low, inst.blocks)
+        A, B, c = O.half_states(P, 0, 8)
+        bits = inst.bitstrings[:2048]
+        ref = O.recombine_bits(A, B, c, bits, inst.n_low)
+        got, _ = gpu_bits(torch, inst, bits, path_range=(0, 8), tile_qubits=11)
+        check(got, ref, "c64")
