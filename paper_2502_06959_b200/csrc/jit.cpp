@@ -107,6 +107,7 @@ struct Gen {
     pos2q.resize(t);
     for (int i = 0; i < t; ++i) pos2q[i] = whole ? i : p.T[i];
     if (const char* e = std::getenv("HSF_JIT_GIVENS")) givens = std::atoi(e) != 0;
+    if (const char* e = std::getenv("HSF_JIT_TPAD")) tpad = std::atoi(e) != 0;
     packed = c64;
     if (const char* e = std::getenv("HSF_JIT_PACKED")) packed = c64 && std::atoi(e) != 0;
   }
@@ -119,6 +120,8 @@ struct Gen {
   // side: two shared-memory round trips and two barriers fewer per tile; the
   // B leaf pass of c5 is bound by the L1 / shared-memory pipe)
   bool direct_ld = false, direct_st = false;
+  bool tpad = true;  // staged tables at the padded index (HSF_JIT_TPAD=0: plain)
+  std::string TP() const { return tpad ? "e + (e >> 4)" : "e"; }
   // G(e) without the tile's base: G is bit-linear, G(b | e) = G(b) | fmap(e)
   uint32_t fmap(uint32_t e) const {
     if (whole) return e;
@@ -211,8 +214,12 @@ struct Gen {
     return gather_expr(g, from, to);
   }
   bool staged(const DevOp& d) const { return d.kind == OP_DIAG && d.soff >= 0; }
+  // staged tables sit at the padded index x + x/16 (entries x and x + 16 on
+  // different banks: the lanes of a register pass differ in high index bits,
+  // 2-way conflicts on c5's B leaf pass, ncu r02f); additive over disjoint bits
   std::string tload(const DevOp& d, int i, const std::string& idx) const {
-    return staged(d) ? table(i) + "[" + idx + "]" : "__ldg(&" + table(i) + "[" + idx + "])";
+    if (!staged(d)) return "__ldg(&" + table(i) + "[" + idx + "])";
+    return tpad ? table(i) + "[(" + idx + ") + ((" + idx + ") >> 4)]" : table(i) + "[" + idx + "]";
   }
 
   int multi = 0;  // T-leaf variant: leaves per CTA (0 = one node per CTA)
@@ -358,10 +365,10 @@ struct Gen {
         if (cp_in_table() && (int)i == first_staged())
           o << "  { const C* g_ = " << ptr << "; const C cpl = cpt ? cpt[k0 + GRP] : make_" << (c64 ? "float2" : "double2")
             << "(1, 0); for (u32 e = TID; e < " << (1u << d.k) << "u; e += NT) " << table(i)
-            << "[e] = cmul(__ldg(&g_[e]), cpl); }\n";
+            << "[" << TP() << "] = cmul(__ldg(&g_[e]), cpl); }\n";
         else
           o << "  { const C* g_ = " << ptr << "; for (u32 e = TID; e < " << (1u << d.k) << "u; e += NT) " << table(i)
-            << "[e] = __ldg(&g_[e]); }\n";
+            << "[" << TP() << "] = __ldg(&g_[e]); }\n";
       } else {
         o << "  const C* __restrict__ " << table(i) << " = " << ptr << ";\n";
       }
@@ -438,7 +445,7 @@ struct Gen {
       if (staged(d)) {
         o << "  C* " << table(i) << " = stab + " << d.soff << ";\n";
         o << "  { const C* g_ = " << ptr << "; for (u32 e = " << TIDs << "; e < " << (1u << d.k)
-          << "u; e += NT) " << table(i) << "[e] = __ldg(&g_[e]); }\n";
+          << "u; e += NT) " << table(i) << "[" << TP() << "] = __ldg(&g_[e]); }\n";
       } else {
         o << "  const C* __restrict__ " << table(i) << " = " << ptr << ";\n";
       }
@@ -887,14 +894,17 @@ struct Gen {
     auto emit_tdiag = [&](size_t r) {  // diagonal: index of element k = i0 | IK[k]
       const DevOp& d = ops[r];
       o << "    { const u32 i0 = " << didx(d, "gb") << ";\n";
+      const bool st = staged(d) && tpad;
+      if (st) o << "      const u32 p0 = i0 + (i0 >> 4);\n";  // padded(i0 | ik) = padded(i0) + padded(ik)
       for (int k = 0; k < 16; ++k) {
         uint32_t ik = 0;
         for (int j = 0; j < 4; ++j)
           if ((k >> j) & 1)
             for (int jj = 0; jj < d.k; ++jj)
               if (d.q[jj] == qreg[j]) ik |= 1u << jj;
-        o << "      v[" << k << "] = cmul(v[" << k << "], " << tload(d, (int)r, "i0 | " + std::to_string(ik) + "u")
-          << ");\n";
+        const std::string ld = st ? table((int)r) + "[p0 + " + std::to_string(ik + (ik >> 4)) + "u]"
+                                  : tload(d, (int)r, "i0 | " + std::to_string(ik) + "u");
+        o << "      v[" << k << "] = cmul(v[" << k << "], " << ld << ");\n";
       }
       o << "    }\n";
     };

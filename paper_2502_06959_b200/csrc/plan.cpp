@@ -1052,10 +1052,11 @@ static void finalize_half(Half& H, size_t elem_bytes) {
         for (int64_t oi = q.op_begin; oi < q.op_end; ++oi) {
           DevOp& d = out[oi];
           d.soff = -1;
-          if (d.kind == OP_DIAG && d.k <= kSmemTableQ &&
-              (size_t)(q.tbl_elems + (1 << d.k)) * elem_bytes <= (size_t)kSmemTableBytes) {
+          // (room for the generated kernels' padded layout x + x/16)
+          const int64_t sz = (1 << d.k) + ((1 << d.k) >> 4);
+          if (d.kind == OP_DIAG && d.k <= kSmemTableQ && (size_t)(q.tbl_elems + sz) * elem_bytes <= (size_t)kSmemTableBytes) {
             d.soff = (int32_t)q.tbl_elems;
-            q.tbl_elems += 1 << d.k;
+            q.tbl_elems += sz;
           }
         }
         np.push_back(q);

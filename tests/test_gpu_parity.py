@@ -1061,14 +1061,16 @@ def test_swapped_prefix_path_sum(torch, name, precision, aop, monkeypatch):
     assert np.abs(out.cpu().numpy() - ref).max() <= tol["c64"]
 
 
-@pytest.mark.parametrize("direct", ["0", "1", "2", "3"])
-def test_direct_register_passes(torch, monkeypatch, direct):
+@pytest.mark.parametrize("direct,tpad", [("0", "1"), ("1", "1"), ("2", "1"), ("3", "1"), ("3", "0")])
+def test_direct_register_passes(torch, monkeypatch, direct, tpad):
     # HSF_JIT_DIRECT bit 0: a pass's first register pass loads from the parent
     # state, bit 1: its last one stores the node state (no shared-memory tile
     # copy); every combination on twins (full output c64 / c128 through the
     # whole-state tier, bitstrings through 2^11-amplitude tiles) matches the
     # oracle; c5 as benched runs the default in test_c5_as_benched_elementwise
+    # (HSF_JIT_TPAD: staged tables at the padded index x + x/16, or plain)
     monkeypatch.setenv("HSF_JIT_DIRECT", direct)
+    monkeypatch.setenv("HSF_JIT_TPAD", tpad)
     for name in ("c3", "c5"):
         inst = make_config(name, twin=True)
         n, g = O.parse_circuit(inst.text)
