@@ -318,6 +318,13 @@ def rooflines(cfg, desc, phase, pk, dtype, cone):
     tr, src = _traffic(cfg["workload"], kname)
     r["traffic"] = tr
     r["traffic_source"] = src
+    if r["bound"] == "hbm" and tr is not None and tr < 0.5 * r["bytes_per_launch"]:
+        # the committed capture shows the operands L2-resident (DRAM traffic
+        # under half the algorithmic bytes, e.g. c3's 2 x 64 MiB leaves): the
+        # bound is the L2 read rate, not HBM
+        r.update({"bound": "l2", "peak": L2_READ_GBS, "frac": r["achieved"] / L2_READ_GBS, "frac_of_hbm_copy":
+                  r["achieved"] / pk["hbm"], "peak_source": "scripts/probe/l2bw.cu (16 B __ldcg over 64 MiB, L2-resident "
+                  "read rate); operands L2-resident per profiles/traffic.json"})
     # simulator window: both trees (concurrent streams) + the operand prep after them
     if cone:  # prefix outputs: half A computes only the rows' light cone (uncounted); half B alone
         t_w = phase[1]
