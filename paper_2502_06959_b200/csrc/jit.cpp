@@ -1217,6 +1217,11 @@ std::vector<void*> jit_compile_all(int device, const std::vector<std::string>& s
       if (D.moduleGetFunction(&f, mod, "hsf_jit_pass") != CUDA_SUCCESS) fail(HSF_ERR_CUDA, "cuModuleGetFunction failed");
       if (D.funcSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, 227 * 1024) != CUDA_SUCCESS)
         fail(HSF_ERR_CUDA, "cuFuncSetAttribute failed");
+      // HSF_JIT_CARVEOUT=p: preferred shared-memory carveout in percent (the
+      // passes stream their global loads, so L1 has nothing to keep); unset =
+      // the driver's choice from the launch's dynamic size
+      if (const char* e = std::getenv("HSF_JIT_CARVEOUT"))
+        D.funcSetAttribute(f, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, std::atoi(e));
       g_cache[{device, sources[todo[k]]}] = (void*)f;  // modules live for the process
     }
     for (size_t i = 0; i < sources.size(); ++i)
