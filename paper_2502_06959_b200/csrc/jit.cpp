@@ -1148,11 +1148,19 @@ static void defer_result(const Gen& g, DeferOut* d) {
   d->scalar = g.carry_scalar;
 }
 
+// cache-operator experiment knob (jit_prelude.cuh): part of the source, so of the cache key
+static std::string ldst_defs() {
+  const char* e = std::getenv("HSF_JIT_LDST");
+  if (!e) return "";
+  const int v = std::atoi(e);
+  return "#define HSF_LD_MODE " + std::to_string(v / 10) + "\n#define HSF_ST_MODE " + std::to_string(v % 10) + "\n";
+}
+
 std::string jit_pass_source(const Half& H, const Pass& ps, bool c64, int threads, int cluster_bits,
                             const std::vector<cd>* coef, int store_mode, DeferOut* defer) {
   Gen g(H, ps, c64, coef);
   g.defer = defer != nullptr && store_mode == 0;
-  std::string src = std::string(kPrelude) + "\n" + g.build("hsf_jit_pass", threads, cluster_bits, store_mode);
+  std::string src = ldst_defs() + std::string(kPrelude) + "\n" + g.build("hsf_jit_pass", threads, cluster_bits, store_mode);
   defer_result(g, defer);
   return src;
 }
@@ -1165,7 +1173,7 @@ std::string jit_tleaf_source(const Half& TL, int leaves, bool c64, const std::ve
   g.pb_first = !g.ops.empty() && g.ops[0].kind == OP_RPASS && !std::getenv("HSF_TLEAF_COPY");
   g.TIDs = "TID";
   g.SYNCs = "asm volatile(\"bar.sync %0, 64;\" :: \"r\"(1u + GRP) : \"memory\")";
-  std::string src = std::string(kPrelude) + "\n" + g.build("hsf_jit_pass", 64 * leaves, 0, 0);
+  std::string src = ldst_defs() + std::string(kPrelude) + "\n" + g.build("hsf_jit_pass", 64 * leaves, 0, 0);
   defer_result(g, defer);
   return src;
 }

@@ -68,8 +68,23 @@ template <>
 __device__ __forceinline__ double2 czero<double2>() { return make_double2(0.0, 0.0); }
 
 // two consecutive amplitudes from / to global memory (16 B for complex64)
+// HSF_LD_MODE / HSF_ST_MODE (env HSF_JIT_LDST = 10 * ld + st, measurement
+// only): cache operators of the passes' 16 B state loads / stores -- 0 default,
+// 1 .cg (L2 only), 2 .cs (streaming, evict first), 3 store .wt
+#ifndef HSF_LD_MODE
+#define HSF_LD_MODE 0
+#endif
+#ifndef HSF_ST_MODE
+#define HSF_ST_MODE 0
+#endif
 __device__ __forceinline__ void ld2(const float2* p, float2& a, float2& b) {
+#if HSF_LD_MODE == 1
+  const float4 x = __ldcg(reinterpret_cast<const float4*>(p));
+#elif HSF_LD_MODE == 2
+  const float4 x = __ldcs(reinterpret_cast<const float4*>(p));
+#else
   const float4 x = *reinterpret_cast<const float4*>(p);
+#endif
   a = make_float2(x.x, x.y);
   b = make_float2(x.z, x.w);
 }
@@ -78,7 +93,15 @@ __device__ __forceinline__ void ld2(const double2* p, double2& a, double2& b) {
   b = p[1];
 }
 __device__ __forceinline__ void st2(float2* p, float2 a, float2 b) {
+#if HSF_ST_MODE == 1
+  __stcg(reinterpret_cast<float4*>(p), make_float4(a.x, a.y, b.x, b.y));
+#elif HSF_ST_MODE == 2
+  __stcs(reinterpret_cast<float4*>(p), make_float4(a.x, a.y, b.x, b.y));
+#elif HSF_ST_MODE == 3
+  __stwt(reinterpret_cast<float4*>(p), make_float4(a.x, a.y, b.x, b.y));
+#else
   *reinterpret_cast<float4*>(p) = make_float4(a.x, a.y, b.x, b.y);
+#endif
 }
 __device__ __forceinline__ void st2(double2* p, double2 a, double2 b) {
   p[0] = a;
