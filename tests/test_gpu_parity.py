@@ -98,6 +98,23 @@ def test_twins_bitstrings(torch, name):
     check(got, ref, "c64")
 
 
+@pytest.mark.parametrize("seed", [101, 102, 103, 104, 105])
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_twins_robustness_seeds(torch, name, seed):
+    # circuit seeds 101..105 beside each config's own seed, in the
+    # config's dtype and default precision / output mode (full output, or the
+    # config's bitstrings)
+    inst = make_config(name, twin=True, seed=seed)
+    n, g = O.parse_circuit(inst.text)
+    psi = O.schrodinger(n, g)
+    if inst.bitstrings is None:
+        got, _ = gpu_full(torch, inst)
+        check(got, psi, inst.dtype)
+    else:
+        got, _ = gpu_bits(torch, inst, inst.bitstrings)
+        check(got, psi[inst.bitstrings.astype(np.int64)], inst.dtype)
+
+
 def test_c1_full_size_complex128(torch):
     inst = make_config("c1")
     n, g = O.parse_circuit(inst.text)
